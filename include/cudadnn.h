@@ -1,0 +1,290 @@
+/*
+ * cudadnn.h — the B200 "CudaDnn" C-ABI: handle look-up tables for device
+ * memory, streams, descriptors and subsystems (RNG, NCCL communicators),
+ * the frozen function-index dispatch, and typed entry points for every op of
+ * one SGD iteration.
+ *
+ * This is the device boundary of the hot path.  It replaces, one for one:
+ *
+ *   reference (/root/reference/proj/core)          this header
+ *   ---------------------------------------------  -------------------------------
+ *   Registry::alloc_buffer  backend.cpp:18-25      cdnn_alloc
+ *   Registry::free_buffer   backend.cpp:27-38      cdnn_free
+ *   Registry::buffer_length backend.cpp:58-60      cdnn_length
+ *   Registry::write / read  backend.cpp:62-73      cdnn_write / cdnn_read
+ *   Registry::buffer (span) backend.cpp:75-79      cdnn_device_ptr (device view)
+ *   Registry::create_rng    backend.cpp:81-86      cdnn_rng_create
+ *   Registry::free_subsystem backend.cpp:100-110   cdnn_subsystem_free
+ *   Registry::live_slots    backend.cpp:112-115    cdnn_live_slots
+ *   Registry::dispatch      backend.cpp:248-305    cdnn_dispatch (indices 1-7 frozen,
+ *                                                  backend.hpp:47-69; new ops append)
+ *   kernels::fill/copy/scal/axpy/dot backend.cpp:131-167   cdnn_fill/copy/scal/axpy/dot
+ *   kernels::gemm           backend.cpp:169-197    cdnn_gemm (tcgen05 TF32 / SIMT FP64)
+ *   kernels::rng_uniform    backend.cpp:199-207    cdnn_rng_uniform (host mt19937_64)
+ *   InnerProductLayer fwd/bwd layers.cpp:124-169   cdnn_ip_forward / cdnn_ip_backward
+ *   ReluLayer   layers.cpp:180-195                 cdnn_relu_forward / _backward
+ *   SigmoidLayer layers.cpp:206-221                cdnn_sigmoid_forward / _backward
+ *   SoftmaxLayer layers.cpp:232-266                cdnn_softmax_forward / _backward
+ *   Solver::apply_update solver.cpp:24-57          cdnn_solver_apply
+ *   (absent: Convolution, Pooling, SoftmaxWithLoss, momentum SGD, NCCL Parallel)
+ *                                                  cdnn_conv_*, cdnn_pool_*,
+ *                                                  cdnn_softmax_loss_*, cdnn_nccl_*
+ *
+ * Conventions:
+ *  - The library owns all device memory; callers hold opaque 64-bit ids.
+ *    Ids are monotone per context and never recycled; 0 is the null handle
+ *    (backend.hpp:17-25).  Handle 0 as a *stream* argument means the
+ *    context's own compute stream.
+ *  - Every entry point returns a cdnn_status; the message of the last failure
+ *    on the calling thread is available from cdnn_last_error().  Status codes
+ *    map 1:1 onto the exception classes of errors.hpp:8-83.
+ *  - Table mutation is serialised per context; buffer contents are ordered
+ *    per stream.  Compute entry points are asynchronous on the
+ *    given stream; cdnn_read/cdnn_write/cdnn_dot synchronise.
+ *  - Element counts are in elements of the buffer's dtype.
+ */
+#ifndef CUDADNN_H_
+#define CUDADNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CDNN_API __attribute__((visibility("default")))
+
+typedef uint64_t cdnn_handle;
+typedef struct cdnn_context* cdnn_ctx;
+
+typedef enum {
+  CDNN_OK = 0,
+  CDNN_INVALID_ARGUMENT = 1, /* InvalidArgument  errors.hpp:14 */
+  CDNN_DANGLING_HANDLE = 2,  /* DanglingHandle   errors.hpp:20 */
+  CDNN_UNKNOWN_FUNCTION = 3, /* UnknownFunction  errors.hpp:26 */
+  CDNN_MODEL_ERROR = 4,      /* ModelError       errors.hpp:32 */
+  CDNN_DATA_STARVATION = 5,  /* DataStarvation   errors.hpp:38 */
+  CDNN_FORMAT_ERROR = 6,     /* FormatError      errors.hpp:44 */
+  CDNN_NOT_FOUND = 7,        /* NotFound         errors.hpp:49 */
+  CDNN_INVALID_STATE = 8,    /* InvalidState     errors.hpp:55 */
+  CDNN_PARSE_ERROR = 9,      /* ParseError       errors.hpp:61 */
+  CDNN_LOAD_ERROR = 10,      /* LoadError        errors.hpp:72 */
+  CDNN_CUDA_ERROR = 11,      /* device / driver failure (no reference analog) */
+  CDNN_NO_DEVICE = 12        /* no CUDA device: the library never falls back to the CPU */
+} cdnn_status;
+
+typedef enum { CDNN_F32 = 0, CDNN_F64 = 1, CDNN_I32 = 2 } cdnn_dtype;
+
+/* handle kinds held in the look-up tables (paper Table 3) */
+typedef enum {
+  CDNN_KIND_BUFFER = 0,
+  CDNN_KIND_STREAM = 1,
+  CDNN_KIND_DESCRIPTOR = 2,
+  CDNN_KIND_SUBSYSTEM = 3,
+  CDNN_KIND_GRAPH = 4
+} cdnn_kind;
+
+/* Frozen dispatch indices (backend.hpp:47-69).  Indices only ever append. */
+enum {
+  CDNN_FN_FILL = 1,        /* dst, n, value */
+  CDNN_FN_COPY = 2,        /* src, dst, n */
+  CDNN_FN_SCAL = 3,        /* n, alpha, x */
+  CDNN_FN_AXPY = 4,        /* n, alpha, x, y */
+  CDNN_FN_DOT = 5,         /* n, x, y -> result */
+  CDNN_FN_GEMM = 6,        /* trans_a, trans_b, m, n, k, alpha, a, b, beta, c */
+  CDNN_FN_RNG_UNIFORM = 7, /* rng, dst, n, lo, hi */
+  /* appended by this library */
+  CDNN_FN_RELU_FWD = 8,    /* x, y, n */
+  CDNN_FN_RELU_BWD = 9,    /* x, dy, dx, n */
+  CDNN_FN_SIGMOID_FWD = 10,/* x, y, n */
+  CDNN_FN_SIGMOID_BWD = 11,/* y, dy, dx, n */
+  CDNN_FN_SOFTMAX_FWD = 12,/* x, y, rows, features */
+  CDNN_FN_SOFTMAX_BWD = 13 /* y, dy, dx, rows, features */
+};
+
+/* ---- diagnostics / context ---------------------------------------------- */
+CDNN_API const char* cdnn_last_error(void);
+CDNN_API const char* cdnn_status_name(int status);
+CDNN_API int cdnn_device_count(int* out);
+CDNN_API int cdnn_ctx_create(int device, cdnn_ctx* out);
+CDNN_API int cdnn_ctx_destroy(cdnn_ctx ctx);
+CDNN_API int cdnn_ctx_device(cdnn_ctx ctx, int* out);
+CDNN_API int cdnn_live_slots(cdnn_ctx ctx, uint64_t* out); /* backend.hpp:99-100 */
+/* number of kernels this context has launched (the bench's gpu_launches claim) */
+CDNN_API int cdnn_launch_count(cdnn_ctx ctx, uint64_t* out);
+
+/* ---- buffers ------------------------------------------------------------- */
+/* zero-initialised; length 0 -> CDNN_INVALID_ARGUMENT (backend.cpp:18-21) */
+CDNN_API int cdnn_alloc(cdnn_ctx ctx, uint64_t length, int dtype, cdnn_handle* out);
+/* unknown, 0 or freed -> CDNN_DANGLING_HANDLE (backend.cpp:27-38) */
+CDNN_API int cdnn_free(cdnn_ctx ctx, cdnn_handle h);
+/* aliasing sub-range [offset, offset+length) of a buffer (flat param/grad arenas) */
+CDNN_API int cdnn_view(cdnn_ctx ctx, cdnn_handle h, uint64_t offset, uint64_t length,
+                       cdnn_handle* out);
+CDNN_API int cdnn_length(cdnn_ctx ctx, cdnn_handle h, uint64_t* out);
+CDNN_API int cdnn_buffer_dtype(cdnn_ctx ctx, cdnn_handle h, int* out);
+CDNN_API int cdnn_device_ptr(cdnn_ctx ctx, cdnn_handle h, void** out);
+/* synchronous host copies of elements [0, n); n > length -> INVALID_ARGUMENT */
+CDNN_API int cdnn_write(cdnn_ctx ctx, cdnn_handle h, const void* host, uint64_t n);
+CDNN_API int cdnn_read(cdnn_ctx ctx, cdnn_handle h, void* host, uint64_t n);
+/* asynchronous copies at an element offset (host memory should be pinned) */
+CDNN_API int cdnn_write_async(cdnn_ctx ctx, cdnn_handle h, uint64_t offset, const void* host,
+                              uint64_t n, cdnn_handle stream);
+CDNN_API int cdnn_read_async(cdnn_ctx ctx, cdnn_handle h, uint64_t offset, void* host,
+                             uint64_t n, cdnn_handle stream);
+CDNN_API int cdnn_host_alloc_pinned(uint64_t bytes, void** out);
+CDNN_API int cdnn_host_free_pinned(void* p);
+
+/* ---- streams / graphs ----------------------------------------------------- */
+CDNN_API int cdnn_stream_create(cdnn_ctx ctx, cdnn_handle* out);
+CDNN_API int cdnn_stream_free(cdnn_ctx ctx, cdnn_handle h);
+CDNN_API int cdnn_stream_sync(cdnn_ctx ctx, cdnn_handle stream);
+/* make `stream` wait for all work currently queued on `on` */
+CDNN_API int cdnn_stream_wait(cdnn_ctx ctx, cdnn_handle stream, cdnn_handle on);
+CDNN_API int cdnn_graph_begin(cdnn_ctx ctx, cdnn_handle stream);
+CDNN_API int cdnn_graph_end(cdnn_ctx ctx, cdnn_handle stream, cdnn_handle* graph_out);
+CDNN_API int cdnn_graph_launch(cdnn_ctx ctx, cdnn_handle graph, cdnn_handle stream);
+CDNN_API int cdnn_graph_free(cdnn_ctx ctx, cdnn_handle graph);
+/* events for device-side timing: elapsed ms between two records */
+CDNN_API int cdnn_event_create(cdnn_ctx ctx, cdnn_handle* out);
+CDNN_API int cdnn_event_record(cdnn_ctx ctx, cdnn_handle ev, cdnn_handle stream);
+CDNN_API int cdnn_event_elapsed(cdnn_ctx ctx, cdnn_handle start, cdnn_handle end, float* ms);
+CDNN_API int cdnn_event_free(cdnn_ctx ctx, cdnn_handle ev);
+
+/* ---- RNG subsystem (host mt19937_64, backend.hpp:31-45) ------------------ */
+CDNN_API int cdnn_rng_create(cdnn_ctx ctx, uint64_t seed, cdnn_handle* out);
+CDNN_API int cdnn_rng_next_u64(cdnn_ctx ctx, cdnn_handle rng, uint64_t* out);
+/* dst[0..n) = lo + (hi-lo)*u, u = (u64>>11)*2^-53, drawn in order (backend.cpp:199-207) */
+CDNN_API int cdnn_rng_uniform(cdnn_ctx ctx, cdnn_handle rng, cdnn_handle dst, uint64_t n,
+                              double lo, double hi);
+CDNN_API int cdnn_subsystem_free(cdnn_ctx ctx, cdnn_handle h);
+
+/* ---- descriptors ---------------------------------------------------------- */
+typedef struct {
+  int n, c, h, w;          /* bottom NCHW */
+  int num_output;          /* Cout */
+  int kernel_h, kernel_w;
+  int stride_h, stride_w;
+  int pad_h, pad_w;
+  int dilation_h, dilation_w;
+  int group;
+} cdnn_conv_params;
+
+typedef enum { CDNN_POOL_MAX = 0, CDNN_POOL_AVE = 1 } cdnn_pool_method;
+
+typedef struct {
+  int n, c, h, w;          /* bottom NCHW */
+  int method;              /* cdnn_pool_method */
+  int kernel_h, kernel_w;
+  int stride_h, stride_w;
+  int pad_h, pad_w;
+  int global_pooling;      /* kernel = full H x W */
+} cdnn_pool_params;
+
+/* Validates and derives output extents (Caffe conv: floor; pooling: ceil). */
+CDNN_API int cdnn_conv_desc_create(cdnn_ctx ctx, const cdnn_conv_params* p, cdnn_handle* out);
+CDNN_API int cdnn_conv_output_shape(cdnn_ctx ctx, cdnn_handle desc, int out_nchw[4]);
+CDNN_API int cdnn_pool_desc_create(cdnn_ctx ctx, const cdnn_pool_params* p, cdnn_handle* out);
+CDNN_API int cdnn_pool_output_shape(cdnn_ctx ctx, cdnn_handle desc, int out_nchw[4]);
+CDNN_API int cdnn_desc_free(cdnn_ctx ctx, cdnn_handle h);
+
+/* ---- legacy function-index dispatch (backend.cpp:248-305) ----------------- */
+/* args are doubles, handle ids encoded as values; `out` receives up to
+ * *nout results (dot).  Unknown index -> CDNN_UNKNOWN_FUNCTION; wrong arity
+ * or non-integral handle/count -> CDNN_INVALID_ARGUMENT.  Synchronous. */
+CDNN_API int cdnn_dispatch(cdnn_ctx ctx, int function_index, const double* args,
+                           uint64_t nargs, double* out, uint64_t* nout);
+
+/* ---- BLAS-like kernels (backend.cpp:131-197) ------------------------------ */
+CDNN_API int cdnn_fill(cdnn_ctx ctx, cdnn_handle dst, uint64_t n, double value, cdnn_handle stream);
+CDNN_API int cdnn_copy(cdnn_ctx ctx, cdnn_handle src, cdnn_handle dst, uint64_t n, cdnn_handle stream);
+CDNN_API int cdnn_scal(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cdnn_handle stream);
+CDNN_API int cdnn_axpy(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cdnn_handle y,
+                       cdnn_handle stream);
+CDNN_API int cdnn_dot(cdnn_ctx ctx, uint64_t n, cdnn_handle x, cdnn_handle y, double* result);
+/* Row-major C = alpha*op(A)*op(B) + beta*C; beta == 0 never reads C.
+ * F32 buffers run on tcgen05 TF32 tensor cores, F64 on the SIMT FP64 path. */
+CDNN_API int cdnn_gemm(cdnn_ctx ctx, int trans_a, int trans_b, int m, int n, int k, double alpha,
+                       cdnn_handle a, cdnn_handle b, double beta, cdnn_handle c, cdnn_handle stream);
+
+/* ---- layers ---------------------------------------------------------------- */
+/* InnerProduct (layers.cpp:124-169).  x: rows x K, w: O x K, bias: O (0 = none)
+ * top = x W^T + bias ; optional fused ReLU (relu != 0). */
+CDNN_API int cdnn_ip_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle w, cdnn_handle bias,
+                             cdnn_handle top, int rows, int k, int o, int relu,
+                             cdnn_handle stream);
+/* dW += dY^T X ; db += colsum(dY) (0 = skip) ; dX = dY W (0 = skip) */
+CDNN_API int cdnn_ip_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle w, cdnn_handle dy,
+                              cdnn_handle dw, cdnn_handle db, cdnn_handle dx, int rows, int k,
+                              int o, cdnn_handle stream);
+
+/* Convolution (Caffe semantics; absent from the reference).
+ * bias may be 0.  backward_filter ACCUMULATES into dw/db (param diffs
+ * accumulate, layers.hpp:84-86); backward_data OVERWRITES dx. */
+CDNN_API int cdnn_conv_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle w,
+                               cdnn_handle bias, cdnn_handle y, cdnn_handle stream);
+CDNN_API int cdnn_conv_backward_data(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w,
+                                     cdnn_handle dy, cdnn_handle dx, cdnn_handle stream);
+CDNN_API int cdnn_conv_backward_filter(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x,
+                                       cdnn_handle dy, cdnn_handle dw, cdnn_handle db,
+                                       cdnn_handle stream);
+
+/* Pooling (Caffe semantics).  mask: I32 buffer of top count
+ * holding the flat h*W+w argmax (MAX only; first max wins, strict >). */
+CDNN_API int cdnn_pool_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle y,
+                               cdnn_handle mask, cdnn_handle stream);
+CDNN_API int cdnn_pool_backward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_handle mask,
+                                cdnn_handle dx, cdnn_handle stream);
+
+/* elementwise (layers.cpp:180-221); n elements */
+CDNN_API int cdnn_relu_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, uint64_t n, cdnn_handle stream);
+CDNN_API int cdnn_relu_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle dy, cdnn_handle dx,
+                                uint64_t n, cdnn_handle stream);
+CDNN_API int cdnn_sigmoid_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, uint64_t n,
+                                  cdnn_handle stream);
+CDNN_API int cdnn_sigmoid_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle dy, cdnn_handle dx,
+                                   uint64_t n, cdnn_handle stream);
+/* whole-sample softmax over `features` values per row (layers.cpp:232-266) */
+CDNN_API int cdnn_softmax_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, int rows,
+                                  int features, cdnn_handle stream);
+CDNN_API int cdnn_softmax_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle dy, cdnn_handle dx,
+                                   int rows, int features, cdnn_handle stream);
+/* SoftmaxWithLoss (Caffe): prob = softmax(x) per row; loss[0] = -sum log p_label / norm.
+ * label: same dtype as x, integral class ids.  norm = rows (normalize) or 1. */
+CDNN_API int cdnn_softmax_loss_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle label,
+                                       cdnn_handle prob, cdnn_handle loss, int rows, int classes,
+                                       int normalize, cdnn_handle stream);
+/* dx = loss_weight * (prob - onehot(label)) / norm */
+CDNN_API int cdnn_softmax_loss_backward(cdnn_ctx ctx, cdnn_handle prob, cdnn_handle label,
+                                        cdnn_handle dx, int rows, int classes, int normalize,
+                                        double loss_weight, cdnn_handle stream);
+
+/* ---- solver (solver.cpp:24-57 + Caffe momentum / weight decay) ----------- */
+typedef enum { CDNN_SOLVER_SGD = 0, CDNN_SOLVER_RMSPROP = 1 } cdnn_solver_method;
+/* One fused pass over n elements of (w, g, hist):
+ *   SGD:      g' = g + wd*w ; v = mom*v + lr*g' ; w -= v      (hist may be 0 iff mom == 0)
+ *             (mom = wd = 0 reproduces `w -= lr*g` bit for bit, solver.cpp:41-43)
+ *   RMSProp:  c = d*c + (1-d)*g*g ; w -= lr*g/(sqrt(c)+eps)     (solver.cpp:50-52)
+ * and then g = 0 (solver.cpp:55). */
+CDNN_API int cdnn_solver_apply(cdnn_ctx ctx, int method, cdnn_handle w, cdnn_handle g,
+                               cdnn_handle hist, uint64_t n, double lr, double momentum,
+                               double weight_decay, double rms_decay, double epsilon,
+                               cdnn_handle stream);
+
+/* ---- NCCL data-parallel subsystem (paper "Parallel object") */
+CDNN_API int cdnn_nccl_available(int* out);
+CDNN_API int cdnn_nccl_unique_id(uint8_t id[128]);
+CDNN_API int cdnn_nccl_comm_create(cdnn_ctx ctx, int nranks, int rank, const uint8_t id[128],
+                                   cdnn_handle* out);
+/* in-place sum all-reduce of elements [offset, offset+n) of buf */
+CDNN_API int cdnn_allreduce_sum(cdnn_ctx ctx, cdnn_handle comm, cdnn_handle buf, uint64_t offset,
+                                uint64_t n, cdnn_handle stream);
+CDNN_API int cdnn_broadcast(cdnn_ctx ctx, cdnn_handle comm, cdnn_handle buf, uint64_t n, int root,
+                            cdnn_handle stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUDADNN_H_ */

@@ -1,0 +1,96 @@
+// gemm_simt.cuh — SIMT implicit-GEMM engine for the FP64 (`real = double`)
+// build: the same operand views and epilogues as the tensor-core engine, on
+// DFMA.  64x64 output tile per 256-thread CTA, 4x4 register micro-tile,
+// 16-deep k slabs double-buffered through shared memory.  Lanes walk m, so
+// the host maps the output's contiguous index to m (coalesced stores).
+#pragma once
+
+#include <cstdint>
+
+#include "operands.cuh"
+
+namespace cdnn {
+namespace simt {
+
+constexpr int TBM = 64, TBN = 64, TBK = 16, kThreads = 256;
+
+template <typename T, class V, int ROWS>
+__device__ __forceinline__ void load_slab(const V& v, T (*s)[ROWS + 1], int row0, int k0, int t) {
+  // ROWS x TBK elements, 256 threads -> ROWS*TBK/256 each
+  constexpr int PER = ROWS * TBK / kThreads;
+  if (v.m_contig()) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = t + i * kThreads;
+      const int r = e % ROWS, k = e / ROWS;
+      s[k][r] = v.at(v.row(row0 + r), k0 + k);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = t + i * kThreads;
+      const int r = e / TBK, k = e % TBK;
+      s[k][r] = v.at(v.row(row0 + r), k0 + k);
+    }
+  }
+}
+
+template <typename T, class VA, class VB, class EPI>
+__global__ void __launch_bounds__(kThreads)
+    simt_gemm_kernel(const VA va, const VB vb, const EPI epi, int M, int N, int K, int kt_per_split) {
+  __shared__ T As[2][TBK][TBM + 1];
+  __shared__ T Bs[2][TBK][TBN + 1];
+  const int t = threadIdx.x;
+  const int tx = t % 16, ty = t / 16;
+  const int m0 = blockIdx.x * TBM, n0 = blockIdx.y * TBN;
+  const int split = blockIdx.z;
+  const int kt_total = (K + TBK - 1) / TBK;
+  const int kt_begin = split * kt_per_split;
+  const int kt_end = min(kt_total, kt_begin + kt_per_split);
+
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+
+  int buf = 0;
+  if (kt_begin < kt_end) {
+    load_slab<T, VA, TBM>(va, As[0], m0, kt_begin * TBK, t);
+    load_slab<T, VB, TBN>(vb, Bs[0], n0, kt_begin * TBK, t);
+  }
+  __syncthreads();
+  for (int kt = kt_begin; kt < kt_end; ++kt) {
+    if (kt + 1 < kt_end) {
+      load_slab<T, VA, TBM>(va, As[buf ^ 1], m0, (kt + 1) * TBK, t);
+      load_slab<T, VB, TBN>(vb, Bs[buf ^ 1], n0, (kt + 1) * TBK, t);
+    }
+#pragma unroll
+    for (int k = 0; k < TBK; ++k) {
+      T a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][k][tx + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][k][ty + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + tx + 16 * i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + ty + 16 * j;
+      if (n < N) epi.store(m, n, acc[i][j], split);
+    }
+  }
+}
+
+}  // namespace simt
+}  // namespace cdnn

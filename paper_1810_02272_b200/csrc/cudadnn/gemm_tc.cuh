@@ -1,0 +1,248 @@
+// gemm_tc.cuh — the sm_100a tensor-core implicit-GEMM engine (TF32 in, FP32 accumulate).
+//
+//   D[m][n] = sum_k A(m,k) * B(n,k)      one 128 x BN output tile per CTA,
+//                                        optional split-K over blockIdx.z
+//
+// Warp roles (192 threads):
+//   warp 0      TMA producer: one elected lane issues cp.async.bulk.tensor for
+//               operands that are K-contiguous, 16 B aligned matrices
+//   warp 1      TMEM allocator + MMA issuer: one lane issues tcgen05.mma
+//               (kind::tf32, M=128, N=BN, K=8) x4 per 32-wide k-slab and
+//               tcgen05.commit's the slab's smem slot back to the producers
+//   warps 2-5   gather producers: build the other operands (im2col / strided /
+//               transposed views, see operands.cuh) straight into the
+//               128B-swizzled K-major smem layout UMMA reads, rounding to TF32;
+//               then the epilogue: tcgen05.ld the accumulator (warp w owns TMEM
+//               lanes 32*(w%4)..+31 = tile rows) and hand each element to EPI.
+//
+// smem per stage: A 128x32 fp32 (16 KB) + B BNx32 fp32; STAGES-deep ring with
+// full/empty mbarriers; accumulator BN fp32 columns of TMEM.
+#pragma once
+
+#include <cstdint>
+
+#include "operands.cuh"
+#include "ptx.cuh"
+
+namespace cdnn {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;            // fp32 elements per 128-byte swizzle row
+constexpr int kThreads = 192;
+constexpr int kProducerThreads = 128;
+
+__host__ __device__ constexpr int tmem_cols_for(int bn) {
+  return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : bn <= 256 ? 256 : 512;
+}
+
+template <int BN, int STAGES>
+__host__ __device__ constexpr int smem_bytes() {
+  return 1024 /*align slack*/ + STAGES * (BM * BK * 4 + BN * BK * 4) + (2 * STAGES + 1) * 8 + 16;
+}
+
+// Byte offset of 16-byte chunk `kc` (0..7) of row `r` in a K-major SWIZZLE_128B tile.
+__device__ __forceinline__ uint32_t sw128(int r, int kc) {
+  return uint32_t(r) * 128u + (uint32_t((kc ^ r) & 7) << 4);
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core-matrix groups
+// 1024 B apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t make_sw128_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;              // LBO (unused for swizzled K-major)
+  d |= uint64_t(1024 >> 4) << 32;      // SBO
+  d |= uint64_t(1) << 46;              // descriptor version
+  d |= uint64_t(2) << 61;              // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=bn.
+__host__ __device__ constexpr uint32_t make_idesc_tf32(int bn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+
+// Fill one ROWS x 32 slab of operand view `v` into swizzled smem at `tile`.
+// Thread t of the 128 producers.  For row-contiguous views each thread owns
+// rows and walks k (lanes = consecutive rows -> coalesced loads); otherwise
+// 8 threads share a row, each taking 4 consecutive k.
+template <int ROWS, class V>
+__device__ __forceinline__ void gather_slab(const V& v, uint32_t tile, int row0, int k0, int t) {
+  static_assert((ROWS * 8) % kProducerThreads == 0, "slab rows must be a multiple of 16");
+  if (v.m_contig()) {
+    if constexpr (ROWS <= kProducerThreads) {
+      constexpr int KGROUPS = kProducerThreads / ROWS;   // threads sharing a row (split over k)
+      const int r = t % ROWS;
+      const auto rw = v.row(row0 + r);
+#pragma unroll
+      for (int kc = t / ROWS; kc < 8; kc += KGROUPS) {
+        const int k = k0 + kc * 4;
+        const float a = ptx::to_tf32(v.at(rw, k + 0)), b = ptx::to_tf32(v.at(rw, k + 1));
+        const float c = ptx::to_tf32(v.at(rw, k + 2)), d = ptx::to_tf32(v.at(rw, k + 3));
+        ptx::st_shared_v4(tile + sw128(r, kc), a, b, c, d);
+      }
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < ROWS / kProducerThreads; ++rr) {
+        const int r = t + rr * kProducerThreads;
+        const auto rw = v.row(row0 + r);
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc) {
+          const int k = k0 + kc * 4;
+          const float a = ptx::to_tf32(v.at(rw, k + 0)), b = ptx::to_tf32(v.at(rw, k + 1));
+          const float c = ptx::to_tf32(v.at(rw, k + 2)), d = ptx::to_tf32(v.at(rw, k + 3));
+          ptx::st_shared_v4(tile + sw128(r, kc), a, b, c, d);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ROWS * 8 / kProducerThreads; ++i) {
+      const int c = t + i * kProducerThreads;
+      const int r = c >> 3, kc = c & 7;
+      const auto rw = v.row(row0 + r);
+      const int k = k0 + kc * 4;
+      const float a = ptx::to_tf32(v.at(rw, k + 0)), b = ptx::to_tf32(v.at(rw, k + 1));
+      const float cc = ptx::to_tf32(v.at(rw, k + 2)), d = ptx::to_tf32(v.at(rw, k + 3));
+      ptx::st_shared_v4(tile + sw128(r, kc), a, b, cc, d);
+    }
+  }
+}
+
+template <class V>
+struct is_tma { static constexpr bool value = false; };
+template <>
+struct is_tma<TmaView> { static constexpr bool value = true; };
+
+template <int BN, int STAGES, class VA, class VB, class EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const VA va, const VB vb, const EPI epi, int M, int N, int K, int kt_per_split) {
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
+  constexpr bool kTmaA = is_tma<VA>::value;
+  constexpr bool kTmaB = is_tma<VB>::value;
+  constexpr uint32_t A_BYTES = BM * BK * 4;
+  constexpr uint32_t B_BYTES = BN * BK * 4;
+  constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accum = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int split = blockIdx.z;
+  const int kt_total = (K + BK - 1) / BK;
+  const int kt_begin = split * kt_per_split;
+  const int kt_end = min(kt_total, kt_begin + kt_per_split);
+  const int nkt = kt_end - kt_begin;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1 + 4);   // TMA warp + 4 producer warps
+      ptx::mbar_init(&empty[s], 1);      // tcgen05.commit
+    }
+    ptx::mbar_init(accum, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      if constexpr (kTmaA) ptx::tma_prefetch_desc(&tmA);
+      if constexpr (kTmaB) ptx::tma_prefetch_desc(&tmB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kt = 0; kt < nkt; ++kt) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        constexpr uint32_t bytes = (kTmaA ? A_BYTES : 0) + (kTmaB ? B_BYTES : 0);
+        if constexpr (bytes > 0) {
+          ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+          const int kc = (kt_begin + kt) * BK;
+          if constexpr (kTmaA) ptx::tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kc, m0);
+          if constexpr (kTmaB) ptx::tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kc, n0);
+        } else {
+          ptx::mbar_arrive(&full[stage]);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_tf32(BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kt = 0; kt < nkt; ++kt) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint64_t adesc = make_sw128_desc(ptx::smem_u32(sA + stage * A_BYTES));
+        const uint64_t bdesc = make_sw128_desc(ptx::smem_u32(sB + stage * B_BYTES));
+#pragma unroll
+        for (int j = 0; j < BK / 8; ++j) {
+          // advance 8 tf32 = 32 bytes along K inside the swizzle row
+          ptx::mma_tf32(tmem, adesc + uint64_t(2 * j), bdesc + uint64_t(2 * j), idesc,
+                        (kt > 0 || j > 0) ? 1u : 0u);
+        }
+        ptx::mma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      ptx::mma_commit(accum);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- gather producers ----------------
+    const int t = threadIdx.x - 64;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kt = 0; kt < nkt; ++kt) {
+      ptx::mbar_wait(&empty[stage], phase ^ 1);
+      const int kc = (kt_begin + kt) * BK;
+      if constexpr (!kTmaA) gather_slab<BM>(va, ptx::smem_u32(sA + stage * A_BYTES), m0, kc, t);
+      if constexpr (!kTmaB) gather_slab<BN>(vb, ptx::smem_u32(sB + stage * B_BYTES), n0, kc, t);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&full[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+    // ---------------- epilogue ----------------
+    ptx::mbar_wait(accum, 0);
+    ptx::tc_fence_after();
+    const int q = warp & 3;
+    const int m = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t r[16];
+      ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), r);
+      ptx::tmem_ld_wait();
+      if (m < M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int n = n0 + c + j;
+          if (n < N) epi.store(m, n, __uint_as_float(r[j]), split);
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+}  // namespace tc
+}  // namespace cdnn

@@ -1,0 +1,169 @@
+// internal.hpp — CudaDnn context and handle look-up tables (paper Table 3).
+//
+// One cdnn_context per device.  Every resource lives in one table keyed by a
+// monotone 64-bit id (never recycled, 0 = null; backend.hpp:17-25,
+// backend.cpp:18-26).  Table mutation is serialised by the context mutex
+// (backend.hpp:113); buffer contents are ordered by streams only.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <functional>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <variant>
+#include <vector>
+
+#include "cudadnn.h"
+#include "operands.cuh"
+
+namespace cdnn {
+
+struct Error {
+  int status;
+  std::string msg;
+};
+[[noreturn]] void fail(int status, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+#define CDNN_CUDA(x) ::cdnn::check_cuda((x), #x)
+
+size_t dtype_size(int dtype);
+
+struct DevAlloc {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = 0;
+  ~DevAlloc();
+};
+
+struct BufferSlot {
+  std::shared_ptr<DevAlloc> alloc;  // shared with views (arena sub-ranges)
+  char* dev = nullptr;              // first element of this buffer / view
+  uint64_t len = 0;
+  int dtype = CDNN_F32;
+};
+
+// Split-K partial-sum scratch bound to one stream.  Grows by allocating a new
+// block and retiring (not freeing) the old one, so CUDA graphs captured
+// against an older block stay valid for the context's lifetime.
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  std::vector<std::shared_ptr<DevAlloc>> blocks;
+  void* get(size_t need, int device);
+};
+
+struct StreamSlot {
+  cudaStream_t s = nullptr;
+  std::shared_ptr<Workspace> ws;
+};
+
+struct ConvDescSlot {
+  cdnn_conv_params p{};
+  int P = 0, Q = 0;
+  ConvGeom geom{};
+  int Kc = 0;    // Cg*R*S   (forward reduction / backward-filter rows)
+  int Kd = 0;    // Cog*R*S  (backward-data reduction)
+  std::shared_ptr<DevAlloc> tables;  // taps | dtaps | koff
+  ConvTap* taps = nullptr;
+  DgradTap* dtaps = nullptr;
+  int* koff = nullptr;
+};
+
+struct PoolDescSlot {
+  cdnn_pool_params p{};
+  int PH = 0, PW = 0;
+};
+
+struct RngSlot {
+  std::mt19937_64 engine;
+};
+
+struct NcclSlot {
+  void* comm = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0;
+};
+
+struct GraphSlot {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct EventSlot {
+  cudaEvent_t ev = nullptr;
+};
+
+using Slot = std::variant<BufferSlot, StreamSlot, ConvDescSlot, PoolDescSlot, RngSlot, NcclSlot,
+                          GraphSlot, EventSlot>;
+
+}  // namespace cdnn
+
+struct cdnn_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // the context's own compute stream (handle 0)
+  std::shared_ptr<cdnn::Workspace> ws;
+  std::mutex mu;
+  uint64_t next_id = 1;
+  std::unordered_map<uint64_t, cdnn::Slot> slots;
+  std::atomic<uint64_t> launches{0};
+  std::mutex tmap_mu;
+  std::unordered_map<std::string, CUtensorMap> tmaps;
+};
+
+namespace cdnn {
+
+using Ctx = cdnn_context;
+
+// RAII: make the context's device current for the duration of an entry point.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(Ctx* c);
+  ~DeviceGuard();
+};
+
+uint64_t insert_slot(Ctx* c, Slot s);
+BufferSlot& buffer(Ctx* c, cdnn_handle h, const char* what);
+BufferSlot* buffer_or_null(Ctx* c, cdnn_handle h, const char* what);
+ConvDescSlot& conv_desc(Ctx* c, cdnn_handle h);
+PoolDescSlot& pool_desc(Ctx* c, cdnn_handle h);
+RngSlot& rng(Ctx* c, cdnn_handle h);
+NcclSlot& nccl(Ctx* c, cdnn_handle h);
+cudaStream_t stream_of(Ctx* c, cdnn_handle h);
+Workspace& workspace_of(Ctx* c, cdnn_handle h);
+void require_len(const BufferSlot& b, uint64_t n, const char* what);
+void require_dtype(const BufferSlot& b, int dtype, const char* what);
+
+// Kernel launch bookkeeping + error check after every launch.
+void count_launch(Ctx* c, int n = 1);
+void check_launch(const char* what);
+
+// Tensor map for a row-major fp32 matrix [rows][K] (row stride ld elements),
+// box {32 k, box_rows}, 128B swizzle.  Cached per (ptr, shape, box).
+const CUtensorMap* tmap_k_major(Ctx* c, const float* ptr, int rows, int K, int64_t ld,
+                                int box_rows);
+
+// Plain GEMM-shaped launches shared by gemm / ip / conv (ops_gemm.cu).
+struct GemmPlan {
+  int bn = 128;
+  int splits = 1;
+  int kt_per_split = 1;
+};
+GemmPlan plan_tc(int M, int N, int K);
+GemmPlan plan_simt(int M, int N, int K);
+
+// Runs f under the C-ABI error guard; returns the cdnn_status.
+int guarded(const std::function<void()>& f);
+Ctx* need_ctx(cdnn_ctx c);
+
+// nccl.cu: destroys a communicator held in an NcclSlot.
+void nccl_destroy(void* comm);
+
+}  // namespace cdnn

@@ -1,0 +1,128 @@
+// launch.cuh — host-side planning and launch of the two implicit-GEMM engines.
+//
+// run_tc:   float  -> tcgen05 TF32 engine (gemm_tc.cuh), TMA for eligible operands
+// run_simt: double -> SIMT FP64 engine (gemm_simt.cuh)
+// Both split K over blockIdx.z when the output has too few tiles to fill the
+// 148 SMs; partial tiles go to the stream's workspace and a second kernel
+// reduces them in fixed split order (deterministic, no float atomics) while
+// applying the op's epilogue.
+#pragma once
+
+#include <cstring>
+
+#include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
+#include "internal.hpp"
+
+namespace cdnn {
+
+constexpr int kNumSMs = 148;
+
+// A request to load a K-contiguous fp32 operand with TMA.
+struct TmaReq {
+  const float* p = nullptr;
+  int rows = 0, K = 0;
+  int64_t ld = 0;
+};
+
+inline bool tma_eligible(const float* p, int rows, int K, int64_t ld, int box_rows) {
+  return p && (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * 4) % 16 == 0) && K >= 32 &&
+         rows >= box_rows && ld >= K;
+}
+
+template <typename T, class EPI>
+__global__ void reduce_splits_kernel(const T* __restrict__ ws, int M, int N, int splits, EPI epi) {
+  const int64_t total = int64_t(M) * N;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int m = int(idx % M), n = int(idx / M);
+    T s = T(0);
+    for (int z = 0; z < splits; ++z) s += ws[(int64_t(z) * N + n) * M + m];
+    epi.store(m, n, s, 0);
+  }
+}
+
+inline int grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  return int(std::min<int64_t>(b, int64_t(kNumSMs) * 32));
+}
+
+template <int BN, class VA, class VB, class EPI>
+void launch_tc_kernel(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& ta,
+                      const CUtensorMap& tb, const VA& va, const VB& vb, const EPI& epi, int M,
+                      int N, int K, int kt_per_split) {
+  constexpr int ST = 4;
+  constexpr int smem = tc::smem_bytes<BN, ST>();
+  auto kern = tc::tc_gemm_kernel<BN, ST, VA, VB, EPI>;
+  static bool attr_set[16] = {};
+  if (!attr_set[c->device & 15]) {
+    CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set[c->device & 15] = true;
+  }
+  kern<<<grid, tc::kThreads, smem, st>>>(ta, tb, va, vb, epi, M, N, K, kt_per_split);
+  check_launch("tc_gemm_kernel");
+  count_launch(c);
+}
+
+template <int BN, class VA, class VB, class EPI>
+void run_tc_bn(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
+               const VA& va, const VB& vb, const EPI& epi, const TmaReq& ra, const TmaReq& rb) {
+  CUtensorMap ta, tb;
+  std::memset(&ta, 0, sizeof ta);
+  std::memset(&tb, 0, sizeof tb);
+  if (tc::is_tma<VA>::value) ta = *tmap_k_major(c, ra.p, ra.rows, ra.K, ra.ld, tc::BM);
+  if (tc::is_tma<VB>::value) tb = *tmap_k_major(c, rb.p, rb.rows, rb.K, rb.ld, BN);
+  dim3 grid((M + tc::BM - 1) / tc::BM, (N + BN - 1) / BN, pl.splits);
+  if (pl.splits == 1) {
+    launch_tc_kernel<BN>(c, st, grid, ta, tb, va, vb, epi, M, N, K, pl.kt_per_split);
+  } else {
+    float* wsp = static_cast<float*>(ws.get(size_t(pl.splits) * M * N * sizeof(float), c->device));
+    PartialEpi<float> pe{wsp, M, N};
+    launch_tc_kernel<BN>(c, st, grid, ta, tb, va, vb, pe, M, N, K, pl.kt_per_split);
+    reduce_splits_kernel<float, EPI><<<grid_for(int64_t(M) * N, 256), 256, 0, st>>>(wsp, M, N, pl.splits, epi);
+    check_launch("reduce_splits_kernel");
+    count_launch(c);
+  }
+}
+
+template <class VA, class VB, class EPI>
+void run_tc(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
+            const VA& va, const VB& vb, const EPI& epi, const TmaReq& ra = {}, const TmaReq& rb = {}) {
+  switch (pl.bn) {
+    case 32: run_tc_bn<32>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
+    case 64: run_tc_bn<64>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
+    default: run_tc_bn<128>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
+  }
+}
+
+// Dense fp32 operand -> TMA when it is K-contiguous and aligned, gather otherwise.
+template <class F>
+void with_operand(const DenseView<float>& v, int box_rows, TmaReq& req, F&& f) {
+  if (!v.mcontig && v.sk == 1 && tma_eligible(v.p, v.rows, v.K, v.sr, box_rows)) {
+    req = TmaReq{v.p, v.rows, v.K, v.sr};
+    f(TmaView{});
+  } else {
+    f(v);
+  }
+}
+
+template <typename T, class VA, class VB, class EPI>
+void run_simt(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
+              const VA& va, const VB& vb, const EPI& epi) {
+  dim3 grid((M + simt::TBM - 1) / simt::TBM, (N + simt::TBN - 1) / simt::TBN, pl.splits);
+  if (pl.splits == 1) {
+    simt::simt_gemm_kernel<T, VA, VB, EPI><<<grid, simt::kThreads, 0, st>>>(va, vb, epi, M, N, K, pl.kt_per_split);
+    check_launch("simt_gemm_kernel");
+    count_launch(c);
+  } else {
+    T* wsp = static_cast<T*>(ws.get(size_t(pl.splits) * M * N * sizeof(T), c->device));
+    PartialEpi<T> pe{wsp, M, N};
+    simt::simt_gemm_kernel<T, VA, VB, PartialEpi<T>><<<grid, simt::kThreads, 0, st>>>(va, vb, pe, M, N, K, pl.kt_per_split);
+    check_launch("simt_gemm_kernel");
+    reduce_splits_kernel<T, EPI><<<grid_for(int64_t(M) * N, 256), 256, 0, st>>>(wsp, M, N, pl.splits, epi);
+    check_launch("reduce_splits_kernel");
+    count_launch(c, 2);
+  }
+}
+
+}  // namespace cdnn

@@ -1,0 +1,600 @@
+// ops_elem.cu — bandwidth-bound kernels: BLAS-1 (backend.cpp:131-167), ReLU /
+// Sigmoid / Softmax (layers.cpp:180-266), SoftmaxWithLoss (Caffe) and the fused
+// solver update (solver.cpp:24-57 + Caffe momentum / weight decay).
+//
+// Elementwise kernels are grid-stride with 128-bit vector access when the
+// buffers are 16-byte aligned; products that the reference rounds separately
+// use explicit _rn intrinsics so FMA contraction cannot change the result
+// (scal, axpy, SGD are bit-identical to the reference's x86 build).
+#include "launch.cuh"
+
+namespace cdnn {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
+template <> __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+template <typename T> __device__ __forceinline__ T sub_rn(T a, T b);
+template <> __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+template <> __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
+__global__ void fill_kernel(T* __restrict__ d, uint64_t n, T v) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) d[i] = v;
+}
+template <typename T>
+__global__ void copy_kernel(const T* __restrict__ s, T* __restrict__ d, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) d[i] = s[i];
+}
+template <typename T>
+__global__ void scal_kernel(T* __restrict__ x, uint64_t n, T a) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) x[i] = mul_rn(x[i], a);
+}
+template <typename T>
+__global__ void axpy_kernel(const T* __restrict__ x, T* __restrict__ y, uint64_t n, T a) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    y[i] = add_rn(y[i], mul_rn(a, x[i]));
+}
+// Deterministic dot: fixed grid, per-block tree, then one block sums partials in order.
+template <typename T>
+__global__ void dot_partial_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, T* __restrict__ part) {
+  __shared__ T sh[kThreads];
+  T s = T(0);
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) s += x[i] * y[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+template <typename T>
+__global__ void sum_partials_kernel(const T* __restrict__ part, int n, T* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    T s = T(0);
+    for (int i = 0; i < n; ++i) s += part[i];
+    *out = s;
+  }
+}
+
+// ---- activations (layers.cpp:180-221) ----------------------------------------
+template <typename T>
+__global__ void relu_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, uint64_t n) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if constexpr (std::is_same_v<T, float>) {
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) % 16 == 0) {
+      const uint64_t n4 = n / 4;
+      for (uint64_t j = i; j < n4; j += stride) {
+        float4 v = reinterpret_cast<const float4*>(x)[j];
+        v.x = v.x > 0.f ? v.x : 0.f; v.y = v.y > 0.f ? v.y : 0.f;
+        v.z = v.z > 0.f ? v.z : 0.f; v.w = v.w > 0.f ? v.w : 0.f;
+        reinterpret_cast<float4*>(y)[j] = v;
+      }
+      for (uint64_t j = n4 * 4 + i; j < n; j += stride) y[j] = x[j] > 0.f ? x[j] : 0.f;
+      return;
+    }
+  }
+  for (; i < n; i += stride) y[i] = x[i] > T(0) ? x[i] : T(0);
+}
+template <typename T>
+__global__ void relu_bwd_kernel(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dx, uint64_t n) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if constexpr (std::is_same_v<T, float>) {
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx)) % 16 == 0) {
+      const uint64_t n4 = n / 4;
+      for (uint64_t j = i; j < n4; j += stride) {
+        const float4 a = reinterpret_cast<const float4*>(x)[j];
+        float4 g = reinterpret_cast<const float4*>(dy)[j];
+        g.x = a.x > 0.f ? g.x : 0.f; g.y = a.y > 0.f ? g.y : 0.f;
+        g.z = a.z > 0.f ? g.z : 0.f; g.w = a.w > 0.f ? g.w : 0.f;
+        reinterpret_cast<float4*>(dx)[j] = g;
+      }
+      for (uint64_t j = n4 * 4 + i; j < n; j += stride) dx[j] = x[j] > 0.f ? dy[j] : 0.f;
+      return;
+    }
+  }
+  for (; i < n; i += stride) dx[i] = x[i] > T(0) ? dy[i] : T(0);
+}
+template <typename T>
+__global__ void sigmoid_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    y[i] = T(1) / (T(1) + exp(-x[i]));
+}
+template <typename T>
+__global__ void sigmoid_bwd_kernel(const T* __restrict__ y, const T* __restrict__ dy, T* __restrict__ dx, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const T v = y[i];
+    dx[i] = mul_rn(mul_rn(dy[i], v), sub_rn(T(1), v));  // td * y * (1 - y), left to right
+  }
+}
+
+// ---- softmax (whole sample, layers.cpp:232-266): one warp per row -------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <typename T>
+__global__ void softmax_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, int rows, int f) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
+    const T* xr = x + int64_t(r) * f;
+    T* yr = y + int64_t(r) * f;
+    T m = xr[0];
+    for (int i = lane; i < f; i += 32) m = max(m, xr[i]);
+    m = warp_max(m);
+    T s = T(0);
+    for (int i = lane; i < f; i += 32) { const T e = exp(xr[i] - m); yr[i] = e; s += e; }
+    s = warp_sum(s);
+    __syncwarp();
+    for (int i = lane; i < f; i += 32) yr[i] = yr[i] / s;
+  }
+}
+template <typename T>
+__global__ void softmax_bwd_kernel(const T* __restrict__ y, const T* __restrict__ dy, T* __restrict__ dx, int rows, int f) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
+    const T* yr = y + int64_t(r) * f;
+    const T* gr = dy + int64_t(r) * f;
+    T* dr = dx + int64_t(r) * f;
+    T w = T(0);
+    for (int i = lane; i < f; i += 32) w += gr[i] * yr[i];
+    w = warp_sum(w);
+    for (int i = lane; i < f; i += 32) dr[i] = yr[i] * (gr[i] - w);
+  }
+}
+
+// SoftmaxWithLoss forward: prob rows + per-row -log(max(p_label, FLT_MIN)).
+template <typename T>
+__global__ void softmax_loss_fwd_kernel(const T* __restrict__ x, const T* __restrict__ label, T* __restrict__ prob,
+                                        T* __restrict__ row_loss, int rows, int f) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
+    const T* xr = x + int64_t(r) * f;
+    T* pr = prob + int64_t(r) * f;
+    T m = xr[0];
+    for (int i = lane; i < f; i += 32) m = max(m, xr[i]);
+    m = warp_max(m);
+    T s = T(0);
+    for (int i = lane; i < f; i += 32) { const T e = exp(xr[i] - m); pr[i] = e; s += e; }
+    s = warp_sum(s);
+    __syncwarp();
+    for (int i = lane; i < f; i += 32) pr[i] = pr[i] / s;
+    __syncwarp();
+    if (lane == 0) {
+      const int lab = static_cast<int>(label[r]);
+      const T p = (lab >= 0 && lab < f) ? pr[lab] : T(0);
+      const T floor_v = sizeof(T) == 4 ? T(1.17549435e-38f) : T(1.17549435e-38f);  // Caffe FLT_MIN
+      row_loss[r] = -log(max(p, floor_v));
+    }
+  }
+}
+template <typename T>
+__global__ void loss_reduce_kernel(const T* __restrict__ row_loss, int rows, T scale, T* __restrict__ out) {
+  __shared__ T sh[kThreads];
+  T s = T(0);
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) s += row_loss[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0] * scale;
+}
+template <typename T>
+__global__ void softmax_loss_bwd_kernel(const T* __restrict__ prob, const T* __restrict__ label, T* __restrict__ dx,
+                                        int rows, int f, T scale) {
+  const int64_t n = int64_t(rows) * f;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(i / f), j = int(i - int64_t(r) * f);
+    const int lab = static_cast<int>(label[r]);
+    dx[i] = (prob[i] - (j == lab ? T(1) : T(0))) * scale;
+  }
+}
+
+// ---- solver: one fused pass, then the gradient is zeroed (solver.cpp:39-55) ----
+template <typename T>
+__global__ void sgd_kernel(T* __restrict__ w, T* __restrict__ g, T* __restrict__ v, uint64_t n, T lr, T mom, T wd) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    T gi = g[i];
+    if (wd != T(0)) gi = add_rn(gi, mul_rn(wd, w[i]));
+    T step = mul_rn(lr, gi);
+    if (v) {
+      if (mom != T(0)) step = add_rn(mul_rn(mom, v[i]), step);
+      v[i] = step;
+    }
+    w[i] = sub_rn(w[i], step);
+    g[i] = T(0);
+  }
+}
+template <typename T>
+__global__ void sgd_vec4_kernel(float4* __restrict__ w, float4* __restrict__ g, float4* __restrict__ v, uint64_t n4,
+                                float lr, float mom, float wd) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 wi = w[i], gi = g[i];
+    float4 vi = v ? v[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    auto upd = [&](float& ww, float gg, float& vv) {
+      if (wd != 0.f) gg = __fadd_rn(gg, __fmul_rn(wd, ww));
+      float step = __fmul_rn(lr, gg);
+      if (mom != 0.f) step = __fadd_rn(__fmul_rn(mom, vv), step);
+      vv = step;
+      ww = __fsub_rn(ww, step);
+    };
+    upd(wi.x, gi.x, vi.x); upd(wi.y, gi.y, vi.y); upd(wi.z, gi.z, vi.z); upd(wi.w, gi.w, vi.w);
+    w[i] = wi;
+    if (v) v[i] = vi;
+    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+template <typename T>
+__global__ void rmsprop_kernel(T* __restrict__ w, T* __restrict__ g, T* __restrict__ c, uint64_t n, T lr, T d, T eps) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const T gi = g[i];
+    // cache = d*cache + (1-d)*g*g ; w -= lr*g / (sqrt(cache) + eps)  (solver.cpp:50-52)
+    const T ci = add_rn(mul_rn(d, c[i]), mul_rn(mul_rn(sub_rn(T(1), d), gi), gi));
+    c[i] = ci;
+    w[i] = sub_rn(w[i], mul_rn(lr, gi) / add_rn(sqrt(ci), eps));
+    g[i] = T(0);
+  }
+}
+
+int blocks_for(uint64_t n) {
+  return int(std::max<uint64_t>(1, std::min<uint64_t>((n + kThreads - 1) / kThreads, uint64_t(kNumSMs) * 8)));
+}
+
+template <class F>
+void by_dtype(int dtype, const char* what, F&& f) {
+  if (dtype == CDNN_F32) f(float{});
+  else if (dtype == CDNN_F64) f(double{});
+  else fail(CDNN_INVALID_ARGUMENT, std::string(what) + ": floating buffers required");
+}
+
+template <typename T>
+T* dptr(const BufferSlot& b) { return reinterpret_cast<T*>(b.dev); }
+
+}  // namespace
+
+// Shared with dispatch.cu.
+double dot_sync(Ctx* c, uint64_t n, BufferSlot& X, BufferSlot& Y) {
+  double result = 0;
+  DeviceGuard g(c);
+  by_dtype(X.dtype, "dot", [&](auto tag) {
+    using T = decltype(tag);
+    constexpr int kBlocks = 256;
+    Workspace& ws = *c->ws;
+    T* part = static_cast<T*>(ws.get((kBlocks + 1) * sizeof(T), c->device));
+    dot_partial_kernel<T><<<kBlocks, kThreads, 0, c->stream>>>(dptr<T>(X), dptr<T>(Y), n, part);
+    sum_partials_kernel<T><<<1, 32, 0, c->stream>>>(part, kBlocks, part + kBlocks);
+    check_launch("dot");
+    count_launch(c, 2);
+    T r;
+    CDNN_CUDA(cudaMemcpyAsync(&r, part + kBlocks, sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    CDNN_CUDA(cudaStreamSynchronize(c->stream));
+    result = static_cast<double>(r);
+  });
+  return result;
+}
+
+}  // namespace cdnn
+
+using namespace cdnn;
+
+extern "C" {
+
+int cdnn_fill(cdnn_ctx ctx, cdnn_handle dst, uint64_t n, double value, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& D = buffer(c, dst, "fill");
+    require_len(D, n, "fill");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    cudaStream_t st = stream_of(c, stream);
+    if (D.dtype == CDNN_I32) {
+      fill_kernel<int><<<blocks_for(n), kThreads, 0, st>>>(dptr<int>(D), n, int(value));
+    } else {
+      by_dtype(D.dtype, "fill", [&](auto tag) {
+        using T = decltype(tag);
+        fill_kernel<T><<<blocks_for(n), kThreads, 0, st>>>(dptr<T>(D), n, T(value));
+      });
+    }
+    check_launch("fill");
+    count_launch(c);
+  });
+}
+
+int cdnn_copy(cdnn_ctx ctx, cdnn_handle src, cdnn_handle dst, uint64_t n, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& S = buffer(c, src, "copy");
+    BufferSlot& D = buffer(c, dst, "copy");
+    require_len(S, n, "copy");
+    require_len(D, n, "copy");
+    require_dtype(D, S.dtype, "copy");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    cudaStream_t st = stream_of(c, stream);
+    if (S.dtype == CDNN_I32) copy_kernel<int><<<blocks_for(n), kThreads, 0, st>>>(dptr<int>(S), dptr<int>(D), n);
+    else by_dtype(S.dtype, "copy", [&](auto tag) {
+      using T = decltype(tag);
+      copy_kernel<T><<<blocks_for(n), kThreads, 0, st>>>(dptr<T>(S), dptr<T>(D), n);
+    });
+    check_launch("copy");
+    count_launch(c);
+  });
+}
+
+int cdnn_scal(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& X = buffer(c, x, "scal");
+    require_len(X, n, "scal");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(X.dtype, "scal", [&](auto tag) {
+      using T = decltype(tag);
+      scal_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(X), n, T(alpha));
+    });
+    check_launch("scal");
+    count_launch(c);
+  });
+}
+
+int cdnn_axpy(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cdnn_handle y, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& X = buffer(c, x, "axpy");
+    BufferSlot& Y = buffer(c, y, "axpy");
+    require_len(X, n, "axpy");
+    require_len(Y, n, "axpy");
+    require_dtype(Y, X.dtype, "axpy");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(X.dtype, "axpy", [&](auto tag) {
+      using T = decltype(tag);
+      axpy_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(X), dptr<T>(Y), n, T(alpha));
+    });
+    check_launch("axpy");
+    count_launch(c);
+  });
+}
+
+int cdnn_dot(cdnn_ctx ctx, uint64_t n, cdnn_handle x, cdnn_handle y, double* result) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& X = buffer(c, x, "dot");
+    BufferSlot& Y = buffer(c, y, "dot");
+    require_len(X, n, "dot");
+    require_len(Y, n, "dot");
+    require_dtype(Y, X.dtype, "dot");
+    if (!result) fail(CDNN_INVALID_ARGUMENT, "dot: null result");
+    *result = n == 0 ? 0.0 : dot_sync(c, n, X, Y);
+  });
+}
+
+int cdnn_relu_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, uint64_t n, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& X = buffer(c, x, "relu x");
+    BufferSlot& Y = buffer(c, y, "relu y");
+    require_len(X, n, "relu x"); require_len(Y, n, "relu y"); require_dtype(Y, X.dtype, "relu");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(X.dtype, "relu", [&](auto tag) {
+      using T = decltype(tag);
+      relu_fwd_kernel<T><<<blocks_for(n / 4 + 1), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(X), dptr<T>(Y), n);
+    });
+    check_launch("relu_fwd");
+    count_launch(c);
+  });
+}
+
+int cdnn_relu_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle dy, cdnn_handle dx, uint64_t n, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& X = buffer(c, x, "relu_bwd x");
+    BufferSlot& DY = buffer(c, dy, "relu_bwd dy");
+    BufferSlot& DX = buffer(c, dx, "relu_bwd dx");
+    require_len(X, n, "relu_bwd"); require_len(DY, n, "relu_bwd"); require_len(DX, n, "relu_bwd");
+    require_dtype(DY, X.dtype, "relu_bwd"); require_dtype(DX, X.dtype, "relu_bwd");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(X.dtype, "relu_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      relu_bwd_kernel<T><<<blocks_for(n / 4 + 1), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(X), dptr<T>(DY), dptr<T>(DX), n);
+    });
+    check_launch("relu_bwd");
+    count_launch(c);
+  });
+}
+
+int cdnn_sigmoid_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, uint64_t n, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& X = buffer(c, x, "sigmoid x");
+    BufferSlot& Y = buffer(c, y, "sigmoid y");
+    require_len(X, n, "sigmoid"); require_len(Y, n, "sigmoid"); require_dtype(Y, X.dtype, "sigmoid");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(X.dtype, "sigmoid", [&](auto tag) {
+      using T = decltype(tag);
+      sigmoid_fwd_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(X), dptr<T>(Y), n);
+    });
+    check_launch("sigmoid_fwd");
+    count_launch(c);
+  });
+}
+
+int cdnn_sigmoid_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle dy, cdnn_handle dx, uint64_t n, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& Y = buffer(c, y, "sigmoid_bwd y");
+    BufferSlot& DY = buffer(c, dy, "sigmoid_bwd dy");
+    BufferSlot& DX = buffer(c, dx, "sigmoid_bwd dx");
+    require_len(Y, n, "sigmoid_bwd"); require_len(DY, n, "sigmoid_bwd"); require_len(DX, n, "sigmoid_bwd");
+    require_dtype(DY, Y.dtype, "sigmoid_bwd"); require_dtype(DX, Y.dtype, "sigmoid_bwd");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(Y.dtype, "sigmoid_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      sigmoid_bwd_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(Y), dptr<T>(DY), dptr<T>(DX), n);
+    });
+    check_launch("sigmoid_bwd");
+    count_launch(c);
+  });
+}
+
+int cdnn_softmax_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, int rows, int f, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (rows <= 0 || f <= 0) fail(CDNN_INVALID_ARGUMENT, "softmax: extents must be positive");
+    BufferSlot& X = buffer(c, x, "softmax x");
+    BufferSlot& Y = buffer(c, y, "softmax y");
+    const uint64_t n = uint64_t(rows) * f;
+    require_len(X, n, "softmax"); require_len(Y, n, "softmax"); require_dtype(Y, X.dtype, "softmax");
+    DeviceGuard g(c);
+    by_dtype(X.dtype, "softmax", [&](auto tag) {
+      using T = decltype(tag);
+      softmax_fwd_kernel<T><<<std::min((rows + 7) / 8, kNumSMs * 16), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(X), dptr<T>(Y), rows, f);
+    });
+    check_launch("softmax_fwd");
+    count_launch(c);
+  });
+}
+
+int cdnn_softmax_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle dy, cdnn_handle dx, int rows, int f,
+                          cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (rows <= 0 || f <= 0) fail(CDNN_INVALID_ARGUMENT, "softmax_bwd: extents must be positive");
+    BufferSlot& Y = buffer(c, y, "softmax_bwd y");
+    BufferSlot& DY = buffer(c, dy, "softmax_bwd dy");
+    BufferSlot& DX = buffer(c, dx, "softmax_bwd dx");
+    const uint64_t n = uint64_t(rows) * f;
+    require_len(Y, n, "softmax_bwd"); require_len(DY, n, "softmax_bwd"); require_len(DX, n, "softmax_bwd");
+    require_dtype(DY, Y.dtype, "softmax_bwd"); require_dtype(DX, Y.dtype, "softmax_bwd");
+    DeviceGuard g(c);
+    by_dtype(Y.dtype, "softmax_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      softmax_bwd_kernel<T><<<std::min((rows + 7) / 8, kNumSMs * 16), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(Y), dptr<T>(DY), dptr<T>(DX), rows, f);
+    });
+    check_launch("softmax_bwd");
+    count_launch(c);
+  });
+}
+
+int cdnn_softmax_loss_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle label, cdnn_handle prob, cdnn_handle loss,
+                              int rows, int classes, int normalize, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (rows <= 0 || classes <= 0) fail(CDNN_INVALID_ARGUMENT, "softmax_loss: extents must be positive");
+    BufferSlot& X = buffer(c, x, "softmax_loss x");
+    BufferSlot& L = buffer(c, label, "softmax_loss label");
+    BufferSlot& P = buffer(c, prob, "softmax_loss prob");
+    BufferSlot& O = buffer(c, loss, "softmax_loss loss");
+    const uint64_t n = uint64_t(rows) * classes;
+    require_len(X, n, "softmax_loss x"); require_len(P, n, "softmax_loss prob");
+    require_len(L, uint64_t(rows), "softmax_loss label"); require_len(O, 1, "softmax_loss loss");
+    for (BufferSlot* b : {&L, &P, &O}) require_dtype(*b, X.dtype, "softmax_loss");
+    DeviceGuard g(c);
+    cudaStream_t st = stream_of(c, stream);
+    Workspace& ws = workspace_of(c, stream);
+    by_dtype(X.dtype, "softmax_loss", [&](auto tag) {
+      using T = decltype(tag);
+      T* row_loss = static_cast<T*>(ws.get(size_t(rows) * sizeof(T), c->device));
+      softmax_loss_fwd_kernel<T><<<std::min((rows + 7) / 8, kNumSMs * 16), kThreads, 0, st>>>(
+          dptr<T>(X), dptr<T>(L), dptr<T>(P), row_loss, rows, classes);
+      loss_reduce_kernel<T><<<1, kThreads, 0, st>>>(row_loss, rows, normalize ? T(1) / T(rows) : T(1), dptr<T>(O));
+    });
+    check_launch("softmax_loss_fwd");
+    count_launch(c, 2);
+  });
+}
+
+int cdnn_softmax_loss_backward(cdnn_ctx ctx, cdnn_handle prob, cdnn_handle label, cdnn_handle dx, int rows,
+                               int classes, int normalize, double loss_weight, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (rows <= 0 || classes <= 0) fail(CDNN_INVALID_ARGUMENT, "softmax_loss_bwd: extents must be positive");
+    BufferSlot& P = buffer(c, prob, "softmax_loss_bwd prob");
+    BufferSlot& L = buffer(c, label, "softmax_loss_bwd label");
+    BufferSlot& DX = buffer(c, dx, "softmax_loss_bwd dx");
+    const uint64_t n = uint64_t(rows) * classes;
+    require_len(P, n, "softmax_loss_bwd"); require_len(DX, n, "softmax_loss_bwd");
+    require_len(L, uint64_t(rows), "softmax_loss_bwd label");
+    require_dtype(L, P.dtype, "softmax_loss_bwd"); require_dtype(DX, P.dtype, "softmax_loss_bwd");
+    DeviceGuard g(c);
+    by_dtype(P.dtype, "softmax_loss_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      const T scale = T(loss_weight) / (normalize ? T(rows) : T(1));
+      softmax_loss_bwd_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(
+          dptr<T>(P), dptr<T>(L), dptr<T>(DX), rows, classes, scale);
+    });
+    check_launch("softmax_loss_bwd");
+    count_launch(c);
+  });
+}
+
+int cdnn_solver_apply(cdnn_ctx ctx, int method, cdnn_handle w, cdnn_handle g, cdnn_handle hist, uint64_t n,
+                      double lr, double momentum, double weight_decay, double rms_decay, double epsilon,
+                      cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& W = buffer(c, w, "solver w");
+    BufferSlot& G = buffer(c, g, "solver g");
+    BufferSlot* H = buffer_or_null(c, hist, "solver history");
+    require_len(W, n, "solver w"); require_len(G, n, "solver g");
+    require_dtype(G, W.dtype, "solver");
+    if (H) { require_len(*H, n, "solver history"); require_dtype(*H, W.dtype, "solver"); }
+    if (method == CDNN_SOLVER_RMSPROP && !H) fail(CDNN_INVALID_ARGUMENT, "solver: RMSProp needs a cache buffer");
+    if (method == CDNN_SOLVER_SGD && momentum != 0.0 && !H) fail(CDNN_INVALID_ARGUMENT, "solver: momentum needs a history buffer");
+    if (method != CDNN_SOLVER_SGD && method != CDNN_SOLVER_RMSPROP) fail(CDNN_INVALID_ARGUMENT, "solver: unknown method");
+    if (n == 0) return;
+    DeviceGuard dg(c);
+    cudaStream_t st = stream_of(c, stream);
+    by_dtype(W.dtype, "solver", [&](auto tag) {
+      using T = decltype(tag);
+      T* hp = H ? dptr<T>(*H) : nullptr;
+      if (method == CDNN_SOLVER_SGD) {
+        const bool vec = std::is_same_v<T, float> && n % 4 == 0 &&
+                         ((reinterpret_cast<uintptr_t>(W.dev) | reinterpret_cast<uintptr_t>(G.dev) |
+                           reinterpret_cast<uintptr_t>(hp)) % 16 == 0);
+        if (vec) {
+          sgd_vec4_kernel<float><<<blocks_for(n / 4), kThreads, 0, st>>>(
+              reinterpret_cast<float4*>(W.dev), reinterpret_cast<float4*>(G.dev), reinterpret_cast<float4*>(hp),
+              n / 4, float(lr), float(momentum), float(weight_decay));
+        } else {
+          sgd_kernel<T><<<blocks_for(n), kThreads, 0, st>>>(dptr<T>(W), dptr<T>(G), hp, n, T(lr), T(momentum),
+                                                             T(weight_decay));
+        }
+      } else {
+        rmsprop_kernel<T><<<blocks_for(n), kThreads, 0, st>>>(dptr<T>(W), dptr<T>(G), hp, n, T(lr), T(rms_decay),
+                                                               T(epsilon));
+      }
+    });
+    check_launch("solver");
+    count_launch(c);
+  });
+}
+
+}  // extern "C"

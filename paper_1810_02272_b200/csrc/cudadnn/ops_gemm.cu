@@ -1,0 +1,194 @@
+// ops_gemm.cu — kernels::gemm (backend.cpp:169-197) and the InnerProduct layer
+// (layers.cpp:124-169) on the implicit-GEMM engines.
+//
+// Orientation: the engines store D with lanes walking m, so every op maps the
+// output's contiguous index to m:
+//   gemm     C[i][j]   (row-major)      m = j, n = i
+//   ip fwd   top[b][o] = x W^T + bias  m = o, n = b, K = input_dim
+//   ip wgrad dW[o][k] += dY^T X        m = k, n = o, K = batch
+//   ip dgrad dX[b][k]  = dY W           m = k, n = b, K = num_output
+#include "launch.cuh"
+
+namespace cdnn {
+
+GemmPlan plan_tc(int M, int N, int K) {
+  GemmPlan p;
+  p.bn = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
+  const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + p.bn - 1) / p.bn);
+  const int kt = (K + tc::BK - 1) / tc::BK;
+  int splits = 1;
+  if (tiles < kNumSMs && kt >= 8) {
+    splits = std::min(kt / 4, (2 * kNumSMs + tiles - 1) / tiles);
+    splits = std::max(splits, 1);
+  }
+  p.kt_per_split = (kt + splits - 1) / splits;
+  p.splits = (kt + p.kt_per_split - 1) / p.kt_per_split;
+  return p;
+}
+
+GemmPlan plan_simt(int M, int N, int K) {
+  GemmPlan p;
+  p.bn = simt::TBN;
+  const int tiles = ((M + simt::TBM - 1) / simt::TBM) * ((N + simt::TBN - 1) / simt::TBN);
+  const int kt = (K + simt::TBK - 1) / simt::TBK;
+  int splits = 1;
+  if (tiles < 2 * kNumSMs && kt >= 16) {
+    splits = std::min(kt / 8, (4 * kNumSMs + tiles - 1) / tiles);
+    splits = std::max(splits, 1);
+  }
+  p.kt_per_split = (kt + splits - 1) / splits;
+  p.splits = (kt + p.kt_per_split - 1) / p.kt_per_split;
+  return p;
+}
+
+// One GEMM D[m][n] = sum_k A(m,k) B(n,k) with dense views, routed by dtype.
+template <typename T>
+static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const DenseView<T>& va,
+                       const DenseView<T>& vb, const StoreEpi<T>& epi) {
+  cudaStream_t st = stream_of(c, stream);
+  Workspace& ws = workspace_of(c, stream);
+  if constexpr (std::is_same_v<T, float>) {
+    const GemmPlan pl = plan_tc(M, N, K);
+    TmaReq ra, rb;
+    with_operand(va, tc::BM, ra, [&](const auto& a) {
+      with_operand(vb, pl.bn, rb, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra, rb); });
+    });
+  } else {
+    const GemmPlan pl = plan_simt(M, N, K);
+    run_simt<T>(c, st, ws, pl, M, N, K, va, vb, epi);
+  }
+}
+
+template <typename T>
+static void gemm_t(Ctx* c, int ta, int tb, int m, int n, int k, double alpha, const BufferSlot& A,
+                   const BufferSlot& B, double beta, BufferSlot& C, cdnn_handle stream) {
+  const T* a = reinterpret_cast<const T*>(A.dev);
+  const T* b = reinterpret_cast<const T*>(B.dev);
+  T* cc = reinterpret_cast<T*>(C.dev);
+  // kernel A(mm=j, p) = opB[p][j]
+  DenseView<T> va = tb ? DenseView<T>{b, int64_t(k), 1, n, k, false}
+                       : DenseView<T>{b, 1, int64_t(n), n, k, true};
+  // kernel B(nn=i, p) = opA[i][p]
+  DenseView<T> vb = ta ? DenseView<T>{a, 1, int64_t(m), m, k, true}
+                       : DenseView<T>{a, int64_t(k), 1, m, k, false};
+  StoreEpi<T> epi{cc, 1, int64_t(n), T(alpha), T(beta), nullptr, false, false};
+  dense_gemm<T>(c, stream, n, m, k, va, vb, epi);
+}
+
+template <typename T>
+__global__ void colsum_accum_kernel(const T* __restrict__ dy, T* __restrict__ db, int rows, int cols) {
+  // db[j] += sum_r dy[r][j]; rows summed in order (layers.cpp:157-163 loop order)
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
+    T s = T(0);
+    for (int r = 0; r < rows; ++r) s += dy[int64_t(r) * cols + j];
+    db[j] += s;
+  }
+}
+
+}  // namespace cdnn
+
+using namespace cdnn;
+
+extern "C" {
+
+int cdnn_gemm(cdnn_ctx ctx, int trans_a, int trans_b, int m, int n, int k, double alpha,
+              cdnn_handle a, cdnn_handle b, double beta, cdnn_handle c, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    if (m <= 0 || n <= 0 || k <= 0) fail(CDNN_INVALID_ARGUMENT, "gemm: m, n, k must be positive");
+    BufferSlot& A = buffer(cx, a, "gemm A");
+    BufferSlot& B = buffer(cx, b, "gemm B");
+    BufferSlot& C = buffer(cx, c, "gemm C");
+    require_len(A, uint64_t(m) * k, "gemm A");
+    require_len(B, uint64_t(k) * n, "gemm B");
+    require_len(C, uint64_t(m) * n, "gemm C");
+    require_dtype(B, A.dtype, "gemm B");
+    require_dtype(C, A.dtype, "gemm C");
+    DeviceGuard g(cx);
+    if (A.dtype == CDNN_F32) gemm_t<float>(cx, trans_a, trans_b, m, n, k, alpha, A, B, beta, C, stream);
+    else if (A.dtype == CDNN_F64) gemm_t<double>(cx, trans_a, trans_b, m, n, k, alpha, A, B, beta, C, stream);
+    else fail(CDNN_INVALID_ARGUMENT, "gemm: floating buffers required");
+  });
+}
+
+int cdnn_ip_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle w, cdnn_handle bias, cdnn_handle top,
+                    int rows, int k, int o, int relu, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (rows <= 0 || k <= 0 || o <= 0) fail(CDNN_INVALID_ARGUMENT, "ip_forward: extents must be positive");
+    BufferSlot& X = buffer(c, x, "ip_forward x");
+    BufferSlot& W = buffer(c, w, "ip_forward w");
+    BufferSlot& Y = buffer(c, top, "ip_forward top");
+    BufferSlot* Bi = buffer_or_null(c, bias, "ip_forward bias");
+    require_len(X, uint64_t(rows) * k, "ip_forward x");
+    require_len(W, uint64_t(o) * k, "ip_forward w");
+    require_len(Y, uint64_t(rows) * o, "ip_forward top");
+    if (Bi) { require_len(*Bi, uint64_t(o), "ip_forward bias"); require_dtype(*Bi, X.dtype, "ip bias"); }
+    require_dtype(W, X.dtype, "ip w");
+    require_dtype(Y, X.dtype, "ip top");
+    DeviceGuard g(c);
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      DenseView<T> va{reinterpret_cast<const T*>(W.dev), int64_t(k), 1, o, k, false};
+      DenseView<T> vb{reinterpret_cast<const T*>(X.dev), int64_t(k), 1, rows, k, false};
+      StoreEpi<T> epi{reinterpret_cast<T*>(Y.dev), 1, int64_t(o), T(1), T(0),
+                      Bi ? reinterpret_cast<const T*>(Bi->dev) : nullptr, true, relu != 0};
+      dense_gemm<T>(c, stream, o, rows, k, va, vb, epi);
+    };
+    if (X.dtype == CDNN_F32) run(float{});
+    else if (X.dtype == CDNN_F64) run(double{});
+    else fail(CDNN_INVALID_ARGUMENT, "ip_forward: floating buffers required");
+  });
+}
+
+int cdnn_ip_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle w, cdnn_handle dy, cdnn_handle dw,
+                     cdnn_handle db, cdnn_handle dx, int rows, int k, int o, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (rows <= 0 || k <= 0 || o <= 0) fail(CDNN_INVALID_ARGUMENT, "ip_backward: extents must be positive");
+    BufferSlot& X = buffer(c, x, "ip_backward x");
+    BufferSlot& W = buffer(c, w, "ip_backward w");
+    BufferSlot& DY = buffer(c, dy, "ip_backward dy");
+    BufferSlot* DW = buffer_or_null(c, dw, "ip_backward dw");
+    BufferSlot* DB = buffer_or_null(c, db, "ip_backward db");
+    BufferSlot* DX = buffer_or_null(c, dx, "ip_backward dx");
+    require_len(X, uint64_t(rows) * k, "ip_backward x");
+    require_len(W, uint64_t(o) * k, "ip_backward w");
+    require_len(DY, uint64_t(rows) * o, "ip_backward dy");
+    if (DW) require_len(*DW, uint64_t(o) * k, "ip_backward dw");
+    if (DB) require_len(*DB, uint64_t(o), "ip_backward db");
+    if (DX) require_len(*DX, uint64_t(rows) * k, "ip_backward dx");
+    for (BufferSlot* b : {&W, &DY, DW, DB, DX})
+      if (b) require_dtype(*b, X.dtype, "ip_backward");
+    DeviceGuard g(c);
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      const T* xp = reinterpret_cast<const T*>(X.dev);
+      const T* wp = reinterpret_cast<const T*>(W.dev);
+      const T* dyp = reinterpret_cast<const T*>(DY.dev);
+      if (DW) {  // dW += dY^T X   (layers.cpp:153-155, beta = 1)
+        DenseView<T> va{xp, 1, int64_t(k), k, rows, true};
+        DenseView<T> vb{dyp, 1, int64_t(o), o, rows, true};
+        StoreEpi<T> epi{reinterpret_cast<T*>(DW->dev), 1, int64_t(k), T(1), T(1), nullptr, false, false};
+        dense_gemm<T>(c, stream, k, o, rows, va, vb, epi);
+      }
+      if (DB) {  // db += column sums of dY (layers.cpp:157-163)
+        colsum_accum_kernel<T><<<grid_for(o, 128), 128, 0, stream_of(c, stream)>>>(
+            dyp, reinterpret_cast<T*>(DB->dev), rows, o);
+        check_launch("colsum");
+        count_launch(c);
+      }
+      if (DX) {  // dX = dY W   (layers.cpp:166-168, beta = 0)
+        DenseView<T> va{wp, 1, int64_t(k), k, o, true};
+        DenseView<T> vb{dyp, int64_t(o), 1, rows, o, false};
+        StoreEpi<T> epi{reinterpret_cast<T*>(DX->dev), 1, int64_t(k), T(1), T(0), nullptr, false, false};
+        dense_gemm<T>(c, stream, k, rows, o, va, vb, epi);
+      }
+    };
+    if (X.dtype == CDNN_F32) run(float{});
+    else if (X.dtype == CDNN_F64) run(double{});
+    else fail(CDNN_INVALID_ARGUMENT, "ip_backward: floating buffers required");
+  });
+}
+
+}  // extern "C"
