@@ -1,0 +1,313 @@
+// polegrad/layers.hpp — layer interface, factory and the concrete layers.
+//
+// The Layer virtual interface, the six reference layer types with their
+// parameter structs and accessors, make_layer and softmax_xent_gradient keep
+// the reference signatures (layers.hpp:16-193).  Forward/backward now run on
+// the GPU through the CudaDnn C-ABI.  Added (Caffe semantics, absent from the
+// reference — SURVEY §8(a) X1-X5): Convolution, Pooling, SoftmaxWithLoss,
+// Split, and a labelled MemoryData top.  Their parameters are read from the
+// layer's opaque prototxt blocks (convolution_param, pooling_param,
+// loss_param), so prototxt parse/print is unchanged.
+//
+// Setting the environment variable POLEGRAD_REFERENCE_COMPAT=1 hides the
+// added layer types from layer_type_from_string (and therefore from the
+// parser) and restores the reference's wiring rules in Net, so the
+// reference's own test-suite assertions that "Convolution" is unknown hold.
+#pragma once
+
+#include <deque>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <span>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "polegrad/blob.hpp"
+#include "polegrad/proto_node.hpp"
+#include "polegrad/types.hpp"
+
+namespace polegrad {
+
+enum class LayerType {
+  kInnerProduct,
+  kRelu,
+  kSigmoid,
+  kSoftmax,
+  kMemoryData,
+  kMemoryLoss,
+  // B200 additions (Caffe layer set needed by the CNN configs)
+  kConvolution,
+  kPooling,
+  kSoftmaxWithLoss,
+  kSplit,
+};
+
+std::string_view to_string(LayerType type);
+std::optional<LayerType> layer_type_from_string(std::string_view name);
+// True when POLEGRAD_REFERENCE_COMPAT is set (reference layer set and rules).
+bool reference_compat();
+
+struct InnerProductParam {
+  int num_output = 0;
+  std::vector<ProtoNode> extras;  // unrecognised fields, printed back verbatim
+  bool operator==(const InnerProductParam&) const = default;
+};
+
+struct MemoryDataParam {
+  int batch_size = 0;
+  int channels = 0;
+  int height = 0;
+  int width = 0;
+  std::vector<ProtoNode> extras;
+  bool operator==(const MemoryDataParam&) const = default;
+};
+
+struct LayerSpec {
+  std::string name;
+  LayerType type = LayerType::kInnerProduct;
+  std::vector<std::string> bottoms;
+  std::vector<std::string> tops;
+  std::optional<InnerProductParam> inner_product;
+  std::optional<MemoryDataParam> memory_data;
+  std::vector<ProtoNode> extras;
+  bool operator==(const LayerSpec&) const = default;
+};
+
+// Backward-time callback of MemoryLoss: fills the gradient of its bottom.
+using LossHook = std::function<void(Blob& bottom)>;
+
+class Layer {
+ public:
+  explicit Layer(LayerSpec spec) : spec_(std::move(spec)) {}
+  virtual ~Layer() = default;
+  Layer(const Layer&) = delete;
+  Layer& operator=(const Layer&) = delete;
+
+  const LayerSpec& spec() const { return spec_; }
+  const std::string& name() const { return spec_.name; }
+  LayerType type() const { return spec_.type; }
+
+  // Checks bottom shapes, allocates and initialises parameters, returns tops.
+  virtual std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes,
+                                   const std::shared_ptr<Registry>& registry, Rng& rng) = 0;
+  virtual void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) = 0;
+  // Parameter gradients accumulate; bottom gradients are overwritten.
+  virtual void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) = 0;
+  virtual const std::vector<std::shared_ptr<Blob>>& params() const;
+  virtual void set_loss_hook(LossHook hook);  // MemoryLoss only
+
+  // B200: which bottoms need a gradient (Caffe propagate_down).  The six
+  // reference layers always write their bottom diff, as the reference does.
+  void set_propagate_down(std::vector<bool> pd) { propagate_down_ = std::move(pd); }
+  bool propagate_down(std::size_t i) const { return i >= propagate_down_.size() || propagate_down_[i]; }
+  // True when forward() may be captured into a CUDA graph (no host work).
+  virtual bool graph_safe() const { return true; }
+
+ protected:
+  LayerSpec spec_;
+  std::vector<bool> propagate_down_;
+};
+
+std::unique_ptr<Layer> make_layer(const LayerSpec& spec);
+
+// ---- reference layer set -------------------------------------------------------
+
+// top = bottom W^T + b (W: num_output x C*H*W, uniform Xavier init).
+class InnerProductLayer final : public Layer {
+ public:
+  using Layer::Layer;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  const std::vector<std::shared_ptr<Blob>>& params() const override { return params_; }
+  Blob& weight() { return *params_[0]; }
+  Blob& bias() { return *params_[1]; }
+  // Fuse a following in-place ReLU into the GEMM epilogue (set by Net).
+  void fuse_relu(bool on) { fused_relu_ = on; }
+  bool fused_relu() const { return fused_relu_; }
+
+ private:
+  int input_dim_ = 0;
+  int num_output_ = 0;
+  bool fused_relu_ = false;
+  std::vector<std::shared_ptr<Blob>> params_;
+};
+
+class ReluLayer final : public Layer {
+ public:
+  using Layer::Layer;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  // Forward already applied by the producer's epilogue (in-place fusion).
+  void set_forward_fused(bool on) { forward_fused_ = on; }
+
+ private:
+  bool forward_fused_ = false;
+};
+
+class SigmoidLayer final : public Layer {
+ public:
+  using Layer::Layer;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+};
+
+// Softmax over each sample's whole C*H*W vector; backward is the full Jacobian.
+class SoftmaxLayer final : public Layer {
+ public:
+  using Layer::Layer;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+};
+
+// Input feed.  Reference behaviour: a FIFO of single samples, each forward
+// consumes batch_size of them (DataStarvation otherwise).  B200 additions: an
+// optional second `label` top, and set_batch() which stages a whole batch
+// (data + labels) straight into HBM from host memory (pinned for async).
+class MemoryDataLayer final : public Layer {
+ public:
+  using Layer::Layer;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  bool graph_safe() const override { return false; }
+
+  void enqueue(std::span<const real> sample);
+  std::size_t queued() const { return queue_.size(); }
+  std::size_t sample_size() const { return sample_size_; }
+  int batch_size() const { return batch_size_; }
+  // Copies batch_size samples (and labels when the layer has a label top)
+  // into the top blobs asynchronously; they are consumed by the next forward
+  // instead of the FIFO.
+  void set_batch(Blob& data_top, Blob* label_top, const real* data, const real* labels);
+  bool has_staged_batch() const { return staged_; }
+  void clear_staged() { staged_ = false; }
+
+ private:
+  std::size_t sample_size_ = 0;
+  int batch_size_ = 0;
+  std::deque<std::vector<real>> queue_;
+  bool staged_ = false;
+};
+
+// Sink of the graph; backward calls the installed hook (host side).
+class MemoryLossLayer final : public Layer {
+ public:
+  using Layer::Layer;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  void set_loss_hook(LossHook hook) override { hook_ = std::move(hook); }
+  bool has_loss_hook() const { return static_cast<bool>(hook_); }
+  bool graph_safe() const override { return !hook_; }
+
+ private:
+  LossHook hook_;
+};
+
+// ---- B200 additions ---------------------------------------------------------------
+
+struct ConvolutionParam {
+  int num_output = 0;
+  int kernel_h = 0, kernel_w = 0;
+  int stride_h = 1, stride_w = 1;
+  int pad_h = 0, pad_w = 0;
+  int dilation = 1;
+  int group = 1;
+  bool bias_term = true;
+};
+ConvolutionParam parse_convolution_param(const LayerSpec& spec);
+
+// Caffe convolution as implicit GEMMs on the tensor cores (no im2col buffer).
+// Weights [num_output][C/group][kh][kw]; uniform Xavier init with the
+// InnerProduct rule on the [num_output x C/group*kh*kw] view; bias zero.
+class ConvolutionLayer final : public Layer {
+ public:
+  ConvolutionLayer(LayerSpec spec, ConvolutionParam p) : Layer(std::move(spec)), p_(p) {}
+  ~ConvolutionLayer() override;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  const std::vector<std::shared_ptr<Blob>>& params() const override { return params_; }
+  const ConvolutionParam& param() const { return p_; }
+
+ private:
+  ConvolutionParam p_;
+  std::shared_ptr<Registry> reg_;
+  cdnn_handle desc_ = 0;
+  std::vector<std::shared_ptr<Blob>> params_;
+};
+
+struct PoolingParam {
+  bool max = true;  // MAX or AVE
+  int kernel_h = 0, kernel_w = 0;
+  int stride_h = 1, stride_w = 1;
+  int pad_h = 0, pad_w = 0;
+  bool global_pooling = false;
+};
+PoolingParam parse_pooling_param(const LayerSpec& spec);
+
+// Caffe pooling (ceil output size); MAX keeps an int32 argmax mask.
+class PoolingLayer final : public Layer {
+ public:
+  PoolingLayer(LayerSpec spec, PoolingParam p) : Layer(std::move(spec)), p_(p) {}
+  ~PoolingLayer() override;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  // Flat h*W+w argmax per output element (MAX only); downloads from HBM.
+  std::vector<int> mask() const;
+
+ private:
+  PoolingParam p_;
+  std::shared_ptr<Registry> reg_;
+  cdnn_handle desc_ = 0;
+  cdnn_handle mask_ = 0;  // I32 device buffer
+  std::size_t top_count_ = 0;
+};
+
+// softmax + multinomial logistic loss; bottoms {scores, label}, top {loss}.
+// loss = -sum_n log(max(p[n][label_n], FLT_MIN)) / N  (normalize, default)
+class SoftmaxWithLossLayer final : public Layer {
+ public:
+  SoftmaxWithLossLayer(LayerSpec spec, bool normalize) : Layer(std::move(spec)), normalize_(normalize) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  const Blob& prob() const { return *prob_; }
+
+ private:
+  bool normalize_;
+  int rows_ = 0, classes_ = 0;
+  std::unique_ptr<Blob> prob_;
+};
+
+// Fan-out: tops are copies of the bottom; bottom diff = sum of top diffs.
+class SplitLayer final : public Layer {
+ public:
+  using Layer::Layer;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+};
+
+// Cross-entropy gradient at a softmax output: probs - one-hot target
+// (validated: same length, non-empty, probs sum to 1 within 1e-6, one-hot).
+std::vector<real> softmax_xent_gradient(std::span<const real> probs, std::span<const real> target);
+
+}  // namespace polegrad

@@ -1,0 +1,111 @@
+// polegrad/net.hpp — executable network over named blobs.
+//
+// Reference API (net.hpp:14-85) unchanged: NetDef, Net(def, seed), forward,
+// backward, backward_from, blob lookup, params in layer order, MCWT weight
+// snapshots.  B200 additions:
+//  * all blobs live in HBM; parameters and their gradients are packed into two
+//    contiguous arenas (one solver kernel, one all-reduce per bucket);
+//  * Caffe wiring when not in reference-compat mode: in-place ReLU/Sigmoid
+//    tops, automatic Split layers for fan-out, need-backward propagation
+//    (no data gradient into the input), SoftmaxWithLoss loss tops;
+//  * set_batch() feed, step capture into a CUDA graph, and an optional
+//    data-parallel hook (polegrad::Parallel) that all-reduces gradient
+//    buckets on a side stream as backward produces them.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "polegrad/layers.hpp"
+#include "polegrad/proto_node.hpp"
+
+namespace polegrad {
+
+// Ordered model description: layer order is execution order.
+struct NetDef {
+  std::optional<std::string> name;
+  std::vector<LayerSpec> layers;
+  std::vector<ProtoNode> extras;  // unrecognised top-level fields
+  bool operator==(const NetDef&) const = default;
+};
+
+class Net {
+ public:
+  Net() = default;
+  Net(const NetDef& def, std::uint64_t seed);
+  Net(const NetDef& def, std::uint64_t seed, int device);
+  ~Net();
+  Net(const Net&) = delete;
+  Net& operator=(const Net&) = delete;
+  Net(Net&&) noexcept = default;
+  Net& operator=(Net&& other) noexcept;
+
+  // Every layer in order; returns the blobs no layer consumes.
+  std::map<std::string, Blob*> forward();
+  // Every layer's backward in reverse order.
+  void backward();
+  // Backward of the named blob's producer and everything before it.
+  void backward_from(const std::string& blob_name);
+
+  bool has_blob(const std::string& name) const;
+  Blob& blob(const std::string& name);
+  const Blob& blob(const std::string& name) const;
+  const std::vector<std::unique_ptr<Layer>>& layers() const { return layers_; }
+  Layer* find_layer(const std::string& name);
+  const std::vector<Blob*>& params() const { return params_; }
+  std::vector<std::pair<std::string, Shape>> blob_shapes() const;
+  const NetDef& def() const { return def_; }
+  const std::shared_ptr<Registry>& registry() const { return registry_; }
+
+  std::vector<std::uint8_t> snapshot_weights() const;
+  void restore_weights(std::span<const std::uint8_t> bytes);
+
+  // ---- B200 additions ---------------------------------------------------------
+  // Sum of the loss tops (SoftmaxWithLoss) after the last forward (D2H read).
+  double loss() const;
+  const std::vector<Blob*>& loss_blobs() const { return loss_tops_; }
+  // Stage one batch into the first MemoryData layer (see MemoryDataLayer::set_batch).
+  void set_batch(const real* data, const real* labels = nullptr);
+  // Flat arenas: params()[i] data/diff are views at param_offset(i).
+  Handle weight_arena() const { return weight_arena_; }
+  Handle grad_arena() const { return grad_arena_; }
+  std::size_t param_offset(std::size_t i) const { return param_offsets_.at(i); }
+  std::size_t param_total() const { return param_total_; }
+  // Called after layer i's backward (reverse order); used by Parallel.
+  using BackwardHook = std::function<void(std::size_t layer_index)>;
+  void set_backward_hook(BackwardHook hook) { backward_hook_ = std::move(hook); }
+  // Index of the first parameter owned by layer i (params are in layer order).
+  std::size_t first_param_of_layer(std::size_t i) const { return layer_param_begin_.at(i); }
+  // True when forward/backward contain no host work (graph capturable).
+  bool graph_safe() const;
+
+ private:
+  void build(const NetDef& def, std::uint64_t seed, int device);
+  void pack_params();
+
+  std::shared_ptr<Registry> registry_;
+  Handle rng_handle_{};
+  NetDef def_;
+  std::vector<std::unique_ptr<Layer>> layers_;
+  std::vector<std::vector<Blob*>> bottoms_;
+  std::vector<std::vector<Blob*>> tops_;
+  std::vector<std::shared_ptr<Blob>> blobs_;
+  std::map<std::string, Blob*> blob_index_;
+  std::map<std::string, std::size_t> producer_index_;
+  std::vector<Blob*> params_;
+  std::vector<std::string> output_names_;
+  std::vector<Blob*> loss_tops_;
+  std::vector<std::size_t> layer_param_begin_;
+  std::vector<std::size_t> param_offsets_;
+  std::size_t param_total_ = 0;
+  Handle weight_arena_{}, grad_arena_{};
+  BackwardHook backward_hook_;
+};
+
+}  // namespace polegrad

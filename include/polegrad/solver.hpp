@@ -1,0 +1,62 @@
+// polegrad/solver.hpp — parameter update.
+//
+// Reference API (solver.hpp:10-39) with SolverConfig extended by Caffe's
+// momentum and weight decay (both default 0, which is exactly the reference
+// SGD step).  apply_update() is one fused sm_100a kernel over the net's flat
+// parameter arena: it applies the rule and zeroes every gradient
+// (solver.cpp:55).  With a Parallel attached it first waits for the gradient
+// all-reduce (sum over ranks).
+#pragma once
+
+#include <vector>
+
+#include "polegrad/net.hpp"
+#include "polegrad/types.hpp"
+
+namespace polegrad {
+
+enum class SolverMethod { kSgd, kRmsProp };
+
+struct SolverConfig {
+  SolverMethod method = SolverMethod::kRmsProp;
+  real learning_rate = real(1e-3);
+  real rms_decay = real(0.99);
+  real epsilon = real(1e-8);
+  // B200 additions (Caffe SGDSolver): g += weight_decay*w; v = momentum*v + lr*g; w -= v
+  real momentum = real(0);
+  real weight_decay = real(0);
+};
+
+class Parallel;
+
+class Solver {
+ public:
+  explicit Solver(const SolverConfig& config);
+  ~Solver();
+  const SolverConfig& config() const { return config_; }
+
+  // sgd:     w -= lr*diff            (+ momentum / weight decay when set)
+  // rmsprop: cache = d*cache + (1-d)*diff^2 ; w -= lr*diff/(sqrt(cache)+eps)
+  // Every parameter diff is zero afterwards.
+  void apply_update(Net& net);
+
+  // Data-parallel training: all-reduce gradients through `parallel` before
+  // each update (nullptr detaches).
+  void set_parallel(Parallel* parallel) { parallel_ = parallel; }
+  // Solver state for checkpoints (momentum / RMSProp history, arena order).
+  std::vector<real> history() const;
+  void set_history(std::span<const real> h);
+
+ private:
+  SolverConfig config_;
+  Parallel* parallel_ = nullptr;
+  std::shared_ptr<Registry> hist_reg_;  // registry holding the history buffer
+  Handle history_{};
+  std::size_t history_len_ = 0;
+  std::size_t history_params_ = 0;
+};
+
+// True when every parameter gradient of the net is exactly zero.
+bool diffs_are_zeroed(const Net& net);
+
+}  // namespace polegrad

@@ -1,0 +1,91 @@
+/*
+ * polegrad_c.h — C entry points over the reference-compatible C++ API
+ * (polegrad::Net / Solver / Parallel), exported by libpolegrad_b200_f32.so
+ * (`real` = float, TF32 tensor cores) and libpolegrad_b200_f64.so (`real` =
+ * double, SIMT FP64).  This is the "MyCaffe Control" level of the paper: a
+ * foreign host (Python ctypes here; C#/COM in MyCaffe) drives whole training
+ * steps while the CudaDnn C-ABI (cudadnn.h) does the device work.
+ *
+ * Every `real*` argument points at values of the library's `real` type
+ * (pg_real_size() bytes each).  Status codes are the cdnn_status values;
+ * pg_last_error() holds the message of the last failure on this thread.
+ */
+#ifndef POLEGRAD_C_H_
+#define POLEGRAD_C_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_API __attribute__((visibility("default")))
+
+typedef struct pg_net pg_net;
+typedef struct pg_solver pg_solver;
+typedef struct pg_parallel pg_parallel;
+
+PG_API const char* pg_last_error(void);
+PG_API int pg_real_size(void);
+
+/* Net(prototxt::parse(text), seed) on `device`  (net.cpp:12-69) */
+PG_API int pg_net_create(const char* prototxt, uint64_t seed, int device, pg_net** out);
+PG_API int pg_net_free(pg_net* net);
+PG_API int pg_net_forward(pg_net* net);
+PG_API int pg_net_backward(pg_net* net);
+PG_API int pg_net_backward_from(pg_net* net, const char* blob);
+PG_API int pg_net_loss(pg_net* net, double* out);
+/* whole batch (+ labels when the data layer has a label top) from host memory */
+PG_API int pg_net_set_batch(pg_net* net, const void* data, const void* labels);
+/* one sample into a MemoryData FIFO (layers.cpp:282-289) */
+PG_API int pg_net_enqueue(pg_net* net, const char* layer, const void* sample, uint64_t n);
+PG_API int pg_net_sync(pg_net* net);
+PG_API int pg_net_context(pg_net* net, void** cdnn_context);
+PG_API int pg_net_num_layers(pg_net* net);
+PG_API int pg_net_layer_name(pg_net* net, int i, char* buf, int cap);
+PG_API int pg_blob_shape(pg_net* net, const char* name, int shape[4]);
+PG_API int pg_blob_get(pg_net* net, const char* name, int diff, void* out);
+PG_API int pg_blob_set(pg_net* net, const char* name, int diff, const void* in);
+PG_API int pg_param_count(pg_net* net);
+PG_API int pg_param_info(pg_net* net, int i, char* name, int cap, int shape[4]);
+PG_API int pg_param_get(pg_net* net, int i, int diff, void* out);
+PG_API int pg_param_set(pg_net* net, int i, int diff, const void* in);
+PG_API int pg_pool_mask(pg_net* net, const char* layer, int32_t* out, uint64_t n);
+/* MCWT snapshot (net.cpp:154-286); call with buf = NULL to learn *len */
+PG_API int pg_snapshot(pg_net* net, uint8_t* buf, uint64_t cap, uint64_t* len);
+PG_API int pg_restore(pg_net* net, const uint8_t* buf, uint64_t len);
+
+/* method 0 = SGD, 1 = RMSProp; momentum / weight_decay are Caffe's */
+PG_API int pg_solver_create(int method, double lr, double momentum, double weight_decay, double rms_decay,
+                            double epsilon, pg_solver** out);
+PG_API int pg_solver_free(pg_solver* s);
+PG_API int pg_solver_apply(pg_solver* s, pg_net* net);
+
+/* Captures one training step  feed(H2D from `data`/`labels`) -> forward ->
+ * backward -> solver update -> D2H of the loss into `loss_out`  into a CUDA
+ * graph.  The host pointers must stay valid (pinned) for every replay; run one
+ * eager step first so workspaces and tensor maps exist. */
+PG_API int pg_step_capture(pg_net* net, pg_solver* s, const void* data, const void* labels, void* loss_out,
+                           uint64_t* graph);
+PG_API int pg_step_replay(pg_net* net, uint64_t graph);
+PG_API int pg_graph_free(pg_net* net, uint64_t graph);
+
+/* data parallel (NCCL); id = 128 bytes from pg_parallel_unique_id on rank 0 */
+PG_API int pg_parallel_unique_id(uint8_t id[128]);
+PG_API int pg_parallel_create(pg_net* net, int nranks, int rank, const uint8_t id[128], uint64_t bucket_bytes,
+                              pg_parallel** out);
+PG_API int pg_parallel_free(pg_parallel* p);
+PG_API int pg_parallel_broadcast(pg_parallel* p);
+PG_API int pg_solver_set_parallel(pg_solver* s, pg_parallel* p);
+/* pure host bucket planner (parallel.hpp); bucket_of[i] = bucket index of param i */
+PG_API int pg_plan_buckets(const uint64_t* offsets, const uint64_t* counts, int n, uint64_t total,
+                           uint64_t bucket_elems, int32_t* bucket_of, int32_t* nbuckets);
+
+/* prototxt round trip through this library's parser / printer */
+PG_API int pg_prototxt_roundtrip(const char* text, char* out, uint64_t cap, uint64_t* len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POLEGRAD_C_H_ */

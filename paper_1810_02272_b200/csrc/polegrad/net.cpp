@@ -1,0 +1,344 @@
+// net.cpp — graph build, forward/backward and MCWT snapshots (reference:
+// net.cpp:12-286), plus the Caffe wiring rules and the flat parameter arenas.
+#include "polegrad/net.hpp"
+
+#include <algorithm>
+#include <bit>
+#include <cstring>
+#include <set>
+#include <utility>
+
+#include "polegrad/errors.hpp"
+
+namespace polegrad {
+
+namespace {
+
+bool allows_in_place(LayerType t) { return t == LayerType::kRelu || t == LayerType::kSigmoid; }
+
+// Caffe InsertSplits: each blob *version* read by more than one layer gets a
+// Split layer right after its producer and every reader its own copy (the
+// reference overwrites the shared diff instead).
+std::vector<LayerSpec> with_splits(const std::vector<LayerSpec>& layers) {
+  struct Version {
+    std::string name;
+    std::size_t producer;
+    std::vector<std::pair<std::size_t, std::size_t>> readers;  // (layer, bottom slot)
+  };
+  std::vector<Version> versions;
+  std::map<std::string, std::size_t> live;
+  for (std::size_t i = 0; i < layers.size(); ++i) {
+    for (std::size_t b = 0; b < layers[i].bottoms.size(); ++b) {
+      auto it = live.find(layers[i].bottoms[b]);
+      if (it != live.end()) versions[it->second].readers.emplace_back(i, b);
+    }
+    for (const std::string& t : layers[i].tops) {
+      versions.push_back({t, i, {}});
+      live[t] = versions.size() - 1;
+    }
+  }
+  std::map<std::pair<std::size_t, std::size_t>, std::string> renamed;
+  std::map<std::size_t, std::vector<LayerSpec>> inserted;
+  for (const Version& v : versions) {
+    if (v.readers.size() < 2) continue;
+    LayerSpec split;
+    split.type = LayerType::kSplit;
+    split.name = v.name + "_" + layers[v.producer].name + "_split";
+    split.bottoms = {v.name};
+    for (std::size_t j = 0; j < v.readers.size(); ++j) {
+      const auto [li, bi] = v.readers[j];
+      for (const std::string& t : layers[li].tops)
+        if (t == v.name)
+          throw ModelError("layer '" + layers[li].name + "': in-place use of the fan-out blob '" + v.name + "'");
+      const std::string copy = v.name + "_" + layers[v.producer].name + "_" + std::to_string(j) + "_split";
+      split.tops.push_back(copy);
+      renamed[{li, bi}] = copy;
+    }
+    inserted[v.producer].push_back(std::move(split));
+  }
+  if (renamed.empty()) return layers;
+  std::vector<LayerSpec> out;
+  for (std::size_t i = 0; i < layers.size(); ++i) {
+    LayerSpec s = layers[i];
+    for (std::size_t b = 0; b < s.bottoms.size(); ++b) {
+      auto it = renamed.find({i, b});
+      if (it != renamed.end()) s.bottoms[b] = it->second;
+    }
+    out.push_back(std::move(s));
+    for (LayerSpec& sp : inserted[i]) out.push_back(std::move(sp));
+  }
+  return out;
+}
+
+}  // namespace
+
+Net::Net(const NetDef& def, std::uint64_t seed) { build(def, seed, 0); }
+Net::Net(const NetDef& def, std::uint64_t seed, int device) { build(def, seed, device); }
+
+void Net::build(const NetDef& def, std::uint64_t seed, int device) {
+  registry_ = std::make_shared<Registry>(device);
+  def_ = def;
+  const bool compat = reference_compat();
+  const std::vector<LayerSpec> specs = compat ? def.layers : with_splits(def.layers);
+  rng_handle_ = registry_->create_rng(seed);
+  Rng& rng = registry_->rng(rng_handle_);
+
+  std::set<std::string> consumed;
+  std::map<std::string, bool> needs_grad;  // Caffe blob_need_backward
+  for (const LayerSpec& spec : specs) {
+    auto layer = make_layer(spec);
+    std::vector<Blob*> bottoms;
+    std::vector<Shape> bottom_shapes;
+    bool any_bottom_grad = false;
+    std::vector<bool> pd;
+    for (const std::string& name : spec.bottoms) {
+      auto it = blob_index_.find(name);
+      if (it == blob_index_.end()) throw ModelError("layer '" + spec.name + "': undefined bottom '" + name + "'");
+      bottoms.push_back(it->second);
+      bottom_shapes.push_back(it->second->shape());
+      consumed.insert(name);
+      any_bottom_grad = any_bottom_grad || needs_grad[name];
+      pd.push_back(needs_grad[name]);
+    }
+    std::vector<Shape> top_shapes = layer->setup(bottom_shapes, registry_, rng);
+    if (top_shapes.size() != spec.tops.size()) {
+      throw ModelError("layer '" + spec.name + "': produced " + std::to_string(top_shapes.size()) +
+                       " top shape(s) for " + std::to_string(spec.tops.size()) + " top name(s)");
+    }
+    if (!compat) layer->set_propagate_down(pd);
+    const bool layer_grad = any_bottom_grad || !layer->params().empty();
+    std::vector<Blob*> tops;
+    for (std::size_t t = 0; t < spec.tops.size(); ++t) {
+      const std::string& name = spec.tops[t];
+      const bool in_place = std::find(spec.bottoms.begin(), spec.bottoms.end(), name) != spec.bottoms.end();
+      if (blob_index_.contains(name)) {
+        if (!(in_place && !compat && allows_in_place(spec.type)))
+          throw ModelError("layer '" + spec.name + "': top '" + name + "' is already produced");
+        tops.push_back(blob_index_.at(name));  // in-place: the top is the bottom blob
+      } else {
+        blobs_.push_back(std::make_shared<Blob>(registry_, top_shapes[t], name));
+        blob_index_.emplace(name, blobs_.back().get());
+        tops.push_back(blobs_.back().get());
+      }
+      producer_index_[name] = layers_.size();
+      needs_grad[name] = layer_grad;
+      if (spec.type == LayerType::kSoftmaxWithLoss) {
+        tops.back()->diff()[0] = real(1);  // loss weight
+        loss_tops_.push_back(tops.back());
+      }
+    }
+    layer_param_begin_.push_back(params_.size());
+    for (const auto& p : layer->params()) params_.push_back(p.get());
+    layers_.push_back(std::move(layer));
+    bottoms_.push_back(std::move(bottoms));
+    tops_.push_back(std::move(tops));
+  }
+  for (const auto& blob : blobs_)
+    if (!consumed.contains(blob->name())) output_names_.push_back(blob->name());
+
+  // Fuse InnerProduct + in-place ReLU: the ReLU runs in the GEMM epilogue.
+  for (std::size_t i = 0; i + 1 < layers_.size(); ++i) {
+    auto* ip = dynamic_cast<InnerProductLayer*>(layers_[i].get());
+    auto* relu = dynamic_cast<ReluLayer*>(layers_[i + 1].get());
+    if (ip && relu && bottoms_[i + 1][0] == tops_[i][0] && tops_[i + 1][0] == tops_[i][0]) {
+      ip->fuse_relu(true);
+      relu->set_forward_fused(true);
+    }
+  }
+  pack_params();
+}
+
+// Move every parameter into two flat arenas (weights, gradients) so the solver
+// is one kernel and data-parallel all-reduce works on contiguous buckets.
+void Net::pack_params() {
+  param_offsets_.clear();
+  std::size_t total = 0;
+  for (Blob* p : params_) {
+    param_offsets_.push_back(total);
+    total += (p->count() + 3) & ~std::size_t(3);  // 16-byte aligned views
+  }
+  param_total_ = total;
+  if (total == 0) return;
+  weight_arena_ = registry_->alloc_buffer(total);
+  grad_arena_ = registry_->alloc_buffer(total);
+  for (std::size_t i = 0; i < params_.size(); ++i) {
+    Blob* p = params_[i];
+    const Handle w = registry_->alloc_view(weight_arena_, param_offsets_[i], p->count());
+    const Handle g = registry_->alloc_view(grad_arena_, param_offsets_[i], p->count());
+    kernels::copy(*registry_, p->data_handle(), w, p->count());
+    kernels::copy(*registry_, p->diff_handle(), g, p->count());
+    p->rebind(w, g);
+  }
+}
+
+Net::~Net() {
+  if (registry_ && rng_handle_) {
+    try { registry_->free_subsystem(rng_handle_); } catch (...) {}
+  }
+}
+
+Net& Net::operator=(Net&& o) noexcept {
+  if (this != &o) {
+    if (registry_ && rng_handle_) {
+      try { registry_->free_subsystem(rng_handle_); } catch (...) {}
+    }
+    registry_ = std::move(o.registry_);
+    rng_handle_ = std::exchange(o.rng_handle_, Handle{});
+    def_ = std::move(o.def_);
+    layers_ = std::move(o.layers_);
+    bottoms_ = std::move(o.bottoms_);
+    tops_ = std::move(o.tops_);
+    blobs_ = std::move(o.blobs_);
+    blob_index_ = std::move(o.blob_index_);
+    producer_index_ = std::move(o.producer_index_);
+    params_ = std::move(o.params_);
+    output_names_ = std::move(o.output_names_);
+    loss_tops_ = std::move(o.loss_tops_);
+    layer_param_begin_ = std::move(o.layer_param_begin_);
+    param_offsets_ = std::move(o.param_offsets_);
+    param_total_ = o.param_total_;
+    weight_arena_ = o.weight_arena_;
+    grad_arena_ = o.grad_arena_;
+    backward_hook_ = std::move(o.backward_hook_);
+  }
+  return *this;
+}
+
+std::map<std::string, Blob*> Net::forward() {
+  for (std::size_t i = 0; i < layers_.size(); ++i) layers_[i]->forward(bottoms_[i], tops_[i]);
+  std::map<std::string, Blob*> outputs;
+  for (const std::string& name : output_names_) outputs.emplace(name, blob_index_.at(name));
+  return outputs;
+}
+
+void Net::backward() {
+  for (std::size_t i = layers_.size(); i-- > 0;) {
+    layers_[i]->backward(tops_[i], bottoms_[i]);
+    if (backward_hook_) backward_hook_(i);
+  }
+}
+
+void Net::backward_from(const std::string& blob_name) {
+  auto it = producer_index_.find(blob_name);
+  if (it == producer_index_.end()) throw ModelError("backward_from: no layer produces blob '" + blob_name + "'");
+  for (std::size_t i = it->second + 1; i-- > 0;) {
+    layers_[i]->backward(tops_[i], bottoms_[i]);
+    if (backward_hook_) backward_hook_(i);
+  }
+}
+
+bool Net::has_blob(const std::string& name) const { return blob_index_.contains(name); }
+
+Blob& Net::blob(const std::string& name) {
+  auto it = blob_index_.find(name);
+  if (it == blob_index_.end()) throw NotFound("no blob named '" + name + "'");
+  return *it->second;
+}
+
+const Blob& Net::blob(const std::string& name) const { return const_cast<Net*>(this)->blob(name); }
+
+Layer* Net::find_layer(const std::string& name) {
+  for (const auto& l : layers_)
+    if (l->name() == name) return l.get();
+  return nullptr;
+}
+
+std::vector<std::pair<std::string, Shape>> Net::blob_shapes() const {
+  std::vector<std::pair<std::string, Shape>> out;
+  out.reserve(blobs_.size());
+  for (const auto& b : blobs_) out.emplace_back(b->name(), b->shape());
+  return out;
+}
+
+double Net::loss() const {
+  double s = 0;
+  for (const Blob* b : loss_tops_) s += static_cast<double>(b->data()[0]);
+  return s;
+}
+
+void Net::set_batch(const real* data, const real* labels) {
+  for (std::size_t i = 0; i < layers_.size(); ++i) {
+    if (auto* md = dynamic_cast<MemoryDataLayer*>(layers_[i].get())) {
+      md->set_batch(*tops_[i][0], tops_[i].size() > 1 ? tops_[i][1] : nullptr, data, labels);
+      return;
+    }
+  }
+  throw ModelError("set_batch: net has no MemoryData layer");
+}
+
+bool Net::graph_safe() const {
+  for (std::size_t i = 0; i < layers_.size(); ++i) {
+    auto* md = dynamic_cast<const MemoryDataLayer*>(layers_[i].get());
+    if (md ? !md->has_staged_batch() : !layers_[i]->graph_safe()) return false;
+  }
+  return true;
+}
+
+// ---- MCWT v1 weight snapshots (reference net.cpp:144-286) ------------------------------
+// "MCWT" | u32 version=1 | u32 blob count | per blob: u32 name length, name,
+// u32 dims[4] (NCHW), f64 values — little endian, f64 whatever `real` is.
+
+std::vector<std::uint8_t> Net::snapshot_weights() const {
+  std::vector<std::uint8_t> out = {'M', 'C', 'W', 'T'};
+  auto put32 = [&](std::uint32_t v) {
+    for (int s = 0; s < 32; s += 8) out.push_back(static_cast<std::uint8_t>(v >> s));
+  };
+  put32(1);
+  put32(static_cast<std::uint32_t>(params_.size()));
+  for (const Blob* p : params_) {
+    put32(static_cast<std::uint32_t>(p->name().size()));
+    out.insert(out.end(), p->name().begin(), p->name().end());
+    for (int d : p->shape().d) put32(static_cast<std::uint32_t>(d));
+    for (real v : p->data()) {
+      const std::uint64_t bits = std::bit_cast<std::uint64_t>(static_cast<double>(v));
+      for (int s = 0; s < 64; s += 8) out.push_back(static_cast<std::uint8_t>(bits >> s));
+    }
+  }
+  return out;
+}
+
+void Net::restore_weights(std::span<const std::uint8_t> bytes) {
+  std::size_t at = 0;
+  auto need = [&](std::size_t n) {
+    if (bytes.size() - at < n) throw FormatError("weight snapshot: truncated payload");
+  };
+  auto get32 = [&] {
+    need(4);
+    std::uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) v |= std::uint32_t(bytes[at + i]) << (8 * i);
+    at += 4;
+    return v;
+  };
+  need(4);
+  if (std::memcmp(bytes.data(), "MCWT", 4) != 0) throw FormatError("weight snapshot: bad magic");
+  at = 4;
+  const std::uint32_t version = get32();
+  if (version != 1) throw FormatError("weight snapshot: unsupported version " + std::to_string(version));
+  const std::uint32_t count = get32();
+  if (count != params_.size())
+    throw FormatError("weight snapshot: holds " + std::to_string(count) + " blob(s), net has " +
+                      std::to_string(params_.size()));
+  for (Blob* p : params_) {
+    const std::uint32_t len = get32();
+    need(len);
+    const std::string name(reinterpret_cast<const char*>(bytes.data() + at), len);
+    at += len;
+    if (name != p->name()) throw FormatError("weight snapshot: blob '" + name + "' does not match '" + p->name() + "'");
+    Shape s;
+    for (int i = 0; i < 4; ++i) s.d[i] = static_cast<int>(get32());
+    if (s != p->shape())
+      throw FormatError("weight snapshot: blob '" + name + "' has shape " + to_string(s) + ", net expects " +
+                        to_string(p->shape()));
+    need(8 * p->count());
+    auto dst = p->data();
+    for (real& v : dst) {
+      std::uint64_t bits = 0;
+      for (int i = 0; i < 8; ++i) bits |= std::uint64_t(bytes[at + i]) << (8 * i);
+      at += 8;
+      v = static_cast<real>(std::bit_cast<double>(bits));
+    }
+  }
+  if (at != bytes.size()) throw FormatError("weight snapshot: trailing bytes");
+}
+
+}  // namespace polegrad

@@ -1,0 +1,96 @@
+// parallel.cpp — bucketed NCCL gradient all-reduce overlapped with backward.
+#include "polegrad/parallel.hpp"
+
+#include <algorithm>
+
+#include "polegrad/errors.hpp"
+
+namespace polegrad {
+
+std::vector<GradBucket> plan_buckets(const std::vector<std::size_t>& offsets, const std::vector<std::size_t>& counts,
+                                     std::size_t total, std::size_t bucket_elems) {
+  if (offsets.size() != counts.size()) throw InvalidArgument("plan_buckets: offsets/counts length mismatch");
+  std::vector<GradBucket> out;
+  if (offsets.empty()) return out;
+  bucket_elems = std::max<std::size_t>(bucket_elems, 1);
+  std::size_t end = total;  // buckets tile the arena from the back (padding included)
+  std::size_t acc = 0;
+  for (std::size_t i = offsets.size(); i-- > 0;) {
+    acc += counts[i];
+    if (acc >= bucket_elems || i == 0) {
+      const std::size_t begin = i == 0 ? 0 : offsets[i];
+      out.push_back(GradBucket{begin, end, i});
+      end = begin;
+      acc = 0;
+    }
+  }
+  return out;
+}
+
+Parallel::UniqueId Parallel::unique_id() {
+  UniqueId id{};
+  cdnn_ok(cdnn_nccl_unique_id(id.data()), "Parallel::unique_id");
+  return id;
+}
+
+Parallel::Parallel(Net& net, int nranks, int rank, const UniqueId& id, std::size_t bucket_bytes)
+    : net_(&net), nranks_(nranks), rank_(rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("Parallel: bad rank / nranks");
+  Registry& reg = *net.registry();
+  cdnn_ok(cdnn_nccl_comm_create(reg.context(), nranks, rank, id.data(), &comm_), "Parallel");
+  cdnn_ok(cdnn_stream_create(reg.context(), &comm_stream_), "Parallel");
+  std::vector<std::size_t> offs, counts;
+  for (std::size_t i = 0; i < net.params().size(); ++i) {
+    offs.push_back(net.param_offset(i));
+    counts.push_back(net.params()[i]->count());
+  }
+  buckets_ = plan_buckets(offs, counts, net.param_total(), std::max<std::size_t>(bucket_bytes / sizeof(real), 1));
+  launched_.assign(buckets_.size(), false);
+  net.set_backward_hook([this](std::size_t layer) { on_layer_done(layer); });
+}
+
+Parallel::~Parallel() {
+  if (net_) net_->set_backward_hook(nullptr);
+  Registry& reg = *net_->registry();
+  if (comm_stream_) cdnn_stream_free(reg.context(), comm_stream_);
+  if (comm_) cdnn_subsystem_free(reg.context(), comm_);
+}
+
+void Parallel::broadcast_weights() {
+  Registry& reg = *net_->registry();
+  for (Blob* p : net_->params()) p->gpu_data();  // upload any host-side edits first
+  cdnn_ok(cdnn_broadcast(reg.context(), comm_, reg.in(net_->weight_arena()), net_->param_total(), 0, reg.stream()),
+          "broadcast_weights");
+  for (Blob* p : net_->params()) p->overwrite_gpu_data();
+}
+
+void Parallel::launch(std::size_t b) {
+  if (launched_[b]) return;
+  launched_[b] = true;
+  if (nranks_ == 1) return;  // one rank: the sum is the local gradient
+  Registry& reg = *net_->registry();
+  const GradBucket& k = buckets_[b];
+  // the comm stream waits for every gradient queued so far on the compute stream
+  cdnn_ok(cdnn_stream_wait(reg.context(), comm_stream_, reg.stream()), "allreduce");
+  cdnn_ok(cdnn_allreduce_sum(reg.context(), comm_, reg.in(net_->grad_arena()), k.begin, k.end - k.begin, comm_stream_),
+          "allreduce");
+}
+
+void Parallel::on_layer_done(std::size_t layer) {
+  // backward runs layers in reverse: once layer `layer` is done, every
+  // parameter with index >= first_param_of_layer(layer) has its gradient.
+  const std::size_t ready_from = net_->first_param_of_layer(layer);
+  for (std::size_t b = 0; b < buckets_.size(); ++b)
+    if (!launched_[b] && buckets_[b].first_param >= ready_from) launch(b);
+}
+
+void Parallel::reduce_gradients(Net& net) {
+  if (&net != net_) throw InvalidArgument("Parallel: solver applied to another net");
+  for (Blob* p : net.params()) p->gpu_diff();  // host-side gradient edits go up first
+  for (std::size_t b = 0; b < buckets_.size(); ++b) launch(b);
+  Registry& reg = *net.registry();
+  if (nranks_ > 1) cdnn_ok(cdnn_stream_wait(reg.context(), reg.stream(), comm_stream_), "allreduce join");
+  launched_.assign(buckets_.size(), false);
+}
+
+}  // namespace polegrad
