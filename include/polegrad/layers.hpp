@@ -289,8 +289,12 @@ class SoftmaxWithLossLayer final : public Layer {
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   const Blob& prob() const { return *prob_; }
+  // Extra factor on the gradient (1/nranks under data parallelism, so the
+  // sum all-reduce of per-rank normalised gradients is the global mean).
+  void set_loss_scale(double s) { loss_scale_ = s; }
 
  private:
+  double loss_scale_ = 1.0;
   bool normalize_;
   int rows_ = 0, classes_ = 0;
   std::unique_ptr<Blob> prob_;

@@ -84,6 +84,8 @@ class Net {
   std::size_t first_param_of_layer(std::size_t i) const { return layer_param_begin_.at(i); }
   // True when forward/backward contain no host work (graph capturable).
   bool graph_safe() const;
+  // Scale the gradient of every SoftmaxWithLoss layer (see Parallel).
+  void set_loss_scale(double s);
 
  private:
   void build(const NetDef& def, std::uint64_t seed, int device);

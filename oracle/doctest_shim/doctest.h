@@ -90,13 +90,21 @@ struct Capture {
 };
 
 inline int run(int argc, char** argv) {
-  const std::string filter = argc > 1 ? argv[1] : "";
+  // args: substrings of the test-case name or source path; "-x" excludes x
+  std::vector<std::string> keep, drop;
+  for (int i = 1; i < argc; ++i) {
+    const std::string a = argv[i];
+    if (!a.empty() && a[0] == '-') drop.push_back(a.substr(1));
+    else keep.push_back(a);
+  }
+  auto hit = [](const TestCase& tc, const std::string& s) {
+    return std::string(tc.name).find(s) != std::string::npos || std::string(tc.file).find(s) != std::string::npos;
+  };
   int failed = 0, ran = 0;
   for (const TestCase& tc : registry()) {
-    // filter: substring of the test-case name or of its source file path
-    if (!filter.empty() && std::string(tc.name).find(filter) == std::string::npos &&
-        std::string(tc.file).find(filter) == std::string::npos)
+    if (!keep.empty() && std::none_of(keep.begin(), keep.end(), [&](const std::string& s) { return hit(tc, s); }))
       continue;
+    if (std::any_of(drop.begin(), drop.end(), [&](const std::string& s) { return hit(tc, s); })) continue;
     ++ran;
     state().current_failed = false;
     try {

@@ -219,7 +219,7 @@ void SoftmaxWithLossLayer::backward(std::span<Blob* const> tops, std::span<Blob*
   const cdnn_handle p = prob_->gpu_data(), lab = bottoms[1]->gpu_data();
   // loss weight 1 (Caffe default); kept on the host so backward is graph capturable
   cdnn_ok(cdnn_softmax_loss_backward(reg.context(), p, lab, bottoms[0]->overwrite_gpu_diff(), rows_, classes_,
-                                     normalize_ ? 1 : 0, 1.0, reg.stream()),
+                                     normalize_ ? 1 : 0, loss_scale_, reg.stream()),
           "SoftmaxWithLoss backward");
 }
 

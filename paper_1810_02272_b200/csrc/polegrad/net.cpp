@@ -266,6 +266,11 @@ void Net::set_batch(const real* data, const real* labels) {
   throw ModelError("set_batch: net has no MemoryData layer");
 }
 
+void Net::set_loss_scale(double s) {
+  for (auto& l : layers_)
+    if (auto* sl = dynamic_cast<SoftmaxWithLossLayer*>(l.get())) sl->set_loss_scale(s);
+}
+
 bool Net::graph_safe() const {
   for (std::size_t i = 0; i < layers_.size(); ++i) {
     auto* md = dynamic_cast<const MemoryDataLayer*>(layers_[i].get());

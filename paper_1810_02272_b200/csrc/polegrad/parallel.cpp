@@ -47,6 +47,10 @@ Parallel::Parallel(Net& net, int nranks, int rank, const UniqueId& id, std::size
   buckets_ = plan_buckets(offs, counts, net.param_total(), std::max<std::size_t>(bucket_bytes / sizeof(real), 1));
   launched_.assign(buckets_.size(), false);
   net.set_backward_hook([this](std::size_t layer) { on_layer_done(layer); });
+  // Normalised losses average over the local batch; 1/nranks makes the SUM
+  // all-reduce the global-batch mean (Caffe divides by solver_count).
+  // MemoryLoss nets inject unnormalised diffs, for which the plain sum is exact.
+  net.set_loss_scale(1.0 / nranks);
 }
 
 Parallel::~Parallel() {

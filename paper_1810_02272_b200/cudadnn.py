@@ -142,6 +142,24 @@ def device_count() -> int:
     return n.value
 
 
+class PinnedBuffer:
+    """Page-locked host memory (cudaMallocHost) viewed as a numpy array; the
+    feed / loss buffers of a captured step must be pinned."""
+
+    def __init__(self, shape, dtype=np.float32):
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        check(load().cdnn_host_alloc_pinned(max(self.nbytes, 1), C.byref(p)))
+        self.ptr = p.value
+        raw = (C.c_uint8 * max(self.nbytes, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(raw, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            load().cdnn_host_free_pinned(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
 class Context:
     """One CudaDnn context (device + handle tables + compute stream)."""
 

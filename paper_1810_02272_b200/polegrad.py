@@ -1,0 +1,317 @@
+"""ctypes binding of include/polegrad_c.h — the reference-compatible Net /
+Solver / Parallel API of the B200 library, in float (TF32 tensor cores) or
+double (SIMT FP64) flavour.
+
+    net = Net(open("models/cifar10_quick.prototxt").read(), seed=1, dtype="f32")
+    solver = Solver(net, method="sgd", lr=1e-3, momentum=0.9, weight_decay=4e-3)
+    net.set_batch(images, labels); net.forward(); net.backward(); solver.apply()
+
+Everything runs on the GPU through libcudadnn.so; without a device the
+constructor raises (status NO_DEVICE) — there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import cudadnn
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+MODELS_DIR = os.path.join(_HERE, "models")
+_LIBS: Dict[str, C.CDLL] = {}
+NP_DTYPE = {"f32": np.float32, "f64": np.float64}
+
+EXPORTS = [
+    "pg_last_error", "pg_real_size", "pg_net_create", "pg_net_free", "pg_net_forward", "pg_net_backward",
+    "pg_net_backward_from", "pg_net_loss", "pg_net_set_batch", "pg_net_enqueue", "pg_net_sync", "pg_net_context",
+    "pg_net_num_layers", "pg_net_layer_name", "pg_blob_shape", "pg_blob_get", "pg_blob_set", "pg_param_count",
+    "pg_param_info", "pg_param_get", "pg_param_set", "pg_pool_mask", "pg_snapshot", "pg_restore",
+    "pg_solver_create", "pg_solver_free", "pg_solver_apply", "pg_step_capture", "pg_step_replay", "pg_graph_free",
+    "pg_parallel_unique_id", "pg_parallel_create", "pg_parallel_free", "pg_parallel_broadcast",
+    "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip",
+]
+
+
+def lib_path(dtype: str) -> str:
+    return os.path.join(cudadnn.LIB_DIR, f"libpolegrad_b200_{dtype}.so")
+
+
+def load(dtype: str = "f32") -> C.CDLL:
+    if dtype not in ("f32", "f64"):
+        raise ValueError("dtype must be 'f32' or 'f64'")
+    if dtype not in _LIBS:
+        path = lib_path(dtype)
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} is not built; run `make -j8` or __graft_entry__.build()")
+        cudadnn.load()  # libcudadnn.so first (rpath $ORIGIN resolves it anyway)
+        lib = C.CDLL(path)
+        vp, i, u64, d, cp = C.c_void_p, C.c_int, C.c_uint64, C.c_double, C.c_char_p
+        sig = {
+            "pg_last_error": ([], cp), "pg_real_size": ([], i),
+            "pg_net_create": ([cp, u64, i, C.POINTER(vp)], i), "pg_net_free": ([vp], i),
+            "pg_net_forward": ([vp], i), "pg_net_backward": ([vp], i), "pg_net_backward_from": ([vp, cp], i),
+            "pg_net_loss": ([vp, C.POINTER(d)], i), "pg_net_set_batch": ([vp, vp, vp], i),
+            "pg_net_enqueue": ([vp, cp, vp, u64], i), "pg_net_sync": ([vp], i),
+            "pg_net_context": ([vp, C.POINTER(vp)], i), "pg_net_num_layers": ([vp], i),
+            "pg_net_layer_name": ([vp, i, cp, i], i), "pg_blob_shape": ([vp, cp, C.POINTER(i)], i),
+            "pg_blob_get": ([vp, cp, i, vp], i), "pg_blob_set": ([vp, cp, i, vp], i),
+            "pg_param_count": ([vp], i), "pg_param_info": ([vp, i, cp, i, C.POINTER(i)], i),
+            "pg_param_get": ([vp, i, i, vp], i), "pg_param_set": ([vp, i, i, vp], i),
+            "pg_pool_mask": ([vp, cp, C.POINTER(C.c_int32), u64], i),
+            "pg_snapshot": ([vp, vp, u64, C.POINTER(u64)], i), "pg_restore": ([vp, vp, u64], i),
+            "pg_solver_create": ([i, d, d, d, d, d, C.POINTER(vp)], i), "pg_solver_free": ([vp], i),
+            "pg_solver_apply": ([vp, vp], i),
+            "pg_step_capture": ([vp, vp, vp, vp, vp, C.POINTER(u64)], i), "pg_step_replay": ([vp, u64], i),
+            "pg_graph_free": ([vp, u64], i), "pg_parallel_unique_id": ([cp], i),
+            "pg_parallel_create": ([vp, i, i, cp, u64, C.POINTER(vp)], i), "pg_parallel_free": ([vp], i),
+            "pg_parallel_broadcast": ([vp], i), "pg_solver_set_parallel": ([vp, vp], i),
+            "pg_plan_buckets": ([C.POINTER(u64), C.POINTER(u64), i, u64, u64, C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int32)], i),
+            "pg_prototxt_roundtrip": ([cp, cp, u64, C.POINTER(u64)], i),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes, fn.restype = args, res
+        _LIBS[dtype] = lib
+    return _LIBS[dtype]
+
+
+class PolegradError(cudadnn.CudnnError):
+    pass
+
+
+def _check(lib: C.CDLL, status: int) -> None:
+    if status != 0:
+        raise PolegradError(status, lib.pg_last_error().decode(errors="replace"))
+
+
+def prototxt_roundtrip(text: str, dtype: str = "f64") -> str:
+    lib = load(dtype)
+    n = C.c_uint64(0)
+    _check(lib, lib.pg_prototxt_roundtrip(text.encode(), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib, lib.pg_prototxt_roundtrip(text.encode(), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def plan_buckets(offsets: List[int], counts: List[int], total: int, bucket_elems: int,
+                 dtype: str = "f32") -> Tuple[List[int], int]:
+    """Host-only bucket planner of polegrad::Parallel (no GPU needed)."""
+    lib = load(dtype)
+    n = len(offsets)
+    o = (C.c_uint64 * max(n, 1))(*offsets)
+    c = (C.c_uint64 * max(n, 1))(*counts)
+    out = (C.c_int32 * max(n, 1))()
+    nb = C.c_int32()
+    _check(lib, lib.pg_plan_buckets(o, c, n, total, bucket_elems, out, C.byref(nb)))
+    return [out[i] for i in range(n)], nb.value
+
+
+def load_model(name: str) -> str:
+    with open(os.path.join(MODELS_DIR, name if name.endswith(".prototxt") else name + ".prototxt")) as f:
+        return f.read()
+
+
+class Net:
+    """polegrad::Net on a CUDA device (reference net.hpp API)."""
+
+    def __init__(self, prototxt: str, seed: int = 1, dtype: str = "f32", device: int = 0):
+        self.dtype = dtype
+        self.np = NP_DTYPE[dtype]
+        self.lib = load(dtype)
+        p = C.c_void_p()
+        _check(self.lib, self.lib.pg_net_create(prototxt.encode(), seed, device, C.byref(p)))
+        self.ptr = p
+        self._shapes: Dict[str, Tuple[int, ...]] = {}
+
+    def close(self) -> None:
+        if self.ptr:
+            _check(self.lib, self.lib.pg_net_free(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, name: str, *args) -> None:
+        _check(self.lib, getattr(self.lib, name)(self.ptr, *args))
+
+    # ---- execution -------------------------------------------------------------------
+    def forward(self) -> None:
+        self._c("pg_net_forward")
+
+    def backward(self) -> None:
+        self._c("pg_net_backward")
+
+    def backward_from(self, blob: str) -> None:
+        self._c("pg_net_backward_from", blob.encode())
+
+    def loss(self) -> float:
+        v = C.c_double()
+        self._c("pg_net_loss", C.byref(v))
+        return v.value
+
+    def set_batch(self, data: np.ndarray, labels: Optional[np.ndarray] = None) -> None:
+        """Synchronous-safe staging: keeps references until the next sync."""
+        self._staged = (np.ascontiguousarray(data, self.np),
+                        None if labels is None else np.ascontiguousarray(labels, self.np))
+        d, l = self._staged
+        self._c("pg_net_set_batch", d.ctypes.data_as(C.c_void_p), None if l is None else l.ctypes.data_as(C.c_void_p))
+        self.sync()
+
+    def set_batch_ptr(self, data_ptr: int, labels_ptr: Optional[int]) -> None:
+        self._c("pg_net_set_batch", C.c_void_p(data_ptr), C.c_void_p(labels_ptr) if labels_ptr else None)
+
+    def enqueue(self, sample: np.ndarray, layer: str = "") -> None:
+        s = np.ascontiguousarray(sample, self.np).ravel()
+        self._c("pg_net_enqueue", layer.encode(), s.ctypes.data_as(C.c_void_p), s.size)
+
+    def sync(self) -> None:
+        self._c("pg_net_sync")
+
+    def context_ptr(self) -> int:
+        p = C.c_void_p()
+        self._c("pg_net_context", C.byref(p))
+        return p.value
+
+    def layer_names(self) -> List[str]:
+        n = self.lib.pg_net_num_layers(self.ptr)
+        out = []
+        buf = C.create_string_buffer(256)
+        for i in range(n):
+            self._c("pg_net_layer_name", i, buf, 256)
+            out.append(buf.value.decode())
+        return out
+
+    # ---- blobs / params -------------------------------------------------------------------
+    def blob_shape(self, name: str) -> Tuple[int, ...]:
+        s = (C.c_int * 4)()
+        self._c("pg_blob_shape", name.encode(), s)
+        return tuple(s)
+
+    def blob(self, name: str, diff: bool = False) -> np.ndarray:
+        shape = self.blob_shape(name)
+        out = np.empty(shape, self.np)
+        self._c("pg_blob_get", name.encode(), int(diff), out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def set_blob(self, name: str, values: np.ndarray, diff: bool = False) -> None:
+        shape = self.blob_shape(name)
+        v = np.ascontiguousarray(values, self.np).reshape(shape)
+        self._c("pg_blob_set", name.encode(), int(diff), v.ctypes.data_as(C.c_void_p))
+
+    def param_info(self) -> List[Tuple[str, Tuple[int, ...]]]:
+        out = []
+        buf = C.create_string_buffer(256)
+        for i in range(self.lib.pg_param_count(self.ptr)):
+            s = (C.c_int * 4)()
+            self._c("pg_param_info", i, buf, 256, s)
+            out.append((buf.value.decode(), tuple(s)))
+        return out
+
+    def param(self, i: int, diff: bool = False) -> np.ndarray:
+        shape = self.param_info()[i][1]
+        out = np.empty(shape, self.np)
+        self._c("pg_param_get", i, int(diff), out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def set_param(self, i: int, values: np.ndarray, diff: bool = False) -> None:
+        shape = self.param_info()[i][1]
+        v = np.ascontiguousarray(values, self.np).reshape(shape)
+        self._c("pg_param_set", i, int(diff), v.ctypes.data_as(C.c_void_p))
+
+    def pool_mask(self, layer: str) -> np.ndarray:
+        # size from the layer's top: look it up through the layer list / blob shapes
+        n = 1 << 26
+        buf = np.empty(0, np.int32)
+        for cap in (1 << 16, 1 << 20, 1 << 24, n):
+            buf = np.empty(cap, np.int32)
+            st = self.lib.pg_pool_mask(self.ptr, layer.encode(), buf.ctypes.data_as(C.POINTER(C.c_int32)), cap)
+            if st == 0:
+                return buf
+            if st != 1:
+                _check(self.lib, st)
+        _check(self.lib, 1)
+        return buf
+
+    def snapshot(self) -> bytes:
+        n = C.c_uint64()
+        self._c("pg_snapshot", None, 0, C.byref(n))
+        buf = (C.c_uint8 * n.value)()
+        self._c("pg_snapshot", buf, n.value, C.byref(n))
+        return bytes(buf)
+
+    def restore(self, blob: bytes) -> None:
+        b = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        self._c("pg_restore", b, len(blob))
+
+
+class Solver:
+    """polegrad::Solver (SGD / RMSProp + Caffe momentum & weight decay)."""
+
+    def __init__(self, net: Net, method: str = "sgd", lr: float = 1e-3, momentum: float = 0.0,
+                 weight_decay: float = 0.0, rms_decay: float = 0.99, epsilon: float = 1e-8):
+        self.net = net
+        self.lib = net.lib
+        p = C.c_void_p()
+        _check(self.lib, self.lib.pg_solver_create(1 if method == "rmsprop" else 0, lr, momentum, weight_decay,
+                                                   rms_decay, epsilon, C.byref(p)))
+        self.ptr = p
+
+    def apply(self) -> None:
+        _check(self.lib, self.lib.pg_solver_apply(self.ptr, self.net.ptr))
+
+    def set_parallel(self, par: Optional["Parallel"]) -> None:
+        _check(self.lib, self.lib.pg_solver_set_parallel(self.ptr, par.ptr if par else None))
+
+    def close(self) -> None:
+        if self.ptr:
+            _check(self.lib, self.lib.pg_solver_free(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class StepGraph:
+    """One captured training step: H2D(pinned batch) -> fwd -> bwd -> update -> D2H(loss)."""
+
+    def __init__(self, net: Net, solver: Solver, data_ptr: int, labels_ptr: Optional[int], loss_ptr: int):
+        self.net = net
+        g = C.c_uint64()
+        _check(net.lib, net.lib.pg_step_capture(net.ptr, solver.ptr, C.c_void_p(data_ptr),
+                                                C.c_void_p(labels_ptr) if labels_ptr else None,
+                                                C.c_void_p(loss_ptr), C.byref(g)))
+        self.graph = g.value
+
+    def replay(self) -> None:
+        _check(self.net.lib, self.net.lib.pg_step_replay(self.net.ptr, self.graph))
+
+
+class Parallel:
+    """polegrad::Parallel — NCCL data parallelism, one rank per process."""
+
+    @staticmethod
+    def unique_id(dtype: str = "f32") -> bytes:
+        lib = load(dtype)
+        buf = C.create_string_buffer(128)
+        _check(lib, lib.pg_parallel_unique_id(buf))
+        return buf.raw[:128]
+
+    def __init__(self, net: Net, nranks: int, rank: int, uid: bytes, bucket_bytes: int = 8 << 20):
+        self.net = net
+        p = C.c_void_p()
+        _check(net.lib, net.lib.pg_parallel_create(net.ptr, nranks, rank, C.c_char_p(uid), bucket_bytes,
+                                                   C.byref(p)))
+        self.ptr = p
+
+    def broadcast(self) -> None:
+        _check(self.net.lib, self.net.lib.pg_parallel_broadcast(self.ptr))

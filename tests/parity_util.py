@@ -1,0 +1,97 @@
+"""Shared helpers for the parity tests: synthetic inputs, the
+per-tensor error metrics and lock-step training of the
+B200 net against the CPU oracle."""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from oracle import pyoracle  # noqa: E402  (test infrastructure only)
+from paper_1810_02272_b200 import polegrad  # noqa: E402
+
+# Tolerances from north_star: 1e-5 relative (FP64) and 2e-3 relative (TF32)
+# after 10 iterations, measured per tensor as relative L2 error.
+TOL = {"f64": 1e-5, "f32": 2e-3}
+
+CONFIGS = {
+    # model, solver kwargs, classes
+    "lenet": ("lenet", dict(method="sgd", lr=0.01, momentum=0.9, weight_decay=5e-4), 10),
+    "cifar10_quick": ("cifar10_quick", dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=4e-3), 10),
+    "pg_mlp": ("pg_mlp", dict(method="rmsprop", lr=1e-3, rms_decay=0.99, epsilon=1e-8), 2),
+}
+
+
+def rel_l2(a, b) -> float:
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    d = float(np.linalg.norm(a - b))
+    n = float(np.linalg.norm(b))
+    return d / n if n > 0 else d
+
+
+def synthetic_batches(shape, classes, iters, seed=2):
+    """U(-1,1) NCHW data and floor(u*C) labels, drawn from one stream."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(iters):
+        x = rng.uniform(-1.0, 1.0, shape)
+        y = np.floor(rng.uniform(0.0, 1.0, shape[0]) * classes)
+        out.append((x, y))
+    return out
+
+
+def data_shape(text: str):
+    _, info = pyoracle.to_spec(text)
+    return tuple(info["data"][2]), len(info["data"][1]) == 2
+
+
+def lockstep(config: str, dtype: str, iters: int = 10, seed: int = 1, check_every: bool = True):
+    """Train the B200 Net and the oracle side by side from identical weights
+    and inputs; returns per-iteration losses/metrics and the final nets."""
+    model, skw, classes = CONFIGS[config]
+    text = polegrad.load_model(model)
+    shape, labelled = data_shape(text)
+    net = polegrad.Net(text, seed=seed, dtype=dtype)
+    orc = pyoracle.OracleNet(text, seed=seed, dtype=dtype)
+    solver = polegrad.Solver(net, **skw)
+    osolver = pyoracle.OracleSolver(orc, **skw)
+    # same seeded init on both sides
+    init_bitexact = all(np.array_equal(net.param(i).astype(np.float64), orc.param(i))
+                        for i in range(len(net.param_info())))
+    batches = synthetic_batches(shape, classes, iters)
+    diff_rng = np.random.default_rng(3)
+    hist = []
+    for x, y in batches:
+        if labelled:
+            net.set_batch(x, y)
+            orc.set_batch(x, y)
+            net.forward()
+            lo = orc.forward()
+            l = net.loss()
+            net.backward()
+            orc.backward()
+        else:  # PG: inject policy-gradient diffs at the logits, backward_from (trainer.cpp:171-216)
+            net.set_batch(x)
+            orc.set_batch(x)
+            net.forward()
+            orc.forward()
+            g = diff_rng.uniform(-1.0, 1.0, net.blob_shape("logits"))
+            net.set_blob("logits", g, diff=True)
+            orc.set_blob("logits", g, diff=True)
+            net.backward_from("logits")
+            orc.backward_from("logits")
+            l = float(np.sum(net.blob("prob")))
+            lo = float(np.sum(orc.blob("prob")))
+        grads = [rel_l2(net.param(i, diff=True), orc.param(i, diff=True)) for i in range(len(net.param_info()))]
+        solver.apply()
+        osolver.apply()
+        hist.append({"loss": l, "oracle_loss": lo, "grad_rel": grads})
+    weights = [rel_l2(net.param(i), orc.param(i)) for i in range(len(net.param_info()))]
+    return {"net": net, "oracle": orc, "hist": hist, "weights_rel": weights, "init_bitexact": init_bitexact,
+            "params": net.param_info()}

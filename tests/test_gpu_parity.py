@@ -1,0 +1,111 @@
+"""End-to-end parity of the B200 training step against the CPU oracle.
+
+Oracle: the unmodified reference Net / Solver for the MLP (pg_mlp) and the
+reference-style extension net for LeNet / CIFAR-10 quick (oracle/ext), both
+built from /root/reference sources by oracle/Makefile.  Same seed -> same
+initial weights (checked bit-exact), same synthetic inputs, 10 iterations.
+Bars (north_star): losses, gradients and updated weights within 1e-5
+relative (FP64) / 2e-3 relative (TF32), per tensor as relative L2; integer
+outputs (pooling argmax masks, predicted labels) bit-exact on identical
+inputs.
+"""
+import numpy as np
+import pytest
+
+from parity_util import TOL, lockstep, pyoracle, polegrad, rel_l2, synthetic_batches
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick"])
+def test_ten_iterations_match_oracle(config, dtype):
+    r = lockstep(config, dtype, iters=10)
+    assert r["init_bitexact"], "seeded initial weights must be identical"
+    tol = TOL[dtype]
+    for it, h in enumerate(r["hist"]):
+        assert abs(h["loss"] - h["oracle_loss"]) <= tol * max(abs(h["oracle_loss"]), 1e-12), (it, h)
+        for (name, _), e in zip(r["params"], h["grad_rel"]):
+            assert e <= tol, (it, name, e)
+    for (name, _), e in zip(r["params"], r["weights_rel"]):
+        assert e <= tol, (name, e)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_pool_masks_bit_exact(dtype):
+    """MAX-pool argmax (int32) on identical inputs: the LeNet / CIFAR pooling shapes."""
+    for (n, c, h, w, k, s) in [(4, 20, 24, 24, 2, 2), (4, 32, 32, 32, 3, 2), (2, 50, 8, 8, 2, 2)]:
+        text = f"""
+layer {{ name: "d" type: "MemoryData" top: "x" memory_data_param {{ batch_size: {n} channels: {c} height: {h} width: {w} }} }}
+layer {{ name: "p" type: "Pooling" bottom: "x" top: "y" pooling_param {{ pool: MAX kernel_size: {k} stride: {s} }} }}
+"""
+        net = polegrad.Net(text, 1, dtype)
+        orc = pyoracle.OracleNet(text, 1, "f64" if dtype == "f64" else "f32")
+        x = np.random.default_rng(n * c + h).standard_normal((n, c, h, w))
+        # ties on purpose: quantise so equal maxima occur inside windows
+        x = np.round(x * 2) / 2
+        net.set_batch(x)
+        orc.set_batch(x)
+        net.forward()
+        orc.forward()
+        cnt = int(np.prod(net.blob_shape("y")))
+        assert np.array_equal(net.pool_mask("p")[:cnt], orc.pool_mask("p", cnt))
+        assert np.array_equal(net.blob("y").astype(np.float64), orc.blob("y"))
+
+
+def test_predicted_labels_bit_exact_fp64():
+    text = polegrad.load_model("cifar10_quick")
+    net = polegrad.Net(text, 1, "f64")
+    orc = pyoracle.OracleNet(text, 1, "f64")
+    (x, y), = synthetic_batches((100, 3, 32, 32), 10, 1)
+    net.set_batch(x, y)
+    orc.set_batch(x, y)
+    net.forward()
+    orc.forward()
+    assert np.array_equal(np.argmax(net.blob("ip2").reshape(100, 10), 1),
+                          np.argmax(orc.blob("ip2").reshape(100, 10), 1))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mcwt_snapshot_transport(dtype):
+    """MCWT bytes written by the oracle restore into the B200 net and back unchanged."""
+    text = polegrad.load_model("lenet")
+    orc = pyoracle.OracleNet(text, 7, dtype)
+    net = polegrad.Net(text, 1, dtype)
+    blob = orc.snapshot()
+    net.restore(blob)
+    assert net.snapshot() == blob
+
+
+def test_step_graph_matches_eager():
+    """CUDA-graph replay of the whole step == eager step, bit for bit."""
+    text = polegrad.load_model("cifar10_quick")
+    batches = synthetic_batches((100, 3, 32, 32), 10, 4)
+    kw = dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=4e-3)
+    a = polegrad.Net(text, 1, "f32")
+    sa = polegrad.Solver(a, **kw)
+    b = polegrad.Net(text, 1, "f32")
+    sb = polegrad.Solver(b, **kw)
+    for x, y in batches[:1]:  # one eager warm-up step on both
+        for n, s in ((a, sa), (b, sb)):
+            n.set_batch(x, y)
+            n.forward()
+            n.backward()
+            s.apply()
+    from paper_1810_02272_b200.cudadnn import PinnedBuffer
+    pd, pl, ploss = PinnedBuffer((100, 3, 32, 32)), PinnedBuffer((100,)), PinnedBuffer((1,))
+    data, lab, loss = pd.array, pl.array, ploss.array
+    g = polegrad.StepGraph(b, sb, pd.ptr, pl.ptr, ploss.ptr)
+    for x, y in batches[1:]:
+        a.set_batch(x, y)
+        a.forward()
+        la = a.loss()
+        a.backward()
+        sa.apply()
+        data[...] = x
+        lab[...] = y
+        g.replay()
+        b.sync()
+        assert loss[0] == np.float32(la)
+    for i in range(len(a.param_info())):
+        assert np.array_equal(a.param(i), b.param(i))
