@@ -114,6 +114,17 @@ CDNN_API int cdnn_live_slots(cdnn_ctx ctx, uint64_t* out); /* backend.hpp:99-100
 /* number of kernels this context has launched (the bench's gpu_launches claim) */
 CDNN_API int cdnn_launch_count(cdnn_ctx ctx, uint64_t* out);
 
+/* Numerics of F32 contractions (gemm / InnerProduct / Convolution):
+ *   CDNN_MATH_TF32X3 (default)  split-precision 3xTF32 on the tensor cores:
+ *                               x = hi + lo, D += A_lo B_hi + A_hi B_lo + A_hi B_hi,
+ *                               FP32-level accuracy (gradient parity with the
+ *                               FP32 reference through ReLU gates)
+ *   CDNN_MATH_TF32              one TF32 MMA per product (fastest; TMA-fed operands)
+ * The environment variable CDNN_MATH=tf32 selects TF32 for new contexts. */
+typedef enum { CDNN_MATH_TF32 = 0, CDNN_MATH_TF32X3 = 1 } cdnn_math_mode;
+CDNN_API int cdnn_set_math_mode(cdnn_ctx ctx, int mode);
+CDNN_API int cdnn_get_math_mode(cdnn_ctx ctx, int* out);
+
 /* ---- buffers ------------------------------------------------------------- */
 /* zero-initialised; length 0 -> CDNN_INVALID_ARGUMENT (backend.cpp:18-21) */
 CDNN_API int cdnn_alloc(cdnn_ctx ctx, uint64_t length, int dtype, cdnn_handle* out);

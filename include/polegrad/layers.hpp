@@ -192,6 +192,7 @@ class MemoryDataLayer final : public Layer {
   void set_batch(Blob& data_top, Blob* label_top, const real* data, const real* labels);
   bool has_staged_batch() const { return staged_; }
   void clear_staged() { staged_ = false; }
+  void mark_staged() { staged_ = true; }
 
  private:
   std::size_t sample_size_ = 0;

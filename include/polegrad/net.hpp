@@ -86,6 +86,12 @@ class Net {
   bool graph_safe() const;
   // Scale the gradient of every SoftmaxWithLoss layer (see Parallel).
   void set_loss_scale(double s);
+  // Treat the data layer's current top contents as this step's batch (inputs
+  // already resident in HBM; no feed copy).
+  void reuse_resident_batch();
+  // One eager step with device events between layers: per-layer forward and
+  // backward milliseconds (layer order) — the kernel-share breakdown.
+  void profile_layers(std::vector<float>& fwd_ms, std::vector<float>& bwd_ms);
 
  private:
   void build(const NetDef& def, std::uint64_t seed, int device);

@@ -68,6 +68,9 @@ PG_API int pg_solver_apply(pg_solver* s, pg_net* net);
 PG_API int pg_step_capture(pg_net* net, pg_solver* s, const void* data, const void* labels, void* loss_out,
                            uint64_t* graph);
 PG_API int pg_step_replay(pg_net* net, uint64_t graph);
+/* data == NULL: no feed copy, the batch already resident in the data blob is reused */
+/* one eager forward+backward with events between layers (per-layer ms, layer order) */
+PG_API int pg_net_profile(pg_net* net, float* fwd_ms, float* bwd_ms, int cap);
 PG_API int pg_graph_free(pg_net* net, uint64_t graph);
 
 /* data parallel (NCCL); id = 128 bytes from pg_parallel_unique_id on rank 0 */

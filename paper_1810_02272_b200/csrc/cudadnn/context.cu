@@ -9,6 +9,7 @@
 //   monotone never-recycled ids                     include/polegrad/backend.hpp:17-25
 //   mt19937_64 + (u64>>11)*2^-53 uniform mapping    include/polegrad/backend.hpp:31-45
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -259,6 +260,9 @@ int cdnn_ctx_create(int device, cdnn_ctx* out) {
     CDNN_CUDA(cudaSetDevice(device));
     CDNN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->ws = std::make_shared<Workspace>();
+    if (const char* m = std::getenv("CDNN_MATH")) {
+      if (std::string(m) == "tf32") c->math_mode = CDNN_MATH_TF32;
+    }
     if (prev >= 0 && prev != device) cudaSetDevice(prev);
     *out = c.release();
   });
@@ -300,6 +304,17 @@ int cdnn_live_slots(cdnn_ctx ctx, uint64_t* out) {
 
 int cdnn_launch_count(cdnn_ctx ctx, uint64_t* out) {
   return guard([&] { *out = need_ctx(ctx)->launches.load(); });
+}
+
+int cdnn_set_math_mode(cdnn_ctx ctx, int mode) {
+  return guard([&] {
+    if (mode != CDNN_MATH_TF32 && mode != CDNN_MATH_TF32X3) fail(CDNN_INVALID_ARGUMENT, "unknown math mode");
+    need_ctx(ctx)->math_mode = mode;
+  });
+}
+
+int cdnn_get_math_mode(cdnn_ctx ctx, int* out) {
+  return guard([&] { *out = need_ctx(ctx)->math_mode; });
 }
 
 // ---- buffers ---------------------------------------------------------------------

@@ -3,20 +3,27 @@
 //   D[m][n] = sum_k A(m,k) * B(n,k)      one 128 x BN output tile per CTA,
 //                                        optional split-K over blockIdx.z
 //
+// Two numerics modes (template SPLIT):
+//   SPLIT = false  plain TF32: operands rounded to TF32, one tcgen05.mma per k8.
+//   SPLIT = true   3xTF32: each operand x = hi + lo with hi = tf32(x),
+//                  lo = tf32(x - hi); D += A_lo B_hi + A_hi B_lo + A_hi B_hi.
+//                  FP32-level accuracy on the TF32 tensor pipe (3 MMAs per k8);
+//                  the default for `real = float`, because plain TF32 flips
+//                  ReLU gates near zero and breaks gradient parity with the
+//                  FP32 reference.
+//
 // Warp roles (192 threads):
 //   warp 0      TMA producer: one elected lane issues cp.async.bulk.tensor for
-//               operands that are K-contiguous, 16 B aligned matrices
+//               operands that are K-contiguous, 16 B aligned matrices (plain
+//               TF32 mode only)
 //   warp 1      TMEM allocator + MMA issuer: one lane issues tcgen05.mma
-//               (kind::tf32, M=128, N=BN, K=8) x4 per 32-wide k-slab and
+//               (kind::tf32, M=128, N=BN, K=8) per 32-wide k-slab and
 //               tcgen05.commit's the slab's smem slot back to the producers
 //   warps 2-5   gather producers: build the other operands (im2col / strided /
 //               transposed views, see operands.cuh) straight into the
-//               128B-swizzled K-major smem layout UMMA reads, rounding to TF32;
-//               then the epilogue: tcgen05.ld the accumulator (warp w owns TMEM
-//               lanes 32*(w%4)..+31 = tile rows) and hand each element to EPI.
-//
-// smem per stage: A 128x32 fp32 (16 KB) + B BNx32 fp32; STAGES-deep ring with
-// full/empty mbarriers; accumulator BN fp32 columns of TMEM.
+//               128B-swizzled K-major smem layout UMMA reads; then the
+//               epilogue: tcgen05.ld the accumulator (warp w owns TMEM lanes
+//               32*(w%4)..+31 = tile rows) and hand each element to EPI.
 #pragma once
 
 #include <cstdint>
@@ -36,9 +43,15 @@ __host__ __device__ constexpr int tmem_cols_for(int bn) {
   return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : bn <= 256 ? 256 : 512;
 }
 
-template <int BN, int STAGES>
+template <int BN, bool SPLIT>
+__host__ __device__ constexpr int stages_for() {
+  return SPLIT ? 3 : 4;
+}
+
+template <int BN, bool SPLIT>
 __host__ __device__ constexpr int smem_bytes() {
-  return 1024 /*align slack*/ + STAGES * (BM * BK * 4 + BN * BK * 4) + (2 * STAGES + 1) * 8 + 16;
+  return 1024 /*align slack*/ + stages_for<BN, SPLIT>() * (BM * BK * 4 + BN * BK * 4) * (SPLIT ? 2 : 1) +
+         (2 * stages_for<BN, SPLIT>() + 1) * 8 + 16;
 }
 
 // Byte offset of 16-byte chunk `kc` (0..7) of row `r` in a K-major SWIZZLE_128B tile.
@@ -63,37 +76,52 @@ __host__ __device__ constexpr uint32_t make_idesc_tf32(int bn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
-// Fill one ROWS x 32 slab of operand view `v` into swizzled smem at `tile`.
-// Thread t of the 128 producers.  For row-contiguous views each thread owns
-// rows and walks k (lanes = consecutive rows -> coalesced loads); otherwise
-// 8 threads share a row, each taking 4 consecutive k.
-template <int ROWS, class V>
-__device__ __forceinline__ void gather_slab(const V& v, uint32_t tile, int row0, int k0, int t) {
+// Four consecutive-k elements of one row.  Views that are K-contiguous and
+// 16-byte aligned at this point load them with one 128-bit access.
+template <class V, class R>
+__device__ __forceinline__ float4 load4(const V& v, const R& rw, int k) {
+  return make_float4(v.at(rw, k), v.at(rw, k + 1), v.at(rw, k + 2), v.at(rw, k + 3));
+}
+template <class R>
+__device__ __forceinline__ float4 load4(const DenseView<float>& v, const R& rw, int k) {
+  if (rw.ok && v.sk == 1 && k + 3 < v.K) {
+    const float* p = v.p + rw.off + k;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) return __ldg(reinterpret_cast<const float4*>(p));
+  }
+  return make_float4(v.at(rw, k), v.at(rw, k + 1), v.at(rw, k + 2), v.at(rw, k + 3));
+}
+
+template <bool SPLIT>
+__device__ __forceinline__ void store4(uint32_t hi_tile, uint32_t lo_tile, uint32_t off, float4 x) {
+  const float a = ptx::to_tf32(x.x), b = ptx::to_tf32(x.y), c = ptx::to_tf32(x.z), d = ptx::to_tf32(x.w);
+  ptx::st_shared_v4(hi_tile + off, a, b, c, d);
+  if constexpr (SPLIT) {
+    ptx::st_shared_v4(lo_tile + off, ptx::to_tf32(x.x - a), ptx::to_tf32(x.y - b), ptx::to_tf32(x.z - c),
+                      ptx::to_tf32(x.w - d));
+  }
+}
+
+// Fill one ROWS x 32 slab of operand view `v` into swizzled smem (hi, and lo
+// when SPLIT).  Thread t of the 128 producers.  Row-contiguous views: each
+// thread owns rows and walks k (lanes = consecutive rows -> coalesced loads);
+// otherwise 8 threads share a row, each taking 4 consecutive k.
+template <int ROWS, bool SPLIT, class V>
+__device__ __forceinline__ void gather_slab(const V& v, uint32_t hi, uint32_t lo, int row0, int k0, int t) {
   static_assert((ROWS * 8) % kProducerThreads == 0, "slab rows must be a multiple of 16");
   if (v.m_contig()) {
     if constexpr (ROWS <= kProducerThreads) {
-      constexpr int KGROUPS = kProducerThreads / ROWS;   // threads sharing a row (split over k)
+      constexpr int KGROUPS = kProducerThreads / ROWS;  // threads sharing a row (split over k)
       const int r = t % ROWS;
       const auto rw = v.row(row0 + r);
 #pragma unroll
-      for (int kc = t / ROWS; kc < 8; kc += KGROUPS) {
-        const int k = k0 + kc * 4;
-        const float a = ptx::to_tf32(v.at(rw, k + 0)), b = ptx::to_tf32(v.at(rw, k + 1));
-        const float c = ptx::to_tf32(v.at(rw, k + 2)), d = ptx::to_tf32(v.at(rw, k + 3));
-        ptx::st_shared_v4(tile + sw128(r, kc), a, b, c, d);
-      }
+      for (int kc = t / ROWS; kc < 8; kc += KGROUPS) store4<SPLIT>(hi, lo, sw128(r, kc), load4(v, rw, k0 + kc * 4));
     } else {
 #pragma unroll
       for (int rr = 0; rr < ROWS / kProducerThreads; ++rr) {
         const int r = t + rr * kProducerThreads;
         const auto rw = v.row(row0 + r);
 #pragma unroll
-        for (int kc = 0; kc < 8; ++kc) {
-          const int k = k0 + kc * 4;
-          const float a = ptx::to_tf32(v.at(rw, k + 0)), b = ptx::to_tf32(v.at(rw, k + 1));
-          const float c = ptx::to_tf32(v.at(rw, k + 2)), d = ptx::to_tf32(v.at(rw, k + 3));
-          ptx::st_shared_v4(tile + sw128(r, kc), a, b, c, d);
-        }
+        for (int kc = 0; kc < 8; ++kc) store4<SPLIT>(hi, lo, sw128(r, kc), load4(v, rw, k0 + kc * 4));
       }
     }
   } else {
@@ -102,10 +130,7 @@ __device__ __forceinline__ void gather_slab(const V& v, uint32_t tile, int row0,
       const int c = t + i * kProducerThreads;
       const int r = c >> 3, kc = c & 7;
       const auto rw = v.row(row0 + r);
-      const int k = k0 + kc * 4;
-      const float a = ptx::to_tf32(v.at(rw, k + 0)), b = ptx::to_tf32(v.at(rw, k + 1));
-      const float cc = ptx::to_tf32(v.at(rw, k + 2)), d = ptx::to_tf32(v.at(rw, k + 3));
-      ptx::st_shared_v4(tile + sw128(r, kc), a, b, cc, d);
+      store4<SPLIT>(hi, lo, sw128(r, kc), load4(v, rw, k0 + kc * 4));
     }
   }
 }
@@ -115,22 +140,28 @@ struct is_tma { static constexpr bool value = false; };
 template <>
 struct is_tma<TmaView> { static constexpr bool value = true; };
 
-template <int BN, int STAGES, class VA, class VB, class EPI>
+template <int BN, bool SPLIT, class VA, class VB, class EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const VA va, const VB vb, const EPI epi, int M, int N, int K, int kt_per_split) {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
   constexpr bool kTmaA = is_tma<VA>::value;
   constexpr bool kTmaB = is_tma<VB>::value;
+  static_assert(!(SPLIT && (kTmaA || kTmaB)), "3xTF32 splits operands in the gather producers");
+  constexpr int STAGES = stages_for<BN, SPLIT>();
   constexpr uint32_t A_BYTES = BM * BK * 4;
   constexpr uint32_t B_BYTES = BN * BK * 4;
+  constexpr uint32_t STAGE_BYTES = (A_BYTES + B_BYTES) * (SPLIT ? 2 : 1);
   constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  // stage s: [A_hi | B_hi | A_lo | B_lo] (lo halves only when SPLIT)
+  auto a_hi = [&](int s) { return smem + s * STAGE_BYTES; };
+  auto b_hi = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES + B_BYTES; };
+  auto b_lo = [&](int s) { return smem + s * STAGE_BYTES + 2 * A_BYTES + B_BYTES; };
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* accum = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
@@ -146,8 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1 + 4);   // TMA warp + 4 producer warps
-      ptx::mbar_init(&empty[s], 1);      // tcgen05.commit
+      ptx::mbar_init(&full[s], 1 + 4);  // TMA warp + 4 producer warps
+      ptx::mbar_init(&empty[s], 1);     // tcgen05.commit
     }
     ptx::mbar_init(accum, 1);
     ptx::fence_mbar_init();
@@ -171,8 +202,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (bytes > 0) {
           ptx::mbar_arrive_expect_tx(&full[stage], bytes);
           const int kc = (kt_begin + kt) * BK;
-          if constexpr (kTmaA) ptx::tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kc, m0);
-          if constexpr (kTmaB) ptx::tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kc, n0);
+          if constexpr (kTmaA) ptx::tma_load_2d(a_hi(stage), &tmA, &full[stage], kc, m0);
+          if constexpr (kTmaB) ptx::tma_load_2d(b_hi(stage), &tmB, &full[stage], kc, n0);
         } else {
           ptx::mbar_arrive(&full[stage]);
         }
@@ -188,13 +219,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kt = 0; kt < nkt; ++kt) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        const uint64_t adesc = make_sw128_desc(ptx::smem_u32(sA + stage * A_BYTES));
-        const uint64_t bdesc = make_sw128_desc(ptx::smem_u32(sB + stage * B_BYTES));
+        const uint64_t ah = make_sw128_desc(ptx::smem_u32(a_hi(stage)));
+        const uint64_t bh = make_sw128_desc(ptx::smem_u32(b_hi(stage)));
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           // advance 8 tf32 = 32 bytes along K inside the swizzle row
-          ptx::mma_tf32(tmem, adesc + uint64_t(2 * j), bdesc + uint64_t(2 * j), idesc,
-                        (kt > 0 || j > 0) ? 1u : 0u);
+          const uint64_t dk = uint64_t(2 * j);
+          uint32_t acc = (kt > 0 || j > 0) ? 1u : 0u;
+          if constexpr (SPLIT) {
+            const uint64_t al = make_sw128_desc(ptx::smem_u32(a_lo(stage)));
+            const uint64_t bl = make_sw128_desc(ptx::smem_u32(b_lo(stage)));
+            ptx::mma_tf32(tmem, al + dk, bh + dk, idesc, acc);  // small terms first
+            ptx::mma_tf32(tmem, ah + dk, bl + dk, idesc, 1u);
+            acc = 1u;
+          }
+          ptx::mma_tf32(tmem, ah + dk, bh + dk, idesc, acc);
         }
         ptx::mma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -210,8 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int kt = 0; kt < nkt; ++kt) {
       ptx::mbar_wait(&empty[stage], phase ^ 1);
       const int kc = (kt_begin + kt) * BK;
-      if constexpr (!kTmaA) gather_slab<BM>(va, ptx::smem_u32(sA + stage * A_BYTES), m0, kc, t);
-      if constexpr (!kTmaB) gather_slab<BN>(vb, ptx::smem_u32(sB + stage * B_BYTES), n0, kc, t);
+      if constexpr (!kTmaA)
+        gather_slab<BM, SPLIT>(va, ptx::smem_u32(a_hi(stage)), ptx::smem_u32(a_lo(stage)), m0, kc, t);
+      if constexpr (!kTmaB)
+        gather_slab<BN, SPLIT>(vb, ptx::smem_u32(b_hi(stage)), ptx::smem_u32(b_lo(stage)), n0, kc, t);
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&full[stage]);

@@ -114,6 +114,7 @@ struct cdnn_context {
   uint64_t next_id = 1;
   std::unordered_map<uint64_t, cdnn::Slot> slots;
   std::atomic<uint64_t> launches{0};
+  int math_mode = CDNN_MATH_TF32X3;  // float GEMM numerics (cdnn_math_mode)
   std::mutex tmap_mu;
   std::unordered_map<std::string, CUtensorMap> tmaps;
 };

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstring>
+#include <type_traits>
 
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
@@ -47,13 +48,12 @@ inline int grid_for(int64_t n, int threads) {
   return int(std::min<int64_t>(b, int64_t(kNumSMs) * 32));
 }
 
-template <int BN, class VA, class VB, class EPI>
+template <int BN, bool SPLIT, class VA, class VB, class EPI>
 void launch_tc_kernel(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& ta,
                       const CUtensorMap& tb, const VA& va, const VB& vb, const EPI& epi, int M,
                       int N, int K, int kt_per_split) {
-  constexpr int ST = 4;
-  constexpr int smem = tc::smem_bytes<BN, ST>();
-  auto kern = tc::tc_gemm_kernel<BN, ST, VA, VB, EPI>;
+  constexpr int smem = tc::smem_bytes<BN, SPLIT>();
+  auto kern = tc::tc_gemm_kernel<BN, SPLIT, VA, VB, EPI>;
   static bool attr_set[16] = {};
   if (!attr_set[c->device & 15]) {
     CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -64,7 +64,7 @@ void launch_tc_kernel(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& ta,
   count_launch(c);
 }
 
-template <int BN, class VA, class VB, class EPI>
+template <int BN, bool SPLIT, class VA, class VB, class EPI>
 void run_tc_bn(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
                const VA& va, const VB& vb, const EPI& epi, const TmaReq& ra, const TmaReq& rb) {
   CUtensorMap ta, tb;
@@ -74,31 +74,45 @@ void run_tc_bn(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M
   if (tc::is_tma<VB>::value) tb = *tmap_k_major(c, rb.p, rb.rows, rb.K, rb.ld, BN);
   dim3 grid((M + tc::BM - 1) / tc::BM, (N + BN - 1) / BN, pl.splits);
   if (pl.splits == 1) {
-    launch_tc_kernel<BN>(c, st, grid, ta, tb, va, vb, epi, M, N, K, pl.kt_per_split);
+    launch_tc_kernel<BN, SPLIT>(c, st, grid, ta, tb, va, vb, epi, M, N, K, pl.kt_per_split);
   } else {
     float* wsp = static_cast<float*>(ws.get(size_t(pl.splits) * M * N * sizeof(float), c->device));
     PartialEpi<float> pe{wsp, M, N};
-    launch_tc_kernel<BN>(c, st, grid, ta, tb, va, vb, pe, M, N, K, pl.kt_per_split);
+    launch_tc_kernel<BN, SPLIT>(c, st, grid, ta, tb, va, vb, pe, M, N, K, pl.kt_per_split);
     reduce_splits_kernel<float, EPI><<<grid_for(int64_t(M) * N, 256), 256, 0, st>>>(wsp, M, N, pl.splits, epi);
     check_launch("reduce_splits_kernel");
     count_launch(c);
   }
 }
 
+// Picks the tile width and the numerics mode: 3xTF32 (context default) or
+// plain TF32; TMA operands exist only in plain TF32 mode.
 template <class VA, class VB, class EPI>
 void run_tc(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
             const VA& va, const VB& vb, const EPI& epi, const TmaReq& ra = {}, const TmaReq& rb = {}) {
-  switch (pl.bn) {
-    case 32: run_tc_bn<32>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
-    case 64: run_tc_bn<64>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
-    default: run_tc_bn<128>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
+  constexpr bool any_tma = tc::is_tma<VA>::value || tc::is_tma<VB>::value;
+  auto go = [&](auto split_tag) {
+    constexpr bool S = decltype(split_tag)::value;
+    switch (pl.bn) {
+      case 32: run_tc_bn<32, S>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
+      case 64: run_tc_bn<64, S>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
+      default: run_tc_bn<128, S>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
+    }
+  };
+  if constexpr (any_tma) {
+    go(std::false_type{});
+  } else {
+    if (c->math_mode == CDNN_MATH_TF32X3) go(std::true_type{});
+    else go(std::false_type{});
   }
 }
 
-// Dense fp32 operand -> TMA when it is K-contiguous and aligned, gather otherwise.
+// Dense fp32 operand -> TMA when it is K-contiguous and aligned and the
+// context runs plain TF32; the gather producers otherwise.
 template <class F>
-void with_operand(const DenseView<float>& v, int box_rows, TmaReq& req, F&& f) {
-  if (!v.mcontig && v.sk == 1 && tma_eligible(v.p, v.rows, v.K, v.sr, box_rows)) {
+void with_operand(Ctx* c, const DenseView<float>& v, int box_rows, TmaReq& req, F&& f) {
+  if (c->math_mode == CDNN_MATH_TF32 && !v.mcontig && v.sk == 1 &&
+      tma_eligible(v.p, v.rows, v.K, v.sr, box_rows)) {
     req = TmaReq{v.p, v.rows, v.K, v.sr};
     f(TmaView{});
   } else {

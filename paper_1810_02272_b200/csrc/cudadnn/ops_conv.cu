@@ -50,7 +50,7 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
     if constexpr (std::is_same_v<T, float>) {
       const GemmPlan pl = plan_tc(M, N, K);
       TmaReq rb;
-      with_operand(vb, pl.bn, rb, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, va, b, epi, TmaReq{}, rb); });
+      with_operand(c, vb, pl.bn, rb, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, va, b, epi, TmaReq{}, rb); });
     } else {
       run_simt<T>(c, st, ws, plan_simt(M, N, K), M, N, K, va, vb, epi);
     }

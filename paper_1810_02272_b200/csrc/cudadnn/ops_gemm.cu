@@ -50,8 +50,8 @@ static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const De
   if constexpr (std::is_same_v<T, float>) {
     const GemmPlan pl = plan_tc(M, N, K);
     TmaReq ra, rb;
-    with_operand(va, tc::BM, ra, [&](const auto& a) {
-      with_operand(vb, pl.bn, rb, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra, rb); });
+    with_operand(c, va, tc::BM, ra, [&](const auto& a) {
+      with_operand(c, vb, pl.bn, rb, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra, rb); });
     });
   } else {
     const GemmPlan pl = plan_simt(M, N, K);

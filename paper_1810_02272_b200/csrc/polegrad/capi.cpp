@@ -212,7 +212,8 @@ int pg_step_capture(pg_net* n, pg_solver* s, const void* data, const void* label
     reg.synchronize();
     cdnn_ok(cdnn_graph_begin(reg.context(), reg.stream()), "step capture");
     try {
-      net.set_batch(static_cast<const real*>(data), static_cast<const real*>(labels));
+      if (data) net.set_batch(static_cast<const real*>(data), static_cast<const real*>(labels));
+      else net.reuse_resident_batch();  // inputs already in HBM
       if (!net.graph_safe()) throw polegrad::InvalidState("step capture: net has host-side layers (loss hooks / FIFO feed)");
       net.forward();
       net.backward();
@@ -232,6 +233,16 @@ int pg_step_capture(pg_net* n, pg_solver* s, const void* data, const void* label
     cdnn_handle g = 0;
     cdnn_ok(cdnn_graph_end(reg.context(), reg.stream(), &g), "step capture");
     *graph = g;
+  });
+}
+
+int pg_net_profile(pg_net* n, float* fwd_ms, float* bwd_ms, int cap) {
+  return run([&] {
+    std::vector<float> f, b;
+    net_of(n).profile_layers(f, b);
+    if (cap < int(f.size())) throw polegrad::InvalidArgument("profile: buffer too small");
+    std::copy(f.begin(), f.end(), fwd_ms);
+    std::copy(b.begin(), b.end(), bwd_ms);
   });
 }
 

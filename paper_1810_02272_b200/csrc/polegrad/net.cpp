@@ -266,6 +266,41 @@ void Net::set_batch(const real* data, const real* labels) {
   throw ModelError("set_batch: net has no MemoryData layer");
 }
 
+void Net::reuse_resident_batch() {
+  for (std::size_t i = 0; i < layers_.size(); ++i) {
+    if (auto* md = dynamic_cast<MemoryDataLayer*>(layers_[i].get())) {
+      for (Blob* t : tops_[i]) t->gpu_data();  // make sure the resident copy is current
+      md->mark_staged();
+      return;
+    }
+  }
+  throw ModelError("reuse_resident_batch: net has no MemoryData layer");
+}
+
+void Net::profile_layers(std::vector<float>& fwd_ms, std::vector<float>& bwd_ms) {
+  cdnn_ctx ctx = registry_->context();
+  const cdnn_handle st = registry_->stream();
+  const std::size_t n = layers_.size();
+  std::vector<cdnn_handle> ev(2 * n + 2, 0);
+  for (auto& e : ev) cdnn_ok(cdnn_event_create(ctx, &e), "profile");
+  cdnn_ok(cdnn_event_record(ctx, ev[0], st), "profile");
+  for (std::size_t i = 0; i < n; ++i) {
+    layers_[i]->forward(bottoms_[i], tops_[i]);
+    cdnn_ok(cdnn_event_record(ctx, ev[i + 1], st), "profile");
+  }
+  for (std::size_t k = 0; k < n; ++k) {
+    const std::size_t i = n - 1 - k;
+    layers_[i]->backward(tops_[i], bottoms_[i]);
+    cdnn_ok(cdnn_event_record(ctx, ev[n + 1 + k], st), "profile");
+  }
+  fwd_ms.assign(n, 0.f);
+  bwd_ms.assign(n, 0.f);
+  for (std::size_t i = 0; i < n; ++i) cdnn_ok(cdnn_event_elapsed(ctx, ev[i], ev[i + 1], &fwd_ms[i]), "profile");
+  for (std::size_t k = 0; k < n; ++k)
+    cdnn_ok(cdnn_event_elapsed(ctx, ev[n + k], ev[n + 1 + k], &bwd_ms[n - 1 - k]), "profile");
+  for (auto e : ev) cdnn_event_free(ctx, e);
+}
+
 void Net::set_loss_scale(double s) {
   for (auto& l : layers_)
     if (auto* sl = dynamic_cast<SoftmaxWithLossLayer*>(l.get())) sl->set_loss_scale(s);

@@ -24,6 +24,7 @@ STATUS = {
     8: "INVALID_STATE", 9: "PARSE_ERROR", 10: "LOAD_ERROR", 11: "CUDA_ERROR", 12: "NO_DEVICE",
 }
 F32, F64, I32 = 0, 1, 2
+MATH_TF32, MATH_TF32X3 = 0, 1
 POOL_MAX, POOL_AVE = 0, 1
 SOLVER_SGD, SOLVER_RMSPROP = 0, 1
 _NP = {F32: np.float32, F64: np.float64, I32: np.int32}
@@ -31,7 +32,8 @@ _NP = {F32: np.float32, F64: np.float64, I32: np.int32}
 # every symbol include/cudadnn.h declares (checked by the CPU test suite)
 EXPORTS = [
     "cdnn_last_error", "cdnn_status_name", "cdnn_device_count", "cdnn_ctx_create", "cdnn_ctx_destroy",
-    "cdnn_ctx_device", "cdnn_live_slots", "cdnn_launch_count", "cdnn_alloc", "cdnn_free", "cdnn_view",
+    "cdnn_ctx_device", "cdnn_live_slots", "cdnn_launch_count", "cdnn_set_math_mode", "cdnn_get_math_mode",
+    "cdnn_alloc", "cdnn_free", "cdnn_view",
     "cdnn_length", "cdnn_buffer_dtype", "cdnn_device_ptr", "cdnn_write", "cdnn_read", "cdnn_write_async",
     "cdnn_read_async", "cdnn_host_alloc_pinned", "cdnn_host_free_pinned", "cdnn_stream_create",
     "cdnn_stream_free", "cdnn_stream_sync", "cdnn_stream_wait", "cdnn_graph_begin", "cdnn_graph_end",
@@ -84,6 +86,7 @@ def load() -> C.CDLL:
             "cdnn_device_count": ([C.POINTER(i)], i), "cdnn_ctx_create": ([i, C.POINTER(vp)], i),
             "cdnn_ctx_destroy": ([vp], i), "cdnn_ctx_device": ([vp, C.POINTER(i)], i),
             "cdnn_live_slots": ([vp, pu64], i), "cdnn_launch_count": ([vp, pu64], i),
+            "cdnn_set_math_mode": ([vp, i], i), "cdnn_get_math_mode": ([vp, C.POINTER(i)], i),
             "cdnn_alloc": ([vp, u64, i, ph], i), "cdnn_free": ([vp, h], i),
             "cdnn_view": ([vp, h, u64, u64, ph], i), "cdnn_length": ([vp, h, pu64], i),
             "cdnn_buffer_dtype": ([vp, h, C.POINTER(i)], i), "cdnn_device_ptr": ([vp, h, C.POINTER(vp)], i),

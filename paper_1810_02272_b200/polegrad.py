@@ -30,6 +30,7 @@ EXPORTS = [
     "pg_net_num_layers", "pg_net_layer_name", "pg_blob_shape", "pg_blob_get", "pg_blob_set", "pg_param_count",
     "pg_param_info", "pg_param_get", "pg_param_set", "pg_pool_mask", "pg_snapshot", "pg_restore",
     "pg_solver_create", "pg_solver_free", "pg_solver_apply", "pg_step_capture", "pg_step_replay", "pg_graph_free",
+    "pg_net_profile",
     "pg_parallel_unique_id", "pg_parallel_create", "pg_parallel_free", "pg_parallel_broadcast",
     "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip",
 ]
@@ -66,6 +67,7 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_solver_apply": ([vp, vp], i),
             "pg_step_capture": ([vp, vp, vp, vp, vp, C.POINTER(u64)], i), "pg_step_replay": ([vp, u64], i),
             "pg_graph_free": ([vp, u64], i), "pg_parallel_unique_id": ([cp], i),
+            "pg_net_profile": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
             "pg_parallel_create": ([vp, i, i, cp, u64, C.POINTER(vp)], i), "pg_parallel_free": ([vp], i),
             "pg_parallel_broadcast": ([vp], i), "pg_solver_set_parallel": ([vp, vp], i),
             "pg_plan_buckets": ([C.POINTER(u64), C.POINTER(u64), i, u64, u64, C.POINTER(C.c_int32),

@@ -24,11 +24,38 @@ TOL = {cd.F32: 2e-3, cd.F64: 1e-12}
 NP = {cd.F32: np.float32, cd.F64: np.float64}
 
 
+@pytest.fixture(params=["tf32x3", "tf32"])
+def math(request, ctx):
+    """Both float numerics modes; 3xTF32 (the default) must also reach ~fp32 accuracy."""
+    mode = cd.MATH_TF32X3 if request.param == "tf32x3" else cd.MATH_TF32
+    ctx.call("cdnn_set_math_mode", mode)
+    yield request.param
+    ctx.call("cdnn_set_math_mode", cd.MATH_TF32X3)
+
+
+def test_tf32x3_reaches_fp32_accuracy(ctx):
+    rng = np.random.default_rng(11)
+    m, n, k = 256, 192, 2048
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    errs = {}
+    for name, mode in (("tf32x3", cd.MATH_TF32X3), ("tf32", cd.MATH_TF32)):
+        ctx.call("cdnn_set_math_mode", mode)
+        ha, hb, hc = ctx.upload(A), ctx.upload(B), ctx.alloc(m * n, cd.F32)
+        ctx.call("cdnn_gemm", 0, 0, m, n, k, 1.0, ha, hb, 0.0, hc, 0)
+        errs[name] = rel_l2(ctx.read(hc), want)
+    ctx.call("cdnn_set_math_mode", cd.MATH_TF32X3)
+    assert errs["tf32x3"] < 2e-6, errs      # fp32-level
+    assert errs["tf32"] < 2e-3, errs        # plain tf32
+    assert errs["tf32x3"] < errs["tf32"] / 50, errs
+
+
 @pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("m,n,k", [(2, 1, 2), (64, 500, 800), (100, 64, 1024), (37, 19, 300), (256, 128, 96),
                                    (1024, 2, 10), (300, 260, 4100)])
-def test_gemm(ctx, dtype, ta, tb, m, n, k):
+def test_gemm(ctx, math, dtype, ta, tb, m, n, k):
     rng = np.random.default_rng(m * 7 + n * 3 + k)
     A = rng.uniform(-1, 1, (k, m) if ta else (m, k))
     B = rng.uniform(-1, 1, (n, k) if tb else (k, n))
@@ -76,7 +103,7 @@ CONV_CASES = [
 
 @pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv(ctx, dtype, case):
+def test_conv(ctx, math, dtype, case):
     n, c, h, w, co, k, s, p, dl, g = case
     rng = np.random.default_rng(sum(case))
     x = rng.uniform(-1, 1, (n, c, h, w))
