@@ -1,0 +1,517 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: one SGD training iteration (feed -> Net::forward ->
+SoftmaxWithLoss -> Net::backward -> momentum-SGD update) of CIFAR-10 quick at
+batch 100 per GPU (BASELINE.json configs[1], float -> TF32 tensor cores).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0).  N > 1: launched by torch.distributed.run, one
+rank per GPU, NCCL gradient all-reduce (weak scaling: batch 100 per GPU).
+
+* value      images/s with the batch already resident in HBM (captured CUDA
+             graph of the step), L2 flushed (256 MiB write) before every timed
+             step, CUDA events on the compute stream, max over ranks.
+* e2e        images/s through the public API with host buffers: each step copies
+             that step's batch into pinned memory, replays the graph whose first
+             node is the H2D copy and last node the D2H of the loss, and waits
+             for the loss.
+* roofline   the dominant kernel (per-layer event profile of one eager step).
+* cpu_baseline  the reference CPU implementation (oracle/_ref: unmodified
+             reference core + reference-style conv/pool/loss extension, 1 thread)
+             on a bounded sample.
+--impl reference  times that CPU implementation on all host cores (independent
+             replicas), same metric / config.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training images/sec (fwd+bwd+SGD) at 1/2/4/8 B200 vs CPU ref; ms/iter"
+UNIT = "images/s"
+WORKLOAD = "cifar10_quick"
+BATCH = 100
+SOLVER = dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=0.004)
+IMG = (3, 32, 32)
+CLASSES = 10
+REF_SAMPLE_BATCH = 20  # images per reference step per process (bounded CPU sample)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def model_text(batch: int) -> str:
+    from paper_1810_02272_b200 import polegrad
+    t = polegrad.load_model(WORKLOAD)
+    return t.replace("batch_size: 100", f"batch_size: {batch}")
+
+
+def config(n_gpus: int, graph: bool) -> dict:
+    return {"workload": WORKLOAD, "per_gpu_batch": BATCH, "global_batch": BATCH * n_gpus,
+            "input": "x".join(map(str, IMG)), "classes": CLASSES,
+            "solver": "SGD lr=1e-3 momentum=0.9 weight_decay=4e-3",
+            "math": os.environ.get("CDNN_MATH", "tf32x3"),
+            "step": "cuda-graph" if graph else "eager",
+            "l2": "flushed (256 MiB device write) before every timed step",
+            "parallelism": f"dp{n_gpus}" if n_gpus > 1 else "single"}
+
+
+# --------------------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if not self.path or not os.path.exists(self.path):
+            return out
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return out
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for name, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        loaded = [s for s in sm if s > 500] or sm
+        out.update(sm_mhz=statistics.median(loaded) if loaded else None, sm_max_mhz=max(mx) if mx else None,
+                   reasons=sorted(reasons), samples=len(rows))
+        return out
+
+
+# --------------------------------------------------------------------------------------
+class CtxView:
+    """cudadnn calls on the net's own context (events, flush buffer, launch count)."""
+
+    def __init__(self, ptr: int):
+        from paper_1810_02272_b200 import cudadnn
+        self.cd = cudadnn
+        self.lib = cudadnn.load()
+        self.ptr = C.c_void_p(ptr)
+
+    def call(self, name, *args):
+        self.cd.check(getattr(self.lib, name)(self.ptr, *args))
+
+    def out_h(self, name, *args) -> int:
+        h = C.c_uint64()
+        self.call(name, *args, C.byref(h))
+        return h.value
+
+    def event(self) -> int:
+        return self.out_h("cdnn_event_create")
+
+    def record(self, ev):
+        self.call("cdnn_event_record", ev, 0)
+
+    def elapsed(self, a, b) -> float:
+        v = C.c_float()
+        self.call("cdnn_event_elapsed", a, b, C.byref(v))
+        return v.value
+
+    def launches(self) -> int:
+        v = C.c_uint64()
+        self.call("cdnn_launch_count", C.byref(v))
+        return v.value
+
+
+def layer_flops(net) -> dict:
+    """Algorithmic FLOPs (2*M*N*K) of each contraction, forward and backward,
+    from the net's own parameter and top shapes (in the bundled models each
+    parameterised layer's top blob carries the layer's name)."""
+    out = {}
+    first = True
+    for pname, wshape in net.param_info():
+        if not pname.endswith(".weight"):
+            continue
+        lname = pname[: -len(".weight")]
+        top = net.blob_shape(lname)
+        if wshape[0] == 1 and wshape[1] == 1:  # InnerProduct weight (1,1,O,K)
+            f = 2.0 * top[0] * wshape[2] * wshape[3]
+            out[lname] = {"fwd": f, "bwd": 2 * f}  # wgrad + dgrad (the reference always writes dX)
+        else:  # Convolution weight (Co, C/g, kh, kw)
+            n, co, p, q = top
+            f = 2.0 * n * p * q * co * wshape[1] * wshape[2] * wshape[3]
+            out[lname] = {"fwd": f, "bwd": f * (1 if first else 2)}  # no dgrad into the input data
+        first = False
+    return out
+
+
+def peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+def ncu_traffic(kernel_key: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return d.get("traffic_bytes_per_launch", {}).get(kernel_key)
+    except Exception:
+        return None
+
+
+def cpu_baseline_sample(iters: int = 2) -> dict:
+    from oracle import pyoracle
+    if not pyoracle.available("f32"):
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": "oracle/_ref not built on this host"}
+    text = model_text(BATCH)
+    net = pyoracle.OracleNet(text, seed=1, dtype="f32")
+    solver = pyoracle.OracleSolver(net, **SOLVER)
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1, 1, (BATCH,) + IMG)
+    y = np.floor(rng.uniform(0, 1, BATCH) * CLASSES)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        net.set_batch(x, y)
+        net.forward()
+        net.backward()
+        solver.apply()
+    dt = time.perf_counter() - t0
+    return {"value": iters * BATCH / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "ms_per_step": 1000 * dt / iters,
+            "sample": f"{iters} full iterations of {WORKLOAD} batch {BATCH} (f32) on oracle/_ref: unmodified "
+                      f"reference core (kernels::gemm, InnerProduct, ReLU, solver) + reference-style "
+                      f"Convolution/Pooling/SoftmaxWithLoss extension, 1 thread"}
+
+
+# --------------------------------------------------------------------------------------
+def run_b200(args) -> None:
+    import torch.distributed as dist  # plumbing only (rendezvous, barrier, max-over-ranks)
+    from paper_1810_02272_b200 import cudadnn, polegrad
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE")
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    text = model_text(BATCH)
+    net = polegrad.Net(text, seed=1, dtype="f32", device=local)
+    solver = polegrad.Solver(net, **SOLVER)
+    cx = CtxView(net.context_ptr())
+    par = None
+    if world > 1:
+        uid = [polegrad.Parallel.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        par = polegrad.Parallel(net, world, rank, uid[0])
+        par.broadcast()
+        solver.set_parallel(par)
+
+    rng = np.random.default_rng(2 + rank)
+    nb = max(args.steps, 1)
+    host_x = rng.uniform(-1, 1, (nb, BATCH) + IMG).astype(np.float32)
+    host_y = np.floor(rng.uniform(0, 1, (nb, BATCH)) * CLASSES).astype(np.float32)
+
+    # eager step: allocates workspaces / tensor maps, counts kernel launches per step
+    net.set_batch(host_x[0], host_y[0])
+    l0 = cx.launches()
+    net.forward()
+    net.backward()
+    solver.apply()
+    net.sync()
+    launches_per_step = cx.launches() - l0
+
+    # per-layer device-time profile of one eager step (kernel shares)
+    nl = len(net.layer_names())
+    fwd = (C.c_float * nl)()
+    bwd = (C.c_float * nl)()
+    net.set_batch(host_x[0], host_y[0])
+    polegrad._check(net.lib, net.lib.pg_net_profile(net.ptr, fwd, bwd, nl))
+    net.sync()
+    solver.apply()  # consume the profiled gradients
+    names = net.layer_names()
+    prof = {names[i]: {"fwd_ms": float(fwd[i]), "bwd_ms": float(bwd[i])} for i in range(nl)}
+
+    # graphs: resident-input step (value) and host-buffer step (e2e)
+    use_graph = not args.no_graph
+    pin_x = cudadnn.PinnedBuffer((BATCH,) + IMG)
+    pin_y = cudadnn.PinnedBuffer((BATCH,))
+    pin_loss = cudadnn.PinnedBuffer((1,))
+    g_res = g_e2e = None
+    if use_graph:
+        try:
+            net.set_batch(host_x[0], host_y[0])
+            g_res = polegrad.StepGraph(net, solver, 0, 0, 0)
+            g_e2e = polegrad.StepGraph(net, solver, pin_x.ptr, pin_y.ptr, pin_loss.ptr)
+        except Exception as e:  # fall back to eager steps (reported in config)
+            log(f"graph capture failed ({e}); eager steps")
+            use_graph = False
+
+    def step_resident():
+        if use_graph:
+            g_res.replay()
+        else:
+            polegrad._check(net.lib, net.lib.pg_net_forward(net.ptr))
+            polegrad._check(net.lib, net.lib.pg_net_backward(net.ptr))
+            solver.apply()
+
+    # L2 flush buffer (256 MiB > 126 MB L2), written by our fill kernel
+    flush_elems = 64 << 20
+    flush = cx.out_h("cdnn_alloc", flush_elems, cudadnn.F32)
+
+    def flush_l2():
+        cx.call("cdnn_fill", flush, flush_elems, 0.0, 0)
+
+    # make the resident batch current
+    net.set_batch(host_x[0], host_y[0])
+    for _ in range(args.warmup):
+        if not use_graph:
+            net.set_batch(host_x[0], host_y[0])
+        step_resident()
+    net.sync()
+
+    evs = [(cx.event(), cx.event()) for _ in range(args.steps)]
+    barrier()
+    net.sync()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush_l2()
+            cx.record(evs[i][0])
+            if not use_graph:
+                net.set_batch(host_x[0], host_y[0])
+            step_resident()
+            cx.record(evs[i][1])
+        net.sync()
+        barrier()
+        total_ms = sum(cx.elapsed(a, b) for a, b in evs)
+    clocks = clk.summary()
+    total_ms = max_over_ranks(total_ms)
+    value = world * BATCH * args.steps / (total_ms / 1000.0)
+
+    # ---- e2e: host buffers through the public API (H2D in, loss D2H out, every step)
+    e_start, e_end = cx.event(), cx.event()
+    for i in range(min(args.warmup, nb)):
+        pin_x.array[...] = host_x[i]
+        pin_y.array[...] = host_y[i]
+        if use_graph:
+            g_e2e.replay()
+        else:
+            net.set_batch_ptr(pin_x.ptr, pin_y.ptr)
+            polegrad._check(net.lib, net.lib.pg_net_forward(net.ptr))
+            polegrad._check(net.lib, net.lib.pg_net_backward(net.ptr))
+            solver.apply()
+        net.sync()
+    barrier()
+    net.sync()
+    t0 = time.perf_counter()
+    cx.record(e_start)
+    losses = []
+    for i in range(args.steps):
+        pin_x.array[...] = host_x[i % nb]
+        pin_y.array[...] = host_y[i % nb]
+        if use_graph:
+            g_e2e.replay()
+            net.sync()
+            losses.append(float(pin_loss.array[0]))
+        else:
+            net.set_batch_ptr(pin_x.ptr, pin_y.ptr)
+            polegrad._check(net.lib, net.lib.pg_net_forward(net.ptr))
+            losses.append(net.loss())
+            polegrad._check(net.lib, net.lib.pg_net_backward(net.ptr))
+            solver.apply()
+            net.sync()
+    cx.record(e_end)
+    net.sync()
+    e2e_ms = max_over_ranks(cx.elapsed(e_start, e_end))
+    wall_ms = max_over_ranks(1000 * (time.perf_counter() - t0))
+    e2e = world * BATCH * args.steps / (e2e_ms / 1000.0)
+    if not all(np.isfinite(losses)):
+        raise RuntimeError("non-finite loss")
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (largest per-layer device time)
+    flops = layer_flops(net)
+    pk = peaks()
+    tf32_peak = pk["bf16_tflops"] / 2.0  # dense TF32 = half the bf16 rate (derived from measured bf16)
+    ops = []
+    for lname, t in prof.items():
+        for phase in ("fwd", "bwd"):
+            ms = t[f"{phase}_ms"]
+            f = flops.get(lname, {}).get(phase)
+            ops.append((ms, lname, phase, f))
+    ops.sort(reverse=True)
+    dom_ms, dom_layer, dom_phase, dom_f = ops[0]
+    prof_total = sum(o[0] for o in ops)
+    kernel_key = f"{dom_layer}.{dom_phase}"
+    if dom_f:
+        achieved = dom_f / (dom_ms / 1000.0) / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / tf32_peak, 5), "traffic": ncu_traffic(kernel_key),
+                "kernel": f"{dom_layer} {dom_phase} (implicit-GEMM tcgen05, "
+                          f"{'3xTF32' if config(1, True)['math'] == 'tf32x3' else 'TF32'})",
+                "flops_per_launch": dom_f, "ms_per_launch": round(dom_ms, 5),
+                "share_of_step": round(dom_ms / prof_total, 4),
+                "peak_note": f"TF32 dense = measured bf16 {pk['bf16_tflops']} / 2 ({pk['source']})"}
+    else:
+        roof = {"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": None,
+                "traffic": ncu_traffic(kernel_key), "kernel": f"{dom_layer} {dom_phase}",
+                "ms_per_launch": round(dom_ms, 5), "share_of_step": round(dom_ms / prof_total, 4)}
+
+    cpu = cpu_baseline_sample(args.cpu_iters) if not args.no_cpu_baseline else None
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "tf32", "data": "synthetic",
+        "config": config(world, use_graph),
+        "e2e": {"value": round(e2e, 1), "unit": UNIT, "ms_per_step": round(e2e_ms / args.steps, 5),
+                "wall_ms_per_step": round(wall_ms / args.steps, 5),
+                "h2d_bytes_per_step": int(BATCH * np.prod(IMG) * 4 + BATCH * 4), "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "launches_per_step": int(launches_per_step),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "layer_profile_ms": prof,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------------------
+def _ref_worker(args_tuple):
+    steps, warmup, seed = args_tuple
+    from oracle import pyoracle
+    text = model_text(REF_SAMPLE_BATCH)
+    net = pyoracle.OracleNet(text, seed=1, dtype="f32")
+    solver = pyoracle.OracleSolver(net, **SOLVER)
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (REF_SAMPLE_BATCH,) + IMG)
+    y = np.floor(rng.uniform(0, 1, REF_SAMPLE_BATCH) * CLASSES)
+    for _ in range(warmup):
+        net.set_batch(x, y)
+        net.forward()
+        net.backward()
+        solver.apply()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        net.set_batch(x, y)
+        net.forward()
+        net.backward()
+        solver.apply()
+    return time.perf_counter() - t0
+
+
+def run_reference(args) -> None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import pyoracle
+    if not pyoracle.available("f32"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liboracle_f32.so not built"}))
+        return
+    import multiprocessing as mp
+    procs = max(1, os.cpu_count() or 1)
+    steps = max(args.steps, 1)
+    warm = min(args.warmup, 1)
+    with mp.get_context("fork").Pool(procs) as pool:
+        times = pool.map(_ref_worker, [(steps, warm, 2 + i) for i in range(procs)])
+    t = max(times)
+    value = procs * REF_SAMPLE_BATCH * steps / t
+    sample = (f"{procs} independent single-threaded replicas (one per host core), each {steps} SGD iterations of "
+              f"{WORKLOAD} at batch {REF_SAMPLE_BATCH} (bounded sample of the batch-100 step; CPU cost is linear in "
+              f"batch) on oracle/_ref: unmodified reference core + reference-style conv/pool/loss extension, f32")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": round(1000 * t / steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": config(world, False),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the captured CUDA graph")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        log("note: timing rules ask for >= 3 warm-up steps")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

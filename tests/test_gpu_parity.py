@@ -20,15 +20,36 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick"])
 def test_ten_iterations_match_oracle(config, dtype):
+    """Free-running 10 iterations: losses every iteration and the weights after
+    10 updates within tolerance (gradients too in FP64, where no near-tie flips)."""
     r = lockstep(config, dtype, iters=10)
     assert r["init_bitexact"], "seeded initial weights must be identical"
     tol = TOL[dtype]
     for it, h in enumerate(r["hist"]):
         assert abs(h["loss"] - h["oracle_loss"]) <= tol * max(abs(h["oracle_loss"]), 1e-12), (it, h)
-        for (name, _), e in zip(r["params"], h["grad_rel"]):
-            assert e <= tol, (it, name, e)
+        if dtype == "f64":
+            for (name, _), e in zip(r["params"], h["grad_rel"]):
+                assert e <= tol, (it, name, e)
     for (name, _), e in zip(r["params"], r["weights_rel"]):
         assert e <= tol, (name, e)
+    print(config, dtype, "max grad rel", max(max(h["grad_rel"]) for h in r["hist"]),
+          "max weight rel", max(r["weights_rel"]))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick"])
+def test_ten_iterations_gradients_on_synced_weights(config, dtype):
+    """Every iteration's gradients on identical inputs and weights (oracle
+    weights restored into the B200 net via MCWT before each step)."""
+    r = lockstep(config, dtype, iters=10, resync_weights=True)
+    tol = TOL[dtype]
+    worst = 0.0
+    for it, h in enumerate(r["hist"]):
+        assert abs(h["loss"] - h["oracle_loss"]) <= tol * max(abs(h["oracle_loss"]), 1e-12), (it, h)
+        for (name, _), e in zip(r["params"], h["grad_rel"]):
+            worst = max(worst, e)
+            assert e <= tol, (it, name, e)
+    print(config, dtype, "max grad rel (synced)", worst)
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
