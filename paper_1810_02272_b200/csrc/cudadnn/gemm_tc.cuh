@@ -27,6 +27,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "operands.cuh"
 #include "ptx.cuh"
@@ -76,20 +77,16 @@ __host__ __device__ constexpr uint32_t make_idesc_tf32(int bn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
-// Four consecutive-k elements of one row.  Views that are K-contiguous and
-// 16-byte aligned at this point load them with one 128-bit access.
-template <class V, class R>
-__device__ __forceinline__ float4 load4(const V& v, const R& rw, int k) {
-  return make_float4(v.at(rw, k), v.at(rw, k + 1), v.at(rw, k + 2), v.at(rw, k + 3));
-}
-template <class R>
-__device__ __forceinline__ float4 load4(const DenseView<float>& v, const R& rw, int k) {
-  if (rw.ok && v.sk == 1 && k + 3 < v.K) {
-    const float* p = v.p + rw.off + k;
-    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) return __ldg(reinterpret_cast<const float4*>(p));
-  }
-  return make_float4(v.at(rw, k), v.at(rw, k + 1), v.at(rw, k + 2), v.at(rw, k + 3));
-}
+template <class V>
+struct is_dense_f32 { static constexpr bool value = false; };
+template <>
+struct is_dense_f32<DenseView<float>> { static constexpr bool value = true; };
+
+// Views with a constant all-ones row (see ConvWgradA) substitute 1.0 for loads.
+template <class V, class = void>
+struct has_ones { static constexpr bool value = false; };
+template <class V>
+struct has_ones<V, std::void_t<decltype(V::kHasOnes)>> { static constexpr bool value = V::kHasOnes; };
 
 template <bool SPLIT>
 __device__ __forceinline__ void store4(uint32_t hi_tile, uint32_t lo_tile, uint32_t off, float4 x) {
@@ -102,36 +99,87 @@ __device__ __forceinline__ void store4(uint32_t hi_tile, uint32_t lo_tile, uint3
 }
 
 // Fill one ROWS x 32 slab of operand view `v` into swizzled smem (hi, and lo
-// when SPLIT).  Thread t of the 128 producers.  Row-contiguous views: each
-// thread owns rows and walks k (lanes = consecutive rows -> coalesced loads);
-// otherwise 8 threads share a row, each taking 4 consecutive k.
+// when SPLIT).  Thread t of the 128 producers.  All addresses of the thread's
+// elements are formed first and every load is issued before any is consumed,
+// so each thread keeps up to 32 independent loads in flight.
+//  * row-contiguous views: a thread owns one row and walks k (lanes =
+//    consecutive rows -> coalesced loads; per-k state is warp-uniform);
+//  * otherwise 8 threads share a row, each owning 4 consecutive k (per-k
+//    state computed once per slab) across ROWS/16 rows; dense K-contiguous
+//    rows use one 128-bit load per 4 elements when aligned.
 template <int ROWS, bool SPLIT, class V>
 __device__ __forceinline__ void gather_slab(const V& v, uint32_t hi, uint32_t lo, int row0, int k0, int t) {
-  static_assert((ROWS * 8) % kProducerThreads == 0, "slab rows must be a multiple of 16");
+  static_assert((ROWS * 8) % kProducerThreads == 0 && ROWS <= kProducerThreads,
+                "slab rows must be a multiple of 16 and at most 128");
+  const float* base = v.base();
   if (v.m_contig()) {
-    if constexpr (ROWS <= kProducerThreads) {
-      constexpr int KGROUPS = kProducerThreads / ROWS;  // threads sharing a row (split over k)
-      const int r = t % ROWS;
-      const auto rw = v.row(row0 + r);
+    constexpr int KG = kProducerThreads / ROWS;  // threads sharing a row (split over k)
+    constexpr int NC = 8 / KG;                   // 16-byte chunks per thread
+    constexpr int E = NC * 4;
+    const int r = t % ROWS, kc0 = t / ROWS;
+    const auto rw = v.row(row0 + r);
+    int off[E];
+    bool ok[E];
 #pragma unroll
-      for (int kc = t / ROWS; kc < 8; kc += KGROUPS) store4<SPLIT>(hi, lo, sw128(r, kc), load4(v, rw, k0 + kc * 4));
-    } else {
+    for (int i = 0; i < NC; ++i)
 #pragma unroll
-      for (int rr = 0; rr < ROWS / kProducerThreads; ++rr) {
-        const int r = t + rr * kProducerThreads;
-        const auto rw = v.row(row0 + r);
+      for (int e = 0; e < 4; ++e) ok[i * 4 + e] = v.addr(rw, v.kx(k0 + (kc0 + i * KG) * 4 + e), off[i * 4 + e]);
+    float val[E];
 #pragma unroll
-        for (int kc = 0; kc < 8; ++kc) store4<SPLIT>(hi, lo, sw128(r, kc), load4(v, rw, k0 + kc * 4));
-      }
-    }
+    for (int j = 0; j < E; ++j) val[j] = ok[j] ? __ldg(base + off[j]) : 0.f;
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+      store4<SPLIT>(hi, lo, sw128(r, kc0 + i * KG),
+                    make_float4(val[i * 4], val[i * 4 + 1], val[i * 4 + 2], val[i * 4 + 3]));
   } else {
+    constexpr int NR = ROWS * 8 / kProducerThreads;  // rows per thread
+    const int kc = t & 7, rbase = t >> 3;
+    typename V::Kx kx[4];
 #pragma unroll
-    for (int i = 0; i < ROWS * 8 / kProducerThreads; ++i) {
-      const int c = t + i * kProducerThreads;
-      const int r = c >> 3, kc = c & 7;
-      const auto rw = v.row(row0 + r);
-      store4<SPLIT>(hi, lo, sw128(r, kc), load4(v, rw, k0 + kc * 4));
+    for (int e = 0; e < 4; ++e) kx[e] = v.kx(k0 + kc * 4 + e);
+    float4 val[NR];
+    if constexpr (is_dense_f32<V>::value) {
+      const bool full = kx[3].ok && v.sk == 1;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const auto rw = v.row(row0 + rbase + 16 * i);
+        const float* p = base + rw.off + kx[0].off;
+        if (full && rw.ok && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+          val[i] = __ldg(reinterpret_cast<const float4*>(p));
+        } else {
+          int o[4];
+          bool k[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) k[e] = v.addr(rw, kx[e], o[e]);
+          val[i] = make_float4(k[0] ? __ldg(base + o[0]) : 0.f, k[1] ? __ldg(base + o[1]) : 0.f,
+                               k[2] ? __ldg(base + o[2]) : 0.f, k[3] ? __ldg(base + o[3]) : 0.f);
+        }
+      }
+    } else {
+      int off[NR * 4];
+      bool ok[NR * 4];
+      bool one[NR];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const auto rw = v.row(row0 + rbase + 16 * i);
+        if constexpr (has_ones<V>::value) one[i] = v.is_one(rw);
+        else one[i] = false;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ok[i * 4 + e] = v.addr(rw, kx[e], off[i * 4 + e]);
+      }
+      float f[NR * 4];
+#pragma unroll
+      for (int j = 0; j < NR * 4; ++j) f[j] = ok[j] ? __ldg(base + off[j]) : 0.f;
+      if constexpr (has_ones<V>::value) {
+#pragma unroll
+        for (int j = 0; j < NR * 4; ++j)
+          if (one[j / 4] && kx[j % 4].ok) f[j] = 1.f;
+      }
+#pragma unroll
+      for (int i = 0; i < NR; ++i) val[i] = make_float4(f[i * 4], f[i * 4 + 1], f[i * 4 + 2], f[i * 4 + 3]);
     }
+#pragma unroll
+    for (int i = 0; i < NR; ++i) store4<SPLIT>(hi, lo, sw128(rbase + 16 * i, kc), val[i]);
   }
 }
 

@@ -31,16 +31,38 @@ inline bool tma_eligible(const float* p, int rows, int K, int64_t ld, int box_ro
          rows >= box_rows && ld >= K;
 }
 
+// Split-K reduction: block (32 m) x (8 split groups); group g sums splits
+// z = g, g+8, ... (loads coalesced along m), then the 8 partials are added in
+// fixed order -> deterministic.  grid = (ceil(M/32), N).
 template <typename T, class EPI>
-__global__ void reduce_splits_kernel(const T* __restrict__ ws, int M, int N, int splits, EPI epi) {
-  const int64_t total = int64_t(M) * N;
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int m = int(idx % M), n = int(idx / M);
-    T s = T(0);
-    for (int z = 0; z < splits; ++z) s += ws[(int64_t(z) * N + n) * M + m];
-    epi.store(m, n, s, 0);
+__global__ void __launch_bounds__(256) reduce_splits_kernel(const T* __restrict__ ws, int M, int N, int splits,
+                                                            EPI epi) {
+  __shared__ T part[8][33];
+  const int mi = threadIdx.x & 31, gi = threadIdx.x >> 5;
+  const int m = blockIdx.x * 32 + mi, n = blockIdx.y;
+  T s = T(0);
+  if (m < M) {
+    const T* p = ws + int64_t(n) * M + m;
+    const int64_t zs = int64_t(N) * M;
+#pragma unroll 4
+    for (int z = gi; z < splits; z += 8) s += p[z * zs];
   }
+  part[gi][mi] = s;
+  __syncthreads();
+  if (gi == 0 && m < M) {
+    T t = part[0][mi];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) t += part[g][mi];
+    epi.store(m, n, t, 0);
+  }
+}
+
+template <typename T, class EPI>
+void launch_reduce(Ctx* c, cudaStream_t st, const T* ws, int M, int N, int splits, const EPI& epi) {
+  dim3 grid((M + 31) / 32, N);
+  reduce_splits_kernel<T, EPI><<<grid, 256, 0, st>>>(ws, M, N, splits, epi);
+  check_launch("reduce_splits_kernel");
+  count_launch(c);
 }
 
 inline int grid_for(int64_t n, int threads) {
@@ -79,9 +101,7 @@ void run_tc_bn(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M
     float* wsp = static_cast<float*>(ws.get(size_t(pl.splits) * M * N * sizeof(float), c->device));
     PartialEpi<float> pe{wsp, M, N};
     launch_tc_kernel<BN, SPLIT>(c, st, grid, ta, tb, va, vb, pe, M, N, K, pl.kt_per_split);
-    reduce_splits_kernel<float, EPI><<<grid_for(int64_t(M) * N, 256), 256, 0, st>>>(wsp, M, N, pl.splits, epi);
-    check_launch("reduce_splits_kernel");
-    count_launch(c);
+    launch_reduce<float>(c, st, wsp, M, N, pl.splits, epi);
   }
 }
 
@@ -133,9 +153,8 @@ void run_simt(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M,
     PartialEpi<T> pe{wsp, M, N};
     simt::simt_gemm_kernel<T, VA, VB, PartialEpi<T>><<<grid, simt::kThreads, 0, st>>>(va, vb, pe, M, N, K, pl.kt_per_split);
     check_launch("simt_gemm_kernel");
-    reduce_splits_kernel<T, EPI><<<grid_for(int64_t(M) * N, 256), 256, 0, st>>>(wsp, M, N, pl.splits, epi);
-    check_launch("reduce_splits_kernel");
-    count_launch(c, 2);
+    count_launch(c);
+    launch_reduce<T>(c, st, wsp, M, N, pl.splits, epi);
   }
 }
 

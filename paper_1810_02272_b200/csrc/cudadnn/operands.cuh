@@ -2,21 +2,25 @@
 //
 // Every GEMM-shaped op of the hot path is expressed as
 //     D[m][n] = sum_k A(m, k) * B(n, k)
-// where A and B are *views*: a `row(r)` step that precomputes per-row state
-// once, and an `at(row, k)` fetch that returns the element (0 outside the
-// matrix, so tile tails contribute nothing).  The views below cover the dense
-// row-major matrices of InnerProduct / gemm (any transpose) and the three
-// convolution contractions (forward im2col, backward-data, backward-filter)
-// without materialising im2col buffers.  The epilogues turn the fp32/fp64
-// accumulator of D into the op's output layout.
+// where A and B are *views* that never materialise im2col buffers.  A view
+// factors element addressing into a per-row part and a per-k part so the
+// gather producers can compute all addresses of a slab first and then issue
+// every load independently (memory-level parallelism):
+//     Row row(r)      per-row state  (e.g. output pixel -> image, h0, w0)
+//     Kx  kx(k)       per-k state    (e.g. filter tap -> channel offset, dh, dw)
+//     bool addr(Row, Kx, int& off)   element offset from base(), false = zero
+// Offsets are 32-bit: every tensor on the path is < 2^31 elements (checked by
+// the host).  The epilogues turn the fp32/fp64 accumulator of D into the op's
+// output layout.
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 namespace cdnn {
 
 // Granlund–Montgomery division by an invariant positive divisor < 2^31:
-// q = mulhi(n, magic) >> shift, exact for 0 <= n < 2^31.
+// q = (t + ((n - t) >> 1)) >> (l - 1), t = mulhi(n, magic), exact for n < 2^32.
 struct FastDiv {
   uint32_t d = 1, magic = 0, shift = 0;
   FastDiv() = default;
@@ -35,6 +39,15 @@ struct FastDiv {
   }
 };
 
+// Generic scalar fetch on top of the address API (SIMT engine, tails).
+template <class V, class R>
+__device__ __forceinline__ auto view_at(const V& v, const R& rw, int k) {
+  using E = std::remove_const_t<std::remove_pointer_t<decltype(v.base())>>;
+  int off;
+  const auto kx = v.kx(k);
+  return v.addr(rw, kx, off) ? __ldg(v.base() + off) : E(0);
+}
+
 // ---------------------------------------------------------------------------
 // Dense strided matrix: A(r, k) = p[r*sr + k*sk].  `mcontig` says which index
 // is memory-contiguous; it only picks the thread->element map of the gather
@@ -45,18 +58,29 @@ struct DenseView {
   int64_t sr, sk;
   int rows, K;
   bool mcontig;
-  struct Row { int64_t off; bool ok; };
-  __device__ __forceinline__ Row row(int r) const { return Row{int64_t(r) * sr, r < rows}; }
+  struct Row { int off; bool ok; };
+  struct Kx { int off; bool ok; };
+  __device__ __forceinline__ const T* base() const { return p; }
+  __device__ __forceinline__ Row row(int r) const { return Row{int(r * sr), r < rows}; }
+  __device__ __forceinline__ Kx kx(int k) const { return Kx{int(k * sk), k < K}; }
+  __device__ __forceinline__ bool addr(const Row& rw, const Kx& x, int& off) const {
+    off = rw.off + x.off;
+    return rw.ok && x.ok;
+  }
   __device__ __forceinline__ T at(const Row& rw, int k) const {
-    return (rw.ok && k < K) ? __ldg(p + rw.off + int64_t(k) * sk) : T(0);
+    return (rw.ok && k < K) ? __ldg(p + rw.off + int(k * sk)) : T(0);
   }
   __device__ __forceinline__ bool m_contig() const { return mcontig; }
 };
 
 // Marker: the operand is K-contiguous and 16-byte aligned, loaded by TMA.
 struct TmaView {
-  struct Row { int dummy; };
-  __device__ __forceinline__ Row row(int) const { return Row{0}; }
+  struct Row { int off; bool ok; };
+  struct Kx { int off; bool ok; };
+  __device__ __forceinline__ const float* base() const { return nullptr; }
+  __device__ __forceinline__ Row row(int) const { return Row{0, false}; }
+  __device__ __forceinline__ Kx kx(int) const { return Kx{0, false}; }
+  __device__ __forceinline__ bool addr(const Row&, const Kx&, int& off) const { off = 0; return false; }
   __device__ __forceinline__ float at(const Row&, int) const { return 0.f; }
   __device__ __forceinline__ bool m_contig() const { return false; }
 };
@@ -82,53 +106,74 @@ struct ConvFwdA {
   const ConvTap* taps;   // Cg*R*S entries
   ConvGeom g;
   int rows, K;
-  struct Row { int64_t base; int h0, w0; bool ok; };
+  struct Row { int base; int h0, w0; bool ok; };
+  struct Kx { int off; int dh, dw; bool ok; };
+  __device__ __forceinline__ const T* base() const { return x; }
   __device__ __forceinline__ Row row(int r) const {
-    Row rw; rw.ok = r < rows;
+    Row rw;
+    rw.ok = r < rows;
     const uint32_t img = g.div_PQ.div(r), pq = r - img * g.P * g.Q;
     const uint32_t pp = g.div_Q.div(pq), qq = pq - pp * g.Q;
-    rw.h0 = int(pp) * g.sh - g.ph; rw.w0 = int(qq) * g.sw - g.pw;
-    rw.base = int64_t(img) * g.C * g.H * g.W + int64_t(rw.h0) * g.W + rw.w0;
+    rw.h0 = int(pp) * g.sh - g.ph;
+    rw.w0 = int(qq) * g.sw - g.pw;
+    rw.base = int(img) * g.C * g.H * g.W + rw.h0 * g.W + rw.w0;
     return rw;
   }
-  __device__ __forceinline__ T at(const Row& rw, int k) const {
-    if (!rw.ok || k >= K) return T(0);
-    const ConvTap t = taps[k];
-    const int h = rw.h0 + t.dh, w = rw.w0 + t.dw;
-    if (unsigned(h) >= unsigned(g.H) || unsigned(w) >= unsigned(g.W)) return T(0);
-    return __ldg(x + rw.base + t.off);
+  __device__ __forceinline__ Kx kx(int k) const {
+    if (k >= K) return Kx{0, 0, 0, false};
+    const int4 t = __ldg(reinterpret_cast<const int4*>(taps) + k);
+    return Kx{t.x, t.y, t.z, true};
   }
+  __device__ __forceinline__ bool addr(const Row& rw, const Kx& t, int& off) const {
+    const int h = rw.h0 + t.dh, w = rw.w0 + t.dw;
+    off = rw.base + t.off;
+    return rw.ok && t.ok && unsigned(h) < unsigned(g.H) && unsigned(w) < unsigned(g.W);
+  }
+  __device__ __forceinline__ T at(const Row& rw, int k) const { return view_at(*this, rw, k); }
   __device__ __forceinline__ bool m_contig() const { return true; }
 };
 
 // Backward-data A: rows m = bottom pixel (img, h, w); k = (co, kr, ks) in the group.
 // A(m,k) = dy[img][co][(h+ph-kr*dh)/sh][(w+pw-ks*dw)/sw] when integral and in range.
 struct DgradTap { int off; int dh; int dw; int pad_; };  // off = co*P*Q
-template <typename T>
+template <typename T, bool UNIT_STRIDE = false>
 struct ConvDgradA {
   const T* dy;           // top diff, offset to the group's first channel
   const DgradTap* taps;  // Cog*R*S entries
   ConvGeom g;
   int rows, K;
-  struct Row { int64_t base; int hp, wp; bool ok; };
+  struct Row { int base; int hp, wp; bool ok; };
+  struct Kx { int off; int dh, dw; bool ok; };
+  __device__ __forceinline__ const T* base() const { return dy; }
   __device__ __forceinline__ Row row(int r) const {
-    Row rw; rw.ok = r < rows;
+    Row rw;
+    rw.ok = r < rows;
     const uint32_t img = g.div_HW.div(r), hw = r - img * g.H * g.W;
     const uint32_t h = g.div_W.div(hw), w = hw - h * g.W;
-    rw.hp = int(h) + g.ph; rw.wp = int(w) + g.pw;
-    rw.base = int64_t(img) * g.Co * g.P * g.Q;
+    rw.hp = int(h) + g.ph;
+    rw.wp = int(w) + g.pw;
+    rw.base = int(img) * g.Co * g.P * g.Q;
     return rw;
   }
-  __device__ __forceinline__ T at(const Row& rw, int k) const {
-    if (!rw.ok || k >= K) return T(0);
-    const DgradTap t = taps[k];
-    int pn = rw.hp - t.dh, qn = rw.wp - t.dw;
-    if (pn < 0 || qn < 0) return T(0);
-    if (g.sh != 1) { if (pn % g.sh) return T(0); pn /= g.sh; }
-    if (g.sw != 1) { if (qn % g.sw) return T(0); qn /= g.sw; }
-    if (pn >= g.P || qn >= g.Q) return T(0);
-    return __ldg(dy + rw.base + t.off + pn * g.Q + qn);
+  __device__ __forceinline__ Kx kx(int k) const {
+    if (k >= K) return Kx{0, 0, 0, false};
+    const int4 t = __ldg(reinterpret_cast<const int4*>(taps) + k);
+    return Kx{t.x, t.y, t.z, true};
   }
+  __device__ __forceinline__ bool addr(const Row& rw, const Kx& t, int& off) const {
+    int pn = rw.hp - t.dh, qn = rw.wp - t.dw;
+    bool ok = rw.ok && t.ok && pn >= 0 && qn >= 0;
+    if constexpr (!UNIT_STRIDE) {
+      const int ps = pn / g.sh, qs = qn / g.sw;
+      ok = ok && ps * g.sh == pn && qs * g.sw == qn;
+      pn = ps;
+      qn = qs;
+    }
+    ok = ok && pn < g.P && qn < g.Q;
+    off = rw.base + t.off + pn * g.Q + qn;
+    return ok;
+  }
+  __device__ __forceinline__ T at(const Row& rw, int k) const { return view_at(*this, rw, k); }
   __device__ __forceinline__ bool m_contig() const { return true; }
 };
 
@@ -140,38 +185,78 @@ struct ConvDgradB {
   const int* koff;       // per k: co*Cg*R*S + kr*S + ks
   int RS;
   int rows, K;
-  struct Row { int64_t off; bool ok; };
-  __device__ __forceinline__ Row row(int r) const { return Row{int64_t(r) * RS, r < rows}; }
-  __device__ __forceinline__ T at(const Row& rw, int k) const {
-    return (rw.ok && k < K) ? __ldg(w + rw.off + koff[k]) : T(0);
+  struct Row { int off; bool ok; };
+  struct Kx { int off; bool ok; };
+  __device__ __forceinline__ const T* base() const { return w; }
+  __device__ __forceinline__ Row row(int r) const { return Row{r * RS, r < rows}; }
+  __device__ __forceinline__ Kx kx(int k) const { return k < K ? Kx{__ldg(koff + k), true} : Kx{0, false}; }
+  __device__ __forceinline__ bool addr(const Row& rw, const Kx& x, int& off) const {
+    off = rw.off + x.off;
+    return rw.ok && x.ok;
   }
+  __device__ __forceinline__ T at(const Row& rw, int k) const { return view_at(*this, rw, k); }
   __device__ __forceinline__ bool m_contig() const { return false; }
 };
 
 // Backward-filter A: rows m = tap (ci, kr, ks); k = output pixel (img, p, q).
+// With `ones_row` an extra row m = rows holds 1.0 for every valid k, so the
+// GEMM also produces D[rows][co] = sum_k dy(co, k): the bias gradient rides
+// along on the tensor cores (no separate reduction kernel).
 template <typename T>
 struct ConvWgradA {
   const T* x;            // bottom data, offset to the group's first channel
   const ConvTap* taps;   // Cg*R*S
   ConvGeom g;
   int rows, K;           // rows = Cg*R*S, K = N*P*Q
-  struct Row { int off, dh, dw; bool ok; };
+  bool ones_row;
+  struct Row { int off, dh, dw; bool ok; bool one; };
+  struct Kx { int base; int h0, w0; bool ok; };
+  static constexpr bool kHasOnes = true;
+  __device__ __forceinline__ const T* base() const { return x; }
   __device__ __forceinline__ Row row(int r) const {
-    Row rw; rw.ok = r < rows;
-    if (rw.ok) { const ConvTap t = taps[r]; rw.off = t.off; rw.dh = t.dh; rw.dw = t.dw; }
-    else { rw.off = 0; rw.dh = 0; rw.dw = 0; }
-    return rw;
+    if (r >= rows) return Row{0, 0, 0, false, ones_row && r == rows};
+    const int4 t = __ldg(reinterpret_cast<const int4*>(taps) + r);
+    return Row{t.x, t.y, t.z, true, false};
   }
-  __device__ __forceinline__ T at(const Row& rw, int k) const {
-    if (!rw.ok || k >= K) return T(0);
+  __device__ __forceinline__ bool is_one(const Row& rw) const { return rw.one; }
+  __device__ __forceinline__ Kx kx(int k) const {
+    Kx p;
+    p.ok = k < K;
     const uint32_t img = g.div_PQ.div(k), pq = k - img * g.P * g.Q;
     const uint32_t pp = g.div_Q.div(pq), qq = pq - pp * g.Q;
-    const int h = int(pp) * g.sh - g.ph + rw.dh, w = int(qq) * g.sw - g.pw + rw.dw;
-    if (unsigned(h) >= unsigned(g.H) || unsigned(w) >= unsigned(g.W)) return T(0);
-    return __ldg(x + int64_t(img) * g.C * g.H * g.W + int64_t(h) * g.W + w +
-                 (rw.off - rw.dh * g.W - rw.dw));
+    p.h0 = int(pp) * g.sh - g.ph;
+    p.w0 = int(qq) * g.sw - g.pw;
+    p.base = int(img) * g.C * g.H * g.W + p.h0 * g.W + p.w0;
+    return p;
+  }
+  __device__ __forceinline__ bool addr(const Row& rw, const Kx& p, int& off) const {
+    const int h = p.h0 + rw.dh, w = p.w0 + rw.dw;
+    off = p.base + rw.off;
+    return rw.ok && p.ok && unsigned(h) < unsigned(g.H) && unsigned(w) < unsigned(g.W);
+  }
+  __device__ __forceinline__ T at(const Row& rw, int k) const {
+    if (rw.one) return k < K ? T(1) : T(0);
+    return view_at(*this, rw, k);
   }
   __device__ __forceinline__ bool m_contig() const { return false; }
+};
+
+// backward-filter epilogue: dw[co][tap] += D[tap][co]; the ones row adds
+// D[Kc][co] into db[co] (param diffs accumulate, layers.hpp:84-86).
+template <typename T>
+struct ConvWgradEpi {
+  T* dw;                 // offset to the group's first filter
+  T* db;                 // offset to the group's first channel, may be null
+  int Kc;
+  __device__ __forceinline__ void store(int m, int n, T acc, int) const {
+    if (m < Kc) {
+      if (!dw) return;
+      T* o = dw + int64_t(n) * Kc + m;
+      *o = *o + acc;
+    } else if (db) {
+      db[n] = db[n] + acc;
+    }
+  }
 };
 
 // Backward-filter B: rows n = co in the group; k = output pixel (img, p, q).
@@ -180,13 +265,19 @@ struct ConvWgradB {
   const T* dy;           // top diff, offset to the group's first channel
   ConvGeom g;
   int rows, K;
-  struct Row { int64_t off; bool ok; };
-  __device__ __forceinline__ Row row(int r) const { return Row{int64_t(r) * g.P * g.Q, r < rows}; }
-  __device__ __forceinline__ T at(const Row& rw, int k) const {
-    if (!rw.ok || k >= K) return T(0);
+  struct Row { int off; bool ok; };
+  struct Kx { int base; bool ok; };
+  __device__ __forceinline__ const T* base() const { return dy; }
+  __device__ __forceinline__ Row row(int r) const { return Row{r * g.P * g.Q, r < rows}; }
+  __device__ __forceinline__ Kx kx(int k) const {
     const uint32_t img = g.div_PQ.div(k), pq = k - img * g.P * g.Q;
-    return __ldg(dy + int64_t(img) * g.Co * g.P * g.Q + rw.off + pq);
+    return Kx{int(img) * g.Co * g.P * g.Q + int(pq), k < K};
   }
+  __device__ __forceinline__ bool addr(const Row& rw, const Kx& p, int& off) const {
+    off = p.base + rw.off;
+    return rw.ok && p.ok;
+  }
+  __device__ __forceinline__ T at(const Row& rw, int k) const { return view_at(*this, rw, k); }
   __device__ __forceinline__ bool m_contig() const { return false; }
 };
 

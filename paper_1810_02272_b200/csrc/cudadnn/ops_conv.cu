@@ -15,25 +15,6 @@ namespace cdnn {
 namespace {
 
 template <typename T>
-__global__ void conv_bias_grad_kernel(const T* __restrict__ dy, T* __restrict__ db, int N, int Co, int PQ) {
-  // one block per output channel; fixed-shape tree -> deterministic
-  __shared__ T sh[256];
-  const int co = blockIdx.x;
-  T s = T(0);
-  for (int img = 0; img < N; ++img) {
-    const T* p = dy + (int64_t(img) * Co + co) * PQ;
-    for (int i = threadIdx.x; i < PQ; i += blockDim.x) s += p[i];
-  }
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) db[co] += sh[0];
-}
-
-template <typename T>
 void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const BufferSlot& Wt,
                     const BufferSlot* B, BufferSlot& Y, cdnn_handle stream) {
   const ConvGeom& g = d.geom;
@@ -67,11 +48,14 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   for (int grp = 0; grp < g.group; ++grp) {
     const T* dy = reinterpret_cast<const T*>(DY.dev) + int64_t(grp) * g.Cog * g.P * g.Q;
     const T* w = reinterpret_cast<const T*>(Wt.dev) + int64_t(grp) * g.Cog * g.Cg * g.R * g.S;
-    ConvDgradA<T> va{dy, d.dtaps, g, M, K};
     ConvDgradB<T> vb{w, d.koff, g.R * g.S, N, K};
     ConvDgradEpi<T> epi{reinterpret_cast<T*>(DX.dev) + int64_t(grp) * g.Cg * g.H * g.W, g};
-    if constexpr (std::is_same_v<T, float>) run_tc(c, st, ws, plan_tc(M, N, K), M, N, K, va, vb, epi);
-    else run_simt<T>(c, st, ws, plan_simt(M, N, K), M, N, K, va, vb, epi);
+    auto go = [&](const auto& va) {
+      if constexpr (std::is_same_v<T, float>) run_tc(c, st, ws, plan_tc(M, N, K), M, N, K, va, vb, epi);
+      else run_simt<T>(c, st, ws, plan_simt(M, N, K), M, N, K, va, vb, epi);
+    };
+    if (g.sh == 1 && g.sw == 1) go(ConvDgradA<T, true>{dy, d.dtaps, g, M, K});
+    else go(ConvDgradA<T, false>{dy, d.dtaps, g, M, K});
   }
 }
 
@@ -81,25 +65,19 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
   const ConvGeom& g = d.geom;
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
-  const int M = d.Kc, N = g.Cog, K = g.N * g.P * g.Q;
-  if (DW) {
-    for (int grp = 0; grp < g.group; ++grp) {
-      const T* x = reinterpret_cast<const T*>(X.dev) + int64_t(grp) * g.Cg * g.H * g.W;
-      const T* dy = reinterpret_cast<const T*>(DY.dev) + int64_t(grp) * g.Cog * g.P * g.Q;
-      ConvWgradA<T> va{x, d.taps, g, M, K};
-      ConvWgradB<T> vb{dy, g, N, K};
-      // dw[co][tap] += D[tap][co]
-      StoreEpi<T> epi{reinterpret_cast<T*>(DW->dev) + int64_t(grp) * g.Cog * M, 1, int64_t(M), T(1), T(1),
-                      nullptr, false, false};
-      if constexpr (std::is_same_v<T, float>) run_tc(c, st, ws, plan_tc(M, N, K), M, N, K, va, vb, epi);
-      else run_simt<T>(c, st, ws, plan_simt(M, N, K), M, N, K, va, vb, epi);
-    }
-  }
-  if (DB) {
-    conv_bias_grad_kernel<T><<<g.Co, 256, 0, st>>>(reinterpret_cast<const T*>(DY.dev),
-                                                   reinterpret_cast<T*>(DB->dev), g.N, g.Co, g.P * g.Q);
-    check_launch("conv_bias_grad");
-    count_launch(c);
+  if (!DW && !DB) return;
+  // rows = taps (+1 all-ones row when the bias gradient is wanted)
+  const int Kc = d.Kc, M = Kc + (DB ? 1 : 0), N = g.Cog, K = g.N * g.P * g.Q;
+  for (int grp = 0; grp < g.group; ++grp) {
+    const T* x = reinterpret_cast<const T*>(X.dev) + int64_t(grp) * g.Cg * g.H * g.W;
+    const T* dy = reinterpret_cast<const T*>(DY.dev) + int64_t(grp) * g.Cog * g.P * g.Q;
+    ConvWgradA<T> va{x, d.taps, g, Kc, K, DB != nullptr};
+    ConvWgradB<T> vb{dy, g, N, K};
+    // dw[co][tap] += D[tap][co] ; db[co] += D[Kc][co]
+    ConvWgradEpi<T> epi{DW ? reinterpret_cast<T*>(DW->dev) + int64_t(grp) * g.Cog * Kc : nullptr,
+                        DB ? reinterpret_cast<T*>(DB->dev) + grp * g.Cog : nullptr, Kc};
+    if constexpr (std::is_same_v<T, float>) run_tc(c, st, ws, plan_tc(M, N, K), M, N, K, va, vb, epi);
+    else run_simt<T>(c, st, ws, plan_simt(M, N, K), M, N, K, va, vb, epi);
   }
 }
 

@@ -1,0 +1,79 @@
+"""Per-op device timing of the convolution / InnerProduct contractions of the
+bench workloads through the C-ABI (CUDA events on the context stream, median
+of N launches, L2-warm).  Prints one JSON line per op.
+
+Usage: python profiles/conv_bench.py [--math tf32x3|tf32] [--reps 20]"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1810_02272_b200 import cudadnn as cd  # noqa: E402
+
+CASES = {
+    # name: n, c, h, w, co, k, stride, pad
+    "cq.conv1": (100, 3, 32, 32, 32, 5, 1, 2),
+    "cq.conv2": (100, 32, 16, 16, 32, 5, 1, 2),
+    "cq.conv3": (100, 32, 8, 8, 64, 5, 1, 2),
+    "lenet.conv1": (64, 1, 28, 28, 20, 5, 1, 0),
+    "lenet.conv2": (64, 20, 12, 12, 50, 5, 1, 0),
+    "alexnet.conv3": (32, 256, 13, 13, 384, 3, 1, 1),
+}
+
+
+def timeit(ctx, fn, reps):
+    evs = [(ctx.event(), ctx.event()) for _ in range(reps)]
+    fn()
+    ctx.sync()
+    for a, b in evs:
+        ctx.record(a)
+        fn()
+        ctx.record(b)
+    ctx.sync()
+    return statistics.median(ctx.elapsed_ms(a, b) for a, b in evs)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--math", default="tf32x3")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    ctx = cd.Context(0)
+    ctx.call("cdnn_set_math_mode", cd.MATH_TF32X3 if args.math == "tf32x3" else cd.MATH_TF32)
+    rng = np.random.default_rng(0)
+    for name, (n, c, h, w, co, k, s, p) in CASES.items():
+        if args.only and args.only not in name:
+            continue
+        d = ctx.conv_desc(n, c, h, w, co, k, s, p)
+        _, _, P, Q = ctx.conv_output_shape(d)
+        x = ctx.upload(rng.uniform(-1, 1, n * c * h * w).astype(np.float32))
+        wt = ctx.upload(rng.uniform(-1, 1, co * c * k * k).astype(np.float32))
+        b = ctx.upload(np.zeros(co, np.float32))
+        y = ctx.alloc(n * co * P * Q, cd.F32)
+        dy = ctx.upload(rng.uniform(-1, 1, n * co * P * Q).astype(np.float32))
+        dx = ctx.alloc(n * c * h * w, cd.F32)
+        dw = ctx.alloc(co * c * k * k, cd.F32)
+        db = ctx.alloc(co, cd.F32)
+        flops = 2.0 * n * P * Q * co * c * k * k
+        ops = {
+            "fwd": lambda: ctx.call("cdnn_conv_forward", d, x, wt, b, y, 0),
+            "dgrad": lambda: ctx.call("cdnn_conv_backward_data", d, wt, dy, dx, 0),
+            "wgrad": lambda: ctx.call("cdnn_conv_backward_filter", d, x, dy, dw, 0, 0),
+        }
+        for op, fn in ops.items():
+            ms = timeit(ctx, fn, args.reps)
+            print(json.dumps({"op": f"{name}.{op}", "math": args.math, "ms": round(ms, 5),
+                              "tflops": round(flops / ms / 1e9, 3), "gflop": round(flops / 1e9, 4)}), flush=True)
+        for hnd in (x, wt, b, y, dy, dx, dw, db):
+            ctx.free(hnd)
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
