@@ -175,6 +175,46 @@ const CUtensorMap* tmap_k_major(Ctx* c, const float* ptr, int rows, int K, int64
   return &res.first->second;
 }
 
+const CUtensorMap* tmap_generic(Ctx* c, const float* ptr, int rank, const uint64_t* dims,
+                                const uint64_t* strides_elems, const uint32_t* box, int swizzle_bytes) {
+  char key[256];
+  int n = std::snprintf(key, sizeof key, "g%p/%d/%d", static_cast<const void*>(ptr), rank, swizzle_bytes);
+  for (int i = 0; i < rank; ++i)
+    n += std::snprintf(key + n, sizeof key - size_t(n), "/%llu:%llu:%u", static_cast<unsigned long long>(dims[i]),
+                       static_cast<unsigned long long>(i ? strides_elems[i - 1] : 1), box[i]);
+  std::lock_guard lock(c->tmap_mu);
+  auto it = c->tmaps.find(key);
+  if (it != c->tmaps.end()) return &it->second;
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+    if (i) gs[i - 1] = strides_elems[i - 1] * 4;
+  }
+  const CUtensorMapSwizzle sw = swizzle_bytes == kSwizzle128Atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                : swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+  const char* l2e = std::getenv("CDNN_TMA_L2");
+  const int l2 = l2e ? std::atoi(l2e) : 0;
+  const CUtensorMapL2promotion promo = l2 == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                       : l2 == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                       : l2 == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<float*>(ptr), gd, gs,
+                           bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(CDNN_CUDA_ERROR, "cuTensorMapEncodeTiled (generic) failed (" + std::to_string(int(r)) + ")");
+  auto res = c->tmaps.emplace(key, m);
+  return &res.first->second;
+}
+
+std::shared_ptr<DevAlloc> device_alloc_shared(size_t bytes, int device) { return device_alloc(bytes, device); }
+
 }  // namespace cdnn
 
 using namespace cdnn;

@@ -76,6 +76,9 @@ struct ConvDescSlot {
   ConvTap* taps = nullptr;
   DgradTap* dtaps = nullptr;
   int* koff = nullptr;
+  // repacked per-tap weights for the TMA direct-conv path (lazily allocated):
+  // [0] forward hi, [1] forward lo, [2] backward-data hi, [3] backward-data lo
+  std::shared_ptr<DevAlloc> repack[4];
 };
 
 struct PoolDescSlot {
@@ -150,6 +153,13 @@ void check_launch(const char* what);
 // box {32 k, box_rows}, 128B swizzle.  Cached per (ptr, shape, box).
 const CUtensorMap* tmap_k_major(Ctx* c, const float* ptr, int rows, int K, int64_t ld,
                                 int box_rows);
+// Generic fp32 tensor map (rank <= 5): dims/strides in elements (innermost
+// first, strides for dims 1..rank-1), box, swizzle span in bytes (32/64/128)
+// or kSwizzle128Atom32 (SWIZZLE_128B_ATOM_32B: the MN-major tf32 UMMA layout).
+constexpr int kSwizzle128Atom32 = 1;
+const CUtensorMap* tmap_generic(Ctx* c, const float* ptr, int rank, const uint64_t* dims,
+                                const uint64_t* strides_elems, const uint32_t* box, int swizzle_bytes);
+std::shared_ptr<DevAlloc> device_alloc_shared(size_t bytes, int device);
 
 // Plain GEMM-shaped launches shared by gemm / ip / conv (ops_gemm.cu).
 struct GemmPlan {

@@ -9,10 +9,109 @@
 // m is always the output's contiguous index, so epilogue stores coalesce.
 // Backward-filter accumulates into dw (param diffs accumulate, layers.hpp:84-86);
 // its bias gradient is a deterministic per-channel reduction.
+#include <cstdlib>
+
+#include "conv_tma.cuh"
 #include "launch.cuh"
 
 namespace cdnn {
 namespace {
+
+bool conv_tma_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CDNN_CONV_TMA");
+    return !(v && std::string(v) == "0");
+  }();
+  return on;
+}
+
+template <int BN, bool SPLIT>
+void launch_conv_tma(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& tin, const CUtensorMap& twh,
+                     const CUtensorMap& twl, const tcconv::ConvTmaArgs& a) {
+  constexpr int smem = tcconv::smem_bytes<BN, SPLIT>();
+  auto kern = tcconv::conv_tma_kernel<BN, SPLIT>;
+  static bool attr_set[16] = {};
+  if (!attr_set[c->device & 15]) {
+    CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set[c->device & 15] = true;
+  }
+  kern<<<grid, tcconv::kThreads, smem, st>>>(tin, twh, twl, a);
+  check_launch("conv_tma_kernel");
+  count_launch(c);
+}
+
+// Direct convolution through TMA tap windows (stride 1, dilation 1, one group).
+// backward_data: out = dx, in = dy, flipped taps.  Returns false when the
+// shape is not eligible (the implicit-GEMM gather path handles it).
+bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const float* in, const float* w,
+                     const float* bias, float* out, cdnn_handle stream) {
+  ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
+  const ConvGeom& g = d.geom;
+  if (!conv_tma_enabled() || g.group != 1 || g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1) return false;
+  // direct-conv extents
+  const int Cin = backward_data ? g.Co : g.C, Hin = backward_data ? g.P : g.H, Win = backward_data ? g.Q : g.W;
+  const int Cout = backward_data ? g.C : g.Co, P = backward_data ? g.H : g.P, Q = backward_data ? g.W : g.Q;
+  const int oh = backward_data ? g.R - 1 - g.ph : g.ph, ow = backward_data ? g.S - 1 - g.pw : g.pw;
+  if (Win % 4 != 0 || Cout > 4096 || Win > 65535) return false;
+  const bool split = c->math_mode == CDNN_MATH_TF32X3;
+  tcconv::ConvTmaArgs a{};
+  a.N = g.N; a.Cin = Cin; a.Hin = Hin; a.Win = Win;
+  a.Cout = Cout; a.P = P; a.Q = Q; a.R = g.R; a.S = g.S; a.oh = oh; a.ow = ow;
+  // 32-pixel atoms of rb = 32/TW image rows; a tile = 4 atoms
+  a.TW = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
+  const int rb = 32 / a.TW, rows = 128 / a.TW;
+  a.TH = std::min(rows, (P + rb - 1) / rb * rb);
+  a.NB = std::max(1, std::min(rows / a.TH, g.N));
+  a.CB = Cin >= 16 ? 32 : 8;
+  a.cblocks = (Cin + a.CB - 1) / a.CB;
+  a.tiles_q = (Q + a.TW - 1) / a.TW;
+  a.tiles_p = (P + a.TH - 1) / a.TH;
+  const int tiles_n = (g.N + a.NB - 1) / a.NB;
+  a.bias = bias;
+  a.out = out;
+  const int tiles = a.tiles_q * a.tiles_p * tiles_n;
+  int bn = Cout <= 32 ? 32 : (Cout <= 64 ? 64 : 128);
+  if (bn > 32 && tiles * ((Cout + bn - 1) / bn) < kNumSMs) bn = bn == 128 ? 64 : 32;
+  const int kpad = a.cblocks * a.CB;
+  const int RS = g.R * g.S;
+  // repack (and pre-split) the weights into the per-tap K-major operand
+  const size_t elems = size_t(RS) * Cout * kpad;
+  const int slot = backward_data ? 2 : 0;
+  if (!d.repack[slot] || d.repack[slot]->bytes < elems * 4) {
+    d.repack[slot] = device_alloc_shared(elems * 4, c->device);
+    d.repack[slot + 1] = device_alloc_shared(elems * 4, c->device);
+  }
+  float* whi = static_cast<float*>(d.repack[slot]->ptr);
+  float* wlo = static_cast<float*>(d.repack[slot + 1]->ptr);
+  cudaStream_t st = stream_of(c, stream);
+  tcconv::repack_weights_kernel<<<grid_for(int64_t(elems), 256), 256, 0, st>>>(
+      w, whi, wlo, g.Co, g.C, g.R, g.S, Cout, kpad, backward_data, split);
+  check_launch("repack_weights");
+  count_launch(c);
+  // tensor maps: input NCHW {W, H, C, N} with box {TW, 1, CB, 1}; weights {kpad, RS*Cout} box {CB, BN}
+  const uint64_t idims[4] = {uint64_t(Win), uint64_t(Hin), uint64_t(Cin), uint64_t(g.N)};
+  const uint64_t istr[3] = {uint64_t(Win), uint64_t(Hin) * Win, uint64_t(Cin) * Hin * Win};
+  // staged window: TW + 4 columns from the 16-byte aligned start (no swizzle)
+  const uint32_t ibox[4] = {uint32_t(a.TW + 4), uint32_t(rb), uint32_t(a.CB), 1u};
+  const CUtensorMap* tin = tmap_generic(c, in, 4, idims, istr, ibox, 0);
+  const uint64_t wdims[2] = {uint64_t(kpad), uint64_t(RS) * Cout};
+  const uint64_t wstr[1] = {uint64_t(kpad)};
+  const uint32_t wbox[2] = {uint32_t(a.CB), uint32_t(bn)};
+  const CUtensorMap* twh = tmap_generic(c, whi, 2, wdims, wstr, wbox, a.CB * 4);
+  const CUtensorMap* twl = tmap_generic(c, wlo, 2, wdims, wstr, wbox, a.CB * 4);
+  dim3 grid(tiles, (Cout + bn - 1) / bn);
+  auto go = [&](auto split_tag) {
+    constexpr bool S = decltype(split_tag)::value;
+    switch (bn) {
+      case 32: launch_conv_tma<32, S>(c, st, grid, *tin, *twh, *twl, a); break;
+      case 64: launch_conv_tma<64, S>(c, st, grid, *tin, *twh, *twl, a); break;
+      default: launch_conv_tma<128, S>(c, st, grid, *tin, *twh, *twl, a); break;
+    }
+  };
+  if (split) go(std::true_type{});
+  else go(std::false_type{});
+  return true;
+}
 
 template <typename T>
 void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const BufferSlot& Wt,
@@ -21,6 +120,11 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.P * g.Q, N = g.Cog, K = d.Kc;
+  if constexpr (std::is_same_v<T, float>) {
+    if (conv_direct_tma(c, d, false, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
+                        B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
+      return;
+  }
   for (int grp = 0; grp < g.group; ++grp) {
     const T* x = reinterpret_cast<const T*>(X.dev) + int64_t(grp) * g.Cg * g.H * g.W;
     const T* w = reinterpret_cast<const T*>(Wt.dev) + int64_t(grp) * g.Cog * K;
@@ -45,6 +149,11 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.H * g.W, N = g.Cg, K = d.Kd;
+  if constexpr (std::is_same_v<T, float>) {
+    if (conv_direct_tma(c, d, true, reinterpret_cast<const float*>(DY.dev), reinterpret_cast<const float*>(Wt.dev),
+                        nullptr, reinterpret_cast<float*>(DX.dev), stream))
+      return;
+  }
   for (int grp = 0; grp < g.group; ++grp) {
     const T* dy = reinterpret_cast<const T*>(DY.dev) + int64_t(grp) * g.Cog * g.P * g.Q;
     const T* w = reinterpret_cast<const T*>(Wt.dev) + int64_t(grp) * g.Cog * g.Cg * g.R * g.S;
