@@ -35,7 +35,7 @@ struct ConvTmaArgs {
   int N, Cin, Hin, Win;     // input of the direct conv (x for fwd, dy for dgrad)
   int Cout, P, Q;           // output extents
   int R, S, oh, ow;         // taps and the coordinate offset of tap (0,0)
-  int TW, TH, NB, CB;       // tile geometry: TW*TH*NB <= 128 pixels, CB channels per stage
+  int TH, NB;               // tile rows per image and images per tile (TW, CB are template params)
   int cblocks;              // ceil(Cin / CB)
   int tiles_q, tiles_p;     // tiles along q and p
   const float* bias;        // may be null (fwd only)
@@ -63,28 +63,32 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo_b
   return d;
 }
 
-// swizzle layout code of an MN-major row of TW fp32 (TMA swizzle span = TW*4 bytes)
-__host__ __device__ constexpr uint32_t layout_for_row_bytes(int bytes) {
-  return bytes == 128 ? 2u : bytes == 64 ? 4u : 6u;  // SW128 / SW64 / SW32
-}
+// per stage: A hi/lo tiles (128 px x CB), B hi/lo (BN x CB), staging window
+template <int TW, int CB>
+__host__ __device__ constexpr uint32_t stg_bytes() { return 4u * CB * (32 / TW) * (TW + 4) * 4u; }
+template <int CB>
+__host__ __device__ constexpr uint32_t a_bytes() { return 128u * CB * 4u; }
+template <int BN, int CB>
+__host__ __device__ constexpr uint32_t b_bytes() { return uint32_t(BN) * CB * 4u; }
+__host__ __device__ constexpr uint32_t round1k(uint32_t b) { return (b + 1023u) & ~1023u; }
 
-// per stage: staging (aligned activation window, no swizzle), A hi/lo tiles, B hi/lo
-__host__ __device__ constexpr uint32_t a_bytes() { return 128 * 32 * 4; }           // 128 px x 32 ch
-__host__ __device__ constexpr uint32_t stg_bytes() { return 32 * 4 * (32 + 16) * 4; }  // 4 atoms x 32 ch x (32 + 4*rb)
-template <int BN>
-__host__ __device__ constexpr uint32_t b_bytes() { return BN * 32 * 4; }
-
-template <int BN>
-__host__ __device__ constexpr int stages() { return BN >= 128 ? 2 : 3; }
-
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, int TW, int CB>
 __host__ __device__ constexpr uint32_t stage_bytes() {
-  return stg_bytes() + (a_bytes() + b_bytes<BN>()) * (SPLIT ? 2 : 1);
+  return round1k((a_bytes<CB>() + b_bytes<BN, CB>()) * (SPLIT ? 2 : 1) + stg_bytes<TW, CB>());
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, int TW, int CB>
+__host__ __device__ constexpr int stages() {
+  // as many stages as fit in ~200 KB (2..6)
+  return int(200u * 1024u / stage_bytes<BN, SPLIT, TW, CB>()) > 6 ? 6
+         : int(200u * 1024u / stage_bytes<BN, SPLIT, TW, CB>()) < 2 ? 2
+                                                                     : int(200u * 1024u / stage_bytes<BN, SPLIT, TW, CB>());
+}
+
+template <int BN, bool SPLIT, int TW, int CB>
 __host__ __device__ constexpr int smem_bytes() {
-  return 1024 + stages<BN>() * int(stage_bytes<BN, SPLIT>()) + (3 * stages<BN>() + 1) * 8 + 16;
+  return 1024 + stages<BN, SPLIT, TW, CB>() * int(stage_bytes<BN, SPLIT, TW, CB>()) +
+         (3 * stages<BN, SPLIT, TW, CB>() + 1) * 8 + 16;
 }
 
 // ATOM_32B swizzle of the MN-major tf32 UMMA layout (128B_BASE32B): 32-byte
@@ -93,18 +97,21 @@ __device__ __forceinline__ uint32_t atom32_off(uint32_t row, uint32_t col) {
   return row * 128u + ((((col >> 3) ^ row) & 3u) << 5) + ((col & 7u) << 2);
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, int TW, int CB>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tma_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_w_hi,
                     const __grid_constant__ CUtensorMap tm_w_lo, const ConvTmaArgs a) {
-  constexpr int ST = stages<BN>();
-  constexpr uint32_t A_BYTES = a_bytes(), B_BYTES = b_bytes<BN>(), STG = stg_bytes();
-  constexpr uint32_t STAGE = stage_bytes<BN, SPLIT>();
+  constexpr int ST = stages<BN, SPLIT, TW, CB>();
+  constexpr int RB = 32 / TW;          // image rows per 32-pixel atom
+  constexpr int SW = TW + 4;           // staged window width (shift 0..3)
+  constexpr uint32_t A_BYTES = a_bytes<CB>(), B_BYTES = b_bytes<BN, CB>();
+  constexpr uint32_t STAGE = stage_bytes<BN, SPLIT, TW, CB>();
+  constexpr uint32_t BOX = uint32_t(SW * RB * CB) * 4u;  // one atom's staged window
   constexpr uint32_t TMEM_COLS = tc::tmem_cols_for(BN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // stage: [A hi | B hi | A lo | B lo | staging]; every tile 1024-B aligned
+  // stage: [A hi | B hi | A lo | B lo | staging]
   auto a_hi = [&](int s) { return smem + s * STAGE; };
   auto b_hi = [&](int s) { return smem + s * STAGE + A_BYTES; };
   auto a_lo = [&](int s) { return smem + s * STAGE + A_BYTES + B_BYTES; };
@@ -122,14 +129,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   t /= a.tiles_q;
   const int tp = t % a.tiles_p;
   const int tn = t / a.tiles_p;
-  const int q0 = tq * a.TW, p0 = tp * a.TH, img0 = tn * a.NB;
+  const int q0 = tq * TW, p0 = tp * a.TH, img0 = tn * a.NB;
   const int n0 = blockIdx.y * BN;
   const int nk = a.R * a.S * a.cblocks;
-  const int rb = 32 / a.TW, hgroups = a.TH / rb;
-  const int nat = min(4, a.NB * hgroups);          // 32-pixel atoms in this tile
-  const int sw_w = a.TW + 4;                        // staged window width (shift 0..3)
-  const uint32_t box_bytes = uint32_t(sw_w * rb * a.CB) * 4u;
-  const uint32_t b_box_bytes = uint32_t(BN * a.CB) * 4u;
+  const int hgroups = a.TH / RB;
+  const int nat = min(4, a.NB * hgroups);  // 32-pixel atoms in this tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -154,22 +158,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (SPLIT) ptx::tma_prefetch_desc(&tm_w_lo);
       int stage = 0;
       uint32_t phase = 0;
+      int cb = 0, kr = 0, ks = 0;
       for (int kt = 0; kt < nk; ++kt) {
-        const int cb = kt % a.cblocks, tap = kt / a.cblocks;
-        const int kr = tap / a.S, ks = tap - kr * a.S;
-        const int x0 = q0 - a.ow + ks;
-        const int x0a = (x0 >> 2) << 2;  // TMA needs 16-byte aligned inner coordinates
+        const int tap = kr * a.S + ks;
+        const int x0a = ((q0 - a.ow + ks) >> 2) << 2;  // TMA needs 16-byte aligned inner coordinates
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[stage], box_bytes * nat + b_box_bytes * (SPLIT ? 2 : 1));
+        ptx::mbar_arrive_expect_tx(&full[stage], BOX * nat + B_BYTES * (SPLIT ? 2 : 1));
         for (int bi = 0; bi < nat; ++bi) {
           const int nb = bi / hgroups, hg = bi - nb * hgroups;
-          tma_load_4d(stg(stage) + bi * box_bytes, &tm_in, &full[stage], x0a, p0 - a.oh + kr + hg * rb, cb * a.CB,
-                      img0 + nb);
+          tma_load_4d(stg(stage) + bi * BOX, &tm_in, &full[stage], x0a, p0 - a.oh + kr + hg * RB, cb * CB, img0 + nb);
         }
         const int wrow = tap * a.Cout + n0;
-        ptx::tma_load_2d(b_hi(stage), &tm_w_hi, &full[stage], cb * a.CB, wrow);
-        if constexpr (SPLIT) ptx::tma_load_2d(b_lo(stage), &tm_w_lo, &full[stage], cb * a.CB, wrow);
+        ptx::tma_load_2d(b_hi(stage), &tm_w_hi, &full[stage], cb * CB, wrow);
+        if constexpr (SPLIT) ptx::tma_load_2d(b_lo(stage), &tm_w_lo, &full[stage], cb * CB, wrow);
         if (++stage == ST) { stage = 0; phase ^= 1; }
+        if (++cb == a.cblocks) { cb = 0; if (++ks == a.S) { ks = 0; ++kr; } }
       }
     }
   } else if (warp == 1) {
@@ -177,12 +180,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // A: MN-major tf32 => 128B_BASE32B layout: rows of 32 pixels (128 B) per
       // channel, 4-channel groups 512 B apart (SBO), atoms CB*128 B apart (LBO)
-      const uint32_t a_lbo = uint32_t(a.CB) * 128u, a_kgrp = 8u * 128u;
+      constexpr uint32_t a_lbo = uint32_t(CB) * 128u, a_kgrp = 8u * 128u;
       // B: K-major rows of CB fp32 (CB=32 -> SW128, CB=8 -> SW32)
-      const uint32_t b_row = uint32_t(a.CB) * 4u;
-      const uint32_t b_layout = b_row == 128 ? 2u : 6u;
-      const uint32_t b_sbo = 8u * b_row;
-      const uint32_t idesc = tc::make_idesc_tf32(BN) | (1u << 15);  // A MN-major, B K-major
+      constexpr uint32_t b_layout = CB == 32 ? 2u : 6u;
+      constexpr uint32_t b_sbo = 8u * CB * 4u;
+      constexpr uint32_t idesc = tc::make_idesc_tf32(BN) | (1u << 15);  // A MN-major, B K-major
       int stage = 0;
       uint32_t phase = 0;
       for (int kt = 0; kt < nk; ++kt) {
@@ -190,7 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         const uint32_t ah = ptx::smem_u32(a_hi(stage)), bh = ptx::smem_u32(b_hi(stage));
         const uint32_t al = ptx::smem_u32(a_lo(stage)), bl = ptx::smem_u32(b_lo(stage));
-        for (int j = 0; j < a.CB / 8; ++j) {
+#pragma unroll
+        for (int j = 0; j < CB / 8; ++j) {
           const uint64_t dA_hi = make_desc(ah + j * a_kgrp, a_lbo, 512u, 1u);
           const uint64_t dB_hi = make_desc(bh + j * 32u, 16u, b_sbo, b_layout);
           uint32_t acc = (kt > 0 || j > 0) ? 1u : 0u;
@@ -211,40 +214,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ---------------- converters: shift + swizzle (+ 3xTF32 split) ----------------
+    // Thread t handles 16-byte output granules (row, col4) with col4 = t & 7
+    // fixed, rows (t >> 3) + 16*i; row = atom*CB + channel.  The staged source
+    // of granule element e sits at row*(RB*SW) + (j/TW)*SW + j%TW + shift,
+    // j = col4*4 + e, so everything but the row term is loop invariant.
     const int tid = threadIdx.x - 64;
-    const int granules = 32 * a.CB;  // 128 px x CB ch / 4
+    const int col4 = tid & 7, row0 = tid >> 3;
+    constexpr int ROWS = 4 * CB;  // atom rows in the A tile
+    int src_e[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = col4 * 4 + e;
+      src_e[e] = (j / TW) * SW + (j % TW);
+    }
     int stage = 0;
     uint32_t phase = 0;
+    int cb = 0, ks = 0;
     for (int kt = 0; kt < nk; ++kt) {
-      const int tap = kt / a.cblocks;
-      const int ks = tap % a.S;
       const int x0 = q0 - a.ow + ks;
       const int delta = x0 - ((x0 >> 2) << 2);
       ptx::mbar_wait(&full[stage], phase);
-      const float* src = reinterpret_cast<const float*>(stg(stage));
+      const float* src = reinterpret_cast<const float*>(stg(stage)) + delta;
       const uint32_t hi = ptx::smem_u32(a_hi(stage)), lo = ptx::smem_u32(a_lo(stage));
-      for (int gidx = tid; gidx < granules; gidx += 128) {
-        // granule = 4 consecutive tile pixels j..j+3 of channel c in atom bi
-        const int col4 = gidx & 7, rowi = gidx >> 3;  // rowi = bi*CB + c
-        const int bi = rowi / a.CB, c = rowi - bi * a.CB;
-        float v[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = col4 * 4 + e;
-          const int hl = j / a.TW, w = j - hl * a.TW;
-          v[e] = bi < nat ? src[((bi * a.CB + c) * rb + hl) * sw_w + delta + w] : 0.f;
-        }
-        const uint32_t off = atom32_off(uint32_t(rowi), uint32_t(col4 * 4));
-        const float h0 = ptx::to_tf32(v[0]), h1 = ptx::to_tf32(v[1]), h2 = ptx::to_tf32(v[2]), h3 = ptx::to_tf32(v[3]);
+      for (int i = 0; i < ROWS / 16; ++i) {
+        const int row = row0 + 16 * i;
+        const float* s = src + row * (RB * SW);
+        float v0 = s[src_e[0]], v1 = s[src_e[1]], v2 = s[src_e[2]], v3 = s[src_e[3]];
+        if (row >= nat * CB) v0 = v1 = v2 = v3 = 0.f;  // atoms past the tile (partial tiles)
+        const uint32_t off = atom32_off(uint32_t(row), uint32_t(col4 * 4));
+        const float h0 = ptx::to_tf32(v0), h1 = ptx::to_tf32(v1), h2 = ptx::to_tf32(v2), h3 = ptx::to_tf32(v3);
         ptx::st_shared_v4(hi + off, h0, h1, h2, h3);
         if constexpr (SPLIT)
-          ptx::st_shared_v4(lo + off, ptx::to_tf32(v[0] - h0), ptx::to_tf32(v[1] - h1), ptx::to_tf32(v[2] - h2),
-                            ptx::to_tf32(v[3] - h3));
+          ptx::st_shared_v4(lo + off, ptx::to_tf32(v0 - h0), ptx::to_tf32(v1 - h1), ptx::to_tf32(v2 - h2),
+                            ptx::to_tf32(v3 - h3));
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&conv[stage]);
       if (++stage == ST) { stage = 0; phase ^= 1; }
+      if (++cb == a.cblocks) { cb = 0; if (++ks == a.S) ks = 0; }
     }
     // ---------------- epilogue: TMEM lane m = atom*32 + hl*TW + w ----------------
     ptx::mbar_wait(accum, 0);
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int m = q * 32 + lane;
     const int bi = m >> 5, within = m & 31;
-    const int nimg = bi / hgroups, hrow = (bi - nimg * hgroups) * rb + within / a.TW, w = within % a.TW;
+    const int nimg = bi / hgroups, hrow = (bi - nimg * hgroups) * RB + within / TW, w = within % TW;
     const int pp = p0 + hrow, qq = q0 + w, img = img0 + nimg;
     const bool valid = bi < nat && img < a.N && pp < a.P && qq < a.Q;
     const int64_t PQ = int64_t(a.P) * a.Q;
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Repack W[co][ci][kr][ks] into the per-tap K-major GEMM operand, padded to cip
+// Repack W[co][ci][kr][ks] into the per-tap K-major GEMM operand, padded to kpad
 // channels, optionally split into (hi, lo) TF32 halves:
 //   forward   : dst[tap][co][ci]                      tap = kr*S + ks
 //   backward  : dst[tap][ci][co] from W[co][ci][R-1-kr][S-1-ks]

@@ -25,11 +25,12 @@ bool conv_tma_enabled() {
   return on;
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, int TW, int CB>
 void launch_conv_tma(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& tin, const CUtensorMap& twh,
                      const CUtensorMap& twl, const tcconv::ConvTmaArgs& a) {
-  constexpr int smem = tcconv::smem_bytes<BN, SPLIT>();
-  auto kern = tcconv::conv_tma_kernel<BN, SPLIT>;
+  constexpr int smem = tcconv::smem_bytes<BN, SPLIT, TW, CB>();
+  static_assert(smem <= 227 * 1024, "conv_tma smem budget");
+  auto kern = tcconv::conv_tma_kernel<BN, SPLIT, TW, CB>;
   static bool attr_set[16] = {};
   if (!attr_set[c->device & 15]) {
     CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -58,13 +59,13 @@ bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, con
   a.N = g.N; a.Cin = Cin; a.Hin = Hin; a.Win = Win;
   a.Cout = Cout; a.P = P; a.Q = Q; a.R = g.R; a.S = g.S; a.oh = oh; a.ow = ow;
   // 32-pixel atoms of rb = 32/TW image rows; a tile = 4 atoms
-  a.TW = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
-  const int rb = 32 / a.TW, rows = 128 / a.TW;
+  const int TW = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
+  const int rb = 32 / TW, rows = 128 / TW;
   a.TH = std::min(rows, (P + rb - 1) / rb * rb);
   a.NB = std::max(1, std::min(rows / a.TH, g.N));
-  a.CB = Cin >= 16 ? 32 : 8;
-  a.cblocks = (Cin + a.CB - 1) / a.CB;
-  a.tiles_q = (Q + a.TW - 1) / a.TW;
+  const int CB = Cin >= 16 ? 32 : 8;
+  a.cblocks = (Cin + CB - 1) / CB;
+  a.tiles_q = (Q + TW - 1) / TW;
   a.tiles_p = (P + a.TH - 1) / a.TH;
   const int tiles_n = (g.N + a.NB - 1) / a.NB;
   a.bias = bias;
@@ -72,7 +73,7 @@ bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, con
   const int tiles = a.tiles_q * a.tiles_p * tiles_n;
   int bn = Cout <= 32 ? 32 : (Cout <= 64 ? 64 : 128);
   if (bn > 32 && tiles * ((Cout + bn - 1) / bn) < kNumSMs) bn = bn == 128 ? 64 : 32;
-  const int kpad = a.cblocks * a.CB;
+  const int kpad = a.cblocks * CB;
   const int RS = g.R * g.S;
   // repack (and pre-split) the weights into the per-tap K-major operand
   const size_t elems = size_t(RS) * Cout * kpad;
@@ -92,21 +93,31 @@ bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, con
   const uint64_t idims[4] = {uint64_t(Win), uint64_t(Hin), uint64_t(Cin), uint64_t(g.N)};
   const uint64_t istr[3] = {uint64_t(Win), uint64_t(Hin) * Win, uint64_t(Cin) * Hin * Win};
   // staged window: TW + 4 columns from the 16-byte aligned start (no swizzle)
-  const uint32_t ibox[4] = {uint32_t(a.TW + 4), uint32_t(rb), uint32_t(a.CB), 1u};
+  const uint32_t ibox[4] = {uint32_t(TW + 4), uint32_t(rb), uint32_t(CB), 1u};
   const CUtensorMap* tin = tmap_generic(c, in, 4, idims, istr, ibox, 0);
   const uint64_t wdims[2] = {uint64_t(kpad), uint64_t(RS) * Cout};
   const uint64_t wstr[1] = {uint64_t(kpad)};
-  const uint32_t wbox[2] = {uint32_t(a.CB), uint32_t(bn)};
-  const CUtensorMap* twh = tmap_generic(c, whi, 2, wdims, wstr, wbox, a.CB * 4);
-  const CUtensorMap* twl = tmap_generic(c, wlo, 2, wdims, wstr, wbox, a.CB * 4);
+  const uint32_t wbox[2] = {uint32_t(CB), uint32_t(bn)};
+  const CUtensorMap* twh = tmap_generic(c, whi, 2, wdims, wstr, wbox, CB * 4);
+  const CUtensorMap* twl = tmap_generic(c, wlo, 2, wdims, wstr, wbox, CB * 4);
   dim3 grid(tiles, (Cout + bn - 1) / bn);
-  auto go = [&](auto split_tag) {
+  auto go_cb = [&](auto split_tag, auto tw_tag, auto cb_tag) {
     constexpr bool S = decltype(split_tag)::value;
+    constexpr int W = decltype(tw_tag)::value, K = decltype(cb_tag)::value;
     switch (bn) {
-      case 32: launch_conv_tma<32, S>(c, st, grid, *tin, *twh, *twl, a); break;
-      case 64: launch_conv_tma<64, S>(c, st, grid, *tin, *twh, *twl, a); break;
-      default: launch_conv_tma<128, S>(c, st, grid, *tin, *twh, *twl, a); break;
+      case 32: launch_conv_tma<32, S, W, K>(c, st, grid, *tin, *twh, *twl, a); break;
+      case 64: launch_conv_tma<64, S, W, K>(c, st, grid, *tin, *twh, *twl, a); break;
+      default: launch_conv_tma<128, S, W, K>(c, st, grid, *tin, *twh, *twl, a); break;
     }
+  };
+  auto go_tw = [&](auto split_tag, auto tw_tag) {
+    if (CB == 32) go_cb(split_tag, tw_tag, std::integral_constant<int, 32>{});
+    else go_cb(split_tag, tw_tag, std::integral_constant<int, 8>{});
+  };
+  auto go = [&](auto split_tag) {
+    if (TW == 32) go_tw(split_tag, std::integral_constant<int, 32>{});
+    else if (TW == 16) go_tw(split_tag, std::integral_constant<int, 16>{});
+    else go_tw(split_tag, std::integral_constant<int, 8>{});
   };
   if (split) go(std::true_type{});
   else go(std::false_type{});
