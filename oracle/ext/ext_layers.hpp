@@ -78,6 +78,8 @@ class PoolingLayer final : public ExtLayer {
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   const std::vector<int>& mask() const { return mask_; }
+  // test hook: replace the argmax decisions of the last forward (oracle-fed parity)
+  void set_mask(const int* m) { std::copy(m, m + mask_.size(), mask_.begin()); }
 
  private:
   PoolParam p_;

@@ -228,6 +228,17 @@ ORC_API int orc_pool_mask(void* net, const char* layer, int* out, uint64_t n) {
   });
 }
 
+ORC_API int orc_set_pool_mask(void* net, const char* layer, const int* in, uint64_t n) {
+  return guard([&] {
+    auto* on = static_cast<OrcNet*>(net);
+    if (!on->ext) throw polegrad::ModelError("set_pool_mask: reference nets have no pooling");
+    auto* pl = dynamic_cast<oracle::PoolingLayer*>(on->ext->layer(layer));
+    if (!pl) throw polegrad::NotFound(std::string("no pooling layer ") + layer);
+    if (n < pl->mask().size()) throw polegrad::InvalidArgument("set_pool_mask: buffer too small");
+    pl->set_mask(in);
+  });
+}
+
 // method 0 = SGD, 1 = RMSProp.  Plain SGD / RMSProp on a reference net runs the
 // unmodified polegrad::Solver; momentum / weight decay use the ExtSolver.
 ORC_API int orc_solver_create(void* net, int method, double lr, double mom, double wd, double decay, double eps,

@@ -51,6 +51,7 @@ def load(dtype: str = "f64") -> C.CDLL:
             "orc_param_get": ([vp, i, i, pd], i), "orc_param_set": ([vp, i, i, pd], i),
             "orc_snapshot": ([vp, vp, u64, C.POINTER(u64)], i), "orc_restore": ([vp, vp, u64], i),
             "orc_pool_mask": ([vp, cp, C.POINTER(C.c_int), u64], i),
+            "orc_set_pool_mask": ([vp, cp, C.POINTER(C.c_int), u64], i),
             "orc_solver_create": ([vp, i, d, d, d, d, d, C.POINTER(vp)], i),
             "orc_solver_apply": ([vp, vp], i), "orc_solver_free": ([vp], None),
             "orc_gemm": ([i, i, i, i, i, d, pd, pd, d, pd], i), "orc_xent_grad": ([pd, pd, i, pd], i),
@@ -270,6 +271,16 @@ class OracleNet:
         out = np.empty(n, np.int32)
         _check(self.lib, self.lib.orc_pool_mask(self.ptr, layer.encode(), out.ctypes.data_as(C.POINTER(C.c_int)), n))
         return out
+
+    def set_pool_mask(self, layer: str, mask: np.ndarray) -> None:
+        m = np.ascontiguousarray(mask, np.int32)
+        _check(self.lib, self.lib.orc_set_pool_mask(self.ptr, layer.encode(), m.ctypes.data_as(C.POINTER(C.c_int)),
+                                                    m.size))
+
+
+def layer_tops(text: str):
+    """(layer name, type, tops) in definition order (test helper)."""
+    return [(_get(l, "name"), _get(l, "type"), _all(l, "top")) for k, l in parse_blocks(text) if k == "layer"]
 
 
 class OracleSolver:

@@ -51,7 +51,34 @@ def data_shape(text: str):
     return tuple(info["data"][2]), len(info["data"][1]) == 2
 
 
-def lockstep(config: str, dtype: str, iters: int = 10, seed: int = 1, resync_weights: bool = False):
+def feed_forward_state(text: str, net, orc) -> dict:
+    """Oracle-fed backward: copy the B200 forward state (every layer top and
+    the MAX-pool argmax masks) into the oracle so both backward passes start
+    from identical activations and routing decisions.  Returns how many
+    pooling-mask entries / ReLU gates differed before the copy (near-tie flips)."""
+    flips = {"pool": 0, "relu": 0, "elements": 0}
+    for name, ltype, tops in pyoracle.layer_tops(text):
+        if ltype in ("MemoryData", "SoftmaxWithLoss", "MemoryLoss"):
+            continue
+        for top in tops:
+            mine = net.blob(top).astype(np.float64)
+            if ltype == "ReLU":
+                flips["relu"] += int(np.count_nonzero((mine > 0) != (orc.blob(top) > 0)))
+            orc.set_blob(top, mine)
+            flips["elements"] += mine.size
+        if ltype == "Pooling":
+            cnt = int(np.prod(net.blob_shape(tops[0])))
+            mask = net.pool_mask(name)[:cnt]
+            try:
+                flips["pool"] += int(np.count_nonzero(mask != orc.pool_mask(name, cnt)))
+                orc.set_pool_mask(name, mask)
+            except pyoracle.OracleError:
+                pass  # AVE pooling keeps no mask
+    return flips
+
+
+def lockstep(config: str, dtype: str, iters: int = 10, seed: int = 1, resync_weights: bool = False,
+             feed_forward: bool = False):
     """Train the B200 Net and the oracle side by side from identical weights
     and inputs; returns per-iteration losses/metrics and the final nets.
 
@@ -84,6 +111,7 @@ def lockstep(config: str, dtype: str, iters: int = 10, seed: int = 1, resync_wei
             net.forward()
             lo = orc.forward()
             l = net.loss()
+            flips = feed_forward_state(text, net, orc) if feed_forward else None
             net.backward()
             orc.backward()
         else:  # PG: inject policy-gradient diffs at the logits, backward_from (trainer.cpp:171-216)
@@ -98,10 +126,11 @@ def lockstep(config: str, dtype: str, iters: int = 10, seed: int = 1, resync_wei
             orc.backward_from("logits")
             l = float(np.sum(net.blob("prob")))
             lo = float(np.sum(orc.blob("prob")))
+            flips = None
         grads = [rel_l2(net.param(i, diff=True), orc.param(i, diff=True)) for i in range(len(net.param_info()))]
         solver.apply()
         osolver.apply()
-        hist.append({"loss": l, "oracle_loss": lo, "grad_rel": grads})
+        hist.append({"loss": l, "oracle_loss": lo, "grad_rel": grads, "flips": flips})
     weights = [rel_l2(net.param(i), orc.param(i)) for i in range(len(net.param_info()))]
     return {"net": net, "oracle": orc, "hist": hist, "weights_rel": weights, "init_bitexact": init_bitexact,
             "params": net.param_info()}

@@ -39,9 +39,13 @@ def test_ten_iterations_match_oracle(config, dtype):
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick"])
 def test_ten_iterations_gradients_on_synced_weights(config, dtype):
-    """Every iteration's gradients on identical inputs and weights (oracle
-    weights restored into the B200 net via MCWT before each step)."""
-    r = lockstep(config, dtype, iters=10, resync_weights=True)
+    """Every iteration's gradients on identical inputs, weights (oracle weights
+    restored into the B200 net via MCWT before each step) and forward state:
+    the B200 activations and argmax masks are fed into the oracle before its
+    backward, so one near-tie flip (~1e-7 rounding differences decide a
+    max-pool winner; one flip moves ~0.5% of a conv1 weight gradient) cannot
+    masquerade as a gradient error.  The number of such flips is bounded."""
+    r = lockstep(config, dtype, iters=10, resync_weights=True, feed_forward=True)
     tol = TOL[dtype]
     worst = 0.0
     for it, h in enumerate(r["hist"]):
@@ -49,7 +53,13 @@ def test_ten_iterations_gradients_on_synced_weights(config, dtype):
         for (name, _), e in zip(r["params"], h["grad_rel"]):
             worst = max(worst, e)
             assert e <= tol, (it, name, e)
-    print(config, dtype, "max grad rel (synced)", worst)
+        if h["flips"]:
+            f = h["flips"]
+            assert f["pool"] + f["relu"] <= max(2, f["elements"] // 100000), (it, f)
+            if dtype == "f64":
+                assert f["pool"] + f["relu"] == 0, (it, f)
+    print(config, dtype, "max grad rel (synced, oracle-fed)", worst,
+          "flips", [h["flips"] for h in r["hist"] if h["flips"]][:3])
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
