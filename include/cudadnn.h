@@ -271,6 +271,44 @@ CDNN_API int cdnn_softmax_loss_backward(cdnn_ctx ctx, cdnn_handle prob, cdnn_han
                                         cdnn_handle dx, int rows, int classes, int normalize,
                                         double loss_weight, cdnn_handle stream);
 
+/* ---- layers of configs 4-5 the reference lacks; Caffe semantics, NCHW,
+ * hw = H*W.  No reference interface to replace: these follow the Caffe layer contracts. */
+/* LRN ACROSS_CHANNELS: scale = k + alpha/size * sum_{window} x^2 ; y = x * scale^-beta.
+ * `scale` (n*c*hw) is kept for backward. local_size odd. */
+CDNN_API int cdnn_lrn_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale, int n,
+                              int c, int hw, int local_size, double alpha, double beta, double k,
+                              cdnn_handle stream);
+/* dx = dy*scale^-beta - 2*alpha*beta/size * x * sum_{window} dy*y/scale */
+CDNN_API int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale,
+                               cdnn_handle dy, cdnn_handle dx, int n, int c, int hw,
+                               int local_size, double alpha, double beta, cdnn_handle stream);
+/* Dropout (train): out[i] = in[i]/(1-ratio) if hash(seed, *counter, i) > ratio*2^32 else 0.
+ * The same call maps forward data and backward diffs (same seed + counter -> same mask).
+ * `counter` is an 8-byte device buffer (u64 iteration), read by the kernel so graph replays
+ * draw fresh masks once cdnn_counter_increment advances it. */
+CDNN_API int cdnn_dropout(cdnn_ctx ctx, cdnn_handle in, cdnn_handle out, uint64_t n, double ratio,
+                          uint64_t seed, cdnn_handle counter, cdnn_handle stream);
+CDNN_API int cdnn_counter_increment(cdnn_ctx ctx, cdnn_handle counter, cdnn_handle stream);
+/* BatchNorm, training statistics over (n, hw) per channel: y = (x - mean) * invstd,
+ * invstd = 1/sqrt(var + eps) (biased variance).  mean/invstd (c) kept for backward. */
+CDNN_API int cdnn_batchnorm_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle mean,
+                                    cdnn_handle invstd, int n, int c, int hw, double eps,
+                                    cdnn_handle stream);
+/* dx = (dy - mean(dy) - y*mean(dy*y)) * invstd ; scratch holds 2*c values */
+CDNN_API int cdnn_batchnorm_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle invstd, cdnn_handle dy,
+                                     cdnn_handle dx, cdnn_handle scratch, int n, int c, int hw,
+                                     cdnn_handle stream);
+/* Scale (per channel): y = x*gamma[c] (+ beta[c] when beta != 0) */
+CDNN_API int cdnn_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_handle beta,
+                                cdnn_handle y, int n, int c, int hw, cdnn_handle stream);
+/* dgamma += sum dy*x ; dbeta += sum dy ; dx = dy*gamma (each skipped when its handle is 0) */
+CDNN_API int cdnn_scale_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_handle dy,
+                                 cdnn_handle dgamma, cdnn_handle dbeta, cdnn_handle dx, int n,
+                                 int c, int hw, cdnn_handle stream);
+/* y = a*x (accumulate = 0) or y = a*x + b*y: Eltwise SUM terms and their backward */
+CDNN_API int cdnn_axpby(cdnn_ctx ctx, uint64_t n, double a, cdnn_handle x, double b, cdnn_handle y,
+                        int accumulate, cdnn_handle stream);
+
 /* ---- solver (solver.cpp:24-57 + Caffe momentum / weight decay) ----------- */
 typedef enum { CDNN_SOLVER_SGD = 0, CDNN_SOLVER_RMSPROP = 1 } cdnn_solver_method;
 /* One fused pass over n elements of (w, g, hist):

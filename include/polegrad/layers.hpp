@@ -42,6 +42,11 @@ enum class LayerType {
   kPooling,
   kSoftmaxWithLoss,
   kSplit,
+  kLRN,
+  kDropout,
+  kBatchNorm,
+  kScale,
+  kEltwise,
 };
 
 std::string_view to_string(LayerType type);
@@ -104,13 +109,21 @@ class Layer {
   bool propagate_down(std::size_t i) const { return i >= propagate_down_.size() || propagate_down_[i]; }
   // True when forward() may be captured into a CUDA graph (no host work).
   virtual bool graph_safe() const { return true; }
+  // B200: set by Net when a later layer rewrites this layer's top (top_clobbered)
+  // or its bottom 0 (bottom_clobbered, including this layer itself running in
+  // place) before backward reads it; layers whose backward needs that data keep
+  // a private copy (Caffe BatchNorm x_norm_, Scale temp_).
+  void set_clobbered(bool top, bool bottom) { top_clobbered_ = top; bottom_clobbered_ = bottom; }
 
  protected:
   LayerSpec spec_;
   std::vector<bool> propagate_down_;
+  bool top_clobbered_ = false, bottom_clobbered_ = false;
 };
 
 std::unique_ptr<Layer> make_layer(const LayerSpec& spec);
+// LRN / Dropout / BatchNorm / Scale / Eltwise from their prototxt param blocks.
+std::unique_ptr<Layer> make_caffe_layer(const LayerSpec& spec);
 
 // ---- reference layer set -------------------------------------------------------
 
@@ -309,6 +322,91 @@ class SplitLayer final : public Layer {
                            Rng& rng) override;
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+};
+
+// ---- configs 4-5 (AlexNet, ResNet-20), Caffe semantics -------------
+
+// LRN ACROSS_CHANNELS (lrn_param: local_size 5, alpha 1, beta 0.75, k 1 defaults).
+class LRNLayer final : public Layer {
+ public:
+  LRNLayer(LayerSpec spec, int size, double alpha, double beta, double k)
+      : Layer(std::move(spec)), size_(size), alpha_(alpha), beta_(beta), k_(k) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+
+ private:
+  int size_;
+  double alpha_, beta_, k_;
+  int n_ = 0, c_ = 0, hw_ = 0;
+  std::unique_ptr<Blob> scale_;
+};
+
+// Dropout (training): counter-hash mask (cdnn_dropout), seed drawn from the net
+// Rng at setup, device-side iteration counter advanced by every forward, so a
+// replayed CUDA graph draws a fresh mask each step.  In place allowed.
+class DropoutLayer final : public Layer {
+ public:
+  DropoutLayer(LayerSpec spec, double ratio) : Layer(std::move(spec)), ratio_(ratio) {}
+  ~DropoutLayer() override;
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+
+ private:
+  double ratio_;
+  std::uint64_t seed_ = 0;
+  std::shared_ptr<Registry> reg_;
+  cdnn_handle counter_ = 0;
+};
+
+// BatchNorm with mini-batch statistics (use_global_stats false); no affine part
+// (Caffe pairs it with Scale).  In place allowed.
+class BatchNormLayer final : public Layer {
+ public:
+  BatchNormLayer(LayerSpec spec, double eps) : Layer(std::move(spec)), eps_(eps) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+
+ private:
+  double eps_;
+  int n_ = 0, c_ = 0, hw_ = 0;
+  std::unique_ptr<Blob> mean_, invstd_, scratch_;
+  std::unique_ptr<Blob> xnorm_;  // private y when the top is rewritten later
+};
+
+// Scale along axis 1 with learnable gamma (filled with 1) and optional beta (0).
+class ScaleLayer final : public Layer {
+ public:
+  ScaleLayer(LayerSpec spec, bool bias) : Layer(std::move(spec)), bias_(bias) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  const std::vector<std::shared_ptr<Blob>>& params() const override { return params_; }
+
+ private:
+  bool bias_;
+  int n_ = 0, c_ = 0, hw_ = 0;
+  std::unique_ptr<Blob> x_;  // private input copy when in place / rewritten
+  std::vector<std::shared_ptr<Blob>> params_;
+};
+
+// Eltwise SUM with optional per-bottom coefficients.
+class EltwiseLayer final : public Layer {
+ public:
+  EltwiseLayer(LayerSpec spec, std::vector<double> coeff) : Layer(std::move(spec)), coeff_(std::move(coeff)) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottom_shapes, const std::shared_ptr<Registry>& registry,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+
+ private:
+  std::vector<double> coeff_;
 };
 
 // Cross-entropy gradient at a softmax output: probs - one-hot target

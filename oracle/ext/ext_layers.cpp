@@ -316,6 +316,231 @@ void SplitLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bo
 }
 
 // ---------------------------------------------------------------------------
+// LRN across channels (Caffe lrn_layer.cpp, restated per element).
+
+std::vector<Shape> LRNLayer::setup(const std::vector<Shape>& b, const std::shared_ptr<Registry>&, Rng&) {
+  one_bottom(spec_, b);
+  if (size_ < 1 || size_ % 2 == 0) throw ModelError("layer '" + spec_.name + "': LRN local_size must be odd");
+  N_ = b[0].n(); C_ = b[0].c(); HW_ = b[0].h() * b[0].w();
+  scale_.assign(b[0].count(), real(0));
+  return {b[0]};
+}
+
+void LRNLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
+  auto x = bottoms[0]->data();
+  auto y = tops[0]->data();
+  const int pre = (size_ - 1) / 2;
+  for (int n = 0; n < N_; ++n)
+    for (int c = 0; c < C_; ++c)
+      for (int i = 0; i < HW_; ++i) {
+        real s = 0;
+        for (int cc = std::max(c - pre, 0); cc < std::min(c - pre + size_, C_); ++cc) {
+          const real v = x[(std::size_t(n) * C_ + cc) * HW_ + i];
+          s += v * v;
+        }
+        const std::size_t at = (std::size_t(n) * C_ + c) * HW_ + i;
+        scale_[at] = real(k_) + real(alpha_) / real(size_) * s;
+        y[at] = x[at] * std::pow(scale_[at], real(-beta_));
+      }
+}
+
+void LRNLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  if (!propagate_down.empty() && !propagate_down[0]) return;
+  auto x = bottoms[0]->data();
+  auto y = tops[0]->data();
+  auto dy = tops[0]->diff();
+  auto dx = bottoms[0]->diff();
+  const int pre = (size_ - 1) / 2, post = size_ - 1 - pre;
+  for (int n = 0; n < N_; ++n)
+    for (int c = 0; c < C_; ++c)
+      for (int i = 0; i < HW_; ++i) {
+        real acc = 0;  // channels whose window contains c: c' in [c - post, c + pre]
+        for (int cc = std::max(c - post, 0); cc < std::min(c + pre + 1, C_); ++cc) {
+          const std::size_t j = (std::size_t(n) * C_ + cc) * HW_ + i;
+          acc += dy[j] * y[j] / scale_[j];
+        }
+        const std::size_t at = (std::size_t(n) * C_ + c) * HW_ + i;
+        dx[at] = dy[at] * std::pow(scale_[at], real(-beta_)) -
+                 real(2) * real(alpha_) * real(beta_) / real(size_) * x[at] * acc;
+      }
+}
+
+// ---------------------------------------------------------------------------
+// Dropout with a counter-based mask (see ext_layers.hpp).
+
+std::uint32_t DropoutLayer::hash(std::uint64_t seed, std::uint64_t iter, std::uint64_t idx) {
+  std::uint64_t z = seed * 0x9E3779B97F4A7C15ull ^ (iter + 1) * 0xBF58476D1CE4E5B9ull ^ (idx + 1) * 0x94D049BB133111EBull;
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return std::uint32_t(z >> 32);
+}
+
+bool DropoutLayer::keep(std::size_t i) const {
+  const auto thr = std::uint32_t(std::min(4294967295.0, ratio_ * 4294967296.0));
+  return hash(seed_, iter_, i) > thr;
+}
+
+std::vector<Shape> DropoutLayer::setup(const std::vector<Shape>& b, const std::shared_ptr<Registry>&, Rng& rng) {
+  one_bottom(spec_, b);
+  if (!(ratio_ >= 0.0 && ratio_ < 1.0)) throw ModelError("layer '" + spec_.name + "': dropout_ratio must be in [0, 1)");
+  seed_ = rng.next_u64();
+  return {b[0]};
+}
+
+void DropoutLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
+  ++iter_;
+  auto x = bottoms[0]->data();
+  auto y = tops[0]->data();
+  const real scale = real(1.0 / (1.0 - ratio_));
+  for (std::size_t i = 0; i < x.size(); ++i) y[i] = keep(i) ? x[i] * scale : real(0);
+}
+
+void DropoutLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  if (!propagate_down.empty() && !propagate_down[0]) return;
+  auto dy = tops[0]->diff();
+  auto dx = bottoms[0]->diff();
+  const real scale = real(1.0 / (1.0 - ratio_));
+  for (std::size_t i = 0; i < dy.size(); ++i) dx[i] = keep(i) ? dy[i] * scale : real(0);
+}
+
+// ---------------------------------------------------------------------------
+// BatchNorm, training statistics (two-pass mean / biased variance in double).
+
+std::vector<Shape> BatchNormLayer::setup(const std::vector<Shape>& b, const std::shared_ptr<Registry>&, Rng&) {
+  one_bottom(spec_, b);
+  N_ = b[0].n(); C_ = b[0].c(); HW_ = b[0].h() * b[0].w();
+  xnorm_.assign(b[0].count(), real(0));
+  invstd_.assign(std::size_t(C_), real(0));
+  return {b[0]};
+}
+
+void BatchNormLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
+  auto x = bottoms[0]->data();
+  auto y = tops[0]->data();
+  const double cnt = double(N_) * HW_;
+  for (int c = 0; c < C_; ++c) {
+    double m = 0, v = 0;
+    for (int n = 0; n < N_; ++n)
+      for (int i = 0; i < HW_; ++i) m += double(x[(std::size_t(n) * C_ + c) * HW_ + i]);
+    m /= cnt;
+    for (int n = 0; n < N_; ++n)
+      for (int i = 0; i < HW_; ++i) {
+        const double d = double(x[(std::size_t(n) * C_ + c) * HW_ + i]) - m;
+        v += d * d;
+      }
+    v /= cnt;
+    const real mean = real(m);
+    invstd_[c] = real(1.0 / std::sqrt(v + eps_));
+    for (int n = 0; n < N_; ++n)
+      for (int i = 0; i < HW_; ++i) {
+        const std::size_t at = (std::size_t(n) * C_ + c) * HW_ + i;
+        xnorm_[at] = (x[at] - mean) * invstd_[c];
+      }
+  }
+  std::copy(xnorm_.begin(), xnorm_.end(), y.begin());
+}
+
+void BatchNormLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  if (!propagate_down.empty() && !propagate_down[0]) return;
+  auto dy = tops[0]->diff();
+  auto dx = bottoms[0]->diff();
+  const double cnt = double(N_) * HW_;
+  for (int c = 0; c < C_; ++c) {
+    double a = 0, b = 0;
+    for (int n = 0; n < N_; ++n)
+      for (int i = 0; i < HW_; ++i) {
+        const std::size_t at = (std::size_t(n) * C_ + c) * HW_ + i;
+        a += double(dy[at]);
+        b += double(dy[at]) * double(xnorm_[at]);
+      }
+    const real ma = real(a / cnt), mb = real(b / cnt);
+    for (int n = 0; n < N_; ++n)
+      for (int i = 0; i < HW_; ++i) {
+        const std::size_t at = (std::size_t(n) * C_ + c) * HW_ + i;
+        dx[at] = (dy[at] - ma - xnorm_[at] * mb) * invstd_[c];
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scale (per channel, learnable gamma / beta).
+
+std::vector<Shape> ScaleLayer::setup(const std::vector<Shape>& b, const std::shared_ptr<Registry>& reg, Rng&) {
+  one_bottom(spec_, b);
+  N_ = b[0].n(); C_ = b[0].c(); HW_ = b[0].h() * b[0].w();
+  params_.clear();
+  params_.push_back(std::make_shared<Blob>(reg, Shape{{1, 1, 1, C_}}, spec_.name + ".weight"));
+  for (real& v : params_[0]->data()) v = real(1);
+  if (bias_) params_.push_back(std::make_shared<Blob>(reg, Shape{{1, 1, 1, C_}}, spec_.name + ".bias"));
+  x_.assign(b[0].count(), real(0));
+  return {b[0]};
+}
+
+void ScaleLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
+  auto x = bottoms[0]->data();
+  std::copy(x.begin(), x.end(), x_.begin());
+  auto y = tops[0]->data();
+  auto g = params_[0]->data();
+  for (std::size_t i = 0; i < x_.size(); ++i) {
+    const std::size_t c = (i / HW_) % C_;
+    y[i] = x_[i] * g[c] + (bias_ ? params_[1]->data()[c] : real(0));
+  }
+}
+
+void ScaleLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  auto dy = tops[0]->diff();
+  auto g = params_[0]->data();
+  auto dg = params_[0]->diff();
+  std::vector<double> sg(C_, 0.0), sb(C_, 0.0);
+  for (std::size_t i = 0; i < x_.size(); ++i) {
+    const std::size_t c = (i / HW_) % C_;
+    sg[c] += double(dy[i]) * double(x_[i]);
+    sb[c] += double(dy[i]);
+  }
+  for (int c = 0; c < C_; ++c) dg[c] += real(sg[c]);
+  if (bias_) {
+    auto db = params_[1]->diff();
+    for (int c = 0; c < C_; ++c) db[c] += real(sb[c]);
+  }
+  if (!propagate_down.empty() && !propagate_down[0]) return;
+  auto dx = bottoms[0]->diff();
+  for (std::size_t i = 0; i < x_.size(); ++i) dx[i] = dy[i] * g[(i / HW_) % C_];
+}
+
+// ---------------------------------------------------------------------------
+// Eltwise SUM.
+
+std::vector<Shape> EltwiseLayer::setup(const std::vector<Shape>& b, const std::shared_ptr<Registry>&, Rng&) {
+  if (b.size() < 2) throw ModelError("layer '" + spec_.name + "': Eltwise takes at least two bottoms");
+  for (const Shape& s : b)
+    if (!(s == b[0])) throw ModelError("layer '" + spec_.name + "': Eltwise bottoms must have equal shapes");
+  if (coeff_.empty()) coeff_.assign(b.size(), 1.0);
+  if (coeff_.size() != b.size()) throw ModelError("layer '" + spec_.name + "': one coeff per bottom required");
+  return {b[0]};
+}
+
+void EltwiseLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
+  auto y = tops[0]->data();
+  for (std::size_t i = 0; i < y.size(); ++i) {
+    real s = real(coeff_[0]) * bottoms[0]->data()[i];
+    for (std::size_t k = 1; k < bottoms.size(); ++k) s = real(coeff_[k]) * bottoms[k]->data()[i] + s;
+    y[i] = s;
+  }
+}
+
+void EltwiseLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  auto dy = tops[0]->diff();
+  for (std::size_t k = 0; k < bottoms.size(); ++k) {
+    if (!propagate_down.empty() && !propagate_down[k]) continue;
+    auto dx = bottoms[k]->diff();
+    for (std::size_t i = 0; i < dy.size(); ++i) dx[i] = real(coeff_[k]) * dy[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
 
 std::vector<Shape> LabelledDataLayer::setup(const std::vector<Shape>& b, const std::shared_ptr<Registry>&, Rng&) {
   if (!b.empty()) throw ModelError("layer '" + spec_.name + "': data layers take no bottoms");

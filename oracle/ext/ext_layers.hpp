@@ -111,6 +111,92 @@ class SplitLayer final : public ExtLayer {
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
 };
 
+// ---- configs 4-5 (AlexNet, ResNet-20) — Caffe layer semantics, plain loops ----------
+
+// LRN ACROSS_CHANNELS (Caffe lrn_layer.cpp CrossChannelForward/Backward_cpu):
+// scale = k + alpha/size * sum_{c' in [c-(size-1)/2, c+(size-1)/2]} x^2 ; y = x*scale^-beta
+class LRNLayer final : public ExtLayer {
+ public:
+  LRNLayer(LayerSpec spec, int size, double alpha, double beta, double k)
+      : ExtLayer(std::move(spec)), size_(size), alpha_(alpha), beta_(beta), k_(k) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottoms, const std::shared_ptr<Registry>& reg,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+
+ private:
+  int size_;
+  double alpha_, beta_, k_;
+  int N_ = 0, C_ = 0, HW_ = 0;
+  std::vector<real> scale_;
+};
+
+// Dropout (train phase): keep iff hash(seed, iteration, i) > ratio * 2^32, kept values
+// scaled by 1/(1-ratio).  The mask is a counter-based hash (same function as the CUDA
+// kernel, ops_layers.cu) so oracle and device draw identical masks; seed = one draw of the
+// net Rng at setup, iteration advanced at the start of every forward.
+class DropoutLayer final : public ExtLayer {
+ public:
+  DropoutLayer(LayerSpec spec, double ratio) : ExtLayer(std::move(spec)), ratio_(ratio) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottoms, const std::shared_ptr<Registry>& reg,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  static std::uint32_t hash(std::uint64_t seed, std::uint64_t iter, std::uint64_t idx);
+
+ private:
+  bool keep(std::size_t i) const;
+  double ratio_;
+  std::uint64_t seed_ = 0, iter_ = 0;
+};
+
+// BatchNorm with mini-batch statistics (use_global_stats false, Caffe batch_norm_layer.cpp):
+// y = (x - mean_c) / sqrt(var_c + eps), biased variance over (N, H, W).
+// Backward: dx = (dy - mean(dy) - y * mean(dy * y)) / sqrt(var + eps).
+class BatchNormLayer final : public ExtLayer {
+ public:
+  BatchNormLayer(LayerSpec spec, double eps) : ExtLayer(std::move(spec)), eps_(eps) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottoms, const std::shared_ptr<Registry>& reg,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+
+ private:
+  double eps_;
+  int N_ = 0, C_ = 0, HW_ = 0;
+  std::vector<real> xnorm_, invstd_;
+};
+
+// Scale (axis 1, one bottom): y = x * gamma_c (+ beta_c); gamma filled with 1, beta 0.
+class ScaleLayer final : public ExtLayer {
+ public:
+  ScaleLayer(LayerSpec spec, bool bias) : ExtLayer(std::move(spec)), bias_(bias) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottoms, const std::shared_ptr<Registry>& reg,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  const std::vector<std::shared_ptr<Blob>>& params() const override { return params_; }
+
+ private:
+  bool bias_;
+  int N_ = 0, C_ = 0, HW_ = 0;
+  std::vector<real> x_;  // input copy (in-place support, as Caffe's temp_)
+  std::vector<std::shared_ptr<Blob>> params_;
+};
+
+// Eltwise SUM: y = sum_i coeff_i * x_i ; dx_i = coeff_i * dy.
+class EltwiseLayer final : public ExtLayer {
+ public:
+  EltwiseLayer(LayerSpec spec, std::vector<double> coeff) : ExtLayer(std::move(spec)), coeff_(std::move(coeff)) {}
+  std::vector<Shape> setup(const std::vector<Shape>& bottoms, const std::shared_ptr<Registry>& reg,
+                           Rng& rng) override;
+  void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
+  void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+
+ private:
+  std::vector<double> coeff_;
+};
+
 // Labelled batch feed: tops {data, label}; one whole batch per forward.
 class LabelledDataLayer final : public ExtLayer {
  public:

@@ -18,7 +18,9 @@ using polegrad::NotFound;
 
 namespace {
 
-bool is_inplace_ok(const std::string& type) { return type == "ReLU" || type == "Sigmoid"; }
+bool is_inplace_ok(const std::string& type) {
+  return type == "ReLU" || type == "Sigmoid" || type == "Dropout" || type == "BatchNorm" || type == "Scale";
+}
 
 // Caffe InsertSplits: a blob version read by more than one layer gets a Split
 // layer right after its producer and each reader gets its own copy.
@@ -131,6 +133,27 @@ std::unique_ptr<polegrad::Layer> make(const LayerDef& d) {
     return std::make_unique<SoftmaxWithLossLayer>(spec_of(d, LayerType::kInnerProduct), d.get("normalize", 1) != 0);
   }
   if (d.type == "Split") return std::make_unique<SplitLayer>(spec_of(d, LayerType::kInnerProduct));
+  if (d.type == "LRN") {
+    if (d.get("norm_region", 0) != 0) throw ModelError("layer '" + d.name + "': only ACROSS_CHANNELS LRN");
+    return std::make_unique<LRNLayer>(spec_of(d, LayerType::kInnerProduct), int(d.get("local_size", 5)),
+                                      d.get("alpha", 1.0), d.get("beta", 0.75), d.get("k", 1.0));
+  }
+  if (d.type == "Dropout")
+    return std::make_unique<DropoutLayer>(spec_of(d, LayerType::kInnerProduct), d.get("dropout_ratio", 0.5));
+  if (d.type == "BatchNorm") {
+    if (d.get("use_global_stats", 0) != 0) throw ModelError("layer '" + d.name + "': training BatchNorm only");
+    return std::make_unique<BatchNormLayer>(spec_of(d, LayerType::kInnerProduct), d.get("eps", 1e-5));
+  }
+  if (d.type == "Scale") {
+    if (d.bottoms.size() != 1) throw ModelError("layer '" + d.name + "': Scale takes one bottom");
+    return std::make_unique<ScaleLayer>(spec_of(d, LayerType::kInnerProduct), d.get("bias_term", 0) != 0);
+  }
+  if (d.type == "Eltwise") {
+    if (d.get("operation", 1) != 1) throw ModelError("layer '" + d.name + "': only Eltwise SUM");
+    std::vector<double> coeff;
+    for (int i = 0; d.p.count("coeff" + std::to_string(i)); ++i) coeff.push_back(d.get("coeff" + std::to_string(i), 1));
+    return std::make_unique<EltwiseLayer>(spec_of(d, LayerType::kInnerProduct), coeff);
+  }
   throw ModelError("layer '" + d.name + "': unknown layer type \"" + d.type + "\"");
 }
 

@@ -174,7 +174,32 @@ def to_spec(text: str) -> Tuple[str, Dict]:
             if _get(lp, "normalize") in ("false", "0"):
                 p["normalize"] = 0.0
             info["loss"] = tops[0] if tops else None
-        kv = ";".join(f"{k}={v!r}" for k, v in p.items())
+        elif t == "LRN":
+            lp = _get(layer, "lrn_param", [])
+            for f in ("local_size", "alpha", "beta", "k"):
+                if _get(lp, f) is not None:
+                    p[f] = float(_get(lp, f))
+            if _get(lp, "norm_region") not in (None, "ACROSS_CHANNELS", "0"):
+                p["norm_region"] = 1.0
+        elif t == "Dropout":
+            dp = _get(layer, "dropout_param", [])
+            if _get(dp, "dropout_ratio") is not None:
+                p["dropout_ratio"] = float(_get(dp, "dropout_ratio"))
+        elif t == "BatchNorm":
+            bp = _get(layer, "batch_norm_param", [])
+            if _get(bp, "eps") is not None:
+                p["eps"] = float(_get(bp, "eps"))
+            if _get(bp, "use_global_stats") in ("true", "1"):
+                p["use_global_stats"] = 1.0
+        elif t == "Scale":
+            sp = _get(layer, "scale_param", [])
+            p["bias_term"] = 1.0 if _get(sp, "bias_term") in ("true", "1") else 0.0
+        elif t == "Eltwise":
+            ep = _get(layer, "eltwise_param", [])
+            p["operation"] = {"PROD": 0.0, "SUM": 1.0, "MAX": 2.0}.get(_get(ep, "operation", "SUM"), -1.0)
+            for i, c in enumerate(_all(ep, "coeff")):
+                p[f"coeff{i}"] = float(c)
+        kv =";".join(f"{k}={v!r}" for k, v in p.items())
         lines.append(f"{t}|{name}|{','.join(bottoms)}|{','.join(tops)}|{kv}")
     return "\n".join(lines) + "\n", info
 

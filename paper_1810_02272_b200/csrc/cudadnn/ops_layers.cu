@@ -1,0 +1,433 @@
+// ops_layers.cu — the remaining Caffe layers of the configs (absent from the
+// reference): LRN (AlexNet), Dropout (AlexNet), BatchNorm + Scale + Eltwise
+// (ResNet-20).  NCHW, one thread per element for the elementwise parts and one
+// block per channel (fixed-shape tree -> deterministic) for the reductions.
+//
+// Dropout draws its mask from a counter-based hash of (seed, iteration, index)
+// — identical on the CPU oracle and the GPU, recomputed in backward (no mask
+// buffer), and the iteration counter lives in device memory so a captured CUDA
+// graph draws a fresh mask on every replay.
+#include "launch.cuh"
+
+namespace cdnn {
+namespace {
+
+constexpr int kT = 256;
+
+template <typename T>
+T* P(const BufferSlot& b) { return reinterpret_cast<T*>(b.dev); }
+
+template <class F>
+void by_dtype(int dtype, const char* what, F&& f) {
+  if (dtype == CDNN_F32) f(float{});
+  else if (dtype == CDNN_F64) f(double{});
+  else fail(CDNN_INVALID_ARGUMENT, std::string(what) + ": floating buffers required");
+}
+
+int blocks(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, int64_t(kNumSMs) * 16))); }
+
+// ---- LRN (ACROSS_CHANNELS): scale = k + alpha/n * sum_{window} x^2 ; y = x * scale^-beta
+template <typename T>
+__global__ void lrn_fwd(const T* __restrict__ x, T* __restrict__ y, T* __restrict__ scale, int N, int C, int HW,
+                        int size, T alpha, T beta, T k) {
+  const int64_t total = int64_t(N) * C * HW;
+  const int pre = (size - 1) / 2;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int hw = int(i % HW);
+    const int c = int((i / HW) % C);
+    const int64_t base = (i / (int64_t(C) * HW)) * C * HW + hw;
+    T s = T(0);
+    const int c0 = max(c - pre, 0), c1 = min(c - pre + size, C);
+    for (int cc = c0; cc < c1; ++cc) {
+      const T v = x[base + int64_t(cc) * HW];
+      s += v * v;
+    }
+    const T sc = k + alpha / T(size) * s;
+    scale[i] = sc;
+    y[i] = x[i] * pow(sc, -beta);
+  }
+}
+
+// dx = dy * scale^-beta - 2*alpha*beta/n * x * sum_{window} dy*y/scale
+template <typename T>
+__global__ void lrn_bwd(const T* __restrict__ x, const T* __restrict__ y, const T* __restrict__ scale,
+                        const T* __restrict__ dy, T* __restrict__ dx, int N, int C, int HW, int size, T alpha, T beta) {
+  const int64_t total = int64_t(N) * C * HW;
+  const int post = size - 1 - (size - 1) / 2;  // channels whose window contains c
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int hw = int(i % HW);
+    const int c = int((i / HW) % C);
+    const int64_t base = (i / (int64_t(C) * HW)) * C * HW + hw;
+    T acc = T(0);
+    const int c0 = max(c - post, 0), c1 = min(c + (size - 1) / 2 + 1, C);
+    for (int cc = c0; cc < c1; ++cc) {
+      const int64_t j = base + int64_t(cc) * HW;
+      acc += dy[j] * y[j] / scale[j];
+    }
+    dx[i] = dy[i] * pow(scale[i], -beta) - T(2) * alpha * beta / T(size) * x[i] * acc;
+  }
+}
+
+// ---- Dropout --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t drop_hash(uint64_t seed, uint64_t iter, uint64_t idx) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull ^ (iter + 1) * 0xBF58476D1CE4E5B9ull ^ (idx + 1) * 0x94D049BB133111EBull;
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return uint32_t(z >> 32);
+}
+
+template <typename T>
+__global__ void dropout_kernel(const T* __restrict__ in, T* __restrict__ out, uint64_t n, uint32_t threshold, T scale,
+                               uint64_t seed, const unsigned long long* __restrict__ iter) {
+  const uint64_t it = *iter;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = drop_hash(seed, it, i) > threshold ? in[i] * scale : T(0);
+}
+
+__global__ void bump_kernel(unsigned long long* iter) { *iter += 1; }
+
+// ---- BatchNorm (training statistics), Scale, Eltwise ----------------------------------
+// one block per channel: mean, inv_std over (N, HW); fixed tree -> deterministic
+template <typename T>
+__global__ void bn_stats(const T* __restrict__ x, T* __restrict__ mean, T* __restrict__ invstd, int N, int C, int HW,
+                         T eps) {
+  __shared__ double sh[kT], sh2[kT];
+  const int c = blockIdx.x;
+  double s = 0, s2 = 0;
+  for (int n = 0; n < N; ++n) {
+    const T* p = x + (int64_t(n) * C + c) * HW;
+    for (int i = threadIdx.x; i < HW; i += blockDim.x) {
+      const double v = double(p[i]);
+      s += v;
+      s2 += v * v;
+    }
+  }
+  sh[threadIdx.x] = s;
+  sh2[threadIdx.x] = s2;
+  __syncthreads();
+  for (int w = kT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) { sh[threadIdx.x] += sh[threadIdx.x + w]; sh2[threadIdx.x] += sh2[threadIdx.x + w]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double cnt = double(N) * HW;
+    const double m = sh[0] / cnt;
+    const double var = sh2[0] / cnt - m * m;
+    mean[c] = T(m);
+    invstd[c] = T(1.0 / sqrt(var + double(eps)));
+  }
+}
+
+template <typename T>
+__global__ void bn_apply(const T* __restrict__ x, const T* __restrict__ mean, const T* __restrict__ invstd,
+                         T* __restrict__ y, int C, int HW, int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int((i / HW) % C);
+    y[i] = (x[i] - mean[c]) * invstd[c];
+  }
+}
+
+// per channel: a = mean(dy), b = mean(dy*y)
+template <typename T>
+__global__ void bn_bwd_stats(const T* __restrict__ y, const T* __restrict__ dy, T* __restrict__ a, T* __restrict__ b,
+                             int N, int C, int HW) {
+  __shared__ double sh[kT], sh2[kT];
+  const int c = blockIdx.x;
+  double s = 0, s2 = 0;
+  for (int n = 0; n < N; ++n) {
+    const int64_t off = (int64_t(n) * C + c) * HW;
+    for (int i = threadIdx.x; i < HW; i += blockDim.x) {
+      s += double(dy[off + i]);
+      s2 += double(dy[off + i]) * double(y[off + i]);
+    }
+  }
+  sh[threadIdx.x] = s;
+  sh2[threadIdx.x] = s2;
+  __syncthreads();
+  for (int w = kT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) { sh[threadIdx.x] += sh[threadIdx.x + w]; sh2[threadIdx.x] += sh2[threadIdx.x + w]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double cnt = double(N) * HW;
+    a[c] = T(sh[0] / cnt);
+    b[c] = T(sh2[0] / cnt);
+  }
+}
+
+// dx = (dy - a - y*b) * inv_std
+template <typename T>
+__global__ void bn_bwd_apply(const T* __restrict__ y, const T* __restrict__ dy, const T* __restrict__ a,
+                             const T* __restrict__ b, const T* __restrict__ invstd, T* __restrict__ dx, int C, int HW,
+                             int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int((i / HW) % C);
+    dx[i] = (dy[i] - a[c] - y[i] * b[c]) * invstd[c];
+  }
+}
+
+template <typename T>
+__global__ void scale_fwd(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ bta,
+                          T* __restrict__ y, int C, int HW, int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int((i / HW) % C);
+    y[i] = x[i] * g[c] + (bta ? bta[c] : T(0));
+  }
+}
+
+// per channel: dgamma += sum dy*x ; dbeta += sum dy  (block per channel)
+template <typename T>
+__global__ void scale_bwd_params(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dg,
+                                 T* __restrict__ db, int N, int C, int HW) {
+  __shared__ double sh[kT], sh2[kT];
+  const int c = blockIdx.x;
+  double s = 0, s2 = 0;
+  for (int n = 0; n < N; ++n) {
+    const int64_t off = (int64_t(n) * C + c) * HW;
+    for (int i = threadIdx.x; i < HW; i += blockDim.x) {
+      s += double(dy[off + i]) * double(x[off + i]);
+      s2 += double(dy[off + i]);
+    }
+  }
+  sh[threadIdx.x] = s;
+  sh2[threadIdx.x] = s2;
+  __syncthreads();
+  for (int w = kT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) { sh[threadIdx.x] += sh[threadIdx.x + w]; sh2[threadIdx.x] += sh2[threadIdx.x + w]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (dg) dg[c] += T(sh[0]);
+    if (db) db[c] += T(sh2[0]);
+  }
+}
+
+template <typename T>
+__global__ void scale_bwd_data(const T* __restrict__ dy, const T* __restrict__ g, T* __restrict__ dx, int C, int HW,
+                               int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x)
+    dx[i] = dy[i] * g[(i / HW) % C];
+}
+
+template <typename T>
+__global__ void axpby_kernel(const T* __restrict__ x, T* __restrict__ y, uint64_t n, T a, T b, bool read_y) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    y[i] = read_y ? a * x[i] + b * y[i] : a * x[i];
+}
+
+}  // namespace
+}  // namespace cdnn
+
+using namespace cdnn;
+
+extern "C" {
+
+int cdnn_lrn_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale, int n, int c, int hw,
+                     int local_size, double alpha, double beta, double k, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    if (n < 1 || c < 1 || hw < 1 || local_size < 1 || local_size % 2 == 0)
+      fail(CDNN_INVALID_ARGUMENT, "lrn: bad extents or even local_size");
+    BufferSlot& X = buffer(cx, x, "lrn x");
+    BufferSlot& Y = buffer(cx, y, "lrn y");
+    BufferSlot& S = buffer(cx, scale, "lrn scale");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    for (BufferSlot* b : {&X, &Y, &S}) { require_len(*b, cnt, "lrn"); require_dtype(*b, X.dtype, "lrn"); }
+    DeviceGuard g(cx);
+    by_dtype(X.dtype, "lrn", [&](auto tag) {
+      using T = decltype(tag);
+      lrn_fwd<T><<<blocks(int64_t(cnt)), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), n, c, hw,
+                                                                        local_size, T(alpha), T(beta), T(k));
+    });
+    check_launch("lrn_fwd");
+    count_launch(cx);
+  });
+}
+
+int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale, cdnn_handle dy, cdnn_handle dx,
+                      int n, int c, int hw, int local_size, double alpha, double beta, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& X = buffer(cx, x, "lrn_bwd x");
+    BufferSlot& Y = buffer(cx, y, "lrn_bwd y");
+    BufferSlot& S = buffer(cx, scale, "lrn_bwd scale");
+    BufferSlot& DY = buffer(cx, dy, "lrn_bwd dy");
+    BufferSlot& DX = buffer(cx, dx, "lrn_bwd dx");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    for (BufferSlot* b : {&X, &Y, &S, &DY, &DX}) { require_len(*b, cnt, "lrn_bwd"); require_dtype(*b, X.dtype, "lrn_bwd"); }
+    DeviceGuard g(cx);
+    by_dtype(X.dtype, "lrn_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      lrn_bwd<T><<<blocks(int64_t(cnt)), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX),
+                                                                        n, c, hw, local_size, T(alpha), T(beta));
+    });
+    check_launch("lrn_bwd");
+    count_launch(cx);
+  });
+}
+
+int cdnn_dropout(cdnn_ctx ctx, cdnn_handle in, cdnn_handle out, uint64_t n, double ratio, uint64_t seed,
+                 cdnn_handle counter, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    if (!(ratio >= 0.0 && ratio < 1.0)) fail(CDNN_INVALID_ARGUMENT, "dropout: ratio must be in [0, 1)");
+    BufferSlot& I = buffer(cx, in, "dropout in");
+    BufferSlot& O = buffer(cx, out, "dropout out");
+    BufferSlot& K = buffer(cx, counter, "dropout counter");
+    require_len(I, n, "dropout");
+    require_len(O, n, "dropout");
+    require_dtype(O, I.dtype, "dropout");
+    if (K.len * dtype_size(K.dtype) < 8) fail(CDNN_INVALID_ARGUMENT, "dropout: counter buffer needs 8 bytes");
+    DeviceGuard g(cx);
+    const uint32_t thr = uint32_t(std::min(4294967295.0, ratio * 4294967296.0));
+    by_dtype(I.dtype, "dropout", [&](auto tag) {
+      using T = decltype(tag);
+      dropout_kernel<T><<<blocks(int64_t(n)), kT, 0, stream_of(cx, stream)>>>(
+          P<T>(I), P<T>(O), n, thr, T(1.0 / (1.0 - ratio)), seed, reinterpret_cast<unsigned long long*>(K.dev));
+    });
+    check_launch("dropout");
+    count_launch(cx);
+  });
+}
+
+int cdnn_counter_increment(cdnn_ctx ctx, cdnn_handle counter, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& K = buffer(cx, counter, "counter");
+    if (K.len * dtype_size(K.dtype) < 8) fail(CDNN_INVALID_ARGUMENT, "counter buffer needs 8 bytes");
+    DeviceGuard g(cx);
+    bump_kernel<<<1, 1, 0, stream_of(cx, stream)>>>(reinterpret_cast<unsigned long long*>(K.dev));
+    check_launch("counter");
+    count_launch(cx);
+  });
+}
+
+int cdnn_batchnorm_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle mean, cdnn_handle invstd, int n,
+                           int c, int hw, double eps, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& X = buffer(cx, x, "bn x");
+    BufferSlot& Y = buffer(cx, y, "bn y");
+    BufferSlot& M = buffer(cx, mean, "bn mean");
+    BufferSlot& V = buffer(cx, invstd, "bn invstd");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    require_len(X, cnt, "bn"); require_len(Y, cnt, "bn"); require_len(M, uint64_t(c), "bn"); require_len(V, uint64_t(c), "bn");
+    for (BufferSlot* b : {&Y, &M, &V}) require_dtype(*b, X.dtype, "bn");
+    DeviceGuard g(cx);
+    cudaStream_t st = stream_of(cx, stream);
+    by_dtype(X.dtype, "bn", [&](auto tag) {
+      using T = decltype(tag);
+      bn_stats<T><<<c, kT, 0, st>>>(P<T>(X), P<T>(M), P<T>(V), n, c, hw, T(eps));
+      bn_apply<T><<<blocks(int64_t(cnt)), kT, 0, st>>>(P<T>(X), P<T>(M), P<T>(V), P<T>(Y), c, hw, int64_t(cnt));
+    });
+    check_launch("bn_fwd");
+    count_launch(cx, 2);
+  });
+}
+
+int cdnn_batchnorm_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle invstd, cdnn_handle dy, cdnn_handle dx,
+                            cdnn_handle scratch, int n, int c, int hw, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& Y = buffer(cx, y, "bn_bwd y");
+    BufferSlot& V = buffer(cx, invstd, "bn_bwd invstd");
+    BufferSlot& DY = buffer(cx, dy, "bn_bwd dy");
+    BufferSlot& DX = buffer(cx, dx, "bn_bwd dx");
+    BufferSlot& S = buffer(cx, scratch, "bn_bwd scratch");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    require_len(Y, cnt, "bn_bwd"); require_len(DY, cnt, "bn_bwd"); require_len(DX, cnt, "bn_bwd");
+    require_len(V, uint64_t(c), "bn_bwd"); require_len(S, 2 * uint64_t(c), "bn_bwd scratch");
+    for (BufferSlot* b : {&V, &DY, &DX, &S}) require_dtype(*b, Y.dtype, "bn_bwd");
+    DeviceGuard g(cx);
+    cudaStream_t st = stream_of(cx, stream);
+    by_dtype(Y.dtype, "bn_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      T* a = P<T>(S);
+      T* b = a + c;
+      bn_bwd_stats<T><<<c, kT, 0, st>>>(P<T>(Y), P<T>(DY), a, b, n, c, hw);
+      bn_bwd_apply<T><<<blocks(int64_t(cnt)), kT, 0, st>>>(P<T>(Y), P<T>(DY), a, b, P<T>(V), P<T>(DX), c, hw,
+                                                           int64_t(cnt));
+    });
+    check_launch("bn_bwd");
+    count_launch(cx, 2);
+  });
+}
+
+int cdnn_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_handle beta, cdnn_handle y, int n, int c,
+                       int hw, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& X = buffer(cx, x, "scale x");
+    BufferSlot& G = buffer(cx, gamma, "scale gamma");
+    BufferSlot* B = buffer_or_null(cx, beta, "scale beta");
+    BufferSlot& Y = buffer(cx, y, "scale y");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    require_len(X, cnt, "scale"); require_len(Y, cnt, "scale"); require_len(G, uint64_t(c), "scale");
+    if (B) { require_len(*B, uint64_t(c), "scale"); require_dtype(*B, X.dtype, "scale"); }
+    require_dtype(G, X.dtype, "scale"); require_dtype(Y, X.dtype, "scale");
+    DeviceGuard g(cx);
+    by_dtype(X.dtype, "scale", [&](auto tag) {
+      using T = decltype(tag);
+      scale_fwd<T><<<blocks(int64_t(cnt)), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(G), B ? P<T>(*B) : nullptr,
+                                                                          P<T>(Y), c, hw, int64_t(cnt));
+    });
+    check_launch("scale_fwd");
+    count_launch(cx);
+  });
+}
+
+int cdnn_scale_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_handle dy, cdnn_handle dgamma,
+                        cdnn_handle dbeta, cdnn_handle dx, int n, int c, int hw, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& X = buffer(cx, x, "scale_bwd x");
+    BufferSlot& G = buffer(cx, gamma, "scale_bwd gamma");
+    BufferSlot& DY = buffer(cx, dy, "scale_bwd dy");
+    BufferSlot* DG = buffer_or_null(cx, dgamma, "scale_bwd dgamma");
+    BufferSlot* DB = buffer_or_null(cx, dbeta, "scale_bwd dbeta");
+    BufferSlot* DX = buffer_or_null(cx, dx, "scale_bwd dx");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    require_len(X, cnt, "scale_bwd"); require_len(DY, cnt, "scale_bwd"); require_len(G, uint64_t(c), "scale_bwd");
+    if (DX) require_len(*DX, cnt, "scale_bwd dx");
+    DeviceGuard g(cx);
+    cudaStream_t st = stream_of(cx, stream);
+    by_dtype(X.dtype, "scale_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      if (DG || DB) {
+        scale_bwd_params<T><<<c, kT, 0, st>>>(P<T>(X), P<T>(DY), DG ? P<T>(*DG) : nullptr, DB ? P<T>(*DB) : nullptr, n,
+                                              c, hw);
+        count_launch(cx);
+      }
+      if (DX) {
+        scale_bwd_data<T><<<blocks(int64_t(cnt)), kT, 0, st>>>(P<T>(DY), P<T>(G), P<T>(*DX), c, hw, int64_t(cnt));
+        count_launch(cx);
+      }
+    });
+    check_launch("scale_bwd");
+  });
+}
+
+// y = a*x (+ b*y when accumulate): Eltwise SUM forward terms and backward copies
+int cdnn_axpby(cdnn_ctx ctx, uint64_t n, double a, cdnn_handle x, double b, cdnn_handle y, int accumulate,
+               cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& X = buffer(cx, x, "axpby x");
+    BufferSlot& Y = buffer(cx, y, "axpby y");
+    require_len(X, n, "axpby"); require_len(Y, n, "axpby"); require_dtype(Y, X.dtype, "axpby");
+    if (n == 0) return;
+    DeviceGuard g(cx);
+    by_dtype(X.dtype, "axpby", [&](auto tag) {
+      using T = decltype(tag);
+      axpby_kernel<T><<<blocks(int64_t(n)), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), n, T(a), T(b),
+                                                                           accumulate != 0);
+    });
+    check_launch("axpby");
+    count_launch(cx);
+  });
+}
+
+}  // extern "C"

@@ -34,6 +34,11 @@ std::string_view to_string(LayerType type) {
     case LayerType::kPooling: return "Pooling";
     case LayerType::kSoftmaxWithLoss: return "SoftmaxWithLoss";
     case LayerType::kSplit: return "Split";
+    case LayerType::kLRN: return "LRN";
+    case LayerType::kDropout: return "Dropout";
+    case LayerType::kBatchNorm: return "BatchNorm";
+    case LayerType::kScale: return "Scale";
+    case LayerType::kEltwise: return "Eltwise";
   }
   return "?";
 }
@@ -42,7 +47,8 @@ std::optional<LayerType> layer_type_from_string(std::string_view name) {
   static constexpr LayerType kReference[] = {LayerType::kInnerProduct, LayerType::kRelu, LayerType::kSigmoid,
                                              LayerType::kSoftmax, LayerType::kMemoryData, LayerType::kMemoryLoss};
   static constexpr LayerType kAdded[] = {LayerType::kConvolution, LayerType::kPooling, LayerType::kSoftmaxWithLoss,
-                                         LayerType::kSplit};
+                                         LayerType::kSplit,       LayerType::kLRN,     LayerType::kDropout,
+                                         LayerType::kBatchNorm,   LayerType::kScale,   LayerType::kEltwise};
   for (LayerType t : kReference)
     if (to_string(t) == name) return t;
   if (!reference_compat())
@@ -76,6 +82,7 @@ Arity arity_of(LayerType t) {
     case LayerType::kMemoryLoss: return {1, 1, 0, 0};
     case LayerType::kSoftmaxWithLoss: return {2, 2, 1, 1};
     case LayerType::kSplit: return {1, 1, 1, 64};
+    case LayerType::kEltwise: return {2, 64, 1, 1};
     default: return {1, 1, 1, 1};
   }
 }
@@ -117,6 +124,11 @@ std::unique_ptr<Layer> make_layer(const LayerSpec& spec) {
       return std::make_unique<SoftmaxWithLossLayer>(spec, normalize);
     }
     case LayerType::kSplit: return std::make_unique<SplitLayer>(spec);
+    case LayerType::kLRN:
+    case LayerType::kDropout:
+    case LayerType::kBatchNorm:
+    case LayerType::kScale:
+    case LayerType::kEltwise: return make_caffe_layer(spec);
   }
   throw ModelError("layer '" + spec.name + "': unhandled layer type");
 }

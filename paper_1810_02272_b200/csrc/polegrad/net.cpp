@@ -14,7 +14,10 @@ namespace polegrad {
 
 namespace {
 
-bool allows_in_place(LayerType t) { return t == LayerType::kRelu || t == LayerType::kSigmoid; }
+bool allows_in_place(LayerType t) {
+  return t == LayerType::kRelu || t == LayerType::kSigmoid || t == LayerType::kDropout || t == LayerType::kBatchNorm ||
+         t == LayerType::kScale;
+}
 
 // Caffe InsertSplits: each blob *version* read by more than one layer gets a
 // Split layer right after its producer and every reader its own copy (the
@@ -135,6 +138,21 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
   }
   for (const auto& blob : blobs_)
     if (!consumed.contains(blob->name())) output_names_.push_back(blob->name());
+
+  // In-place rewrites after a layer ran: which layers must keep private copies
+  // of data their backward reads (Caffe BatchNorm x_norm_, Scale temp_).
+  for (std::size_t i = 0; i < layers_.size(); ++i) {
+    auto rewritten_after = [&](const Blob* b) {
+      for (std::size_t j = i + 1; j < layers_.size(); ++j)
+        if (std::find(tops_[j].begin(), tops_[j].end(), b) != tops_[j].end() &&
+            std::find(bottoms_[j].begin(), bottoms_[j].end(), b) != bottoms_[j].end())
+          return true;
+      return false;
+    };
+    const bool top = !tops_[i].empty() && rewritten_after(tops_[i][0]);
+    const bool bottom = !bottoms_[i].empty() && rewritten_after(bottoms_[i][0]);
+    layers_[i]->set_clobbered(top, bottom);
+  }
 
   // Fuse InnerProduct + in-place ReLU: the ReLU runs in the GEMM epilogue.
   for (std::size_t i = 0; i + 1 < layers_.size(); ++i) {

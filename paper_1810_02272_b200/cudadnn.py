@@ -46,7 +46,9 @@ EXPORTS = [
     "cdnn_relu_backward", "cdnn_sigmoid_forward", "cdnn_sigmoid_backward", "cdnn_softmax_forward",
     "cdnn_softmax_backward", "cdnn_softmax_loss_forward", "cdnn_softmax_loss_backward", "cdnn_solver_apply",
     "cdnn_nccl_available", "cdnn_nccl_unique_id", "cdnn_nccl_comm_create", "cdnn_allreduce_sum",
-    "cdnn_broadcast",
+    "cdnn_broadcast", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_dropout", "cdnn_counter_increment",
+    "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
+    "cdnn_axpby",
 ]
 
 
@@ -125,6 +127,14 @@ def load() -> C.CDLL:
             "cdnn_nccl_available": ([C.POINTER(i)], i), "cdnn_nccl_unique_id": ([C.c_char_p], i),
             "cdnn_nccl_comm_create": ([vp, i, i, C.c_char_p, ph], i),
             "cdnn_allreduce_sum": ([vp, h, h, u64, u64, h], i), "cdnn_broadcast": ([vp, h, h, u64, i, h], i),
+            "cdnn_lrn_forward": ([vp, h, h, h, i, i, i, i, d, d, d, h], i),
+            "cdnn_lrn_backward": ([vp, h, h, h, h, h, i, i, i, i, d, d, h], i),
+            "cdnn_dropout": ([vp, h, h, u64, d, u64, h, h], i), "cdnn_counter_increment": ([vp, h, h], i),
+            "cdnn_batchnorm_forward": ([vp, h, h, h, h, i, i, i, d, h], i),
+            "cdnn_batchnorm_backward": ([vp, h, h, h, h, h, i, i, i, h], i),
+            "cdnn_scale_forward": ([vp, h, h, h, h, i, i, i, h], i),
+            "cdnn_scale_backward": ([vp, h, h, h, h, h, h, i, i, i, h], i),
+            "cdnn_axpby": ([vp, u64, d, h, d, h, i, h], i),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

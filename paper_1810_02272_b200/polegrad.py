@@ -112,9 +112,14 @@ def plan_buckets(offsets: List[int], counts: List[int], total: int, bucket_elems
     return [out[i] for i in range(n)], nb.value
 
 
-def load_model(name: str) -> str:
+def load_model(name: str, batch: Optional[int] = None) -> str:
+    """Prototxt text of a bundled model; `batch` rewrites the MemoryData batch_size."""
     with open(os.path.join(MODELS_DIR, name if name.endswith(".prototxt") else name + ".prototxt")) as f:
-        return f.read()
+        text = f.read()
+    if batch is not None:
+        import re
+        text = re.sub(r"batch_size:\s*\d+", f"batch_size: {int(batch)}", text, count=1)
+    return text
 
 
 class Net:

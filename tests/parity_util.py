@@ -20,10 +20,14 @@ from paper_1810_02272_b200 import polegrad  # noqa: E402
 TOL = {"f64": 1e-5, "f32": 2e-3}
 
 CONFIGS = {
-    # model, solver kwargs, classes
-    "lenet": ("lenet", dict(method="sgd", lr=0.01, momentum=0.9, weight_decay=5e-4), 10),
-    "cifar10_quick": ("cifar10_quick", dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=4e-3), 10),
-    "pg_mlp": ("pg_mlp", dict(method="rmsprop", lr=1e-3, rms_decay=0.99, epsilon=1e-8), 2),
+    # model, solver kwargs, classes, batch override (None = the prototxt's)
+    "lenet": ("lenet", dict(method="sgd", lr=0.01, momentum=0.9, weight_decay=5e-4), 10, None),
+    "cifar10_quick": ("cifar10_quick", dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=4e-3), 10, None),
+    "pg_mlp": ("pg_mlp", dict(method="rmsprop", lr=1e-3, rms_decay=0.99, epsilon=1e-8), 2, None),
+    # AlexNet at a reduced batch: the oracle's naive GEMM needs ~2 s per image-iteration
+    # (SURVEY §7 item 8); ResNet-20 at batch 16 (per-rank BN statistics over 16 images)
+    "alexnet": ("alexnet", dict(method="sgd", lr=0.01, momentum=0.9, weight_decay=5e-4), 1000, 2),
+    "resnet20": ("resnet20", dict(method="sgd", lr=0.1, momentum=0.9, weight_decay=1e-4), 10, 16),
 }
 
 
@@ -89,8 +93,8 @@ def lockstep(config: str, dtype: str, iters: int = 10, seed: int = 1, resync_wei
     trajectories amplify those flips in the gradients of the first layers
     (SURVEY §7.3 item 5), so gradient parity is asserted per iteration on
     synced weights, while losses and weights are asserted free-running."""
-    model, skw, classes = CONFIGS[config]
-    text = polegrad.load_model(model)
+    model, skw, classes, batch = CONFIGS[config]
+    text = polegrad.load_model(model, batch)
     shape, labelled = data_shape(text)
     net = polegrad.Net(text, seed=seed, dtype=dtype)
     orc = pyoracle.OracleNet(text, seed=seed, dtype=dtype)

@@ -200,3 +200,94 @@ def test_sgd_momentum_bit_exact(ctx, dtype):
     assert np.array_equal(ctx.read(hv), vv)
     assert np.array_equal(ctx.read(hw), ww)
     assert not ctx.read(hg).any()
+
+
+# ---- config 4-5 layers (LRN, Dropout, BatchNorm, Scale, Eltwise) vs torch fp64 -----------
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("n,c,h,w,size", [(2, 96, 13, 13, 5), (3, 7, 5, 4, 3), (1, 4, 1, 1, 5)])
+def test_lrn(ctx, dtype, n, c, h, w, size):
+    rng = np.random.default_rng(n * c + size)
+    dt = NP[dtype]
+    x = rng.uniform(-3, 3, (n, c, h, w)).astype(dt)
+    alpha, beta, k = 1e-2, 0.75, 1.0
+    xt = torch.from_numpy(x.astype(np.float64)).requires_grad_()
+    yt = torch.nn.functional.local_response_norm(xt, size, alpha=alpha, beta=beta, k=k)
+    dy = rng.uniform(-1, 1, yt.shape)
+    yt.backward(torch.from_numpy(dy))
+    hx, hy, hs = ctx.upload(x), ctx.alloc(x.size, dtype), ctx.alloc(x.size, dtype)
+    ctx.call("cdnn_lrn_forward", hx, hy, hs, n, c, h * w, size, alpha, beta, k, 0)
+    tol = 1e-6 if dtype == cd.F32 else 1e-13
+    assert rel_l2(ctx.read(hy), yt.detach().numpy()) <= tol
+    hdy, hdx = ctx.upload(dy.astype(dt)), ctx.alloc(x.size, dtype)
+    ctx.call("cdnn_lrn_backward", hx, hy, hs, hdy, hdx, n, c, h * w, size, alpha, beta, 0)
+    assert rel_l2(ctx.read(hdx), xt.grad.numpy()) <= tol * 10
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+def test_dropout_mask_matches_hash_and_advances(ctx, dtype):
+    from test_cpu_oracle_caffe import np_drop_hash
+    dt = NP[dtype]
+    n, ratio, seed = 100003, 0.5, 0x1234_5678_9ABC_DEF0
+    x = np.random.default_rng(1).uniform(0.5, 1.5, n).astype(dt)
+    hx, hy, hk = ctx.upload(x), ctx.alloc(n, dtype), ctx.alloc(1, cd.F64)
+    ctx.call("cdnn_fill", hk, 1, 0.0, 0)
+    thr = np.uint32(int(ratio * 2 ** 32))
+    for it in (0, 1, 2):
+        ctx.call("cdnn_dropout", hx, hy, n, ratio, seed, hk, 0)
+        keep = np_drop_hash(seed, it, np.arange(n)) > thr
+        y = ctx.read(hy)
+        assert np.array_equal(y != 0, keep)
+        assert np.array_equal(y[keep], (x[keep] * dt(1 / (1 - ratio))).astype(dt))
+        ctx.call("cdnn_counter_increment", hk, 0)
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("shape", [(128, 16, 32, 32), (8, 64, 8, 8), (3, 5, 1, 1)])
+def test_batchnorm(ctx, dtype, shape):
+    n, c, h, w = shape
+    rng = np.random.default_rng(c)
+    dt = NP[dtype]
+    x = (rng.standard_normal(shape) * 2 + 1).astype(dt)
+    xt = torch.from_numpy(x.astype(np.float64)).requires_grad_()
+    yt = torch.nn.functional.batch_norm(xt, None, None, training=True, eps=1e-5)
+    dy = rng.uniform(-1, 1, shape)
+    yt.backward(torch.from_numpy(dy))
+    hx, hy = ctx.upload(x), ctx.alloc(x.size, dtype)
+    hm, hv, hs = ctx.alloc(c, dtype), ctx.alloc(c, dtype), ctx.alloc(2 * c, dtype)
+    ctx.call("cdnn_batchnorm_forward", hx, hy, hm, hv, n, c, h * w, 1e-5, 0)
+    tol = 1e-5 if dtype == cd.F32 else 1e-12
+    assert rel_l2(ctx.read(hy), yt.detach().numpy()) <= tol
+    assert rel_l2(ctx.read(hm), x.astype(np.float64).mean(axis=(0, 2, 3))) <= tol
+    hdy, hdx = ctx.upload(dy.astype(dt)), ctx.alloc(x.size, dtype)
+    ctx.call("cdnn_batchnorm_backward", hy, hv, hdy, hdx, hs, n, c, h * w, 0)
+    assert rel_l2(ctx.read(hdx), xt.grad.numpy()) <= tol * 10
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("bias", [True, False])
+def test_scale_and_axpby(ctx, dtype, bias):
+    n, c, h, w = 16, 32, 8, 8
+    rng = np.random.default_rng(9)
+    dt = NP[dtype]
+    x = rng.standard_normal((n, c, h, w)).astype(dt)
+    g = rng.uniform(0.5, 1.5, c).astype(dt)
+    b = rng.uniform(-1, 1, c).astype(dt)
+    dy = rng.standard_normal((n, c, h, w)).astype(dt)
+    hx, hg, hb, hy = ctx.upload(x), ctx.upload(g), ctx.upload(b), ctx.alloc(x.size, dtype)
+    ctx.call("cdnn_scale_forward", hx, hg, hb if bias else 0, hy, n, c, h * w, 0)
+    want = x.astype(np.float64) * g[None, :, None, None] + (b[None, :, None, None] if bias else 0)
+    tol = 1e-6 if dtype == cd.F32 else 1e-14
+    assert rel_l2(ctx.read(hy), want) <= tol
+    dg0 = rng.standard_normal(c).astype(dt)  # gradients accumulate
+    hdy, hdg, hdb, hdx = ctx.upload(dy), ctx.upload(dg0), ctx.upload(np.zeros(c, dt)), ctx.alloc(x.size, dtype)
+    ctx.call("cdnn_scale_backward", hx, hg, hdy, hdg, hdb if bias else 0, hdx, n, c, h * w, 0)
+    d64 = dy.astype(np.float64)
+    assert rel_l2(ctx.read(hdg), dg0 + (d64 * x).sum(axis=(0, 2, 3))) <= tol
+    if bias:
+        assert rel_l2(ctx.read(hdb), d64.sum(axis=(0, 2, 3))) <= tol
+    assert rel_l2(ctx.read(hdx), d64 * g[None, :, None, None]) <= tol
+    # Eltwise SUM building block: y = 2*x ; y = -0.5*dy + 1*y
+    ctx.call("cdnn_axpby", x.size, 2.0, hx, 0.0, hy, 0, 0)
+    ctx.call("cdnn_axpby", x.size, -0.5, hdy, 1.0, hy, 1, 0)
+    assert rel_l2(ctx.read(hy), 2 * x.astype(np.float64) - 0.5 * d64) <= tol

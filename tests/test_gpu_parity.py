@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick"])
+@pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick", "alexnet", "resnet20"])
 def test_ten_iterations_match_oracle(config, dtype):
     """Free-running 10 iterations: losses every iteration and the weights after
     10 updates within tolerance (gradients too in FP64, where no near-tie flips)."""
@@ -37,7 +37,7 @@ def test_ten_iterations_match_oracle(config, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick"])
+@pytest.mark.parametrize("config", ["pg_mlp", "lenet", "cifar10_quick", "alexnet", "resnet20"])
 def test_ten_iterations_gradients_on_synced_weights(config, dtype):
     """Every iteration's gradients on identical inputs, weights (oracle weights
     restored into the B200 net via MCWT before each step) and forward state:
