@@ -14,25 +14,37 @@ namespace {
 
 struct PoolGeom {
   int N, C, H, W, PH, PW, kh, kw, sh, sw, ph, pw;
+  // 32-bit index decomposition without hardware division (SASS integer division
+  // is a ~20-instruction sequence; these kernels are issue-bound otherwise)
+  FastDiv divW, divHW, divPW, divPHW, divSH, divSW;
 };
 
+// (plane, h, w) of a flat NCHW index within planes of H x W
+struct Idx3 {
+  uint32_t plane, h, w;
+};
+__device__ __forceinline__ Idx3 split3(uint32_t i, const FastDiv& dhw, const FastDiv& dw, uint32_t HW, uint32_t W) {
+  const uint32_t plane = dhw.div(i);
+  const uint32_t r = i - plane * HW;
+  const uint32_t h = dw.div(r);
+  return {plane, h, r - h * W};
+}
+
 template <typename T>
-__global__ void max_pool_fwd(const T* __restrict__ x, T* __restrict__ y, int* __restrict__ mask, PoolGeom g) {
-  const int64_t total = int64_t(g.N) * g.C * g.PH * g.PW;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int pw = int(i % g.PW);
-    const int ph = int((i / g.PW) % g.PH);
-    const int64_t nc = i / (int64_t(g.PW) * g.PH);
-    int hs = ph * g.sh - g.ph, ws = pw * g.sw - g.pw;
+__global__ void __launch_bounds__(256) max_pool_fwd(const T* __restrict__ x, T* __restrict__ y, int* __restrict__ mask,
+                                                    PoolGeom g, uint32_t total) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, g.divPHW, g.divPW, uint32_t(g.PH * g.PW), uint32_t(g.PW));
+    int hs = int(q.h) * g.sh - g.ph, ws = int(q.w) * g.sw - g.pw;
     const int he = min(hs + g.kh, g.H), we = min(ws + g.kw, g.W);
     hs = max(hs, 0);
     ws = max(ws, 0);
-    const T* plane = x + nc * g.H * g.W;
+    const T* plane = x + size_t(q.plane) * uint32_t(g.H * g.W);
     T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
     int arg = -1;
     for (int h = hs; h < he; ++h)
       for (int w = ws; w < we; ++w) {
-        const T v = plane[h * g.W + w];
+        const T v = __ldg(plane + h * g.W + w);
         if (v > best) { best = v; arg = h * g.W + w; }
       }
     y[i] = best;
@@ -40,66 +52,65 @@ __global__ void max_pool_fwd(const T* __restrict__ x, T* __restrict__ y, int* __
   }
 }
 
+// gather: every bottom element sums the top diffs of the windows whose argmax is it
 template <typename T>
-__global__ void max_pool_bwd(const T* __restrict__ dy, const int* __restrict__ mask, T* __restrict__ dx, PoolGeom g) {
-  const int64_t total = int64_t(g.N) * g.C * g.H * g.W;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int w = int(i % g.W);
-    const int h = int((i / g.W) % g.H);
-    const int64_t nc = i / (int64_t(g.W) * g.H);
-    // windows [ph*sh - pad, +kh) that contain h
-    const int phs = (h + g.ph < g.kh) ? 0 : (h + g.ph - g.kh) / g.sh + 1;
-    const int phe = min((h + g.ph) / g.sh + 1, g.PH);
-    const int pws = (w + g.pw < g.kw) ? 0 : (w + g.pw - g.kw) / g.sw + 1;
-    const int pwe = min((w + g.pw) / g.sw + 1, g.PW);
-    const int me = h * g.W + w;
-    const int64_t base = nc * g.PH * g.PW;
+__global__ void __launch_bounds__(256) max_pool_bwd(const T* __restrict__ dy, const int* __restrict__ mask,
+                                                    T* __restrict__ dx, PoolGeom g, uint32_t total) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, g.divHW, g.divW, uint32_t(g.H * g.W), uint32_t(g.W));
+    const int h = int(q.h) + g.ph, w = int(q.w) + g.pw;
+    // windows [p*s - pad, +k) that contain the element
+    const int phs = h < g.kh ? 0 : int(g.divSH.div(uint32_t(h - g.kh))) + 1;
+    const int phe = min(int(g.divSH.div(uint32_t(h))) + 1, g.PH);
+    const int pws = w < g.kw ? 0 : int(g.divSW.div(uint32_t(w - g.kw))) + 1;
+    const int pwe = min(int(g.divSW.div(uint32_t(w))) + 1, g.PW);
+    const int me = int(q.h) * g.W + int(q.w);
+    const size_t base = size_t(q.plane) * uint32_t(g.PH * g.PW);
     T s = T(0);
     for (int ph = phs; ph < phe; ++ph)
-      for (int pw = pws; pw < pwe; ++pw)
-        if (mask[base + ph * g.PW + pw] == me) s += dy[base + ph * g.PW + pw];
+      for (int pw = pws; pw < pwe; ++pw) {
+        const size_t o = base + ph * g.PW + pw;
+        if (__ldg(mask + o) == me) s += __ldg(dy + o);
+      }
     dx[i] = s;
   }
 }
 
 template <typename T>
-__global__ void ave_pool_fwd(const T* __restrict__ x, T* __restrict__ y, PoolGeom g) {
-  const int64_t total = int64_t(g.N) * g.C * g.PH * g.PW;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int pw = int(i % g.PW);
-    const int ph = int((i / g.PW) % g.PH);
-    const int64_t nc = i / (int64_t(g.PW) * g.PH);
-    int hs = ph * g.sh - g.ph, ws = pw * g.sw - g.pw;
+__global__ void __launch_bounds__(256) ave_pool_fwd(const T* __restrict__ x, T* __restrict__ y, PoolGeom g,
+                                                    uint32_t total) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, g.divPHW, g.divPW, uint32_t(g.PH * g.PW), uint32_t(g.PW));
+    int hs = int(q.h) * g.sh - g.ph, ws = int(q.w) * g.sw - g.pw;
     int he = min(hs + g.kh, g.H + g.ph), we = min(ws + g.kw, g.W + g.pw);
     const int pool = (he - hs) * (we - ws);
     hs = max(hs, 0); ws = max(ws, 0);
     he = min(he, g.H); we = min(we, g.W);
-    const T* plane = x + nc * g.H * g.W;
+    const T* plane = x + size_t(q.plane) * uint32_t(g.H * g.W);
     T s = T(0);
     for (int h = hs; h < he; ++h)
-      for (int w = ws; w < we; ++w) s += plane[h * g.W + w];
+      for (int w = ws; w < we; ++w) s += __ldg(plane + h * g.W + w);
     y[i] = s / T(pool);
   }
 }
 
 template <typename T>
-__global__ void ave_pool_bwd(const T* __restrict__ dy, T* __restrict__ dx, PoolGeom g) {
-  const int64_t total = int64_t(g.N) * g.C * g.H * g.W;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int w = int(i % g.W) + g.pw;
-    const int h = int((i / g.W) % g.H) + g.ph;
-    const int64_t nc = i / (int64_t(g.W) * g.H);
-    const int phs = (h < g.kh) ? 0 : (h - g.kh) / g.sh + 1;
-    const int phe = min(h / g.sh + 1, g.PH);
-    const int pws = (w < g.kw) ? 0 : (w - g.kw) / g.sw + 1;
-    const int pwe = min(w / g.sw + 1, g.PW);
-    const int64_t base = nc * g.PH * g.PW;
+__global__ void __launch_bounds__(256) ave_pool_bwd(const T* __restrict__ dy, T* __restrict__ dx, PoolGeom g,
+                                                    uint32_t total) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, g.divHW, g.divW, uint32_t(g.H * g.W), uint32_t(g.W));
+    const int h = int(q.h) + g.ph, w = int(q.w) + g.pw;
+    const int phs = h < g.kh ? 0 : int(g.divSH.div(uint32_t(h - g.kh))) + 1;
+    const int phe = min(int(g.divSH.div(uint32_t(h))) + 1, g.PH);
+    const int pws = w < g.kw ? 0 : int(g.divSW.div(uint32_t(w - g.kw))) + 1;
+    const int pwe = min(int(g.divSW.div(uint32_t(w))) + 1, g.PW);
+    const size_t base = size_t(q.plane) * uint32_t(g.PH * g.PW);
     T s = T(0);
     for (int ph = phs; ph < phe; ++ph)
       for (int pw = pws; pw < pwe; ++pw) {
         const int hs = ph * g.sh - g.ph, ws = pw * g.sw - g.pw;
         const int he = min(hs + g.kh, g.H + g.ph), we = min(ws + g.kw, g.W + g.pw);
-        s += dy[base + ph * g.PW + pw] / T((he - hs) * (we - ws));
+        s += __ldg(dy + base + ph * g.PW + pw) / T((he - hs) * (we - ws));
       }
     dx[i] = s;
   }
@@ -107,7 +118,12 @@ __global__ void ave_pool_bwd(const T* __restrict__ dy, T* __restrict__ dx, PoolG
 
 PoolGeom geom_of(const PoolDescSlot& d) {
   const auto& p = d.p;
-  return PoolGeom{p.n, p.c, p.h, p.w, d.PH, d.PW, p.kernel_h, p.kernel_w, p.stride_h, p.stride_w, p.pad_h, p.pad_w};
+  PoolGeom g{p.n, p.c, p.h, p.w, d.PH, d.PW, p.kernel_h, p.kernel_w, p.stride_h, p.stride_w, p.pad_h, p.pad_w,
+             FastDiv(uint32_t(p.w)), FastDiv(uint32_t(p.h * p.w)), FastDiv(uint32_t(d.PW)),
+             FastDiv(uint32_t(d.PH * d.PW)), FastDiv(uint32_t(p.stride_h)), FastDiv(uint32_t(p.stride_w))};
+  if (uint64_t(p.n) * p.c * p.h * p.w >= (1ull << 31))
+    fail(CDNN_INVALID_ARGUMENT, "pool: tensors of 2^31 elements or more are not supported");
+  return g;
 }
 
 }  // namespace
@@ -138,9 +154,10 @@ int cdnn_pool_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle
       using T = decltype(tag);
       if (d.p.method == CDNN_POOL_MAX)
         max_pool_fwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(X.dev), reinterpret_cast<T*>(Y.dev),
-                                                 M ? reinterpret_cast<int*>(M->dev) : nullptr, g);
+                                                 M ? reinterpret_cast<int*>(M->dev) : nullptr, g, uint32_t(nout));
       else
-        ave_pool_fwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(X.dev), reinterpret_cast<T*>(Y.dev), g);
+        ave_pool_fwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(X.dev), reinterpret_cast<T*>(Y.dev), g,
+                                                 uint32_t(nout));
     };
     if (X.dtype == CDNN_F32) run(float{});
     else if (X.dtype == CDNN_F64) run(double{});
@@ -175,9 +192,10 @@ int cdnn_pool_backward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_hand
       using T = decltype(tag);
       if (d.p.method == CDNN_POOL_MAX)
         max_pool_bwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(DY.dev), reinterpret_cast<const int*>(M->dev),
-                                                 reinterpret_cast<T*>(DX.dev), g);
+                                                 reinterpret_cast<T*>(DX.dev), g, uint32_t(nin));
       else
-        ave_pool_bwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(DY.dev), reinterpret_cast<T*>(DX.dev), g);
+        ave_pool_bwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(DY.dev), reinterpret_cast<T*>(DX.dev), g,
+                                                 uint32_t(nin));
     };
     if (DY.dtype == CDNN_F32) run(float{});
     else if (DY.dtype == CDNN_F64) run(double{});
