@@ -1,0 +1,336 @@
+// conv_tap.cuh — "tap-shift" implicit-GEMM convolution on tcgen05 (stride 1,
+// any dilation, one group per launch), fp32 NCHW in/out, tf32 / 3xTF32 math.
+//
+//   out[img][n][p][q] = sum_{r,s,c} Wt[r*S+s][n][c] * in_pad[img][c][p + r*dh][q + s*dw]
+//
+// Forward:       in = x,  out = y,  Wt[tap][co][ci],          in_pad offset (ph, pw)
+// Backward-data: in = dy, out = dx,  Wt[tap][ci][co] flipped,  offset (dh(R-1)-ph, dw(S-1)-pw)
+//
+// Virtual pixel grid: every image is laid out as Hv x Wv rows (Hv = P + dh(R-1),
+// Wv = Q + dw(S-1)), row v = img*Hv*Wv + hp*Wv + wp holding the padded input
+// pixel (hp, wp).  Output pixel (p, q) is virtual row p*Wv + q, and the input
+// pixel its tap (r, s) reads is that row plus the constant r*dh*Wv + s*dw.  So
+// a tile stages the input rows [m0, m0 + 128 + halo) ONCE per 32-channel block
+// — channels-last, K-major, 128B-swizzled, split into tf32 hi/lo — and every
+// tap is the same smem tile with its UMMA descriptor start moved by whole
+// 128-byte rows (the 128B swizzle is address based, so arbitrary row offsets
+// are legal: profiles/dbg/umma_rowshift.cu).  The per-tap conversion work of
+// an im2col / window-staging design (R*S times the input) disappears; rows
+// whose (p, q) fall in the padding columns are computed and dropped by the
+// epilogue.  Weights arrive per (block, tap) by TMA, pre-split K-major.
+//
+// Persistent CTAs (one per SM) walk the tiles; every stage is pipelined
+// against the others: A tiles double-buffered, weights in an mbarrier ring,
+// two TMEM accumulators so the epilogue of tile i overlaps the MMAs of i+1.
+// Warp roles (320 threads): warp 0 TMA producer of the weights, warp 1 TMEM
+// owner + single-thread MMA issuer, warps 2-5 stage input tiles, warps 6-9
+// epilogue (TMEM -> registers -> coalesced NCHW stores, + bias).
+#pragma once
+
+#include <cstdint>
+
+#include "gemm_tc.cuh"
+#include "operands.cuh"
+#include "ptx.cuh"
+
+namespace cdnn {
+namespace tctap {
+
+constexpr int kThreads = 320;
+constexpr int kMaxStages = 16;
+
+struct TapArgs {
+  const float* in;
+  const float* bias;  // fwd only, may be null
+  float* out;
+  int N, Cin, Hin, Win;  // direct-conv input (x or dy) of this group
+  int Cout, P, Q;        // direct-conv output extents of this group
+  int R, S, dh, dw, oh, ow;
+  int Hv, Wv;            // virtual grid
+  int Mv;                // N * Hv * Wv
+  int rows;              // staged rows per tile (multiple of 8)
+  int cblocks;           // ceil(Cin / 32)
+  int wrows;             // rows per tap in the repacked weights
+  int n0_base;           // first repacked-weight row of this group
+  int tiles_m, tiles;    // m tiles, m tiles x n blocks
+  int in_cstride;        // channel stride of `in` (Hin*Win)
+  int64_t in_nstride;    // image stride of `in`
+  int64_t out_nstride;   // image stride of `out`
+  int nbuf, stages;      // A buffers (1|2), weight ring depth
+  FastDiv div_hwv, div_wv;
+  unsigned long long* trace;  // debug timeline (CDNN_TAP_TRACE), null in production
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// trace slots per CTA: 0 start, 1 setup done, 2+3*i: tile i {A staged, MMAs issued, epilogue done}
+constexpr int kTraceSlots = 32;
+#define TAP_TRACE(slot) \
+  do { if (a.trace && (slot) < kTraceSlots) a.trace[blockIdx.x * kTraceSlots + (slot)] = gtime(); } while (0)
+
+__host__ __device__ constexpr uint32_t b_stage_bytes(int bn, bool split) { return uint32_t(bn) * 128u * (split ? 2u : 1u); }
+__host__ __device__ constexpr uint32_t a_buf_bytes(int rows, bool split) { return uint32_t(rows) * 128u * (split ? 2u : 1u); }
+
+inline int smem_bytes(int rows, int nbuf, int stages, int bn, bool split) {
+  return 1024 + nbuf * int(a_buf_bytes(rows, split)) + stages * int(b_stage_bytes(bn, split)) +
+         (2 * kMaxStages + 8 + 1) * 8 + 16;
+}
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;              // LBO (unused for swizzled K-major) = 16 B
+  d |= uint64_t(1024 >> 4) << 32;      // SBO = 8 rows x 128 B
+  d |= uint64_t(1) << 46;              // descriptor version
+  d |= uint64_t(2) << 61;              // SWIZZLE_128B
+  return d;
+}
+
+// Stage 8 channels (two 16-byte granules) of one virtual row: hi (and lo) tf32.
+template <bool SPLIT>
+__device__ __forceinline__ void put_row8(uint32_t rbase, uint32_t lo_off, int row, int g8, const float (&x)[8]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int g4 = g8 * 2 + h;
+    const uint32_t off = rbase + (uint32_t((g4 ^ (row & 7)) & 7) << 4);
+    const float h0 = ptx::to_tf32(x[4 * h]), h1 = ptx::to_tf32(x[4 * h + 1]);
+    const float h2 = ptx::to_tf32(x[4 * h + 2]), h3 = ptx::to_tf32(x[4 * h + 3]);
+    ptx::st_shared_v4(off, h0, h1, h2, h3);
+    if constexpr (SPLIT)
+      ptx::st_shared_v4(off + lo_off, ptx::to_tf32(x[4 * h] - h0), ptx::to_tf32(x[4 * h + 1] - h1),
+                        ptx::to_tf32(x[4 * h + 2] - h2), ptx::to_tf32(x[4 * h + 3] - h3));
+  }
+}
+
+template <int BN, bool SPLIT>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_tap_kernel(const __grid_constant__ CUtensorMap tm_w_hi, const __grid_constant__ CUtensorMap tm_w_lo,
+                    const TapArgs a) {
+  constexpr uint32_t TMEM_COLS = tc::tmem_cols_for(2 * BN);
+  constexpr uint32_t B_STAGE = b_stage_bytes(BN, SPLIT);
+  constexpr uint32_t B_HALF = uint32_t(BN) * 128u;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t A_BUF = a_buf_bytes(a.rows, SPLIT), A_HALF = uint32_t(a.rows) * 128u;
+  uint8_t* abase = smem;
+  uint8_t* bbase = smem + a.nbuf * A_BUF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bbase + a.stages * B_STAGE);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* a_full = empty + kMaxStages;
+  uint64_t* a_empty = a_full + 2;
+  uint64_t* t_full = a_empty + 2;
+  uint64_t* t_empty = t_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int taps = a.R * a.S;
+  // Concurrent CTAs walk the taps from different starting points, so the 148
+  // weight streams hit different L2 lines instead of the same ones at once.
+  const int rot = int(blockIdx.x % uint32_t(taps));
+
+  if (threadIdx.x == 0) {
+    TAP_TRACE(0);
+    for (int s = 0; s < a.stages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&a_full[b], 4);
+      ptx::mbar_init(&a_empty[b], 1);
+      ptx::mbar_init(&t_full[b], 1);
+      ptx::mbar_init(&t_empty[b], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TAP_TRACE(1);
+
+  if (warp == 0) {
+    // ---------------- weights: TMA per (tile, channel block, tap) ----------------
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tm_w_hi);
+      if constexpr (SPLIT) ptx::tma_prefetch_desc(&tm_w_lo);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+        const int n0 = a.n0_base + (t / a.tiles_m) * BN;
+        for (int cb = 0; cb < a.cblocks; ++cb)
+          for (int it = 0; it < taps; ++it) {
+            const int tap = it + rot < taps ? it + rot : it + rot - taps;
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[stage], B_STAGE);
+            uint8_t* b = bbase + stage * B_STAGE;
+            ptx::tma_load_2d(b, &tm_w_hi, &full[stage], cb * 32, tap * a.wrows + n0);
+            if constexpr (SPLIT) ptx::tma_load_2d(b + B_HALF, &tm_w_lo, &full[stage], cb * 32, tap * a.wrows + n0);
+            if (++stage == a.stages) { stage = 0; phase ^= 1; }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::make_idesc_tf32(BN);  // A, B K-major
+      int stage = 0;
+      uint32_t phase = 0;
+      int aseq = 0, ts = 0;
+      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++ts) {
+        const int acc_buf = ts & 1;
+        if (ts >= 2) ptx::mbar_wait(&t_empty[acc_buf], uint32_t((ts >> 1) - 1) & 1u);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem + uint32_t(acc_buf * BN);
+        bool first = true;
+        for (int cb = 0; cb < a.cblocks; ++cb, ++aseq) {
+          const int buf = aseq % a.nbuf;
+          ptx::mbar_wait(&a_full[buf], uint32_t(aseq / a.nbuf) & 1u);
+          ptx::tc_fence_after();
+          const int nk8 = (min(32, a.Cin - cb * 32) + 7) >> 3;
+          // descriptors are built once; per MMA only the 16-byte-unit start
+          // address in the low word moves (smem < 256 KB: no carry out of 14 bits)
+          const uint64_t dA = desc_sw128(ptx::smem_u32(abase + buf * A_BUF));
+          const uint64_t dAl = dA + (A_HALF >> 4);
+          for (int it = 0; it < taps; ++it) {
+            const int tap = it + rot < taps ? it + rot : it + rot - taps;
+            const int r = tap / a.S, s = tap - r * a.S;
+            const uint64_t shift = uint64_t(r * a.dh * a.Wv + s * a.dw) * 8u;  // rows x 128 B in 16 B units
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint64_t dB = desc_sw128(ptx::smem_u32(bbase + stage * B_STAGE));
+            const uint64_t dBl = dB + (B_HALF >> 4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (j < nk8) {
+                const uint64_t kj = uint64_t(j) * 2u;  // +32 B per k8 step
+                uint32_t acc = first ? 0u : 1u;
+                if constexpr (SPLIT) {
+                  ptx::mma_tf32(d_tmem, dAl + shift + kj, dB + kj, idesc, acc);
+                  ptx::mma_tf32(d_tmem, dA + shift + kj, dBl + kj, idesc, 1u);
+                  acc = 1u;
+                }
+                ptx::mma_tf32(d_tmem, dA + shift + kj, dB + kj, idesc, acc);
+                first = false;
+              }
+            }
+            ptx::mma_commit(&empty[stage]);
+            if (++stage == a.stages) { stage = 0; phase ^= 1; }
+          }
+          ptx::mma_commit(&a_empty[buf]);
+        }
+        ptx::mma_commit(&t_full[acc_buf]);
+        TAP_TRACE(3 + 3 * ts);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    // ---------------- input tiles: channels-last, swizzled, hi/lo ----------------
+    const int tid = threadIdx.x - 64;
+    const int HWv = a.Hv * a.Wv;
+    int aseq = 0;
+    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+      const int m0 = (t % a.tiles_m) * 128;
+      for (int cb = 0; cb < a.cblocks; ++cb, ++aseq) {
+        const int buf = aseq % a.nbuf;
+        if (aseq >= a.nbuf) ptx::mbar_wait(&a_empty[buf], uint32_t(aseq / a.nbuf - 1) & 1u);
+        const int c0 = cb * 32;
+        const int kc = min(32, a.Cin - c0);
+        const int g8n = (kc + 7) >> 3;  // 8-channel groups the MMAs read
+        const uint32_t hi = ptx::smem_u32(abase + buf * A_BUF);
+        for (int row = tid; row < a.rows; row += 128) {
+          const int v = m0 + row;
+          bool inb = false;
+          const float* src = a.in;
+          if (v < a.Mv) {
+            const int img = int(a.div_hwv.div(uint32_t(v)));
+            const int rem = v - img * HWv;
+            const int hp = int(a.div_wv.div(uint32_t(rem)));
+            const int h = hp - a.oh, w = rem - hp * a.Wv - a.ow;
+            inb = h >= 0 && h < a.Hin && w >= 0 && w < a.Win;
+            src = a.in + int64_t(img) * a.in_nstride + int64_t(c0) * a.in_cstride + h * a.Win + w;
+          }
+          const uint32_t rbase = hi + uint32_t(row) * 128u;
+          if (g8n == 4 && kc == 32) {
+            // full block: issue all 32 loads before any conversion (latency hiding)
+            float x[4][8];
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[g8][e] = inb ? __ldg(src + int64_t(g8 * 8 + e) * a.in_cstride) : 0.f;
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) put_row8<SPLIT>(rbase, A_HALF, row, g8, x[g8]);
+          } else {
+            for (int g8 = 0; g8 < g8n; ++g8) {
+              float x[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int c = g8 * 8 + e;
+                x[e] = (inb && c < kc) ? __ldg(src + int64_t(c) * a.in_cstride) : 0.f;
+              }
+              put_row8<SPLIT>(rbase, A_HALF, row, g8, x);
+            }
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&a_full[buf]);
+        if (tid == 0 && cb == a.cblocks - 1) TAP_TRACE(2 + 3 * (aseq / a.cblocks));
+      }
+    }
+  } else {
+    // ---------------- epilogue: TMEM lane m <-> virtual row m0 + m ----------------
+    const int q4 = warp & 3;  // TMEM lane quadrant this warp may access
+    const int HWv = a.Hv * a.Wv;
+    const int64_t PQ = int64_t(a.P) * a.Q;
+    int ts = 0;
+    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++ts) {
+      const int acc_buf = ts & 1;
+      const int m0 = (t % a.tiles_m) * 128;
+      const int nc0 = (t / a.tiles_m) * BN;  // output channel of TMEM column 0 (within the group)
+      ptx::mbar_wait(&t_full[acc_buf], uint32_t(ts >> 1) & 1u);
+      ptx::tc_fence_after();
+      const int v = m0 + q4 * 32 + lane;
+      const int img = int(a.div_hwv.div(uint32_t(v)));
+      const int rem = v - img * HWv;
+      const int p = int(a.div_wv.div(uint32_t(rem)));
+      const int q = rem - p * a.Wv;
+      const bool valid = v < a.Mv && p < a.P && q < a.Q;
+      float* outp = a.out + int64_t(img) * a.out_nstride + int64_t(p) * a.Q + q;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * BN + cc), r);
+        ptx::tmem_ld_wait();
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = nc0 + cc + j;
+            if (n < a.Cout) {
+              float o = __uint_as_float(r[j]);
+              if (a.bias) o += __ldg(a.bias + n);
+              outp[int64_t(n) * PQ] = o;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&t_empty[acc_buf]);
+      if (warp == 6 && lane == 0) TAP_TRACE(4 + 3 * ts);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+}  // namespace tctap
+}  // namespace cdnn

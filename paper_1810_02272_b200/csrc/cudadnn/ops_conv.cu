@@ -9,8 +9,11 @@
 // m is always the output's contiguous index, so epilogue stores coalesce.
 // Backward-filter accumulates into dw (param diffs accumulate, layers.hpp:84-86);
 // its bias gradient is a deterministic per-channel reduction.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
+#include "conv_tap.cuh"
 #include "conv_tma.cuh"
 #include "launch.cuh"
 
@@ -23,6 +26,168 @@ bool conv_tma_enabled() {
     return !(v && std::string(v) == "0");
   }();
   return on;
+}
+
+bool conv_tap_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CDNN_CONV_TAP");
+    return !(v && std::string(v) == "0");
+  }();
+  return on;
+}
+
+// Group-aware repack of W[Co][Cg][R][S] into the per-tap K-major operand, padded to
+// kpad channels, (hi, lo) TF32 split:
+//   forward : dst[tap][co][ci]      (ci within the group)
+//   backward: dst[tap][ci][co]      (co within ci's group), taps flipped
+__global__ void repack_tap_kernel(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int Co,
+                                  int C, int Cg, int Cog, int R, int S, int kpad, bool backward, bool split) {
+  const int rows = backward ? C : Co;
+  const int total = R * S * rows * kpad;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int k = i % kpad;
+    const int row = (i / kpad) % rows;
+    const int tap = i / (kpad * rows);
+    const int kr = tap / S, ks = tap % S;
+    float v = 0.f;
+    if (!backward) {
+      if (k < Cg) v = w[((row * Cg + k) * R + kr) * S + ks];
+    } else if (k < Cog) {
+      const int grp = row / Cg;
+      v = w[(((grp * Cog + k) * Cg + (row - grp * Cg)) * R + (R - 1 - kr)) * S + (S - 1 - ks)];
+    }
+    const float h = split ? ptx::to_tf32(v) : v;
+    hi[i] = h;
+    if (split) lo[i] = ptx::to_tf32(v - h);
+  }
+}
+
+template <int BN, bool SPLIT>
+void launch_conv_tap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const CUtensorMap& twh, const CUtensorMap& twl,
+                     const tctap::TapArgs& a) {
+  auto kern = tctap::conv_tap_kernel<BN, SPLIT>;
+  static int attr_smem[16] = {};
+  if (attr_smem[c->device & 15] < smem) {
+    CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_smem[c->device & 15] = smem;
+  }
+  static const bool trace = std::getenv("CDNN_TAP_TRACE") != nullptr;
+  if (!trace) {
+    kern<<<grid, tctap::kThreads, smem, st>>>(twh, twl, a);
+    check_launch("conv_tap_kernel");
+    count_launch(c);
+    return;
+  }
+  // debug timeline: per-CTA globaltimer stamps, printed as offsets from the earliest start
+  const size_t n = size_t(grid.x) * tctap::kTraceSlots;
+  unsigned long long* dbg = nullptr;
+  CDNN_CUDA(cudaMalloc(&dbg, n * 8));
+  CDNN_CUDA(cudaMemset(dbg, 0, n * 8));
+  tctap::TapArgs at = a;
+  at.trace = dbg;
+  CDNN_CUDA(cudaStreamSynchronize(st));
+  kern<<<grid, tctap::kThreads, smem, st>>>(twh, twl, at);
+  check_launch("conv_tap_kernel");
+  CDNN_CUDA(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> h(n);
+  CDNN_CUDA(cudaMemcpy(h.data(), dbg, n * 8, cudaMemcpyDeviceToHost));
+  cudaFree(dbg);
+  unsigned long long t0 = ~0ull;
+  for (unsigned i = 0; i < grid.x; ++i) t0 = std::min(t0, h[i * tctap::kTraceSlots]);
+  for (unsigned i = 0; i < grid.x; i += std::max(1u, grid.x / 6)) {
+    std::fprintf(stderr, "tap cta %3u:", i);
+    for (int s = 0; s < tctap::kTraceSlots; ++s) {
+      const unsigned long long v = h[i * tctap::kTraceSlots + s];
+      if (v) std::fprintf(stderr, " %d:%.2f", s, (v - t0) / 1000.0);
+    }
+    std::fprintf(stderr, "\n");
+  }
+  count_launch(c);
+}
+
+// Tap-shift implicit GEMM (conv_tap.cuh): stride 1, any dilation, any group count.
+// Returns false when the staged tile does not fit shared memory.
+bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const float* in, const float* w,
+              const float* bias, float* out, cdnn_handle stream) {
+  ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
+  const ConvGeom& g = d.geom;
+  if (!conv_tap_enabled() || g.sh != 1 || g.sw != 1) return false;
+  const int G = g.group;
+  const int Cin = backward_data ? g.Cog : g.Cg, Hin = backward_data ? g.P : g.H, Win = backward_data ? g.Q : g.W;
+  const int Cout = backward_data ? g.Cg : g.Cog, P = backward_data ? g.H : g.P, Q = backward_data ? g.W : g.Q;
+  const int CinT = backward_data ? g.Co : g.C, CoutT = backward_data ? g.C : g.Co;
+  const int oh = backward_data ? g.dh * (g.R - 1) - g.ph : g.ph, ow = backward_data ? g.dw * (g.S - 1) - g.pw : g.pw;
+  if (oh < 0 || ow < 0) return false;  // padding wider than the dilated kernel: not a plain shift
+  tctap::TapArgs a{};
+  a.N = g.N; a.Cin = Cin; a.Hin = Hin; a.Win = Win; a.Cout = Cout; a.P = P; a.Q = Q;
+  a.R = g.R; a.S = g.S; a.dh = g.dh; a.dw = g.dw; a.oh = oh; a.ow = ow;
+  a.Hv = P + g.dh * (g.R - 1);
+  a.Wv = Q + g.dw * (g.S - 1);
+  if (int64_t(g.N) * a.Hv * a.Wv >= (int64_t(1) << 31)) return false;
+  a.Mv = g.N * a.Hv * a.Wv;
+  a.rows = (128 + g.dh * (g.R - 1) * a.Wv + g.dw * (g.S - 1) + 7) & ~7;
+  a.cblocks = (Cin + 31) / 32;
+  a.in_cstride = Hin * Win;
+  a.in_nstride = int64_t(CinT) * Hin * Win;
+  a.out_nstride = int64_t(CoutT) * P * Q;
+  a.div_hwv = FastDiv(uint32_t(a.Hv * a.Wv));
+  a.div_wv = FastDiv(uint32_t(a.Wv));
+  const bool split = c->math_mode == CDNN_MATH_TF32X3;
+  const int tiles = (a.Mv + 127) / 128;
+  int bn = Cout <= 32 ? 32 : (Cout <= 64 ? 64 : 128);
+  if (bn > 32 && tiles * G * ((Cout + bn - 1) / bn) < kNumSMs) bn = bn == 128 ? 64 : 32;
+  // shared memory: A buffers (double-buffered over channel blocks when they fit) + B ring
+  constexpr int kBudget = 227 * 1024;
+  a.nbuf = 2;
+  auto fits = [&](int nbuf, int stages) { return tctap::smem_bytes(a.rows, nbuf, stages, bn, split) <= kBudget; };
+  if (!fits(a.nbuf, 2)) a.nbuf = 1;
+  if (!fits(a.nbuf, 2)) return false;
+  a.stages = 2;
+  while (a.stages < tctap::kMaxStages && fits(a.nbuf, a.stages + 1)) ++a.stages;
+  const int smem = tctap::smem_bytes(a.rows, a.nbuf, a.stages, bn, split);
+  // weights: repacked per call (they change every step), pre-split
+  const int kpad = a.cblocks * 32;
+  a.wrows = CoutT;
+  const int RS = g.R * g.S;
+  const size_t elems = size_t(RS) * CoutT * kpad;
+  const int slot = backward_data ? 2 : 0;
+  if (!d.repack[slot] || d.repack[slot]->bytes < elems * 4) {
+    d.repack[slot] = device_alloc_shared(elems * 4, c->device);
+    d.repack[slot + 1] = device_alloc_shared(elems * 4, c->device);
+  }
+  float* whi = static_cast<float*>(d.repack[slot]->ptr);
+  float* wlo = static_cast<float*>(d.repack[slot + 1]->ptr);
+  cudaStream_t st = stream_of(c, stream);
+  repack_tap_kernel<<<grid_for(int64_t(elems), 256), 256, 0, st>>>(w, whi, wlo, g.Co, g.C, g.Cg, g.Cog, g.R, g.S,
+                                                                   kpad, backward_data, split);
+  check_launch("repack_tap");
+  count_launch(c);
+  const uint64_t wdims[2] = {uint64_t(kpad), uint64_t(RS) * CoutT};
+  const uint64_t wstr[1] = {uint64_t(kpad)};
+  const uint32_t wbox[2] = {32u, uint32_t(bn)};
+  const CUtensorMap* twh = tmap_generic(c, whi, 2, wdims, wstr, wbox, 128);
+  const CUtensorMap* twl = tmap_generic(c, wlo, 2, wdims, wstr, wbox, 128);
+  a.tiles_m = tiles;
+  a.tiles = tiles * ((Cout + bn - 1) / bn);
+  dim3 grid(std::min(a.tiles, kNumSMs));  // persistent: one CTA per SM walks the tiles
+  for (int grp = 0; grp < G; ++grp) {
+    tctap::TapArgs ag = a;
+    ag.in = in + int64_t(grp) * Cin * Hin * Win;
+    ag.out = out + int64_t(grp) * Cout * P * Q;
+    ag.bias = bias ? bias + grp * Cout : nullptr;
+    ag.n0_base = grp * Cout;
+    auto go = [&](auto split_tag) {
+      constexpr bool SP = decltype(split_tag)::value;
+      switch (bn) {
+        case 32: launch_conv_tap<32, SP>(c, st, grid, smem, *twh, *twl, ag); break;
+        case 64: launch_conv_tap<64, SP>(c, st, grid, smem, *twh, *twl, ag); break;
+        default: launch_conv_tap<128, SP>(c, st, grid, smem, *twh, *twl, ag); break;
+      }
+    };
+    if (split) go(std::true_type{});
+    else go(std::false_type{});
+  }
+  return true;
 }
 
 template <int BN, bool SPLIT, int TW, int CB>
@@ -132,6 +297,9 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.P * g.Q, N = g.Cog, K = d.Kc;
   if constexpr (std::is_same_v<T, float>) {
+    if (conv_tap(c, d, false, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
+                 B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
+      return;
     if (conv_direct_tma(c, d, false, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
                         B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
       return;
@@ -161,6 +329,9 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.H * g.W, N = g.Cg, K = d.Kd;
   if constexpr (std::is_same_v<T, float>) {
+    if (conv_tap(c, d, true, reinterpret_cast<const float*>(DY.dev), reinterpret_cast<const float*>(Wt.dev), nullptr,
+                 reinterpret_cast<float*>(DX.dev), stream))
+      return;
     if (conv_direct_tma(c, d, true, reinterpret_cast<const float*>(DY.dev), reinterpret_cast<const float*>(Wt.dev),
                         nullptr, reinterpret_cast<float*>(DX.dev), stream))
       return;

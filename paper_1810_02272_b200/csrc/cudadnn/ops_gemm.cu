@@ -11,6 +11,12 @@
 
 namespace cdnn {
 
+// fp32 GEMMs up to this many multiply-adds take the SIMT engine (CDNN_SIMT_MACS overrides)
+const int64_t kSimtMaxMacs = [] {
+  const char* v = std::getenv("CDNN_SIMT_MACS");
+  return v ? std::atoll(v) : (int64_t(1) << 26);
+}();
+
 GemmPlan plan_tc(int M, int N, int K) {
   GemmPlan p;
   p.bn = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
@@ -32,8 +38,8 @@ GemmPlan plan_simt(int M, int N, int K) {
   const int tiles = ((M + simt::TBM - 1) / simt::TBM) * ((N + simt::TBN - 1) / simt::TBN);
   const int kt = (K + simt::TBK - 1) / simt::TBK;
   int splits = 1;
-  if (tiles < 2 * kNumSMs && kt >= 16) {
-    splits = std::min(kt / 8, (4 * kNumSMs + tiles - 1) / tiles);
+  if (tiles < 2 * kNumSMs && kt >= 4) {  // small grids: split K down to 2 slabs per CTA
+    splits = std::min(kt / 2, (2 * kNumSMs + tiles - 1) / tiles);
     splits = std::max(splits, 1);
   }
   p.kt_per_split = (kt + splits - 1) / splits;
@@ -48,6 +54,13 @@ static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const De
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
   if constexpr (std::is_same_v<T, float>) {
+    // Small contractions (the CIFAR / LeNet / PG InnerProducts) are latency
+    // bound: a tensor-core tile pipeline with a handful of CTAs loses to the
+    // exact-fp32 SIMT engine split wide over K.
+    if (int64_t(M) * N * K <= kSimtMaxMacs) {
+      run_simt<T>(c, st, ws, plan_simt(M, N, K), M, N, K, va, vb, epi);
+      return;
+    }
     const GemmPlan pl = plan_tc(M, N, K);
     TmaReq ra, rb;
     with_operand(c, va, tc::BM, ra, [&](const auto& a) {
@@ -75,13 +88,24 @@ static void gemm_t(Ctx* c, int ta, int tb, int m, int n, int k, double alpha, co
   dense_gemm<T>(c, stream, n, m, k, va, vb, epi);
 }
 
+// db[j] += sum_r dy[r][j] (layers.cpp:157-163): 32 columns x 8 row strands per
+// block, fixed-shape tree over the strands (deterministic), coalesced rows.
 template <typename T>
-__global__ void colsum_accum_kernel(const T* __restrict__ dy, T* __restrict__ db, int rows, int cols) {
-  // db[j] += sum_r dy[r][j]; rows summed in order (layers.cpp:157-163 loop order)
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
-    T s = T(0);
-    for (int r = 0; r < rows; ++r) s += dy[int64_t(r) * cols + j];
-    db[j] += s;
+__global__ void __launch_bounds__(256) colsum_accum_kernel(const T* __restrict__ dy, T* __restrict__ db, int rows,
+                                                           int cols) {
+  __shared__ T part[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
+  T s = T(0);
+  if (j < cols)
+    for (int r = ty; r < rows; r += 8) s += dy[int64_t(r) * cols + j];
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && j < cols) {
+    T t = part[0][tx];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += part[k][tx];
+    db[j] += t;
   }
 }
 
@@ -173,7 +197,7 @@ int cdnn_ip_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle w, cdnn_handle dy,
         dense_gemm<T>(c, stream, k, o, rows, va, vb, epi);
       }
       if (DB) {  // db += column sums of dY (layers.cpp:157-163)
-        colsum_accum_kernel<T><<<grid_for(o, 128), 128, 0, stream_of(c, stream)>>>(
+        colsum_accum_kernel<T><<<(o + 31) / 32, 256, 0, stream_of(c, stream)>>>(
             dyp, reinterpret_cast<T*>(DB->dev), rows, o);
         check_launch("colsum");
         count_launch(c);

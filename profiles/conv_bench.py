@@ -16,13 +16,19 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1810_02272_b200 import cudadnn as cd  # noqa: E402
 
 CASES = {
-    # name: n, c, h, w, co, k, stride, pad
+    # name: n, c, h, w, co, k, stride, pad[, group]
     "cq.conv1": (100, 3, 32, 32, 32, 5, 1, 2),
     "cq.conv2": (100, 32, 16, 16, 32, 5, 1, 2),
     "cq.conv3": (100, 32, 8, 8, 64, 5, 1, 2),
     "lenet.conv1": (64, 1, 28, 28, 20, 5, 1, 0),
     "lenet.conv2": (64, 20, 12, 12, 50, 5, 1, 0),
-    "alexnet.conv3": (32, 256, 13, 13, 384, 3, 1, 1),
+    "rn.stage1": (128, 16, 32, 32, 16, 3, 1, 1),
+    "rn.stage3": (128, 64, 8, 8, 64, 3, 1, 1),
+    "alexnet.conv1": (256, 3, 227, 227, 96, 11, 4, 0),
+    "alexnet.conv2": (256, 96, 27, 27, 256, 5, 1, 2, 2),
+    "alexnet.conv3": (256, 256, 13, 13, 384, 3, 1, 1),
+    "alexnet.conv4": (256, 384, 13, 13, 384, 3, 1, 1, 2),
+    "alexnet.conv5": (256, 384, 13, 13, 256, 3, 1, 1, 2),
 }
 
 
@@ -47,20 +53,22 @@ def main():
     ctx = cd.Context(0)
     ctx.call("cdnn_set_math_mode", cd.MATH_TF32X3 if args.math == "tf32x3" else cd.MATH_TF32)
     rng = np.random.default_rng(0)
-    for name, (n, c, h, w, co, k, s, p) in CASES.items():
+    for name, case in CASES.items():
+        n, c, h, w, co, k, s, p = case[:8]
+        g = case[8] if len(case) > 8 else 1
         if args.only and args.only not in name:
             continue
-        d = ctx.conv_desc(n, c, h, w, co, k, s, p)
+        d = ctx.conv_desc(n, c, h, w, co, k, s, p, 1, g)
         _, _, P, Q = ctx.conv_output_shape(d)
         x = ctx.upload(rng.uniform(-1, 1, n * c * h * w).astype(np.float32))
-        wt = ctx.upload(rng.uniform(-1, 1, co * c * k * k).astype(np.float32))
+        wt = ctx.upload(rng.uniform(-1, 1, co * c // g * k * k).astype(np.float32))
         b = ctx.upload(np.zeros(co, np.float32))
         y = ctx.alloc(n * co * P * Q, cd.F32)
         dy = ctx.upload(rng.uniform(-1, 1, n * co * P * Q).astype(np.float32))
         dx = ctx.alloc(n * c * h * w, cd.F32)
-        dw = ctx.alloc(co * c * k * k, cd.F32)
+        dw = ctx.alloc(co * c // g * k * k, cd.F32)
         db = ctx.alloc(co, cd.F32)
-        flops = 2.0 * n * P * Q * co * c * k * k
+        flops = 2.0 * n * P * Q * co * c // g * k * k
         ops = {
             "fwd": lambda: ctx.call("cdnn_conv_forward", d, x, wt, b, y, 0),
             "dgrad": lambda: ctx.call("cdnn_conv_backward_data", d, wt, dy, dx, 0),

@@ -98,6 +98,12 @@ CONV_CASES = [
     (2, 8, 13, 13, 12, 3, 1, 1, 1, 2),      # grouped
     (2, 16, 15, 15, 32, 3, 2, 1, 1, 1),     # ResNet downsample
     (2, 4, 9, 9, 8, 3, 1, 2, 2, 1),         # dilation
+    (2, 96, 13, 13, 64, 3, 1, 1, 1, 1),     # three 32-channel blocks (tap-shift kernel, double-buffered A)
+    (2, 48, 27, 27, 64, 5, 1, 2, 1, 2),     # AlexNet conv2 shape, grouped, 24 channels per group
+    (4, 16, 32, 32, 16, 3, 1, 1, 1, 1),     # ResNet-20 stage 1
+    (2, 64, 8, 8, 32, 1, 1, 0, 1, 1),       # 1x1
+    (1, 64, 13, 13, 256, 3, 1, 1, 1, 1),    # two 128-wide output blocks
+    (2, 8, 12, 10, 8, 3, 1, 0, 3, 1),       # dilation 3, no padding
 ]
 
 

@@ -16,8 +16,9 @@ from parity_util import TOL, float_vs_truth, lockstep, pyoracle, polegrad, rel_l
 
 pytestmark = pytest.mark.gpu
 
-# deep ReLU/BN nets whose float trajectories are chaotic (see parity_util.float_vs_truth)
-CHAOTIC = ("alexnet", "resnet20")
+# max-pool / deep ReLU-BN nets whose float trajectories are chaotic (see parity_util.float_vs_truth);
+# LeNet: one max-pool flip moves ~0.5% of the 20-element conv1 bias gradient
+CHAOTIC = ("lenet", "alexnet", "resnet20")
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
