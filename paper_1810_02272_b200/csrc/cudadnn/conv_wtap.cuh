@@ -1,0 +1,301 @@
+// conv_wtap.cuh — tap-shift backward-filter (weight gradient) on tcgen05 for
+// stride-1 convolutions, fp32 NCHW, tf32 / 3xTF32 math.
+//
+//   dW[co][c][r][s] = sum_v dY_v[v][co] * X_v[v + r*dh*Wv + s*dw][c]
+//
+// on the virtual pixel grid of conv_tap.cuh (v = img*Hv*Wv + p*Wv + q; dY_v is
+// zero on the padding rows/columns, X_v is the zero-padded input).  The GEMM
+// per kernel row r and group of four taps s0..s0+3 is
+//
+//   D[(j, c)][co] += sum_k X_v[k + r*dh*Wv + (s0+j)*dw][c] * dY_v[k][co]
+//
+// with the A operand MN-major (rows = virtual pixels, 128-byte rows of 32
+// channels, 128B_BASE32B swizzle) and its four 32-row M atoms placed a
+// constant number of rows apart (LBO): one MMA covers four taps of the same
+// staged tile (overlapping atoms, profiles/dbg/umma_m64.cu mode 1).  The host
+// packs the R x S taps into such groups along kernel rows (stride dw) and the
+// leftover columns along kernel columns (stride dh*Wv): 7 groups for 5x5.
+// B = dY^T is K-major.
+// Each CTA accumulates a contiguous range of virtual pixels (split-K) for one
+// 32-channel block, a set of kernel rows and a block of output channels, and
+// writes its partial dW (and the bias partial from the dY it staged) to
+// ws[split][co][m'] with m' = (r*S + s)*Cg + c (channel innermost, so a warp's
+// 32 TMEM lanes store one coalesced 128-byte row; m' = Kc for the bias); the
+// deterministic reduce_splits_kernel adds the splits and permutes m' into the
+// Caffe filter layout [co][c][r][s] while accumulating into dw / db.
+//
+// Warps (192 threads): warp 1 TMEM owner + MMA issuer, warps 2-5 stage the
+// pixel chunks (double-buffered) and run the epilogue, warp 0 idles.
+#pragma once
+
+#include <cstdint>
+
+#include "gemm_tc.cuh"
+#include "operands.cuh"
+#include "ptx.cuh"
+
+namespace cdnn {
+namespace tcwtap {
+
+constexpr int kThreads = 192;
+constexpr int KC = 64;  // virtual pixels per chunk (K per pipeline stage)
+constexpr int kMaxGroups = 32;
+
+// Four taps whose X rows sit a constant number of virtual rows apart (along a
+// kernel row: dw; along a kernel column: dh*Wv) form one MMA's M atoms.
+struct TapGroup {
+  int start;    // virtual-row offset of atom 0 (r*dh*Wv + s*dw)
+  int stride;   // rows between atoms
+  int tap[4];   // r*S + s per atom, -1 = unused atom
+};
+
+struct WtapArgs {
+  const float* x;   // bottom data, offset to the group's first channel
+  const float* dy;  // top diff, offset to the group's first channel
+  float* ws;        // partials [split][Cog][Kc + 1]
+  int N, Cg, H, W, Cog, P, Q, R, S, dh, dw, ph, pw;
+  int Hv, Wv, Mv;
+  int64_t x_nstride, dy_nstride;  // image strides (full tensors)
+  int Kc;                         // Cg * R * S
+  int cblocks, ggroups, coblocks;  // channel blocks, tap-group sets, co blocks
+  int ngroups;
+  TapGroup groups[kMaxGroups];
+  int gbegin[kMaxGroups + 1];      // tap-group set i = groups[gbegin[i], gbegin[i+1])
+  int rows_lo[kMaxGroups];         // per set: first staged row offset
+  int splits, chunks_per_split, nchunks;
+  int rowsA;                      // staged X rows per chunk (multiple of 8)
+  int want_bias;
+  FastDiv div_hwv, div_wv;
+};
+
+__host__ __device__ constexpr uint32_t a_bytes(int rowsA, bool split) { return uint32_t(rowsA) * 128u * (split ? 2u : 1u); }
+__host__ __device__ constexpr uint32_t b_bytes(int bn, bool split) { return uint32_t(bn) * KC * 4u * (split ? 2u : 1u); }
+inline int smem_bytes(int rowsA, int bn, bool split) {
+  return 1024 + 2 * int(a_bytes(rowsA, split) + b_bytes(bn, split)) + bn * 4 + 8 * 8 + 16;
+}
+
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(layout & 7) << 61;
+  return d;
+}
+
+template <int BN, bool SPLIT>
+__global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a) {
+  constexpr int TM = 128;
+  const int item = blockIdx.y;
+  const int cb = item % a.cblocks;
+  const int gg = (item / a.cblocks) % a.ggroups;
+  const int cob = item / (a.cblocks * a.ggroups);
+  const int g0 = a.gbegin[gg], ngroups = a.gbegin[gg + 1] - g0;
+  const int rlo = a.rows_lo[gg];
+  const int n0 = cob * BN;
+  const int z = blockIdx.x;
+  const int ch0 = z * a.chunks_per_split, ch1 = min(a.nchunks, ch0 + a.chunks_per_split);
+  const bool do_bias = a.want_bias && cb == 0 && gg == 0;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t A_B = a_bytes(a.rowsA, SPLIT), A_H = uint32_t(a.rowsA) * 128u;
+  constexpr uint32_t B_B = b_bytes(BN, SPLIT), B_H = uint32_t(BN) * KC * 4u;
+  const uint32_t STAGE = A_B + B_B;  // multiple of 1024 (rowsA % 8 == 0, BN*KC*4 % 1024 == 0)
+  float* bias_acc = reinterpret_cast<float*>(smem + 2 * STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(bias_acc + BN);
+  uint64_t* empty = full + 2;
+  uint64_t* accum = empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < uint32_t(ngroups * BN)) tmem_cols <<= 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&full[b], 4);
+      ptx::mbar_init(&empty[b], 1);
+    }
+    ptx::mbar_init(accum, 1);
+    ptx::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < BN; i += kThreads) bias_acc[i] = 0.f;
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int HWv = a.Hv * a.Wv;
+
+  if (warp == 1) {
+    if (lane == 0 && ch1 > ch0) {
+      // A MN-major (bit 15), B K-major; M = 128 = four 32-channel tap atoms, N = BN output channels
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (uint32_t(BN >> 3) << 17) |
+                                 (uint32_t(TM >> 4) << 24);
+      for (int ch = ch0; ch < ch1; ++ch) {
+        const int b = (ch - ch0) & 1;
+        ptx::mbar_wait(&full[b], uint32_t((ch - ch0) >> 1) & 1u);
+        ptx::tc_fence_after();
+        const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
+        for (int k8 = 0; k8 < KC / 8; ++k8) {
+          const uint64_t dB = desc(bbase + uint32_t(k8 >> 2) * (BN * 128u) + uint32_t(k8 & 3) * 32u, 16, 1024, 2);
+          const uint64_t dBl = dB + (B_H >> 4);
+          for (int g = 0; g < ngroups; ++g) {
+            const TapGroup& tg = a.groups[g0 + g];
+            const uint32_t row = uint32_t(tg.start - rlo + k8 * 8);
+            const uint64_t dA = desc(abase + row * 128u, uint32_t(tg.stride) * 128u, 512, 1);
+            const uint32_t d_tmem = tmem + uint32_t(g * BN);
+            uint32_t acc = (ch > ch0 || k8 > 0) ? 1u : 0u;
+            if constexpr (SPLIT) {
+              ptx::mma_tf32(d_tmem, dA + (A_H >> 4), dB, idesc, acc);
+              ptx::mma_tf32(d_tmem, dA, dBl, idesc, 1u);
+              acc = 1u;
+            }
+            ptx::mma_tf32(d_tmem, dA, dB, idesc, acc);
+          }
+        }
+        ptx::mma_commit(&empty[b]);
+      }
+      ptx::mma_commit(accum);
+    }
+    __syncwarp();
+  } else if (warp >= 2) {
+    const int tid = threadIdx.x - 64;
+    const int c0 = cb * 32, kc = min(32, a.Cg - c0);
+    const int64_t HW = int64_t(a.H) * a.W, PQ = int64_t(a.P) * a.Q;
+    for (int ch = ch0; ch < ch1; ++ch) {
+      const int b = (ch - ch0) & 1;
+      if (ch - ch0 >= 2) ptx::mbar_wait(&empty[b], uint32_t(((ch - ch0) >> 1) - 1) & 1u);
+      const int v0 = ch * KC;
+      const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
+      // ---- A: X_v rows [v0 + rlo, + rowsA), MN-major 128B_BASE32B.  One thread
+      // per pixel row loads all 32 channels before converting (32 loads in flight).
+      const int vA0 = v0 + rlo;
+      for (int row = tid; row < a.rowsA; row += 128) {
+        const int v = vA0 + row;
+        bool inb = false;
+        const float* src = a.x;
+        if (v < a.Mv) {
+          const int img = int(a.div_hwv.div(uint32_t(v)));
+          const int rem = v - img * HWv;
+          const int hp = int(a.div_wv.div(uint32_t(rem)));
+          const int h = hp - a.ph, w = rem - hp * a.Wv - a.pw;
+          inb = h >= 0 && h < a.H && w >= 0 && w < a.W;
+          src = a.x + int64_t(img) * a.x_nstride + int64_t(c0) * HW + int64_t(h) * a.W + w;
+        }
+        float xv[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xv[u][e] = (inb && u * 8 + e < kc) ? __ldg(src + (u * 8 + e) * HW) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t off = uint32_t(row) * 128u + (uint32_t((u ^ (row & 3)) & 3) << 5);
+          float hv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) hv[e] = ptx::to_tf32(xv[u][e]);
+          ptx::st_shared_v4(abase + off, hv[0], hv[1], hv[2], hv[3]);
+          ptx::st_shared_v4(abase + off + 16, hv[4], hv[5], hv[6], hv[7]);
+          if constexpr (SPLIT) {
+            ptx::st_shared_v4(abase + A_H + off, ptx::to_tf32(xv[u][0] - hv[0]), ptx::to_tf32(xv[u][1] - hv[1]),
+                              ptx::to_tf32(xv[u][2] - hv[2]), ptx::to_tf32(xv[u][3] - hv[3]));
+            ptx::st_shared_v4(abase + A_H + off + 16, ptx::to_tf32(xv[u][4] - hv[4]), ptx::to_tf32(xv[u][5] - hv[5]),
+                              ptx::to_tf32(xv[u][6] - hv[6]), ptx::to_tf32(xv[u][7] - hv[7]));
+          }
+        }
+      }
+      // ---- B: dY^T [co][v0 .. v0+KC), K-major SW128 in 32-pixel blocks.  One thread per
+      // (co, 16-pixel strip): 16 loads in flight, one index decomposition per strip.
+      for (int it = tid; it < BN * (KC / 16); it += 128) {
+        const int strip = it % (KC / 16), col = it / (KC / 16);
+        const int co = n0 + col;
+        float yv[16];
+        {
+          int v = v0 + strip * 16;
+          int img = int(a.div_hwv.div(uint32_t(v)));
+          const int rem = v - img * HWv;
+          int p = int(a.div_wv.div(uint32_t(rem)));
+          int q = rem - p * a.Wv;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            yv[e] = (v < a.Mv && co < a.Cog && p < a.P && q < a.Q)
+                        ? __ldg(a.dy + int64_t(img) * a.dy_nstride + co * PQ + int64_t(p) * a.Q + q)
+                        : 0.f;
+            ++v;
+            if (++q == a.Wv) {
+              q = 0;
+              if (++p == a.Hv) { p = 0; ++img; }
+            }
+          }
+        }
+        if (do_bias) {  // the KC/16 = 4 lanes sharing `col` reduce in a fixed shuffle tree
+          float sb = 0.f;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) sb += yv[e];
+          sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+          sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+          if ((lane & 3) == 0) bias_acc[col] += sb;
+        }
+        const int kb = strip >> 1;  // 32-pixel block
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int gi = (strip & 1) * 4 + g;  // 16-byte granule within the 128-byte row
+          const uint32_t off = uint32_t(kb) * (BN * 128u) + uint32_t(col) * 128u + (uint32_t((gi ^ (col & 7)) & 7) << 4);
+          const float h0 = ptx::to_tf32(yv[4 * g]), h1 = ptx::to_tf32(yv[4 * g + 1]);
+          const float h2 = ptx::to_tf32(yv[4 * g + 2]), h3 = ptx::to_tf32(yv[4 * g + 3]);
+          ptx::st_shared_v4(bbase + off, h0, h1, h2, h3);
+          if constexpr (SPLIT)
+            ptx::st_shared_v4(bbase + B_H + off, ptx::to_tf32(yv[4 * g] - h0), ptx::to_tf32(yv[4 * g + 1] - h1),
+                              ptx::to_tf32(yv[4 * g + 2] - h2), ptx::to_tf32(yv[4 * g + 3] - h3));
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&full[b]);
+    }
+    // ---- epilogue: TMEM lane (j*32 + c) of group g = tap (r, s0 + j), channel c
+    const int q4 = warp & 3;  // lane quadrant = tap atom j
+    float* wsz = a.ws + int64_t(z) * a.Cog * (a.Kc + 1);
+    if (ch1 > ch0) {
+      ptx::mbar_wait(accum, 0);
+      ptx::tc_fence_after();
+    }
+    const int c = c0 + lane;
+    for (int g = 0; g < ngroups; ++g) {
+      const int tap = a.groups[g0 + g].tap[q4];
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 16) {
+        uint32_t rv[16];
+        if (ch1 > ch0) {
+          ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(g * BN + cc), rv);
+          ptx::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) rv[j] = 0u;
+        }
+        if (tap >= 0 && c < a.Cg) {
+          const int m = tap * a.Cg + c;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int co = n0 + cc + j;
+            if (co < a.Cog) wsz[int64_t(co) * (a.Kc + 1) + m] = __uint_as_float(rv[j]);
+          }
+        }
+      }
+    }
+    if (do_bias && warp == 2) {
+      for (int col = lane; col < BN; col += 32)
+        if (n0 + col < a.Cog) wsz[int64_t(n0 + col) * (a.Kc + 1) + a.Kc] = bias_acc[col];
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, tmem_cols);
+  }
+}
+
+}  // namespace tcwtap
+}  // namespace cdnn

@@ -259,6 +259,25 @@ struct ConvWgradEpi {
   }
 };
 
+// Reduce epilogue of the tap-shift backward-filter partials: m' = tap*Cg + c
+// (channel innermost) -> Caffe filter index c*R*S + tap; m' == Kc -> bias.
+template <typename T>
+struct ConvWgradPermEpi {
+  T* dw;                 // offset to the group's first filter, may be null
+  T* db;                 // offset to the group's first channel, may be null
+  int Kc, Cg, RS;
+  __device__ __forceinline__ void store(int m, int n, T acc, int) const {
+    if (m < Kc) {
+      if (!dw) return;
+      const int tap = m / Cg, c = m - tap * Cg;
+      T* o = dw + int64_t(n) * Kc + c * RS + tap;
+      *o = *o + acc;
+    } else if (db) {
+      db[n] = db[n] + acc;
+    }
+  }
+};
+
 // Backward-filter B: rows n = co in the group; k = output pixel (img, p, q).
 template <typename T>
 struct ConvWgradB {

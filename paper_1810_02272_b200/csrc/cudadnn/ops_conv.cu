@@ -15,6 +15,7 @@
 
 #include "conv_tap.cuh"
 #include "conv_tma.cuh"
+#include "conv_wtap.cuh"
 #include "launch.cuh"
 
 namespace cdnn {
@@ -190,6 +191,128 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   return true;
 }
 
+template <int BN, bool SPLIT>
+void launch_conv_wtap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const tcwtap::WtapArgs& a) {
+  auto kern = tcwtap::conv_wtap_kernel<BN, SPLIT>;
+  static int attr_smem[16] = {};
+  if (attr_smem[c->device & 15] < smem) {
+    CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_smem[c->device & 15] = smem;
+  }
+  kern<<<grid, tcwtap::kThreads, smem, st>>>(a);
+  check_launch("conv_wtap_kernel");
+  count_launch(c);
+}
+
+// Tap-shift backward-filter (conv_wtap.cuh) for stride-1 convolutions with at
+// least 16 channels per group; split-K partials + the deterministic reduce.
+bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* dy, float* dw, float* db,
+                    cdnn_handle stream) {
+  const ConvGeom& g = d.geom;
+  if (!conv_tap_enabled() || g.sh != 1 || g.sw != 1 || g.Cg < 16) return false;
+  const bool split = c->math_mode == CDNN_MATH_TF32X3;
+  tcwtap::WtapArgs a{};
+  a.N = g.N; a.Cg = g.Cg; a.H = g.H; a.W = g.W; a.Cog = g.Cog; a.P = g.P; a.Q = g.Q;
+  a.R = g.R; a.S = g.S; a.dh = g.dh; a.dw = g.dw; a.ph = g.ph; a.pw = g.pw;
+  a.Hv = g.P + g.dh * (g.R - 1);
+  a.Wv = g.Q + g.dw * (g.S - 1);
+  if (int64_t(g.N) * a.Hv * a.Wv >= (int64_t(1) << 31)) return false;
+  a.Mv = g.N * a.Hv * a.Wv;
+  a.x_nstride = int64_t(g.C) * g.H * g.W;
+  a.dy_nstride = int64_t(g.Co) * g.P * g.Q;
+  a.Kc = g.Cg * g.R * g.S;
+  a.div_hwv = FastDiv(uint32_t(a.Hv * a.Wv));
+  a.div_wv = FastDiv(uint32_t(a.Wv));
+  const int bn = g.Cog <= 32 ? 32 : (g.Cog <= 64 ? 64 : 128);
+  a.cblocks = (g.Cg + 31) / 32;
+  a.coblocks = (g.Cog + bn - 1) / bn;
+  // pack the taps into groups of four equally spaced X rows: along kernel rows
+  // (stride dw) while four columns remain, then the leftover columns along
+  // kernel columns (stride dh*Wv), then what is left along its row
+  std::vector<tcwtap::TapGroup> groups;
+  auto add = [&](int r, int s, int dr, int ds, int n) {
+    tcwtap::TapGroup tg{};
+    tg.start = r * g.dh * a.Wv + s * g.dw;
+    tg.stride = dr * g.dh * a.Wv + ds * g.dw;
+    for (int j = 0; j < 4; ++j) tg.tap[j] = j < n ? (r + j * dr) * g.S + (s + j * ds) : -1;
+    if (n == 1) tg.stride = g.dw;
+    groups.push_back(tg);
+  };
+  const int sfull = g.S / 4 * 4, rfull = g.R / 4 * 4;
+  for (int r = 0; r < g.R; ++r)
+    for (int s = 0; s < sfull; s += 4) add(r, s, 0, 1, 4);
+  for (int s = sfull; s < g.S; ++s)
+    for (int r = 0; r < rfull; r += 4) add(r, s, 1, 0, 4);
+  for (int r = rfull; r < g.R; ++r)
+    if (sfull < g.S) add(r, sfull, 0, 1, g.S - sfull);
+  if (int(groups.size()) > tcwtap::kMaxGroups) return false;
+  a.ngroups = int(groups.size());
+  for (int i = 0; i < a.ngroups; ++i) a.groups[i] = groups[i];
+  // sets of groups per CTA: TMEM columns (groups x bn) <= 256 lets two CTAs share an SM
+  constexpr int kBudget = 227 * 1024;
+  int per_set = std::max(1, 256 / bn);
+  int smem = 0;
+  bool widened = false;
+  for (;;) {
+    a.ggroups = (a.ngroups + per_set - 1) / per_set;
+    int rows_max = 0;
+    for (int i = 0; i < a.ggroups; ++i) {
+      a.gbegin[i] = i * a.ngroups / a.ggroups;
+      a.gbegin[i + 1] = (i + 1) * a.ngroups / a.ggroups;
+      int lo = 1 << 30, hi = 0;
+      for (int k = a.gbegin[i]; k < a.gbegin[i + 1]; ++k) {
+        lo = std::min(lo, groups[k].start);
+        hi = std::max(hi, groups[k].start + 3 * groups[k].stride);
+      }
+      a.rows_lo[i] = lo;
+      rows_max = std::max(rows_max, hi - lo);
+    }
+    a.rowsA = (tcwtap::KC + rows_max + 7) & ~7;
+    smem = tcwtap::smem_bytes(a.rowsA, bn, split);
+    // one CTA per SM anyway (shared memory): use the whole 512-column TMEM
+    if (!widened && smem > 113 * 1024 && per_set < 512 / bn) {
+      widened = true;
+      per_set = std::max(1, 512 / bn);
+      continue;
+    }
+    if (smem <= kBudget) break;
+    if (per_set == 1) return false;
+    per_set = std::max(1, per_set / 2);
+  }
+  const int items = a.cblocks * a.ggroups * a.coblocks;
+  a.nchunks = (a.Mv + tcwtap::KC - 1) / tcwtap::KC;
+  const int target = (smem <= 113 * 1024 ? 2 : 1) * kNumSMs;
+  int splits = std::max(1, std::min(a.nchunks, (target + items - 1) / items));
+  a.chunks_per_split = (a.nchunks + splits - 1) / splits;
+  a.splits = (a.nchunks + a.chunks_per_split - 1) / a.chunks_per_split;
+  a.want_bias = db != nullptr;
+  cudaStream_t st = stream_of(c, stream);
+  Workspace& wsp = workspace_of(c, stream);
+  const size_t ws_elems = size_t(a.splits) * g.Cog * (a.Kc + 1);
+  float* ws = static_cast<float*>(wsp.get(ws_elems * sizeof(float), c->device));
+  dim3 grid(a.splits, items);
+  for (int grp = 0; grp < g.group; ++grp) {
+    tcwtap::WtapArgs ag = a;
+    ag.x = x + int64_t(grp) * g.Cg * g.H * g.W;
+    ag.dy = dy + int64_t(grp) * g.Cog * g.P * g.Q;
+    ag.ws = ws;
+    auto go = [&](auto split_tag) {
+      constexpr bool SP = decltype(split_tag)::value;
+      switch (bn) {
+        case 32: launch_conv_wtap<32, SP>(c, st, grid, smem, ag); break;
+        case 64: launch_conv_wtap<64, SP>(c, st, grid, smem, ag); break;
+        default: launch_conv_wtap<128, SP>(c, st, grid, smem, ag); break;
+      }
+    };
+    if (split) go(std::true_type{});
+    else go(std::false_type{});
+    ConvWgradPermEpi<float> epi{dw ? dw + int64_t(grp) * g.Cog * a.Kc : nullptr, db ? db + grp * g.Cog : nullptr,
+                                a.Kc, g.Cg, g.R * g.S};
+    launch_reduce(c, st, ws, a.Kc + 1, g.Cog, a.splits, epi);
+  }
+  return true;
+}
+
 template <int BN, bool SPLIT, int TW, int CB>
 void launch_conv_tma(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& tin, const CUtensorMap& twh,
                      const CUtensorMap& twl, const tcconv::ConvTmaArgs& a) {
@@ -359,6 +482,12 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
   if (!DW && !DB) return;
   // rows = taps (+1 all-ones row when the bias gradient is wanted)
   const int Kc = d.Kc, M = Kc + (DB ? 1 : 0), N = g.Cog, K = g.N * g.P * g.Q;
+  if constexpr (std::is_same_v<T, float>) {
+    if (conv_wgrad_tap(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(DY.dev),
+                       DW ? reinterpret_cast<float*>(DW->dev) : nullptr, DB ? reinterpret_cast<float*>(DB->dev) : nullptr,
+                       stream))
+      return;
+  }
   for (int grp = 0; grp < g.group; ++grp) {
     const T* x = reinterpret_cast<const T*>(X.dev) + int64_t(grp) * g.Cg * g.H * g.W;
     const T* dy = reinterpret_cast<const T*>(DY.dev) + int64_t(grp) * g.Cog * g.P * g.Q;
