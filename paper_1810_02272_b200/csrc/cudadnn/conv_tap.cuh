@@ -57,6 +57,7 @@ struct TapArgs {
   int64_t in_nstride;    // image stride of `in`
   int64_t out_nstride;   // image stride of `out`
   int nbuf, stages;      // A buffers (1|2), weight ring depth
+  int fold;              // S folded into the channels (k = s*Cin + c, Cin*S <= 32): R taps of K = S*Cin
   FastDiv div_hwv, div_wv;
   unsigned long long* trace;  // debug timeline (CDNN_TAP_TRACE), null in production
 };
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int taps = a.R * a.S;
+  const int taps = a.fold ? a.R : a.R * a.S;
   // Concurrent CTAs walk the taps from different starting points, so the 148
   // weight streams hit different L2 lines instead of the same ones at once.
   const int rot = int(blockIdx.x % uint32_t(taps));
@@ -191,14 +192,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int buf = aseq % a.nbuf;
           ptx::mbar_wait(&a_full[buf], uint32_t(aseq / a.nbuf) & 1u);
           ptx::tc_fence_after();
-          const int nk8 = (min(32, a.Cin - cb * 32) + 7) >> 3;
+          const int nk8 = ((a.fold ? a.S * a.Cin : min(32, a.Cin - cb * 32)) + 7) >> 3;
           // descriptors are built once; per MMA only the 16-byte-unit start
           // address in the low word moves (smem < 256 KB: no carry out of 14 bits)
           const uint64_t dA = desc_sw128(ptx::smem_u32(abase + buf * A_BUF));
           const uint64_t dAl = dA + (A_HALF >> 4);
           for (int it = 0; it < taps; ++it) {
             const int tap = it + rot < taps ? it + rot : it + rot - taps;
-            const int r = tap / a.S, s = tap - r * a.S;
+            const int r = a.fold ? tap : tap / a.S, s = a.fold ? 0 : tap - r * a.S;
             const uint64_t shift = uint64_t(r * a.dh * a.Wv + s * a.dw) * 8u;  // rows x 128 B in 16 B units
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
@@ -242,6 +243,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kc = min(32, a.Cin - c0);
         const int g8n = (kc + 7) >> 3;  // 8-channel groups the MMAs read
         const uint32_t hi = ptx::smem_u32(abase + buf * A_BUF);
+        if (a.fold) {
+          // folded row: element k = s*Cin + c holds X_v[v + s*dw][c]; one index
+          // decomposition per row, then (s, c) and the pixel advance incrementally
+          const int kf = a.S * a.Cin, g8f = (kf + 7) >> 3;
+          for (int row = tid; row < a.rows; row += 128) {
+            const uint32_t rbase = hi + uint32_t(row) * 128u;
+            int v = m0 + row;
+            int img = int(a.div_hwv.div(uint32_t(v)));
+            const int rem0 = v - img * HWv;
+            int hp = int(a.div_wv.div(uint32_t(rem0)));
+            int wp = rem0 - hp * a.Wv;
+            auto tap_src = [&](bool& ok) {
+              const int h = hp - a.oh, w = wp - a.ow;
+              ok = v < a.Mv && h >= 0 && h < a.Hin && w >= 0 && w < a.Win;
+              return a.in + int64_t(img) * a.in_nstride + h * a.Win + w;
+            };
+            bool ok;
+            const float* src = tap_src(ok);
+            int c = 0;
+            float x[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              x[k] = (k < kf && ok) ? __ldg(src + int64_t(c) * a.in_cstride) : 0.f;
+              if (++c == a.Cin) {
+                c = 0;
+                v += a.dw;
+                wp += a.dw;
+                while (wp >= a.Wv) {
+                  wp -= a.Wv;
+                  if (++hp == a.Hv) { hp = 0; ++img; }
+                }
+                src = tap_src(ok);
+              }
+            }
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8)
+              if (g8 < g8f) {
+                float xx[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) xx[e] = x[g8 * 8 + e];
+                put_row8<SPLIT>(rbase, A_HALF, row, g8, xx);
+              }
+          }
+        } else
         for (int row = tid; row < a.rows; row += 128) {
           const int v = m0 + row;
           bool inb = false;

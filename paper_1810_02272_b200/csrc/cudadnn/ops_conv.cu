@@ -41,21 +41,32 @@ bool conv_tap_enabled() {
 // kpad channels, (hi, lo) TF32 split:
 //   forward : dst[tap][co][ci]      (ci within the group)
 //   backward: dst[tap][ci][co]      (co within ci's group), taps flipped
+//   fold    : the kernel row's S taps live in k = s*Cd + c (Cd = channels of the direct conv)
 __global__ void repack_tap_kernel(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int Co,
-                                  int C, int Cg, int Cog, int R, int S, int kpad, bool backward, bool split) {
+                                  int C, int Cg, int Cog, int R, int S, int kpad, bool backward, bool split, bool fold) {
   const int rows = backward ? C : Co;
-  const int total = R * S * rows * kpad;
+  const int taps = fold ? R : R * S;
+  const int Cd = backward ? Cog : Cg;
+  const int total = taps * rows * kpad;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int k = i % kpad;
+    int k = i % kpad;
     const int row = (i / kpad) % rows;
     const int tap = i / (kpad * rows);
-    const int kr = tap / S, ks = tap % S;
+    int kr = fold ? tap : tap / S, ks = fold ? 0 : tap % S;
+    bool ok = k < Cd;
+    if (fold) {
+      ks = k / Cd;
+      k -= ks * Cd;
+      ok = ks < S;
+    }
     float v = 0.f;
-    if (!backward) {
-      if (k < Cg) v = w[((row * Cg + k) * R + kr) * S + ks];
-    } else if (k < Cog) {
-      const int grp = row / Cg;
-      v = w[(((grp * Cog + k) * Cg + (row - grp * Cg)) * R + (R - 1 - kr)) * S + (S - 1 - ks)];
+    if (ok) {
+      if (!backward) {
+        v = w[((row * Cg + k) * R + kr) * S + ks];
+      } else {
+        const int grp = row / Cg;
+        v = w[(((grp * Cog + k) * Cg + (row - grp * Cg)) * R + (R - 1 - kr)) * S + (S - 1 - ks)];
+      }
     }
     const float h = split ? ptx::to_tf32(v) : v;
     hi[i] = h;
@@ -113,6 +124,14 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
   const ConvGeom& g = d.geom;
   if (!conv_tap_enabled() || g.sh != 1 || g.sw != 1) return false;
+  // 2-7 input channels with wide filters (CIFAR conv1): the window-staging kernel
+  // (conv_tma.cuh) measures faster (profiles/r01_conv_bench.txt); it takes them when eligible
+  {
+    const int cin = backward_data ? g.Cog : g.Cg, win = backward_data ? g.Q : g.W;
+    if (g.group == 1 && g.dh == 1 && g.dw == 1 && cin > 1 && cin < 8 && cin * g.S > 8 && win % 4 == 0 &&
+        conv_tma_enabled())
+      return false;
+  }
   const int G = g.group;
   const int Cin = backward_data ? g.Cog : g.Cg, Hin = backward_data ? g.P : g.H, Win = backward_data ? g.Q : g.W;
   const int Cout = backward_data ? g.Cg : g.Cog, P = backward_data ? g.H : g.P, Q = backward_data ? g.W : g.Q;
@@ -126,8 +145,13 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   a.Wv = Q + g.dw * (g.S - 1);
   if (int64_t(g.N) * a.Hv * a.Wv >= (int64_t(1) << 31)) return false;
   a.Mv = g.N * a.Hv * a.Wv;
-  a.rows = (128 + g.dh * (g.R - 1) * a.Wv + g.dw * (g.S - 1) + 7) & ~7;
-  a.cblocks = (Cin + 31) / 32;
+  static const bool fold_ok = [] {
+    const char* v = std::getenv("CDNN_TAP_FOLD");
+    return !(v && std::string(v) == "0");
+  }();
+  a.fold = (fold_ok && Cin < 16 && Cin * g.S <= 32) ? 1 : 0;
+  a.rows = (128 + g.dh * (g.R - 1) * a.Wv + (a.fold ? 0 : g.dw * (g.S - 1)) + 7) & ~7;
+  a.cblocks = a.fold ? 1 : (Cin + 31) / 32;
   a.in_cstride = Hin * Win;
   a.in_nstride = int64_t(CinT) * Hin * Win;
   a.out_nstride = int64_t(CoutT) * P * Q;
@@ -149,7 +173,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   // weights: repacked per call (they change every step), pre-split
   const int kpad = a.cblocks * 32;
   a.wrows = CoutT;
-  const int RS = g.R * g.S;
+  const int RS = a.fold ? g.R : g.R * g.S;  // taps of the repacked operand
   const size_t elems = size_t(RS) * CoutT * kpad;
   const int slot = backward_data ? 2 : 0;
   if (!d.repack[slot] || d.repack[slot]->bytes < elems * 4) {
@@ -160,7 +184,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   float* wlo = static_cast<float*>(d.repack[slot + 1]->ptr);
   cudaStream_t st = stream_of(c, stream);
   repack_tap_kernel<<<grid_for(int64_t(elems), 256), 256, 0, st>>>(w, whi, wlo, g.Co, g.C, g.Cg, g.Cog, g.R, g.S,
-                                                                   kpad, backward_data, split);
+                                                                   kpad, backward_data, split, a.fold != 0);
   check_launch("repack_tap");
   count_launch(c);
   const uint64_t wdims[2] = {uint64_t(kpad), uint64_t(RS) * CoutT};
