@@ -468,6 +468,47 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
   }
 }
 
+// Strided backward-data as a direct gather: one thread per bottom element
+// (img, c, h, w) visits only the taps whose output pixel exists,
+// p = (h + ph - r*dh) / sh with zero remainder, so none of the (sh*sw - 1)/(sh*sw)
+// structurally-zero products of the implicit-GEMM view are computed.  Exact
+// FMA accumulation in T, co-major order; consecutive threads walk w (dY loads
+// near-coalesced, filter loads warp-uniform).
+template <typename T>
+__global__ void __launch_bounds__(256) conv_dgrad_direct_kernel(const T* __restrict__ w, const T* __restrict__ dy,
+                                                                T* __restrict__ dx, ConvGeom g, int64_t total) {
+  // columns in phase-major order: j -> x = (j / Wq) + (j % Wq) * sw, so a warp shares
+  // one column phase (same valid taps, no divergence) and reads consecutive q
+  const int Wq = (g.W + g.sw - 1) / g.sw, Wj = Wq * g.sw;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int j = int(i % Wj);
+    const int x = j / Wq + (j % Wq) * g.sw;
+    if (x >= g.W) continue;
+    const int y = int((i / Wj) % g.H);
+    const int c = int((i / (int64_t(Wj) * g.H)) % g.C);
+    const int img = int(i / (int64_t(Wj) * g.H * g.C));
+    const int grp = c / g.Cg, cg = c - grp * g.Cg;
+    T acc = T(0);
+    for (int r = 0; r < g.R; ++r) {
+      const int ty = y + g.ph - r * g.dh;
+      if (ty < 0 || ty % g.sh) continue;
+      const int p = ty / g.sh;
+      if (p >= g.P) continue;
+      for (int s = 0; s < g.S; ++s) {
+        const int tx = x + g.pw - s * g.dw;
+        if (tx < 0 || tx % g.sw) continue;
+        const int q = tx / g.sw;
+        if (q >= g.Q) continue;
+        const T* wp = w + ((int64_t(grp) * g.Cog * g.Cg + cg) * g.R + r) * g.S + s;
+        const T* dp = dy + ((int64_t(img) * g.Co + int64_t(grp) * g.Cog) * g.P + p) * g.Q + q;
+        const int64_t wstep = int64_t(g.Cg) * g.R * g.S, dstep = int64_t(g.P) * g.Q;
+        for (int co = 0; co < g.Cog; ++co) acc = fma(__ldg(wp + co * wstep), __ldg(dp + co * dstep), acc);
+      }
+    }
+    dx[((int64_t(img) * g.C + c) * g.H + y) * g.W + x] = acc;
+  }
+}
+
 template <typename T>
 void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, const BufferSlot& DY,
                           BufferSlot& DX, cdnn_handle stream) {
@@ -475,6 +516,14 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.H * g.W, N = g.Cg, K = d.Kd;
+  if (g.sh > 1 || g.sw > 1) {
+    const int64_t total = int64_t(g.N) * g.C * g.H * ((g.W + g.sw - 1) / g.sw * g.sw);
+    conv_dgrad_direct_kernel<T><<<grid_for(total, 256), 256, 0, st>>>(
+        reinterpret_cast<const T*>(Wt.dev), reinterpret_cast<const T*>(DY.dev), reinterpret_cast<T*>(DX.dev), g, total);
+    check_launch("conv_dgrad_direct");
+    count_launch(c);
+    return;
+  }
   if constexpr (std::is_same_v<T, float>) {
     if (conv_tap(c, d, true, reinterpret_cast<const float*>(DY.dev), reinterpret_cast<const float*>(Wt.dev), nullptr,
                  reinterpret_cast<float*>(DX.dev), stream))
