@@ -42,12 +42,31 @@ sys.path.insert(0, ROOT)
 
 METRIC = "training images/sec (fwd+bwd+SGD) at 1/2/4/8 B200 vs CPU ref; ms/iter"
 UNIT = "images/s"
+# BASELINE.json configs; the default (headline) workload is configs[1].  ref_batch:
+# images per reference-CPU step per process (bounded sample; CPU cost is linear in batch).
+WORKLOADS = {
+    "cifar10_quick": dict(batch=100, img=(3, 32, 32), classes=10, ref_batch=20, cpu_batch=100,
+                          solver=dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=0.004)),
+    "lenet": dict(batch=64, img=(1, 28, 28), classes=10, ref_batch=64, cpu_batch=64,
+                  solver=dict(method="sgd", lr=0.01, momentum=0.9, weight_decay=5e-4)),
+    "alexnet": dict(batch=256, img=(3, 227, 227), classes=1000, ref_batch=1, cpu_batch=2,
+                    solver=dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=5e-4)),
+    "resnet20": dict(batch=128, img=(3, 32, 32), classes=10, ref_batch=8, cpu_batch=16,
+                     solver=dict(method="sgd", lr=0.1, momentum=0.9, weight_decay=1e-4)),
+}
 WORKLOAD = "cifar10_quick"
 BATCH = 100
-SOLVER = dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=0.004)
+SOLVER = WORKLOADS[WORKLOAD]["solver"]
 IMG = (3, 32, 32)
 CLASSES = 10
 REF_SAMPLE_BATCH = 20  # images per reference step per process (bounded CPU sample)
+
+
+def select_workload(name: str) -> None:
+    global WORKLOAD, BATCH, SOLVER, IMG, CLASSES, REF_SAMPLE_BATCH
+    w = WORKLOADS[name]
+    WORKLOAD, BATCH, SOLVER, IMG, CLASSES, REF_SAMPLE_BATCH = (name, w["batch"], w["solver"], w["img"],
+                                                               w["classes"], w["ref_batch"])
 
 
 def log(*a):
@@ -56,14 +75,14 @@ def log(*a):
 
 def model_text(batch: int) -> str:
     from paper_1810_02272_b200 import polegrad
-    t = polegrad.load_model(WORKLOAD)
-    return t.replace("batch_size: 100", f"batch_size: {batch}")
+    return polegrad.load_model(WORKLOAD, batch)
 
 
 def config(n_gpus: int, graph: bool) -> dict:
     return {"workload": WORKLOAD, "per_gpu_batch": BATCH, "global_batch": BATCH * n_gpus,
             "input": "x".join(map(str, IMG)), "classes": CLASSES,
-            "solver": "SGD lr=1e-3 momentum=0.9 weight_decay=4e-3",
+            "solver": f"SGD lr={SOLVER['lr']:g} momentum={SOLVER['momentum']:g} "
+                      f"weight_decay={SOLVER['weight_decay']:g}",
             "math": os.environ.get("CDNN_MATH", "tf32x3"),
             "step": "cuda-graph" if graph else "eager",
             "l2": "flushed (256 MiB device write) before every timed step",
@@ -173,7 +192,12 @@ def layer_flops(net) -> dict:
         if not pname.endswith(".weight"):
             continue
         lname = pname[: -len(".weight")]
-        top = net.blob_shape(lname)
+        try:
+            top = net.blob_shape(lname)
+        except Exception:  # in-place layers (Scale) have no top of their own name
+            continue
+        if wshape[0] == 1 and wshape[1] == 1 and wshape[2] == 1:  # Scale (1,1,1,C): elementwise
+            continue
         if wshape[0] == 1 and wshape[1] == 1:  # InnerProduct weight (1,1,O,K)
             f = 2.0 * top[0] * wshape[2] * wshape[3]
             out[lname] = {"fwd": f, "bwd": 2 * f}  # wgrad + dgrad (the reference always writes dX)
@@ -208,12 +232,13 @@ def cpu_baseline_sample(iters: int = 2) -> dict:
     if not pyoracle.available("f32"):
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                 "sample": "oracle/_ref not built on this host"}
-    text = model_text(BATCH)
+    cb = WORKLOADS[WORKLOAD]["cpu_batch"]
+    text = model_text(cb)
     net = pyoracle.OracleNet(text, seed=1, dtype="f32")
     solver = pyoracle.OracleSolver(net, **SOLVER)
     rng = np.random.default_rng(2)
-    x = rng.uniform(-1, 1, (BATCH,) + IMG)
-    y = np.floor(rng.uniform(0, 1, BATCH) * CLASSES)
+    x = rng.uniform(-1, 1, (cb,) + IMG)
+    y = np.floor(rng.uniform(0, 1, cb) * CLASSES)
     t0 = time.perf_counter()
     for _ in range(iters):
         net.set_batch(x, y)
@@ -221,9 +246,9 @@ def cpu_baseline_sample(iters: int = 2) -> dict:
         net.backward()
         solver.apply()
     dt = time.perf_counter() - t0
-    return {"value": iters * BATCH / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+    return {"value": iters * cb / dt, "unit": UNIT, "cores": 1, "kind": "reference",
             "ms_per_step": 1000 * dt / iters,
-            "sample": f"{iters} full iterations of {WORKLOAD} batch {BATCH} (f32) on oracle/_ref: unmodified "
+            "sample": f"{iters} iterations of {WORKLOAD} at batch {cb} (f32) on oracle/_ref: unmodified "
                       f"reference core (kernels::gemm, InnerProduct, ReLU, solver) + reference-style "
                       f"Convolution/Pooling/SoftmaxWithLoss extension, 1 thread"}
 
@@ -537,7 +562,10 @@ def main() -> None:
     ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the captured CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cifar10_quick",
+                    help="BASELINE.json config to run (default: the headline CIFAR-10 quick)")
     args = ap.parse_args()
+    select_workload(args.workload)
     if args.warmup < 3 and args.impl == "b200":
         log("note: timing rules ask for >= 3 warm-up steps")
     if args.impl == "reference":

@@ -509,6 +509,55 @@ __global__ void __launch_bounds__(256) conv_dgrad_direct_kernel(const T* __restr
   }
 }
 
+// dY of a strided convolution scattered onto the stride-1 output grid of the same
+// filter (P1 = H + 2ph - dh(R-1) rows): up[t][u] = dY[t/sh][u/sw] on the stride
+// lattice, 0 elsewhere.  Backward-data and backward-filter of the strided conv are
+// then the stride-1 ones on `up` (sh*sw x the MACs, all on the tensor cores).
+__global__ void zero_insert_kernel(const float* __restrict__ dy, float* __restrict__ up, int64_t planes, int P, int Q,
+                                   int P1, int Q1, int sh, int sw) {
+  const int64_t total = planes * P1 * Q1;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int u = int(i % Q1);
+    const int t = int((i / Q1) % P1);
+    const int64_t pl = i / (int64_t(Q1) * P1);
+    float v = 0.f;
+    if (t % sh == 0 && u % sw == 0 && t / sh < P && u / sw < Q) v = dy[(pl * P + t / sh) * Q + u / sw];
+    up[i] = v;
+  }
+}
+
+// Runs `body(up)` with dY zero-inserted and the descriptor's geometry switched to
+// the stride-1 equivalent; returns body's result (false = not handled).
+template <class F>
+bool with_zero_inserted(Ctx* c, const ConvDescSlot& dconst, const float* dy, cdnn_handle stream, F body) {
+  ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
+  const ConvGeom g = d.geom;
+  const int P1 = g.H + 2 * g.ph - g.dh * (g.R - 1), Q1 = g.W + 2 * g.pw - g.dw * (g.S - 1);
+  if (P1 < 1 || Q1 < 1) return false;
+  const size_t elems = size_t(g.N) * g.Co * P1 * Q1;
+  if (!d.upsampled || d.upsampled->bytes < elems * 4) d.upsampled = device_alloc_shared(elems * 4, c->device);
+  float* up = static_cast<float*>(d.upsampled->ptr);
+  cudaStream_t st = stream_of(c, stream);
+  zero_insert_kernel<<<grid_for(int64_t(elems), 256), 256, 0, st>>>(dy, up, int64_t(g.N) * g.Co, g.P, g.Q, P1, Q1,
+                                                                     g.sh, g.sw);
+  check_launch("zero_insert");
+  count_launch(c);
+  ConvGeom g1 = g;
+  g1.sh = g1.sw = 1;
+  g1.P = P1;
+  g1.Q = Q1;
+  d.geom = g1;
+  bool ok = false;
+  try {
+    ok = body(static_cast<const float*>(up));
+  } catch (...) {
+    d.geom = g;
+    throw;
+  }
+  d.geom = g;
+  return ok;
+}
+
 template <typename T>
 void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, const BufferSlot& DY,
                           BufferSlot& DX, cdnn_handle stream) {
@@ -516,6 +565,14 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.H * g.W, N = g.Cg, K = d.Kd;
+  if constexpr (std::is_same_v<T, float>) {
+    if ((g.sh > 1 || g.sw > 1) && conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 &&
+        with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, [&](const float* up) {
+          return conv_tap(c, d, true, up, reinterpret_cast<const float*>(Wt.dev), nullptr,
+                          reinterpret_cast<float*>(DX.dev), stream);
+        }))
+      return;
+  }
   if (g.sh > 1 || g.sw > 1) {
     const int64_t total = int64_t(g.N) * g.C * g.H * ((g.W + g.sw - 1) / g.sw * g.sw);
     conv_dgrad_direct_kernel<T><<<grid_for(total, 256), 256, 0, st>>>(
@@ -556,10 +613,16 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
   // rows = taps (+1 all-ones row when the bias gradient is wanted)
   const int Kc = d.Kc, M = Kc + (DB ? 1 : 0), N = g.Cog, K = g.N * g.P * g.Q;
   if constexpr (std::is_same_v<T, float>) {
-    if (conv_wgrad_tap(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(DY.dev),
-                       DW ? reinterpret_cast<float*>(DW->dev) : nullptr, DB ? reinterpret_cast<float*>(DB->dev) : nullptr,
-                       stream))
+    float* dw = DW ? reinterpret_cast<float*>(DW->dev) : nullptr;
+    float* db = DB ? reinterpret_cast<float*>(DB->dev) : nullptr;
+    const float* x = reinterpret_cast<const float*>(X.dev);
+    if (g.sh == 1 && g.sw == 1) {
+      if (conv_wgrad_tap(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) return;
+    } else if (conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 && g.Cg >= 16 &&
+               with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream,
+                                  [&](const float* up) { return conv_wgrad_tap(c, d, x, up, dw, db, stream); })) {
       return;
+    }
   }
   for (int grp = 0; grp < g.group; ++grp) {
     const T* x = reinterpret_cast<const T*>(X.dev) + int64_t(grp) * g.Cg * g.H * g.W;

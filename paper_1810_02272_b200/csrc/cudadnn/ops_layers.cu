@@ -90,126 +90,125 @@ __global__ void dropout_kernel(const T* __restrict__ in, T* __restrict__ out, ui
 __global__ void bump_kernel(unsigned long long* iter) { *iter += 1; }
 
 // ---- BatchNorm (training statistics), Scale, Eltwise ----------------------------------
-// one block per channel: mean, inv_std over (N, HW); fixed tree -> deterministic
-template <typename T>
-__global__ void bn_stats(const T* __restrict__ x, T* __restrict__ mean, T* __restrict__ invstd, int N, int C, int HW,
-                         T eps) {
-  __shared__ double sh[kT], sh2[kT];
-  const int c = blockIdx.x;
-  double s = 0, s2 = 0;
-  for (int n = 0; n < N; ++n) {
-    const T* p = x + (int64_t(n) * C + c) * HW;
-    for (int i = threadIdx.x; i < HW; i += blockDim.x) {
-      const double v = double(p[i]);
-      s += v;
-      s2 += v * v;
+// Per-channel sums over (N, HW) are two-level and deterministic: grid (C, splits),
+// each block reduces a fixed range of images into one double pair (fixed-shape
+// tree), then one thread per channel adds the split partials in order.  The
+// elementwise passes index by plane (blockIdx.y = img*C + c): no per-element
+// division, float4 when HW % 4 == 0.
+
+enum ChanOp { kSumSq = 0, kSumDot = 1 };  // (x, x*x) | (a, a*b)
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(kT) chan_partials(const T* __restrict__ u, const T* __restrict__ w, double2* part,
+                                                    int N, int C, int HW, int splits) {
+  __shared__ double sh0[kT], sh1[kT];
+  const int c = blockIdx.x, sp = blockIdx.y;
+  const int n0 = int(int64_t(N) * sp / splits), n1 = int(int64_t(N) * (sp + 1) / splits);
+  double s0 = 0, s1 = 0;
+  for (int n = n0; n < n1; ++n) {
+    const int64_t off = (int64_t(n) * C + c) * HW;
+    for (int i = threadIdx.x; i < HW; i += kT) {
+      const double a = double(u[off + i]);
+      if (OP == kSumSq) { s0 += a; s1 += a * a; }
+      else { s0 += a; s1 += a * double(w[off + i]); }
     }
   }
-  sh[threadIdx.x] = s;
-  sh2[threadIdx.x] = s2;
+  sh0[threadIdx.x] = s0;
+  sh1[threadIdx.x] = s1;
   __syncthreads();
-  for (int w = kT / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) { sh[threadIdx.x] += sh[threadIdx.x + w]; sh2[threadIdx.x] += sh2[threadIdx.x + w]; }
+  for (int k = kT / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) { sh0[threadIdx.x] += sh0[threadIdx.x + k]; sh1[threadIdx.x] += sh1[threadIdx.x + k]; }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    const double cnt = double(N) * HW;
-    const double m = sh[0] / cnt;
-    const double var = sh2[0] / cnt - m * m;
-    mean[c] = T(m);
-    invstd[c] = T(1.0 / sqrt(var + double(eps)));
-  }
+  if (threadIdx.x == 0) part[int64_t(c) * splits + sp] = make_double2(sh0[0], sh1[0]);
+}
+
+__device__ __forceinline__ double2 sum_parts(const double2* part, int c, int splits) {
+  double s0 = 0, s1 = 0;
+  for (int k = 0; k < splits; ++k) { s0 += part[int64_t(c) * splits + k].x; s1 += part[int64_t(c) * splits + k].y; }
+  return make_double2(s0, s1);
+}
+
+template <typename T>
+__global__ void bn_finalize(const double2* part, int splits, int C, double cnt, double eps, T* mean, T* invstd) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double2 s = sum_parts(part, c, splits);
+  const double m = s.x / cnt, var = s.y / cnt - m * m;
+  mean[c] = T(m);
+  invstd[c] = T(1.0 / sqrt(var + eps));
+}
+
+// a = mean(dy), b = mean(dy*y)
+template <typename T>
+__global__ void bn_bwd_finalize(const double2* part, int splits, int C, double cnt, T* a, T* b) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double2 s = sum_parts(part, c, splits);
+  a[c] = T(s.x / cnt);
+  b[c] = T(s.y / cnt);
+}
+
+// dbeta += sum dy ; dgamma += sum dy*x
+template <typename T>
+__global__ void scale_finalize(const double2* part, int splits, int C, T* dg, T* db) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double2 s = sum_parts(part, c, splits);
+  if (db) db[c] += T(s.x);
+  if (dg) dg[c] += T(s.y);
+}
+
+// Plane-indexed elementwise: out = f(i, c) over plane (img, c); F(v0, v1, c) per element.
+template <typename T, class F>
+__device__ __forceinline__ void plane_apply(T* __restrict__ out, int64_t off, int HW, F f) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) out[off + i] = f(off + i);
 }
 
 template <typename T>
 __global__ void bn_apply(const T* __restrict__ x, const T* __restrict__ mean, const T* __restrict__ invstd,
-                         T* __restrict__ y, int C, int HW, int64_t total) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int c = int((i / HW) % C);
-    y[i] = (x[i] - mean[c]) * invstd[c];
-  }
+                         T* __restrict__ y, int C, int HW) {
+  const int c = blockIdx.y % C;
+  const T m = mean[c], is = invstd[c];
+  const int64_t off = int64_t(blockIdx.y) * HW;
+  plane_apply(y, off, HW, [&](int64_t i) { return (x[i] - m) * is; });
 }
 
-// per channel: a = mean(dy), b = mean(dy*y)
-template <typename T>
-__global__ void bn_bwd_stats(const T* __restrict__ y, const T* __restrict__ dy, T* __restrict__ a, T* __restrict__ b,
-                             int N, int C, int HW) {
-  __shared__ double sh[kT], sh2[kT];
-  const int c = blockIdx.x;
-  double s = 0, s2 = 0;
-  for (int n = 0; n < N; ++n) {
-    const int64_t off = (int64_t(n) * C + c) * HW;
-    for (int i = threadIdx.x; i < HW; i += blockDim.x) {
-      s += double(dy[off + i]);
-      s2 += double(dy[off + i]) * double(y[off + i]);
-    }
-  }
-  sh[threadIdx.x] = s;
-  sh2[threadIdx.x] = s2;
-  __syncthreads();
-  for (int w = kT / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) { sh[threadIdx.x] += sh[threadIdx.x + w]; sh2[threadIdx.x] += sh2[threadIdx.x + w]; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double cnt = double(N) * HW;
-    a[c] = T(sh[0] / cnt);
-    b[c] = T(sh2[0] / cnt);
-  }
-}
-
-// dx = (dy - a - y*b) * inv_std
 template <typename T>
 __global__ void bn_bwd_apply(const T* __restrict__ y, const T* __restrict__ dy, const T* __restrict__ a,
-                             const T* __restrict__ b, const T* __restrict__ invstd, T* __restrict__ dx, int C, int HW,
-                             int64_t total) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int c = int((i / HW) % C);
-    dx[i] = (dy[i] - a[c] - y[i] * b[c]) * invstd[c];
-  }
+                             const T* __restrict__ b, const T* __restrict__ invstd, T* __restrict__ dx, int C, int HW) {
+  const int c = blockIdx.y % C;
+  const T ac = a[c], bc = b[c], is = invstd[c];
+  const int64_t off = int64_t(blockIdx.y) * HW;
+  plane_apply(dx, off, HW, [&](int64_t i) { return (dy[i] - ac - y[i] * bc) * is; });
 }
 
 template <typename T>
 __global__ void scale_fwd(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ bta,
-                          T* __restrict__ y, int C, int HW, int64_t total) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int c = int((i / HW) % C);
-    y[i] = x[i] * g[c] + (bta ? bta[c] : T(0));
-  }
-}
-
-// per channel: dgamma += sum dy*x ; dbeta += sum dy  (block per channel)
-template <typename T>
-__global__ void scale_bwd_params(const T* __restrict__ x, const T* __restrict__ dy, T* __restrict__ dg,
-                                 T* __restrict__ db, int N, int C, int HW) {
-  __shared__ double sh[kT], sh2[kT];
-  const int c = blockIdx.x;
-  double s = 0, s2 = 0;
-  for (int n = 0; n < N; ++n) {
-    const int64_t off = (int64_t(n) * C + c) * HW;
-    for (int i = threadIdx.x; i < HW; i += blockDim.x) {
-      s += double(dy[off + i]) * double(x[off + i]);
-      s2 += double(dy[off + i]);
-    }
-  }
-  sh[threadIdx.x] = s;
-  sh2[threadIdx.x] = s2;
-  __syncthreads();
-  for (int w = kT / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) { sh[threadIdx.x] += sh[threadIdx.x + w]; sh2[threadIdx.x] += sh2[threadIdx.x + w]; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (dg) dg[c] += T(sh[0]);
-    if (db) db[c] += T(sh2[0]);
-  }
+                          T* __restrict__ y, int C, int HW) {
+  const int c = blockIdx.y % C;
+  const T gc = g[c], bc = bta ? bta[c] : T(0);
+  const int64_t off = int64_t(blockIdx.y) * HW;
+  plane_apply(y, off, HW, [&](int64_t i) { return x[i] * gc + bc; });
 }
 
 template <typename T>
-__global__ void scale_bwd_data(const T* __restrict__ dy, const T* __restrict__ g, T* __restrict__ dx, int C, int HW,
-                               int64_t total) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x)
-    dx[i] = dy[i] * g[(i / HW) % C];
+__global__ void scale_bwd_data(const T* __restrict__ dy, const T* __restrict__ g, T* __restrict__ dx, int C, int HW) {
+  const int c = blockIdx.y % C;
+  const T gc = g[c];
+  const int64_t off = int64_t(blockIdx.y) * HW;
+  plane_apply(dx, off, HW, [&](int64_t i) { return dy[i] * gc; });
+}
+
+// launch helpers: splits so each partial block covers ~32k elements; plane grid
+inline int chan_splits(int N, int C, int HW) {
+  // >= 4 blocks per SM in total, >= 2048 elements per block, <= N
+  const int64_t want = (4 * kNumSMs + C - 1) / C;
+  const int64_t cap = std::max<int64_t>(1, int64_t(N) * HW / 2048);
+  return int(std::max<int64_t>(1, std::min<int64_t>({int64_t(N), want, cap})));
+}
+inline dim3 plane_grid(int N, int C, int HW) {
+  return dim3(unsigned(std::max(1, std::min((HW + kT - 1) / kT, 64))), unsigned(N * C));
 }
 
 template <typename T>
@@ -316,15 +315,19 @@ int cdnn_batchnorm_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_hand
     const uint64_t cnt = uint64_t(n) * c * hw;
     require_len(X, cnt, "bn"); require_len(Y, cnt, "bn"); require_len(M, uint64_t(c), "bn"); require_len(V, uint64_t(c), "bn");
     for (BufferSlot* b : {&Y, &M, &V}) require_dtype(*b, X.dtype, "bn");
+    if (n * c > 65535) fail(CDNN_INVALID_ARGUMENT, "bn: n*c must be <= 65535");
     DeviceGuard g(cx);
     cudaStream_t st = stream_of(cx, stream);
+    const int splits = chan_splits(n, c, hw);
+    double2* part = static_cast<double2*>(workspace_of(cx, stream).get(size_t(c) * splits * sizeof(double2), cx->device));
     by_dtype(X.dtype, "bn", [&](auto tag) {
       using T = decltype(tag);
-      bn_stats<T><<<c, kT, 0, st>>>(P<T>(X), P<T>(M), P<T>(V), n, c, hw, T(eps));
-      bn_apply<T><<<blocks(int64_t(cnt)), kT, 0, st>>>(P<T>(X), P<T>(M), P<T>(V), P<T>(Y), c, hw, int64_t(cnt));
+      chan_partials<T, kSumSq><<<dim3(c, splits), kT, 0, st>>>(P<T>(X), nullptr, part, n, c, hw, splits);
+      bn_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, double(n) * hw, eps, P<T>(M), P<T>(V));
+      bn_apply<T><<<plane_grid(n, c, hw), kT, 0, st>>>(P<T>(X), P<T>(M), P<T>(V), P<T>(Y), c, hw);
     });
     check_launch("bn_fwd");
-    count_launch(cx, 2);
+    count_launch(cx, 3);
   });
 }
 
@@ -341,18 +344,21 @@ int cdnn_batchnorm_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle invstd, cdn
     require_len(Y, cnt, "bn_bwd"); require_len(DY, cnt, "bn_bwd"); require_len(DX, cnt, "bn_bwd");
     require_len(V, uint64_t(c), "bn_bwd"); require_len(S, 2 * uint64_t(c), "bn_bwd scratch");
     for (BufferSlot* b : {&V, &DY, &DX, &S}) require_dtype(*b, Y.dtype, "bn_bwd");
+    if (n * c > 65535) fail(CDNN_INVALID_ARGUMENT, "bn_bwd: n*c must be <= 65535");
     DeviceGuard g(cx);
     cudaStream_t st = stream_of(cx, stream);
+    const int splits = chan_splits(n, c, hw);
+    double2* part = static_cast<double2*>(workspace_of(cx, stream).get(size_t(c) * splits * sizeof(double2), cx->device));
     by_dtype(Y.dtype, "bn_bwd", [&](auto tag) {
       using T = decltype(tag);
       T* a = P<T>(S);
       T* b = a + c;
-      bn_bwd_stats<T><<<c, kT, 0, st>>>(P<T>(Y), P<T>(DY), a, b, n, c, hw);
-      bn_bwd_apply<T><<<blocks(int64_t(cnt)), kT, 0, st>>>(P<T>(Y), P<T>(DY), a, b, P<T>(V), P<T>(DX), c, hw,
-                                                           int64_t(cnt));
+      chan_partials<T, kSumDot><<<dim3(c, splits), kT, 0, st>>>(P<T>(DY), P<T>(Y), part, n, c, hw, splits);
+      bn_bwd_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, double(n) * hw, a, b);
+      bn_bwd_apply<T><<<plane_grid(n, c, hw), kT, 0, st>>>(P<T>(Y), P<T>(DY), a, b, P<T>(V), P<T>(DX), c, hw);
     });
     check_launch("bn_bwd");
-    count_launch(cx, 2);
+    count_launch(cx, 3);
   });
 }
 
@@ -368,11 +374,12 @@ int cdnn_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_hand
     require_len(X, cnt, "scale"); require_len(Y, cnt, "scale"); require_len(G, uint64_t(c), "scale");
     if (B) { require_len(*B, uint64_t(c), "scale"); require_dtype(*B, X.dtype, "scale"); }
     require_dtype(G, X.dtype, "scale"); require_dtype(Y, X.dtype, "scale");
+    if (n * c > 65535) fail(CDNN_INVALID_ARGUMENT, "scale: n*c must be <= 65535");
     DeviceGuard g(cx);
     by_dtype(X.dtype, "scale", [&](auto tag) {
       using T = decltype(tag);
-      scale_fwd<T><<<blocks(int64_t(cnt)), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(G), B ? P<T>(*B) : nullptr,
-                                                                          P<T>(Y), c, hw, int64_t(cnt));
+      scale_fwd<T><<<plane_grid(n, c, hw), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(G),
+                                                                          B ? P<T>(*B) : nullptr, P<T>(Y), c, hw);
     });
     check_launch("scale_fwd");
     count_launch(cx);
@@ -392,17 +399,22 @@ int cdnn_scale_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_han
     const uint64_t cnt = uint64_t(n) * c * hw;
     require_len(X, cnt, "scale_bwd"); require_len(DY, cnt, "scale_bwd"); require_len(G, uint64_t(c), "scale_bwd");
     if (DX) require_len(*DX, cnt, "scale_bwd dx");
+    if (n * c > 65535) fail(CDNN_INVALID_ARGUMENT, "scale_bwd: n*c must be <= 65535");
     DeviceGuard g(cx);
     cudaStream_t st = stream_of(cx, stream);
     by_dtype(X.dtype, "scale_bwd", [&](auto tag) {
       using T = decltype(tag);
       if (DG || DB) {
-        scale_bwd_params<T><<<c, kT, 0, st>>>(P<T>(X), P<T>(DY), DG ? P<T>(*DG) : nullptr, DB ? P<T>(*DB) : nullptr, n,
-                                              c, hw);
-        count_launch(cx);
+        const int splits = chan_splits(n, c, hw);
+        double2* part =
+            static_cast<double2*>(workspace_of(cx, stream).get(size_t(c) * splits * sizeof(double2), cx->device));
+        chan_partials<T, kSumDot><<<dim3(c, splits), kT, 0, st>>>(P<T>(DY), P<T>(X), part, n, c, hw, splits);
+        scale_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, DG ? P<T>(*DG) : nullptr,
+                                                          DB ? P<T>(*DB) : nullptr);
+        count_launch(cx, 2);
       }
       if (DX) {
-        scale_bwd_data<T><<<blocks(int64_t(cnt)), kT, 0, st>>>(P<T>(DY), P<T>(G), P<T>(*DX), c, hw, int64_t(cnt));
+        scale_bwd_data<T><<<plane_grid(n, c, hw), kT, 0, st>>>(P<T>(DY), P<T>(G), P<T>(*DX), c, hw);
         count_launch(cx);
       }
     });
