@@ -8,6 +8,8 @@
 // all-reduce (sum over ranks).
 #pragma once
 
+#include <cstdint>
+#include <span>
 #include <vector>
 
 #include "polegrad/net.hpp"
@@ -46,6 +48,17 @@ class Solver {
   // Solver state for checkpoints (momentum / RMSProp history, arena order).
   std::vector<real> history() const;
   void set_history(std::span<const real> h);
+  std::uint64_t iterations() const { return iterations_; }
+
+  // Checkpoint of the solver state (the reference saves none):
+  //   "MCSS", u32 version (1), u32 method (0 sgd, 1 rmsprop), u64 updates,
+  //   u64 n, n x f64 history (arena order; n = 0 for a stateless solver or
+  //   before the first update) — little endian, values widened to f64 like MCWT.
+  // restore_state() may run before the first update (the history is then
+  // installed on the next apply_update); FormatError on a malformed payload,
+  // InvalidState when the method or the parameter count does not match.
+  std::vector<std::uint8_t> snapshot_state() const;
+  void restore_state(std::span<const std::uint8_t> bytes);
 
  private:
   SolverConfig config_;
@@ -54,6 +67,8 @@ class Solver {
   Handle history_{};
   std::size_t history_len_ = 0;
   std::size_t history_params_ = 0;
+  std::uint64_t iterations_ = 0;
+  std::vector<real> pending_;  // restored history awaiting the first update
 };
 
 // True when every parameter gradient of the net is exactly zero.

@@ -60,6 +60,11 @@ PG_API int pg_solver_create(int method, double lr, double momentum, double weigh
                             double epsilon, pg_solver** out);
 PG_API int pg_solver_free(pg_solver* s);
 PG_API int pg_solver_apply(pg_solver* s, pg_net* net);
+/* solver-state checkpoint ("MCSS": update count + momentum / RMSProp history);
+ * call with buf = NULL to learn *len.  Restore before or after the first update. */
+PG_API int pg_solver_snapshot(pg_solver* s, uint8_t* buf, uint64_t cap, uint64_t* len);
+PG_API int pg_solver_restore(pg_solver* s, const uint8_t* buf, uint64_t len);
+PG_API int pg_solver_iterations(pg_solver* s, uint64_t* out);
 
 /* Captures one training step  feed(H2D from `data`/`labels`) -> forward ->
  * backward -> solver update -> D2H of the loss into `loss_out`  into a CUDA

@@ -205,6 +205,22 @@ int pg_solver_free(pg_solver* s) { return run([&] { delete s; }); }
 
 int pg_solver_apply(pg_solver* s, pg_net* n) { return run([&] { s->solver->apply_update(net_of(n)); }); }
 
+int pg_solver_snapshot(pg_solver* s, uint8_t* buf, uint64_t cap, uint64_t* len) {
+  return run([&] {
+    const auto bytes = s->solver->snapshot_state();
+    *len = bytes.size();
+    if (buf && cap >= bytes.size()) std::memcpy(buf, bytes.data(), bytes.size());
+  });
+}
+
+int pg_solver_restore(pg_solver* s, const uint8_t* buf, uint64_t len) {
+  return run([&] { s->solver->restore_state(std::span<const std::uint8_t>(buf, len)); });
+}
+
+int pg_solver_iterations(pg_solver* s, uint64_t* out) {
+  return run([&] { *out = s->solver->iterations(); });
+}
+
 int pg_step_capture(pg_net* n, pg_solver* s, const void* data, const void* labels, void* loss_out, uint64_t* graph) {
   return run([&] {
     polegrad::Net& net = net_of(n);

@@ -2,6 +2,9 @@
 // (reference: solver.cpp:10-68).
 #include "polegrad/solver.hpp"
 
+#include <bit>
+#include <cstring>
+
 #include "polegrad/errors.hpp"
 #include "polegrad/parallel.hpp"
 
@@ -35,6 +38,11 @@ void Solver::apply_update(Net& net) {
       history_len_ = net.param_total();
       history_params_ = params.size();
       hist_reg_ = net.registry();
+      if (!pending_.empty()) {
+        if (pending_.size() != history_len_) throw InvalidState("solver: restored history does not match the net");
+        reg.write(history_, pending_);
+        pending_.clear();
+      }
     } else if (net.param_total() != history_len_ || params.size() != history_params_) {
       throw InvalidState("solver: net parameter count changed mid-run");
     } else if (hist_reg_ != net.registry()) {
@@ -65,6 +73,55 @@ void Solver::apply_update(Net& net) {
     p->overwrite_gpu_data();
     p->overwrite_gpu_diff();
   }
+  ++iterations_;
+}
+
+std::vector<std::uint8_t> Solver::snapshot_state() const {
+  std::vector<std::uint8_t> out{'M', 'C', 'S', 'S'};
+  auto put = [&](std::uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) out.push_back(std::uint8_t(v >> (8 * i)));
+  };
+  put(1, 4);
+  put(config_.method == SolverMethod::kRmsProp ? 1 : 0, 4);
+  put(iterations_, 8);
+  const std::vector<real> h = history_ ? hist_reg_->read(history_) : pending_;
+  put(h.size(), 8);
+  for (real v : h) put(std::bit_cast<std::uint64_t>(static_cast<double>(v)), 8);
+  return out;
+}
+
+void Solver::restore_state(std::span<const std::uint8_t> b) {
+  std::size_t pos = 0;
+  auto need = [&](std::size_t n) {
+    if (b.size() - pos < n) throw FormatError("solver state: truncated payload");
+  };
+  auto get = [&](int bytes) {
+    need(std::size_t(bytes));
+    std::uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= std::uint64_t(b[pos + i]) << (8 * i);
+    pos += std::size_t(bytes);
+    return v;
+  };
+  need(4);
+  if (std::memcmp(b.data(), "MCSS", 4) != 0) throw FormatError("solver state: bad magic");
+  pos = 4;
+  if (get(4) != 1) throw FormatError("solver state: unsupported version");
+  const std::uint64_t method = get(4);
+  if (method != (config_.method == SolverMethod::kRmsProp ? 1u : 0u))
+    throw InvalidState("solver state: saved by a different update rule");
+  const std::uint64_t iters = get(8);
+  const std::uint64_t n = get(8);
+  if (n > (b.size() - pos) / 8) throw FormatError("solver state: truncated payload");
+  std::vector<real> h(n);
+  for (auto& v : h) v = static_cast<real>(std::bit_cast<double>(get(8)));
+  if (pos != b.size()) throw FormatError("solver state: trailing bytes");
+  if (history_) {
+    if (n != history_len_) throw InvalidState("solver state: history length does not match the net");
+    hist_reg_->write(history_, h);
+  } else {
+    pending_ = std::move(h);
+  }
+  iterations_ = iters;
 }
 
 std::vector<real> Solver::history() const {

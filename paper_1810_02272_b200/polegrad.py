@@ -32,7 +32,8 @@ EXPORTS = [
     "pg_solver_create", "pg_solver_free", "pg_solver_apply", "pg_step_capture", "pg_step_replay", "pg_graph_free",
     "pg_net_profile",
     "pg_parallel_unique_id", "pg_parallel_create", "pg_parallel_free", "pg_parallel_broadcast",
-    "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip",
+    "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip", "pg_solver_snapshot",
+    "pg_solver_restore", "pg_solver_iterations",
 ]
 
 
@@ -64,7 +65,8 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_pool_mask": ([vp, cp, C.POINTER(C.c_int32), u64], i),
             "pg_snapshot": ([vp, vp, u64, C.POINTER(u64)], i), "pg_restore": ([vp, vp, u64], i),
             "pg_solver_create": ([i, d, d, d, d, d, C.POINTER(vp)], i), "pg_solver_free": ([vp], i),
-            "pg_solver_apply": ([vp, vp], i),
+            "pg_solver_apply": ([vp, vp], i), "pg_solver_snapshot": ([vp, vp, u64, C.POINTER(u64)], i),
+            "pg_solver_restore": ([vp, vp, u64], i), "pg_solver_iterations": ([vp, C.POINTER(u64)], i),
             "pg_step_capture": ([vp, vp, vp, vp, vp, C.POINTER(u64)], i), "pg_step_replay": ([vp, u64], i),
             "pg_graph_free": ([vp, u64], i), "pg_parallel_unique_id": ([cp], i),
             "pg_net_profile": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
@@ -275,6 +277,24 @@ class Solver:
 
     def set_parallel(self, par: Optional["Parallel"]) -> None:
         _check(self.lib, self.lib.pg_solver_set_parallel(self.ptr, par.ptr if par else None))
+
+    def snapshot(self) -> bytes:
+        """Solver-state checkpoint ("MCSS": update count + momentum / RMSProp history)."""
+        n = C.c_uint64()
+        _check(self.lib, self.lib.pg_solver_snapshot(self.ptr, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        _check(self.lib, self.lib.pg_solver_snapshot(self.ptr, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
+    def restore(self, blob: bytes) -> None:
+        b = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(self.lib, self.lib.pg_solver_restore(self.ptr, b, len(blob)))
+
+    @property
+    def iterations(self) -> int:
+        v = C.c_uint64()
+        _check(self.lib, self.lib.pg_solver_iterations(self.ptr, C.byref(v)))
+        return v.value
 
     def close(self) -> None:
         if self.ptr:
