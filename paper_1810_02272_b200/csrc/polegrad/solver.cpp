@@ -64,7 +64,8 @@ void Solver::apply_update(Net& net) {
   const auto& c = config_;
   cdnn_ok(cdnn_solver_apply(reg.context(),
                             c.method == SolverMethod::kRmsProp ? CDNN_SOLVER_RMSPROP : CDNN_SOLVER_SGD,
-                            reg.in(net.weight_arena()), reg.in(net.grad_arena()), stateful ? reg.in(history_) : 0,
+                            reg.inout(net.weight_arena()), reg.inout(net.grad_arena()),
+                            stateful ? reg.inout(history_) : 0,
                             net.param_total(), static_cast<double>(c.learning_rate), static_cast<double>(c.momentum),
                             static_cast<double>(c.weight_decay), static_cast<double>(c.rms_decay),
                             static_cast<double>(c.epsilon), reg.stream()),
