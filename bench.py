@@ -14,8 +14,8 @@ rank per GPU, NCCL gradient all-reduce (weak scaling: batch 100 per GPU).
 * e2e        images/s through the public API with host buffers: each step copies
              that step's batch into pinned memory, replays the graph whose first
              node is the H2D copy and last node the D2H of the loss, and reads
-             the loss; two pinned buffers let the host stage batch i+1 while
-             step i runs.
+             the loss; polegrad.FeedRing (two pinned slots) lets the host stage
+             batch i+1 while step i runs.
 * roofline   the dominant kernel (per-layer event profile of one eager step).
 * cpu_baseline  the reference CPU implementation (oracle/_ref: unmodified
              reference core + reference-style conv/pool/loss extension, 1 thread)
@@ -372,44 +372,34 @@ def run_b200(args) -> None:
     value = world * BATCH * args.steps / (total_ms / 1000.0)
 
     # ---- e2e: host buffers through the public API (H2D in, loss D2H out, every step)
-    # Graph path is software-pipelined over two pinned input/loss buffers: while
-    # step i runs, the host stages batch i+1 into the other buffer and enqueues
-    # step i+1 (its graph begins with that H2D copy); step i's loss is read once
-    # it completes.  Every step still copies its own inputs and reads its loss.
+    # Graph path: polegrad.FeedRing (pinned-memory feed ring):
+    # push() stages batch i+1 into a free pinned slot while step i runs, each
+    # slot's captured step starts with its H2D copy and ends with the loss D2H;
+    # pop_loss() reads every step's loss.
     e_start, e_end = cx.event(), cx.event()
     if use_graph:
-        pins = [(pin_x, pin_y, pin_loss),
-                (cudadnn.PinnedBuffer((BATCH,) + IMG), cudadnn.PinnedBuffer((BATCH,)), cudadnn.PinnedBuffer((1,)))]
-        graphs = [g_e2e, polegrad.StepGraph(net, solver, pins[1][0].ptr, pins[1][1].ptr, pins[1][2].ptr)]
+        ring = polegrad.FeedRing(net, solver, 2)
 
-        def fill(b, i):
-            pins[b][0].array[...] = host_x[i % nb]
-            pins[b][1].array[...] = host_y[i % nb]
-
-        def run_pipelined(n, sink):
-            sev = [(cx.event(), cx.event()) for _ in range(n)]
-            fill(0, 0)
-            cx.record(sev[0][0])
-            graphs[0].replay()
-            cx.record(sev[0][1])
+        def run_ring(n, sink):
+            inflight = 0
             for i in range(n):
-                b = i & 1
-                if i + 1 < n:
-                    fill(b ^ 1, i + 1)
-                    cx.record(sev[i + 1][0])
-                    graphs[b ^ 1].replay()
-                    cx.record(sev[i + 1][1])
-                cx.elapsed(sev[i][0], sev[i][1])  # waits for step i
-                sink.append(float(pins[b][2].array[0]))
+                if inflight == 2:
+                    sink.append(ring.pop_loss())
+                    inflight -= 1
+                ring.push(host_x[i % nb], host_y[i % nb])
+                inflight += 1
+            while inflight:
+                sink.append(ring.pop_loss())
+                inflight -= 1
 
-        run_pipelined(max(2, args.warmup), [])
+        run_ring(max(2, args.warmup), [])
         net.sync()
         barrier()
         net.sync()
         losses = []
         t0 = time.perf_counter()
         cx.record(e_start)
-        run_pipelined(args.steps, losses)
+        run_ring(args.steps, losses)
         cx.record(e_end)
         net.sync()
     else:

@@ -162,6 +162,8 @@ CDNN_API int cdnn_event_create(cdnn_ctx ctx, cdnn_handle* out);
 CDNN_API int cdnn_event_record(cdnn_ctx ctx, cdnn_handle ev, cdnn_handle stream);
 CDNN_API int cdnn_event_elapsed(cdnn_ctx ctx, cdnn_handle start, cdnn_handle end, float* ms);
 CDNN_API int cdnn_event_free(cdnn_ctx ctx, cdnn_handle ev);
+/* host waits until the work captured by the event's last record has completed */
+CDNN_API int cdnn_event_sync(cdnn_ctx ctx, cdnn_handle ev);
 
 /* ---- RNG subsystem (host mt19937_64, backend.hpp:31-45) ------------------ */
 CDNN_API int cdnn_rng_create(cdnn_ctx ctx, uint64_t seed, cdnn_handle* out);

@@ -89,6 +89,13 @@ class Net {
   // Treat the data layer's current top contents as this step's batch (inputs
   // already resident in HBM; no feed copy).
   void reuse_resident_batch();
+  // Zero every parameter gradient on the device (one fill over the grad arena).
+  void zero_param_diffs();
+  // First MemoryData layer (the feed), or nullptr.
+  MemoryDataLayer* feed_layer();
+  // After replaying a captured step: every blob's and parameter's device copy
+  // is newest (replays bypass the host-side coherence records).
+  void mark_device_fresh();
   // One eager step with device events between layers: per-layer forward and
   // backward milliseconds (layer order) — the kernel-share breakdown.
   void profile_layers(std::vector<float>& fwd_ms, std::vector<float>& bwd_ms);

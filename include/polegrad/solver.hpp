@@ -49,6 +49,11 @@ class Solver {
   std::vector<real> history() const;
   void set_history(std::span<const real> h);
   std::uint64_t iterations() const { return iterations_; }
+  // Allocate the history (and install a restored one) without updating, so a
+  // following graph capture performs no allocation.
+  void prepare(Net& net);
+  // Bookkeeping for captured updates: captures are not updates, replays are.
+  void uncount_updates(std::int64_t n) { iterations_ = std::uint64_t(std::int64_t(iterations_) - n); }
 
   // Checkpoint of the solver state (the reference saves none):
   //   "MCSS", u32 version (1), u32 method (0 sgd, 1 rmsprop), u64 updates,

@@ -23,6 +23,7 @@ extern "C" {
 
 typedef struct pg_net pg_net;
 typedef struct pg_solver pg_solver;
+typedef struct pg_feed_ring pg_feed_ring;
 typedef struct pg_parallel pg_parallel;
 
 PG_API const char* pg_last_error(void);
@@ -65,6 +66,16 @@ PG_API int pg_solver_apply(pg_solver* s, pg_net* net);
 PG_API int pg_solver_snapshot(pg_solver* s, uint8_t* buf, uint64_t cap, uint64_t* len);
 PG_API int pg_solver_restore(pg_solver* s, const uint8_t* buf, uint64_t len);
 PG_API int pg_solver_iterations(pg_solver* s, uint64_t* out);
+
+/* pinned-memory feed ring (include/polegrad/feed.hpp): depth captured steps, each
+ * H2D(slot) -> forward -> backward -> update -> D2H(loss).  push() stages a batch
+ * (labels may be NULL for label-less feeds) into a free slot and enqueues its step;
+ * pop_loss() waits for the oldest step and returns its loss. */
+PG_API int pg_feed_ring_create(pg_net* net, pg_solver* s, int depth, pg_feed_ring** out);
+PG_API int pg_feed_ring_free(pg_feed_ring* r);
+PG_API int pg_feed_ring_push(pg_feed_ring* r, const void* data, uint64_t n_data, const void* labels,
+                             uint64_t n_labels);
+PG_API int pg_feed_ring_pop_loss(pg_feed_ring* r, double* loss);
 
 /* Captures one training step  feed(H2D from `data`/`labels`) -> forward ->
  * backward -> solver update -> D2H of the loss into `loss_out`  into a CUDA

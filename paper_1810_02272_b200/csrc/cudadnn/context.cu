@@ -606,6 +606,14 @@ int cdnn_event_elapsed(cdnn_ctx ctx, cdnn_handle start, cdnn_handle end, float* 
     CDNN_CUDA(cudaEventElapsedTime(ms, a.ev, b.ev));
   });
 }
+int cdnn_event_sync(cdnn_ctx ctx, cdnn_handle ev) {
+  return guard([&] {
+    Ctx* c = need_ctx(ctx);
+    EventSlot& e = slot_as<EventSlot>(c, ev, "event_sync", "event");
+    DeviceGuard g(c);
+    CDNN_CUDA(cudaEventSynchronize(e.ev));
+  });
+}
 int cdnn_event_free(cdnn_ctx ctx, cdnn_handle ev) {
   return guard([&] {
     Ctx* c = need_ctx(ctx);

@@ -9,6 +9,7 @@
 #include "polegrad/prototxt.hpp"
 #include "polegrad/solver.hpp"
 #include "polegrad_c.h"
+#include "polegrad/feed.hpp"
 
 struct pg_net {
   std::unique_ptr<polegrad::Net> net;
@@ -221,6 +222,29 @@ int pg_solver_iterations(pg_solver* s, uint64_t* out) {
   return run([&] { *out = s->solver->iterations(); });
 }
 
+struct pg_feed_ring {
+  std::unique_ptr<polegrad::FeedRing> ring;
+};
+
+int pg_feed_ring_create(pg_net* n, pg_solver* s, int depth, pg_feed_ring** out) {
+  return run([&] {
+    auto r = std::make_unique<pg_feed_ring>();
+    r->ring = std::make_unique<polegrad::FeedRing>(net_of(n), *s->solver, depth);
+    *out = r.release();
+  });
+}
+
+int pg_feed_ring_free(pg_feed_ring* r) { return run([&] { delete r; }); }
+
+int pg_feed_ring_push(pg_feed_ring* r, const void* data, uint64_t n_data, const void* labels, uint64_t n_labels) {
+  return run([&] {
+    r->ring->push(std::span<const real>(static_cast<const real*>(data), n_data),
+                  std::span<const real>(static_cast<const real*>(labels), labels ? n_labels : 0));
+  });
+}
+
+int pg_feed_ring_pop_loss(pg_feed_ring* r, double* loss) { return run([&] { *loss = r->ring->pop_loss(); }); }
+
 int pg_step_capture(pg_net* n, pg_solver* s, const void* data, const void* labels, void* loss_out, uint64_t* graph) {
   return run([&] {
     polegrad::Net& net = net_of(n);
@@ -266,6 +290,7 @@ int pg_step_replay(pg_net* n, uint64_t graph) {
   return run([&] {
     polegrad::Registry& reg = *net_of(n).registry();
     cdnn_ok(cdnn_graph_launch(reg.context(), graph, reg.stream()), "step replay");
+    net_of(n).mark_device_fresh();
   });
 }
 

@@ -1,0 +1,105 @@
+// feed.cpp — pinned-memory feed ring (include/polegrad/feed.hpp).
+#include "polegrad/feed.hpp"
+
+#include <cstring>
+
+#include "polegrad/errors.hpp"
+#include "polegrad/layers.hpp"
+
+namespace polegrad {
+
+FeedRing::FeedRing(Net& net, Solver& solver, int depth) : net_(net), solver_(solver) {
+  if (depth < 1) throw InvalidArgument("feed ring: depth must be >= 1");
+  MemoryDataLayer* feed = net.feed_layer();
+  if (!feed) throw ModelError("feed ring: the net has no MemoryData layer");
+  if (net.loss_blobs().empty()) throw InvalidState("feed ring: the net has no loss top");
+  data_len_ = std::size_t(feed->batch_size()) * feed->sample_size();
+  label_len_ = feed->spec().tops.size() > 1 ? std::size_t(feed->batch_size()) : 0;
+  Registry& reg = *net.registry();
+  cdnn_ctx ctx = reg.context();
+  try {
+    slots_.resize(std::size_t(depth));
+    for (Slot& s : slots_) {
+      void* p = nullptr;
+      cdnn_ok(cdnn_host_alloc_pinned((data_len_ + label_len_ + 1) * sizeof(real), &p), "feed ring");
+      s.data = static_cast<real*>(p);
+      s.labels = label_len_ ? s.data + data_len_ : nullptr;
+      s.loss = s.data + data_len_ + label_len_;
+      std::memset(p, 0, (data_len_ + label_len_ + 1) * sizeof(real));
+      cdnn_ok(cdnn_event_create(ctx, &s.done), "feed ring");
+    }
+    // One eager forward/backward on a zero batch creates every lazily allocated
+    // resource (workspaces, tensor maps, repacked weights) outside the capture;
+    // its gradients are discarded and the solver history is allocated without
+    // an update, so the weights are untouched.
+    net.set_batch(slots_[0].data, slots_[0].labels);
+    if (!net.graph_safe()) throw InvalidState("feed ring: net has host-side layers (loss hooks / FIFO feed)");
+    net.forward();
+    net.backward();
+    net.zero_param_diffs();
+    solver.prepare(net);
+    reg.synchronize();
+    for (Slot& s : slots_) {
+      // capture: H2D(slot) -> forward -> backward -> update -> D2H(loss)
+      cdnn_ok(cdnn_graph_begin(ctx, reg.stream()), "feed ring capture");
+      try {
+        net.set_batch(s.data, s.labels);
+        net.forward();
+        net.backward();
+        solver.apply_update(net);
+        cdnn_ok(cdnn_read_async(ctx, net.loss_blobs()[0]->gpu_data(), 0, s.loss, 1, reg.stream()), "feed ring");
+      } catch (...) {
+        cdnn_handle dead = 0;
+        cdnn_graph_end(ctx, reg.stream(), &dead);
+        if (dead) cdnn_graph_free(ctx, dead);
+        throw;
+      }
+      cdnn_ok(cdnn_graph_end(ctx, reg.stream(), &s.graph), "feed ring capture");
+    }
+    solver.uncount_updates(std::uint64_t(depth));  // captures are not updates
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+FeedRing::~FeedRing() { release(); }
+
+void FeedRing::release() noexcept {
+  Registry& reg = *net_.registry();
+  try { reg.synchronize(); } catch (...) {}
+  for (Slot& s : slots_) {
+    if (s.graph) cdnn_graph_free(reg.context(), s.graph);
+    if (s.done) cdnn_event_free(reg.context(), s.done);
+    if (s.data) cdnn_host_free_pinned(s.data);
+    s = Slot{};
+  }
+  slots_.clear();
+}
+
+void FeedRing::push(std::span<const real> data, std::span<const real> labels) {
+  if (data.size() != data_len_) throw InvalidArgument("feed ring: batch has the wrong number of values");
+  if (labels.size() != label_len_) throw InvalidArgument("feed ring: wrong number of labels");
+  if (pushed_ - popped_ >= slots_.size()) throw InvalidState("feed ring: full, pop_loss() first");
+  Slot& s = slots_[pushed_ % slots_.size()];
+  // the slot's previous step was popped, so its graph has finished reading it
+  std::memcpy(s.data, data.data(), data_len_ * sizeof(real));
+  if (label_len_) std::memcpy(s.labels, labels.data(), label_len_ * sizeof(real));
+  Registry& reg = *net_.registry();
+  cdnn_ok(cdnn_graph_launch(reg.context(), s.graph, reg.stream()), "feed ring push");
+  cdnn_ok(cdnn_event_record(reg.context(), s.done, reg.stream()), "feed ring push");
+  ++pushed_;
+  solver_.uncount_updates(-1);  // one real update
+}
+
+double FeedRing::pop_loss() {
+  if (pushed_ == popped_) throw InvalidState("feed ring: no step in flight");
+  Slot& s = slots_[popped_ % slots_.size()];
+  cdnn_ok(cdnn_event_sync(net_.registry()->context(), s.done), "feed ring pop");
+  ++popped_;
+  // the graph's kernels bypassed the blob coherence records: device is newest
+  net_.mark_device_fresh();
+  return static_cast<double>(*s.loss);
+}
+
+}  // namespace polegrad

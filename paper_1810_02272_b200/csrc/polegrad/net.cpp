@@ -284,6 +284,30 @@ void Net::set_batch(const real* data, const real* labels) {
   throw ModelError("set_batch: net has no MemoryData layer");
 }
 
+void Net::zero_param_diffs() {
+  if (!param_total_) return;
+  Registry& reg = *registry_;
+  cdnn_ok(cdnn_fill(reg.context(), reg.out(grad_arena_), param_total_, 0.0, reg.stream()), "zero_param_diffs");
+  for (Blob* p : params_) p->overwrite_gpu_diff();
+}
+
+MemoryDataLayer* Net::feed_layer() {
+  for (auto& l : layers_)
+    if (auto* md = dynamic_cast<MemoryDataLayer*>(l.get())) return md;
+  return nullptr;
+}
+
+void Net::mark_device_fresh() {
+  for (auto& b : blobs_) {
+    b->overwrite_gpu_data();
+    b->overwrite_gpu_diff();
+  }
+  for (Blob* p : params_) {
+    p->overwrite_gpu_data();
+    p->overwrite_gpu_diff();
+  }
+}
+
 void Net::reuse_resident_batch() {
   for (std::size_t i = 0; i < layers_.size(); ++i) {
     if (auto* md = dynamic_cast<MemoryDataLayer*>(layers_[i].get())) {

@@ -27,7 +27,7 @@ Solver::~Solver() {
   }
 }
 
-void Solver::apply_update(Net& net) {
+void Solver::prepare(Net& net) {
   const auto& params = net.params();
   if (params.empty()) return;
   Registry& reg = *net.registry();
@@ -54,6 +54,14 @@ void Solver::apply_update(Net& net) {
       reg.write(history_, h);
     }
   }
+}
+
+void Solver::apply_update(Net& net) {
+  const auto& params = net.params();
+  if (params.empty()) return;
+  Registry& reg = *net.registry();
+  const bool stateful = config_.method == SolverMethod::kRmsProp || config_.momentum != real(0);
+  prepare(net);
   if (parallel_) parallel_->reduce_gradients(net);
   // Make every parameter view current on the device, run one kernel over the
   // arenas, then mark the views device-newest (their host mirrors are stale).

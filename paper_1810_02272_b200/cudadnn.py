@@ -38,7 +38,7 @@ EXPORTS = [
     "cdnn_read_async", "cdnn_host_alloc_pinned", "cdnn_host_free_pinned", "cdnn_stream_create",
     "cdnn_stream_free", "cdnn_stream_sync", "cdnn_stream_wait", "cdnn_graph_begin", "cdnn_graph_end",
     "cdnn_graph_launch", "cdnn_graph_free", "cdnn_event_create", "cdnn_event_record", "cdnn_event_elapsed",
-    "cdnn_event_free", "cdnn_rng_create", "cdnn_rng_next_u64", "cdnn_rng_uniform", "cdnn_subsystem_free",
+    "cdnn_event_free", "cdnn_event_sync", "cdnn_rng_create", "cdnn_rng_next_u64", "cdnn_rng_uniform", "cdnn_subsystem_free",
     "cdnn_conv_desc_create", "cdnn_conv_output_shape", "cdnn_pool_desc_create", "cdnn_pool_output_shape",
     "cdnn_desc_free", "cdnn_dispatch", "cdnn_fill", "cdnn_copy", "cdnn_scal", "cdnn_axpy", "cdnn_dot",
     "cdnn_gemm", "cdnn_ip_forward", "cdnn_ip_backward", "cdnn_conv_forward", "cdnn_conv_backward_data",
@@ -101,6 +101,7 @@ def load() -> C.CDLL:
             "cdnn_graph_launch": ([vp, h, h], i), "cdnn_graph_free": ([vp, h], i),
             "cdnn_event_create": ([vp, ph], i), "cdnn_event_record": ([vp, h, h], i),
             "cdnn_event_elapsed": ([vp, h, h, C.POINTER(C.c_float)], i), "cdnn_event_free": ([vp, h], i),
+            "cdnn_event_sync": ([vp, h], i),
             "cdnn_rng_create": ([vp, u64, ph], i), "cdnn_rng_next_u64": ([vp, h, pu64], i),
             "cdnn_rng_uniform": ([vp, h, h, u64, d, d], i), "cdnn_subsystem_free": ([vp, h], i),
             "cdnn_conv_desc_create": ([vp, C.POINTER(ConvParams), ph], i),

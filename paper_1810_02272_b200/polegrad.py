@@ -33,7 +33,8 @@ EXPORTS = [
     "pg_net_profile",
     "pg_parallel_unique_id", "pg_parallel_create", "pg_parallel_free", "pg_parallel_broadcast",
     "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip", "pg_solver_snapshot",
-    "pg_solver_restore", "pg_solver_iterations",
+    "pg_solver_restore", "pg_solver_iterations", "pg_feed_ring_create", "pg_feed_ring_free", "pg_feed_ring_push",
+    "pg_feed_ring_pop_loss",
 ]
 
 
@@ -67,6 +68,8 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_solver_create": ([i, d, d, d, d, d, C.POINTER(vp)], i), "pg_solver_free": ([vp], i),
             "pg_solver_apply": ([vp, vp], i), "pg_solver_snapshot": ([vp, vp, u64, C.POINTER(u64)], i),
             "pg_solver_restore": ([vp, vp, u64], i), "pg_solver_iterations": ([vp, C.POINTER(u64)], i),
+            "pg_feed_ring_create": ([vp, vp, i, C.POINTER(vp)], i), "pg_feed_ring_free": ([vp], i),
+            "pg_feed_ring_push": ([vp, vp, u64, vp, u64], i), "pg_feed_ring_pop_loss": ([vp, C.POINTER(d)], i),
             "pg_step_capture": ([vp, vp, vp, vp, vp, C.POINTER(u64)], i), "pg_step_replay": ([vp, u64], i),
             "pg_graph_free": ([vp, u64], i), "pg_parallel_unique_id": ([cp], i),
             "pg_net_profile": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
@@ -321,6 +324,44 @@ class StepGraph:
 
     def replay(self) -> None:
         _check(self.net.lib, self.net.lib.pg_step_replay(self.net.ptr, self.graph))
+
+
+class FeedRing:
+    """polegrad::FeedRing — pinned-memory feed ring of `depth` captured steps
+    (H2D(slot) -> forward -> backward -> update -> D2H(loss)); push() stages the
+    next batch on the host while earlier steps run, pop_loss() returns losses
+    in push order."""
+
+    def __init__(self, net: Net, solver: "Solver", depth: int = 2):
+        self.net = net
+        self.lib = net.lib
+        self._keep = solver
+        p = C.c_void_p()
+        _check(self.lib, self.lib.pg_feed_ring_create(net.ptr, solver.ptr, depth, C.byref(p)))
+        self.ptr = p
+
+    def push(self, data: np.ndarray, labels: Optional[np.ndarray] = None) -> None:
+        x = np.ascontiguousarray(data, dtype=self.net.np)
+        y = None if labels is None else np.ascontiguousarray(labels, dtype=self.net.np)
+        _check(self.lib, self.lib.pg_feed_ring_push(self.ptr, x.ctypes.data, x.size,
+                                                    None if y is None else y.ctypes.data,
+                                                    0 if y is None else y.size))
+
+    def pop_loss(self) -> float:
+        v = C.c_double()
+        _check(self.lib, self.lib.pg_feed_ring_pop_loss(self.ptr, C.byref(v)))
+        return v.value
+
+    def close(self) -> None:
+        if self.ptr:
+            _check(self.lib, self.lib.pg_feed_ring_free(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Parallel:

@@ -58,3 +58,53 @@ def test_restore_rejects_other_rule():
     other = polegrad.Solver(net, method="sgd", lr=1e-3, momentum=0.9)
     with pytest.raises(Exception, match="different update rule"):
         other.restore(blob)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_feed_ring_matches_eager_steps(depth):
+    """The pinned feed ring trains exactly like eager steps."""
+    text = polegrad.load_model("cifar10_quick")
+    batches = synthetic_batches((100, 3, 32, 32), 10, 6, seed=8)
+    kw = CONFIGS["cifar10_quick"][1]
+    a = polegrad.Net(text, 1, "f32")
+    sa = polegrad.Solver(a, **kw)
+    b = polegrad.Net(text, 1, "f32")
+    sb = polegrad.Solver(b, **kw)
+    eager = []
+    for x, y in batches:
+        a.set_batch(x, y)
+        a.forward()
+        eager.append(a.loss())
+        a.backward()
+        sa.apply()
+    ring = polegrad.FeedRing(b, sb, depth)
+    got, inflight = [], 0
+    for x, y in batches:
+        if inflight == depth:
+            got.append(ring.pop_loss())
+            inflight -= 1
+        ring.push(x, y)
+        inflight += 1
+    while inflight:
+        got.append(ring.pop_loss())
+        inflight -= 1
+    assert [np.float32(v) for v in got] == [np.float32(v) for v in eager]
+    for i in range(len(a.param_info())):
+        assert np.array_equal(a.param(i), b.param(i))
+    with pytest.raises(Exception, match="no step in flight"):
+        ring.pop_loss()
+    ring.close()
+
+
+def test_feed_ring_rejects_overfill():
+    text = polegrad.load_model("cifar10_quick")
+    net = polegrad.Net(text, 1, "f32")
+    s = polegrad.Solver(net, method="sgd", lr=1e-3)
+    ring = polegrad.FeedRing(net, s, 1)
+    (x, y), = synthetic_batches((100, 3, 32, 32), 10, 1)
+    ring.push(x, y)
+    with pytest.raises(Exception, match="full"):
+        ring.push(x, y)
+    ring.pop_loss()
+    with pytest.raises(Exception, match="wrong number"):
+        ring.push(x[:50], y)
