@@ -110,7 +110,13 @@ template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tap_kernel(const __grid_constant__ CUtensorMap tm_w_hi, const __grid_constant__ CUtensorMap tm_w_lo,
                     const TapArgs a) {
-  constexpr uint32_t TMEM_COLS = tc::tmem_cols_for(2 * BN);
+  // 3xTF32 with BN <= 64: one MMA against [B_hi | B_lo] (N = 2*BN) gives A_hi*B_hi
+  // and A_hi*B_lo in two column halves, a second adds A_lo*B_hi into the first;
+  // the epilogue sums the halves.  2 MMAs per k-step instead of 3 and a third
+  // less A traffic (the A operand's shared-memory reads bound N <= 64 tiles).
+  constexpr bool CAT = SPLIT && BN <= 64;
+  constexpr int ACC = CAT ? 2 * BN : BN;  // accumulator columns per buffer
+  constexpr uint32_t TMEM_COLS = tc::tmem_cols_for(2 * ACC);
   constexpr uint32_t B_STAGE = b_stage_bytes(BN, SPLIT);
   constexpr uint32_t B_HALF = uint32_t(BN) * 128u;
 
@@ -179,6 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = tc::make_idesc_tf32(BN);  // A, B K-major
+      constexpr uint32_t idesc_cat = tc::make_idesc_tf32(2 * BN);
       int stage = 0;
       uint32_t phase = 0;
       int aseq = 0, ts = 0;
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int acc_buf = ts & 1;
         if (ts >= 2) ptx::mbar_wait(&t_empty[acc_buf], uint32_t((ts >> 1) - 1) & 1u);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem + uint32_t(acc_buf * BN);
+        const uint32_t d_tmem = tmem + uint32_t(acc_buf * ACC);
         bool first = true;
         for (int cb = 0; cb < a.cblocks; ++cb, ++aseq) {
           const int buf = aseq % a.nbuf;
@@ -210,12 +217,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (j < nk8) {
                 const uint64_t kj = uint64_t(j) * 2u;  // +32 B per k8 step
                 uint32_t acc = first ? 0u : 1u;
-                if constexpr (SPLIT) {
-                  ptx::mma_tf32(d_tmem, dAl + shift + kj, dB + kj, idesc, acc);
-                  ptx::mma_tf32(d_tmem, dA + shift + kj, dBl + kj, idesc, 1u);
-                  acc = 1u;
+                if constexpr (CAT) {
+                  // [B_hi | B_lo] are contiguous BN-row blocks: one N = 2*BN operand
+                  ptx::mma_tf32(d_tmem, dA + shift + kj, dB + kj, idesc_cat, acc);
+                  ptx::mma_tf32(d_tmem, dAl + shift + kj, dB + kj, idesc, 1u);
+                } else {
+                  if constexpr (SPLIT) {
+                    ptx::mma_tf32(d_tmem, dAl + shift + kj, dB + kj, idesc, acc);
+                    ptx::mma_tf32(d_tmem, dA + shift + kj, dBl + kj, idesc, 1u);
+                    acc = 1u;
+                  }
+                  ptx::mma_tf32(d_tmem, dA + shift + kj, dB + kj, idesc, acc);
                 }
-                ptx::mma_tf32(d_tmem, dA + shift + kj, dB + kj, idesc, acc);
                 first = false;
               }
             }
@@ -349,7 +362,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 16) {
         uint32_t r[16];
-        ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * BN + cc), r);
+        ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * ACC + cc), r);
+        if constexpr (CAT) {
+          uint32_t r2[16];
+          ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * ACC + BN + cc), r2);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+        }
         ptx::tmem_ld_wait();
         if (valid) {
 #pragma unroll
