@@ -101,15 +101,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t A_B = a_bytes(a.rowsA, SPLIT), A_H = uint32_t(a.rowsA) * 128u;
-  constexpr uint32_t B_B = b_bytes(BN, SPLIT), B_H = uint32_t(BN) * KC * 4u;
+  constexpr uint32_t B_B = b_bytes(BN, SPLIT);
   const uint32_t STAGE = A_B + B_B;  // multiple of 1024 (rowsA % 8 == 0, BN*KC*4 % 1024 == 0)
   float* bias_acc = reinterpret_cast<float*>(smem + 2 * STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(bias_acc + BN);
   uint64_t* empty = full + 2;
   uint64_t* accum = empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  // 3xTF32 with BN <= 64: [dY_hi | dY_lo] concatenated along N (one MMA gives
+  // X_hi*dY_hi and X_hi*dY_lo in two column halves; X_lo*dY_hi adds into the
+  // first), 2 MMAs per k-step instead of 3; the epilogue sums the halves.
+  constexpr bool CAT = SPLIT && BN <= 64;
+  constexpr int ACC = CAT ? 2 * BN : BN;
+  // B layout per 32-pixel block: [hi rows BN | lo rows BN] (lo only when SPLIT)
+  constexpr uint32_t B_KB = uint32_t(SPLIT ? 2 : 1) * BN * 128u;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < uint32_t(ngroups * BN)) tmem_cols <<= 1;
+  while (tmem_cols < uint32_t(ngroups * ACC)) tmem_cols <<= 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -133,26 +140,33 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
       // A MN-major (bit 15), B K-major; M = 128 = four 32-channel tap atoms, N = BN output channels
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (uint32_t(BN >> 3) << 17) |
                                  (uint32_t(TM >> 4) << 24);
+      constexpr uint32_t idesc_cat = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
+                                     (uint32_t((2 * BN) >> 3) << 17) | (uint32_t(TM >> 4) << 24);
       for (int ch = ch0; ch < ch1; ++ch) {
         const int b = (ch - ch0) & 1;
         ptx::mbar_wait(&full[b], uint32_t((ch - ch0) >> 1) & 1u);
         ptx::tc_fence_after();
         const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
         for (int k8 = 0; k8 < KC / 8; ++k8) {
-          const uint64_t dB = desc(bbase + uint32_t(k8 >> 2) * (BN * 128u) + uint32_t(k8 & 3) * 32u, 16, 1024, 2);
-          const uint64_t dBl = dB + (B_H >> 4);
+          const uint64_t dB = desc(bbase + uint32_t(k8 >> 2) * B_KB + uint32_t(k8 & 3) * 32u, 16, 1024, 2);
+          const uint64_t dBl = dB + ((uint32_t(BN) * 128u) >> 4);
           for (int g = 0; g < ngroups; ++g) {
             const TapGroup& tg = a.groups[g0 + g];
             const uint32_t row = uint32_t(tg.start - rlo + k8 * 8);
             const uint64_t dA = desc(abase + row * 128u, uint32_t(tg.stride) * 128u, 512, 1);
-            const uint32_t d_tmem = tmem + uint32_t(g * BN);
+            const uint32_t d_tmem = tmem + uint32_t(g * ACC);
             uint32_t acc = (ch > ch0 || k8 > 0) ? 1u : 0u;
-            if constexpr (SPLIT) {
-              ptx::mma_tf32(d_tmem, dA + (A_H >> 4), dB, idesc, acc);
-              ptx::mma_tf32(d_tmem, dA, dBl, idesc, 1u);
-              acc = 1u;
+            if constexpr (CAT) {
+              ptx::mma_tf32(d_tmem, dA, dB, idesc_cat, acc);
+              ptx::mma_tf32(d_tmem, dA + (A_H >> 4), dB, idesc, 1u);
+            } else {
+              if constexpr (SPLIT) {
+                ptx::mma_tf32(d_tmem, dA + (A_H >> 4), dB, idesc, acc);
+                ptx::mma_tf32(d_tmem, dA, dBl, idesc, 1u);
+                acc = 1u;
+              }
+              ptx::mma_tf32(d_tmem, dA, dB, idesc, acc);
             }
-            ptx::mma_tf32(d_tmem, dA, dB, idesc, acc);
           }
         }
         ptx::mma_commit(&empty[b]);
@@ -241,13 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int gi = (strip & 1) * 4 + g;  // 16-byte granule within the 128-byte row
-          const uint32_t off = uint32_t(kb) * (BN * 128u) + uint32_t(col) * 128u + (uint32_t((gi ^ (col & 7)) & 7) << 4);
+            const uint32_t off = uint32_t(kb) * B_KB + uint32_t(col) * 128u + (uint32_t((gi ^ (col & 7)) & 7) << 4);
           const float h0 = ptx::to_tf32(yv[4 * g]), h1 = ptx::to_tf32(yv[4 * g + 1]);
           const float h2 = ptx::to_tf32(yv[4 * g + 2]), h3 = ptx::to_tf32(yv[4 * g + 3]);
           ptx::st_shared_v4(bbase + off, h0, h1, h2, h3);
-          if constexpr (SPLIT)
-            ptx::st_shared_v4(bbase + B_H + off, ptx::to_tf32(yv[4 * g] - h0), ptx::to_tf32(yv[4 * g + 1] - h1),
-                              ptx::to_tf32(yv[4 * g + 2] - h2), ptx::to_tf32(yv[4 * g + 3] - h3));
+          if constexpr (SPLIT)  // lo rows BN..2BN-1 of the block (swizzle phase unchanged: BN % 8 == 0)
+            ptx::st_shared_v4(bbase + off + uint32_t(BN) * 128u, ptx::to_tf32(yv[4 * g] - h0),
+                              ptx::to_tf32(yv[4 * g + 1] - h1), ptx::to_tf32(yv[4 * g + 2] - h2),
+                              ptx::to_tf32(yv[4 * g + 3] - h3));
         }
       }
       ptx::fence_proxy_async_smem();
@@ -268,7 +283,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
       for (int cc = 0; cc < BN; cc += 16) {
         uint32_t rv[16];
         if (ch1 > ch0) {
-          ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(g * BN + cc), rv);
+          ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(g * ACC + cc), rv);
+          if constexpr (CAT) {
+            uint32_t r2[16];
+            ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(g * ACC + BN + cc), r2);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) rv[j] = __float_as_uint(__uint_as_float(rv[j]) + __uint_as_float(r2[j]));
+          }
           ptx::tmem_ld_wait();
         } else {
 #pragma unroll

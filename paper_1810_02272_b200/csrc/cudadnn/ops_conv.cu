@@ -272,9 +272,11 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   if (int(groups.size()) > tcwtap::kMaxGroups) return false;
   a.ngroups = int(groups.size());
   for (int i = 0; i < a.ngroups; ++i) a.groups[i] = groups[i];
-  // sets of groups per CTA: TMEM columns (groups x bn) <= 256 lets two CTAs share an SM
+  // sets of groups per CTA: TMEM columns (groups x accumulator width) <= 256 lets two
+  // CTAs share an SM; 3xTF32 with bn <= 64 accumulates [hi | lo] halves (2 x bn)
   constexpr int kBudget = 227 * 1024;
-  int per_set = std::max(1, 256 / bn);
+  const int acc_cols = (split && bn <= 64) ? 2 * bn : bn;
+  int per_set = std::max(1, 256 / acc_cols);
   int smem = 0;
   bool widened = false;
   for (;;) {
@@ -294,9 +296,9 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
     a.rowsA = (tcwtap::KC + rows_max + 7) & ~7;
     smem = tcwtap::smem_bytes(a.rowsA, bn, split);
     // one CTA per SM anyway (shared memory): use the whole 512-column TMEM
-    if (!widened && smem > 113 * 1024 && per_set < 512 / bn) {
+    if (!widened && smem > 113 * 1024 && per_set < 512 / acc_cols) {
       widened = true;
-      per_set = std::max(1, 512 / bn);
+      per_set = std::max(1, 512 / acc_cols);
       continue;
     }
     if (smem <= kBudget) break;
