@@ -109,6 +109,18 @@ class Layer {
   bool propagate_down(std::size_t i) const { return i >= propagate_down_.size() || propagate_down_[i]; }
   // True when forward() may be captured into a CUDA graph (no host work).
   virtual bool graph_safe() const { return true; }
+  // B200: backward() split into two independent halves that Net may run on two
+  // streams (parameter gradients || bottom gradient).  Only layers that return
+  // true implement them; backward() stays their sequential composition.
+  virtual bool can_split_backward() const { return false; }
+  virtual void backward_weights(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+    (void)tops;
+    (void)bottoms;
+  }
+  virtual void backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+    (void)tops;
+    (void)bottoms;
+  }
   // B200: set by Net when a later layer rewrites this layer's top (top_clobbered)
   // or its bottom 0 (bottom_clobbered, including this layer itself running in
   // place) before backward reads it; layers whose backward needs that data keep
@@ -136,6 +148,9 @@ class InnerProductLayer final : public Layer {
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   const std::vector<std::shared_ptr<Blob>>& params() const override { return params_; }
+  bool can_split_backward() const override { return true; }
+  void backward_weights(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  void backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   Blob& weight() { return *params_[0]; }
   Blob& bias() { return *params_[1]; }
   // Fuse a following in-place ReLU into the GEMM epilogue (set by Net).
@@ -256,6 +271,9 @@ class ConvolutionLayer final : public Layer {
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   const std::vector<std::shared_ptr<Blob>>& params() const override { return params_; }
   const ConvolutionParam& param() const { return p_; }
+  bool can_split_backward() const override { return propagate_down(0); }
+  void backward_weights(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  void backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
 
  private:
   ConvolutionParam p_;

@@ -121,6 +121,10 @@ class Net {
   std::size_t param_total_ = 0;
   Handle weight_arena_{}, grad_arena_{};
   BackwardHook backward_hook_;
+  // parameter-gradient halves of splittable layers run here, in parallel with
+  // the bottom-gradient chain on the registry stream (CDNN_SPLIT_BACKWARD=0 off)
+  cdnn_handle side_stream_ = 0;
+  void backward_layer(std::size_t i, bool& forked);
 };
 
 }  // namespace polegrad

@@ -79,8 +79,9 @@ struct ConvDescSlot {
   // repacked per-tap weights for the TMA direct-conv path (lazily allocated):
   // [0] forward hi, [1] forward lo, [2] backward-data hi, [3] backward-data lo
   std::shared_ptr<DevAlloc> repack[4];
-  // zero-inserted dY (strided backward through the stride-1 tap kernels), grow-only
-  std::shared_ptr<DevAlloc> upsampled;
+  // zero-inserted dY (strided backward through the stride-1 tap kernels), grow-only;
+  // [0] backward-data, [1] backward-filter (they may run on two streams at once)
+  std::shared_ptr<DevAlloc> upsampled[2];
 };
 
 struct PoolDescSlot {

@@ -531,14 +531,15 @@ __global__ void zero_insert_kernel(const float* __restrict__ dy, float* __restri
 // Runs `body(up)` with dY zero-inserted and the descriptor's geometry switched to
 // the stride-1 equivalent; returns body's result (false = not handled).
 template <class F>
-bool with_zero_inserted(Ctx* c, const ConvDescSlot& dconst, const float* dy, cdnn_handle stream, F body) {
+bool with_zero_inserted(Ctx* c, const ConvDescSlot& dconst, const float* dy, cdnn_handle stream, int which, F body) {
   ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
   const ConvGeom g = d.geom;
   const int P1 = g.H + 2 * g.ph - g.dh * (g.R - 1), Q1 = g.W + 2 * g.pw - g.dw * (g.S - 1);
   if (P1 < 1 || Q1 < 1) return false;
   const size_t elems = size_t(g.N) * g.Co * P1 * Q1;
-  if (!d.upsampled || d.upsampled->bytes < elems * 4) d.upsampled = device_alloc_shared(elems * 4, c->device);
-  float* up = static_cast<float*>(d.upsampled->ptr);
+  auto& buf = d.upsampled[which];
+  if (!buf || buf->bytes < elems * 4) buf = device_alloc_shared(elems * 4, c->device);
+  float* up = static_cast<float*>(buf->ptr);
   cudaStream_t st = stream_of(c, stream);
   zero_insert_kernel<<<grid_for(int64_t(elems), 256), 256, 0, st>>>(dy, up, int64_t(g.N) * g.Co, g.P, g.Q, P1, Q1,
                                                                      g.sh, g.sw);
@@ -569,7 +570,7 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   const int M = g.N * g.H * g.W, N = g.Cg, K = d.Kd;
   if constexpr (std::is_same_v<T, float>) {
     if ((g.sh > 1 || g.sw > 1) && conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 &&
-        with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, [&](const float* up) {
+        with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, 0, [&](const float* up) {
           return conv_tap(c, d, true, up, reinterpret_cast<const float*>(Wt.dev), nullptr,
                           reinterpret_cast<float*>(DX.dev), stream);
         }))
@@ -621,7 +622,7 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
     if (g.sh == 1 && g.sw == 1) {
       if (conv_wgrad_tap(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) return;
     } else if (conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 && g.Cg >= 16 &&
-               with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream,
+               with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, 1,
                                   [&](const float* up) { return conv_wgrad_tap(c, d, x, up, dw, db, stream); })) {
       return;
     }

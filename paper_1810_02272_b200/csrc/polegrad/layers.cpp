@@ -171,6 +171,23 @@ void InnerProductLayer::backward(std::span<Blob* const> tops, std::span<Blob* co
           "InnerProduct backward");
 }
 
+void InnerProductLayer::backward_weights(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  Blob& x = *bottoms[0];
+  Registry& reg = x.registry();
+  cdnn_ok(cdnn_ip_backward(reg.context(), x.gpu_data(), weight().gpu_data(), tops[0]->gpu_diff(),
+                           weight().mutable_gpu_diff(), bias().mutable_gpu_diff(), 0, x.shape().n(), input_dim_,
+                           num_output_, reg.stream()),
+          "InnerProduct backward");
+}
+
+void InnerProductLayer::backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  Blob& x = *bottoms[0];
+  Registry& reg = x.registry();
+  cdnn_ok(cdnn_ip_backward(reg.context(), x.gpu_data(), weight().gpu_data(), tops[0]->gpu_diff(), 0, 0,
+                           x.overwrite_gpu_diff(), x.shape().n(), input_dim_, num_output_, reg.stream()),
+          "InnerProduct backward");
+}
+
 // ---- ReLU / Sigmoid / Softmax (layers.cpp:174-266) ---------------------------------
 
 std::vector<Shape> ReluLayer::setup(const std::vector<Shape>& s, const std::shared_ptr<Registry>&, Rng&) {

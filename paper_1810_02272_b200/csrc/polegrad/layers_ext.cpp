@@ -131,16 +131,23 @@ void ConvolutionLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* c
 }
 
 void ConvolutionLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  backward_weights(tops, bottoms);
+  if (propagate_down(0)) backward_inputs(tops, bottoms);
+}
+
+void ConvolutionLayer::backward_weights(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
   Registry& reg = *reg_;
   const cdnn_handle dy = tops[0]->gpu_diff(), x = bottoms[0]->gpu_data();
   const cdnn_handle dw = params_[0]->mutable_gpu_diff();
   const cdnn_handle db = p_.bias_term ? params_[1]->mutable_gpu_diff() : 0;
   cdnn_ok(cdnn_conv_backward_filter(reg.context(), desc_, x, dy, dw, db, reg.stream()), "Convolution backward");
-  if (propagate_down(0)) {
-    const cdnn_handle w = params_[0]->gpu_data();
-    cdnn_ok(cdnn_conv_backward_data(reg.context(), desc_, w, dy, bottoms[0]->overwrite_gpu_diff(), reg.stream()),
-            "Convolution backward");
-  }
+}
+
+void ConvolutionLayer::backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  Registry& reg = *reg_;
+  const cdnn_handle w = params_[0]->gpu_data(), dy = tops[0]->gpu_diff();
+  cdnn_ok(cdnn_conv_backward_data(reg.context(), desc_, w, dy, bottoms[0]->overwrite_gpu_diff(), reg.stream()),
+          "Convolution backward");
 }
 
 // ---- Pooling ------------------------------------------------------------------------

@@ -3,6 +3,7 @@
 #include "polegrad/net.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <bit>
 #include <cstring>
 #include <set>
@@ -190,6 +191,12 @@ void Net::pack_params() {
 }
 
 Net::~Net() {
+  if (registry_ && side_stream_) {
+    try {
+      registry_->synchronize();
+      cdnn_stream_free(registry_->context(), side_stream_);
+    } catch (...) {}
+  }
   if (registry_ && rng_handle_) {
     try { registry_->free_subsystem(rng_handle_); } catch (...) {}
   }
@@ -202,6 +209,7 @@ Net& Net::operator=(Net&& o) noexcept {
     }
     registry_ = std::move(o.registry_);
     rng_handle_ = std::exchange(o.rng_handle_, Handle{});
+    side_stream_ = std::exchange(o.side_stream_, cdnn_handle{0});
     def_ = std::move(o.def_);
     layers_ = std::move(o.layers_);
     bottoms_ = std::move(o.bottoms_);
@@ -229,20 +237,68 @@ std::map<std::string, Blob*> Net::forward() {
   return outputs;
 }
 
+namespace {
+bool split_backward_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CDNN_SPLIT_BACKWARD");
+    return !(v && std::string(v) == "0");
+  }();
+  return on;
+}
+}  // namespace
+
+// Layer i's backward.  Splittable layers (Convolution with a bottom gradient,
+// InnerProduct) fork their parameter-gradient half onto the side stream: it
+// only reads the top diff and bottom data and writes parameter diffs, none of
+// which the remaining bottom-gradient chain touches; the solver joins it.
+void Net::backward_layer(std::size_t i, bool& forked) {
+  Layer& l = *layers_[i];
+  const bool split = split_backward_enabled() && !backward_hook_ && !reference_compat() && l.can_split_backward();
+  if (!split) {
+    l.backward(tops_[i], bottoms_[i]);
+    return;
+  }
+  Registry& reg = *registry_;
+  const cdnn_handle main = reg.stream();
+  if (!side_stream_) cdnn_ok(cdnn_stream_create(reg.context(), &side_stream_), "backward side stream");
+  // bring every operand current on the main stream before the fork
+  for (Blob* t : tops_[i]) t->gpu_diff();
+  for (Blob* b : bottoms_[i]) b->gpu_data();
+  for (const auto& p : l.params()) {
+    p->gpu_data();
+    p->mutable_gpu_diff();
+  }
+  cdnn_ok(cdnn_stream_wait(reg.context(), side_stream_, main), "backward fork");
+  reg.set_stream(side_stream_);
+  try {
+    l.backward_weights(tops_[i], bottoms_[i]);
+  } catch (...) {
+    reg.set_stream(main);
+    throw;
+  }
+  reg.set_stream(main);
+  l.backward_inputs(tops_[i], bottoms_[i]);
+  forked = true;
+}
+
 void Net::backward() {
+  bool forked = false;
   for (std::size_t i = layers_.size(); i-- > 0;) {
-    layers_[i]->backward(tops_[i], bottoms_[i]);
+    backward_layer(i, forked);
     if (backward_hook_) backward_hook_(i);
   }
+  if (forked) cdnn_ok(cdnn_stream_wait(registry_->context(), registry_->stream(), side_stream_), "backward join");
 }
 
 void Net::backward_from(const std::string& blob_name) {
   auto it = producer_index_.find(blob_name);
   if (it == producer_index_.end()) throw ModelError("backward_from: no layer produces blob '" + blob_name + "'");
+  bool forked = false;
   for (std::size_t i = it->second + 1; i-- > 0;) {
-    layers_[i]->backward(tops_[i], bottoms_[i]);
+    backward_layer(i, forked);
     if (backward_hook_) backward_hook_(i);
   }
+  if (forked) cdnn_ok(cdnn_stream_wait(registry_->context(), registry_->stream(), side_stream_), "backward join");
 }
 
 bool Net::has_blob(const std::string& name) const { return blob_index_.contains(name); }
