@@ -308,10 +308,11 @@ def run_b200(args) -> None:
     nl = len(net.layer_names())
     fwd = (C.c_float * nl)()
     bwd = (C.c_float * nl)()
-    net.set_batch(host_x[0], host_y[0])
-    polegrad._check(net.lib, net.lib.pg_net_profile(net.ptr, fwd, bwd, nl))
-    net.sync()
-    solver.apply()  # consume the profiled gradients
+    for _ in range(2):  # the first pass creates the sequential-backward workspaces
+        net.set_batch(host_x[0], host_y[0])
+        polegrad._check(net.lib, net.lib.pg_net_profile(net.ptr, fwd, bwd, nl))
+        net.sync()
+        solver.apply()  # consume the profiled gradients
     names = net.layer_names()
     prof = {names[i]: {"fwd_ms": float(fwd[i]), "bwd_ms": float(bwd[i])} for i in range(nl)}
 
