@@ -82,6 +82,11 @@ struct ConvDescSlot {
   // zero-inserted dY (strided backward through the stride-1 tap kernels), grow-only;
   // [0] backward-data, [1] backward-filter (they may run on two streams at once)
   std::shared_ptr<DevAlloc> upsampled[2];
+  // space-to-depth rewrite of a strided convolution (stride s -> stride 1 over C*s*s
+  // channels): the equivalent descriptor and its grow-only operand buffers
+  // [0] X' forward, [1] W', [2] X' backward-filter, [3] dW', [4] dX'
+  std::shared_ptr<ConvDescSlot> s2d;
+  std::shared_ptr<DevAlloc> s2d_buf[5];
 };
 
 struct PoolDescSlot {

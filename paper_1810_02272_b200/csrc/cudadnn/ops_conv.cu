@@ -438,6 +438,153 @@ bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, con
   return true;
 }
 
+// ---- space-to-depth: stride-s convolution == stride-1 convolution over C*s*s channels
+// X'[n][(dy*s + dx)*C + c][h'][w'] = x_pad[n][c][s*h' + dy][s*w' + dx]
+// W'[co][(dy*s + dx)*C + c][r'][t'] = W[co][c][s*r' + dy][s*t' + dx]   (0 past the filter)
+// with kernel ceil(R/s) x ceil(S/s), no padding, same output P x Q.  AlexNet conv1
+// (11x11, stride 4, 3 channels) becomes a 3x3 convolution over 48 channels that the
+// tap-shift kernels run on the tensor cores.
+bool s2d_eligible(const ConvGeom& g) {
+  return conv_tap_enabled() && g.sh == g.sw && g.sh >= 2 && g.dh == 1 && g.dw == 1 && g.group == 1 &&
+         g.C * g.sh * g.sw <= 128 && (g.R + g.sh - 1) / g.sh <= 4 && (g.S + g.sw - 1) / g.sw <= 4;
+}
+
+ConvDescSlot& s2d_desc(Ctx* c, const ConvDescSlot& dconst) {
+  ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
+  if (!d.s2d) {
+    const ConvGeom& g = d.geom;
+    const int s = g.sh;
+    auto child = std::make_shared<ConvDescSlot>();
+    ConvGeom& h = child->geom;
+    h.N = g.N; h.C = g.C * s * s; h.Co = g.Co; h.P = g.P; h.Q = g.Q;
+    h.R = (g.R + s - 1) / s; h.S = (g.S + s - 1) / s;
+    h.H = g.P + h.R - 1; h.W = g.Q + h.S - 1;
+    h.sh = h.sw = 1; h.ph = h.pw = 0; h.dh = h.dw = 1;
+    h.group = 1; h.Cg = h.C; h.Cog = h.Co;
+    h.div_PQ = FastDiv(uint32_t(h.P * h.Q)); h.div_Q = FastDiv(uint32_t(h.Q));
+    h.div_HW = FastDiv(uint32_t(h.H * h.W)); h.div_W = FastDiv(uint32_t(h.W));
+    child->P = h.P; child->Q = h.Q;
+    child->Kc = h.Cg * h.R * h.S;
+    child->Kd = h.Cog * h.R * h.S;
+    d.s2d = child;
+  }
+  (void)c;
+  return *d.s2d;
+}
+
+float* s2d_buffer(Ctx* c, const ConvDescSlot& dconst, int which, size_t elems) {
+  ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
+  auto& b = d.s2d_buf[which];
+  if (!b || b->bytes < elems * 4) b = device_alloc_shared(elems * 4, c->device);
+  return static_cast<float*>(b->ptr);
+}
+
+__global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict__ xs, ConvGeom g, ConvGeom h) {
+  const int s = g.sh;
+  const int64_t total = int64_t(h.N) * h.C * h.H * h.W;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int w2 = int(i % h.W);
+    const int h2 = int((i / h.W) % h.H);
+    const int cc = int((i / (int64_t(h.W) * h.H)) % h.C);
+    const int n = int(i / (int64_t(h.W) * h.H * h.C));
+    const int c = cc % g.C, ph = cc / g.C, dy = ph / s, dx = ph % s;
+    const int y = s * h2 + dy - g.ph, xx = s * w2 + dx - g.pw;
+    xs[i] = (y >= 0 && y < g.H && xx >= 0 && xx < g.W) ? x[((int64_t(n) * g.C + c) * g.H + y) * g.W + xx] : 0.f;
+  }
+}
+
+__global__ void s2d_weight_kernel(const float* __restrict__ w, float* __restrict__ ws, ConvGeom g, ConvGeom h) {
+  const int s = g.sh;
+  const int total = h.Co * h.C * h.R * h.S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t2 = i % h.S, r2 = (i / h.S) % h.R, cc = (i / (h.S * h.R)) % h.C, co = i / (h.S * h.R * h.C);
+    const int c = cc % g.C, ph = cc / g.C, dy = ph / s, dx = ph % s;
+    const int r = s * r2 + dy, t = s * t2 + dx;
+    ws[i] = (r < g.R && t < g.S) ? w[((co * g.C + c) * g.R + r) * g.S + t] : 0.f;
+  }
+}
+
+// dW[co][c][r][t] += dW'[co][(dy*s + dx)*C + c][r/s][t/s]
+__global__ void s2d_dweight_kernel(const float* __restrict__ dws, float* __restrict__ dw, ConvGeom g, ConvGeom h) {
+  const int s = g.sh;
+  const int total = g.Co * g.C * g.R * g.S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t = i % g.S, r = (i / g.S) % g.R, c = (i / (g.S * g.R)) % g.C, co = i / (g.S * g.R * g.C);
+    const int cc = ((r % s) * s + (t % s)) * g.C + c;
+    dw[i] += dws[((co * h.C + cc) * h.R + r / s) * h.S + t / s];
+  }
+}
+
+// dX[n][c][y][x] = dX'[n][(dy*s + dx)*C + c][(y+ph)/s][(x+pw)/s]
+__global__ void d2s_input_kernel(const float* __restrict__ dxs, float* __restrict__ dx, ConvGeom g, ConvGeom h) {
+  const int s = g.sh;
+  const int64_t total = int64_t(g.N) * g.C * g.H * g.W;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int xx = int(i % g.W);
+    const int y = int((i / g.W) % g.H);
+    const int c = int((i / (int64_t(g.W) * g.H)) % g.C);
+    const int n = int(i / (int64_t(g.W) * g.H * g.C));
+    const int yp = y + g.ph, xp = xx + g.pw;
+    const int h2 = yp / s, w2 = xp / s;
+    const int cc = ((yp % s) * s + (xp % s)) * g.C + c;
+    dx[i] = (h2 < h.H && w2 < h.W) ? dxs[((int64_t(n) * h.C + cc) * h.H + h2) * h.W + w2] : 0.f;
+  }
+}
+
+bool conv_wgrad_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float* dy, float* dw, float* db,
+                    cdnn_handle stream) {
+  if (!s2d_eligible(d.geom)) return false;
+  ConvDescSlot& e = s2d_desc(c, d);
+  const ConvGeom &g = d.geom, &h = e.geom;
+  if (h.C < 16) return false;
+  cudaStream_t st = stream_of(c, stream);
+  float* xs = s2d_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
+  float* dws = s2d_buffer(c, d, 3, size_t(h.Co) * h.C * h.R * h.S);
+  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xs, g, h);
+  CDNN_CUDA(cudaMemsetAsync(dws, 0, size_t(h.Co) * h.C * h.R * h.S * 4, st));
+  check_launch("s2d");
+  count_launch(c);
+  if (!conv_wgrad_tap(c, e, xs, dy, dw ? dws : nullptr, db, stream)) return false;
+  if (dw) {
+    s2d_dweight_kernel<<<grid_for(int64_t(g.Co) * g.C * g.R * g.S, 256), 256, 0, st>>>(dws, dw, g, h);
+    check_launch("s2d_dweight");
+    count_launch(c);
+  }
+  return true;
+}
+
+bool conv_dgrad_s2d(Ctx* c, const ConvDescSlot& d, const float* w, const float* dy, float* dx, cdnn_handle stream) {
+  if (!s2d_eligible(d.geom)) return false;
+  ConvDescSlot& e = s2d_desc(c, d);
+  const ConvGeom &g = d.geom, &h = e.geom;
+  cudaStream_t st = stream_of(c, stream);
+  float* wsb = s2d_buffer(c, d, 1, size_t(h.Co) * h.C * h.R * h.S);
+  float* dxs = s2d_buffer(c, d, 4, size_t(h.N) * h.C * h.H * h.W);
+  s2d_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R * h.S, 256), 256, 0, st>>>(w, wsb, g, h);
+  check_launch("s2d");
+  count_launch(c);
+  if (!conv_tap(c, e, true, dy, wsb, nullptr, dxs, stream)) return false;
+  d2s_input_kernel<<<grid_for(int64_t(g.N) * g.C * g.H * g.W, 256), 256, 0, st>>>(dxs, dx, g, h);
+  check_launch("d2s");
+  count_launch(c);
+  return true;
+}
+
+bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float* w, const float* bias, float* y,
+                      cdnn_handle stream) {
+  if (!s2d_eligible(d.geom)) return false;
+  ConvDescSlot& e = s2d_desc(c, d);
+  const ConvGeom &g = d.geom, &h = e.geom;
+  cudaStream_t st = stream_of(c, stream);
+  float* xs = s2d_buffer(c, d, 0, size_t(h.N) * h.C * h.H * h.W);
+  float* wsb = s2d_buffer(c, d, 1, size_t(h.Co) * h.C * h.R * h.S);
+  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xs, g, h);
+  s2d_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R * h.S, 256), 256, 0, st>>>(w, wsb, g, h);
+  check_launch("s2d");
+  count_launch(c, 2);
+  return conv_tap(c, e, false, xs, wsb, bias, y, stream);
+}
+
 template <typename T>
 void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const BufferSlot& Wt,
                     const BufferSlot* B, BufferSlot& Y, cdnn_handle stream) {
@@ -446,6 +593,9 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.P * g.Q, N = g.Cog, K = d.Kc;
   if constexpr (std::is_same_v<T, float>) {
+    if (conv_forward_s2d(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
+                         B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
+      return;
     if (conv_tap(c, d, false, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
                  B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
       return;
@@ -569,6 +719,10 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.H * g.W, N = g.Cg, K = d.Kd;
   if constexpr (std::is_same_v<T, float>) {
+    if ((g.sh > 1 || g.sw > 1) &&
+        conv_dgrad_s2d(c, d, reinterpret_cast<const float*>(Wt.dev), reinterpret_cast<const float*>(DY.dev),
+                       reinterpret_cast<float*>(DX.dev), stream))
+      return;
     if ((g.sh > 1 || g.sw > 1) && conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 &&
         with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, 0, [&](const float* up) {
           return conv_tap(c, d, true, up, reinterpret_cast<const float*>(Wt.dev), nullptr,
@@ -621,6 +775,8 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
     const float* x = reinterpret_cast<const float*>(X.dev);
     if (g.sh == 1 && g.sw == 1) {
       if (conv_wgrad_tap(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) return;
+    } else if (conv_wgrad_s2d(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) {
+      return;
     } else if (conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 && g.Cg >= 16 &&
                with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, 1,
                                   [&](const float* up) { return conv_wgrad_tap(c, d, x, up, dw, db, stream); })) {
