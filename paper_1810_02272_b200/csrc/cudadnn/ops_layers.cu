@@ -27,44 +27,65 @@ void by_dtype(int dtype, const char* what, F&& f) {
 int blocks(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, int64_t(kNumSMs) * 16))); }
 
 // ---- LRN (ACROSS_CHANNELS): scale = k + alpha/n * sum_{window} x^2 ; y = x * scale^-beta
+// One thread per pixel (img, hw) walks the channels with a running window sum
+// (entering square added, leaving square subtracted; the leaving value is an
+// L1 hit), so the tensor is read ~once, coalesced across threads (consecutive hw).
+template <typename T>
+__device__ __forceinline__ T neg_pow(T sc, T beta) {
+  if constexpr (sizeof(T) == 4) return exp2f(-beta * log2f(sc));
+  else return pow(sc, -beta);
+}
+
 template <typename T>
 __global__ void lrn_fwd(const T* __restrict__ x, T* __restrict__ y, T* __restrict__ scale, int N, int C, int HW,
                         int size, T alpha, T beta, T k) {
-  const int64_t total = int64_t(N) * C * HW;
-  const int pre = (size - 1) / 2;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int hw = int(i % HW);
-    const int c = int((i / HW) % C);
-    const int64_t base = (i / (int64_t(C) * HW)) * C * HW + hw;
-    T s = T(0);
-    const int c0 = max(c - pre, 0), c1 = min(c - pre + size, C);
-    for (int cc = c0; cc < c1; ++cc) {
+  const int64_t pixels = int64_t(N) * HW;
+  const int pre = (size - 1) / 2, post = size - 1 - pre;
+  const T aN = alpha / T(size);
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < pixels; p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t img = p / HW, hw = p - img * HW;
+    const int64_t base = img * C * HW + hw;
+    T s = T(0);  // sum of squares over [c - pre, c + post]
+    for (int cc = 0; cc < post && cc < C; ++cc) {
       const T v = x[base + int64_t(cc) * HW];
       s += v * v;
     }
-    const T sc = k + alpha / T(size) * s;
-    scale[i] = sc;
-    y[i] = x[i] * pow(sc, -beta);
+    for (int c = 0; c < C; ++c) {
+      const int cin = c + post, cout = c - pre - 1;
+      if (cin < C) { const T v = x[base + int64_t(cin) * HW]; s += v * v; }
+      if (cout >= 0) { const T v = x[base + int64_t(cout) * HW]; s -= v * v; }
+      s = s > T(0) ? s : T(0);
+      const int64_t o = base + int64_t(c) * HW;
+      const T sc = k + aN * s;
+      scale[o] = sc;
+      y[o] = x[o] * neg_pow(sc, beta);
+    }
   }
 }
 
-// dx = dy * scale^-beta - 2*alpha*beta/n * x * sum_{window} dy*y/scale
+// dx = dy * scale^-beta - 2*alpha*beta/n * x * sum_{c' : c in window(c')} dy*y/scale
 template <typename T>
 __global__ void lrn_bwd(const T* __restrict__ x, const T* __restrict__ y, const T* __restrict__ scale,
                         const T* __restrict__ dy, T* __restrict__ dx, int N, int C, int HW, int size, T alpha, T beta) {
-  const int64_t total = int64_t(N) * C * HW;
-  const int post = size - 1 - (size - 1) / 2;  // channels whose window contains c
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int hw = int(i % HW);
-    const int c = int((i / HW) % C);
-    const int64_t base = (i / (int64_t(C) * HW)) * C * HW + hw;
-    T acc = T(0);
-    const int c0 = max(c - post, 0), c1 = min(c + (size - 1) / 2 + 1, C);
-    for (int cc = c0; cc < c1; ++cc) {
-      const int64_t j = base + int64_t(cc) * HW;
-      acc += dy[j] * y[j] / scale[j];
+  const int64_t pixels = int64_t(N) * HW;
+  const int pre = (size - 1) / 2, post = size - 1 - pre;
+  const T coef = T(2) * alpha * beta / T(size);
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < pixels; p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t img = p / HW, hw = p - img * HW;
+    const int64_t base = img * C * HW + hw;
+    auto t = [&](int cc) {
+      const int64_t o = base + int64_t(cc) * HW;
+      return dy[o] * y[o] / scale[o];
+    };
+    T acc = T(0);  // sum of t over [c - post, c + pre]
+    for (int cc = 0; cc < pre && cc < C; ++cc) acc += t(cc);
+    for (int c = 0; c < C; ++c) {
+      const int cin = c + pre, cout = c - post - 1;
+      if (cin < C) acc += t(cin);
+      if (cout >= 0) acc -= t(cout);
+      const int64_t o = base + int64_t(c) * HW;
+      dx[o] = dy[o] * neg_pow(scale[o], beta) - coef * x[o] * acc;
     }
-    dx[i] = dy[i] * pow(scale[i], -beta) - T(2) * alpha * beta / T(size) * x[i] * acc;
   }
 }
 
@@ -238,7 +259,7 @@ int cdnn_lrn_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle sca
     DeviceGuard g(cx);
     by_dtype(X.dtype, "lrn", [&](auto tag) {
       using T = decltype(tag);
-      lrn_fwd<T><<<blocks(int64_t(cnt)), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), n, c, hw,
+      lrn_fwd<T><<<blocks(int64_t(n) * hw), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), n, c, hw,
                                                                         local_size, T(alpha), T(beta), T(k));
     });
     check_launch("lrn_fwd");
@@ -260,7 +281,7 @@ int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle sc
     DeviceGuard g(cx);
     by_dtype(X.dtype, "lrn_bwd", [&](auto tag) {
       using T = decltype(tag);
-      lrn_bwd<T><<<blocks(int64_t(cnt)), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX),
+      lrn_bwd<T><<<blocks(int64_t(n) * hw), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX),
                                                                         n, c, hw, local_size, T(alpha), T(beta));
     });
     check_launch("lrn_bwd");
