@@ -24,8 +24,9 @@
 // deterministic reduce_splits_kernel adds the splits and permutes m' into the
 // Caffe filter layout [co][c][r][s] while accumulating into dw / db.
 //
-// Warps (192 threads): warp 1 TMEM owner + MMA issuer, warps 2-5 stage the
-// pixel chunks (double-buffered) and run the epilogue, warp 0 idles.
+// Warps (320 threads): warp 1 TMEM owner + MMA issuer, warps 2-9 stage the
+// pixel chunks (double-buffered; eight warps for enough loads in flight),
+// warps 2-5 also run the epilogue (one TMEM lane quadrant each), warp 0 idles.
 #pragma once
 
 #include <cstdint>
@@ -37,7 +38,8 @@
 namespace cdnn {
 namespace tcwtap {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 1 MMA, warps 2-9 stage (2-5 also run the epilogue)
+constexpr int kStagers = 256;
 constexpr int KC = 64;  // virtual pixels per chunk (K per pipeline stage)
 constexpr int kMaxGroups = 32;
 
@@ -85,7 +87,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
 }
 
 template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) conv_wtap_kernel(const WtapArgs a) {
   constexpr int TM = 128;
   const int item = blockIdx.y;
   const int cb = item % a.cblocks;
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&full[b], 4);
+      ptx::mbar_init(&full[b], kStagers / 32);
       ptx::mbar_init(&empty[b], 1);
     }
     ptx::mbar_init(accum, 1);
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
       // ---- A: X_v rows [v0 + rlo, + rowsA), MN-major 128B_BASE32B.  One thread
       // per pixel row loads all 32 channels before converting (32 loads in flight).
       const int vA0 = v0 + rlo;
-      for (int row = tid; row < a.rowsA; row += 128) {
+      for (int row = tid; row < a.rowsA; row += kStagers) {
         const int v = vA0 + row;
         bool inb = false;
         const float* src = a.x;
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
       }
       // ---- B: dY^T [co][v0 .. v0+KC), K-major SW128 in 32-pixel blocks.  One thread per
       // (co, 16-pixel strip): 16 loads in flight, one index decomposition per strip.
-      for (int it = tid; it < BN * (KC / 16); it += 128) {
+      for (int it = tid; it < BN * (KC / 16); it += kStagers) {
         const int strip = it % (KC / 16), col = it / (KC / 16);
         const int co = n0 + col;
         float yv[16];
@@ -269,7 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&full[b]);
     }
-    // ---- epilogue: TMEM lane (j*32 + c) of group g = tap (r, s0 + j), channel c
+    // ---- epilogue (warps 2-5): TMEM lane (j*32 + c) of group g = tap (r, s0 + j), channel c
+    if (warp >= 6) goto done;
+    {
     const int q4 = warp & 3;  // lane quadrant = tap atom j
     float* wsz = a.ws + int64_t(z) * a.Cog * (a.Kc + 1);
     if (ch1 > ch0) {
@@ -310,7 +314,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_wtap_kernel(const WtapArgs a
       for (int col = lane; col < BN; col += 32)
         if (n0 + col < a.Cog) wsz[int64_t(n0 + col) * (a.Kc + 1) + a.Kc] = bias_acc[col];
     }
+    }
   }
+done:
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
