@@ -16,7 +16,7 @@ struct PoolGeom {
   int N, C, H, W, PH, PW, kh, kw, sh, sw, ph, pw;
   // 32-bit index decomposition without hardware division (SASS integer division
   // is a ~20-instruction sequence; these kernels are issue-bound otherwise)
-  FastDiv divW, divHW, divPW, divPHW, divSH, divSW;
+  FastDiv divW, divHW, divPW, divPHW, divSH, divSW, divH;
 };
 
 // (plane, h, w) of a flat NCHW index within planes of H x W
@@ -55,24 +55,34 @@ __global__ void __launch_bounds__(256) max_pool_fwd(const T* __restrict__ x, T* 
 // gather: every bottom element sums the top diffs of the windows whose argmax is it
 template <typename T>
 __global__ void __launch_bounds__(256) max_pool_bwd(const T* __restrict__ dy, const int* __restrict__ mask,
-                                                    T* __restrict__ dx, PoolGeom g, uint32_t total) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const Idx3 q = split3(i, g.divHW, g.divW, uint32_t(g.H * g.W), uint32_t(g.W));
-    const int h = int(q.h) + g.ph, w = int(q.w) + g.pw;
-    // windows [p*s - pad, +k) that contain the element
+                                                    T* __restrict__ dx, PoolGeom g, uint32_t total4) {
+  // four consecutive bottom elements of one row per thread: the row's window range
+  // (and the plane / row decomposition) is computed once per thread
+  const uint32_t W4 = uint32_t(g.W + 3) >> 2;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += gridDim.x * blockDim.x) {
+    const uint32_t row = i / W4, w0 = (i - row * W4) * 4;  // row = plane*H + h (W4 small: cheap)
+    const uint32_t plane = g.divH.div(row), hq = row - plane * uint32_t(g.H);
+    const int h = int(hq) + g.ph;
     const int phs = h < g.kh ? 0 : int(g.divSH.div(uint32_t(h - g.kh))) + 1;
     const int phe = min(int(g.divSH.div(uint32_t(h))) + 1, g.PH);
-    const int pws = w < g.kw ? 0 : int(g.divSW.div(uint32_t(w - g.kw))) + 1;
-    const int pwe = min(int(g.divSW.div(uint32_t(w))) + 1, g.PW);
-    const int me = int(q.h) * g.W + int(q.w);
-    const size_t base = size_t(q.plane) * uint32_t(g.PH * g.PW);
-    T s = T(0);
-    for (int ph = phs; ph < phe; ++ph)
-      for (int pw = pws; pw < pwe; ++pw) {
-        const size_t o = base + ph * g.PW + pw;
-        if (__ldg(mask + o) == me) s += __ldg(dy + o);
-      }
-    dx[i] = s;
+    const size_t base = size_t(plane) * uint32_t(g.PH * g.PW);
+    const size_t out = size_t(row) * uint32_t(g.W);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int wq = int(w0) + e;
+      if (wq >= g.W) break;
+      const int w = wq + g.pw;
+      const int pws = w < g.kw ? 0 : int(g.divSW.div(uint32_t(w - g.kw))) + 1;
+      const int pwe = min(int(g.divSW.div(uint32_t(w))) + 1, g.PW);
+      const int me = int(hq) * g.W + wq;
+      T s = T(0);
+      for (int ph = phs; ph < phe; ++ph)
+        for (int pw = pws; pw < pwe; ++pw) {
+          const size_t o = base + ph * g.PW + pw;
+          if (__ldg(mask + o) == me) s += __ldg(dy + o);
+        }
+      dx[out + wq] = s;
+    }
   }
 }
 
@@ -120,7 +130,8 @@ PoolGeom geom_of(const PoolDescSlot& d) {
   const auto& p = d.p;
   PoolGeom g{p.n, p.c, p.h, p.w, d.PH, d.PW, p.kernel_h, p.kernel_w, p.stride_h, p.stride_w, p.pad_h, p.pad_w,
              FastDiv(uint32_t(p.w)), FastDiv(uint32_t(p.h * p.w)), FastDiv(uint32_t(d.PW)),
-             FastDiv(uint32_t(d.PH * d.PW)), FastDiv(uint32_t(p.stride_h)), FastDiv(uint32_t(p.stride_w))};
+             FastDiv(uint32_t(d.PH * d.PW)), FastDiv(uint32_t(p.stride_h)), FastDiv(uint32_t(p.stride_w)),
+             FastDiv(uint32_t(p.h))};
   if (uint64_t(p.n) * p.c * p.h * p.w >= (1ull << 31))
     fail(CDNN_INVALID_ARGUMENT, "pool: tensors of 2^31 elements or more are not supported");
   return g;
@@ -190,9 +201,12 @@ int cdnn_pool_backward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_hand
     const int blocks = grid_for(int64_t(nin), 256);
     auto run = [&](auto tag) {
       using T = decltype(tag);
-      if (d.p.method == CDNN_POOL_MAX)
-        max_pool_bwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(DY.dev), reinterpret_cast<const int*>(M->dev),
-                                                 reinterpret_cast<T*>(DX.dev), g, uint32_t(nin));
+      if (d.p.method == CDNN_POOL_MAX) {
+        const uint64_t n4 = uint64_t(g.N) * g.C * g.H * ((g.W + 3) / 4);
+        max_pool_bwd<T><<<grid_for(int64_t(n4), 256), 256, 0, st>>>(
+            reinterpret_cast<const T*>(DY.dev), reinterpret_cast<const int*>(M->dev), reinterpret_cast<T*>(DX.dev), g,
+            uint32_t(n4));
+      }
       else
         ave_pool_bwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(DY.dev), reinterpret_cast<T*>(DX.dev), g,
                                                  uint32_t(nin));
