@@ -237,6 +237,11 @@ CDNN_API int cdnn_ip_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle w, cdnn_h
  * accumulate, layers.hpp:84-86); backward_data OVERWRITES dx. */
 CDNN_API int cdnn_conv_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle w,
                                cdnn_handle bias, cdnn_handle y, cdnn_handle stream);
+/* cdnn_conv_forward with flags: CDNN_CONV_RELU applies max(y, 0) in the epilogue (a
+ * following in-place ReLU fused, layers.cpp:184 semantics) */
+enum { CDNN_CONV_RELU = 1 };
+CDNN_API int cdnn_conv_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle w,
+                                  cdnn_handle bias, cdnn_handle y, int flags, cdnn_handle stream);
 CDNN_API int cdnn_conv_backward_data(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w,
                                      cdnn_handle dy, cdnn_handle dx, cdnn_handle stream);
 CDNN_API int cdnn_conv_backward_filter(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x,
@@ -247,6 +252,11 @@ CDNN_API int cdnn_conv_backward_filter(cdnn_ctx ctx, cdnn_handle desc, cdnn_hand
  * holding the flat h*W+w argmax (MAX only; first max wins, strict >). */
 CDNN_API int cdnn_pool_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle y,
                                cdnn_handle mask, cdnn_handle stream);
+/* cdnn_pool_forward with flags: CDNN_POOL_RELU clamps the pooled output at 0 (a following
+ * in-place ReLU fused; the argmax mask is the pooling's, unchanged) */
+enum { CDNN_POOL_RELU = 1 };
+CDNN_API int cdnn_pool_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle y,
+                                  cdnn_handle mask, int flags, cdnn_handle stream);
 CDNN_API int cdnn_pool_backward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_handle mask,
                                 cdnn_handle dx, cdnn_handle stream);
 
@@ -300,6 +310,18 @@ CDNN_API int cdnn_batchnorm_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, 
 CDNN_API int cdnn_batchnorm_backward(cdnn_ctx ctx, cdnn_handle y, cdnn_handle invstd, cdnn_handle dy,
                                      cdnn_handle dx, cdnn_handle scratch, int n, int c, int hw,
                                      cdnn_handle stream);
+/* BatchNorm followed by Scale, fused: xnorm = (x - mean)*invstd (kept for backward),
+ * z = gamma*xnorm + beta (beta may be 0) */
+CDNN_API int cdnn_batchnorm_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle xnorm, cdnn_handle z,
+                                          cdnn_handle mean, cdnn_handle invstd, cdnn_handle gamma,
+                                          cdnn_handle beta, int n, int c, int hw, double eps,
+                                          cdnn_handle stream);
+/* dbeta += sum dz ; dgamma += sum dz*xnorm ;
+ * dx = gamma*invstd*(dz - mean(dz) - xnorm*mean(dz*xnorm)) (skipped when dx == 0); scratch 2*c */
+CDNN_API int cdnn_batchnorm_scale_backward(cdnn_ctx ctx, cdnn_handle xnorm, cdnn_handle invstd,
+                                           cdnn_handle gamma, cdnn_handle dz, cdnn_handle dx,
+                                           cdnn_handle dgamma, cdnn_handle dbeta, cdnn_handle scratch,
+                                           int n, int c, int hw, cdnn_handle stream);
 /* Scale (per channel): y = x*gamma[c] (+ beta[c] when beta != 0) */
 CDNN_API int cdnn_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_handle beta,
                                 cdnn_handle y, int n, int c, int hw, cdnn_handle stream);

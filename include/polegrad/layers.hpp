@@ -274,11 +274,14 @@ class ConvolutionLayer final : public Layer {
   bool can_split_backward() const override { return propagate_down(0); }
   void backward_weights(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   void backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  // Fuse a following in-place ReLU into the convolution epilogue (set by Net).
+  void fuse_relu(bool on) { fused_relu_ = on; }
 
  private:
   ConvolutionParam p_;
   std::shared_ptr<Registry> reg_;
   cdnn_handle desc_ = 0;
+  bool fused_relu_ = false;
   std::vector<std::shared_ptr<Blob>> params_;
 };
 
@@ -302,8 +305,11 @@ class PoolingLayer final : public Layer {
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   // Flat h*W+w argmax per output element (MAX only); downloads from HBM.
   std::vector<int> mask() const;
+  // Fuse a following in-place ReLU into the pooling output (set by Net).
+  void fuse_relu(bool on) { fused_relu_ = on; }
 
  private:
+  bool fused_relu_ = false;
   PoolingParam p_;
   std::shared_ptr<Registry> reg_;
   cdnn_handle desc_ = 0;
@@ -382,6 +388,7 @@ class DropoutLayer final : public Layer {
 
 // BatchNorm with mini-batch statistics (use_global_stats false); no affine part
 // (Caffe pairs it with Scale).  In place allowed.
+class ScaleLayer;
 class BatchNormLayer final : public Layer {
  public:
   BatchNormLayer(LayerSpec spec, double eps) : Layer(std::move(spec)), eps_(eps) {}
@@ -389,8 +396,14 @@ class BatchNormLayer final : public Layer {
                            Rng& rng) override;
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  // Fuse the following Scale layer (set by Net): forward writes the Scale's top
+  // z = gamma*xnorm + beta directly, backward reads its top diff and produces the
+  // Scale's parameter gradients too (one reduction pass each way).
+  void fuse_scale(ScaleLayer* scale, Blob* scale_top) { fused_ = scale; z_ = scale_top; }
 
  private:
+  ScaleLayer* fused_ = nullptr;
+  Blob* z_ = nullptr;
   double eps_;
   int n_ = 0, c_ = 0, hw_ = 0;
   std::unique_ptr<Blob> mean_, invstd_, scratch_;
@@ -406,8 +419,13 @@ class ScaleLayer final : public Layer {
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   const std::vector<std::shared_ptr<Blob>>& params() const override { return params_; }
+  // Forward/backward done by the preceding BatchNorm (BatchNormLayer::fuse_scale).
+  void set_fused(bool on) { fused_ = on; }
+  Blob& gamma() { return *params_[0]; }
+  Blob* beta() { return bias_ ? params_[1].get() : nullptr; }
 
  private:
+  bool fused_ = false;
   bool bias_;
   int n_ = 0, c_ = 0, hw_ = 0;
   std::unique_ptr<Blob> x_;  // private input copy when in place / rewritten

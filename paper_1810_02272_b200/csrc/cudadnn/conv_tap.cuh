@@ -57,6 +57,7 @@ struct TapArgs {
   int64_t in_nstride;    // image stride of `in`
   int64_t out_nstride;   // image stride of `out`
   int nbuf, stages;      // A buffers (1|2), weight ring depth
+  int relu;              // fused in-place ReLU in the epilogue (forward)
   int fold;              // S folded into the channels (k = s*Cin + c, Cin*S <= 32): R taps of K = S*Cin
   FastDiv div_hwv, div_wv;
   unsigned long long* trace;  // debug timeline (CDNN_TAP_TRACE), null in production
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (n < a.Cout) {
               float o = __uint_as_float(r[j]);
               if (a.bias) o += __ldg(a.bias + n);
+              if (a.relu) o = o > 0.f ? o : 0.f;
               outp[int64_t(n) * PQ] = o;
             }
           }

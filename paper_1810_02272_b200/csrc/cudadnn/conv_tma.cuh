@@ -40,6 +40,7 @@ struct ConvTmaArgs {
   int tiles_q, tiles_p;     // tiles along q and p
   const float* bias;        // may be null (fwd only)
   float* out;
+  int relu;                 // fused in-place ReLU (fwd only)
 };
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (n < a.Cout) {
             float v = __uint_as_float(r[j]);
             if (a.bias) v += a.bias[n];
+            if (a.relu) v = v > 0.f ? v : 0.f;
             outp[int64_t(n) * PQ] = v;
           }
         }

@@ -338,10 +338,12 @@ struct ConvFwdEpi {
   T* y;                  // offset to the group's first output channel
   const T* bias;         // offset to the group's first channel, may be null
   ConvGeom g;
+  bool relu = false;     // fused in-place ReLU (max(v, 0), strict > like layers.cpp:184)
   __device__ __forceinline__ void store(int m, int n, T acc, int) const {
     const uint32_t img = g.div_PQ.div(m), pq = m - img * g.P * g.Q;
     T v = acc;
     if (bias) v += bias[n];
+    if (relu) v = v > T(0) ? v : T(0);
     y[(int64_t(img) * g.Co + n) * g.P * g.Q + pq] = v;
   }
 };

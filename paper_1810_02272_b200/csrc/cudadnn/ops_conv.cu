@@ -120,7 +120,7 @@ void launch_conv_tap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const CUtenso
 // Tap-shift implicit GEMM (conv_tap.cuh): stride 1, any dilation, any group count.
 // Returns false when the staged tile does not fit shared memory.
 bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const float* in, const float* w,
-              const float* bias, float* out, cdnn_handle stream) {
+              const float* bias, float* out, cdnn_handle stream, bool relu = false) {
   ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
   const ConvGeom& g = d.geom;
   if (!conv_tap_enabled() || g.sh != 1 || g.sw != 1) return false;
@@ -141,6 +141,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   tctap::TapArgs a{};
   a.N = g.N; a.Cin = Cin; a.Hin = Hin; a.Win = Win; a.Cout = Cout; a.P = P; a.Q = Q;
   a.R = g.R; a.S = g.S; a.dh = g.dh; a.dw = g.dw; a.oh = oh; a.ow = ow;
+  a.relu = relu ? 1 : 0;
   a.Hv = P + g.dh * (g.R - 1);
   a.Wv = Q + g.dw * (g.S - 1);
   if (int64_t(g.N) * a.Hv * a.Wv >= (int64_t(1) << 31)) return false;
@@ -359,7 +360,7 @@ void launch_conv_tma(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& tin,
 // backward_data: out = dx, in = dy, flipped taps.  Returns false when the
 // shape is not eligible (the implicit-GEMM gather path handles it).
 bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const float* in, const float* w,
-                     const float* bias, float* out, cdnn_handle stream) {
+                     const float* bias, float* out, cdnn_handle stream, bool relu = false) {
   ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
   const ConvGeom& g = d.geom;
   if (!conv_tma_enabled() || g.group != 1 || g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1) return false;
@@ -384,6 +385,7 @@ bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, con
   const int tiles_n = (g.N + a.NB - 1) / a.NB;
   a.bias = bias;
   a.out = out;
+  a.relu = relu ? 1 : 0;
   const int tiles = a.tiles_q * a.tiles_p * tiles_n;
   int bn = Cout <= 32 ? 32 : (Cout <= 64 ? 64 : 128);
   if (bn > 32 && tiles * ((Cout + bn - 1) / bn) < kNumSMs) bn = bn == 128 ? 64 : 32;
@@ -571,7 +573,7 @@ bool conv_dgrad_s2d(Ctx* c, const ConvDescSlot& d, const float* w, const float* 
 }
 
 bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float* w, const float* bias, float* y,
-                      cdnn_handle stream) {
+                      cdnn_handle stream, bool relu = false) {
   if (!s2d_eligible(d.geom)) return false;
   ConvDescSlot& e = s2d_desc(c, d);
   const ConvGeom &g = d.geom, &h = e.geom;
@@ -582,25 +584,26 @@ bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float
   s2d_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R * h.S, 256), 256, 0, st>>>(w, wsb, g, h);
   check_launch("s2d");
   count_launch(c, 2);
-  return conv_tap(c, e, false, xs, wsb, bias, y, stream);
+  return conv_tap(c, e, false, xs, wsb, bias, y, stream, relu);
 }
 
 template <typename T>
 void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const BufferSlot& Wt,
-                    const BufferSlot* B, BufferSlot& Y, cdnn_handle stream) {
+                    const BufferSlot* B, BufferSlot& Y, cdnn_handle stream, bool relu) {
   const ConvGeom& g = d.geom;
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
   const int M = g.N * g.P * g.Q, N = g.Cog, K = d.Kc;
   if constexpr (std::is_same_v<T, float>) {
     if (conv_forward_s2d(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
-                         B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
+                         B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream,
+                         relu))
       return;
     if (conv_tap(c, d, false, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
-                 B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
+                 B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream, relu))
       return;
     if (conv_direct_tma(c, d, false, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
-                        B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream))
+                        B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream, relu))
       return;
   }
   for (int grp = 0; grp < g.group; ++grp) {
@@ -609,7 +612,7 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
     ConvFwdA<T> va{x, d.taps, g, M, K};
     DenseView<T> vb{w, int64_t(K), 1, N, K, false};
     ConvFwdEpi<T> epi{reinterpret_cast<T*>(Y.dev) + int64_t(grp) * g.Cog * g.P * g.Q,
-                      B ? reinterpret_cast<const T*>(B->dev) + grp * g.Cog : nullptr, g};
+                      B ? reinterpret_cast<const T*>(B->dev) + grp * g.Cog : nullptr, g, relu};
     if constexpr (std::is_same_v<T, float>) {
       const GemmPlan pl = plan_tc(M, N, K);
       TmaReq rb;
@@ -805,6 +808,11 @@ extern "C" {
 
 int cdnn_conv_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle w, cdnn_handle bias,
                       cdnn_handle y, cdnn_handle stream) {
+  return cdnn_conv_forward_ex(ctx, desc, x, w, bias, y, 0, stream);
+}
+
+int cdnn_conv_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle w, cdnn_handle bias,
+                         cdnn_handle y, int flags, cdnn_handle stream) {
   return guarded([&] {
     Ctx* c = need_ctx(ctx);
     const ConvDescSlot& d = conv_desc(c, desc);
@@ -820,8 +828,9 @@ int cdnn_conv_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle
     require_dtype(W, X.dtype, "conv w");
     require_dtype(Y, X.dtype, "conv y");
     DeviceGuard dg(c);
-    if (X.dtype == CDNN_F32) conv_forward_t<float>(c, d, X, W, B, Y, stream);
-    else if (X.dtype == CDNN_F64) conv_forward_t<double>(c, d, X, W, B, Y, stream);
+    const bool relu = (flags & CDNN_CONV_RELU) != 0;
+    if (X.dtype == CDNN_F32) conv_forward_t<float>(c, d, X, W, B, Y, stream, relu);
+    else if (X.dtype == CDNN_F64) conv_forward_t<double>(c, d, X, W, B, Y, stream, relu);
     else fail(CDNN_INVALID_ARGUMENT, "conv: floating buffers required");
   });
 }

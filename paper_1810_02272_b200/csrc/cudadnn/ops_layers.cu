@@ -221,6 +221,45 @@ __global__ void scale_bwd_data(const T* __restrict__ dy, const T* __restrict__ g
   plane_apply(dx, off, HW, [&](int64_t i) { return dy[i] * gc; });
 }
 
+// ---- fused BatchNorm + Scale (z = gamma*xn + beta, xn = (x - mean)*invstd) ----------
+template <typename T>
+__global__ void bn_scale_apply(const T* __restrict__ x, const T* __restrict__ mean, const T* __restrict__ invstd,
+                               const T* __restrict__ g, const T* __restrict__ bta, T* __restrict__ xn,
+                               T* __restrict__ z, int C, int HW) {
+  const int c = blockIdx.y % C;
+  const T m = mean[c], is = invstd[c], gc = g[c], bc = bta ? bta[c] : T(0);
+  const int64_t off = int64_t(blockIdx.y) * HW;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) {
+    const T v = (x[off + i] - m) * is;
+    xn[off + i] = v;
+    z[off + i] = v * gc + bc;
+  }
+}
+
+// backward sums (S0 = sum dz, S1 = sum dz*xn): dbeta += S0, dgamma += S1,
+// a = S0/M, b = S1/M for dx = gamma*invstd*(dz - a - xn*b)
+template <typename T>
+__global__ void bn_scale_finalize(const double2* part, int splits, int C, double cnt, T* dg, T* db, T* a, T* b) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double2 s = sum_parts(part, c, splits);
+  if (db) db[c] += T(s.x);
+  if (dg) dg[c] += T(s.y);
+  a[c] = T(s.x / cnt);
+  b[c] = T(s.y / cnt);
+}
+
+template <typename T>
+__global__ void bn_scale_bwd_apply(const T* __restrict__ xn, const T* __restrict__ dz, const T* __restrict__ a,
+                                   const T* __restrict__ b, const T* __restrict__ invstd, const T* __restrict__ g,
+                                   T* __restrict__ dx, int C, int HW) {
+  const int c = blockIdx.y % C;
+  const T ac = a[c], bc = b[c], k = invstd[c] * g[c];
+  const int64_t off = int64_t(blockIdx.y) * HW;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x)
+    dx[off + i] = (dz[off + i] - ac - xn[off + i] * bc) * k;
+}
+
 // launch helpers: splits so each partial block covers ~32k elements; plane grid
 inline int chan_splits(int N, int C, int HW) {
   // >= 4 blocks per SM in total, >= 2048 elements per block, <= N
@@ -440,6 +479,80 @@ int cdnn_scale_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_han
       }
     });
     check_launch("scale_bwd");
+  });
+}
+
+int cdnn_batchnorm_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle xnorm, cdnn_handle z, cdnn_handle mean,
+                                 cdnn_handle invstd, cdnn_handle gamma, cdnn_handle beta, int n, int c, int hw,
+                                 double eps, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& X = buffer(cx, x, "bn_scale x");
+    BufferSlot& XN = buffer(cx, xnorm, "bn_scale xnorm");
+    BufferSlot& Z = buffer(cx, z, "bn_scale z");
+    BufferSlot& M = buffer(cx, mean, "bn_scale mean");
+    BufferSlot& V = buffer(cx, invstd, "bn_scale invstd");
+    BufferSlot& G = buffer(cx, gamma, "bn_scale gamma");
+    BufferSlot* B = buffer_or_null(cx, beta, "bn_scale beta");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    for (BufferSlot* b : {&X, &XN, &Z}) require_len(*b, cnt, "bn_scale");
+    for (BufferSlot* b : {&M, &V, &G}) require_len(*b, uint64_t(c), "bn_scale");
+    if (B) require_len(*B, uint64_t(c), "bn_scale");
+    for (BufferSlot* b : {&XN, &Z, &M, &V, &G, B}) if (b) require_dtype(*b, X.dtype, "bn_scale");
+    if (n * c > 65535) fail(CDNN_INVALID_ARGUMENT, "bn_scale: n*c must be <= 65535");
+    DeviceGuard g(cx);
+    cudaStream_t st = stream_of(cx, stream);
+    const int splits = chan_splits(n, c, hw);
+    double2* part = static_cast<double2*>(workspace_of(cx, stream).get(size_t(c) * splits * sizeof(double2), cx->device));
+    by_dtype(X.dtype, "bn_scale", [&](auto tag) {
+      using T = decltype(tag);
+      chan_partials<T, kSumSq><<<dim3(c, splits), kT, 0, st>>>(P<T>(X), nullptr, part, n, c, hw, splits);
+      bn_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, double(n) * hw, eps, P<T>(M), P<T>(V));
+      bn_scale_apply<T><<<plane_grid(n, c, hw), kT, 0, st>>>(P<T>(X), P<T>(M), P<T>(V), P<T>(G), B ? P<T>(*B) : nullptr,
+                                                            P<T>(XN), P<T>(Z), c, hw);
+    });
+    check_launch("bn_scale_fwd");
+    count_launch(cx, 3);
+  });
+}
+
+int cdnn_batchnorm_scale_backward(cdnn_ctx ctx, cdnn_handle xnorm, cdnn_handle invstd, cdnn_handle gamma,
+                                  cdnn_handle dz, cdnn_handle dx, cdnn_handle dgamma, cdnn_handle dbeta,
+                                  cdnn_handle scratch, int n, int c, int hw, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& XN = buffer(cx, xnorm, "bn_scale_bwd xnorm");
+    BufferSlot& V = buffer(cx, invstd, "bn_scale_bwd invstd");
+    BufferSlot& G = buffer(cx, gamma, "bn_scale_bwd gamma");
+    BufferSlot& DZ = buffer(cx, dz, "bn_scale_bwd dz");
+    BufferSlot* DX = buffer_or_null(cx, dx, "bn_scale_bwd dx");
+    BufferSlot* DG = buffer_or_null(cx, dgamma, "bn_scale_bwd dgamma");
+    BufferSlot* DB = buffer_or_null(cx, dbeta, "bn_scale_bwd dbeta");
+    BufferSlot& S = buffer(cx, scratch, "bn_scale_bwd scratch");
+    const uint64_t cnt = uint64_t(n) * c * hw;
+    require_len(XN, cnt, "bn_scale_bwd"); require_len(DZ, cnt, "bn_scale_bwd");
+    if (DX) require_len(*DX, cnt, "bn_scale_bwd");
+    require_len(V, uint64_t(c), "bn_scale_bwd"); require_len(G, uint64_t(c), "bn_scale_bwd");
+    require_len(S, 2 * uint64_t(c), "bn_scale_bwd scratch");
+    for (BufferSlot* b : {&V, &G, &DZ, &S, DX, DG, DB}) if (b) require_dtype(*b, XN.dtype, "bn_scale_bwd");
+    if (n * c > 65535) fail(CDNN_INVALID_ARGUMENT, "bn_scale_bwd: n*c must be <= 65535");
+    DeviceGuard g(cx);
+    cudaStream_t st = stream_of(cx, stream);
+    const int splits = chan_splits(n, c, hw);
+    double2* part = static_cast<double2*>(workspace_of(cx, stream).get(size_t(c) * splits * sizeof(double2), cx->device));
+    by_dtype(XN.dtype, "bn_scale_bwd", [&](auto tag) {
+      using T = decltype(tag);
+      T* a = P<T>(S);
+      T* b = a + c;
+      chan_partials<T, kSumDot><<<dim3(c, splits), kT, 0, st>>>(P<T>(DZ), P<T>(XN), part, n, c, hw, splits);
+      bn_scale_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, double(n) * hw, DG ? P<T>(*DG) : nullptr,
+                                                           DB ? P<T>(*DB) : nullptr, a, b);
+      if (DX)
+        bn_scale_bwd_apply<T><<<plane_grid(n, c, hw), kT, 0, st>>>(P<T>(XN), P<T>(DZ), a, b, P<T>(V), P<T>(G),
+                                                                  P<T>(*DX), c, hw);
+    });
+    check_launch("bn_scale_bwd");
+    count_launch(cx, DX ? 3 : 2);
   });
 }
 

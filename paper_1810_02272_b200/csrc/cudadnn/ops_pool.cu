@@ -32,7 +32,7 @@ __device__ __forceinline__ Idx3 split3(uint32_t i, const FastDiv& dhw, const Fas
 
 template <typename T>
 __global__ void __launch_bounds__(256) max_pool_fwd(const T* __restrict__ x, T* __restrict__ y, int* __restrict__ mask,
-                                                    PoolGeom g, uint32_t total) {
+                                                    PoolGeom g, uint32_t total, bool relu) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Idx3 q = split3(i, g.divPHW, g.divPW, uint32_t(g.PH * g.PW), uint32_t(g.PW));
     int hs = int(q.h) * g.sh - g.ph, ws = int(q.w) * g.sw - g.pw;
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) max_pool_fwd(const T* __restrict__ x, T* 
         const T v = __ldg(plane + h * g.W + w);
         if (v > best) { best = v; arg = h * g.W + w; }
       }
-    y[i] = best;
+    y[i] = relu ? (best > T(0) ? best : T(0)) : best;  // fused in-place ReLU on the pooled top
     if (mask) mask[i] = arg;
   }
 }
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) max_pool_bwd(const T* __restrict__ dy, co
 
 template <typename T>
 __global__ void __launch_bounds__(256) ave_pool_fwd(const T* __restrict__ x, T* __restrict__ y, PoolGeom g,
-                                                    uint32_t total) {
+                                                    uint32_t total, bool relu) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Idx3 q = split3(i, g.divPHW, g.divPW, uint32_t(g.PH * g.PW), uint32_t(g.PW));
     int hs = int(q.h) * g.sh - g.ph, ws = int(q.w) * g.sw - g.pw;
@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(256) ave_pool_fwd(const T* __restrict__ x, T* 
     T s = T(0);
     for (int h = hs; h < he; ++h)
       for (int w = ws; w < we; ++w) s += __ldg(plane + h * g.W + w);
-    y[i] = s / T(pool);
+    const T v = s / T(pool);
+    y[i] = relu ? (v > T(0) ? v : T(0)) : v;
   }
 }
 
@@ -146,7 +147,13 @@ extern "C" {
 
 int cdnn_pool_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle y, cdnn_handle mask,
                       cdnn_handle stream) {
+  return cdnn_pool_forward_ex(ctx, desc, x, y, mask, 0, stream);
+}
+
+int cdnn_pool_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle y, cdnn_handle mask, int flags,
+                         cdnn_handle stream) {
   return guarded([&] {
+    const bool relu = (flags & CDNN_POOL_RELU) != 0;
     Ctx* c = need_ctx(ctx);
     PoolDescSlot d = pool_desc(c, desc);
     BufferSlot& X = buffer(c, x, "pool x");
@@ -165,10 +172,10 @@ int cdnn_pool_forward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle
       using T = decltype(tag);
       if (d.p.method == CDNN_POOL_MAX)
         max_pool_fwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(X.dev), reinterpret_cast<T*>(Y.dev),
-                                                 M ? reinterpret_cast<int*>(M->dev) : nullptr, g, uint32_t(nout));
+                                                 M ? reinterpret_cast<int*>(M->dev) : nullptr, g, uint32_t(nout), relu);
       else
         ave_pool_fwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(X.dev), reinterpret_cast<T*>(Y.dev), g,
-                                                 uint32_t(nout));
+                                                 uint32_t(nout), relu);
     };
     if (X.dtype == CDNN_F32) run(float{});
     else if (X.dtype == CDNN_F64) run(double{});

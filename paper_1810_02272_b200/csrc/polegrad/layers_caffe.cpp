@@ -181,6 +181,18 @@ std::vector<Shape> BatchNormLayer::setup(const std::vector<Shape>& s, const std:
 
 void BatchNormLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
   Registry& reg = bottoms[0]->registry();
+  if (fused_) {
+    const cdnn_handle x = bottoms[0]->gpu_data();
+    const cdnn_handle z = z_ == bottoms[0] ? z_->mutable_gpu_data() : z_->overwrite_gpu_data();
+    Blob* beta = fused_->beta();
+    cdnn_ok(cdnn_batchnorm_scale_forward(reg.context(), x, xnorm_->overwrite_gpu_data(), z,
+                                         mean_->overwrite_gpu_data(), invstd_->overwrite_gpu_data(),
+                                         fused_->gamma().gpu_data(), beta ? beta->gpu_data() : 0, n_, c_, hw_, eps_,
+                                         reg.stream()),
+            "BatchNorm+Scale forward");
+    (void)tops;
+    return;
+  }
   const cdnn_handle mean = mean_->overwrite_gpu_data(), inv = invstd_->overwrite_gpu_data();
   const bool in_place = tops[0] == bottoms[0];
   const cdnn_handle x = bottoms[0]->gpu_data();
@@ -197,8 +209,22 @@ void BatchNormLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* con
 }
 
 void BatchNormLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
-  if (!propagate_down(0)) return;
   Registry& reg = bottoms[0]->registry();
+  if (fused_) {
+    Blob* beta = fused_->beta();
+    const cdnn_handle dz = z_->gpu_diff();
+    const cdnn_handle dx = !propagate_down(0)   ? 0
+                           : z_ == bottoms[0] ? bottoms[0]->mutable_gpu_diff()
+                                              : bottoms[0]->overwrite_gpu_diff();
+    cdnn_ok(cdnn_batchnorm_scale_backward(reg.context(), xnorm_->gpu_data(), invstd_->gpu_data(),
+                                          fused_->gamma().gpu_data(), dz, dx, fused_->gamma().mutable_gpu_diff(),
+                                          beta ? beta->mutable_gpu_diff() : 0, scratch_->overwrite_gpu_data(), n_, c_,
+                                          hw_, reg.stream()),
+            "BatchNorm+Scale backward");
+    (void)tops;
+    return;
+  }
+  if (!propagate_down(0)) return;
   const cdnn_handle inv = invstd_->gpu_data();
   const cdnn_handle y = top_clobbered_ ? xnorm_->gpu_data() : tops[0]->gpu_data();
   const cdnn_handle dy = tops[0]->gpu_diff();
@@ -224,6 +250,7 @@ std::vector<Shape> ScaleLayer::setup(const std::vector<Shape>& s, const std::sha
 }
 
 void ScaleLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
+  if (fused_) return;
   Registry& reg = bottoms[0]->registry();
   const bool in_place = tops[0] == bottoms[0];
   cdnn_handle x = bottoms[0]->gpu_data();
@@ -238,6 +265,7 @@ void ScaleLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> 
 }
 
 void ScaleLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  if (fused_) return;
   Registry& reg = bottoms[0]->registry();
   const bool in_place = tops[0] == bottoms[0];
   const cdnn_handle x = (in_place || bottom_clobbered_) ? x_->gpu_data() : bottoms[0]->gpu_data();

@@ -126,7 +126,8 @@ void ConvolutionLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* c
   Registry& reg = *reg_;
   const cdnn_handle x = bottoms[0]->gpu_data(), w = params_[0]->gpu_data();
   const cdnn_handle b = p_.bias_term ? params_[1]->gpu_data() : 0;
-  cdnn_ok(cdnn_conv_forward(reg.context(), desc_, x, w, b, tops[0]->overwrite_gpu_data(), reg.stream()),
+  cdnn_ok(cdnn_conv_forward_ex(reg.context(), desc_, x, w, b, tops[0]->overwrite_gpu_data(),
+                               fused_relu_ ? CDNN_CONV_RELU : 0, reg.stream()),
           "Convolution forward");
 }
 
@@ -178,7 +179,8 @@ std::vector<Shape> PoolingLayer::setup(const std::vector<Shape>& s, const std::s
 void PoolingLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
   Registry& reg = *reg_;
   const cdnn_handle x = bottoms[0]->gpu_data();
-  cdnn_ok(cdnn_pool_forward(reg.context(), desc_, x, tops[0]->overwrite_gpu_data(), mask_, reg.stream()),
+  cdnn_ok(cdnn_pool_forward_ex(reg.context(), desc_, x, tops[0]->overwrite_gpu_data(), mask_,
+                               fused_relu_ ? CDNN_POOL_RELU : 0, reg.stream()),
           "Pooling forward");
 }
 

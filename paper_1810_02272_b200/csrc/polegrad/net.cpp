@@ -155,12 +155,32 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
     layers_[i]->set_clobbered(top, bottom);
   }
 
-  // Fuse InnerProduct + in-place ReLU: the ReLU runs in the GEMM epilogue.
+  // Fuse BatchNorm + the Scale reading its top (CDNN_FUSE_BN_SCALE=0 keeps them apart).
+  static const bool fuse_bn = [] {
+    const char* v = std::getenv("CDNN_FUSE_BN_SCALE");
+    return !(v && std::string(v) == "0");
+  }();
+  for (std::size_t i = 0; fuse_bn && i + 1 < layers_.size(); ++i) {
+    auto* bn = dynamic_cast<BatchNormLayer*>(layers_[i].get());
+    auto* sc = dynamic_cast<ScaleLayer*>(layers_[i + 1].get());
+    if (bn && sc && bottoms_[i + 1][0] == tops_[i][0]) {
+      bn->fuse_scale(sc, tops_[i + 1][0]);
+      sc->set_fused(true);
+    }
+  }
+
+  // Fuse InnerProduct / Convolution + in-place ReLU: the ReLU runs in the epilogue.
   for (std::size_t i = 0; i + 1 < layers_.size(); ++i) {
-    auto* ip = dynamic_cast<InnerProductLayer*>(layers_[i].get());
     auto* relu = dynamic_cast<ReluLayer*>(layers_[i + 1].get());
-    if (ip && relu && bottoms_[i + 1][0] == tops_[i][0] && tops_[i + 1][0] == tops_[i][0]) {
+    if (!relu || bottoms_[i + 1][0] != tops_[i][0] || tops_[i + 1][0] != tops_[i][0]) continue;
+    if (auto* ip = dynamic_cast<InnerProductLayer*>(layers_[i].get())) {
       ip->fuse_relu(true);
+      relu->set_forward_fused(true);
+    } else if (auto* conv = dynamic_cast<ConvolutionLayer*>(layers_[i].get()); conv && !compat) {
+      conv->fuse_relu(true);
+      relu->set_forward_fused(true);
+    } else if (auto* pool = dynamic_cast<PoolingLayer*>(layers_[i].get()); pool && !compat) {
+      pool->fuse_relu(true);
       relu->set_forward_fused(true);
     }
   }

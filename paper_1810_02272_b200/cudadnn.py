@@ -48,7 +48,8 @@ EXPORTS = [
     "cdnn_nccl_available", "cdnn_nccl_unique_id", "cdnn_nccl_comm_create", "cdnn_allreduce_sum",
     "cdnn_broadcast", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_dropout", "cdnn_counter_increment",
     "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
-    "cdnn_axpby",
+    "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
+    "cdnn_pool_forward_ex",
 ]
 
 
@@ -116,9 +117,10 @@ def load() -> C.CDLL:
             "cdnn_ip_forward": ([vp, h, h, h, h, i, i, i, i, h], i),
             "cdnn_ip_backward": ([vp, h, h, h, h, h, h, i, i, i, h], i),
             "cdnn_conv_forward": ([vp, h, h, h, h, h, h], i),
+            "cdnn_conv_forward_ex": ([vp, h, h, h, h, h, i, h], i),
             "cdnn_conv_backward_data": ([vp, h, h, h, h, h], i),
             "cdnn_conv_backward_filter": ([vp, h, h, h, h, h, h], i),
-            "cdnn_pool_forward": ([vp, h, h, h, h, h], i), "cdnn_pool_backward": ([vp, h, h, h, h, h], i),
+            "cdnn_pool_forward": ([vp, h, h, h, h, h], i), "cdnn_pool_forward_ex": ([vp, h, h, h, h, i, h], i), "cdnn_pool_backward": ([vp, h, h, h, h, h], i),
             "cdnn_relu_forward": ([vp, h, h, u64, h], i), "cdnn_relu_backward": ([vp, h, h, h, u64, h], i),
             "cdnn_sigmoid_forward": ([vp, h, h, u64, h], i), "cdnn_sigmoid_backward": ([vp, h, h, h, u64, h], i),
             "cdnn_softmax_forward": ([vp, h, h, i, i, h], i), "cdnn_softmax_backward": ([vp, h, h, h, i, i, h], i),
@@ -136,6 +138,8 @@ def load() -> C.CDLL:
             "cdnn_scale_forward": ([vp, h, h, h, h, i, i, i, h], i),
             "cdnn_scale_backward": ([vp, h, h, h, h, h, h, i, i, i, h], i),
             "cdnn_axpby": ([vp, u64, d, h, d, h, i, h], i),
+            "cdnn_batchnorm_scale_forward": ([vp, h, h, h, h, h, h, h, i, i, i, d, h], i),
+            "cdnn_batchnorm_scale_backward": ([vp, h, h, h, h, h, h, h, h, i, i, i, h], i),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

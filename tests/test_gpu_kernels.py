@@ -297,3 +297,25 @@ def test_scale_and_axpby(ctx, dtype, bias):
     ctx.call("cdnn_axpby", x.size, 2.0, hx, 0.0, hy, 0, 0)
     ctx.call("cdnn_axpby", x.size, -0.5, hdy, 1.0, hy, 1, 0)
     assert rel_l2(ctx.read(hy), 2 * x.astype(np.float64) - 0.5 * d64) <= tol
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("case", [(2, 32, 16, 16, 32, 5, 1, 2, 1, 1), (3, 3, 32, 32, 32, 5, 1, 2, 1, 1),
+                                  (2, 3, 35, 35, 16, 11, 4, 0, 1, 1), (2, 8, 13, 13, 12, 3, 1, 1, 1, 2)])
+def test_conv_forward_fused_relu(ctx, dtype, case):
+    """cdnn_conv_forward_ex(CDNN_CONV_RELU) == relu(conv) on every forward path (tap, window-TMA,
+    space-to-depth, gather)."""
+    n, c, h, w, co, k, s, p, dl, g = case
+    rng = np.random.default_rng(sum(case) + 1)
+    x = rng.uniform(-1, 1, (n, c, h, w))
+    wt = rng.uniform(-1, 1, (co, c // g, k, k))
+    b = rng.uniform(-1, 1, co)
+    y = np.maximum(conv_ref(x, wt, b, s, p, dl, g), 0.0)
+    dt = NP[dtype]
+    d = ctx.conv_desc(n, c, h, w, co, k, s, p, dl, g)
+    hx, hw, hb = ctx.upload(x.astype(dt)), ctx.upload(wt.astype(dt)), ctx.upload(b.astype(dt))
+    hy = ctx.alloc(y.size, dtype)
+    ctx.call("cdnn_conv_forward_ex", d, hx, hw, hb, hy, 1, 0)
+    out = ctx.read(hy)
+    assert rel_l2(out, y) <= TOL[dtype]
+    assert (out >= 0).all()
