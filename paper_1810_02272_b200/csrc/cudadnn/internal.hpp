@@ -59,6 +59,13 @@ struct Workspace {
   size_t bytes = 0;
   std::vector<std::shared_ptr<DevAlloc>> blocks;
   void* get(size_t need, int device);
+  // a second, independent scratch on the same stream (operand transposes that must
+  // stay alive while the split-K partials use this one)
+  std::unique_ptr<Workspace> second;
+  Workspace& aux() {
+    if (!second) second = std::make_unique<Workspace>();
+    return *second;
+  }
 };
 
 struct StreamSlot {

@@ -47,6 +47,34 @@ GemmPlan plan_simt(int M, int N, int K) {
   return p;
 }
 
+// Tiled transpose: in [R][C] (leading dimension ld) -> out [C][R] (leading dimension R).
+__global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out, int R, int C, int64_t ld) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = r0 + j, c = c0 + threadIdx.x;
+    tile[j][threadIdx.x] = (r < R && c < C) ? in[int64_t(r) * ld + c] : 0.f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int c = c0 + j, r = r0 + threadIdx.x;
+    if (c < C && r < R) out[int64_t(c) * R + r] = tile[threadIdx.x][j];
+  }
+}
+
+// An MN-contiguous operand of a large tensor-core GEMM, copied K-major: the
+// producers then load 16-byte K vectors instead of scalars (one extra HBM pass,
+// repaid many times by the contraction).
+DenseView<float> k_major_copy(Ctx* c, cudaStream_t st, Workspace& scratch, size_t offset_elems,
+                              const DenseView<float>& v) {
+  float* out = static_cast<float*>(scratch.ptr) + offset_elems;
+  dim3 grid((v.rows + 31) / 32, (v.K + 31) / 32);
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(v.p, out, v.K, v.rows, v.sk);
+  check_launch("transpose");
+  count_launch(c);
+  return DenseView<float>{out, int64_t(v.K), 1, v.rows, v.K, false};
+}
+
 // One GEMM D[m][n] = sum_k A(m,k) B(n,k) with dense views, routed by dtype.
 template <typename T>
 static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const DenseView<T>& va,
@@ -62,6 +90,18 @@ static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const De
       return;
     }
     const GemmPlan pl = plan_tc(M, N, K);
+    if (int64_t(M) * N * K >= (int64_t(1) << 28) && (va.mcontig || vb.mcontig)) {
+      Workspace& aux = ws.aux();
+      const size_t na = va.mcontig ? size_t(va.rows) * va.K : 0, nb = vb.mcontig ? size_t(vb.rows) * vb.K : 0;
+      aux.get((na + nb) * sizeof(float), c->device);
+      const DenseView<float> ka = va.mcontig ? k_major_copy(c, st, aux, 0, va) : va;
+      const DenseView<float> kb = vb.mcontig ? k_major_copy(c, st, aux, na, vb) : vb;
+      TmaReq ra2, rb2;
+      with_operand(c, ka, tc::BM, ra2, [&](const auto& a) {
+        with_operand(c, kb, pl.bn, rb2, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra2, rb2); });
+      });
+      return;
+    }
     TmaReq ra, rb;
     with_operand(c, va, tc::BM, ra, [&](const auto& a) {
       with_operand(c, vb, pl.bn, rb, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra, rb); });
