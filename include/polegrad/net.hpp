@@ -91,6 +91,8 @@ class Net {
   void reuse_resident_batch();
   // Zero every parameter gradient on the device (one fill over the grad arena).
   void zero_param_diffs();
+  // Stream of the parameter-gradient halves of the two-stream backward (0 until used).
+  cdnn_handle side_stream() const { return side_stream_; }
   // First MemoryData layer (the feed), or nullptr.
   MemoryDataLayer* feed_layer();
   // After replaying a captured step: every blob's and parameter's device copy

@@ -273,7 +273,7 @@ bool split_backward_enabled() {
 // which the remaining bottom-gradient chain touches; the solver joins it.
 void Net::backward_layer(std::size_t i, bool& forked) {
   Layer& l = *layers_[i];
-  const bool split = split_backward_enabled() && !backward_hook_ && !reference_compat() && l.can_split_backward();
+  const bool split = split_backward_enabled() && !reference_compat() && l.can_split_backward();
   if (!split) {
     l.backward(tops_[i], bottoms_[i]);
     return;

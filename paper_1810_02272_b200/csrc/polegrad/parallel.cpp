@@ -71,11 +71,12 @@ void Parallel::broadcast_weights() {
 void Parallel::launch(std::size_t b) {
   if (launched_[b]) return;
   launched_[b] = true;
-  if (nranks_ == 1) return;  // one rank: the sum is the local gradient
   Registry& reg = *net_->registry();
   const GradBucket& k = buckets_[b];
-  // the comm stream waits for every gradient queued so far on the compute stream
+  // the comm stream waits for every gradient queued so far on the compute stream and
+  // on the backward side stream (parameter-gradient halves, Net::backward_layer)
   cdnn_ok(cdnn_stream_wait(reg.context(), comm_stream_, reg.stream()), "allreduce");
+  if (net_->side_stream()) cdnn_ok(cdnn_stream_wait(reg.context(), comm_stream_, net_->side_stream()), "allreduce");
   cdnn_ok(cdnn_allreduce_sum(reg.context(), comm_, reg.in(net_->grad_arena()), k.begin, k.end - k.begin, comm_stream_),
           "allreduce");
 }
@@ -93,7 +94,7 @@ void Parallel::reduce_gradients(Net& net) {
   for (Blob* p : net.params()) p->gpu_diff();  // host-side gradient edits go up first
   for (std::size_t b = 0; b < buckets_.size(); ++b) launch(b);
   Registry& reg = *net.registry();
-  if (nranks_ > 1) cdnn_ok(cdnn_stream_wait(reg.context(), reg.stream(), comm_stream_), "allreduce join");
+  cdnn_ok(cdnn_stream_wait(reg.context(), reg.stream(), comm_stream_), "allreduce join");
   launched_.assign(buckets_.size(), false);
 }
 

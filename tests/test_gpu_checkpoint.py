@@ -1,6 +1,8 @@
 """Checkpoint / resume: MCWT weights + MCSS solver state
 taken mid-run restore into a fresh Net and Solver, and the resumed run is bit
 identical to the uninterrupted one (same kernels, deterministic reductions)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -108,3 +110,33 @@ def test_feed_ring_rejects_overfill():
     ring.pop_loss()
     with pytest.raises(Exception, match="wrong number"):
         ring.push(x[:50], y)
+
+
+def test_parallel_one_rank_nccl_matches_single_process():
+    """polegrad::Parallel end to end on a real NCCL communicator (1 rank on this
+    1-GPU box): weight broadcast, bucketed all-reduce on the comm stream hooked
+    into the two-stream backward, join before the update.  A 1-rank sum is the
+    identity, so training is bit-identical to the plain single-process run."""
+    cd = polegrad.cudadnn
+    ok = C.c_int()
+    cd.load().cdnn_nccl_available(C.byref(ok))
+    if not ok.value:
+        pytest.skip("NCCL not loadable")
+    text = polegrad.load_model("cifar10_quick")
+    kw = CONFIGS["cifar10_quick"][1]
+    batches = synthetic_batches((100, 3, 32, 32), 10, 4, seed=9)
+    a = polegrad.Net(text, 1, "f32")
+    sa = polegrad.Solver(a, **kw)
+    b = polegrad.Net(text, 1, "f32")
+    sb = polegrad.Solver(b, **kw)
+    par = polegrad.Parallel(b, 1, 0, polegrad.Parallel.unique_id(), bucket_bytes=64 << 10)
+    sb.set_parallel(par)
+    par.broadcast()
+    for x, y in batches:
+        for n, s in ((a, sa), (b, sb)):
+            n.set_batch(x, y)
+            n.forward()
+            n.backward()
+            s.apply()
+    for i in range(len(a.param_info())):
+        assert np.array_equal(a.param(i), b.param(i)), a.param_info()[i]
