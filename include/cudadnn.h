@@ -333,6 +333,15 @@ CDNN_API int cdnn_scale_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma,
 CDNN_API int cdnn_axpby(cdnn_ctx ctx, uint64_t n, double a, cdnn_handle x, double b, cdnn_handle y,
                         int accumulate, cdnn_handle stream);
 
+/* ---- policy-gradient diff injection (trainer.cpp:42-113) ----
+ * dlogit (rows x classes) = modulated log-prob gradient of n steps, 0 for rows >= n:
+ *   softmax (sigmoid = 0): (prob - onehot(action)) * return
+ *   sigmoid (sigmoid = 1, classes = 1): -((action == 0 ? 1 - p : -p) * return)
+ * actions / returns: n values in the prob buffer's dtype. */
+CDNN_API int cdnn_pg_diff(cdnn_ctx ctx, cdnn_handle prob, cdnn_handle actions, cdnn_handle returns,
+                          cdnn_handle dlogit, int rows, int n, int classes, int sigmoid,
+                          cdnn_handle stream);
+
 /* ---- solver (solver.cpp:24-57 + Caffe momentum / weight decay) ----------- */
 typedef enum { CDNN_SOLVER_SGD = 0, CDNN_SOLVER_RMSPROP = 1 } cdnn_solver_method;
 /* One fused pass over n elements of (w, g, hist):

@@ -89,6 +89,14 @@ class Net {
   // Treat the data layer's current top contents as this step's batch (inputs
   // already resident in HBM; no feed copy).
   void reuse_resident_batch();
+  // Policy-gradient step of a whole episode batch: after a
+  // forward of the first n rows of the feed, write the modulated log-prob
+  // gradients (trainer.cpp:42-113: softmax (p - onehot(a))*G, sigmoid -(dlogp*G))
+  // into `logit_blob`'s diff on the device (rows >= n get 0) and run
+  // backward_from(logit_blob) once -- the batched equivalent of the reference's
+  // per-step accumulate_step (trainer.cpp:204-216).  One H2D of 2n values.
+  void pg_backward(const std::string& logit_blob, const std::string& prob_blob, std::span<const real> actions,
+                   std::span<const real> returns, bool sigmoid);
   // Zero every parameter gradient on the device (one fill over the grad arena).
   void zero_param_diffs();
   // Stream of the parameter-gradient halves of the two-stream backward (0 until used).
@@ -126,6 +134,7 @@ class Net {
   // parameter-gradient halves of splittable layers run here, in parallel with
   // the bottom-gradient chain on the registry stream (CDNN_SPLIT_BACKWARD=0 off)
   cdnn_handle side_stream_ = 0;
+  Handle pg_actions_{}, pg_returns_{};  // pg_backward inputs (batch-sized)
   void backward_layer(std::size_t i, bool& forked);
 };
 

@@ -35,6 +35,10 @@ PG_API int pg_net_free(pg_net* net);
 PG_API int pg_net_forward(pg_net* net);
 PG_API int pg_net_backward(pg_net* net);
 PG_API int pg_net_backward_from(pg_net* net, const char* blob);
+/* policy-gradient episode batch (Net::pg_backward, trainer.cpp:42-216 batched on the
+ * device): n actions / returns in `real`, sigmoid = 1 for the sigmoid policy head */
+PG_API int pg_net_pg_backward(pg_net* net, const char* logit_blob, const char* prob_blob, const void* actions,
+                              const void* returns, uint64_t n, int sigmoid);
 PG_API int pg_net_loss(pg_net* net, double* out);
 /* whole batch (+ labels when the data layer has a label top) from host memory */
 PG_API int pg_net_set_batch(pg_net* net, const void* data, const void* labels);

@@ -260,6 +260,27 @@ __global__ void bn_scale_bwd_apply(const T* __restrict__ xn, const T* __restrict
     dx[off + i] = (dz[off + i] - ac - xn[off + i] * bc) * k;
 }
 
+// ---- policy-gradient diff injection (trainer.cpp:42-113 restated on the device) ----------
+// softmax: dlogit[r][c] = (p[r][c] - [c == a_r]) * G_r        (dlogps_softmax, sign +1)
+// sigmoid: dlogit[r][0] = -((a_r == 0 ? 1 - p : -p) * G_r)    (dlogps_sigmoid, sign -1)
+// rows >= n (padding of a fixed-batch net) get 0, so they add nothing to the gradients.
+template <typename T>
+__global__ void pg_diff_kernel(const T* __restrict__ prob, const T* __restrict__ act, const T* __restrict__ ret,
+                               T* __restrict__ dlogit, int rows, int n, int classes, int sigmoid) {
+  const int64_t total = int64_t(rows) * classes;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(i / classes), c = int(i - int64_t(r) * classes);
+    T v = T(0);
+    if (r < n) {
+      const int a = int(act[r]);
+      const T p = prob[i], g = ret[r];
+      if (sigmoid) v = -((a == 0 ? T(1) - p : T(0) - p) * g);
+      else v = (p - (c == a ? T(1) : T(0))) * g;
+    }
+    dlogit[i] = v;
+  }
+}
+
 // launch helpers: splits so each partial block covers ~32k elements; plane grid
 inline int chan_splits(int N, int C, int HW) {
   // >= 4 blocks per SM in total, >= 2048 elements per block, <= N
@@ -553,6 +574,32 @@ int cdnn_batchnorm_scale_backward(cdnn_ctx ctx, cdnn_handle xnorm, cdnn_handle i
     });
     check_launch("bn_scale_bwd");
     count_launch(cx, DX ? 3 : 2);
+  });
+}
+
+int cdnn_pg_diff(cdnn_ctx ctx, cdnn_handle prob, cdnn_handle actions, cdnn_handle returns, cdnn_handle dlogit,
+                 int rows, int n, int classes, int sigmoid, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* cx = need_ctx(ctx);
+    BufferSlot& Pb = buffer(cx, prob, "pg_diff prob");
+    BufferSlot& A = buffer(cx, actions, "pg_diff actions");
+    BufferSlot& R = buffer(cx, returns, "pg_diff returns");
+    BufferSlot& D = buffer(cx, dlogit, "pg_diff dlogit");
+    if (rows < 1 || classes < 1 || n < 0 || n > rows) fail(CDNN_INVALID_ARGUMENT, "pg_diff: bad extents");
+    if (sigmoid && classes != 1) fail(CDNN_INVALID_ARGUMENT, "pg_diff: the sigmoid variant has one logit per row");
+    if (!sigmoid && classes < 2) fail(CDNN_INVALID_ARGUMENT, "pg_diff: the softmax variant needs >= 2 logits");
+    const uint64_t cnt = uint64_t(rows) * classes;
+    require_len(Pb, cnt, "pg_diff"); require_len(D, cnt, "pg_diff");
+    require_len(A, uint64_t(std::max(n, 1)), "pg_diff actions"); require_len(R, uint64_t(std::max(n, 1)), "pg_diff returns");
+    for (BufferSlot* b : {&A, &R, &D}) require_dtype(*b, Pb.dtype, "pg_diff");
+    DeviceGuard g(cx);
+    by_dtype(Pb.dtype, "pg_diff", [&](auto tag) {
+      using T = decltype(tag);
+      pg_diff_kernel<T><<<blocks(int64_t(cnt)), kT, 0, stream_of(cx, stream)>>>(P<T>(Pb), P<T>(A), P<T>(R), P<T>(D),
+                                                                               rows, n, classes, sigmoid);
+    });
+    check_launch("pg_diff");
+    count_launch(cx);
   });
 }
 

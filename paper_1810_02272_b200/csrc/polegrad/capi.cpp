@@ -87,6 +87,14 @@ int pg_net_set_batch(pg_net* n, const void* data, const void* labels) {
   return run([&] { net_of(n).set_batch(static_cast<const real*>(data), static_cast<const real*>(labels)); });
 }
 
+int pg_net_pg_backward(pg_net* n, const char* logit_blob, const char* prob_blob, const void* actions,
+                       const void* returns, uint64_t count, int sigmoid) {
+  return run([&] {
+    net_of(n).pg_backward(logit_blob, prob_blob, std::span<const real>(static_cast<const real*>(actions), count),
+                          std::span<const real>(static_cast<const real*>(returns), count), sigmoid != 0);
+  });
+}
+
 int pg_net_enqueue(pg_net* n, const char* layer, const void* sample, uint64_t count) {
   return run([&] {
     data_layer(net_of(n), layer)->enqueue(std::span<const real>(static_cast<const real*>(sample), count));

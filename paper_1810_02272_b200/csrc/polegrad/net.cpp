@@ -360,6 +360,34 @@ void Net::set_batch(const real* data, const real* labels) {
   throw ModelError("set_batch: net has no MemoryData layer");
 }
 
+void Net::pg_backward(const std::string& logit_blob, const std::string& prob_blob, std::span<const real> actions,
+                      std::span<const real> returns, bool sigmoid) {
+  Blob& logit = blob(logit_blob);
+  Blob& prob = blob(prob_blob);
+  const int rows = logit.shape().n();
+  const int classes = int(logit.count() / std::size_t(rows));
+  if (prob.count() != logit.count()) throw InvalidArgument("pg_backward: prob and logit blobs differ in size");
+  if (actions.size() != returns.size()) throw InvalidArgument("pg_backward: one return per action required");
+  if (actions.size() > std::size_t(rows))
+    throw InvalidArgument("pg_backward: " + std::to_string(actions.size()) + " steps exceed the batch of " +
+                          std::to_string(rows));
+  Registry& reg = *registry_;
+  const std::size_t n = actions.size();
+  if (!pg_actions_) {
+    pg_actions_ = reg.alloc_buffer(std::size_t(rows));
+    pg_returns_ = reg.alloc_buffer(std::size_t(rows));
+  }
+  std::vector<real> a(std::size_t(rows), real(0)), g(std::size_t(rows), real(0));
+  std::copy(actions.begin(), actions.end(), a.begin());
+  std::copy(returns.begin(), returns.end(), g.begin());
+  reg.write(pg_actions_, a);
+  reg.write(pg_returns_, g);
+  cdnn_ok(cdnn_pg_diff(reg.context(), prob.gpu_data(), reg.in(pg_actions_), reg.in(pg_returns_),
+                       logit.overwrite_gpu_diff(), rows, int(n), classes, sigmoid ? 1 : 0, reg.stream()),
+          "pg_backward");
+  backward_from(logit_blob);
+}
+
 void Net::zero_param_diffs() {
   if (!param_total_) return;
   Registry& reg = *registry_;

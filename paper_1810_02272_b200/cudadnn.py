@@ -49,7 +49,7 @@ EXPORTS = [
     "cdnn_broadcast", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_dropout", "cdnn_counter_increment",
     "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
     "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
-    "cdnn_pool_forward_ex",
+    "cdnn_pool_forward_ex", "cdnn_pg_diff",
 ]
 
 
@@ -138,6 +138,7 @@ def load() -> C.CDLL:
             "cdnn_scale_forward": ([vp, h, h, h, h, i, i, i, h], i),
             "cdnn_scale_backward": ([vp, h, h, h, h, h, h, i, i, i, h], i),
             "cdnn_axpby": ([vp, u64, d, h, d, h, i, h], i),
+            "cdnn_pg_diff": ([vp, h, h, h, h, i, i, i, i, h], i),
             "cdnn_batchnorm_scale_forward": ([vp, h, h, h, h, h, h, h, i, i, i, d, h], i),
             "cdnn_batchnorm_scale_backward": ([vp, h, h, h, h, h, h, h, h, i, i, i, h], i),
         }

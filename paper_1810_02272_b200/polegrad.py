@@ -34,7 +34,7 @@ EXPORTS = [
     "pg_parallel_unique_id", "pg_parallel_create", "pg_parallel_free", "pg_parallel_broadcast",
     "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip", "pg_solver_snapshot",
     "pg_solver_restore", "pg_solver_iterations", "pg_feed_ring_create", "pg_feed_ring_free", "pg_feed_ring_push",
-    "pg_feed_ring_pop_loss",
+    "pg_feed_ring_pop_loss", "pg_net_pg_backward",
 ]
 
 
@@ -56,6 +56,7 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_last_error": ([], cp), "pg_real_size": ([], i),
             "pg_net_create": ([cp, u64, i, C.POINTER(vp)], i), "pg_net_free": ([vp], i),
             "pg_net_forward": ([vp], i), "pg_net_backward": ([vp], i), "pg_net_backward_from": ([vp, cp], i),
+            "pg_net_pg_backward": ([vp, cp, cp, vp, vp, u64, i], i),
             "pg_net_loss": ([vp, C.POINTER(d)], i), "pg_net_set_batch": ([vp, vp, vp], i),
             "pg_net_enqueue": ([vp, cp, vp, u64], i), "pg_net_sync": ([vp], i),
             "pg_net_context": ([vp, C.POINTER(vp)], i), "pg_net_num_layers": ([vp], i),
@@ -162,6 +163,13 @@ class Net:
 
     def backward_from(self, blob: str) -> None:
         self._c("pg_net_backward_from", blob.encode())
+
+    def pg_backward(self, actions, returns, logit: str = "logits", prob: str = "prob", sigmoid: bool = False) -> None:
+        """Policy-gradient episode batch on the device (Net::pg_backward)."""
+        a = np.ascontiguousarray(actions, dtype=self.np)
+        g = np.ascontiguousarray(returns, dtype=self.np)
+        self._c("pg_net_pg_backward", logit.encode(), prob.encode(), a.ctypes.data, g.ctypes.data, a.size,
+                1 if sigmoid else 0)
 
     def loss(self) -> float:
         v = C.c_double()

@@ -1,0 +1,59 @@
+"""Policy-gradient episode on the device: one batched forward
+of an episode's states, the modulated log-prob gradients computed on the device
+(cdnn_pg_diff) and ONE backward_from(logits) give the same parameter gradients
+as the reference trainer's per-step path (trainer.cpp:204-216: batch-1 forward,
+pending diff copied into the logits, backward_from, accumulated over the
+episode), run here through the unmodified reference Net (oracle)."""
+import numpy as np
+import pytest
+
+from parity_util import TOL, pyoracle, polegrad, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def discount(rewards, gamma, normalize):
+    """trainer.cpp:64-90 (discount_rewards)"""
+    out = np.zeros(len(rewards))
+    running = 0.0
+    for t in range(len(rewards) - 1, -1, -1):
+        running = rewards[t] + gamma * running
+        out[t] = running
+    if normalize:
+        out -= out.mean()
+        sd = np.sqrt((out * out).mean())
+        if sd >= 1e-10:
+            out /= sd
+    return out
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("steps", [1, 37, 64])
+def test_batched_episode_gradient_matches_per_step_reference(dtype, steps):
+    rng = np.random.default_rng(steps)
+    states = rng.uniform(-1, 1, (steps, 4, 1, 1))
+    rewards = np.ones(steps)
+    returns = discount(rewards, 0.99, normalize=True)
+    # reference: batch-1 net, one step at a time (the oracle is the unmodified reference Net)
+    orc = pyoracle.OracleNet(polegrad.load_model("pg_mlp", 1), 1, dtype)
+    actions = np.zeros(steps)
+    for t in range(steps):
+        orc.set_batch(states[t:t + 1])
+        orc.forward()
+        p = orc.blob("prob").ravel()
+        a = int(rng.uniform() < p[1])  # sampled action
+        actions[t] = a
+        d = p.copy()
+        d[a] -= 1.0
+        orc.set_blob("logits", (d * returns[t]).reshape(1, 1, 1, 2), diff=True)
+        orc.backward_from("logits")
+    # B200: one batch-64 forward of the episode (padded), device diffs, one backward
+    net = polegrad.Net(polegrad.load_model("pg_mlp", 64), 1, dtype)
+    x = np.zeros((64, 4, 1, 1))
+    x[:steps] = states
+    net.set_batch(x)
+    net.forward()
+    net.pg_backward(actions, returns)
+    for i, (name, _) in enumerate(net.param_info()):
+        err = rel_l2(net.param(i, diff=True), orc.param(i, diff=True))
+        assert err <= TOL[dtype], (name, err)
