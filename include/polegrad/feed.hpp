@@ -15,6 +15,7 @@
 #include <span>
 #include <vector>
 
+#include "polegrad/imagedb.hpp"
 #include "polegrad/net.hpp"
 #include "polegrad/solver.hpp"
 
@@ -33,6 +34,11 @@ class FeedRing {
   // when the feed has no label top) into the next slot and enqueues its step.
   // InvalidState when every slot holds a loss not yet popped.
   void push(std::span<const real> data, std::span<const real> labels);
+  // Samples one batch from `dataset` (imagedb::Dataset::sample, one draw per image
+  // from `rng`) and gathers the tensors and labels straight into the next pinned
+  // slot, then enqueues its step.  InvalidArgument when a
+  // sampled tensor does not match the feed's sample size.
+  void push_sampled(const imagedb::Dataset& dataset, imagedb::SampleMethod method, bool use_boost, Rng& rng);
   // Waits for the oldest pushed step and returns its loss.  InvalidState when
   // nothing is in flight.
   double pop_loss();
@@ -48,10 +54,12 @@ class FeedRing {
     cdnn_handle graph = 0;
     cdnn_handle done = 0;  // event recorded after the slot's step
   };
+  Slot& acquire();
+  void launch(Slot& s);
   Net& net_;
   Solver& solver_;
   std::vector<Slot> slots_;
-  std::size_t data_len_ = 0, label_len_ = 0;
+  std::size_t data_len_ = 0, label_len_ = 0, batch_ = 0;
   std::uint64_t pushed_ = 0, popped_ = 0;
 };
 

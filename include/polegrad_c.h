@@ -25,6 +25,8 @@ typedef struct pg_net pg_net;
 typedef struct pg_solver pg_solver;
 typedef struct pg_feed_ring pg_feed_ring;
 typedef struct pg_parallel pg_parallel;
+typedef struct pg_imagedb pg_imagedb;
+typedef struct pg_rng pg_rng;
 
 PG_API const char* pg_last_error(void);
 PG_API int pg_real_size(void);
@@ -80,6 +82,23 @@ PG_API int pg_feed_ring_free(pg_feed_ring* r);
 PG_API int pg_feed_ring_push(pg_feed_ring* r, const void* data, uint64_t n_data, const void* labels,
                              uint64_t n_labels);
 PG_API int pg_feed_ring_pop_loss(pg_feed_ring* r, double* loss);
+/* samples one batch from `db` (method 0 uniform, 1 label-balanced; one draw of
+ * `rng` per image, polegrad/imagedb.hpp) straight into the next pinned slot and
+ * enqueues its step */
+PG_API int pg_feed_ring_push_sampled(pg_feed_ring* r, const pg_imagedb* db, int method, int use_boost, pg_rng* rng);
+
+/* labelled image dataset (include/polegrad/imagedb.hpp; reference imagedb.hpp:12-53).
+ * load: CDNN_LOAD_ERROR with the 1-based index line in pg_last_error(). */
+PG_API int pg_imagedb_load(const char* index_path, pg_imagedb** out);
+PG_API int pg_imagedb_free(pg_imagedb* db);
+PG_API int pg_imagedb_size(const pg_imagedb* db, uint64_t* out);
+PG_API int pg_imagedb_set_boost(pg_imagedb* db, int64_t id, double boost);
+/* n draws of Dataset::sample -> entry ids (the same sequence push_sampled gathers) */
+PG_API int pg_imagedb_sample(const pg_imagedb* db, int method, int use_boost, pg_rng* rng, uint64_t n,
+                             int64_t* ids);
+/* polegrad::Rng (mt19937_64; uniform01 = (next >> 11) * 2^-53) */
+PG_API int pg_rng_create(uint64_t seed, pg_rng** out);
+PG_API int pg_rng_free(pg_rng* rng);
 
 /* Captures one training step  feed(H2D from `data`/`labels`) -> forward ->
  * backward -> solver update -> D2H of the loss into `loss_out`  into a CUDA

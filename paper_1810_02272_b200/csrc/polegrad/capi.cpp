@@ -10,6 +10,7 @@
 #include "polegrad/solver.hpp"
 #include "polegrad_c.h"
 #include "polegrad/feed.hpp"
+#include "polegrad/imagedb.hpp"
 
 struct pg_net {
   std::unique_ptr<polegrad::Net> net;
@@ -252,6 +253,58 @@ int pg_feed_ring_push(pg_feed_ring* r, const void* data, uint64_t n_data, const 
 }
 
 int pg_feed_ring_pop_loss(pg_feed_ring* r, double* loss) { return run([&] { *loss = r->ring->pop_loss(); }); }
+
+struct pg_imagedb {
+  polegrad::imagedb::Dataset db;
+};
+struct pg_rng {
+  polegrad::Rng rng;
+};
+
+namespace {
+polegrad::imagedb::SampleMethod sample_method(int method) {
+  if (method != 0 && method != 1) throw polegrad::InvalidArgument("sample method must be 0 (uniform) or 1 (label balanced)");
+  return method ? polegrad::imagedb::SampleMethod::kLabelBalanced : polegrad::imagedb::SampleMethod::kUniform;
+}
+}  // namespace
+
+int pg_feed_ring_push_sampled(pg_feed_ring* r, const pg_imagedb* db, int method, int use_boost, pg_rng* rng) {
+  return run([&] {
+    if (!r || !db || !rng) throw polegrad::InvalidArgument("null ring, dataset or rng");
+    r->ring->push_sampled(db->db, sample_method(method), use_boost != 0, rng->rng);
+  });
+}
+
+int pg_imagedb_load(const char* index_path, pg_imagedb** out) {
+  return run([&] {
+    if (!index_path || !out) throw polegrad::InvalidArgument("null path or out");
+    auto d = std::make_unique<pg_imagedb>();
+    d->db = polegrad::imagedb::load(index_path);
+    *out = d.release();
+  });
+}
+
+int pg_imagedb_free(pg_imagedb* db) { return run([&] { delete db; }); }
+
+int pg_imagedb_size(const pg_imagedb* db, uint64_t* out) { return run([&] { *out = db->db.size(); }); }
+
+int pg_imagedb_set_boost(pg_imagedb* db, int64_t id, double boost) {
+  return run([&] { db->db.set_boost(id, static_cast<real>(boost)); });
+}
+
+int pg_imagedb_sample(const pg_imagedb* db, int method, int use_boost, pg_rng* rng, uint64_t n, int64_t* ids) {
+  return run([&] {
+    if (!db || !rng || (n && !ids)) throw polegrad::InvalidArgument("null dataset, rng or ids");
+    const auto m = sample_method(method);
+    for (uint64_t i = 0; i < n; ++i) ids[i] = db->db.sample(m, use_boost != 0, rng->rng).id;
+  });
+}
+
+int pg_rng_create(uint64_t seed, pg_rng** out) {
+  return run([&] { *out = new pg_rng{polegrad::Rng(seed)}; });
+}
+
+int pg_rng_free(pg_rng* rng) { return run([&] { delete rng; }); }
 
 int pg_step_capture(pg_net* n, pg_solver* s, const void* data, const void* labels, void* loss_out, uint64_t* graph) {
   return run([&] {

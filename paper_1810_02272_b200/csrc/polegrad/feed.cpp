@@ -13,7 +13,8 @@ FeedRing::FeedRing(Net& net, Solver& solver, int depth) : net_(net), solver_(sol
   MemoryDataLayer* feed = net.feed_layer();
   if (!feed) throw ModelError("feed ring: the net has no MemoryData layer");
   if (net.loss_blobs().empty()) throw InvalidState("feed ring: the net has no loss top");
-  data_len_ = std::size_t(feed->batch_size()) * feed->sample_size();
+  batch_ = std::size_t(feed->batch_size());
+  data_len_ = batch_ * feed->sample_size();
   label_len_ = feed->spec().tops.size() > 1 ? std::size_t(feed->batch_size()) : 0;
   Registry& reg = *net.registry();
   cdnn_ctx ctx = reg.context();
@@ -77,19 +78,41 @@ void FeedRing::release() noexcept {
   slots_.clear();
 }
 
-void FeedRing::push(std::span<const real> data, std::span<const real> labels) {
-  if (data.size() != data_len_) throw InvalidArgument("feed ring: batch has the wrong number of values");
-  if (labels.size() != label_len_) throw InvalidArgument("feed ring: wrong number of labels");
+FeedRing::Slot& FeedRing::acquire() {
   if (pushed_ - popped_ >= slots_.size()) throw InvalidState("feed ring: full, pop_loss() first");
-  Slot& s = slots_[pushed_ % slots_.size()];
   // the slot's previous step was popped, so its graph has finished reading it
-  std::memcpy(s.data, data.data(), data_len_ * sizeof(real));
-  if (label_len_) std::memcpy(s.labels, labels.data(), label_len_ * sizeof(real));
+  return slots_[pushed_ % slots_.size()];
+}
+
+void FeedRing::launch(Slot& s) {
   Registry& reg = *net_.registry();
   cdnn_ok(cdnn_graph_launch(reg.context(), s.graph, reg.stream()), "feed ring push");
   cdnn_ok(cdnn_event_record(reg.context(), s.done, reg.stream()), "feed ring push");
   ++pushed_;
   solver_.uncount_updates(-1);  // one real update
+}
+
+void FeedRing::push(std::span<const real> data, std::span<const real> labels) {
+  if (data.size() != data_len_) throw InvalidArgument("feed ring: batch has the wrong number of values");
+  if (labels.size() != label_len_) throw InvalidArgument("feed ring: wrong number of labels");
+  Slot& s = acquire();
+  std::memcpy(s.data, data.data(), data_len_ * sizeof(real));
+  if (label_len_) std::memcpy(s.labels, labels.data(), label_len_ * sizeof(real));
+  launch(s);
+}
+
+void FeedRing::push_sampled(const imagedb::Dataset& dataset, imagedb::SampleMethod method, bool use_boost, Rng& rng) {
+  Slot& s = acquire();
+  const std::size_t per = data_len_ / batch_;
+  for (std::size_t b = 0; b < batch_; ++b) {
+    const imagedb::Entry& e = dataset.sample(method, use_boost, rng);
+    if (e.tensor.size() != per)
+      throw InvalidArgument("feed ring: sampled entry " + std::to_string(e.id) + " has " +
+                            std::to_string(e.tensor.size()) + " values, the feed takes " + std::to_string(per));
+    std::memcpy(s.data + b * per, e.tensor.data(), per * sizeof(real));
+    if (label_len_) s.labels[b] = static_cast<real>(e.label);
+  }
+  launch(s);
 }
 
 double FeedRing::pop_loss() {

@@ -34,7 +34,9 @@ EXPORTS = [
     "pg_parallel_unique_id", "pg_parallel_create", "pg_parallel_free", "pg_parallel_broadcast",
     "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip", "pg_solver_snapshot",
     "pg_solver_restore", "pg_solver_iterations", "pg_feed_ring_create", "pg_feed_ring_free", "pg_feed_ring_push",
-    "pg_feed_ring_pop_loss", "pg_net_pg_backward",
+    "pg_feed_ring_pop_loss", "pg_net_pg_backward", "pg_feed_ring_push_sampled", "pg_imagedb_load",
+    "pg_imagedb_free", "pg_imagedb_size", "pg_imagedb_set_boost", "pg_imagedb_sample", "pg_rng_create",
+    "pg_rng_free",
 ]
 
 
@@ -79,6 +81,11 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_plan_buckets": ([C.POINTER(u64), C.POINTER(u64), i, u64, u64, C.POINTER(C.c_int32),
                                  C.POINTER(C.c_int32)], i),
             "pg_prototxt_roundtrip": ([cp, cp, u64, C.POINTER(u64)], i),
+            "pg_feed_ring_push_sampled": ([vp, vp, i, i, vp], i),
+            "pg_imagedb_load": ([cp, C.POINTER(vp)], i), "pg_imagedb_free": ([vp], i),
+            "pg_imagedb_size": ([vp, C.POINTER(u64)], i), "pg_imagedb_set_boost": ([vp, C.c_int64, d], i),
+            "pg_imagedb_sample": ([vp, i, i, vp, u64, C.POINTER(C.c_int64)], i),
+            "pg_rng_create": ([u64, C.POINTER(vp)], i), "pg_rng_free": ([vp], i),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -355,6 +362,12 @@ class FeedRing:
                                                     None if y is None else y.ctypes.data,
                                                     0 if y is None else y.size))
 
+    def push_sampled(self, db: "ImageDB", rng: "Rng", method: str = "uniform", use_boost: bool = False) -> None:
+        """Samples one batch from `db` (one `rng` draw per image) and gathers it
+        straight into the next pinned slot (polegrad::FeedRing::push_sampled)."""
+        _check(self.lib, self.lib.pg_feed_ring_push_sampled(self.ptr, db.ptr, _SAMPLE_METHODS[method],
+                                                            int(use_boost), rng.ptr))
+
     def pop_loss(self) -> float:
         v = C.c_double()
         _check(self.lib, self.lib.pg_feed_ring_pop_loss(self.ptr, C.byref(v)))
@@ -370,6 +383,81 @@ class FeedRing:
             self.close()
         except Exception:
             pass
+
+
+_SAMPLE_METHODS = {"uniform": 0, "label_balanced": 1}
+
+
+class _Owned:
+    _free = ""
+
+    def close(self) -> None:
+        if getattr(self, "ptr", None):
+            _check(self.lib, getattr(self.lib, self._free)(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Rng(_Owned):
+    """polegrad::Rng (mt19937_64, uniform01 = (next >> 11) * 2^-53)."""
+    _free = "pg_rng_free"
+
+    def __init__(self, seed: int, dtype: str = "f32"):
+        self.lib = load(dtype)
+        p = C.c_void_p()
+        _check(self.lib, self.lib.pg_rng_create(seed, C.byref(p)))
+        self.ptr = p
+
+
+class ImageDB(_Owned):
+    """polegrad::imagedb::Dataset loaded from an index file (reference imagedb.hpp:12-53;
+    format in include/polegrad/imagedb.hpp, writer: write_imagedb)."""
+    _free = "pg_imagedb_free"
+
+    def __init__(self, index_path: str, dtype: str = "f32"):
+        self.lib = load(dtype)
+        p = C.c_void_p()
+        _check(self.lib, self.lib.pg_imagedb_load(str(index_path).encode(), C.byref(p)))
+        self.ptr = p
+
+    def __len__(self) -> int:
+        n = C.c_uint64()
+        _check(self.lib, self.lib.pg_imagedb_size(self.ptr, C.byref(n)))
+        return n.value
+
+    def set_boost(self, entry_id: int, boost: float) -> None:
+        _check(self.lib, self.lib.pg_imagedb_set_boost(self.ptr, entry_id, boost))
+
+    def sample(self, rng: Rng, n: int, method: str = "uniform", use_boost: bool = False) -> np.ndarray:
+        ids = np.zeros(n, dtype=np.int64)
+        _check(self.lib, self.lib.pg_imagedb_sample(self.ptr, _SAMPLE_METHODS[method], int(use_boost), rng.ptr, n,
+                                                    ids.ctypes.data_as(C.POINTER(C.c_int64))))
+        return ids
+
+
+def write_imagedb(directory: str, entries) -> str:
+    """Writes `entries` = [(id, label, boost, tensor CxHxW float array), ...] in the
+    index format polegrad::imagedb::load reads; returns the index path."""
+    os.makedirs(directory, exist_ok=True)
+    lines = []
+    for eid, label, boost, tensor in entries:
+        t = np.ascontiguousarray(tensor, dtype="<f4")
+        if t.ndim != 3:
+            raise ValueError("tensor must be C x H x W")
+        name = f"{eid}.bin"
+        with open(os.path.join(directory, name), "wb") as f:
+            f.write(np.asarray(t.shape, dtype="<u4").tobytes())
+            f.write(t.tobytes())
+        lines.append(f"{eid},{label},{boost},{name}")
+    index = os.path.join(directory, "index.csv")
+    with open(index, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    return index
 
 
 class Parallel:

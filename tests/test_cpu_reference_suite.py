@@ -1,7 +1,7 @@
 """Oracle pinning and boundary-input parity on the CPU (no GPU needed).
 
 * reftests_ref  — the reference's own unit tests (backend, blob, layers, net,
-  solver, prototxt: 75 cases / ~4.5k assertions, incl. the gemm / softmax / FD
+  solver, prototxt, imagedb: 88 cases / ~4.5k assertions, incl. the gemm / softmax / FD
   known-answer tests of SURVEY §8(c)) compiled against the UNMODIFIED reference
   core: the oracle is the reference, and this proves the build is faithful.
 * reftests_b200 prototxt cases — the same unmodified prototxt tests compiled
@@ -29,7 +29,7 @@ def _run(args, env=None):
 def test_reference_suite_passes_on_reference_core():
     rc, out = _run([REF_BIN])
     assert rc == 0, out[-3000:]
-    assert "75 passed | 0 failed" in out
+    assert "88 passed | 0 failed" in out
 
 
 @pytest.mark.skipif(not (os.path.exists(B200_BIN) and HAVE_REF), reason="reftests_b200 not built here")
@@ -47,3 +47,13 @@ def test_extended_mode_only_flips_the_convolution_assertion():
     assert "9 passed | 1 failed" in out and "| 1 failed" in out, out[-2000:]
     # the one failing case is the reference's "Convolution is unknown" check
     assert "layer validation errors point at the offending line" in out, out[-2000:]
+
+
+@pytest.mark.skipif(not (os.path.exists(B200_BIN) and HAVE_REF), reason="reftests_b200 not built here")
+def test_reference_imagedb_suite_on_b200_library():
+    """The reference's imagedb tests (dataset, label-balanced / boosted sampling
+    statistics, index + tensor-file loading and its error lines) against the B200
+    library's own imagedb (host-only)."""
+    rc, out = _run([B200_BIN, "imagedb_test"])
+    assert rc == 0, out[-3000:]
+    assert "13 passed | 0 failed" in out

@@ -112,6 +112,54 @@ def test_feed_ring_rejects_overfill():
         ring.push(x[:50], y)
 
 
+@pytest.mark.parametrize("method,use_boost", [("uniform", False), ("label_balanced", True)])
+def test_feed_ring_push_sampled_matches_eager(tmp_path, method, use_boost):
+    """imagedb -> pinned slot gather: push_sampled trains
+    exactly like eager steps on the batches the same Rng seed samples."""
+    rs = np.random.RandomState(4)
+    entries = [(int(k * 13 + 5), int(rs.randint(0, 10)), float(1 + rs.randint(0, 3)),
+                rs.uniform(-1, 1, (3, 32, 32)).astype(np.float32)) for k in range(260)]
+    db = polegrad.ImageDB(polegrad.write_imagedb(str(tmp_path), entries))
+    by_id = {e[0]: e for e in entries}
+    text = polegrad.load_model("cifar10_quick")
+    kw = CONFIGS["cifar10_quick"][1]
+    steps = 5
+    ids = db.sample(polegrad.Rng(77), 100 * steps, method, use_boost).reshape(steps, 100)
+    a = polegrad.Net(text, 1, "f32")
+    sa = polegrad.Solver(a, **kw)
+    eager = []
+    for row in ids:
+        x = np.stack([by_id[i][3] for i in row])
+        y = np.array([by_id[i][1] for i in row], dtype=np.float32)
+        a.set_batch(x, y)
+        a.forward()
+        eager.append(a.loss())
+        a.backward()
+        sa.apply()
+    b = polegrad.Net(text, 1, "f32")
+    sb = polegrad.Solver(b, **kw)
+    ring = polegrad.FeedRing(b, sb, 2)
+    rng = polegrad.Rng(77)
+    got = []
+    for k in range(steps):
+        if k >= 2:
+            got.append(ring.pop_loss())
+        ring.push_sampled(db, rng, method, use_boost)
+    got += [ring.pop_loss(), ring.pop_loss()]
+    assert [np.float32(v) for v in got] == [np.float32(v) for v in eager]
+    for i in range(len(a.param_info())):
+        assert np.array_equal(a.param(i), b.param(i))
+    ring.close()
+
+
+def test_feed_ring_push_sampled_rejects_wrong_tensor(tmp_path):
+    db = polegrad.ImageDB(polegrad.write_imagedb(str(tmp_path), [(1, 0, 1.0, np.zeros((1, 2, 2)))]))
+    net = polegrad.Net(polegrad.load_model("cifar10_quick"), 1, "f32")
+    ring = polegrad.FeedRing(net, polegrad.Solver(net, method="sgd", lr=1e-3), 1)
+    with pytest.raises(Exception, match="sampled entry 1 has 4 values"):
+        ring.push_sampled(db, polegrad.Rng(1))
+
+
 def test_parallel_one_rank_nccl_matches_single_process():
     """polegrad::Parallel end to end on a real NCCL communicator (1 rank on this
     1-GPU box): weight broadcast, bucketed all-reduce on the comm stream hooked

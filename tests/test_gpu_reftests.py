@@ -1,5 +1,5 @@
 """The reference's own unit tests (/root/reference/proj/tests: backend, blob,
-layers, net, solver, prototxt; 75 cases), compiled unmodified against the
+layers, net, solver, prototxt, imagedb; 88 cases), compiled unmodified against the
 B200 library (oracle/_ref/reftests_b200, built by oracle/Makefile with a
 doctest stand-in) and run on the GPU in reference-compat mode.  The prototxt
 corpus case reads files under /root/reference, which does not exist on the
