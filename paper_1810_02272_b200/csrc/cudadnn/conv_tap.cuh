@@ -183,10 +183,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+    {
       constexpr uint32_t idesc = tc::make_idesc_tf32(BN);  // A, B K-major
       constexpr uint32_t idesc_cat = tc::make_idesc_tf32(2 * BN);
+      // Everything the loop needs is derived from kernel parameters and loop
+      // counters (uniform registers); the tap's row shift advances by adds.
+      const uint32_t s_step = uint32_t(a.dw) * 8u;                     // one filter column, 16 B units
+      const uint32_t r_step = uint32_t(a.dh * a.Wv) * 8u;              // one filter row
+      const int S_eff = a.fold ? 1 : a.S;
+      const int r_rot = rot / S_eff, s_rot = rot - r_rot * S_eff;
+      const uint32_t shift_rot = uint32_t(r_rot) * r_step + uint32_t(s_rot) * s_step;
+      const uint32_t a0 = ptx::smem_u32(abase), b0 = ptx::smem_u32(bbase);
       int stage = 0;
       uint32_t phase = 0;
       int aseq = 0, ts = 0;
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ts >= 2) ptx::mbar_wait(&t_empty[acc_buf], uint32_t((ts >> 1) - 1) & 1u);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(acc_buf * ACC);
-        bool first = true;
+        uint32_t acc0 = 0u;  // first MMA of the tile overwrites the accumulator
         for (int cb = 0; cb < a.cblocks; ++cb, ++aseq) {
           const int buf = aseq % a.nbuf;
           ptx::mbar_wait(&a_full[buf], uint32_t(aseq / a.nbuf) & 1u);
@@ -203,43 +211,55 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nk8 = ((a.fold ? a.S * a.Cin : min(32, a.Cin - cb * 32)) + 7) >> 3;
           // descriptors are built once; per MMA only the 16-byte-unit start
           // address in the low word moves (smem < 256 KB: no carry out of 14 bits)
-          const uint64_t dA = desc_sw128(ptx::smem_u32(abase + buf * A_BUF));
+          const uint64_t dA = desc_sw128(a0 + uint32_t(buf) * A_BUF);
           const uint64_t dAl = dA + (A_HALF >> 4);
+          uint32_t shift = shift_rot;
+          int r = r_rot, s = s_rot;
           for (int it = 0; it < taps; ++it) {
-            const int tap = it + rot < taps ? it + rot : it + rot - taps;
-            const int r = a.fold ? tap : tap / a.S, s = a.fold ? 0 : tap - r * a.S;
-            const uint64_t shift = uint64_t(r * a.dh * a.Wv + s * a.dw) * 8u;  // rows x 128 B in 16 B units
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            const uint64_t dB = desc_sw128(ptx::smem_u32(bbase + stage * B_STAGE));
+            const uint64_t dB = desc_sw128(b0 + uint32_t(stage) * B_STAGE);
             const uint64_t dBl = dB + (B_HALF >> 4);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              if (j < nk8) {
-                const uint64_t kj = uint64_t(j) * 2u;  // +32 B per k8 step
-                uint32_t acc = first ? 0u : 1u;
-                if constexpr (CAT) {
-                  // [B_hi | B_lo] are contiguous BN-row blocks: one N = 2*BN operand
-                  ptx::mma_tf32(d_tmem, dA + shift + kj, dB + kj, idesc_cat, acc);
-                  ptx::mma_tf32(d_tmem, dAl + shift + kj, dB + kj, idesc, 1u);
-                } else {
-                  if constexpr (SPLIT) {
-                    ptx::mma_tf32(d_tmem, dAl + shift + kj, dB + kj, idesc, acc);
-                    ptx::mma_tf32(d_tmem, dA + shift + kj, dBl + kj, idesc, 1u);
-                    acc = 1u;
-                  }
-                  ptx::mma_tf32(d_tmem, dA + shift + kj, dB + kj, idesc, acc);
+            const uint64_t ah = dA + shift, al = dAl + shift;
+            auto k8 = [&](int j, uint32_t acc) {
+              const uint64_t kj = uint64_t(j) * 2u;  // +32 B per k8 step
+              if constexpr (CAT) {
+                // [B_hi | B_lo] are contiguous BN-row blocks: one N = 2*BN operand
+                ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc_cat, acc);
+                ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, 1u);
+              } else {
+                if constexpr (SPLIT) {
+                  ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, acc);
+                  ptx::mma_tf32_elect(d_tmem, ah + kj, dBl + kj, idesc, 1u);
+                  acc = 1u;
                 }
-                first = false;
+                ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc, acc);
               }
+            };
+            if (nk8 == 4) {
+              k8(0, acc0);
+              k8(1, 1u);
+              k8(2, 1u);
+              k8(3, 1u);
+            } else {
+              k8(0, acc0);
+              for (int j = 1; j < nk8; ++j) k8(j, 1u);
             }
-            ptx::mma_commit(&empty[stage]);
+            acc0 = 1u;
+            ptx::mma_commit_elect(&empty[stage]);
             if (++stage == a.stages) { stage = 0; phase ^= 1; }
+            // next tap (rotated order wraps to tap 0)
+            if (++s == S_eff) {
+              s = 0;
+              if (++r == a.R) { r = 0; shift = 0; } else shift += r_step - uint32_t(S_eff - 1) * s_step;
+            } else {
+              shift += s_step;
+            }
           }
-          ptx::mma_commit(&a_empty[buf]);
+          ptx::mma_commit_elect(&a_empty[buf]);
         }
-        ptx::mma_commit(&t_full[acc_buf]);
-        TAP_TRACE(3 + 3 * ts);
+        ptx::mma_commit_elect(&t_full[acc_buf]);
+        if (lane == 0) TAP_TRACE(3 + 3 * ts);
       }
     }
     __syncwarp();

@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+    {
       // A: MN-major tf32 => 128B_BASE32B layout: rows of 32 pixels (128 B) per
       // channel, 4-channel groups 512 B apart (SBO), atoms CB*128 B apart (LBO)
       constexpr uint32_t a_lbo = uint32_t(CB) * 128u, a_kgrp = 8u * 128u;
@@ -201,16 +201,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (SPLIT) {
             const uint64_t dA_lo = make_desc(al + j * a_kgrp, a_lbo, 512u, 1u);
             const uint64_t dB_lo = make_desc(bl + j * 32u, 16u, b_sbo, b_layout);
-            ptx::mma_tf32(tmem, dA_lo, dB_hi, idesc, acc);
-            ptx::mma_tf32(tmem, dA_hi, dB_lo, idesc, 1u);
+            ptx::mma_tf32_elect(tmem, dA_lo, dB_hi, idesc, acc);
+            ptx::mma_tf32_elect(tmem, dA_hi, dB_lo, idesc, 1u);
             acc = 1u;
           }
-          ptx::mma_tf32(tmem, dA_hi, dB_hi, idesc, acc);
+          ptx::mma_tf32_elect(tmem, dA_hi, dB_hi, idesc, acc);
         }
-        ptx::mma_commit(&empty[stage]);
+        ptx::mma_commit_elect(&empty[stage]);
         if (++stage == ST) { stage = 0; phase ^= 1; }
       }
-      ptx::mma_commit(accum);
+      ptx::mma_commit_elect(accum);
     }
     __syncwarp();
   } else {

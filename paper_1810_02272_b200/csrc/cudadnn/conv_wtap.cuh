@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv_wtap_kernel(const WtapArgs a
   const int HWv = a.Hv * a.Wv;
 
   if (warp == 1) {
-    if (lane == 0 && ch1 > ch0) {
+    if (ch1 > ch0) {  // whole warp runs the loop, one elected lane issues
       // A MN-major (bit 15), B K-major; M = 128 = four 32-channel tap atoms, N = BN output channels
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (uint32_t(BN >> 3) << 17) |
                                  (uint32_t(TM >> 4) << 24);
@@ -159,21 +159,21 @@ __global__ void __launch_bounds__(kThreads, 2) conv_wtap_kernel(const WtapArgs a
             const uint32_t d_tmem = tmem + uint32_t(g * ACC);
             uint32_t acc = (ch > ch0 || k8 > 0) ? 1u : 0u;
             if constexpr (CAT) {
-              ptx::mma_tf32(d_tmem, dA, dB, idesc_cat, acc);
-              ptx::mma_tf32(d_tmem, dA + (A_H >> 4), dB, idesc, 1u);
+              ptx::mma_tf32_elect(d_tmem, dA, dB, idesc_cat, acc);
+              ptx::mma_tf32_elect(d_tmem, dA + (A_H >> 4), dB, idesc, 1u);
             } else {
               if constexpr (SPLIT) {
-                ptx::mma_tf32(d_tmem, dA + (A_H >> 4), dB, idesc, acc);
-                ptx::mma_tf32(d_tmem, dA, dBl, idesc, 1u);
+                ptx::mma_tf32_elect(d_tmem, dA + (A_H >> 4), dB, idesc, acc);
+                ptx::mma_tf32_elect(d_tmem, dA, dBl, idesc, 1u);
                 acc = 1u;
               }
-              ptx::mma_tf32(d_tmem, dA, dB, idesc, acc);
+              ptx::mma_tf32_elect(d_tmem, dA, dB, idesc, acc);
             }
           }
         }
-        ptx::mma_commit(&empty[b]);
+        ptx::mma_commit_elect(&empty[b]);
       }
-      ptx::mma_commit(accum);
+      ptx::mma_commit_elect(accum);
     }
     __syncwarp();
   } else if (warp >= 2) {

@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+    {
       constexpr uint32_t idesc = make_idesc_tf32(BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -277,16 +277,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (SPLIT) {
             const uint64_t al = make_sw128_desc(ptx::smem_u32(a_lo(stage)));
             const uint64_t bl = make_sw128_desc(ptx::smem_u32(b_lo(stage)));
-            ptx::mma_tf32(tmem, al + dk, bh + dk, idesc, acc);  // small terms first
-            ptx::mma_tf32(tmem, ah + dk, bl + dk, idesc, 1u);
+            ptx::mma_tf32_elect(tmem, al + dk, bh + dk, idesc, acc);  // small terms first
+            ptx::mma_tf32_elect(tmem, ah + dk, bl + dk, idesc, 1u);
             acc = 1u;
           }
-          ptx::mma_tf32(tmem, ah + dk, bh + dk, idesc, acc);
+          ptx::mma_tf32_elect(tmem, ah + dk, bh + dk, idesc, acc);
         }
-        ptx::mma_commit(&empty[stage]);
+        ptx::mma_commit_elect(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      ptx::mma_commit(accum);
+      ptx::mma_commit_elect(accum);
     }
     __syncwarp();
   } else {

@@ -2,9 +2,11 @@
 // per "tap": 4 k8 steps x {A_hi x [B_hi|B_lo] (N=64), A_lo x B_hi (N=32)} on a
 // row-shifted A start, then tcgen05.commit to an mbarrier -- 25 taps per tile.
 // Variants: 0 = pattern as in conv_tap, 1 = no per-tap commit, 2 = fixed A (no shift),
-// 3 = only N=32 MMAs (3 per k8, no concatenation).  Prints cycles per MMA.
+// 3 = only N=32 MMAs (3 per k8, no concatenation), 4 = separate accumulators per shape,
+// 5 = uniform N=64 pair into one accumulator, 6 = uniform N=64 pair into two, 7 = one N=64 per k8.  Prints cycles per MMA.
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include "../../paper_1810_02272_b200/csrc/cudadnn/ptx.cuh"
 using namespace cdnn;
@@ -16,13 +18,13 @@ __device__ uint64_t d128(uint32_t a) {
   return d;
 }
 
-__global__ void bench(int variant, int tiles, unsigned long long* out) {
+__global__ void bench(int variant, int tiles, unsigned long long* out, int fill) {
   extern __shared__ uint8_t raw[];
   uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar[16];
   __shared__ uint32_t slot;
   const int tid = threadIdx.x, warp = tid / 32;
-  for (int i = tid; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(s)[i] = 0.f;
+  for (int i = tid; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(s)[i] = fill ? __uint_as_float(((i * 2654435761u) & 0x007FE000u) | 0x3F000000u) * ((i & 1) ? -1.f : 1.f) : 0.f;
   if (tid == 0) { for (int i = 0; i < 16; ++i) ptx::mbar_init(&bar[i], 1); ptx::fence_mbar_init(); }
   if (warp == 0) ptx::tmem_alloc(&slot, 128);
   ptx::fence_proxy_async_smem();
@@ -45,7 +47,22 @@ __global__ void bench(int variant, int tiles, unsigned long long* out) {
         const uint64_t dBl = dB + (4096 >> 4);
         for (int j = 0; j < 4; ++j) {
           const uint64_t kj = uint64_t(j) * 2u;
-          if (variant == 3) {
+          if (variant == 4) {  // separate accumulators for the two shapes
+            ptx::mma_tf32(tm, dA + shift + kj, dB + kj, idesc64, 1u);
+            ptx::mma_tf32(tm + 64, dAl + shift + kj, dB + kj, idesc32, 1u);
+            nmma += 2;
+          } else if (variant == 5) {  // uniform N=64 shape, same accumulator (A_lo x [B_hi|B_lo])
+            ptx::mma_tf32(tm, dA + shift + kj, dB + kj, idesc64, 1u);
+            ptx::mma_tf32(tm, dAl + shift + kj, dB + kj, idesc64, 1u);
+            nmma += 2;
+          } else if (variant == 6) {  // uniform N=64, two accumulators
+            ptx::mma_tf32(tm, dA + shift + kj, dB + kj, idesc64, 1u);
+            ptx::mma_tf32(tm + 64, dAl + shift + kj, dB + kj, idesc64, 1u);
+            nmma += 2;
+          } else if (variant == 7) {  // only A_hi x [B_hi|B_lo]: one N=64 MMA per k8
+            ptx::mma_tf32(tm, dA + shift + kj, dB + kj, idesc64, 1u);
+            nmma += 1;
+          } else if (variant == 3) {
             ptx::mma_tf32(tm, dAl + shift + kj, dB + kj, idesc32, 1u);
             ptx::mma_tf32(tm, dA + shift + kj, dBl + kj, idesc32, 1u);
             ptx::mma_tf32(tm, dA + shift + kj, dB + kj, idesc32, 1u);
@@ -70,13 +87,14 @@ __global__ void bench(int variant, int tiles, unsigned long long* out) {
   if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc(tm, 128); }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int fill = argc > 1 ? atoi(argv[1]) : 0;
   unsigned long long* d;
   cudaMalloc(&d, 16);
   const int smem = 170 * 1024;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int v = 0; v < 4; ++v) {
-    bench<<<148, 128, smem>>>(v, 4, d);
+  for (int v = 0; v < 8; ++v) {
+    bench<<<148, 128, smem>>>(v, 4, d, fill);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("v%d err %s\n", v, cudaGetErrorString(e)); return 1; }
     unsigned long long h[2];
