@@ -52,7 +52,7 @@ __host__ __device__ constexpr int stages_for() {
 template <int BN, bool SPLIT>
 __host__ __device__ constexpr int smem_bytes() {
   return 1024 /*align slack*/ + stages_for<BN, SPLIT>() * (BM * BK * 4 + BN * BK * 4) * (SPLIT ? 2 : 1) +
-         (2 * stages_for<BN, SPLIT>() + 1) * 8 + 16;
+         (3 * stages_for<BN, SPLIT>() + 1) * 8 + 16;
 }
 
 // Byte offset of 16-byte chunk `kc` (0..7) of row `r` in a K-major SWIZZLE_128B tile.
@@ -188,6 +188,24 @@ struct is_tma { static constexpr bool value = false; };
 template <>
 struct is_tma<TmaView> { static constexpr bool value = true; };
 
+// 3xTF32 with a TMA-fed operand: TMA lands the raw fp32 tile (128B-swizzled,
+// K-major) in the hi buffer; the producer warps then round it to tf32 in place
+// and write the residual into the lo buffer at the same offset (the two layouts
+// are identical, so the split is elementwise).  `rows` x 32 fp32 per tile.
+template <int ROWS>
+__device__ __forceinline__ void split_in_place(uint32_t hi, uint32_t lo, int t) {
+  constexpr int CHUNKS = ROWS * 8;  // 16-byte chunks
+#pragma unroll
+  for (int i = t; i < CHUNKS; i += kProducerThreads) {
+    const uint32_t off = uint32_t(i) * 16u;
+    float4 x;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                 : "r"(hi + off));
+    store4<true>(hi, lo, off, x);
+  }
+}
+
 template <int BN, bool SPLIT, class VA, class VB, class EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -195,7 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
   constexpr bool kTmaA = is_tma<VA>::value;
   constexpr bool kTmaB = is_tma<VB>::value;
-  static_assert(!(SPLIT && (kTmaA || kTmaB)), "3xTF32 splits operands in the gather producers");
+  // 3xTF32 + TMA: TMA lands raw tiles (landed[]), the producers split them
+  constexpr bool kSplitTma = SPLIT && (kTmaA || kTmaB);
   constexpr int STAGES = stages_for<BN, SPLIT>();
   constexpr uint32_t A_BYTES = BM * BK * 4;
   constexpr uint32_t B_BYTES = BN * BK * 4;
@@ -212,7 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* accum = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* landed = accum + 1;  // kSplitTma only: STAGES barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(landed + STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -229,6 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&empty[s], 1);     // tcgen05.commit
     }
     ptx::mbar_init(accum, 1);
+    if constexpr (kSplitTma)
+      for (int st = 0; st < STAGES; ++st) ptx::mbar_init(&landed[st], 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -247,7 +269,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kt = 0; kt < nkt; ++kt) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         constexpr uint32_t bytes = (kTmaA ? A_BYTES : 0) + (kTmaB ? B_BYTES : 0);
-        if constexpr (bytes > 0) {
+        if constexpr (kSplitTma) {
+          // raw tiles -> landed[]; the producers split them and complete full[]
+          ptx::mbar_arrive_expect_tx(&landed[stage], bytes);
+          const int kc = (kt_begin + kt) * BK;
+          if constexpr (kTmaA) ptx::tma_load_2d(a_hi(stage), &tmA, &landed[stage], kc, m0);
+          if constexpr (kTmaB) ptx::tma_load_2d(b_hi(stage), &tmB, &landed[stage], kc, n0);
+          ptx::mbar_arrive(&full[stage]);
+        } else if constexpr (bytes > 0) {
           ptx::mbar_arrive_expect_tx(&full[stage], bytes);
           const int kc = (kt_begin + kt) * BK;
           if constexpr (kTmaA) ptx::tma_load_2d(a_hi(stage), &tmA, &full[stage], kc, m0);
@@ -301,6 +330,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         gather_slab<BM, SPLIT>(va, ptx::smem_u32(a_hi(stage)), ptx::smem_u32(a_lo(stage)), m0, kc, t);
       if constexpr (!kTmaB)
         gather_slab<BN, SPLIT>(vb, ptx::smem_u32(b_hi(stage)), ptx::smem_u32(b_lo(stage)), n0, kc, t);
+      if constexpr (kSplitTma) {
+        ptx::mbar_wait(&landed[stage], phase);
+        if constexpr (kTmaA) split_in_place<BM>(ptx::smem_u32(a_hi(stage)), ptx::smem_u32(a_lo(stage)), t);
+        if constexpr (kTmaB) split_in_place<BN>(ptx::smem_u32(b_hi(stage)), ptx::smem_u32(b_lo(stage)), t);
+      }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&full[stage]);
@@ -317,10 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), r);
       ptx::tmem_ld_wait();
       if (m < M) {
+        if constexpr (std::is_same_v<EPI, StoreEpi<float>>) {
+          epi.store16(m, n0 + c, r, N);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int n = n0 + c + j;
-          if (n < N) epi.store(m, n, __uint_as_float(r[j]), split);
+          for (int j = 0; j < 16; ++j) {
+            const int n = n0 + c + j;
+            if (n < N) epi.store(m, n, __uint_as_float(r[j]), split);
+          }
         }
       }
     }

@@ -94,6 +94,11 @@ struct ConvDescSlot {
   // [0] X' forward, [1] W', [2] X' backward-filter, [3] dW', [4] dX'
   std::shared_ptr<ConvDescSlot> s2d;
   std::shared_ptr<DevAlloc> s2d_buf[5];
+  // column fold of a small-channel stride-1 convolution (S filter columns folded
+  // into C*S >= 16 channels, R x 1 kernel): descriptor and grow-only buffers
+  // [0] X' forward, [1] W', [2] X' backward-filter, [3] dW'
+  std::shared_ptr<ConvDescSlot> cf;
+  std::shared_ptr<DevAlloc> cf_buf[4];
 };
 
 struct PoolDescSlot {

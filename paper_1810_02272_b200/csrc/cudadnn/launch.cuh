@@ -57,8 +57,28 @@ __global__ void __launch_bounds__(256) reduce_splits_kernel(const T* __restrict_
   }
 }
 
+// Few splits (<= 8): block = 32 m x 8 n, each thread adds its splits in order.
+template <typename T, class EPI>
+__global__ void __launch_bounds__(256) reduce_few_splits_kernel(const T* __restrict__ ws, int M, int N, int splits,
+                                                                EPI epi) {
+  const int m = blockIdx.x * 32 + (threadIdx.x & 31), n = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (m >= M || n >= N) return;
+  const T* p = ws + int64_t(n) * M + m;
+  const int64_t zs = int64_t(N) * M;
+  T s = p[0];
+  for (int z = 1; z < splits; ++z) s += p[z * zs];
+  epi.store(m, n, s, 0);
+}
+
 template <typename T, class EPI>
 void launch_reduce(Ctx* c, cudaStream_t st, const T* ws, int M, int N, int splits, const EPI& epi) {
+  if (splits <= 8) {
+    dim3 grid((M + 31) / 32, (N + 7) / 8);
+    reduce_few_splits_kernel<T, EPI><<<grid, 256, 0, st>>>(ws, M, N, splits, epi);
+    check_launch("reduce_few_splits_kernel");
+    count_launch(c);
+    return;
+  }
   dim3 grid((M + 31) / 32, N);
   reduce_splits_kernel<T, EPI><<<grid, 256, 0, st>>>(ws, M, N, splits, epi);
   check_launch("reduce_splits_kernel");
@@ -106,7 +126,7 @@ void run_tc_bn(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M
 }
 
 // Picks the tile width and the numerics mode: 3xTF32 (context default) or
-// plain TF32; TMA operands exist only in plain TF32 mode.
+// plain TF32.
 template <class VA, class VB, class EPI>
 void run_tc(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
             const VA& va, const VB& vb, const EPI& epi, const TmaReq& ra = {}, const TmaReq& rb = {}) {
@@ -119,19 +139,16 @@ void run_tc(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, i
       default: run_tc_bn<128, S>(c, st, ws, pl, M, N, K, va, vb, epi, ra, rb); break;
     }
   };
-  if constexpr (any_tma) {
-    go(std::false_type{});
-  } else {
-    if (c->math_mode == CDNN_MATH_TF32X3) go(std::true_type{});
-    else go(std::false_type{});
-  }
+  (void)any_tma;  // TMA operands are split in the kernel in 3xTF32 mode
+  if (c->math_mode == CDNN_MATH_TF32X3) go(std::true_type{});
+  else go(std::false_type{});
 }
 
-// Dense fp32 operand -> TMA when it is K-contiguous and aligned and the
-// context runs plain TF32; the gather producers otherwise.
+// Dense fp32 operand -> TMA when it is K-contiguous and aligned (3xTF32: the
+// producers split the landed tile); the gather producers otherwise.
 template <class F>
 void with_operand(Ctx* c, const DenseView<float>& v, int box_rows, TmaReq& req, F&& f) {
-  if (c->math_mode == CDNN_MATH_TF32 && !v.mcontig && v.sk == 1 &&
+  if (!v.mcontig && v.sk == 1 &&
       tma_eligible(v.p, v.rows, v.K, v.sr, box_rows)) {
     req = TmaReq{v.p, v.rows, v.K, v.sr};
     f(TmaView{});

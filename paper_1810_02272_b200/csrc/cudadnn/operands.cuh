@@ -320,6 +320,25 @@ struct StoreEpi {
     if (relu) v = v > T(0) ? v : T(0);
     *o = v;
   }
+  // 16 consecutive n of one m (a tcgen05.ld row): every read of the old C is
+  // issued before the first store (the compiler cannot reorder loads past
+  // possibly-aliasing stores, which serialised one memory latency per element).
+  __device__ __forceinline__ void store16(int m, int n0, const uint32_t (&r)[16], int N) const {
+    T* o = out + int64_t(m) * sm + int64_t(n0) * sn;
+    T prev[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) prev[j] = (beta != T(0) && n0 + j < N) ? o[int64_t(j) * sn] : T(0);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (n0 + j < N) {
+        T v = alpha * T(__uint_as_float(r[j]));
+        if (beta != T(0)) v += beta * prev[j];
+        if (bias) v += bias[bias_on_m ? m : n0 + j];
+        if (relu) v = v > T(0) ? v : T(0);
+        o[int64_t(j) * sn] = v;
+      }
+    }
+  }
 };
 
 // split-K partials: ws[split][n][m] (m contiguous so lanes coalesce)

@@ -29,6 +29,14 @@ bool conv_tma_enabled() {
   return on;
 }
 
+bool cf_route_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CDNN_CONV_CF");
+    return !(v && std::string(v) == "0");
+  }();
+  return on;
+}
+
 bool conv_tap_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("CDNN_CONV_TAP");
@@ -309,7 +317,10 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   const int items = a.cblocks * a.ggroups * a.coblocks;
   a.nchunks = (a.Mv + tcwtap::KC - 1) / tcwtap::KC;
   const int target = (smem <= 113 * 1024 ? 2 : 1) * kNumSMs;
-  int splits = std::max(1, std::min(a.nchunks, (target + items - 1) / items));
+  // whole waves: the largest split count whose grid still fits the resident slots
+  // (a 168-CTA grid on 148 one-CTA SMs runs as two waves, the second one 20 CTAs wide)
+  int splits = items >= target ? 1 : target / items;
+  splits = std::max(1, std::min(a.nchunks, splits));
   a.chunks_per_split = (a.nchunks + splits - 1) / splits;
   a.splits = (a.nchunks + a.chunks_per_split - 1) / a.chunks_per_split;
   a.want_bias = db != nullptr;
@@ -587,6 +598,117 @@ bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float
   return conv_tap(c, e, false, xs, wsb, bias, y, stream, relu);
 }
 
+// ---- column fold: a stride-1 convolution over C < 16 channels (CIFAR / LeNet conv1)
+// == an R x 1 convolution over C' = max(16, C*S) channels with the S filter columns
+// folded into the channels (zero channels past C*S):
+//   X'[n][s*C + c][y][q] = x[n][c][y][q + s - pw]          (0 outside), H' = H, W' = Q
+//   W'[co][s*C + c][r][0] = W[co][c][r][s]
+// Same output P x Q, row padding kept (ph), no column padding.  The 16+ channel
+// operand runs on the tap-shift kernels at full 8-wide K steps (and the backward
+// filter on conv_wtap, which needs >= 16 channels), instead of staging 3-channel
+// rows with scalar gathers.
+bool cf_eligible(const ConvGeom& g) {
+  return conv_tap_enabled() && g.sh == 1 && g.sw == 1 && g.dh == 1 && g.dw == 1 && g.group == 1 && g.C < 16 &&
+         g.C * g.S <= 32 && g.S > 1 && g.pw < g.S;
+}
+
+ConvDescSlot& cf_desc(const ConvDescSlot& dconst) {
+  ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
+  if (!d.cf) {
+    const ConvGeom& g = d.geom;
+    auto child = std::make_shared<ConvDescSlot>();
+    ConvGeom& h = child->geom;
+    h = g;
+    h.C = std::max(16, g.C * g.S);
+    h.W = g.Q;
+    h.S = 1;
+    h.pw = 0;
+    h.Cg = h.C; h.Cog = h.Co;
+    h.div_PQ = FastDiv(uint32_t(h.P * h.Q)); h.div_Q = FastDiv(uint32_t(h.Q));
+    h.div_HW = FastDiv(uint32_t(h.H * h.W)); h.div_W = FastDiv(uint32_t(h.W));
+    child->P = h.P; child->Q = h.Q;
+    child->Kc = h.Cg * h.R * h.S;
+    child->Kd = h.Cog * h.R * h.S;
+    d.cf = child;
+  }
+  return *d.cf;
+}
+
+float* cf_buffer(Ctx* c, const ConvDescSlot& dconst, int which, size_t elems) {
+  ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
+  auto& b = d.cf_buf[which];
+  if (!b || b->bytes < elems * 4) b = device_alloc_shared(elems * 4, c->device);
+  return static_cast<float*>(b->ptr);
+}
+
+// One thread per X' element; consecutive threads walk q (coalesced both ways).
+__global__ void cf_input_kernel(const float* __restrict__ x, float* __restrict__ xf, ConvGeom g, ConvGeom h) {
+  const int64_t total = int64_t(h.N) * h.C * h.H * h.W;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int q = int(i % h.W);
+    const int y = int((i / h.W) % h.H);
+    const int cc = int((i / (int64_t(h.W) * h.H)) % h.C);
+    const int n = int(i / (int64_t(h.W) * h.H * h.C));
+    const int s = cc / g.C, c = cc - s * g.C;
+    const int xx = q + s - g.pw;
+    xf[i] = (s < g.S && xx >= 0 && xx < g.W) ? __ldg(x + ((int64_t(n) * g.C + c) * g.H + y) * g.W + xx) : 0.f;
+  }
+}
+
+__global__ void cf_weight_kernel(const float* __restrict__ w, float* __restrict__ wf, ConvGeom g, ConvGeom h) {
+  const int total = h.Co * h.C * h.R;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int r = i % h.R, cc = (i / h.R) % h.C, co = i / (h.R * h.C);
+    const int s = cc / g.C, c = cc - s * g.C;
+    wf[i] = s < g.S ? w[((co * g.C + c) * g.R + r) * g.S + s] : 0.f;
+  }
+}
+
+// dW[co][c][r][s] += dW'[co][s*C + c][r]
+__global__ void cf_dweight_kernel(const float* __restrict__ dwf, float* __restrict__ dw, ConvGeom g, ConvGeom h) {
+  const int total = g.Co * g.C * g.R * g.S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int s = i % g.S, r = (i / g.S) % g.R, c = (i / (g.S * g.R)) % g.C, co = i / (g.S * g.R * g.C);
+    dw[i] += dwf[(co * h.C + s * g.C + c) * h.R + r];
+  }
+}
+
+bool conv_forward_cf(Ctx* c, const ConvDescSlot& d, const float* x, const float* w, const float* bias, float* y,
+                     cdnn_handle stream, bool relu) {
+  if (!cf_eligible(d.geom)) return false;
+  ConvDescSlot& e = cf_desc(d);
+  const ConvGeom &g = d.geom, &h = e.geom;
+  cudaStream_t st = stream_of(c, stream);
+  float* xf = cf_buffer(c, d, 0, size_t(h.N) * h.C * h.H * h.W);
+  float* wf = cf_buffer(c, d, 1, size_t(h.Co) * h.C * h.R);
+  cf_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xf, g, h);
+  cf_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R, 256), 256, 0, st>>>(w, wf, g, h);
+  check_launch("column fold");
+  count_launch(c, 2);
+  return conv_tap(c, e, false, xf, wf, bias, y, stream, relu);
+}
+
+bool conv_wgrad_cf(Ctx* c, const ConvDescSlot& d, const float* x, const float* dy, float* dw, float* db,
+                   cdnn_handle stream) {
+  if (!cf_eligible(d.geom)) return false;
+  ConvDescSlot& e = cf_desc(d);
+  const ConvGeom &g = d.geom, &h = e.geom;
+  cudaStream_t st = stream_of(c, stream);
+  float* xf = cf_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
+  float* dwf = dw ? cf_buffer(c, d, 3, size_t(h.Co) * h.C * h.R) : nullptr;
+  cf_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xf, g, h);
+  check_launch("column fold");
+  count_launch(c);
+  if (dwf) CDNN_CUDA(cudaMemsetAsync(dwf, 0, size_t(h.Co) * h.C * h.R * 4, st));
+  if (!conv_wgrad_tap(c, e, xf, dy, dwf, db, stream)) return false;
+  if (dw) {
+    cf_dweight_kernel<<<grid_for(int64_t(g.Co) * g.C * g.R * g.S, 256), 256, 0, st>>>(dwf, dw, g, h);
+    check_launch("cf_dweight");
+    count_launch(c);
+  }
+  return true;
+}
+
 template <typename T>
 void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const BufferSlot& Wt,
                     const BufferSlot* B, BufferSlot& Y, cdnn_handle stream, bool relu) {
@@ -598,6 +720,11 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
     if (conv_forward_s2d(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
                          B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream,
                          relu))
+      return;
+    if (cf_route_enabled() &&
+        conv_forward_cf(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
+                        B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream,
+                        relu))
       return;
     if (conv_tap(c, d, false, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
                  B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream, relu))
@@ -777,6 +904,10 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
     float* db = DB ? reinterpret_cast<float*>(DB->dev) : nullptr;
     const float* x = reinterpret_cast<const float*>(X.dev);
     if (g.sh == 1 && g.sw == 1) {
+      // (the column fold is slower than the gather engine for the backward filter; forward only)
+      if (cf_route_enabled() && std::getenv("CDNN_CF_WGRAD") &&
+          conv_wgrad_cf(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream))
+        return;
       if (conv_wgrad_tap(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) return;
     } else if (conv_wgrad_s2d(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) {
       return;

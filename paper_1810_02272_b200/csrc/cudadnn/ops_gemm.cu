@@ -24,8 +24,15 @@ GemmPlan plan_tc(int M, int N, int K) {
   const int kt = (K + tc::BK - 1) / tc::BK;
   int splits = 1;
   if (tiles < kNumSMs && kt >= 8) {
-    splits = std::min(kt / 4, (2 * kNumSMs + tiles - 1) / tiles);
-    splits = std::max(splits, 1);
+    // one CTA per SM (shared memory): pick the split count with the best
+    // whole-wave occupancy up to ~2 waves, fewest splits on ties
+    const int smax = std::max(1, std::min(kt / 4, (2 * kNumSMs + tiles - 1) / tiles));
+    double best = 0.0;
+    for (int sp = 1; sp <= smax; ++sp) {
+      const int ctas = tiles * sp, waves = (ctas + kNumSMs - 1) / kNumSMs;
+      const double eff = double(ctas) / (double(waves) * kNumSMs);
+      if (eff > best + 1e-9) { best = eff; splits = sp; }
+    }
   }
   p.kt_per_split = (kt + splits - 1) / splits;
   p.splits = (kt + p.kt_per_split - 1) / p.kt_per_split;

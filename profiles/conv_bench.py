@@ -80,6 +80,31 @@ def main():
                               "tflops": round(flops / ms / 1e9, 3), "gflop": round(flops / 1e9, 4)}), flush=True)
         for hnd in (x, wt, b, y, dy, dx, dw, db):
             ctx.free(hnd)
+    # InnerProduct layers (forward, backward = dW + db + dX) of AlexNet / CIFAR-quick
+    IP = {"alexnet.fc6": (256, 9216, 4096), "alexnet.fc7": (256, 4096, 4096), "alexnet.fc8": (256, 4096, 1000),
+          "cq.ip1": (100, 1024, 64)}
+    for name, (rows, k, o) in IP.items():
+        if args.only and args.only not in name:
+            continue
+        x = ctx.upload(rng.uniform(-1, 1, rows * k).astype(np.float32))
+        wt = ctx.upload(rng.uniform(-1, 1, o * k).astype(np.float32))
+        b = ctx.upload(np.zeros(o, np.float32))
+        y = ctx.alloc(rows * o, cd.F32)
+        dy = ctx.upload(rng.uniform(-1, 1, rows * o).astype(np.float32))
+        dx = ctx.alloc(rows * k, cd.F32)
+        dw = ctx.alloc(o * k, cd.F32)
+        db = ctx.alloc(o, cd.F32)
+        flops = 2.0 * rows * k * o
+        ops = {
+            "fwd": (lambda: ctx.call("cdnn_ip_forward", x, wt, b, y, rows, k, o, 0, 0), flops),
+            "bwd": (lambda: ctx.call("cdnn_ip_backward", x, wt, dy, dw, db, dx, rows, k, o, 0), 2 * flops),
+        }
+        for op, (fn, fl) in ops.items():
+            ms = timeit(ctx, fn, args.reps)
+            print(json.dumps({"op": f"{name}.{op}", "math": args.math, "ms": round(ms, 5),
+                              "tflops": round(fl / ms / 1e9, 3), "gflop": round(fl / 1e9, 4)}), flush=True)
+        for hnd in (x, wt, b, y, dy, dx, dw, db):
+            ctx.free(hnd)
     ctx.close()
 
 

@@ -319,3 +319,28 @@ def test_conv_forward_fused_relu(ctx, dtype, case):
     out = ctx.read(hy)
     assert rel_l2(out, y) <= TOL[dtype]
     assert (out >= 0).all()
+
+
+@pytest.mark.parametrize("rows,k,o", [(256, 2304, 1024), (200, 1000, 520), (256, 4096, 1000)])
+def test_ip_large_tensor_core(ctx, math, rows, k, o):
+    """InnerProduct forward / backward at AlexNet-like sizes (tcgen05 engine, TMA-fed
+    operands split into tf32 hi/lo in the kernel): 3xTF32 must reach fp32 accuracy."""
+    rng = np.random.default_rng(rows + k + o)
+    X = rng.uniform(-1, 1, (rows, k)).astype(np.float32)
+    W = rng.uniform(-1, 1, (o, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, o).astype(np.float32)
+    dY = rng.uniform(-1, 1, (rows, o)).astype(np.float32)
+    dW0 = rng.uniform(-1, 1, (o, k)).astype(np.float32)
+    hx, hw, hb, hdy = ctx.upload(X), ctx.upload(W), ctx.upload(b), ctx.upload(dY)
+    hy, hdx = ctx.alloc(rows * o, cd.F32), ctx.alloc(rows * k, cd.F32)
+    hdw, hdb = ctx.upload(dW0), ctx.alloc(o, cd.F32)
+    ctx.call("cdnn_ip_forward", hx, hw, hb, hy, rows, k, o, 0, 0)
+    ctx.call("cdnn_ip_backward", hx, hw, hdy, hdw, hdb, hdx, rows, k, o, 0)
+    Xd, Wd, dYd = X.astype(np.float64), W.astype(np.float64), dY.astype(np.float64)
+    tol = 1e-5 if math == "tf32x3" else 2e-3  # fp32 accumulation over K <= 4096 terms
+    assert rel_l2(ctx.read(hy).reshape(rows, o), Xd @ Wd.T + b) <= tol
+    assert rel_l2(ctx.read(hdx).reshape(rows, k), dYd @ Wd) <= tol
+    assert rel_l2(ctx.read(hdw).reshape(o, k) - dW0, dYd.T @ Xd) <= tol * 4
+    assert rel_l2(ctx.read(hdb), dYd.sum(0)) <= 1e-6
+    for h in (hx, hw, hb, hdy, hy, hdx, hdw, hdb):
+        ctx.free(h)
