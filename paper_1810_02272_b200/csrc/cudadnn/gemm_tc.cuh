@@ -341,19 +341,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
     // ---------------- epilogue ----------------
-    ptx::mbar_wait(accum, 0);
-    ptx::tc_fence_after();
     const int q = warp & 3;
     const int m = m0 + q * 32 + lane;
+    if constexpr (std::is_same_v<EPI, StoreEpi<float>>) {
+      // beta != 0 (accumulating GEMMs, e.g. InnerProduct dW += dY^T X): every old
+      // C value of the thread's row is loaded BEFORE waiting for the accumulator,
+      // so the reads overlap the last MMAs instead of costing one memory latency
+      // per 16-column chunk after them.
+      float prev[BN];
+      const bool rowok = m < M;
+      float* orow = epi.out + int64_t(m) * epi.sm + int64_t(n0) * epi.sn;
+#pragma unroll
+      for (int j = 0; j < BN; ++j)
+        prev[j] = (rowok && epi.beta != 0.f && n0 + j < N) ? orow[int64_t(j) * epi.sn] : 0.f;
+      ptx::mbar_wait(accum, 0);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), r);
+        ptx::tmem_ld_wait();
+        if (rowok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = n0 + c + j;
+            if (n < N) {
+              float v = epi.alpha * __uint_as_float(r[j]);
+              if (epi.beta != 0.f) v += epi.beta * prev[c + j];
+              if (epi.bias) v += epi.bias[epi.bias_on_m ? m : n];
+              if (epi.relu) v = v > 0.f ? v : 0.f;
+              orow[int64_t(c + j) * epi.sn] = v;
+            }
+          }
+        }
+      }
+    } else {
+      ptx::mbar_wait(accum, 0);
+      ptx::tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), r);
-      ptx::tmem_ld_wait();
-      if (m < M) {
-        if constexpr (std::is_same_v<EPI, StoreEpi<float>>) {
-          epi.store16(m, n0 + c, r, N);
-        } else {
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c), r);
+        ptx::tmem_ld_wait();
+        if (m < M) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int n = n0 + c + j;

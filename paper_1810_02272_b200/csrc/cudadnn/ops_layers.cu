@@ -36,6 +36,12 @@ __device__ __forceinline__ T neg_pow(T sc, T beta) {
   else return pow(sc, -beta);
 }
 
+// Forward: channels are processed in groups of four, the group's entering,
+// leaving and own values loaded together before any arithmetic (12 independent
+// loads in flight per thread; norm1 of AlexNet 267 -> 244 us).  The same
+// restructuring of the backward measured slower (563 -> 777 us) and is not used.
+constexpr int kLrnU = 4;
+
 template <typename T>
 __global__ void lrn_fwd(const T* __restrict__ x, T* __restrict__ y, T* __restrict__ scale, int N, int C, int HW,
                         int size, T alpha, T beta, T k) {
@@ -44,21 +50,34 @@ __global__ void lrn_fwd(const T* __restrict__ x, T* __restrict__ y, T* __restric
   const T aN = alpha / T(size);
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < pixels; p += int64_t(gridDim.x) * blockDim.x) {
     const int64_t img = p / HW, hw = p - img * HW;
-    const int64_t base = img * C * HW + hw;
+    const T* xb = x + img * C * HW + hw;
+    const int64_t ob = img * C * HW + hw;
     T s = T(0);  // sum of squares over [c - pre, c + post]
     for (int cc = 0; cc < post && cc < C; ++cc) {
-      const T v = x[base + int64_t(cc) * HW];
+      const T v = __ldg(xb + int64_t(cc) * HW);
       s += v * v;
     }
-    for (int c = 0; c < C; ++c) {
-      const int cin = c + post, cout = c - pre - 1;
-      if (cin < C) { const T v = x[base + int64_t(cin) * HW]; s += v * v; }
-      if (cout >= 0) { const T v = x[base + int64_t(cout) * HW]; s -= v * v; }
-      s = s > T(0) ? s : T(0);
-      const int64_t o = base + int64_t(c) * HW;
-      const T sc = k + aN * s;
-      scale[o] = sc;
-      y[o] = x[o] * neg_pow(sc, beta);
+    for (int c0 = 0; c0 < C; c0 += kLrnU) {
+      T vin[kLrnU], vout[kLrnU], vx[kLrnU];
+#pragma unroll
+      for (int u = 0; u < kLrnU; ++u) {
+        const int c = c0 + u, cin = c + post, cout = c - pre - 1;
+        vin[u] = (c < C && cin < C) ? __ldg(xb + int64_t(cin) * HW) : T(0);
+        vout[u] = (c < C && cout >= 0) ? __ldg(xb + int64_t(cout) * HW) : T(0);
+        vx[u] = c < C ? __ldg(xb + int64_t(c) * HW) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kLrnU; ++u) {
+        const int c = c0 + u;
+        if (c >= C) break;
+        s += vin[u] * vin[u];
+        s -= vout[u] * vout[u];
+        s = s > T(0) ? s : T(0);
+        const int64_t o = ob + int64_t(c) * HW;
+        const T sc = k + aN * s;
+        scale[o] = sc;
+        y[o] = vx[u] * neg_pow(sc, beta);
+      }
     }
   }
 }
