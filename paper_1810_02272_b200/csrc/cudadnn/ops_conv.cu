@@ -641,17 +641,25 @@ float* cf_buffer(Ctx* c, const ConvDescSlot& dconst, int which, size_t elems) {
   return static_cast<float*>(b->ptr);
 }
 
-// One thread per X' element; consecutive threads walk q (coalesced both ways).
+// One warp-strided sweep per X' row (n, s*C + c, y): lanes walk q, so the loads
+// of a row are one contiguous (shifted) run of the input row and the stores are
+// coalesced; 32-bit index math (X' < 2^31 elements).
 __global__ void cf_input_kernel(const float* __restrict__ x, float* __restrict__ xf, ConvGeom g, ConvGeom h) {
-  const int64_t total = int64_t(h.N) * h.C * h.H * h.W;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int q = int(i % h.W);
-    const int y = int((i / h.W) % h.H);
-    const int cc = int((i / (int64_t(h.W) * h.H)) % h.C);
-    const int n = int(i / (int64_t(h.W) * h.H * h.C));
+  const int rows = h.N * h.C * h.H;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const int y = row % h.H;
+    const int cc = (row / h.H) % h.C;
+    const int n = row / (h.H * h.C);
     const int s = cc / g.C, c = cc - s * g.C;
-    const int xx = q + s - g.pw;
-    xf[i] = (s < g.S && xx >= 0 && xx < g.W) ? __ldg(x + ((int64_t(n) * g.C + c) * g.H + y) * g.W + xx) : 0.f;
+    float* out = xf + size_t(row) * h.W;
+    const bool live = s < g.S;
+    const float* in = x + (size_t(n) * g.C + c) * g.H * g.W + size_t(y) * g.W;
+    for (int q = lane; q < h.W; q += 32) {
+      const int xx = q + s - g.pw;
+      out[q] = (live && xx >= 0 && xx < g.W) ? __ldg(in + xx) : 0.f;
+    }
   }
 }
 
@@ -681,7 +689,7 @@ bool conv_forward_cf(Ctx* c, const ConvDescSlot& d, const float* x, const float*
   cudaStream_t st = stream_of(c, stream);
   float* xf = cf_buffer(c, d, 0, size_t(h.N) * h.C * h.H * h.W);
   float* wf = cf_buffer(c, d, 1, size_t(h.Co) * h.C * h.R);
-  cf_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xf, g, h);
+  cf_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32, 256), 256, 0, st>>>(x, xf, g, h);
   cf_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R, 256), 256, 0, st>>>(w, wf, g, h);
   check_launch("column fold");
   count_launch(c, 2);
@@ -696,7 +704,7 @@ bool conv_wgrad_cf(Ctx* c, const ConvDescSlot& d, const float* x, const float* d
   cudaStream_t st = stream_of(c, stream);
   float* xf = cf_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
   float* dwf = dw ? cf_buffer(c, d, 3, size_t(h.Co) * h.C * h.R) : nullptr;
-  cf_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xf, g, h);
+  cf_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32, 256), 256, 0, st>>>(x, xf, g, h);
   check_launch("column fold");
   count_launch(c);
   if (dwf) CDNN_CUDA(cudaMemsetAsync(dwf, 0, size_t(h.Co) * h.C * h.R * 4, st));
