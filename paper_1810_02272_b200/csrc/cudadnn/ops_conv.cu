@@ -492,17 +492,26 @@ float* s2d_buffer(Ctx* c, const ConvDescSlot& dconst, int which, size_t elems) {
   return static_cast<float*>(b->ptr);
 }
 
+// One warp-strided sweep per X' row (n, cc, h'): lanes walk w' (stores coalesced,
+// loads a stride-s run of one input row); 32-bit index math (X' < 2^31 elements).
 __global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict__ xs, ConvGeom g, ConvGeom h) {
   const int s = g.sh;
-  const int64_t total = int64_t(h.N) * h.C * h.H * h.W;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int w2 = int(i % h.W);
-    const int h2 = int((i / h.W) % h.H);
-    const int cc = int((i / (int64_t(h.W) * h.H)) % h.C);
-    const int n = int(i / (int64_t(h.W) * h.H * h.C));
+  const int rows = h.N * h.C * h.H;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const int h2 = row % h.H;
+    const int cc = (row / h.H) % h.C;
+    const int n = row / (h.H * h.C);
     const int c = cc % g.C, ph = cc / g.C, dy = ph / s, dx = ph % s;
-    const int y = s * h2 + dy - g.ph, xx = s * w2 + dx - g.pw;
-    xs[i] = (y >= 0 && y < g.H && xx >= 0 && xx < g.W) ? x[((int64_t(n) * g.C + c) * g.H + y) * g.W + xx] : 0.f;
+    const int y = s * h2 + dy - g.ph;
+    float* out = xs + size_t(row) * h.W;
+    const bool yok = y >= 0 && y < g.H;
+    const float* in = x + (size_t(n) * g.C + c) * g.H * g.W + size_t(yok ? y : 0) * g.W;
+    for (int w2 = lane; w2 < h.W; w2 += 32) {
+      const int xx = s * w2 + dx - g.pw;
+      out[w2] = (yok && xx >= 0 && xx < g.W) ? __ldg(in + xx) : 0.f;
+    }
   }
 }
 
@@ -553,7 +562,7 @@ bool conv_wgrad_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   cudaStream_t st = stream_of(c, stream);
   float* xs = s2d_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
   float* dws = s2d_buffer(c, d, 3, size_t(h.Co) * h.C * h.R * h.S);
-  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xs, g, h);
+  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32, 256), 256, 0, st>>>(x, xs, g, h);
   CDNN_CUDA(cudaMemsetAsync(dws, 0, size_t(h.Co) * h.C * h.R * h.S * 4, st));
   check_launch("s2d");
   count_launch(c);
@@ -591,7 +600,7 @@ bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float
   cudaStream_t st = stream_of(c, stream);
   float* xs = s2d_buffer(c, d, 0, size_t(h.N) * h.C * h.H * h.W);
   float* wsb = s2d_buffer(c, d, 1, size_t(h.Co) * h.C * h.R * h.S);
-  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * h.W, 256), 256, 0, st>>>(x, xs, g, h);
+  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32, 256), 256, 0, st>>>(x, xs, g, h);
   s2d_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R * h.S, 256), 256, 0, st>>>(w, wsb, g, h);
   check_launch("s2d");
   count_launch(c, 2);
@@ -805,14 +814,18 @@ __global__ void __launch_bounds__(256) conv_dgrad_direct_kernel(const T* __restr
 // then the stride-1 ones on `up` (sh*sw x the MACs, all on the tensor cores).
 __global__ void zero_insert_kernel(const float* __restrict__ dy, float* __restrict__ up, int64_t planes, int P, int Q,
                                    int P1, int Q1, int sh, int sw) {
-  const int64_t total = planes * P1 * Q1;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int u = int(i % Q1);
-    const int t = int((i / Q1) % P1);
-    const int64_t pl = i / (int64_t(Q1) * P1);
-    float v = 0.f;
-    if (t % sh == 0 && u % sw == 0 && t / sh < P && u / sw < Q) v = dy[(pl * P + t / sh) * Q + u / sw];
-    up[i] = v;
+  // one warp-strided sweep per output row (plane, t): 32-bit math, coalesced stores
+  const int64_t rows = planes * P1;
+  const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; row < rows; row += warps) {
+    const int t = int(row % P1);
+    const int64_t pl = row / P1;
+    float* out = up + row * Q1;
+    const bool trow = t % sh == 0 && t / sh < P;
+    const float* in = dy + (pl * P + (trow ? t / sh : 0)) * Q;
+    for (int u = lane; u < Q1; u += 32)
+      out[u] = (trow && u % sw == 0 && u / sw < Q) ? __ldg(in + u / sw) : 0.f;
   }
 }
 
@@ -829,7 +842,7 @@ bool with_zero_inserted(Ctx* c, const ConvDescSlot& dconst, const float* dy, cdn
   if (!buf || buf->bytes < elems * 4) buf = device_alloc_shared(elems * 4, c->device);
   float* up = static_cast<float*>(buf->ptr);
   cudaStream_t st = stream_of(c, stream);
-  zero_insert_kernel<<<grid_for(int64_t(elems), 256), 256, 0, st>>>(dy, up, int64_t(g.N) * g.Co, g.P, g.Q, P1, Q1,
+  zero_insert_kernel<<<grid_for(int64_t(g.N) * g.Co * P1 * 32, 256), 256, 0, st>>>(dy, up, int64_t(g.N) * g.Co, g.P, g.Q, P1, Q1,
                                                                      g.sh, g.sw);
   check_launch("zero_insert");
   count_launch(c);

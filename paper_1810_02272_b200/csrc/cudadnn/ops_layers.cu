@@ -108,6 +108,104 @@ __global__ void lrn_bwd(const T* __restrict__ x, const T* __restrict__ y, const 
   }
 }
 
+// Compile-time window (local_size 3 / 5, AlexNet uses 5): the window's values
+// live in a register ring, so every tensor is read exactly once per pixel
+// (forward: x; backward: x, y, scale, dy) and the leaving channel is never
+// re-fetched; the entering channel's loads are issued kLrnU channels ahead.
+template <typename T, int SIZE>
+__global__ void lrn_fwd_ring(const T* __restrict__ x, T* __restrict__ y, T* __restrict__ scale, int N, int C, int HW,
+                             T alpha, T beta, T k) {
+  constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
+  const int64_t pixels = int64_t(N) * HW;
+  const T aN = alpha / T(SIZE);
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < pixels; p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t img = p / HW, hw = p - img * HW;
+    const int64_t base = img * C * HW + hw;
+    T xr[SIZE];  // x of channels c - pre .. c + post (0 outside [0, C))
+#pragma unroll
+    for (int j = 0; j < SIZE; ++j) {
+      const int cc = j - pre;
+      xr[j] = (cc >= 0 && cc < C) ? __ldg(x + base + int64_t(cc) * HW) : T(0);
+    }
+    for (int c0 = 0; c0 < C; c0 += kLrnU) {
+      T nx[kLrnU];  // entering channels c + post + 1 for the group's kLrnU channels
+#pragma unroll
+      for (int u = 0; u < kLrnU; ++u) {
+        const int cin = c0 + u + post + 1;
+        nx[u] = cin < C ? __ldg(x + base + int64_t(cin) * HW) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kLrnU; ++u) {
+        const int c = c0 + u;
+        if (c >= C) break;
+        T sum = T(0);
+#pragma unroll
+        for (int j = 0; j < SIZE; ++j) sum += xr[j] * xr[j];
+        const int64_t o = base + int64_t(c) * HW;
+        const T sc = k + aN * sum;
+        scale[o] = sc;
+        y[o] = xr[pre] * neg_pow(sc, beta);
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
+        xr[SIZE - 1] = nx[u];
+      }
+    }
+  }
+}
+
+template <typename T, int SIZE>
+__global__ void lrn_bwd_ring(const T* __restrict__ x, const T* __restrict__ y, const T* __restrict__ scale,
+                             const T* __restrict__ dy, T* __restrict__ dx, int N, int C, int HW, T alpha, T beta) {
+  constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
+  const int64_t pixels = int64_t(N) * HW;
+  const T coef = T(2) * alpha * beta / T(SIZE);
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < pixels; p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t img = p / HW, hw = p - img * HW;
+    const int64_t base = img * C * HW + hw;
+    // rings over channels c - post .. c + pre: t = dy*y/scale, and dy, scale for the output
+    T tr[SIZE], dyr[SIZE], scr[SIZE];
+#pragma unroll
+    for (int j = 0; j < SIZE; ++j) {
+      const int cc = j - post;
+      if (cc >= 0 && cc < C) {
+        const int64_t o = base + int64_t(cc) * HW;
+        dyr[j] = __ldg(dy + o);
+        scr[j] = __ldg(scale + o);
+        tr[j] = dyr[j] * __ldg(y + o) / scr[j];
+      } else {
+        dyr[j] = T(0); scr[j] = T(1); tr[j] = T(0);
+      }
+    }
+    for (int c0 = 0; c0 < C; c0 += kLrnU) {
+      T ndy[kLrnU], ny[kLrnU], nsc[kLrnU], xv[kLrnU];
+#pragma unroll
+      for (int u = 0; u < kLrnU; ++u) {
+        const int c = c0 + u, cin = c + pre + 1;
+        const bool in = cin < C;
+        const int64_t oi = base + int64_t(in ? cin : 0) * HW;
+        ndy[u] = in ? __ldg(dy + oi) : T(0);
+        ny[u] = in ? __ldg(y + oi) : T(0);
+        nsc[u] = in ? __ldg(scale + oi) : T(1);
+        xv[u] = c < C ? __ldg(x + base + int64_t(c) * HW) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kLrnU; ++u) {
+        const int c = c0 + u;
+        if (c >= C) break;
+        T acc = T(0);
+#pragma unroll
+        for (int j = 0; j < SIZE; ++j) acc += tr[j];
+        dx[base + int64_t(c) * HW] = dyr[post] * neg_pow(scr[post], beta) - coef * xv[u] * acc;
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; scr[j] = scr[j + 1]; }
+        dyr[SIZE - 1] = ndy[u];
+        scr[SIZE - 1] = nsc[u];
+        tr[SIZE - 1] = ndy[u] * ny[u] / nsc[u];
+      }
+    }
+  }
+}
+
 // ---- Dropout --------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t drop_hash(uint64_t seed, uint64_t iter, uint64_t idx) {
   uint64_t z = seed * 0x9E3779B97F4A7C15ull ^ (iter + 1) * 0xBF58476D1CE4E5B9ull ^ (idx + 1) * 0x94D049BB133111EBull;
@@ -338,8 +436,14 @@ int cdnn_lrn_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle sca
     DeviceGuard g(cx);
     by_dtype(X.dtype, "lrn", [&](auto tag) {
       using T = decltype(tag);
-      lrn_fwd<T><<<blocks(int64_t(n) * hw), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), n, c, hw,
-                                                                        local_size, T(alpha), T(beta), T(k));
+      cudaStream_t st = stream_of(cx, stream);
+      const int nb = blocks(int64_t(n) * hw);
+      if (local_size == 5)
+        lrn_fwd_ring<T, 5><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), n, c, hw, T(alpha), T(beta), T(k));
+      else if (local_size == 3)
+        lrn_fwd_ring<T, 3><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), n, c, hw, T(alpha), T(beta), T(k));
+      else
+        lrn_fwd<T><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), n, c, hw, local_size, T(alpha), T(beta), T(k));
     });
     check_launch("lrn_fwd");
     count_launch(cx);
@@ -360,8 +464,15 @@ int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle sc
     DeviceGuard g(cx);
     by_dtype(X.dtype, "lrn_bwd", [&](auto tag) {
       using T = decltype(tag);
-      lrn_bwd<T><<<blocks(int64_t(n) * hw), kT, 0, stream_of(cx, stream)>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX),
-                                                                        n, c, hw, local_size, T(alpha), T(beta));
+      cudaStream_t st = stream_of(cx, stream);
+      const int nb = blocks(int64_t(n) * hw);
+      if (local_size == 5)
+        lrn_bwd_ring<T, 5><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, T(alpha), T(beta));
+      else if (local_size == 3)
+        lrn_bwd_ring<T, 3><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, T(alpha), T(beta));
+      else
+        lrn_bwd<T><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, local_size, T(alpha),
+                                      T(beta));
     });
     check_launch("lrn_bwd");
     count_launch(cx);
