@@ -46,13 +46,25 @@ __host__ __device__ constexpr int tmem_cols_for(int bn) {
 
 template <int BN, bool SPLIT>
 __host__ __device__ constexpr int stages_for() {
-  return SPLIT ? 3 : 4;
+  // BN = 32 (skinny GEMMs: small-filter backward-filter, narrow layers): two
+  // stages keep a CTA under half the shared memory, so two CTAs share an SM and
+  // twice the gather loads are in flight per SM.
+  return BN <= 32 ? 2 : (SPLIT ? 3 : 4);
 }
+
+// CTAs of one tile shape resident per SM (shared memory bound).
+template <int BN, bool SPLIT>
+__host__ __device__ constexpr int ctas_per_sm();
 
 template <int BN, bool SPLIT>
 __host__ __device__ constexpr int smem_bytes() {
   return 1024 /*align slack*/ + stages_for<BN, SPLIT>() * (BM * BK * 4 + BN * BK * 4) * (SPLIT ? 2 : 1) +
          (3 * stages_for<BN, SPLIT>() + 1) * 8 + 16;
+}
+
+template <int BN, bool SPLIT>
+__host__ __device__ constexpr int ctas_per_sm() {
+  return (227 * 1024) / smem_bytes<BN, SPLIT>() >= 2 ? 2 : 1;
 }
 
 // Byte offset of 16-byte chunk `kc` (0..7) of row `r` in a K-major SWIZZLE_128B tile.
@@ -207,7 +219,7 @@ __device__ __forceinline__ void split_in_place(uint32_t hi, uint32_t lo, int t) 
 }
 
 template <int BN, bool SPLIT, class VA, class VB, class EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const VA va, const VB vb, const EPI epi, int M, int N, int K, int kt_per_split) {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");

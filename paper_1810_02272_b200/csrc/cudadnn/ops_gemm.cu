@@ -23,14 +23,16 @@ GemmPlan plan_tc(int M, int N, int K) {
   const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + p.bn - 1) / p.bn);
   const int kt = (K + tc::BK - 1) / tc::BK;
   int splits = 1;
-  if (tiles < kNumSMs && kt >= 8) {
-    // one CTA per SM (shared memory): pick the split count with the best
-    // whole-wave occupancy up to ~2 waves, fewest splits on ties
-    const int smax = std::max(1, std::min(kt / 4, (2 * kNumSMs + tiles - 1) / tiles));
+  // resident CTA slots: one per SM, two for the 32-wide tiles (tc::ctas_per_sm)
+  const int slots = kNumSMs * (p.bn == 32 ? tc::ctas_per_sm<32, true>() : 1);
+  if (tiles < slots && kt >= 8) {
+    // pick the split count with the best whole-wave occupancy of the resident
+    // slots up to ~2 waves, fewest splits on ties
+    const int smax = std::max(1, std::min(kt / 4, (2 * slots + tiles - 1) / tiles));
     double best = 0.0;
     for (int sp = 1; sp <= smax; ++sp) {
-      const int ctas = tiles * sp, waves = (ctas + kNumSMs - 1) / kNumSMs;
-      const double eff = double(ctas) / (double(waves) * kNumSMs);
+      const int ctas = tiles * sp, waves = (ctas + slots - 1) / slots;
+      const double eff = double(ctas) / (double(waves) * slots);
       if (eff > best + 1e-9) { best = eff; splits = sp; }
     }
   }
