@@ -19,7 +19,8 @@
 // whose (p, q) fall in the padding columns are computed and dropped by the
 // epilogue.  Weights arrive per (block, tap) by TMA, pre-split K-major.
 //
-// Persistent CTAs (one per SM) walk the tiles; every stage is pipelined
+// Persistent CTAs (one per SM; two for the staging-bound small-channel convs)
+// walk the tiles; every stage is pipelined
 // against the others: A tiles double-buffered, weights in an mbarrier ring,
 // two TMEM accumulators so the epilogue of tile i overlaps the MMAs of i+1.
 // Warp roles (320 threads): warp 0 TMA producer of the weights, warp 1 TMEM
@@ -108,7 +109,7 @@ __device__ __forceinline__ void put_row8(uint32_t rbase, uint32_t lo_off, int ro
 }
 
 template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     conv_tap_kernel(const __grid_constant__ CUtensorMap tm_w_hi, const __grid_constant__ CUtensorMap tm_w_lo,
                     const TapArgs a) {
   // 3xTF32 with BN <= 64: one MMA against [B_hi | B_lo] (N = 2*BN) gives A_hi*B_hi

@@ -171,9 +171,20 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   int bn = Cout <= 32 ? 32 : (Cout <= 64 ? 64 : 128);
   if (bn > 32 && tiles * G * ((Cout + bn - 1) / bn) < kNumSMs) bn = bn == 128 ? 64 : 32;
   // shared memory: A buffers (double-buffered over channel blocks when they fit) + B ring
-  constexpr int kBudget = 227 * 1024;
+  int budget = 227 * 1024;
+  // Few MMAs per staged tile (small channel counts: the column-folded conv1s) leave
+  // the four stager warps as the bottleneck: size the CTA for two per SM so twice
+  // the staging runs per SM (TMEM: 2 x <= 256 columns).
+  const int taps_eff = a.fold ? g.R : g.R * g.S;
+  const int nk8_max = ((a.fold ? g.S * Cin : std::min(32, Cin)) + 7) >> 3;
+  const bool staging_bound = a.cblocks == 1 && taps_eff * nk8_max <= 16;
+  int ctas_per_sm = 1;
+  if (staging_bound && tctap::smem_bytes(a.rows, 1, 2, bn, split) <= 113 * 1024) {
+    budget = 113 * 1024;
+    ctas_per_sm = 2;
+  }
   a.nbuf = 2;
-  auto fits = [&](int nbuf, int stages) { return tctap::smem_bytes(a.rows, nbuf, stages, bn, split) <= kBudget; };
+  auto fits = [&](int nbuf, int stages) { return tctap::smem_bytes(a.rows, nbuf, stages, bn, split) <= budget; };
   if (!fits(a.nbuf, 2)) a.nbuf = 1;
   if (!fits(a.nbuf, 2)) return false;
   a.stages = 2;
@@ -203,7 +214,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   const CUtensorMap* twl = tmap_generic(c, wlo, 2, wdims, wstr, wbox, 128);
   a.tiles_m = tiles;
   a.tiles = tiles * ((Cout + bn - 1) / bn);
-  dim3 grid(std::min(a.tiles, kNumSMs));  // persistent: one CTA per SM walks the tiles
+  dim3 grid(std::min(a.tiles, ctas_per_sm * kNumSMs));  // persistent: CTAs walk the tiles
   for (int grp = 0; grp < G; ++grp) {
     tctap::TapArgs ag = a;
     ag.in = in + int64_t(grp) * Cin * Hin * Win;
