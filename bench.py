@@ -460,6 +460,9 @@ def run_b200(args) -> None:
                 "kernel": f"{dom_layer} {dom_phase} (implicit-GEMM tcgen05, "
                           f"{'3xTF32' if config(1, True)['math'] == 'tf32x3' else 'TF32'})",
                 "flops_per_launch": dom_f, "ms_per_launch": round(dom_ms, 5),
+                # 3xTF32 issues three TF32 products per multiply-add (hi*hi, hi*lo, lo*hi):
+                # the tensor-core work behind the algorithmic FLOPs, against the same peak
+                "mma_frac": round(achieved * (3 if config(1, True)['math'] == 'tf32x3' else 1) / tf32_peak, 5),
                 "share_of_step": round(dom_ms / prof_total, 4),
                 "peak_note": f"TF32 dense = measured bf16 {pk['bf16_tflops']} / 2 ({pk['source']})"}
     else:

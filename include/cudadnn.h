@@ -244,6 +244,11 @@ CDNN_API int cdnn_conv_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x,
                                   cdnn_handle bias, cdnn_handle y, int flags, cdnn_handle stream);
 CDNN_API int cdnn_conv_backward_data(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w,
                                      cdnn_handle dy, cdnn_handle dx, cdnn_handle stream);
+/* cdnn_conv_backward_data with a fused ReLU gate (see cdnn_pool_backward_ex; 0 = none):
+ * applied in the tap kernels' epilogue, else by a trailing gate pass */
+CDNN_API int cdnn_conv_backward_data_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w,
+                                        cdnn_handle dy, cdnn_handle dx, cdnn_handle gate,
+                                        cdnn_handle stream);
 CDNN_API int cdnn_conv_backward_filter(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x,
                                        cdnn_handle dy, cdnn_handle dw, cdnn_handle db,
                                        cdnn_handle stream);
@@ -259,6 +264,11 @@ CDNN_API int cdnn_pool_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x,
                                   cdnn_handle mask, int flags, cdnn_handle stream);
 CDNN_API int cdnn_pool_backward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_handle mask,
                                 cdnn_handle dx, cdnn_handle stream);
+/* Backward entry points with a fused ReLU gate: dx = gate > 0 ? grad : 0 elementwise,
+ * gate = the data of the in-place ReLU on this layer's bottom (its backward,
+ * layers.cpp:188-195, then no longer runs); gate 0 = the plain entry point. */
+CDNN_API int cdnn_pool_backward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_handle mask,
+                                   cdnn_handle dx, cdnn_handle gate, cdnn_handle stream);
 
 /* elementwise (layers.cpp:180-221); n elements */
 CDNN_API int cdnn_relu_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, uint64_t n, cdnn_handle stream);
@@ -294,6 +304,10 @@ CDNN_API int cdnn_lrn_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_h
 CDNN_API int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale,
                                cdnn_handle dy, cdnn_handle dx, int n, int c, int hw,
                                int local_size, double alpha, double beta, cdnn_handle stream);
+/* cdnn_lrn_backward with a fused ReLU gate (see cdnn_pool_backward_ex; 0 = none) */
+CDNN_API int cdnn_lrn_backward_ex(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale,
+                                  cdnn_handle dy, cdnn_handle dx, int n, int c, int hw, int local_size,
+                                  double alpha, double beta, cdnn_handle gate, cdnn_handle stream);
 /* Dropout (train): out[i] = in[i]/(1-ratio) if hash(seed, *counter, i) > ratio*2^32 else 0.
  * The same call maps forward data and backward diffs (same seed + counter -> same mask).
  * `counter` is an 8-byte device buffer (u64 iteration), read by the kernel so graph replays

@@ -126,11 +126,17 @@ class Layer {
   // place) before backward reads it; layers whose backward needs that data keep
   // a private copy (Caffe BatchNorm x_norm_, Scale temp_).
   void set_clobbered(bool top, bool bottom) { top_clobbered_ = top; bottom_clobbered_ = bottom; }
+  // B200: set by Net when this layer's backward also applies the backward of the
+  // in-place ReLU on its bottom 0 (dx = bottom data > 0 ? dx : 0, layers.cpp:188-195
+  // semantics); that ReLU's own backward pass then does not run.
+  virtual bool supports_relu_gate() const { return false; }
+  void set_relu_gate(bool on) { relu_gate_ = on; }
 
  protected:
   LayerSpec spec_;
   std::vector<bool> propagate_down_;
   bool top_clobbered_ = false, bottom_clobbered_ = false;
+  bool relu_gate_ = false;
 };
 
 std::unique_ptr<Layer> make_layer(const LayerSpec& spec);
@@ -173,9 +179,12 @@ class ReluLayer final : public Layer {
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   // Forward already applied by the producer's epilogue (in-place fusion).
   void set_forward_fused(bool on) { forward_fused_ = on; }
+  // Backward applied by the consumer's backward (Layer::set_relu_gate).
+  void set_backward_fused(bool on) { backward_fused_ = on; }
 
  private:
   bool forward_fused_ = false;
+  bool backward_fused_ = false;
 };
 
 class SigmoidLayer final : public Layer {
@@ -276,6 +285,7 @@ class ConvolutionLayer final : public Layer {
   void backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   // Fuse a following in-place ReLU into the convolution epilogue (set by Net).
   void fuse_relu(bool on) { fused_relu_ = on; }
+  bool supports_relu_gate() const override { return true; }
 
  private:
   ConvolutionParam p_;
@@ -305,6 +315,7 @@ class PoolingLayer final : public Layer {
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   // Flat h*W+w argmax per output element (MAX only); downloads from HBM.
   std::vector<int> mask() const;
+  bool supports_relu_gate() const override { return true; }
   // Fuse a following in-place ReLU into the pooling output (set by Net).
   void fuse_relu(bool on) { fused_relu_ = on; }
 
@@ -359,6 +370,7 @@ class LRNLayer final : public Layer {
                            Rng& rng) override;
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  bool supports_relu_gate() const override { return true; }
 
  private:
   int size_;

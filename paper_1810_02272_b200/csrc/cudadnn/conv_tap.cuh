@@ -60,6 +60,7 @@ struct TapArgs {
   int nbuf, stages;      // A buffers (1|2), weight ring depth
   int relu;              // fused in-place ReLU in the epilogue (forward)
   int fold;              // S folded into the channels (k = s*Cin + c, Cin*S <= 32): R taps of K = S*Cin
+  const float* gate;     // backward-data: fused in-place ReLU backward, out = gate > 0 ? out : 0 (same layout)
   FastDiv div_hwv, div_wv;
   unsigned long long* trace;  // debug timeline (CDNN_TAP_TRACE), null in production
 };
@@ -109,7 +110,7 @@ __device__ __forceinline__ void put_row8(uint32_t rbase, uint32_t lo_off, int ro
 }
 
 template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
     conv_tap_kernel(const __grid_constant__ CUtensorMap tm_w_hi, const __grid_constant__ CUtensorMap tm_w_lo,
                     const TapArgs a) {
   // 3xTF32 with BN <= 64: one MMA against [B_hi | B_lo] (N = 2*BN) gives A_hi*B_hi
@@ -372,8 +373,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int acc_buf = ts & 1;
       const int m0 = (t % a.tiles_m) * 128;
       const int nc0 = (t / a.tiles_m) * BN;  // output channel of TMEM column 0 (within the group)
-      ptx::mbar_wait(&t_full[acc_buf], uint32_t(ts >> 1) & 1u);
-      ptx::tc_fence_after();
       const int v = m0 + q4 * 32 + lane;
       const int img = int(a.div_hwv.div(uint32_t(v)));
       const int rem = v - img * HWv;
@@ -381,8 +380,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int q = rem - p * a.Wv;
       const bool valid = v < a.Mv && p < a.P && q < a.Q;
       float* outp = a.out + int64_t(img) * a.out_nstride + int64_t(p) * a.Q + q;
-#pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 16) {
+      const float* gatep = a.gate ? a.gate + (outp - a.out) : nullptr;  // dereferenced only for valid rows
+      // One output chunk: 16 accumulator columns -> (+ bias, ReLU, gate) -> NCHW stores.
+      auto store_chunk = [&](int cc, const float (&gv)[16]) {
         uint32_t r[16];
         ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * ACC + cc), r);
         if constexpr (CAT) {
@@ -394,16 +394,57 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         ptx::tmem_ld_wait();
         if (valid) {
+          // bias reads for the 16 columns issued before the first store (the stores
+          // may alias them as far as the compiler knows)
+          float bv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = nc0 + cc + j;
+            bv[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
+          }
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int n = nc0 + cc + j;
             if (n < a.Cout) {
-              float o = __uint_as_float(r[j]);
-              if (a.bias) o += __ldg(a.bias + n);
+              float o = __uint_as_float(r[j]) + bv[j];
               if (a.relu) o = o > 0.f ? o : 0.f;
+              if (!(gv[j] > 0.f)) o = 0.f;
               outp[int64_t(n) * PQ] = o;
             }
           }
+        }
+      };
+      // (warp-uniform branch: tcgen05.ld is warp-collective)
+      if (a.gate == nullptr) {
+        ptx::mbar_wait(&t_full[acc_buf], uint32_t(ts >> 1) & 1u);
+        ptx::tc_fence_after();
+        float ones[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) ones[j] = 1.f;
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += 16) store_chunk(cc, ones);
+      } else {
+        // fused ReLU gate (backward-data): the reads do not depend on the accumulator,
+        // so chunk 0's are issued before waiting for it and chunk i+1's before chunk i
+        // is stored -- the gate adds no memory latency per chunk to the epilogue.
+        float gnext[16];
+        auto load_gate = [&](int cc, float (&g)[16]) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = nc0 + cc + j;
+            g[j] = (valid && n < a.Cout) ? __ldg(gatep + int64_t(n) * PQ) : 1.f;
+          }
+        };
+        load_gate(0, gnext);
+        ptx::mbar_wait(&t_full[acc_buf], uint32_t(ts >> 1) & 1u);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < BN; cc += 16) {
+          float gv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) gv[j] = gnext[j];
+          if (cc + 16 < BN) load_gate(cc + 16, gnext);
+          store_chunk(cc, gv);
         }
       }
       ptx::tc_fence_before();

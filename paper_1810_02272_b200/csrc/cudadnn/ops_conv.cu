@@ -128,7 +128,7 @@ void launch_conv_tap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const CUtenso
 // Tap-shift implicit GEMM (conv_tap.cuh): stride 1, any dilation, any group count.
 // Returns false when the staged tile does not fit shared memory.
 bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const float* in, const float* w,
-              const float* bias, float* out, cdnn_handle stream, bool relu = false) {
+              const float* bias, float* out, cdnn_handle stream, bool relu = false, const float* gate = nullptr) {
   ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
   const ConvGeom& g = d.geom;
   if (!conv_tap_enabled() || g.sh != 1 || g.sw != 1) return false;
@@ -179,7 +179,8 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   const int nk8_max = ((a.fold ? g.S * Cin : std::min(32, Cin)) + 7) >> 3;
   const bool staging_bound = a.cblocks == 1 && taps_eff * nk8_max <= 16;
   int ctas_per_sm = 1;
-  if (staging_bound && tctap::smem_bytes(a.rows, 1, 2, bn, split) <= 113 * 1024) {
+  // (32-wide tiles only: their kernel is register-bounded for two CTAs per SM)
+  if (staging_bound && bn == 32 && tctap::smem_bytes(a.rows, 1, 2, bn, split) <= 113 * 1024) {
     budget = 113 * 1024;
     ctas_per_sm = 2;
   }
@@ -219,6 +220,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
     tctap::TapArgs ag = a;
     ag.in = in + int64_t(grp) * Cin * Hin * Win;
     ag.out = out + int64_t(grp) * Cout * P * Q;
+    ag.gate = gate ? gate + int64_t(grp) * Cout * P * Q : nullptr;
     ag.bias = bias ? bias + grp * Cout : nullptr;
     ag.n0_base = grp * Cout;
     auto go = [&](auto split_tag) {
@@ -873,9 +875,35 @@ bool with_zero_inserted(Ctx* c, const ConvDescSlot& dconst, const float* dy, cdn
   return ok;
 }
 
+// dx = gate > 0 ? dx : 0 in place (a fused ReLU backward the route could not apply
+// in its epilogue)
+template <typename T>
+__global__ void relu_gate_kernel(const T* __restrict__ gate, T* __restrict__ dx, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    if (!(gate[i] > T(0))) dx[i] = T(0);
+}
+
+template <typename T>
+void conv_backward_data_impl(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, const BufferSlot& DY,
+                             BufferSlot& DX, cdnn_handle stream, const T* gate, bool& gated);
+
 template <typename T>
 void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, const BufferSlot& DY,
-                          BufferSlot& DX, cdnn_handle stream) {
+                          BufferSlot& DX, cdnn_handle stream, const T* gate = nullptr) {
+  bool gated = false;
+  conv_backward_data_impl<T>(c, d, Wt, DY, DX, stream, gate, gated);
+  if (gate && !gated) {
+    const ConvGeom& g = d.geom;
+    const int64_t n = int64_t(g.N) * g.C * g.H * g.W;
+    relu_gate_kernel<T><<<grid_for(n, 256), 256, 0, stream_of(c, stream)>>>(gate, reinterpret_cast<T*>(DX.dev), n);
+    check_launch("relu_gate");
+    count_launch(c);
+  }
+}
+
+template <typename T>
+void conv_backward_data_impl(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, const BufferSlot& DY,
+                             BufferSlot& DX, cdnn_handle stream, const T* gate, bool& gated) {
   const ConvGeom& g = d.geom;
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
@@ -902,8 +930,10 @@ void conv_backward_data_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt, c
   }
   if constexpr (std::is_same_v<T, float>) {
     if (conv_tap(c, d, true, reinterpret_cast<const float*>(DY.dev), reinterpret_cast<const float*>(Wt.dev), nullptr,
-                 reinterpret_cast<float*>(DX.dev), stream))
+                 reinterpret_cast<float*>(DX.dev), stream, false, gate)) {
+      gated = gate != nullptr;
       return;
+    }
     if (conv_direct_tma(c, d, true, reinterpret_cast<const float*>(DY.dev), reinterpret_cast<const float*>(Wt.dev),
                         nullptr, reinterpret_cast<float*>(DX.dev), stream))
       return;
@@ -1000,6 +1030,11 @@ int cdnn_conv_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_han
 
 int cdnn_conv_backward_data(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w, cdnn_handle dy, cdnn_handle dx,
                             cdnn_handle stream) {
+  return cdnn_conv_backward_data_ex(ctx, desc, w, dy, dx, 0, stream);
+}
+
+int cdnn_conv_backward_data_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w, cdnn_handle dy, cdnn_handle dx,
+                               cdnn_handle gate, cdnn_handle stream) {
   return guarded([&] {
     Ctx* c = need_ctx(ctx);
     const ConvDescSlot& d = conv_desc(c, desc);
@@ -1012,9 +1047,13 @@ int cdnn_conv_backward_data(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w, cdnn_
     require_len(DX, uint64_t(g.N) * g.C * g.H * g.W, "conv_bwd_data dx");
     require_dtype(DY, W.dtype, "conv_bwd_data");
     require_dtype(DX, W.dtype, "conv_bwd_data");
+    BufferSlot* G = buffer_or_null(c, gate, "conv_bwd_data gate");
+    if (G) { require_len(*G, uint64_t(g.N) * g.C * g.H * g.W, "conv_bwd_data gate"); require_dtype(*G, W.dtype, "gate"); }
     DeviceGuard dg(c);
-    if (W.dtype == CDNN_F32) conv_backward_data_t<float>(c, d, W, DY, DX, stream);
-    else if (W.dtype == CDNN_F64) conv_backward_data_t<double>(c, d, W, DY, DX, stream);
+    if (W.dtype == CDNN_F32)
+      conv_backward_data_t<float>(c, d, W, DY, DX, stream, G ? reinterpret_cast<const float*>(G->dev) : nullptr);
+    else if (W.dtype == CDNN_F64)
+      conv_backward_data_t<double>(c, d, W, DY, DX, stream, G ? reinterpret_cast<const double*>(G->dev) : nullptr);
     else fail(CDNN_INVALID_ARGUMENT, "conv_bwd_data: floating buffers required");
   });
 }

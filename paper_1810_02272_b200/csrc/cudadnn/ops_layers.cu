@@ -85,7 +85,8 @@ __global__ void lrn_fwd(const T* __restrict__ x, T* __restrict__ y, T* __restric
 // dx = dy * scale^-beta - 2*alpha*beta/n * x * sum_{c' : c in window(c')} dy*y/scale
 template <typename T>
 __global__ void lrn_bwd(const T* __restrict__ x, const T* __restrict__ y, const T* __restrict__ scale,
-                        const T* __restrict__ dy, T* __restrict__ dx, int N, int C, int HW, int size, T alpha, T beta) {
+                        const T* __restrict__ dy, T* __restrict__ dx, int N, int C, int HW, int size, T alpha, T beta,
+                        const T* __restrict__ gate) {
   const int64_t pixels = int64_t(N) * HW;
   const int pre = (size - 1) / 2, post = size - 1 - pre;
   const T coef = T(2) * alpha * beta / T(size);
@@ -103,7 +104,8 @@ __global__ void lrn_bwd(const T* __restrict__ x, const T* __restrict__ y, const 
       if (cin < C) acc += t(cin);
       if (cout >= 0) acc -= t(cout);
       const int64_t o = base + int64_t(c) * HW;
-      dx[o] = dy[o] * neg_pow(scale[o], beta) - coef * x[o] * acc;
+      const T g = dy[o] * neg_pow(scale[o], beta) - coef * x[o] * acc;
+      dx[o] = (gate && !(gate[o] > T(0))) ? T(0) : g;
     }
   }
 }
@@ -155,7 +157,8 @@ __global__ void lrn_fwd_ring(const T* __restrict__ x, T* __restrict__ y, T* __re
 
 template <typename T, int SIZE>
 __global__ void lrn_bwd_ring(const T* __restrict__ x, const T* __restrict__ y, const T* __restrict__ scale,
-                             const T* __restrict__ dy, T* __restrict__ dx, int N, int C, int HW, T alpha, T beta) {
+                             const T* __restrict__ dy, T* __restrict__ dx, int N, int C, int HW, T alpha, T beta,
+                             const T* __restrict__ gate) {
   constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
   const int64_t pixels = int64_t(N) * HW;
   const T coef = T(2) * alpha * beta / T(SIZE);
@@ -195,7 +198,9 @@ __global__ void lrn_bwd_ring(const T* __restrict__ x, const T* __restrict__ y, c
         T acc = T(0);
 #pragma unroll
         for (int j = 0; j < SIZE; ++j) acc += tr[j];
-        dx[base + int64_t(c) * HW] = dyr[post] * neg_pow(scr[post], beta) - coef * xv[u] * acc;
+        const T g = dyr[post] * neg_pow(scr[post], beta) - coef * xv[u] * acc;
+        // fused backward of an in-place ReLU on this layer's bottom (gate = its data)
+        dx[base + int64_t(c) * HW] = (gate && !(__ldg(gate + base + int64_t(c) * HW) > T(0))) ? T(0) : g;
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; scr[j] = scr[j + 1]; }
         dyr[SIZE - 1] = ndy[u];
@@ -452,6 +457,12 @@ int cdnn_lrn_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle sca
 
 int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale, cdnn_handle dy, cdnn_handle dx,
                       int n, int c, int hw, int local_size, double alpha, double beta, cdnn_handle stream) {
+  return cdnn_lrn_backward_ex(ctx, x, y, scale, dy, dx, n, c, hw, local_size, alpha, beta, 0, stream);
+}
+
+int cdnn_lrn_backward_ex(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale, cdnn_handle dy, cdnn_handle dx,
+                         int n, int c, int hw, int local_size, double alpha, double beta, cdnn_handle gate,
+                         cdnn_handle stream) {
   return guarded([&] {
     Ctx* cx = need_ctx(ctx);
     BufferSlot& X = buffer(cx, x, "lrn_bwd x");
@@ -459,20 +470,23 @@ int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle sc
     BufferSlot& S = buffer(cx, scale, "lrn_bwd scale");
     BufferSlot& DY = buffer(cx, dy, "lrn_bwd dy");
     BufferSlot& DX = buffer(cx, dx, "lrn_bwd dx");
+    BufferSlot* G = buffer_or_null(cx, gate, "lrn_bwd gate");
     const uint64_t cnt = uint64_t(n) * c * hw;
-    for (BufferSlot* b : {&X, &Y, &S, &DY, &DX}) { require_len(*b, cnt, "lrn_bwd"); require_dtype(*b, X.dtype, "lrn_bwd"); }
+    for (BufferSlot* b : {&X, &Y, &S, &DY, &DX, G})
+      if (b) { require_len(*b, cnt, "lrn_bwd"); require_dtype(*b, X.dtype, "lrn_bwd"); }
     DeviceGuard g(cx);
     by_dtype(X.dtype, "lrn_bwd", [&](auto tag) {
       using T = decltype(tag);
       cudaStream_t st = stream_of(cx, stream);
       const int nb = blocks(int64_t(n) * hw);
+      const T* gp = G ? reinterpret_cast<const T*>(G->dev) : nullptr;
       if (local_size == 5)
-        lrn_bwd_ring<T, 5><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, T(alpha), T(beta));
+        lrn_bwd_ring<T, 5><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, T(alpha), T(beta), gp);
       else if (local_size == 3)
-        lrn_bwd_ring<T, 3><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, T(alpha), T(beta));
+        lrn_bwd_ring<T, 3><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, T(alpha), T(beta), gp);
       else
         lrn_bwd<T><<<nb, kT, 0, st>>>(P<T>(X), P<T>(Y), P<T>(S), P<T>(DY), P<T>(DX), n, c, hw, local_size, T(alpha),
-                                      T(beta));
+                                      T(beta), gp);
     });
     check_launch("lrn_bwd");
     count_launch(cx);

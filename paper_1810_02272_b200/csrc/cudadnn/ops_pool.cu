@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(256) max_pool_fwd(const T* __restrict__ x, T* 
 // gather: every bottom element sums the top diffs of the windows whose argmax is it
 template <typename T>
 __global__ void __launch_bounds__(256) max_pool_bwd(const T* __restrict__ dy, const int* __restrict__ mask,
-                                                    T* __restrict__ dx, PoolGeom g, uint32_t total4) {
+                                                    T* __restrict__ dx, PoolGeom g, uint32_t total4,
+                                                    const T* __restrict__ gate) {
   // four consecutive bottom elements of one row per thread: the row's window range
   // (and the plane / row decomposition) is computed once per thread
   const uint32_t W4 = uint32_t(g.W + 3) >> 2;
@@ -81,7 +82,8 @@ __global__ void __launch_bounds__(256) max_pool_bwd(const T* __restrict__ dy, co
           const size_t o = base + ph * g.PW + pw;
           if (__ldg(mask + o) == me) s += __ldg(dy + o);
         }
-      dx[out + wq] = s;
+      // fused backward of an in-place ReLU on the pooling's bottom (gate = its data)
+      dx[out + wq] = (gate && !(__ldg(gate + out + wq) > T(0))) ? T(0) : s;
     }
   }
 }
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(256) ave_pool_fwd(const T* __restrict__ x, T* 
 
 template <typename T>
 __global__ void __launch_bounds__(256) ave_pool_bwd(const T* __restrict__ dy, T* __restrict__ dx, PoolGeom g,
-                                                    uint32_t total) {
+                                                    uint32_t total, const T* __restrict__ gate) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Idx3 q = split3(i, g.divHW, g.divW, uint32_t(g.H * g.W), uint32_t(g.W));
     const int h = int(q.h) + g.ph, w = int(q.w) + g.pw;
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(256) ave_pool_bwd(const T* __restrict__ dy, T*
         const int he = min(hs + g.kh, g.H + g.ph), we = min(ws + g.kw, g.W + g.pw);
         s += __ldg(dy + base + ph * g.PW + pw) / T((he - hs) * (we - ws));
       }
-    dx[i] = s;
+    dx[i] = (gate && !(__ldg(gate + i) > T(0))) ? T(0) : s;
   }
 }
 
@@ -187,17 +189,24 @@ int cdnn_pool_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_han
 
 int cdnn_pool_backward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_handle mask, cdnn_handle dx,
                        cdnn_handle stream) {
+  return cdnn_pool_backward_ex(ctx, desc, dy, mask, dx, 0, stream);
+}
+
+int cdnn_pool_backward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_handle mask, cdnn_handle dx,
+                          cdnn_handle gate, cdnn_handle stream) {
   return guarded([&] {
     Ctx* c = need_ctx(ctx);
     PoolDescSlot d = pool_desc(c, desc);
     BufferSlot& DY = buffer(c, dy, "pool_bwd dy");
     BufferSlot& DX = buffer(c, dx, "pool_bwd dx");
     BufferSlot* M = buffer_or_null(c, mask, "pool_bwd mask");
+    BufferSlot* G = buffer_or_null(c, gate, "pool_bwd gate");
     const PoolGeom g = geom_of(d);
     const uint64_t nin = uint64_t(g.N) * g.C * g.H * g.W, nout = uint64_t(g.N) * g.C * g.PH * g.PW;
     require_len(DY, nout, "pool_bwd dy");
     require_len(DX, nin, "pool_bwd dx");
     require_dtype(DX, DY.dtype, "pool_bwd");
+    if (G) { require_len(*G, nin, "pool_bwd gate"); require_dtype(*G, DY.dtype, "pool_bwd gate"); }
     if (d.p.method == CDNN_POOL_MAX) {
       if (!M) fail(CDNN_INVALID_ARGUMENT, "pool_bwd: MAX pooling needs the argmax mask");
       require_len(*M, nout, "pool_bwd mask");
@@ -212,11 +221,11 @@ int cdnn_pool_backward(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_hand
         const uint64_t n4 = uint64_t(g.N) * g.C * g.H * ((g.W + 3) / 4);
         max_pool_bwd<T><<<grid_for(int64_t(n4), 256), 256, 0, st>>>(
             reinterpret_cast<const T*>(DY.dev), reinterpret_cast<const int*>(M->dev), reinterpret_cast<T*>(DX.dev), g,
-            uint32_t(n4));
+            uint32_t(n4), G ? reinterpret_cast<const T*>(G->dev) : nullptr);
       }
       else
         ave_pool_bwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(DY.dev), reinterpret_cast<T*>(DX.dev), g,
-                                                 uint32_t(nin));
+                                                 uint32_t(nin), G ? reinterpret_cast<const T*>(G->dev) : nullptr);
     };
     if (DY.dtype == CDNN_F32) run(float{});
     else if (DY.dtype == CDNN_F64) run(double{});

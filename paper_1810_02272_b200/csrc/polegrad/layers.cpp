@@ -204,6 +204,7 @@ void ReluLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> t
 }
 
 void ReluLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
+  if (backward_fused_) return;  // the consumer's backward applied the gate
   Registry& reg = bottoms[0]->registry();
   const cdnn_handle x = bottoms[0]->gpu_data(), dy = tops[0]->gpu_diff();
   cdnn_ok(cdnn_relu_backward(reg.context(), x, dy, bottoms[0]->overwrite_gpu_diff(), bottoms[0]->count(), reg.stream()),

@@ -124,9 +124,10 @@ void LRNLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> to
 void LRNLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
   if (!propagate_down(0)) return;
   Registry& reg = bottoms[0]->registry();
-  cdnn_ok(cdnn_lrn_backward(reg.context(), bottoms[0]->gpu_data(), tops[0]->gpu_data(), scale_->gpu_data(),
-                            tops[0]->gpu_diff(), bottoms[0]->overwrite_gpu_diff(), n_, c_, hw_, size_, alpha_, beta_,
-                            reg.stream()),
+  const cdnn_handle x = bottoms[0]->gpu_data();
+  cdnn_ok(cdnn_lrn_backward_ex(reg.context(), x, tops[0]->gpu_data(), scale_->gpu_data(), tops[0]->gpu_diff(),
+                               bottoms[0]->overwrite_gpu_diff(), n_, c_, hw_, size_, alpha_, beta_,
+                               relu_gate_ ? x : 0, reg.stream()),
           "LRN backward");
 }
 

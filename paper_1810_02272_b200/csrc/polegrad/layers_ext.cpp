@@ -147,7 +147,9 @@ void ConvolutionLayer::backward_weights(std::span<Blob* const> tops, std::span<B
 void ConvolutionLayer::backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
   Registry& reg = *reg_;
   const cdnn_handle w = params_[0]->gpu_data(), dy = tops[0]->gpu_diff();
-  cdnn_ok(cdnn_conv_backward_data(reg.context(), desc_, w, dy, bottoms[0]->overwrite_gpu_diff(), reg.stream()),
+  const cdnn_handle gate = relu_gate_ ? bottoms[0]->gpu_data() : 0;
+  cdnn_ok(cdnn_conv_backward_data_ex(reg.context(), desc_, w, dy, bottoms[0]->overwrite_gpu_diff(), gate,
+                                     reg.stream()),
           "Convolution backward");
 }
 
@@ -188,7 +190,8 @@ void PoolingLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> 
   if (!propagate_down(0)) return;
   Registry& reg = *reg_;
   const cdnn_handle dy = tops[0]->gpu_diff();
-  cdnn_ok(cdnn_pool_backward(reg.context(), desc_, dy, mask_, bottoms[0]->overwrite_gpu_diff(), reg.stream()),
+  const cdnn_handle gate = relu_gate_ ? bottoms[0]->gpu_data() : 0;
+  cdnn_ok(cdnn_pool_backward_ex(reg.context(), desc_, dy, mask_, bottoms[0]->overwrite_gpu_diff(), gate, reg.stream()),
           "Pooling backward");
 }
 

@@ -184,6 +184,32 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
       relu->set_forward_fused(true);
     }
   }
+  // Fuse an in-place ReLU's backward into the backward of the layer that consumes
+  // its top (Pooling, LRN, Convolution dgrad): that layer writes the ReLU blob's
+  // diff gated by the blob's data, and the ReLU pass disappears.  Only when the
+  // consumer directly follows the ReLU and nothing else reads or rewrites the blob
+  // (CDNN_FUSE_RELU_BWD=0 keeps them apart).
+  static const bool fuse_relu_bwd = [] {
+    const char* v = std::getenv("CDNN_FUSE_RELU_BWD");
+    return !(v && std::string(v) == "0");
+  }();
+  for (std::size_t i = 0; fuse_relu_bwd && !compat && i + 1 < layers_.size(); ++i) {
+    auto* relu = dynamic_cast<ReluLayer*>(layers_[i].get());
+    if (!relu || bottoms_[i].size() != 1 || tops_[i].size() != 1 || bottoms_[i][0] != tops_[i][0]) continue;
+    Blob* b = tops_[i][0];
+    Layer* consumer = layers_[i + 1].get();
+    if (!consumer->supports_relu_gate() || bottoms_[i + 1].empty() || bottoms_[i + 1][0] != b) continue;
+    bool other_use = false;
+    for (std::size_t k = i + 1; k < layers_.size() && !other_use; ++k) {
+      for (std::size_t q = 0; q < bottoms_[k].size(); ++q)
+        if (bottoms_[k][q] == b && !(k == i + 1 && q == 0)) other_use = true;
+      for (Blob* t : tops_[k])
+        if (t == b) other_use = true;
+    }
+    if (other_use) continue;
+    consumer->set_relu_gate(true);
+    relu->set_backward_fused(true);
+  }
   pack_params();
 }
 

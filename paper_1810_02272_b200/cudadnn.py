@@ -41,12 +41,12 @@ EXPORTS = [
     "cdnn_event_free", "cdnn_event_sync", "cdnn_rng_create", "cdnn_rng_next_u64", "cdnn_rng_uniform", "cdnn_subsystem_free",
     "cdnn_conv_desc_create", "cdnn_conv_output_shape", "cdnn_pool_desc_create", "cdnn_pool_output_shape",
     "cdnn_desc_free", "cdnn_dispatch", "cdnn_fill", "cdnn_copy", "cdnn_scal", "cdnn_axpy", "cdnn_dot",
-    "cdnn_gemm", "cdnn_ip_forward", "cdnn_ip_backward", "cdnn_conv_forward", "cdnn_conv_backward_data",
-    "cdnn_conv_backward_filter", "cdnn_pool_forward", "cdnn_pool_backward", "cdnn_relu_forward",
+    "cdnn_gemm", "cdnn_ip_forward", "cdnn_ip_backward", "cdnn_conv_forward", "cdnn_conv_backward_data", "cdnn_conv_backward_data_ex",
+    "cdnn_conv_backward_filter", "cdnn_pool_forward", "cdnn_pool_backward", "cdnn_pool_backward_ex", "cdnn_relu_forward",
     "cdnn_relu_backward", "cdnn_sigmoid_forward", "cdnn_sigmoid_backward", "cdnn_softmax_forward",
     "cdnn_softmax_backward", "cdnn_softmax_loss_forward", "cdnn_softmax_loss_backward", "cdnn_solver_apply",
     "cdnn_nccl_available", "cdnn_nccl_unique_id", "cdnn_nccl_comm_create", "cdnn_allreduce_sum",
-    "cdnn_broadcast", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_dropout", "cdnn_counter_increment",
+    "cdnn_broadcast", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_lrn_backward_ex", "cdnn_dropout", "cdnn_counter_increment",
     "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
     "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
     "cdnn_pool_forward_ex", "cdnn_pg_diff",
@@ -119,8 +119,10 @@ def load() -> C.CDLL:
             "cdnn_conv_forward": ([vp, h, h, h, h, h, h], i),
             "cdnn_conv_forward_ex": ([vp, h, h, h, h, h, i, h], i),
             "cdnn_conv_backward_data": ([vp, h, h, h, h, h], i),
+            "cdnn_conv_backward_data_ex": ([vp, h, h, h, h, h, h], i),
             "cdnn_conv_backward_filter": ([vp, h, h, h, h, h, h], i),
             "cdnn_pool_forward": ([vp, h, h, h, h, h], i), "cdnn_pool_forward_ex": ([vp, h, h, h, h, i, h], i), "cdnn_pool_backward": ([vp, h, h, h, h, h], i),
+            "cdnn_pool_backward_ex": ([vp, h, h, h, h, h, h], i),
             "cdnn_relu_forward": ([vp, h, h, u64, h], i), "cdnn_relu_backward": ([vp, h, h, h, u64, h], i),
             "cdnn_sigmoid_forward": ([vp, h, h, u64, h], i), "cdnn_sigmoid_backward": ([vp, h, h, h, u64, h], i),
             "cdnn_softmax_forward": ([vp, h, h, i, i, h], i), "cdnn_softmax_backward": ([vp, h, h, h, i, i, h], i),
@@ -132,6 +134,7 @@ def load() -> C.CDLL:
             "cdnn_allreduce_sum": ([vp, h, h, u64, u64, h], i), "cdnn_broadcast": ([vp, h, h, u64, i, h], i),
             "cdnn_lrn_forward": ([vp, h, h, h, i, i, i, i, d, d, d, h], i),
             "cdnn_lrn_backward": ([vp, h, h, h, h, h, i, i, i, i, d, d, h], i),
+            "cdnn_lrn_backward_ex": ([vp, h, h, h, h, h, i, i, i, i, d, d, h, h], i),
             "cdnn_dropout": ([vp, h, h, u64, d, u64, h, h], i), "cdnn_counter_increment": ([vp, h, h], i),
             "cdnn_batchnorm_forward": ([vp, h, h, h, h, i, i, i, d, h], i),
             "cdnn_batchnorm_backward": ([vp, h, h, h, h, h, i, i, i, h], i),

@@ -73,6 +73,8 @@ def main():
             "fwd": lambda: ctx.call("cdnn_conv_forward", d, x, wt, b, y, 0),
             "dgrad": lambda: ctx.call("cdnn_conv_backward_data", d, wt, dy, dx, 0),
             "wgrad": lambda: ctx.call("cdnn_conv_backward_filter", d, x, dy, dw, 0, 0),
+            # backward-data with the fused ReLU gate (gate = the layer's own input here)
+            "dgrad_gate": lambda: ctx.call("cdnn_conv_backward_data_ex", d, wt, dy, dx, x, 0),
         }
         for op, fn in ops.items():
             ms = timeit(ctx, fn, args.reps)

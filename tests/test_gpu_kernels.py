@@ -344,3 +344,48 @@ def test_ip_large_tensor_core(ctx, math, rows, k, o):
     assert rel_l2(ctx.read(hdb), dYd.sum(0)) <= 1e-6
     for h in (hx, hw, hb, hdy, hy, hdx, hdw, hdb):
         ctx.free(h)
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+def test_fused_relu_gate_backward(ctx, dtype):
+    """cdnn_{pool,lrn,conv}_backward_*_ex(gate) == plain backward followed by the ReLU
+    backward on the gate data (layers.cpp:188-195), bit for bit; gate 0 == plain."""
+    rng = np.random.default_rng(17)
+    dt = NP[dtype]
+    n, c, h, w = 3, 16, 12, 12
+    gate = rng.standard_normal((n, c, h, w)).astype(dt)   # the in-place ReLU's data
+    gate[gate < 0] = 0                                      # (post-ReLU values: zeros and positives)
+    hg = ctx.upload(gate)
+    mask_on = gate > 0
+
+    # pooling (MAX 3x3/2 and AVE 2x2/2)
+    for method, k, s in ((cd.POOL_MAX, 3, 2), (cd.POOL_AVE, 2, 2)):
+        d = ctx.pool_desc(n, c, h, w, method, k, s, 0)
+        ph, pw = ctx.pool_output_shape(d)[2:]
+        hy, hm = ctx.alloc(n * c * ph * pw, dtype), ctx.alloc(n * c * ph * pw, cd.I32)
+        ctx.call("cdnn_pool_forward", d, hg, hy, hm, 0)
+        hdy = ctx.upload(rng.standard_normal(n * c * ph * pw).astype(dt))
+        plain, fused = ctx.alloc(gate.size, dtype), ctx.alloc(gate.size, dtype)
+        ctx.call("cdnn_pool_backward", d, hdy, hm, plain, 0)
+        ctx.call("cdnn_pool_backward_ex", d, hdy, hm, fused, hg, 0)
+        assert np.array_equal(ctx.read(fused), np.where(mask_on.ravel(), ctx.read(plain), 0))
+
+    # LRN (the gate is the LRN's own bottom data)
+    hy, hs = ctx.alloc(gate.size, dtype), ctx.alloc(gate.size, dtype)
+    ctx.call("cdnn_lrn_forward", hg, hy, hs, n, c, h * w, 5, 1e-2, 0.75, 1.0, 0)
+    hdy = ctx.upload(rng.standard_normal(gate.size).astype(dt))
+    plain, fused = ctx.alloc(gate.size, dtype), ctx.alloc(gate.size, dtype)
+    ctx.call("cdnn_lrn_backward", hg, hy, hs, hdy, plain, n, c, h * w, 5, 1e-2, 0.75, 0)
+    ctx.call("cdnn_lrn_backward_ex", hg, hy, hs, hdy, fused, n, c, h * w, 5, 1e-2, 0.75, hg, 0)
+    assert np.array_equal(ctx.read(fused), np.where(mask_on.ravel(), ctx.read(plain), 0))
+
+    # convolution backward-data (stride 1: tap-kernel epilogue; stride 2: trailing gate pass)
+    for stride in (1, 2):
+        d = ctx.conv_desc(n, c, h, w, 32, 3, stride, 1)
+        P, Q = ctx.conv_output_shape(d)[2:]
+        hw_ = ctx.upload(rng.standard_normal(32 * c * 9).astype(dt))
+        hdy = ctx.upload(rng.standard_normal(n * 32 * P * Q).astype(dt))
+        plain, fused = ctx.alloc(gate.size, dtype), ctx.alloc(gate.size, dtype)
+        ctx.call("cdnn_conv_backward_data", d, hw_, hdy, plain, 0)
+        ctx.call("cdnn_conv_backward_data_ex", d, hw_, hdy, fused, hg, 0)
+        assert np.array_equal(ctx.read(fused), np.where(mask_on.ravel(), ctx.read(plain), 0))
