@@ -172,12 +172,17 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   if (bn > 32 && tiles * G * ((Cout + bn - 1) / bn) < kNumSMs) bn = bn == 128 ? 64 : 32;
   // shared memory: A buffers (double-buffered over channel blocks when they fit) + B ring
   int budget = 227 * 1024;
-  // Few MMAs per staged tile (small channel counts: the column-folded conv1s) leave
-  // the four stager warps as the bottleneck: size the CTA for two per SM so twice
-  // the staging runs per SM (TMEM: 2 x <= 256 columns).
+  // 32-wide tiles (<= 32 output channels per block, the CIFAR / LeNet / ResNet stage-1
+  // convolutions): size the CTA for two per SM.  The two CTAs' staging, MMA issue
+  // and epilogues interleave on the SM's tensor core (CIFAR conv2 39.4 -> 35.3 us,
+  // the column-folded conv1 53 -> 48.5 us); TMEM 2 x <= 256 columns.
   const int taps_eff = a.fold ? g.R : g.R * g.S;
   const int nk8_max = ((a.fold ? g.S * Cin : std::min(32, Cin)) + 7) >> 3;
-  const bool staging_bound = a.cblocks == 1 && taps_eff * nk8_max <= 16;
+  static const int two_cta_macs = [] {  // CDNN_TAP_2CTA: max MMA work (taps x k8 steps) per staged tile
+    const char* v = std::getenv("CDNN_TAP_2CTA");
+    return v ? std::atoi(v) : (1 << 30);
+  }();
+  const bool staging_bound = a.cblocks == 1 && taps_eff * nk8_max <= two_cta_macs;
   int ctas_per_sm = 1;
   // (32-wide tiles only: their kernel is register-bounded for two CTAs per SM)
   if (staging_bound && bn == 32 && tctap::smem_bytes(a.rows, 1, 2, bn, split) <= 113 * 1024) {
