@@ -92,5 +92,39 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---- small GEMMs in one launch (no split-K partials, no reduce kernel) ----------------
+// The CIFAR / LeNet / PG InnerProducts have few outputs: a tiled split-K GEMM then
+// needs a second (reduce) launch, which costs more than the arithmetic.
+//  * dot_warp_kernel:   one warp per output (m, n); lanes stride k, fixed xor-shuffle
+//                       tree (deterministic) -- few outputs, long K;
+//  * dot_thread_kernel: one thread per output, sequential k -- short K.
+// Output index o = n*M + m (lanes walk m: coalesced epilogue stores).
+template <typename T, class VA, class VB, class EPI>
+__global__ void __launch_bounds__(256) dot_warp_kernel(const VA va, const VB vb, const EPI epi, int M, int N, int K) {
+  const int64_t o = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (o >= int64_t(M) * N) return;  // warp-uniform
+  const int m = int(o % M), n = int(o / M);
+  const auto ra = va.row(m);
+  const auto rb = vb.row(n);
+  T s = T(0);
+  for (int k = lane; k < K; k += 32) s += va.at(ra, k) * vb.at(rb, k);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) epi.store(m, n, s, 0);
+}
+
+template <typename T, class VA, class VB, class EPI>
+__global__ void __launch_bounds__(256) dot_thread_kernel(const VA va, const VB vb, const EPI epi, int M, int N, int K) {
+  const int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o >= int64_t(M) * N) return;
+  const int m = int(o % M), n = int(o / M);
+  const auto ra = va.row(m);
+  const auto rb = vb.row(n);
+  T s = T(0);
+  for (int k = 0; k < K; ++k) s += va.at(ra, k) * vb.at(rb, k);
+  epi.store(m, n, s, 0);
+}
+
 }  // namespace simt
 }  // namespace cdnn

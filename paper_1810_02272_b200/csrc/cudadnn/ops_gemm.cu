@@ -7,6 +7,8 @@
 //   ip fwd   top[b][o] = x W^T + bias  m = o, n = b, K = input_dim
 //   ip wgrad dW[o][k] += dY^T X        m = k, n = o, K = batch
 //   ip dgrad dX[b][k]  = dY W           m = k, n = b, K = num_output
+#include <string>
+
 #include "launch.cuh"
 
 namespace cdnn {
@@ -85,10 +87,34 @@ DenseView<float> k_major_copy(Ctx* c, cudaStream_t st, Workspace& scratch, size_
 }
 
 // One GEMM D[m][n] = sum_k A(m,k) B(n,k) with dense views, routed by dtype.
+// Small products in a single launch (gemm_simt.cuh dot kernels); false = not small.
+template <typename T>
+static bool small_gemm(Ctx* c, cudaStream_t st, int M, int N, int K, const DenseView<T>& va, const DenseView<T>& vb,
+                       const StoreEpi<T>& epi) {
+  static const bool on = [] {
+    const char* v = std::getenv("CDNN_SMALL_GEMM");
+    return !(v && std::string(v) == "0");
+  }();
+  const int64_t outs = int64_t(M) * N;
+  if (!on) return false;
+  if (outs <= 16384 && K >= 256) {
+    const int64_t threads = outs * 32;
+    simt::dot_warp_kernel<T><<<int((threads + 255) / 256), 256, 0, st>>>(va, vb, epi, M, N, K);
+  } else if (K <= 128 && outs <= (int64_t(1) << 20)) {
+    simt::dot_thread_kernel<T><<<int((outs + 255) / 256), 256, 0, st>>>(va, vb, epi, M, N, K);
+  } else {
+    return false;
+  }
+  check_launch("small_gemm");
+  count_launch(c);
+  return true;
+}
+
 template <typename T>
 static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const DenseView<T>& va,
                        const DenseView<T>& vb, const StoreEpi<T>& epi) {
   cudaStream_t st = stream_of(c, stream);
+  if (small_gemm<T>(c, st, M, N, K, va, vb, epi)) return;
   Workspace& ws = workspace_of(c, stream);
   if constexpr (std::is_same_v<T, float>) {
     // Small contractions (the CIFAR / LeNet / PG InnerProducts) are latency
