@@ -212,6 +212,9 @@ CDNN_API int cdnn_dispatch(cdnn_ctx ctx, int function_index, const double* args,
 /* ---- BLAS-like kernels (backend.cpp:131-197) ------------------------------ */
 CDNN_API int cdnn_fill(cdnn_ctx ctx, cdnn_handle dst, uint64_t n, double value, cdnn_handle stream);
 CDNN_API int cdnn_copy(cdnn_ctx ctx, cdnn_handle src, cdnn_handle dst, uint64_t n, cdnn_handle stream);
+/* dst[dst_offset .. +n) = src[src_offset .. +n) on the stream (device to device, capturable) */
+CDNN_API int cdnn_copy_range(cdnn_ctx ctx, cdnn_handle src, uint64_t src_offset, cdnn_handle dst,
+                             uint64_t dst_offset, uint64_t n, cdnn_handle stream);
 CDNN_API int cdnn_scal(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cdnn_handle stream);
 CDNN_API int cdnn_axpy(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cdnn_handle y,
                        cdnn_handle stream);

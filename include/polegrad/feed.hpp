@@ -52,7 +52,8 @@ class FeedRing {
     real* labels = nullptr;
     real* loss = nullptr;
     cdnn_handle graph = 0;
-    cdnn_handle done = 0;  // event recorded after the slot's step
+    cdnn_handle done = 0;     // event recorded after the slot's step
+    cdnn_handle staged = 0;   // device copy of the slot's batch (data, then labels)
   };
   Slot& acquire();
   void launch(Slot& s);
@@ -60,6 +61,7 @@ class FeedRing {
   Solver& solver_;
   std::vector<Slot> slots_;
   std::size_t data_len_ = 0, label_len_ = 0, batch_ = 0;
+  cdnn_handle copy_stream_ = 0;  // H2D of the next batches, overlapping the running step
   std::uint64_t pushed_ = 0, popped_ = 0;
 };
 

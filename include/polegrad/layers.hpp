@@ -227,6 +227,8 @@ class MemoryDataLayer final : public Layer {
   // into the top blobs asynchronously; they are consumed by the next forward
   // instead of the FIFO.
   void set_batch(Blob& data_top, Blob* label_top, const real* data, const real* labels);
+  // device-resident batch: `staged` holds the data then the labels (see Net::set_batch_device)
+  void set_batch_device(Blob& data_top, Blob* label_top, cdnn_handle staged);
   bool has_staged_batch() const { return staged_; }
   void clear_staged() { staged_ = false; }
   void mark_staged() { staged_ = true; }

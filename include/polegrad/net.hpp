@@ -72,6 +72,9 @@ class Net {
   const std::vector<Blob*>& loss_blobs() const { return loss_tops_; }
   // Stage one batch into the first MemoryData layer (see MemoryDataLayer::set_batch).
   void set_batch(const real* data, const real* labels = nullptr);
+  // Same from a device buffer holding the batch's data followed by its labels (a
+  // device-to-device copy, capturable; used by the feed ring's staged slots).
+  void set_batch_device(cdnn_handle staged);
   // Flat arenas: params()[i] data/diff are views at param_offset(i).
   Handle weight_arena() const { return weight_arena_; }
   Handle grad_arena() const { return grad_arena_; }

@@ -323,6 +323,23 @@ int cdnn_fill(cdnn_ctx ctx, cdnn_handle dst, uint64_t n, double value, cdnn_hand
   });
 }
 
+int cdnn_copy_range(cdnn_ctx ctx, cdnn_handle src, uint64_t src_offset, cdnn_handle dst, uint64_t dst_offset,
+                    uint64_t n, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    BufferSlot& S = buffer(c, src, "copy_range");
+    BufferSlot& D = buffer(c, dst, "copy_range");
+    require_dtype(D, S.dtype, "copy_range");
+    require_len(S, src_offset + n, "copy_range src");
+    require_len(D, dst_offset + n, "copy_range dst");
+    if (n == 0) return;
+    DeviceGuard g(c);
+    const size_t es = dtype_size(S.dtype);
+    CDNN_CUDA(cudaMemcpyAsync(static_cast<char*>(D.dev) + dst_offset * es, static_cast<const char*>(S.dev) + src_offset * es,
+                              n * es, cudaMemcpyDeviceToDevice, stream_of(c, stream)));
+  });
+}
+
 int cdnn_copy(cdnn_ctx ctx, cdnn_handle src, cdnn_handle dst, uint64_t n, cdnn_handle stream) {
   return guarded([&] {
     Ctx* c = need_ctx(ctx);

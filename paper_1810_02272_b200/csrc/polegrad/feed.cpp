@@ -28,7 +28,9 @@ FeedRing::FeedRing(Net& net, Solver& solver, int depth) : net_(net), solver_(sol
       s.loss = s.data + data_len_ + label_len_;
       std::memset(p, 0, (data_len_ + label_len_ + 1) * sizeof(real));
       cdnn_ok(cdnn_event_create(ctx, &s.done), "feed ring");
+      cdnn_ok(cdnn_alloc(ctx, data_len_ + label_len_, kRealDtype, &s.staged), "feed ring");
     }
+    cdnn_ok(cdnn_stream_create(ctx, &copy_stream_), "feed ring");
     // One eager forward/backward on a zero batch creates every lazily allocated
     // resource (workspaces, tensor maps, repacked weights) outside the capture;
     // its gradients are discarded and the solver history is allocated without
@@ -41,10 +43,12 @@ FeedRing::FeedRing(Net& net, Solver& solver, int depth) : net_(net), solver_(sol
     solver.prepare(net);
     reg.synchronize();
     for (Slot& s : slots_) {
-      // capture: H2D(slot) -> forward -> backward -> update -> D2H(loss)
+      // capture: D2D(slot's staged batch) -> forward -> backward -> update -> D2H(loss).
+      // The slot's H2D runs on the copy stream at push time, overlapping the step
+      // in flight (push() orders the graph after it).
       cdnn_ok(cdnn_graph_begin(ctx, reg.stream()), "feed ring capture");
       try {
-        net.set_batch(s.data, s.labels);
+        net.set_batch_device(s.staged);
         net.forward();
         net.backward();
         solver.apply_update(net);
@@ -72,10 +76,13 @@ void FeedRing::release() noexcept {
   for (Slot& s : slots_) {
     if (s.graph) cdnn_graph_free(reg.context(), s.graph);
     if (s.done) cdnn_event_free(reg.context(), s.done);
+    if (s.staged) cdnn_free(reg.context(), s.staged);
     if (s.data) cdnn_host_free_pinned(s.data);
     s = Slot{};
   }
   slots_.clear();
+  if (copy_stream_) cdnn_stream_free(reg.context(), copy_stream_);
+  copy_stream_ = 0;
 }
 
 FeedRing::Slot& FeedRing::acquire() {
@@ -86,7 +93,13 @@ FeedRing::Slot& FeedRing::acquire() {
 
 void FeedRing::launch(Slot& s) {
   Registry& reg = *net_.registry();
-  cdnn_ok(cdnn_graph_launch(reg.context(), s.graph, reg.stream()), "feed ring push");
+  cdnn_ctx ctx = reg.context();
+  // H2D of this slot's batch on the copy stream (the slot's previous step has
+  // finished -- acquire() -- so nothing still reads its staged buffer), then the
+  // step, ordered after the copy
+  cdnn_ok(cdnn_write_async(ctx, s.staged, 0, s.data, data_len_ + label_len_, copy_stream_), "feed ring push");
+  cdnn_ok(cdnn_stream_wait(ctx, reg.stream(), copy_stream_), "feed ring push");
+  cdnn_ok(cdnn_graph_launch(ctx, s.graph, reg.stream()), "feed ring push");
   cdnn_ok(cdnn_event_record(reg.context(), s.done, reg.stream()), "feed ring push");
   ++pushed_;
   solver_.uncount_updates(-1);  // one real update

@@ -285,6 +285,18 @@ void MemoryDataLayer::set_batch(Blob& data_top, Blob* label_top, const real* dat
   staged_ = true;
 }
 
+void MemoryDataLayer::set_batch_device(Blob& data_top, Blob* label_top, cdnn_handle staged) {
+  Registry& reg = data_top.registry();
+  const std::size_t n = std::size_t(batch_size_) * sample_size_;
+  cdnn_ok(cdnn_copy_range(reg.context(), staged, 0, data_top.overwrite_gpu_data(), 0, n, reg.stream()),
+          "set_batch_device data");
+  if (label_top)
+    cdnn_ok(cdnn_copy_range(reg.context(), staged, n, label_top->overwrite_gpu_data(), 0, std::size_t(batch_size_),
+                            reg.stream()),
+            "set_batch_device labels");
+  staged_ = true;
+}
+
 void MemoryDataLayer::forward(std::span<Blob* const>, std::span<Blob* const> tops) {
   if (staged_) {  // batch already in HBM (set_batch); consumed by this forward
     staged_ = false;

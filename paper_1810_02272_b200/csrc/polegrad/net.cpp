@@ -386,6 +386,16 @@ void Net::set_batch(const real* data, const real* labels) {
   throw ModelError("set_batch: net has no MemoryData layer");
 }
 
+void Net::set_batch_device(cdnn_handle staged) {
+  for (std::size_t i = 0; i < layers_.size(); ++i) {
+    if (auto* md = dynamic_cast<MemoryDataLayer*>(layers_[i].get())) {
+      md->set_batch_device(*tops_[i][0], tops_[i].size() > 1 ? tops_[i][1] : nullptr, staged);
+      return;
+    }
+  }
+  throw ModelError("set_batch_device: net has no MemoryData layer");
+}
+
 void Net::pg_backward(const std::string& logit_blob, const std::string& prob_blob, std::span<const real> actions,
                       std::span<const real> returns, bool sigmoid) {
   Blob& logit = blob(logit_blob);

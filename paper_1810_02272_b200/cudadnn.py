@@ -46,7 +46,7 @@ EXPORTS = [
     "cdnn_relu_backward", "cdnn_sigmoid_forward", "cdnn_sigmoid_backward", "cdnn_softmax_forward",
     "cdnn_softmax_backward", "cdnn_softmax_loss_forward", "cdnn_softmax_loss_backward", "cdnn_solver_apply",
     "cdnn_nccl_available", "cdnn_nccl_unique_id", "cdnn_nccl_comm_create", "cdnn_allreduce_sum",
-    "cdnn_broadcast", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_lrn_backward_ex", "cdnn_dropout", "cdnn_counter_increment",
+    "cdnn_broadcast", "cdnn_copy_range", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_lrn_backward_ex", "cdnn_dropout", "cdnn_counter_increment",
     "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
     "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
     "cdnn_pool_forward_ex", "cdnn_pg_diff",
@@ -111,6 +111,7 @@ def load() -> C.CDLL:
             "cdnn_pool_output_shape": ([vp, h, C.POINTER(i)], i), "cdnn_desc_free": ([vp, h], i),
             "cdnn_dispatch": ([vp, i, C.POINTER(d), u64, C.POINTER(d), pu64], i),
             "cdnn_fill": ([vp, h, u64, d, h], i), "cdnn_copy": ([vp, h, h, u64, h], i),
+            "cdnn_copy_range": ([vp, h, u64, h, u64, u64, h], i),
             "cdnn_scal": ([vp, u64, d, h, h], i), "cdnn_axpy": ([vp, u64, d, h, h, h], i),
             "cdnn_dot": ([vp, u64, h, h, C.POINTER(d)], i),
             "cdnn_gemm": ([vp, i, i, i, i, i, d, h, h, d, h, h], i),
