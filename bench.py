@@ -374,12 +374,22 @@ def run_b200(args) -> None:
 
     # ---- e2e: host buffers through the public API (H2D in, loss D2H out, every step)
     # Graph path: polegrad.FeedRing (pinned-memory feed ring):
-    # push() stages batch i+1 into a free pinned slot while step i runs, each
-    # slot's captured step starts with its H2D copy and ends with the loss D2H;
-    # pop_loss() reads every step's loss.
+    # push_pinned() enqueues batch i+1's H2D from page-locked host memory on the
+    # ring's copy stream while step i runs; each slot's captured step starts with a
+    # device copy of its staged batch and ends with the loss D2H; pop_loss() reads
+    # every step's loss.
     e_start, e_end = cx.event(), cx.event()
     if use_graph:
         ring = polegrad.FeedRing(net, solver, 2)
+        # the step inputs sit in page-locked host memory (three batches cycled);
+        # push_pinned enqueues each step's H2D straight from them
+        npin = min(3, nb)
+        pins = []
+        for j in range(npin):
+            px, py = cudadnn.PinnedBuffer((BATCH,) + IMG), cudadnn.PinnedBuffer((BATCH,))
+            px.array[...] = host_x[j]
+            py.array[...] = host_y[j]
+            pins.append((px, py))
 
         def run_ring(n, sink):
             inflight = 0
@@ -387,7 +397,8 @@ def run_b200(args) -> None:
                 if inflight == 2:
                     sink.append(ring.pop_loss())
                     inflight -= 1
-                ring.push(host_x[i % nb], host_y[i % nb])
+                px, py = pins[i % npin]
+                ring.push_pinned(px, py)
                 inflight += 1
             while inflight:
                 sink.append(ring.pop_loss())

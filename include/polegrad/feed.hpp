@@ -34,6 +34,10 @@ class FeedRing {
   // when the feed has no label top) into the next slot and enqueues its step.
   // InvalidState when every slot holds a loss not yet popped.
   void push(std::span<const real> data, std::span<const real> labels);
+  // Zero-copy variant: the batch already sits in page-locked host memory
+  // (cdnn_host_alloc_pinned); its H2D is enqueued straight from there.  The
+  // buffers must stay unchanged until this step's pop_loss().
+  void push_pinned(std::span<const real> data, std::span<const real> labels);
   // Samples one batch from `dataset` (imagedb::Dataset::sample, one draw per image
   // from `rng`) and gathers the tensors and labels straight into the next pinned
   // slot, then enqueues its step.  InvalidArgument when a
@@ -56,7 +60,7 @@ class FeedRing {
     cdnn_handle staged = 0;   // device copy of the slot's batch (data, then labels)
   };
   Slot& acquire();
-  void launch(Slot& s);
+  void launch(Slot& s, const real* data = nullptr, const real* labels = nullptr);
   Net& net_;
   Solver& solver_;
   std::vector<Slot> slots_;

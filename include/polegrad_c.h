@@ -81,6 +81,10 @@ PG_API int pg_feed_ring_create(pg_net* net, pg_solver* s, int depth, pg_feed_rin
 PG_API int pg_feed_ring_free(pg_feed_ring* r);
 PG_API int pg_feed_ring_push(pg_feed_ring* r, const void* data, uint64_t n_data, const void* labels,
                              uint64_t n_labels);
+/* zero-copy push: data/labels are page-locked (cdnn_host_alloc_pinned) and stay
+ * unchanged until this step's loss is popped; the H2D is enqueued from them */
+PG_API int pg_feed_ring_push_pinned(pg_feed_ring* r, const void* data, uint64_t n_data, const void* labels,
+                                    uint64_t n_labels);
 PG_API int pg_feed_ring_pop_loss(pg_feed_ring* r, double* loss);
 /* samples one batch from `db` (method 0 uniform, 1 label-balanced; one draw of
  * `rng` per image, polegrad/imagedb.hpp) straight into the next pinned slot and

@@ -252,6 +252,14 @@ int pg_feed_ring_push(pg_feed_ring* r, const void* data, uint64_t n_data, const 
   });
 }
 
+int pg_feed_ring_push_pinned(pg_feed_ring* r, const void* data, uint64_t n_data, const void* labels,
+                             uint64_t n_labels) {
+  return run([&] {
+    r->ring->push_pinned(std::span<const real>(static_cast<const real*>(data), n_data),
+                         std::span<const real>(static_cast<const real*>(labels), labels ? n_labels : 0));
+  });
+}
+
 int pg_feed_ring_pop_loss(pg_feed_ring* r, double* loss) { return run([&] { *loss = r->ring->pop_loss(); }); }
 
 struct pg_imagedb {

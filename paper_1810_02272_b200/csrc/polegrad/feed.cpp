@@ -91,13 +91,18 @@ FeedRing::Slot& FeedRing::acquire() {
   return slots_[pushed_ % slots_.size()];
 }
 
-void FeedRing::launch(Slot& s) {
+void FeedRing::launch(Slot& s, const real* data, const real* labels) {
   Registry& reg = *net_.registry();
   cdnn_ctx ctx = reg.context();
   // H2D of this slot's batch on the copy stream (the slot's previous step has
   // finished -- acquire() -- so nothing still reads its staged buffer), then the
   // step, ordered after the copy
-  cdnn_ok(cdnn_write_async(ctx, s.staged, 0, s.data, data_len_ + label_len_, copy_stream_), "feed ring push");
+  if (!data) {
+    cdnn_ok(cdnn_write_async(ctx, s.staged, 0, s.data, data_len_ + label_len_, copy_stream_), "feed ring push");
+  } else {
+    cdnn_ok(cdnn_write_async(ctx, s.staged, 0, data, data_len_, copy_stream_), "feed ring push");
+    if (label_len_) cdnn_ok(cdnn_write_async(ctx, s.staged, data_len_, labels, label_len_, copy_stream_), "feed ring push");
+  }
   cdnn_ok(cdnn_stream_wait(ctx, reg.stream(), copy_stream_), "feed ring push");
   cdnn_ok(cdnn_graph_launch(ctx, s.graph, reg.stream()), "feed ring push");
   cdnn_ok(cdnn_event_record(reg.context(), s.done, reg.stream()), "feed ring push");
@@ -126,6 +131,13 @@ void FeedRing::push_sampled(const imagedb::Dataset& dataset, imagedb::SampleMeth
     if (label_len_) s.labels[b] = static_cast<real>(e.label);
   }
   launch(s);
+}
+
+void FeedRing::push_pinned(std::span<const real> data, std::span<const real> labels) {
+  if (data.size() != data_len_) throw InvalidArgument("feed ring: batch has the wrong number of values");
+  if (labels.size() != label_len_) throw InvalidArgument("feed ring: wrong number of labels");
+  Slot& s = acquire();
+  launch(s, data.data(), label_len_ ? labels.data() : nullptr);
 }
 
 double FeedRing::pop_loss() {

@@ -33,7 +33,7 @@ EXPORTS = [
     "pg_net_profile",
     "pg_parallel_unique_id", "pg_parallel_create", "pg_parallel_free", "pg_parallel_broadcast",
     "pg_solver_set_parallel", "pg_plan_buckets", "pg_prototxt_roundtrip", "pg_solver_snapshot",
-    "pg_solver_restore", "pg_solver_iterations", "pg_feed_ring_create", "pg_feed_ring_free", "pg_feed_ring_push",
+    "pg_solver_restore", "pg_solver_iterations", "pg_feed_ring_create", "pg_feed_ring_free", "pg_feed_ring_push", "pg_feed_ring_push_pinned",
     "pg_feed_ring_pop_loss", "pg_net_pg_backward", "pg_feed_ring_push_sampled", "pg_imagedb_load",
     "pg_imagedb_free", "pg_imagedb_size", "pg_imagedb_set_boost", "pg_imagedb_sample", "pg_rng_create",
     "pg_rng_free",
@@ -72,7 +72,8 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_solver_apply": ([vp, vp], i), "pg_solver_snapshot": ([vp, vp, u64, C.POINTER(u64)], i),
             "pg_solver_restore": ([vp, vp, u64], i), "pg_solver_iterations": ([vp, C.POINTER(u64)], i),
             "pg_feed_ring_create": ([vp, vp, i, C.POINTER(vp)], i), "pg_feed_ring_free": ([vp], i),
-            "pg_feed_ring_push": ([vp, vp, u64, vp, u64], i), "pg_feed_ring_pop_loss": ([vp, C.POINTER(d)], i),
+            "pg_feed_ring_push": ([vp, vp, u64, vp, u64], i),
+            "pg_feed_ring_push_pinned": ([vp, vp, u64, vp, u64], i), "pg_feed_ring_pop_loss": ([vp, C.POINTER(d)], i),
             "pg_step_capture": ([vp, vp, vp, vp, vp, C.POINTER(u64)], i), "pg_step_replay": ([vp, u64], i),
             "pg_graph_free": ([vp, u64], i), "pg_parallel_unique_id": ([cp], i),
             "pg_net_profile": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
@@ -361,6 +362,13 @@ class FeedRing:
         _check(self.lib, self.lib.pg_feed_ring_push(self.ptr, x.ctypes.data, x.size,
                                                     None if y is None else y.ctypes.data,
                                                     0 if y is None else y.size))
+
+    def push_pinned(self, data, labels=None) -> None:
+        """Zero-copy push of batches already in page-locked memory (cudadnn.PinnedBuffer):
+        the H2D is enqueued from them; keep them unchanged until this step's pop_loss()."""
+        _check(self.lib, self.lib.pg_feed_ring_push_pinned(self.ptr, data.ptr, data.array.size,
+                                                           None if labels is None else labels.ptr,
+                                                           0 if labels is None else labels.array.size))
 
     def push_sampled(self, db: "ImageDB", rng: "Rng", method: str = "uniform", use_boost: bool = False) -> None:
         """Samples one batch from `db` (one `rng` draw per image) and gathers it

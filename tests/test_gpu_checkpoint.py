@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from parity_util import CONFIGS, data_shape, polegrad, synthetic_batches
+from paper_1810_02272_b200 import cudadnn
 
 pytestmark = pytest.mark.gpu
 
@@ -62,9 +63,12 @@ def test_restore_rejects_other_rule():
         other.restore(blob)
 
 
+@pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("depth", [1, 2, 3])
-def test_feed_ring_matches_eager_steps(depth):
-    """The pinned feed ring trains exactly like eager steps."""
+def test_feed_ring_matches_eager_steps(depth, pinned):
+    """The pinned feed ring trains exactly like eager steps, with
+    host batches copied into its slots (push) or enqueued from the caller's pinned
+    buffers (push_pinned, zero-copy)."""
     text = polegrad.load_model("cifar10_quick")
     batches = synthetic_batches((100, 3, 32, 32), 10, 6, seed=8)
     kw = CONFIGS["cifar10_quick"][1]
@@ -80,12 +84,19 @@ def test_feed_ring_matches_eager_steps(depth):
         a.backward()
         sa.apply()
     ring = polegrad.FeedRing(b, sb, depth)
-    got, inflight = [], 0
+    got, inflight, keep = [], 0, []
     for x, y in batches:
         if inflight == depth:
             got.append(ring.pop_loss())
             inflight -= 1
-        ring.push(x, y)
+        if pinned:
+            px, py = cudadnn.PinnedBuffer(x.shape), cudadnn.PinnedBuffer(y.shape)
+            px.array[...] = x
+            py.array[...] = y
+            keep.append((px, py))  # unchanged until the step's loss is popped
+            ring.push_pinned(px, py)
+        else:
+            ring.push(x, y)
         inflight += 1
     while inflight:
         got.append(ring.pop_loss())
