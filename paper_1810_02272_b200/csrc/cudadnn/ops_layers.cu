@@ -199,8 +199,10 @@ __global__ void lrn_bwd_ring(const T* __restrict__ x, const T* __restrict__ y, c
 #pragma unroll
         for (int j = 0; j < SIZE; ++j) acc += tr[j];
         const T g = dyr[post] * neg_pow(scr[post], beta) - coef * xv[u] * acc;
-        // fused backward of an in-place ReLU on this layer's bottom (gate = its data)
-        dx[base + int64_t(c) * HW] = (gate && !(__ldg(gate + base + int64_t(c) * HW) > T(0))) ? T(0) : g;
+        // fused backward of an in-place ReLU on this layer's bottom (gate = its data:
+        // normally the very buffer x, whose value is already in a register)
+        const bool open = !gate || (gate == x ? xv[u] > T(0) : __ldg(gate + base + int64_t(c) * HW) > T(0));
+        dx[base + int64_t(c) * HW] = open ? g : T(0);
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; scr[j] = scr[j + 1]; }
         dyr[SIZE - 1] = ndy[u];

@@ -7,6 +7,8 @@
 // AVE: Caffe's divisor counts padded positions but not the overhang past
 //      H+pad; backward spreads top_diff/pool_size over the clipped window.
 // One thread per output (forward) / input (backward) element; NCHW planes.
+#include <cstdlib>
+
 #include "launch.cuh"
 
 namespace cdnn {
@@ -88,6 +90,47 @@ __global__ void __launch_bounds__(256) max_pool_bwd(const T* __restrict__ dy, co
   }
 }
 
+// Fixed-window MAX backward: one bottom element per thread, consecutive threads on
+// consecutive columns (coalesced gate loads and dx stores); at most R = ceil(K/S)
+// windows per dimension cover an element, visited in the same (ph, pw) order as
+// max_pool_bwd, so the sums are bit-identical.  The kernel is latency-bound (a
+// resident thread walks ~250 AlexNet pool1 elements), so every load of an element
+// -- gate, the R*R mask entries and the R*R top diffs -- is issued at once: one
+// memory round trip per element instead of gate -> mask -> diff in series.
+template <typename T, int K, int S>
+__global__ void __launch_bounds__(256) max_pool_bwd_k(const T* __restrict__ dy, const int* __restrict__ mask,
+                                                      T* __restrict__ dx, PoolGeom g, uint32_t total,
+                                                      const T* __restrict__ gate) {
+  constexpr int R = (K + S - 1) / S;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, g.divHW, g.divW, uint32_t(g.H * g.W), uint32_t(g.W));
+    const int h = int(q.h) + g.ph, w = int(q.w) + g.pw;
+    const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
+    const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
+    const int me = int(q.h) * g.W + int(q.w);
+    const size_t base = size_t(q.plane) * uint32_t(g.PH * g.PW);
+    const bool open = !gate || __ldg(gate + i) > T(0);
+    int m[R][R];
+    T v[R][R];
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        const bool ok = phs + a < phe && pws + b < pwe;
+        const size_t o = base + (phs + a) * g.PW + pws + b;
+        m[a][b] = ok ? __ldg(mask + o) : -1;
+        v[a][b] = ok ? __ldg(dy + o) : T(0);
+      }
+    T s = T(0);
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b)
+        if (m[a][b] == me) s += v[a][b];
+    dx[i] = open ? s : T(0);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) ave_pool_fwd(const T* __restrict__ x, T* __restrict__ y, PoolGeom g,
                                                     uint32_t total, bool relu) {
@@ -127,6 +170,82 @@ __global__ void __launch_bounds__(256) ave_pool_bwd(const T* __restrict__ dy, T*
       }
     dx[i] = (gate && !(__ldg(gate + i) > T(0))) ? T(0) : s;
   }
+}
+
+// Fixed-window AVE pooling: unrolled K x K window, same h-major summation order
+// and Caffe divisor (padded positions counted, overhang past H+pad not) as
+// ave_pool_fwd, so outputs are bit-identical.
+template <typename T, int K, int S>
+__global__ void __launch_bounds__(256) ave_pool_fwd_k(const T* __restrict__ x, T* __restrict__ y, PoolGeom g,
+                                                      uint32_t total, bool relu) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, g.divPHW, g.divPW, uint32_t(g.PH * g.PW), uint32_t(g.PW));
+    const int hs = int(q.h) * S - g.ph, ws = int(q.w) * S - g.pw;
+    const int pool = (min(hs + K, g.H + g.ph) - hs) * (min(ws + K, g.W + g.pw) - ws);
+    const T* plane = x + size_t(q.plane) * uint32_t(g.H * g.W);
+    T v[K][K];
+    bool ok[K][K];
+#pragma unroll
+    for (int a = 0; a < K; ++a)
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const int h = hs + a, w = ws + b;
+        ok[a][b] = h >= 0 && h < g.H && w >= 0 && w < g.W;
+        v[a][b] = ok[a][b] ? __ldg(plane + h * g.W + w) : T(0);
+      }
+    T s = T(0);
+#pragma unroll
+    for (int a = 0; a < K; ++a)
+#pragma unroll
+      for (int b = 0; b < K; ++b)
+        if (ok[a][b]) s += v[a][b];
+    const T r = s / T(pool);
+    y[i] = relu ? (r > T(0) ? r : T(0)) : r;
+  }
+}
+
+// Fixed-window AVE backward: one bottom element per thread, at most ceil(K/S)^2
+// covering windows, visited in ave_pool_bwd's (ph, pw) order (bit-identical sums).
+template <typename T, int K, int S>
+__global__ void __launch_bounds__(256) ave_pool_bwd_k(const T* __restrict__ dy, T* __restrict__ dx, PoolGeom g,
+                                                      uint32_t total, const T* __restrict__ gate) {
+  constexpr int R = (K + S - 1) / S;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, g.divHW, g.divW, uint32_t(g.H * g.W), uint32_t(g.W));
+    const int h = int(q.h) + g.ph, w = int(q.w) + g.pw;
+    const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
+    const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
+    const size_t base = size_t(q.plane) * uint32_t(g.PH * g.PW);
+    const bool open = !gate || __ldg(gate + i) > T(0);
+    T v[R][R];
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b)
+        v[a][b] = (phs + a < phe && pws + b < pwe) ? __ldg(dy + base + (phs + a) * g.PW + pws + b) : T(0);
+    T s = T(0);
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b)
+        if (phs + a < phe && pws + b < pwe) {
+          const int hs0 = (phs + a) * S - g.ph, ws0 = (pws + b) * S - g.pw;
+          const int pool = (min(hs0 + K, g.H + g.ph) - hs0) * (min(ws0 + K, g.W + g.pw) - ws0);
+          s += v[a][b] / T(pool);
+        }
+    dx[i] = open ? s : T(0);
+  }
+}
+
+// 32 / 22 for square 3x3 / 2x2 windows of stride 2 (the unrolled kernels, MAX and
+// AVE), else 0; CDNN_POOL_GENERIC=1 forces the dynamic-window kernels (A/B checks)
+int fixed_window(const PoolGeom& g) {
+  static const bool generic = [] {
+    const char* e = std::getenv("CDNN_POOL_GENERIC");
+    return e && e[0] == '1';
+  }();
+  if (generic || g.sh != 2 || g.sw != 2 || g.kh != g.kw) return 0;
+  return g.kh == 3 ? 32 : g.kh == 2 ? 22 : 0;
 }
 
 PoolGeom geom_of(const PoolDescSlot& d) {
@@ -172,12 +291,19 @@ int cdnn_pool_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_han
     const int blocks = grid_for(int64_t(nout), 256);
     auto run = [&](auto tag) {
       using T = decltype(tag);
-      if (d.p.method == CDNN_POOL_MAX)
-        max_pool_fwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(X.dev), reinterpret_cast<T*>(Y.dev),
-                                                 M ? reinterpret_cast<int*>(M->dev) : nullptr, g, uint32_t(nout), relu);
-      else
-        ave_pool_fwd<T><<<blocks, 256, 0, st>>>(reinterpret_cast<const T*>(X.dev), reinterpret_cast<T*>(Y.dev), g,
-                                                 uint32_t(nout), relu);
+      const T* xp = reinterpret_cast<const T*>(X.dev);
+      T* yp = reinterpret_cast<T*>(Y.dev);
+      int* mp = M ? reinterpret_cast<int*>(M->dev) : nullptr;
+      if (d.p.method == CDNN_POOL_MAX) {
+        // (an unrolled 3x3/2 variant measured slower: AlexNet pool1 158 vs 148 us)
+        max_pool_fwd<T><<<blocks, 256, 0, st>>>(xp, yp, mp, g, uint32_t(nout), relu);
+      } else {
+        switch (fixed_window(g)) {
+          case 32: ave_pool_fwd_k<T, 3, 2><<<blocks, 256, 0, st>>>(xp, yp, g, uint32_t(nout), relu); break;
+          case 22: ave_pool_fwd_k<T, 2, 2><<<blocks, 256, 0, st>>>(xp, yp, g, uint32_t(nout), relu); break;
+          default: ave_pool_fwd<T><<<blocks, 256, 0, st>>>(xp, yp, g, uint32_t(nout), relu);
+        }
+      }
     };
     if (X.dtype == CDNN_F32) run(float{});
     else if (X.dtype == CDNN_F64) run(double{});
@@ -217,7 +343,18 @@ int cdnn_pool_backward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_h
     const int blocks = grid_for(int64_t(nin), 256);
     auto run = [&](auto tag) {
       using T = decltype(tag);
-      if (d.p.method == CDNN_POOL_MAX) {
+      const int fw = fixed_window(g);
+      const T* dyp = reinterpret_cast<const T*>(DY.dev);
+      T* dxp = reinterpret_cast<T*>(DX.dev);
+      const T* gp = G ? reinterpret_cast<const T*>(G->dev) : nullptr;
+      if (fw && d.p.method == CDNN_POOL_MAX) {
+        const int* mp = reinterpret_cast<const int*>(M->dev);
+        if (fw == 32) max_pool_bwd_k<T, 3, 2><<<blocks, 256, 0, st>>>(dyp, mp, dxp, g, uint32_t(nin), gp);
+        else max_pool_bwd_k<T, 2, 2><<<blocks, 256, 0, st>>>(dyp, mp, dxp, g, uint32_t(nin), gp);
+      } else if (fw) {
+        if (fw == 32) ave_pool_bwd_k<T, 3, 2><<<blocks, 256, 0, st>>>(dyp, dxp, g, uint32_t(nin), gp);
+        else ave_pool_bwd_k<T, 2, 2><<<blocks, 256, 0, st>>>(dyp, dxp, g, uint32_t(nin), gp);
+      } else if (d.p.method == CDNN_POOL_MAX) {
         const uint64_t n4 = uint64_t(g.N) * g.C * g.H * ((g.W + 3) / 4);
         max_pool_bwd<T><<<grid_for(int64_t(n4), 256), 256, 0, st>>>(
             reinterpret_cast<const T*>(DY.dev), reinterpret_cast<const int*>(M->dev), reinterpret_cast<T*>(DX.dev), g,

@@ -95,6 +95,8 @@ CONV_CASES = [
     (2, 32, 16, 16, 32, 5, 1, 2, 1, 1),     # CIFAR-quick conv2
     (2, 32, 8, 8, 64, 5, 1, 2, 1, 1),       # CIFAR-quick conv3
     (2, 3, 35, 35, 16, 11, 4, 0, 1, 1),     # AlexNet conv1 shape (small)
+    (2, 2, 31, 30, 16, 7, 2, 3, 1, 1),      # space-to-depth stem: padded, ragged, s = 2
+    (2, 1, 37, 40, 16, 9, 8, 1, 1, 1),      # space-to-depth stem: s = 8 phases per input row
     (2, 8, 13, 13, 12, 3, 1, 1, 1, 2),      # grouped
     (2, 16, 15, 15, 32, 3, 2, 1, 1, 1),     # ResNet downsample
     (2, 4, 9, 9, 8, 3, 1, 2, 2, 1),         # dilation
@@ -389,3 +391,47 @@ def test_fused_relu_gate_backward(ctx, dtype):
         ctx.call("cdnn_conv_backward_data", d, hw_, hdy, plain, 0)
         ctx.call("cdnn_conv_backward_data_ex", d, hw_, hdy, fused, hg, 0)
         assert np.array_equal(ctx.read(fused), np.where(mask_on.ravel(), ctx.read(plain), 0))
+
+
+_POOL_DIGEST = r'''
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1810_02272_b200 import cudadnn as cd
+ctx = cd.Context(0)
+h = hashlib.sha1()
+for dtype, dt in ((cd.F32, np.float32), (cd.F64, np.float64)):
+    for n, c, H, W, k, s, p in ((3, 5, 55, 55, 3, 2, 0), (2, 4, 13, 13, 3, 2, 1), (2, 3, 24, 24, 2, 2, 0),
+                                (2, 3, 7, 9, 2, 2, 1), (1, 2, 32, 32, 3, 2, 0)):
+        rng = np.random.default_rng(n * H + W)
+        x = np.round(rng.standard_normal(n * c * H * W), 1).astype(dt)   # ties: first maximum must win
+        for method in (cd.POOL_MAX, cd.POOL_AVE):
+            d = ctx.pool_desc(n, c, H, W, method, k, s, p)
+            P, Q = ctx.pool_output_shape(d)[2:]
+            hx, hy, hm = ctx.upload(x), ctx.alloc(n * c * P * Q, dtype), ctx.alloc(n * c * P * Q, cd.I32)
+            ctx.call("cdnn_pool_forward", d, hx, hy, hm, 0)
+            hdy = ctx.upload(rng.standard_normal(n * c * P * Q).astype(dt))
+            hdx, hdg = ctx.alloc(x.size, dtype), ctx.alloc(x.size, dtype)
+            ctx.call("cdnn_pool_backward", d, hdy, hm, hdx, 0)
+            ctx.call("cdnn_pool_backward_ex", d, hdy, hm, hdg, hx, 0)
+            for o in (hy, hm, hdx, hdg):
+                h.update(ctx.read(o).tobytes())
+print(h.hexdigest())
+'''
+
+
+def test_pool_fixed_window_kernels_equal_generic():
+    """The unrolled 3x3/2 and 2x2/2 MAX / AVE kernels (default) produce the same bytes as the
+    dynamic-window kernels (CDNN_POOL_GENERIC=1): outputs, argmax masks, gated and
+    plain backward, float and double, padded and ragged planes, tied maxima."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for generic in ("0", "1"):
+        env = dict(os.environ, CDNN_POOL_GENERIC=generic)
+        r = subprocess.run([sys.executable, "-c", _POOL_DIGEST, root], env=env, capture_output=True, text=True,
+                           timeout=300, check=True)
+        out[generic] = r.stdout.strip().splitlines()[-1]
+    assert out["0"] == out["1"]
