@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(256) dot_warp_kernel(const VA va, const VB vb,
   const auto ra = va.row(m);
   const auto rb = vb.row(n);
   T s = T(0);
+#pragma unroll 8  // loads of eight k-steps in flight; the summation order is unchanged
   for (int k = lane; k < K; k += 32) s += va.at(ra, k) * vb.at(rb, k);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(256) dot_thread_kernel(const VA va, const VB v
   const auto ra = va.row(m);
   const auto rb = vb.row(n);
   T s = T(0);
+#pragma unroll 16  // latency-bound: sixteen k-steps of loads in flight, same summation order
   for (int k = 0; k < K; ++k) s += va.at(ra, k) * vb.at(rb, k);
   epi.store(m, n, s, 0);
 }

@@ -97,7 +97,7 @@ static bool small_gemm(Ctx* c, cudaStream_t st, int M, int N, int K, const Dense
   }();
   const int64_t outs = int64_t(M) * N;
   if (!on) return false;
-  if (outs <= 16384 && K >= 256) {
+  if (outs <= 16384 && K >= 64) {  // few outputs: a warp per output (CIFAR ip2 dW 640 x K=100: 29 -> ~3 us)
     const int64_t threads = outs * 32;
     simt::dot_warp_kernel<T><<<int((threads + 255) / 256), 256, 0, st>>>(va, vb, epi, M, N, K);
   } else if (K <= 128 && outs <= (int64_t(1) << 20)) {
