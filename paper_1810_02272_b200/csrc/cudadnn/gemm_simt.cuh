@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) dot_warp_kernel(const VA va, const VB vb,
   if (lane == 0) epi.store(m, n, s, 0);
 }
 
-template <typename T, class VA, class VB, class EPI>
+template <typename T, int UNROLL, class VA, class VB, class EPI>
 __global__ void __launch_bounds__(256) dot_thread_kernel(const VA va, const VB vb, const EPI epi, int M, int N, int K) {
   const int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (o >= int64_t(M) * N) return;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) dot_thread_kernel(const VA va, const VB v
   const auto ra = va.row(m);
   const auto rb = vb.row(n);
   T s = T(0);
-#pragma unroll 16  // latency-bound: sixteen k-steps of loads in flight, same summation order
+#pragma unroll UNROLL  // few threads: latency-bound, UNROLL k-steps of loads in flight (same summation order)
   for (int k = 0; k < K; ++k) s += va.at(ra, k) * vb.at(rb, k);
   epi.store(m, n, s, 0);
 }

@@ -510,11 +510,37 @@ float* s2d_buffer(Ctx* c, const ConvDescSlot& dconst, int which, size_t elems) {
   return static_cast<float*>(b->ptr);
 }
 
+// One warp-strided sweep per X' row (n, cc, h'): lanes walk w' (stores coalesced,
+// loads a stride-s run of one input row); 32-bit index math (X' < 2^31 elements).
+// Used for s < 4 (ResNet 3x3/2 downsampling: measured faster there than the
+// grouped kernel below, 64 vs 71 us for res2_0 forward).
+__global__ void s2d_input_rows_kernel(const float* __restrict__ x, float* __restrict__ xs, ConvGeom g, ConvGeom h) {
+  const int s = g.sh;
+  const int rows = h.N * h.C * h.H;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const int h2 = row % h.H;
+    const int cc = (row / h.H) % h.C;
+    const int n = row / (h.H * h.C);
+    const int c = cc % g.C, ph = cc / g.C, dy = ph / s, dx = ph % s;
+    const int y = s * h2 + dy - g.ph;
+    float* out = xs + size_t(row) * h.W;
+    const bool yok = y >= 0 && y < g.H;
+    const float* in = x + (size_t(n) * g.C + c) * g.H * g.W + size_t(yok ? y : 0) * g.W;
+    for (int w2 = lane; w2 < h.W; w2 += 32) {
+      const int xx = s * w2 + dx - g.pw;
+      out[w2] = (yok && xx >= 0 && xx < g.W) ? __ldg(in + xx) : 0.f;
+    }
+  }
+}
+
 // One warp per X' row group (n, c, dy, h'): the s rows X'[n][(dy*s + dx)*C + c][h']
 // for dx = 0..s-1 all come from input row y = s*h' + dy - pad, so a lane issues
 // the s loads of its w' together (they cover one contiguous run of the input row:
 // every line is used by the group) before the s coalesced stores; one index
-// decomposition per group, s x the loads in flight of a row-per-warp sweep.
+// decomposition per group, s x the loads in flight of a row-per-warp sweep
+// (AlexNet conv1, s = 4: 335 -> 145 us).
 __global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict__ xs, ConvGeom g, ConvGeom h) {
   const int s = g.sh;
   const int groups = h.N * g.C * s * h.H;
@@ -544,6 +570,13 @@ __global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict_
           if (d0 + j < s) out[(d0 + j) * step + w2] = v[j];
       }
   }
+}
+
+void s2d_input(const float* x, float* xs, const ConvGeom& g, const ConvGeom& h, cudaStream_t st) {
+  if (g.sh >= 4)
+    s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32 / g.sh, 256), 256, 0, st>>>(x, xs, g, h);
+  else
+    s2d_input_rows_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32, 256), 256, 0, st>>>(x, xs, g, h);
 }
 
 __global__ void s2d_weight_kernel(const float* __restrict__ w, float* __restrict__ ws, ConvGeom g, ConvGeom h) {
@@ -593,7 +626,7 @@ bool conv_wgrad_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   cudaStream_t st = stream_of(c, stream);
   float* xs = s2d_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
   float* dws = s2d_buffer(c, d, 3, size_t(h.Co) * h.C * h.R * h.S);
-  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32 / g.sh, 256), 256, 0, st>>>(x, xs, g, h);
+  s2d_input(x, xs, g, h, st);
   CDNN_CUDA(cudaMemsetAsync(dws, 0, size_t(h.Co) * h.C * h.R * h.S * 4, st));
   check_launch("s2d");
   count_launch(c);
@@ -631,7 +664,7 @@ bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float
   cudaStream_t st = stream_of(c, stream);
   float* xs = s2d_buffer(c, d, 0, size_t(h.N) * h.C * h.H * h.W);
   float* wsb = s2d_buffer(c, d, 1, size_t(h.Co) * h.C * h.R * h.S);
-  s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32 / g.sh, 256), 256, 0, st>>>(x, xs, g, h);
+  s2d_input(x, xs, g, h, st);
   s2d_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R * h.S, 256), 256, 0, st>>>(w, wsb, g, h);
   check_launch("s2d");
   count_launch(c, 2);

@@ -97,11 +97,19 @@ static bool small_gemm(Ctx* c, cudaStream_t st, int M, int N, int K, const Dense
   }();
   const int64_t outs = int64_t(M) * N;
   if (!on) return false;
-  if (outs <= 16384 && K >= 64) {  // few outputs: a warp per output (CIFAR ip2 dW 640 x K=100: 29 -> ~3 us)
+  static const int64_t warp_outs = [] {  // K in [64, 256): warp-per-output up to this many outputs
+    const char* v = std::getenv("CDNN_SMALL_GEMM_WARP_OUTS");
+    return v ? int64_t(std::atoll(v)) : int64_t(2048);  // LeNet ip2 dW (5000) measured faster per thread
+  }();
+  // few outputs: a warp per output (CIFAR ip2 dW 640 x K=100: 29 -> 5.5 us)
+  if (outs <= 16384 && (K >= 256 || (K >= 64 && outs <= warp_outs))) {
     const int64_t threads = outs * 32;
     simt::dot_warp_kernel<T><<<int((threads + 255) / 256), 256, 0, st>>>(va, vb, epi, M, N, K);
   } else if (K <= 128 && outs <= (int64_t(1) << 20)) {
-    simt::dot_thread_kernel<T><<<int((outs + 255) / 256), 256, 0, st>>>(va, vb, epi, M, N, K);
+    if (outs <= (int64_t(1) << 17))  // few threads (CIFAR ip1 dW 65536 x K=100: 27 -> 15 us)
+      simt::dot_thread_kernel<T, 16><<<int((outs + 255) / 256), 256, 0, st>>>(va, vb, epi, M, N, K);
+    else  // enough threads to hide the latency (LeNet ip1 dW 400000 x K=64)
+      simt::dot_thread_kernel<T, 4><<<int((outs + 255) / 256), 256, 0, st>>>(va, vb, epi, M, N, K);
   } else {
     return false;
   }
