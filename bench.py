@@ -1,12 +1,15 @@
 #!/usr/bin/env python3
 """Benchmark of the hot path: one SGD training iteration (feed -> Net::forward ->
-SoftmaxWithLoss -> Net::backward -> momentum-SGD update) of CIFAR-10 quick at
-batch 100 per GPU (BASELINE.json configs[1], float -> TF32 tensor cores).
+SoftmaxWithLoss -> Net::backward -> momentum-SGD update) of AlexNet at batch
+256 per GPU (BASELINE.json configs[3], the largest single-GPU config; float ->
+3xTF32 tensor cores).  The other configs are behind --workload.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload alexnet|cifar10_quick|lenet|resnet20] [--dtype f32|f64]
 
-Prints ONE JSON line (rank 0).  N > 1: launched by torch.distributed.run, one
-rank per GPU, NCCL gradient all-reduce (weak scaling: batch 100 per GPU).
+Prints ONE JSON line (rank 0).  N > 1: one rank per GPU (launched by
+torch.distributed.run, or bench.py re-executes itself under it when WORLD_SIZE
+is unset), NCCL gradient all-reduce (weak scaling: the per-GPU batch is fixed).
 
 * value      images/s with the batch already resident in HBM (captured CUDA
              graph of the step), L2 flushed (256 MiB write) before every timed
@@ -54,12 +57,14 @@ WORKLOADS = {
     "resnet20": dict(batch=128, img=(3, 32, 32), classes=10, ref_batch=8, cpu_batch=16,
                      solver=dict(method="sgd", lr=0.1, momentum=0.9, weight_decay=1e-4)),
 }
-WORKLOAD = "cifar10_quick"
-BATCH = 100
+DEFAULT_WORKLOAD = "alexnet"
+WORKLOAD = DEFAULT_WORKLOAD
+BATCH = WORKLOADS[WORKLOAD]["batch"]
 SOLVER = WORKLOADS[WORKLOAD]["solver"]
-IMG = (3, 32, 32)
-CLASSES = 10
-REF_SAMPLE_BATCH = 20  # images per reference step per process (bounded CPU sample)
+IMG = WORKLOADS[WORKLOAD]["img"]
+CLASSES = WORKLOADS[WORKLOAD]["classes"]
+REF_SAMPLE_BATCH = WORKLOADS[WORKLOAD]["ref_batch"]  # images per reference step per process
+DTYPE = "f32"
 
 
 def select_workload(name: str) -> None:
@@ -78,15 +83,20 @@ def model_text(batch: int) -> str:
     return polegrad.load_model(WORKLOAD, batch)
 
 
-def config(n_gpus: int, graph: bool) -> dict:
+def config(n_gpus: int) -> dict:
+    """The workload (identical on both arms)."""
     return {"workload": WORKLOAD, "per_gpu_batch": BATCH, "global_batch": BATCH * n_gpus,
-            "input": "x".join(map(str, IMG)), "classes": CLASSES,
+            "input": "x".join(map(str, IMG)), "classes": CLASSES, "real": DTYPE,
             "solver": f"SGD lr={SOLVER['lr']:g} momentum={SOLVER['momentum']:g} "
                       f"weight_decay={SOLVER['weight_decay']:g}",
-            "math": os.environ.get("CDNN_MATH", "tf32x3"),
-            "step": "cuda-graph" if graph else "eager",
             "l2": "flushed (256 MiB device write) before every timed step",
             "parallelism": f"dp{n_gpus}" if n_gpus > 1 else "single"}
+
+
+def dtype_label() -> str:
+    if DTYPE == "f64":
+        return "fp64 (SIMT DFMA)"
+    return "fp32 (3xTF32 tensor cores)" if os.environ.get("CDNN_MATH", "tf32x3") == "tf32x3" else "fp32 (TF32)"
 
 
 # --------------------------------------------------------------------------------------
@@ -210,21 +220,51 @@ def layer_flops(net) -> dict:
 
 
 def peaks() -> dict:
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    """Roofline denominators: HBM and bf16 from the driver's MEASURED_PEAKS.json; the
+    dense TF32 (float path) and FP64 (double path) cuBLAS rates from
+    profiles/r02_peaks.json, measured on a B200 of this pool by
+    profiles/measure_peaks.py (MEASURED_PEAKS.json carries no TF32 / FP64 figure)."""
+    out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
     try:
-        d = json.load(open(path))
-        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]), "source": "measured"}
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        out.update(hbm_gbs=float(d["hbm_gbs"]), bf16_tflops=float(d["bf16_tflops"]), source="measured")
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+        pass
+    try:
+        m = json.load(open(os.path.join(ROOT, "profiles", "r02_peaks.json")))
+        out["tf32_tflops"] = float(m["tf32"]["burst_tflops"])
+        out["fp64_tflops"] = float(m["fp64"]["burst_tflops"])
+        out["tc_source"] = ("measured: torch.matmul 8192^3 burst on a B200 of this pool "
+                            "(profiles/r02_peaks.json, profiles/measure_peaks.py)")
+    except Exception:
+        out["tf32_tflops"] = out["bf16_tflops"] / 2.0
+        out["fp64_tflops"] = None
+        out["tc_source"] = f"derived: bf16 {out['bf16_tflops']} / 2 ({out['source']})"
+    return out
 
 
 def ncu_traffic(kernel_key: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    """DRAM bytes (read + write) per launch of the dominant layer op, from the committed
+    ncu capture of THIS workload, batch and dtype (profiles/ncu_summary.json, keyed
+    '<workload>/b<batch>/<dtype>' -> '<layer>.<fwd|bwd>'); None when no capture exists."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        return d.get("traffic_bytes_per_launch", {}).get(kernel_key)
+        return d["traffic_bytes_per_launch"][f"{WORKLOAD}/b{BATCH}/{DTYPE}"].get(kernel_key)
     except Exception:
         return None
+
+
+def host_cpu() -> dict:
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 def cpu_baseline_sample(iters: int = 2) -> dict:
@@ -247,7 +287,7 @@ def cpu_baseline_sample(iters: int = 2) -> dict:
         solver.apply()
     dt = time.perf_counter() - t0
     return {"value": iters * cb / dt, "unit": UNIT, "cores": 1, "kind": "reference",
-            "ms_per_step": 1000 * dt / iters,
+            "ms_per_step": 1000 * dt / iters, **host_cpu(),
             "sample": f"{iters} iterations of {WORKLOAD} at batch {cb} (f32) on oracle/_ref: unmodified "
                       f"reference core (kernels::gemm, InnerProduct, ReLU, solver) + reference-style "
                       f"Convolution/Pooling/SoftmaxWithLoss extension, 1 thread"}
@@ -279,7 +319,7 @@ def run_b200(args) -> None:
         return float(t.item())
 
     text = model_text(BATCH)
-    net = polegrad.Net(text, seed=1, dtype="f32", device=local)
+    net = polegrad.Net(text, seed=1, dtype=DTYPE, device=local)
     solver = polegrad.Solver(net, **SOLVER)
     cx = CtxView(net.context_ptr())
     par = None
@@ -289,11 +329,18 @@ def run_b200(args) -> None:
         par = polegrad.Parallel(net, world, rank, uid[0])
         par.broadcast()
         solver.set_parallel(par)
+    nccl_ranks = par.info() if par else None
+    if nccl_ranks:
+        log(f"rank {rank}: NCCL communicator reports {nccl_ranks['nranks']} ranks (this one {nccl_ranks['rank']}), "
+            f"{nccl_ranks['buckets']} gradient buckets")
+        if nccl_ranks["nranks"] != world:
+            raise RuntimeError(f"NCCL communicator has {nccl_ranks['nranks']} ranks, WORLD_SIZE {world}")
 
+    npd = polegrad.NP_DTYPE[DTYPE]
     rng = np.random.default_rng(2 + rank)
-    nb = max(args.steps, 1)
-    host_x = rng.uniform(-1, 1, (nb, BATCH) + IMG).astype(np.float32)
-    host_y = np.floor(rng.uniform(0, 1, (nb, BATCH)) * CLASSES).astype(np.float32)
+    nb = min(3, max(args.steps, 1))  # distinct host batches, cycled
+    host_x = rng.uniform(-1, 1, (nb, BATCH) + IMG).astype(npd)
+    host_y = np.floor(rng.uniform(0, 1, (nb, BATCH)) * CLASSES).astype(npd)
 
     # eager step: allocates workspaces / tensor maps, counts kernel launches per step
     net.set_batch(host_x[0], host_y[0])
@@ -318,9 +365,9 @@ def run_b200(args) -> None:
 
     # graphs: resident-input step (value) and host-buffer step (e2e)
     use_graph = not args.no_graph
-    pin_x = cudadnn.PinnedBuffer((BATCH,) + IMG)
-    pin_y = cudadnn.PinnedBuffer((BATCH,))
-    pin_loss = cudadnn.PinnedBuffer((1,))
+    pin_x = cudadnn.PinnedBuffer((BATCH,) + IMG, npd)
+    pin_y = cudadnn.PinnedBuffer((BATCH,), npd)
+    pin_loss = cudadnn.PinnedBuffer((1,), npd)
     g_res = g_e2e = None
     if use_graph:
         try:
@@ -386,7 +433,7 @@ def run_b200(args) -> None:
         npin = min(3, nb)
         pins = []
         for j in range(npin):
-            px, py = cudadnn.PinnedBuffer((BATCH,) + IMG), cudadnn.PinnedBuffer((BATCH,))
+            px, py = cudadnn.PinnedBuffer((BATCH,) + IMG, npd), cudadnn.PinnedBuffer((BATCH,), npd)
             px.array[...] = host_x[j]
             py.array[...] = host_y[j]
             pins.append((px, py))
@@ -404,6 +451,20 @@ def run_b200(args) -> None:
                 sink.append(ring.pop_loss())
                 inflight -= 1
 
+        def run_ring_pageable(n, sink):
+            # the caller's pageable numpy batches: FeedRing.push copies each into the
+            # ring's page-locked slot (host memcpy) before enqueueing its H2D
+            inflight = 0
+            for i in range(n):
+                if inflight == 2:
+                    sink.append(ring.pop_loss())
+                    inflight -= 1
+                ring.push(host_x[i % nb], host_y[i % nb])
+                inflight += 1
+            while inflight:
+                sink.append(ring.pop_loss())
+                inflight -= 1
+
         run_ring(max(2, args.warmup), [])
         net.sync()
         barrier()
@@ -414,6 +475,16 @@ def run_b200(args) -> None:
         run_ring(args.steps, losses)
         cx.record(e_end)
         net.sync()
+        wall_ms_pinned = 1000 * (time.perf_counter() - t0)
+        # same through pageable host arrays (the host memcpy into the pinned slot included)
+        p_start, p_end = cx.event(), cx.event()
+        barrier()
+        net.sync()
+        cx.record(p_start)
+        run_ring_pageable(args.steps, losses)
+        cx.record(p_end)
+        net.sync()
+        pageable_ms = max_over_ranks(cx.elapsed(p_start, p_end))
     else:
         for i in range(min(args.warmup, nb)):
             pin_x.array[...] = host_x[i]
@@ -440,7 +511,9 @@ def run_b200(args) -> None:
         cx.record(e_end)
         net.sync()
     e2e_ms = max_over_ranks(cx.elapsed(e_start, e_end))
-    wall_ms = max_over_ranks(1000 * (time.perf_counter() - t0))
+    wall_ms = max_over_ranks(wall_ms_pinned if use_graph else 1000 * (time.perf_counter() - t0))
+    if not use_graph:
+        pageable_ms = None
     e2e = world * BATCH * args.steps / (e2e_ms / 1000.0)
     if not all(np.isfinite(losses)):
         raise RuntimeError("non-finite loss")
@@ -450,10 +523,11 @@ def run_b200(args) -> None:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (largest per-layer device time)
+    # ---- roofline of the dominant layer op (largest per-layer device time)
     flops = layer_flops(net)
     pk = peaks()
-    tf32_peak = pk["bf16_tflops"] / 2.0  # dense TF32 = half the bf16 rate (derived from measured bf16)
+    math3 = DTYPE == "f32" and os.environ.get("CDNN_MATH", "tf32x3") == "tf32x3"
+    tc_peak = pk["tf32_tflops"] if DTYPE == "f32" else pk["fp64_tflops"]
     ops = []
     for lname, t in prof.items():
         for phase in ("fwd", "bwd"):
@@ -464,37 +538,49 @@ def run_b200(args) -> None:
     dom_ms, dom_layer, dom_phase, dom_f = ops[0]
     prof_total = sum(o[0] for o in ops)
     kernel_key = f"{dom_layer}.{dom_phase}"
-    if dom_f:
+    if dom_f and tc_peak:
         achieved = dom_f / (dom_ms / 1000.0) / 1e12
-        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
-                "frac": round(achieved / tf32_peak, 5), "traffic": ncu_traffic(kernel_key),
-                "kernel": f"{dom_layer} {dom_phase} (implicit-GEMM tcgen05, "
-                          f"{'3xTF32' if config(1, True)['math'] == 'tf32x3' else 'TF32'})",
+        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(tc_peak, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / tc_peak, 5), "traffic": ncu_traffic(kernel_key),
+                "kernel": f"{dom_layer} {dom_phase} ("
+                          + ("implicit-GEMM tcgen05, " + ("3xTF32" if math3 else "TF32") if DTYPE == "f32"
+                             else "SIMT FP64") + ")",
                 "flops_per_launch": dom_f, "ms_per_launch": round(dom_ms, 5),
-                # 3xTF32 issues three TF32 products per multiply-add (hi*hi, hi*lo, lo*hi):
-                # the tensor-core work behind the algorithmic FLOPs, against the same peak
-                "mma_frac": round(achieved * (3 if config(1, True)['math'] == 'tf32x3' else 1) / tf32_peak, 5),
                 "share_of_step": round(dom_ms / prof_total, 4),
-                "peak_note": f"TF32 dense = measured bf16 {pk['bf16_tflops']} / 2 ({pk['source']})"}
+                "peak_note": ("dense TF32 " if DTYPE == "f32" else "dense FP64 ") + pk["tc_source"]}
+        if math3:
+            # 3xTF32 issues three TF32 products per multiply-add (hi*hi, hi*lo, lo*hi):
+            # the tensor-core work behind the algorithmic FLOPs, against the same peak
+            roof["mma_frac"] = round(3 * achieved / tc_peak, 5)
     else:
         roof = {"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": None,
                 "traffic": ncu_traffic(kernel_key), "kernel": f"{dom_layer} {dom_phase}",
                 "ms_per_launch": round(dom_ms, 5), "share_of_step": round(dom_ms / prof_total, 4)}
 
     cpu = cpu_baseline_sample(args.cpu_iters) if not args.no_cpu_baseline else None
+    esz = 8 if DTYPE == "f64" else 4
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "tf32", "data": "synthetic",
-        "config": config(world, use_graph),
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(), "data": "synthetic",
+        "config": config(world),
+        "step": "cuda-graph" if use_graph else "eager",
         "e2e": {"value": round(e2e, 1), "unit": UNIT, "ms_per_step": round(e2e_ms / args.steps, 5),
                 "wall_ms_per_step": round(wall_ms / args.steps, 5),
-                "h2d_bytes_per_step": int(BATCH * np.prod(IMG) * 4 + BATCH * 4), "d2h_bytes_per_step": 4},
+                "h2d_bytes_per_step": int(BATCH * np.prod(IMG) * esz + BATCH * esz), "d2h_bytes_per_step": esz,
+                "host_copy": "each step's batch H2D from page-locked host memory (FeedRing.push_pinned) and its "
+                             "loss D2H, inside the timed region",
+                "pageable": None if pageable_ms is None else {
+                    "value": round(world * BATCH * args.steps / (pageable_ms / 1000.0), 1),
+                    "ms_per_step": round(pageable_ms / args.steps, 5),
+                    "how": "FeedRing.push from pageable numpy arrays: the host memcpy into the ring's pinned "
+                           "slot, the H2D and the loss D2H every step, overlapped with the step in flight"}},
         "gpu_launches": int(launches_per_step * args.steps),
         "launches_per_step": int(launches_per_step),
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clocks,
+        "nccl_ranks": nccl_ranks,
         "layer_profile_ms": prof,
     }
     print(json.dumps(line), flush=True)
@@ -503,15 +589,22 @@ def run_b200(args) -> None:
 
 
 # --------------------------------------------------------------------------------------
+def ref_batch_per_process(procs: int) -> int:
+    """Images per reference step per host process: the bench batch split over the
+    host cores, capped by the workload's bounded-sample size (AlexNet: one image per
+    core per step, ~1.6 s; a whole batch-256 step would take ~7 min per core)."""
+    return max(1, min(-(-BATCH // procs), REF_SAMPLE_BATCH))
+
+
 def _ref_worker(args_tuple):
-    steps, warmup, seed = args_tuple
+    steps, warmup, seed, nb = args_tuple
     from oracle import pyoracle
-    text = model_text(REF_SAMPLE_BATCH)
-    net = pyoracle.OracleNet(text, seed=1, dtype="f32")
+    text = model_text(nb)
+    net = pyoracle.OracleNet(text, seed=1, dtype=DTYPE)
     solver = pyoracle.OracleSolver(net, **SOLVER)
     rng = np.random.default_rng(seed)
-    x = rng.uniform(-1, 1, (REF_SAMPLE_BATCH,) + IMG)
-    y = np.floor(rng.uniform(0, 1, REF_SAMPLE_BATCH) * CLASSES)
+    x = rng.uniform(-1, 1, (nb,) + IMG)
+    y = np.floor(rng.uniform(0, 1, nb) * CLASSES)
     for _ in range(warmup):
         net.set_batch(x, y)
         net.forward()
@@ -532,30 +625,46 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     from oracle import pyoracle
-    if not pyoracle.available("f32"):
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/liboracle_f32.so not built"}))
+    if not pyoracle.available(DTYPE):
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref/liboracle_{DTYPE}.so not built"}))
         return
+    pyoracle.load(DTYPE)  # mapped in this (parent) process too, before the workers fork
     import multiprocessing as mp
     procs = max(1, os.cpu_count() or 1)
+    nb = ref_batch_per_process(procs)
     steps = max(args.steps, 1)
-    warm = min(args.warmup, 1)
     with mp.get_context("fork").Pool(procs) as pool:
-        times = pool.map(_ref_worker, [(steps, warm, 2 + i) for i in range(procs)])
+        times = pool.map(_ref_worker, [(steps, args.warmup, 2 + i, nb) for i in range(procs)])
     t = max(times)
-    value = procs * REF_SAMPLE_BATCH * steps / t
-    sample = (f"{procs} independent single-threaded replicas (one per host core), each {steps} SGD iterations of "
-              f"{WORKLOAD} at batch {REF_SAMPLE_BATCH} (bounded sample of the batch-100 step; CPU cost is linear in "
-              f"batch) on oracle/_ref: unmodified reference core + reference-style conv/pool/loss extension, f32")
+    value = procs * nb * steps / t
+    sample = (f"{procs} single-threaded processes (one per host core: the reference has no threads), each step "
+              f"{procs} x {nb} = {procs * nb} images of the batch-{BATCH} {WORKLOAD} step"
+              + (" (the whole bench batch)" if procs * nb >= BATCH else " (bounded sample; CPU cost is linear in batch)")
+              + f", {args.warmup} warm-up + {steps} timed SGD iterations, slowest process timed; oracle/_ref: "
+              f"unmodified reference core + reference-style conv/pool/loss extension, {DTYPE}")
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": round(1000 * t / steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-        "config": config(world, False),
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic", "impl": "reference",
+        "config": config(world),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, **host_cpu()},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def respawn_under_torchrun(args) -> None:
+    """`bench.py --gpus N` without a launcher: re-execute under torch.distributed.run,
+    one rank per GPU, so N > 1 never silently measures one rank."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log("launching", " ".join(cmd))
+    os.execv(sys.executable, cmd)
 
 
 def main() -> None:
@@ -567,10 +676,16 @@ def main() -> None:
     ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the captured CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cifar10_quick",
-                    help="BASELINE.json config to run (default: the headline CIFAR-10 quick)")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD,
+                    help="BASELINE.json config to run (default: AlexNet b256, configs[3])")
+    ap.add_argument("--dtype", choices=["f32", "f64"], default="f32",
+                    help="the library's real type (f32: 3xTF32 tensor cores; f64: SIMT FP64)")
     args = ap.parse_args()
     select_workload(args.workload)
+    global DTYPE
+    DTYPE = args.dtype
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        respawn_under_torchrun(args)
     if args.warmup < 3 and args.impl == "b200":
         log("note: timing rules ask for >= 3 warm-up steps")
     if args.impl == "reference":

@@ -376,6 +376,9 @@ CDNN_API int cdnn_nccl_available(int* out);
 CDNN_API int cdnn_nccl_unique_id(uint8_t id[128]);
 CDNN_API int cdnn_nccl_comm_create(cdnn_ctx ctx, int nranks, int rank, const uint8_t id[128],
                                    cdnn_handle* out);
+/* the communicator's size and this process's rank, as NCCL reports them
+ * (ncclCommCount / ncclCommUserRank) */
+CDNN_API int cdnn_nccl_comm_info(cdnn_ctx ctx, cdnn_handle comm, int* nranks, int* rank);
 /* in-place sum all-reduce of elements [offset, offset+n) of buf */
 CDNN_API int cdnn_allreduce_sum(cdnn_ctx ctx, cdnn_handle comm, cdnn_handle buf, uint64_t offset,
                                 uint64_t n, cdnn_handle stream);

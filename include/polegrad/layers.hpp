@@ -392,6 +392,9 @@ class DropoutLayer final : public Layer {
                            Rng& rng) override;
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  // Device iteration counter (one F64) the mask hash reads; Net saves / restores it
+  // around steps that must not advance the mask sequence (feed-ring warm-up).
+  cdnn_handle counter() const { return counter_; }
 
  private:
   double ratio_;

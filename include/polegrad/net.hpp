@@ -83,6 +83,12 @@ class Net {
   // Called after layer i's backward (reverse order); used by Parallel.
   using BackwardHook = std::function<void(std::size_t layer_index)>;
   void set_backward_hook(BackwardHook hook) { backward_hook_ = std::move(hook); }
+  const BackwardHook& backward_hook() const { return backward_hook_; }
+  // Dropout iteration counters (layer order; synchronous D2H / H2D): an eager
+  // step that must leave no trace (FeedRing warm-up) restores them afterwards, so
+  // ring training draws the same mask sequence as eager training.
+  std::vector<double> dropout_counters();
+  void set_dropout_counters(const std::vector<double>& values);
   // Index of the first parameter owned by layer i (params are in layer order).
   std::size_t first_param_of_layer(std::size_t i) const { return layer_param_begin_.at(i); }
   // True when forward/backward contain no host work (graph capturable).

@@ -13,6 +13,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "polegrad/net.hpp"
@@ -37,6 +38,13 @@ class Parallel {
   static UniqueId unique_id();  // call on rank 0, share out of band
 
   Parallel(Net& net, int nranks, int rank, const UniqueId& id, std::size_t bucket_bytes = std::size_t(8) << 20);
+  // Host-transport replica: the same buckets, backward hook, loss scale and join,
+  // but each bucket is copied to the host, combined by `transport` across ranks
+  // (op 0: in-place SUM all-reduce; op 1: broadcast from rank 0) and copied back,
+  // synchronously.  For running the data-parallel protocol where NCCL cannot (several
+  // ranks on one GPU, CPU-side collectives such as gloo); not graph-capturable.
+  using HostTransport = std::function<void(int op, real* host, std::size_t offset, std::size_t n)>;
+  Parallel(Net& net, int nranks, int rank, HostTransport transport, std::size_t bucket_bytes = std::size_t(8) << 20);
   ~Parallel();
   Parallel(const Parallel&) = delete;
   Parallel& operator=(const Parallel&) = delete;
@@ -44,6 +52,11 @@ class Parallel {
   int nranks() const { return nranks_; }
   int rank() const { return rank_; }
   const std::vector<GradBucket>& buckets() const { return buckets_; }
+  // Size and rank as the communicator reports them (NCCL: ncclCommCount /
+  // ncclCommUserRank; host transport: the constructor's).
+  std::pair<int, int> comm_info() const;
+  // Bucket all-reduces issued so far (a captured step issues one per bucket).
+  std::uint64_t launches() const { return launches_; }
 
   // Rank 0's weights to every rank (start of training).
   void broadcast_weights();
@@ -52,6 +65,7 @@ class Parallel {
   void reduce_gradients(Net& net);
 
  private:
+  void init_buckets(std::size_t bucket_bytes);
   void on_layer_done(std::size_t layer_index);
   void launch(std::size_t b);
 
@@ -59,8 +73,10 @@ class Parallel {
   int nranks_, rank_;
   cdnn_handle comm_ = 0;
   cdnn_handle comm_stream_ = 0;
+  HostTransport transport_;
   std::vector<GradBucket> buckets_;
   std::vector<bool> launched_;
+  std::uint64_t launches_ = 0;
 };
 
 }  // namespace polegrad

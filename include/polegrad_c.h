@@ -120,6 +120,14 @@ PG_API int pg_graph_free(pg_net* net, uint64_t graph);
 PG_API int pg_parallel_unique_id(uint8_t id[128]);
 PG_API int pg_parallel_create(pg_net* net, int nranks, int rank, const uint8_t id[128], uint64_t bucket_bytes,
                               pg_parallel** out);
+/* host-transport replica (polegrad::Parallel HostTransport): every bucket is copied to
+ * the host and passed to `transport` (op 0: in-place SUM all-reduce across ranks;
+ * op 1: broadcast from rank 0), which returns 0 on success; synchronous */
+typedef int (*pg_host_transport)(void* user, int op, void* host, uint64_t offset, uint64_t n);
+PG_API int pg_parallel_create_host(pg_net* net, int nranks, int rank, pg_host_transport transport, void* user,
+                                   uint64_t bucket_bytes, pg_parallel** out);
+/* communicator size / rank as NCCL reports them, bucket count, bucket all-reduces issued */
+PG_API int pg_parallel_info(pg_parallel* p, int* nranks, int* rank, int* nbuckets, uint64_t* launches);
 PG_API int pg_parallel_free(pg_parallel* p);
 PG_API int pg_parallel_broadcast(pg_parallel* p);
 PG_API int pg_solver_set_parallel(pg_solver* s, pg_parallel* p);

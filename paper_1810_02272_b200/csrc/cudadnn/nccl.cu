@@ -23,6 +23,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   bool ok = false;
 };
 
@@ -40,7 +42,9 @@ NcclApi& api() {
     x.AllReduce = reinterpret_cast<decltype(x.AllReduce)>(dlsym(x.lib, "ncclAllReduce"));
     x.Broadcast = reinterpret_cast<decltype(x.Broadcast)>(dlsym(x.lib, "ncclBroadcast"));
     x.GetErrorString = reinterpret_cast<decltype(x.GetErrorString)>(dlsym(x.lib, "ncclGetErrorString"));
-    x.ok = x.GetUniqueId && x.CommInitRank && x.CommDestroy && x.AllReduce && x.Broadcast;
+    x.CommCount = reinterpret_cast<decltype(x.CommCount)>(dlsym(x.lib, "ncclCommCount"));
+    x.CommUserRank = reinterpret_cast<decltype(x.CommUserRank)>(dlsym(x.lib, "ncclCommUserRank"));
+    x.ok = x.CommCount && x.CommUserRank && x.GetUniqueId && x.CommInitRank && x.CommDestroy && x.AllReduce && x.Broadcast;
     return x;
   }();
   return a;
@@ -105,6 +109,16 @@ int cdnn_nccl_comm_create(cdnn_ctx ctx, int nranks, int rank, const uint8_t id[1
     s.nranks = nranks;
     s.rank = rank;
     *out = insert_slot(c, s);
+  });
+}
+
+int cdnn_nccl_comm_info(cdnn_ctx ctx, cdnn_handle comm, int* nranks, int* rank) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    NcclSlot& s = nccl(c, comm);
+    NcclApi& a = need_api();
+    nccl_check(a.CommCount(static_cast<ncclComm_t>(s.comm), nranks), "ncclCommCount");
+    nccl_check(a.CommUserRank(static_cast<ncclComm_t>(s.comm), rank), "ncclCommUserRank");
   });
 }
 

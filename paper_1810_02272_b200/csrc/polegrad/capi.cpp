@@ -386,6 +386,31 @@ int pg_parallel_create(pg_net* n, int nranks, int rank, const uint8_t id[128], u
   });
 }
 
+int pg_parallel_create_host(pg_net* n, int nranks, int rank, pg_host_transport transport, void* user,
+                            uint64_t bucket_bytes, pg_parallel** out) {
+  return run([&] {
+    if (!transport) throw polegrad::InvalidArgument("pg_parallel_create_host: null transport");
+    auto fn = [transport, user](int op, polegrad::real* host, std::size_t offset, std::size_t count) {
+      if (transport(user, op, host, offset, count) != 0)
+        throw polegrad::InvalidState("Parallel host transport failed (op " + std::to_string(op) + ")");
+    };
+    auto p = std::make_unique<pg_parallel>();
+    p->par = std::make_unique<polegrad::Parallel>(net_of(n), nranks, rank, fn,
+                                                  bucket_bytes ? bucket_bytes : (std::size_t(8) << 20));
+    *out = p.release();
+  });
+}
+
+int pg_parallel_info(pg_parallel* p, int* nranks, int* rank, int* nbuckets, uint64_t* launches) {
+  return run([&] {
+    const auto [n, r] = p->par->comm_info();
+    if (nranks) *nranks = n;
+    if (rank) *rank = r;
+    if (nbuckets) *nbuckets = int(p->par->buckets().size());
+    if (launches) *launches = p->par->launches();
+  });
+}
+
 int pg_parallel_free(pg_parallel* p) { return run([&] { delete p; }); }
 int pg_parallel_broadcast(pg_parallel* p) { return run([&] { p->par->broadcast_weights(); }); }
 int pg_solver_set_parallel(pg_solver* s, pg_parallel* p) {

@@ -35,13 +35,29 @@ FeedRing::FeedRing(Net& net, Solver& solver, int depth) : net_(net), solver_(sol
     // resource (workspaces, tensor maps, repacked weights) outside the capture;
     // its gradients are discarded and the solver history is allocated without
     // an update, so the weights are untouched.
+    // The warm-up leaves no trace: the backward hook (Parallel's bucket
+    // all-reduces) is detached, so no collective is launched on the comm stream
+    // outside the captured steps (it would race zero_param_diffs and leave the
+    // buckets marked launched for the first capture), and the Dropout
+    // iteration counters are restored, so ring training draws the same masks as
+    // eager training.
     net.set_batch(slots_[0].data, slots_[0].labels);
     if (!net.graph_safe()) throw InvalidState("feed ring: net has host-side layers (loss hooks / FIFO feed)");
-    net.forward();
-    net.backward();
+    const std::vector<double> counters = net.dropout_counters();
+    Net::BackwardHook hook = net.backward_hook();
+    net.set_backward_hook(nullptr);
+    try {
+      net.forward();
+      net.backward();
+    } catch (...) {
+      net.set_backward_hook(std::move(hook));
+      throw;
+    }
+    net.set_backward_hook(std::move(hook));
     net.zero_param_diffs();
     solver.prepare(net);
     reg.synchronize();
+    net.set_dropout_counters(counters);
     for (Slot& s : slots_) {
       // capture: D2D(slot's staged batch) -> forward -> backward -> update -> D2H(loss).
       // The slot's H2D runs on the copy stream at push time, overlapping the step

@@ -424,6 +424,29 @@ void Net::pg_backward(const std::string& logit_blob, const std::string& prob_blo
   backward_from(logit_blob);
 }
 
+std::vector<double> Net::dropout_counters() {
+  std::vector<double> out;
+  registry_->synchronize();
+  for (const auto& l : layers_)
+    if (auto* d = dynamic_cast<DropoutLayer*>(l.get())) {
+      double v = 0;
+      cdnn_ok(cdnn_read(registry_->context(), d->counter(), &v, 1), "dropout_counters");
+      out.push_back(v);
+    }
+  return out;
+}
+
+void Net::set_dropout_counters(const std::vector<double>& values) {
+  std::size_t k = 0;
+  registry_->synchronize();
+  for (const auto& l : layers_)
+    if (auto* d = dynamic_cast<DropoutLayer*>(l.get())) {
+      if (k >= values.size()) throw InvalidArgument("set_dropout_counters: too few values");
+      cdnn_ok(cdnn_write(registry_->context(), d->counter(), &values[k++], 1), "set_dropout_counters");
+    }
+  if (k != values.size()) throw InvalidArgument("set_dropout_counters: too many values");
+}
+
 void Net::zero_param_diffs() {
   if (!param_total_) return;
   Registry& reg = *registry_;

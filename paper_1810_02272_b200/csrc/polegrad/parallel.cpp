@@ -39,6 +39,18 @@ Parallel::Parallel(Net& net, int nranks, int rank, const UniqueId& id, std::size
   Registry& reg = *net.registry();
   cdnn_ok(cdnn_nccl_comm_create(reg.context(), nranks, rank, id.data(), &comm_), "Parallel");
   cdnn_ok(cdnn_stream_create(reg.context(), &comm_stream_), "Parallel");
+  init_buckets(bucket_bytes);
+}
+
+Parallel::Parallel(Net& net, int nranks, int rank, HostTransport transport, std::size_t bucket_bytes)
+    : net_(&net), nranks_(nranks), rank_(rank), transport_(std::move(transport)) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("Parallel: bad rank / nranks");
+  if (!transport_) throw InvalidArgument("Parallel: empty host transport");
+  init_buckets(bucket_bytes);
+}
+
+void Parallel::init_buckets(std::size_t bucket_bytes) {
+  Net& net = *net_;
   std::vector<std::size_t> offs, counts;
   for (std::size_t i = 0; i < net.params().size(); ++i) {
     offs.push_back(net.param_offset(i));
@@ -50,7 +62,14 @@ Parallel::Parallel(Net& net, int nranks, int rank, const UniqueId& id, std::size
   // Normalised losses average over the local batch; 1/nranks makes the SUM
   // all-reduce the global-batch mean (Caffe divides by solver_count).
   // MemoryLoss nets inject unnormalised diffs, for which the plain sum is exact.
-  net.set_loss_scale(1.0 / nranks);
+  net.set_loss_scale(1.0 / nranks_);
+}
+
+std::pair<int, int> Parallel::comm_info() const {
+  if (transport_) return {nranks_, rank_};
+  int n = 0, r = 0;
+  cdnn_ok(cdnn_nccl_comm_info(net_->registry()->context(), comm_, &n, &r), "Parallel::comm_info");
+  return {n, r};
 }
 
 Parallel::~Parallel() {
@@ -63,16 +82,43 @@ Parallel::~Parallel() {
 void Parallel::broadcast_weights() {
   Registry& reg = *net_->registry();
   for (Blob* p : net_->params()) p->gpu_data();  // upload any host-side edits first
-  cdnn_ok(cdnn_broadcast(reg.context(), comm_, reg.in(net_->weight_arena()), net_->param_total(), 0, reg.stream()),
-          "broadcast_weights");
+  if (transport_) {
+    std::vector<real> host(net_->param_total());
+    cdnn_ok(cdnn_read_async(reg.context(), reg.in(net_->weight_arena()), 0, host.data(), host.size(), reg.stream()),
+            "broadcast_weights");
+    reg.synchronize();
+    transport_(1, host.data(), 0, host.size());
+    cdnn_ok(cdnn_write_async(reg.context(), reg.in(net_->weight_arena()), 0, host.data(), host.size(), reg.stream()),
+            "broadcast_weights");
+    reg.synchronize();
+  } else {
+    cdnn_ok(cdnn_broadcast(reg.context(), comm_, reg.in(net_->weight_arena()), net_->param_total(), 0, reg.stream()),
+            "broadcast_weights");
+  }
   for (Blob* p : net_->params()) p->overwrite_gpu_data();
 }
 
 void Parallel::launch(std::size_t b) {
   if (launched_[b]) return;
   launched_[b] = true;
+  ++launches_;
   Registry& reg = *net_->registry();
   const GradBucket& k = buckets_[b];
+  if (transport_) {
+    // every gradient queued so far on the compute and side streams, then the host round trip
+    if (net_->side_stream()) cdnn_ok(cdnn_stream_sync(reg.context(), net_->side_stream()), "allreduce");
+    std::vector<real> host(k.end - k.begin);
+    cdnn_ok(cdnn_read_async(reg.context(), reg.in(net_->grad_arena()), k.begin, host.data(), host.size(),
+                            reg.stream()),
+            "allreduce");
+    reg.synchronize();
+    transport_(0, host.data(), k.begin, host.size());
+    cdnn_ok(cdnn_write_async(reg.context(), reg.in(net_->grad_arena()), k.begin, host.data(), host.size(),
+                             reg.stream()),
+            "allreduce");
+    reg.synchronize();
+    return;
+  }
   // the comm stream waits for every gradient queued so far on the compute stream and
   // on the backward side stream (parameter-gradient halves, Net::backward_layer)
   cdnn_ok(cdnn_stream_wait(reg.context(), comm_stream_, reg.stream()), "allreduce");
@@ -94,7 +140,7 @@ void Parallel::reduce_gradients(Net& net) {
   for (Blob* p : net.params()) p->gpu_diff();  // host-side gradient edits go up first
   for (std::size_t b = 0; b < buckets_.size(); ++b) launch(b);
   Registry& reg = *net.registry();
-  cdnn_ok(cdnn_stream_wait(reg.context(), reg.stream(), comm_stream_), "allreduce join");
+  if (comm_stream_) cdnn_ok(cdnn_stream_wait(reg.context(), reg.stream(), comm_stream_), "allreduce join");
   launched_.assign(buckets_.size(), false);
 }
 

@@ -36,8 +36,11 @@ EXPORTS = [
     "pg_solver_restore", "pg_solver_iterations", "pg_feed_ring_create", "pg_feed_ring_free", "pg_feed_ring_push", "pg_feed_ring_push_pinned",
     "pg_feed_ring_pop_loss", "pg_net_pg_backward", "pg_feed_ring_push_sampled", "pg_imagedb_load",
     "pg_imagedb_free", "pg_imagedb_size", "pg_imagedb_set_boost", "pg_imagedb_sample", "pg_rng_create",
-    "pg_rng_free",
+    "pg_rng_free", "pg_parallel_create_host", "pg_parallel_info",
 ]
+
+# int transport(void* user, int op, void* host, uint64_t offset, uint64_t n)
+HOST_TRANSPORT = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64)
 
 
 def lib_path(dtype: str) -> str:
@@ -79,6 +82,8 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_net_profile": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
             "pg_parallel_create": ([vp, i, i, cp, u64, C.POINTER(vp)], i), "pg_parallel_free": ([vp], i),
             "pg_parallel_broadcast": ([vp], i), "pg_solver_set_parallel": ([vp, vp], i),
+            "pg_parallel_create_host": ([vp, i, i, HOST_TRANSPORT, vp, u64, C.POINTER(vp)], i),
+            "pg_parallel_info": ([vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(u64)], i),
             "pg_plan_buckets": ([C.POINTER(u64), C.POINTER(u64), i, u64, u64, C.POINTER(C.c_int32),
                                  C.POINTER(C.c_int32)], i),
             "pg_prototxt_roundtrip": ([cp, cp, u64, C.POINTER(u64)], i),
@@ -365,7 +370,18 @@ class FeedRing:
 
     def push_pinned(self, data, labels=None) -> None:
         """Zero-copy push of batches already in page-locked memory (cudadnn.PinnedBuffer):
-        the H2D is enqueued from them; keep them unchanged until this step's pop_loss()."""
+        the H2D is enqueued from them; keep them unchanged until this step's pop_loss().
+        The buffers must hold the net's real type (float32 for the f32 library, float64
+        for f64): the library copies count * sizeof(real) bytes from them."""
+        for name, buf in (("data", data), ("labels", labels)):
+            if buf is None:
+                continue
+            arr = buf.array
+            if arr.dtype != np.dtype(self.net.np) or not arr.flags.c_contiguous:
+                raise TypeError(f"push_pinned: {name} buffer is {arr.dtype}"
+                                f"{'' if arr.flags.c_contiguous else ' (not C-contiguous)'}; "
+                                f"the {self.net.dtype} library needs a C-contiguous {np.dtype(self.net.np)} "
+                                f"PinnedBuffer")
         _check(self.lib, self.lib.pg_feed_ring_push_pinned(self.ptr, data.ptr, data.array.size,
                                                            None if labels is None else labels.ptr,
                                                            0 if labels is None else labels.array.size))
@@ -485,5 +501,49 @@ class Parallel:
                                                    C.byref(p)))
         self.ptr = p
 
+    @classmethod
+    def host(cls, net: Net, nranks: int, rank: int, transport, bucket_bytes: int = 8 << 20) -> "Parallel":
+        """Host-transport replica: `transport(op, array, offset)` combines one bucket
+        (a numpy view of the host copy, the net's real type) across ranks in place:
+        op 0 = SUM all-reduce, op 1 = broadcast from rank 0 (e.g. over gloo)."""
+        self = cls.__new__(cls)
+        self.net = net
+
+        def tramp(_user, op, ptr, offset, n):
+            try:
+                arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_float if net.np == np.float32
+                                                                  else C.c_double)), shape=(n,))
+                transport(op, arr, offset)
+                return 0
+            except Exception:  # reported to the caller as a failed transport
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._tramp = HOST_TRANSPORT(tramp)  # keep alive as long as the Parallel
+        p = C.c_void_p()
+        _check(net.lib, net.lib.pg_parallel_create_host(net.ptr, nranks, rank, self._tramp, None, bucket_bytes,
+                                                        C.byref(p)))
+        self.ptr = p
+        return self
+
+    def info(self) -> dict:
+        """Communicator size / rank as NCCL reports them, buckets, all-reduces issued."""
+        n, r, nb, la = C.c_int(), C.c_int(), C.c_int(), C.c_uint64()
+        _check(self.net.lib, self.net.lib.pg_parallel_info(self.ptr, C.byref(n), C.byref(r), C.byref(nb),
+                                                           C.byref(la)))
+        return {"nranks": n.value, "rank": r.value, "buckets": nb.value, "launches": la.value}
+
     def broadcast(self) -> None:
         _check(self.net.lib, self.net.lib.pg_parallel_broadcast(self.ptr))
+
+    def close(self) -> None:
+        if getattr(self, "ptr", None):
+            _check(self.net.lib, self.net.lib.pg_parallel_free(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
