@@ -311,6 +311,21 @@ CDNN_API int cdnn_lrn_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_
 CDNN_API int cdnn_lrn_backward_ex(cdnn_ctx ctx, cdnn_handle x, cdnn_handle y, cdnn_handle scale,
                                   cdnn_handle dy, cdnn_handle dx, int n, int c, int hw, int local_size,
                                   double alpha, double beta, cdnn_handle gate, cdnn_handle stream);
+/* LRN fused with the MAX pooling that consumes its top (ops_lrnpool.cu): pool_desc
+ * describes the pooling over the LRN's NCHW shape.  Supported (out = 1): local_size 3
+ * or 5, MAX, no padding, square 3x3/2 or 2x2/2 windows.  Forward writes the LRN top
+ * (kept observable), the pooled top and the argmax mask, bit-identical to
+ * cdnn_lrn_forward + cdnn_pool_forward_ex (flags: CDNN_POOL_RELU); no scale tensor.
+ * Backward takes the POOLED top's diff and mask and writes the LRN bottom diff,
+ * bit-identical to cdnn_pool_backward + cdnn_lrn_backward_ex; gate 0 or x (the
+ * in-place ReLU on the LRN bottom, fused). */
+CDNN_API int cdnn_lrn_pool_supported(cdnn_ctx ctx, cdnn_handle pool_desc, int local_size, int* out);
+CDNN_API int cdnn_lrn_pool_forward(cdnn_ctx ctx, cdnn_handle pool_desc, cdnn_handle x, cdnn_handle lrn_top,
+                                   cdnn_handle pool_top, cdnn_handle mask, int local_size, double alpha,
+                                   double beta, double k, int flags, cdnn_handle stream);
+CDNN_API int cdnn_lrn_pool_backward(cdnn_ctx ctx, cdnn_handle pool_desc, cdnn_handle x, cdnn_handle pool_dy,
+                                    cdnn_handle mask, cdnn_handle dx, cdnn_handle gate, int local_size,
+                                    double alpha, double beta, double k, cdnn_handle stream);
 /* Dropout (train): out[i] = in[i]/(1-ratio) if hash(seed, *counter, i) > ratio*2^32 else 0.
  * The same call maps forward data and backward diffs (same seed + counter -> same mask).
  * `counter` is an 8-byte device buffer (u64 iteration), read by the kernel so graph replays

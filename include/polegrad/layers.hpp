@@ -307,6 +307,7 @@ struct PoolingParam {
 PoolingParam parse_pooling_param(const LayerSpec& spec);
 
 // Caffe pooling (ceil output size); MAX keeps an int32 argmax mask.
+class LRNLayer;
 class PoolingLayer final : public Layer {
  public:
   PoolingLayer(LayerSpec spec, PoolingParam p) : Layer(std::move(spec)), p_(p) {}
@@ -320,9 +321,19 @@ class PoolingLayer final : public Layer {
   bool supports_relu_gate() const override { return true; }
   // Fuse a following in-place ReLU into the pooling output (set by Net).
   void fuse_relu(bool on) { fused_relu_ = on; }
+  // The LRN producing this layer's bottom runs inside this layer's forward
+  // (cdnn_lrn_pool_forward, reading the LRN's bottom `lrn_bottom`), and this
+  // layer's backward runs inside the LRN's (set by Net, see LRNLayer::fuse_pool).
+  void fuse_lrn(const LRNLayer* lrn, Blob* lrn_bottom) { fused_lrn_ = lrn; lrn_bottom_ = lrn_bottom; }
+  bool is_max() const { return p_.max; }
+  cdnn_handle desc() const { return desc_; }
+  cdnn_handle mask_handle() const { return mask_; }
+  bool relu_fused() const { return fused_relu_; }
 
  private:
   bool fused_relu_ = false;
+  const LRNLayer* fused_lrn_ = nullptr;
+  Blob* lrn_bottom_ = nullptr;
   PoolingParam p_;
   std::shared_ptr<Registry> reg_;
   cdnn_handle desc_ = 0;
@@ -373,8 +384,20 @@ class LRNLayer final : public Layer {
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
   bool supports_relu_gate() const override { return true; }
+  // LRN -> MAX Pooling fusion (set by Net when the pooling is this layer's only
+  // consumer and cdnn_lrn_pool_supported): this forward does nothing (the
+  // pooling's forward computes both tops), and this backward takes the pooled
+  // top's diff and mask directly (cdnn_lrn_pool_backward); the LRN top's diff and
+  // the scale tensor are then never materialised.
+  void fuse_pool(const PoolingLayer* pool, Blob* pool_top) { fused_pool_ = pool; pool_top_ = pool_top; }
+  int size() const { return size_; }
+  double alpha() const { return alpha_; }
+  double beta() const { return beta_; }
+  double k() const { return k_; }
 
  private:
+  const PoolingLayer* fused_pool_ = nullptr;
+  Blob* pool_top_ = nullptr;
   int size_;
   double alpha_, beta_, k_;
   int n_ = 0, c_ = 0, hw_ = 0;

@@ -1,0 +1,383 @@
+// ops_lrnpool.cu — LRN (ACROSS_CHANNELS) fused with the MAX pooling that consumes
+// its top (AlexNet norm1 -> pool1, norm2 -> pool2).  Neither layer exists in the
+// reference; the semantics are Caffe's, exactly those of the unfused kernels
+// (ops_layers.cu lrn_fwd_ring / lrn_bwd_ring, ops_pool.cu max_pool_fwd /
+// max_pool_bwd_k): the same expressions in the same order, so the LRN top, the
+// pooled top, the int32 argmax mask and the bottom gradient are bit-identical
+// to LRN followed by Pooling (tests/test_gpu_kernels.py checks that).
+//
+// HBM traffic per element of the LRN bottom x (f32; AlexNet conv1: 74.3 M):
+//   unfused forward   x + y + scale (LRN) + y + pool/mask (1/4.5 each)   ~ 18 B
+//   fused forward     x + y (kept: the blob stays observable) + pool/mask ~  9.8 B
+//   unfused backward  pool dy/mask, norm dy (LRN: x, y, scale, dy, dx)   ~ 25.8 B
+//   fused backward    x + pool dy/mask + dx (scale, y and the LRN top diff are
+//                     recomputed in registers; nothing else is stored)   ~  9.8 B
+// The scale tensor is not stored at all.
+//
+// Forward: one block per (image, band of TR pooled rows); one thread per input
+// pixel of the band's (TR-1)*S+K input rows walks the channels with the x ring
+// of lrn_fwd_ring, G channels per step, and parks the normalised values in a
+// double-buffered shared tile from which the block's pool threads take the
+// 3x3 / 2x2 window maxima (one __syncthreads per G channels).  Halo rows between
+// bands are computed twice (12% more x reads, from L2) and stored once.
+// Backward: one thread per input pixel walks the channels; for the entering
+// channel e = c + pre it recomputes scale(e) = k + alpha/n * sum x^2, y(e) and the
+// LRN top diff (the pool backward gather over the <= R x R windows holding the
+// pixel, in max_pool_bwd_k's order), then dx(c) from the rings of lrn_bwd_ring.
+#include "launch.cuh"
+
+namespace cdnn {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T lrn_neg_pow(T sc, T beta) {  // == ops_layers.cu neg_pow
+  if constexpr (sizeof(T) == 4) return exp2f(-beta * log2f(sc));
+  else return pow(sc, -beta);
+}
+
+constexpr int kG = 4;  // channels per step (loads in flight; one block barrier per step)
+
+struct LrnPoolGeom {
+  int N, C, H, W, PH, PW;
+  int TR, rows_in;  // pooled rows per band, input rows per band
+  int bands;
+};
+
+template <typename T, int SIZE, int K, int S>
+__global__ void lrn_maxpool_fwd(const T* __restrict__ x, T* __restrict__ ynorm, T* __restrict__ ypool,
+                                int* __restrict__ mask, LrnPoolGeom g, T alpha, T beta, T k, bool relu) {
+  constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
+  extern __shared__ uint8_t smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);  // [2][kG][rows_in * W]
+  const int band = blockIdx.x, img = blockIdx.y;
+  const int pr0 = band * g.TR, pr1 = min(g.PH, pr0 + g.TR);
+  const int r0 = pr0 * S, r1 = min(g.H, (pr1 - 1) * S + K);
+  // rows whose LRN top this band stores (halo rows belong to the next band)
+  const int own1 = band + 1 == g.bands ? g.H : min(g.H, pr1 * S);
+  const int npix = (r1 - r0) * g.W, tsz = g.rows_in * g.W;
+  const int HW = g.H * g.W, PHW = g.PH * g.PW;
+  const T aN = alpha / T(SIZE);
+  const int p = threadIdx.x;
+  const bool active = p < npix;
+  const int h = r0 + (active ? p / g.W : 0);
+  const int64_t base = int64_t(img) * g.C * HW + int64_t(h) * g.W + (active ? p % g.W : 0);
+  const bool own = active && h < own1;
+  T xr[SIZE];
+#pragma unroll
+  for (int j = 0; j < SIZE; ++j) {
+    const int cc = j - pre;
+    xr[j] = (active && cc >= 0 && cc < g.C) ? __ldg(x + base + int64_t(cc) * HW) : T(0);
+  }
+  const int items = kG * (pr1 - pr0) * g.PW;
+  for (int c0 = 0, step = 0; c0 < g.C; c0 += kG, ++step) {
+    T* buf = tile + (step & 1) * kG * tsz;
+    if (active) {
+      T nx[kG];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int cin = c0 + u + post + 1;
+        nx[u] = cin < g.C ? __ldg(x + base + int64_t(cin) * HW) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int c = c0 + u;
+        if (c >= g.C) break;
+        T sum = T(0);
+#pragma unroll
+        for (int j = 0; j < SIZE; ++j) sum += xr[j] * xr[j];
+        const T sc = k + aN * sum;
+        const T yv = xr[pre] * lrn_neg_pow(sc, beta);
+        buf[u * tsz + p] = yv;
+        if (own) ynorm[base + int64_t(c) * HW] = yv;
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
+        xr[SIZE - 1] = nx[u];
+      }
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int u = it / ((pr1 - pr0) * g.PW);
+      const int c = c0 + u;
+      if (c >= g.C) continue;
+      const int rem = it - u * ((pr1 - pr0) * g.PW);
+      const int prl = rem / g.PW, pw = rem - prl * g.PW;
+      const int hs = (pr0 + prl) * S, ws = pw * S;
+      const int he = min(hs + K, g.H), we = min(ws + K, g.W);
+      const T* t = buf + u * tsz;
+      T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
+      int arg = -1;
+      for (int hh = hs; hh < he; ++hh)
+        for (int ww = ws; ww < we; ++ww) {
+          const T v = t[(hh - r0) * g.W + ww];
+          if (v > best) { best = v; arg = hh * g.W + ww; }
+        }
+      const int64_t o = (int64_t(img) * g.C + c) * PHW + int64_t(pr0 + prl) * g.PW + pw;
+      ypool[o] = relu ? (best > T(0) ? best : T(0)) : best;
+      mask[o] = arg;
+    }
+    // the next step writes the other buffer; the one after waits at its barrier
+  }
+}
+
+template <typename T, int SIZE, int K, int S>
+__global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
+                                                       const int* __restrict__ mask, T* __restrict__ dx,
+                                                       LrnPoolGeom g, T alpha, T beta, T k, bool gate_x) {
+  constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
+  constexpr int R = (K + S - 1) / S;
+  const int HW = g.H * g.W, PHW = g.PH * g.PW;
+  const int64_t pixels = int64_t(g.N) * HW;
+  const T aN = alpha / T(SIZE);
+  const T coef = T(2) * alpha * beta / T(SIZE);
+  for (int64_t pix = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; pix < pixels;
+       pix += int64_t(gridDim.x) * blockDim.x) {
+    const int img = int(pix / HW), hw = int(pix - int64_t(img) * HW);
+    const int h = hw / g.W, w = hw - (hw / g.W) * g.W;
+    const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
+    const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
+    const int64_t base = int64_t(img) * g.C * HW + hw;
+    const int64_t pbase = int64_t(img) * g.C * PHW + int64_t(phs) * g.PW + pws;
+    // the LRN top diff of channel cc at this pixel: max_pool_bwd_k's gather
+    auto gather = [&](int cc, int (&m)[R][R], T (&v)[R][R]) {
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          const bool ok = cc < g.C && phs + a < phe && pws + b < pwe;
+          const int64_t o = pbase + int64_t(cc) * PHW + a * g.PW + b;
+          m[a][b] = ok ? __ldg(mask + o) : -1;
+          v[a][b] = ok ? __ldg(pdy + o) : T(0);
+        }
+    };
+    auto ndy_of = [&](const int (&m)[R][R], const T (&v)[R][R]) {
+      T s = T(0);
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int b = 0; b < R; ++b)
+          if (m[a][b] == hw) s += v[a][b];
+      return s;
+    };
+    // rings over channels c - post .. c + pre: t = dy*y/scale, dy, scale (lrn_bwd_ring).
+    // Before the step for channel c they hold channels c-1-post .. c-1+pre (index 0 is
+    // shifted out first); so ahead of c = 0, index j holds channel j - 1 - post.
+    T tr[SIZE], dyr[SIZE], scr[SIZE];
+#pragma unroll
+    for (int j = 0; j < SIZE; ++j) { dyr[j] = T(0); scr[j] = T(1); tr[j] = T(0); }
+#pragma unroll
+    for (int j = 1; j < SIZE; ++j) {
+      const int cc = j - 1 - post;  // channels -post .. pre-1; only 0 .. pre-1 are real
+      if (cc >= 0 && cc < g.C) {
+        T sum = T(0);
+#pragma unroll
+        for (int q = 0; q < SIZE; ++q) {
+          const int cx = cc - pre + q;
+          const T xv = (cx >= 0 && cx < g.C) ? __ldg(x + base + int64_t(cx) * HW) : T(0);
+          sum += xv * xv;
+        }
+        const T sc = k + aN * sum;
+        const T yv = __ldg(x + base + int64_t(cc) * HW) * lrn_neg_pow(sc, beta);
+        int m[R][R];
+        T v[R][R];
+        gather(cc, m, v);
+        const T d = ndy_of(m, v);
+        dyr[j] = d;
+        scr[j] = sc;
+        tr[j] = d * yv / sc;
+      }
+    }
+    // x ring: x(c .. c + SIZE - 1), the window of the entering channel c + pre
+    T xr[SIZE];
+#pragma unroll
+    for (int j = 0; j < SIZE - 1; ++j) xr[j] = (j < g.C) ? __ldg(x + base + int64_t(j) * HW) : T(0);
+    xr[SIZE - 1] = T(0);
+    for (int c0 = 0; c0 < g.C; c0 += kG) {
+      T nx[kG];
+      int nm[kG][R][R];
+      T nv[kG][R][R];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int cin = c0 + u + SIZE - 1;
+        nx[u] = cin < g.C ? __ldg(x + base + int64_t(cin) * HW) : T(0);
+        gather(c0 + u + pre, nm[u], nv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int c = c0 + u;
+        if (c >= g.C) break;
+        xr[SIZE - 1] = nx[u];  // x(c .. c + SIZE - 1)
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; scr[j] = scr[j + 1]; }
+        const int e = c + pre;
+        if (e < g.C) {
+          T sum = T(0);
+#pragma unroll
+          for (int j = 0; j < SIZE; ++j) sum += xr[j] * xr[j];
+          const T sc = k + aN * sum;
+          const T yv = xr[pre] * lrn_neg_pow(sc, beta);
+          const T d = ndy_of(nm[u], nv[u]);
+          dyr[SIZE - 1] = d;
+          scr[SIZE - 1] = sc;
+          tr[SIZE - 1] = d * yv / sc;
+        } else {
+          dyr[SIZE - 1] = T(0); scr[SIZE - 1] = T(1); tr[SIZE - 1] = T(0);
+        }
+        T acc = T(0);
+#pragma unroll
+        for (int j = 0; j < SIZE; ++j) acc += tr[j];
+        const T xc = xr[0];
+        const T gval = dyr[post] * lrn_neg_pow(scr[post], beta) - coef * xc * acc;
+        dx[base + int64_t(c) * HW] = (!gate_x || xc > T(0)) ? gval : T(0);
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
+      }
+    }
+  }
+}
+
+LrnPoolGeom lrn_pool_geom(const PoolDescSlot& d, int smem_cap_elems) {
+  const auto& p = d.p;
+  LrnPoolGeom g{p.n, p.c, p.h, p.w, d.PH, d.PW, 1, 0, 0};
+  const int K = p.kernel_h, S = p.stride_h;
+  // band height: about 512 input pixels per block
+  int tr = std::max(1, ((512 / std::max(1, p.w)) - K) / S + 1);
+  tr = std::min(tr, d.PH);
+  while (tr > 1 && ((tr - 1) * S + K) * p.w > std::min(1024, smem_cap_elems)) --tr;
+  g.TR = tr;
+  g.rows_in = (tr - 1) * S + K;
+  g.bands = (d.PH + tr - 1) / tr;
+  return g;
+}
+
+bool fusable(const PoolDescSlot& d, int size) {
+  const auto& p = d.p;
+  const bool window = p.kernel_h == p.kernel_w && p.stride_h == p.stride_w &&
+                      ((p.kernel_h == 3 && p.stride_h == 2) || (p.kernel_h == 2 && p.stride_h == 2));
+  return p.method == CDNN_POOL_MAX && !p.global_pooling && p.pad_h == 0 && p.pad_w == 0 && window &&
+         (size == 3 || size == 5) && p.kernel_h * p.w <= 1024 &&
+         uint64_t(p.n) * p.c * p.h * p.w < (1ull << 31);
+}
+
+template <typename T, int SIZE, int K, int S>
+void launch_fwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, T* yn, T* yp, int* m, double alpha,
+                double beta, double k, bool relu) {
+  const LrnPoolGeom g = lrn_pool_geom(d, 1024);
+  const int threads = ((g.rows_in * g.W + 31) / 32) * 32;
+  const size_t smem = size_t(2) * kG * g.rows_in * g.W * sizeof(T);
+  lrn_maxpool_fwd<T, SIZE, K, S><<<dim3(g.bands, g.N), threads, smem, st>>>(x, yn, yp, m, g, T(alpha), T(beta),
+                                                                            T(k), relu);
+  check_launch("lrn_maxpool_fwd");
+  count_launch(c);
+}
+
+template <typename T, int SIZE, int K, int S>
+void launch_bwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, const T* pdy, const int* m, T* dx,
+                double alpha, double beta, double k, bool gate_x) {
+  const LrnPoolGeom g = lrn_pool_geom(d, 1024);
+  const int64_t pixels = int64_t(g.N) * g.H * g.W;
+  lrn_maxpool_bwd<T, SIZE, K, S><<<grid_for(pixels, 256), 256, 0, st>>>(x, pdy, m, dx, g, T(alpha), T(beta), T(k),
+                                                                         gate_x);
+  check_launch("lrn_maxpool_bwd");
+  count_launch(c);
+}
+
+template <class F>
+void dispatch_shape(const PoolDescSlot& d, int size, F&& f) {
+  const int K = d.p.kernel_h;
+  if (size == 5 && K == 3) f(std::integral_constant<int, 5>{}, std::integral_constant<int, 3>{});
+  else if (size == 5 && K == 2) f(std::integral_constant<int, 5>{}, std::integral_constant<int, 2>{});
+  else if (size == 3 && K == 3) f(std::integral_constant<int, 3>{}, std::integral_constant<int, 3>{});
+  else f(std::integral_constant<int, 3>{}, std::integral_constant<int, 2>{});
+}
+
+}  // namespace
+}  // namespace cdnn
+
+using namespace cdnn;
+
+extern "C" {
+
+int cdnn_lrn_pool_supported(cdnn_ctx ctx, cdnn_handle pool_desc_h, int local_size, int* out) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    *out = fusable(pool_desc(c, pool_desc_h), local_size) ? 1 : 0;
+  });
+}
+
+int cdnn_lrn_pool_forward(cdnn_ctx ctx, cdnn_handle pool_desc_h, cdnn_handle x, cdnn_handle lrn_top,
+                          cdnn_handle pool_top, cdnn_handle mask, int local_size, double alpha, double beta, double k,
+                          int flags, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    const PoolDescSlot d = pool_desc(c, pool_desc_h);
+    if (!fusable(d, local_size)) fail(CDNN_INVALID_ARGUMENT, "lrn_pool: unsupported LRN / pooling combination");
+    BufferSlot& X = buffer(c, x, "lrn_pool x");
+    BufferSlot& YN = buffer(c, lrn_top, "lrn_pool lrn top");
+    BufferSlot& YP = buffer(c, pool_top, "lrn_pool pool top");
+    BufferSlot& M = buffer(c, mask, "lrn_pool mask");
+    const uint64_t nin = uint64_t(d.p.n) * d.p.c * d.p.h * d.p.w, nout = uint64_t(d.p.n) * d.p.c * d.PH * d.PW;
+    require_len(X, nin, "lrn_pool x");
+    require_len(YN, nin, "lrn_pool lrn top");
+    require_len(YP, nout, "lrn_pool pool top");
+    require_len(M, nout, "lrn_pool mask");
+    require_dtype(YN, X.dtype, "lrn_pool");
+    require_dtype(YP, X.dtype, "lrn_pool");
+    require_dtype(M, CDNN_I32, "lrn_pool mask");
+    DeviceGuard dg(c);
+    cudaStream_t st = stream_of(c, stream);
+    const bool relu = (flags & CDNN_POOL_RELU) != 0;
+    dispatch_shape(d, local_size, [&](auto sz, auto kk) {
+      constexpr int SIZE = decltype(sz)::value, K = decltype(kk)::value;
+      if (X.dtype == CDNN_F32)
+        launch_fwd<float, SIZE, K, 2>(c, st, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<float*>(YN.dev),
+                                      reinterpret_cast<float*>(YP.dev), reinterpret_cast<int*>(M.dev), alpha, beta, k,
+                                      relu);
+      else if (X.dtype == CDNN_F64)
+        launch_fwd<double, SIZE, K, 2>(c, st, d, reinterpret_cast<const double*>(X.dev),
+                                       reinterpret_cast<double*>(YN.dev), reinterpret_cast<double*>(YP.dev),
+                                       reinterpret_cast<int*>(M.dev), alpha, beta, k, relu);
+      else
+        fail(CDNN_INVALID_ARGUMENT, "lrn_pool: floating buffers required");
+    });
+  });
+}
+
+int cdnn_lrn_pool_backward(cdnn_ctx ctx, cdnn_handle pool_desc_h, cdnn_handle x, cdnn_handle pool_dy,
+                           cdnn_handle mask, cdnn_handle dx, cdnn_handle gate, int local_size, double alpha,
+                           double beta, double k, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    const PoolDescSlot d = pool_desc(c, pool_desc_h);
+    if (!fusable(d, local_size)) fail(CDNN_INVALID_ARGUMENT, "lrn_pool: unsupported LRN / pooling combination");
+    if (gate && gate != x) fail(CDNN_INVALID_ARGUMENT, "lrn_pool backward: the ReLU gate must be the LRN bottom x");
+    BufferSlot& X = buffer(c, x, "lrn_pool_bwd x");
+    BufferSlot& DY = buffer(c, pool_dy, "lrn_pool_bwd pool dy");
+    BufferSlot& M = buffer(c, mask, "lrn_pool_bwd mask");
+    BufferSlot& DX = buffer(c, dx, "lrn_pool_bwd dx");
+    const uint64_t nin = uint64_t(d.p.n) * d.p.c * d.p.h * d.p.w, nout = uint64_t(d.p.n) * d.p.c * d.PH * d.PW;
+    require_len(X, nin, "lrn_pool_bwd x");
+    require_len(DX, nin, "lrn_pool_bwd dx");
+    require_len(DY, nout, "lrn_pool_bwd pool dy");
+    require_len(M, nout, "lrn_pool_bwd mask");
+    require_dtype(DX, X.dtype, "lrn_pool_bwd");
+    require_dtype(DY, X.dtype, "lrn_pool_bwd");
+    require_dtype(M, CDNN_I32, "lrn_pool_bwd mask");
+    DeviceGuard dg(c);
+    cudaStream_t st = stream_of(c, stream);
+    dispatch_shape(d, local_size, [&](auto sz, auto kk) {
+      constexpr int SIZE = decltype(sz)::value, K = decltype(kk)::value;
+      if (X.dtype == CDNN_F32)
+        launch_bwd<float, SIZE, K, 2>(c, st, d, reinterpret_cast<const float*>(X.dev),
+                                      reinterpret_cast<const float*>(DY.dev), reinterpret_cast<const int*>(M.dev),
+                                      reinterpret_cast<float*>(DX.dev), alpha, beta, k, gate != 0);
+      else if (X.dtype == CDNN_F64)
+        launch_bwd<double, SIZE, K, 2>(c, st, d, reinterpret_cast<const double*>(X.dev),
+                                       reinterpret_cast<const double*>(DY.dev), reinterpret_cast<const int*>(M.dev),
+                                       reinterpret_cast<double*>(DX.dev), alpha, beta, k, gate != 0);
+      else
+        fail(CDNN_INVALID_ARGUMENT, "lrn_pool: floating buffers required");
+    });
+  });
+}
+
+}  // extern "C"

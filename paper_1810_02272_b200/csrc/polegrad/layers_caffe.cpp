@@ -115,6 +115,7 @@ std::vector<Shape> LRNLayer::setup(const std::vector<Shape>& s, const std::share
 void LRNLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
   if (top_clobbered_ || bottom_clobbered_)
     throw ModelError("layer '" + spec_.name + "': LRN data rewritten in place before backward is unsupported");
+  if (fused_pool_) return;  // computed by the consuming pooling layer's forward
   Registry& reg = bottoms[0]->registry();
   cdnn_ok(cdnn_lrn_forward(reg.context(), bottoms[0]->gpu_data(), tops[0]->overwrite_gpu_data(),
                            scale_->overwrite_gpu_data(), n_, c_, hw_, size_, alpha_, beta_, k_, reg.stream()),
@@ -125,6 +126,13 @@ void LRNLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bott
   if (!propagate_down(0)) return;
   Registry& reg = bottoms[0]->registry();
   const cdnn_handle x = bottoms[0]->gpu_data();
+  if (fused_pool_) {  // pooling backward + LRN backward in one pass (ops_lrnpool.cu)
+    cdnn_ok(cdnn_lrn_pool_backward(reg.context(), fused_pool_->desc(), x, pool_top_->gpu_diff(),
+                                   fused_pool_->mask_handle(), bottoms[0]->overwrite_gpu_diff(), relu_gate_ ? x : 0,
+                                   size_, alpha_, beta_, k_, reg.stream()),
+            "LRN + Pooling backward");
+    return;
+  }
   cdnn_ok(cdnn_lrn_backward_ex(reg.context(), x, tops[0]->gpu_data(), scale_->gpu_data(), tops[0]->gpu_diff(),
                                bottoms[0]->overwrite_gpu_diff(), n_, c_, hw_, size_, alpha_, beta_,
                                relu_gate_ ? x : 0, reg.stream()),

@@ -180,6 +180,14 @@ std::vector<Shape> PoolingLayer::setup(const std::vector<Shape>& s, const std::s
 
 void PoolingLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
   Registry& reg = *reg_;
+  if (fused_lrn_) {  // LRN + pooling in one pass over the LRN's bottom (ops_lrnpool.cu)
+    const LRNLayer& l = *fused_lrn_;
+    cdnn_ok(cdnn_lrn_pool_forward(reg.context(), desc_, lrn_bottom_->gpu_data(), bottoms[0]->overwrite_gpu_data(),
+                                  tops[0]->overwrite_gpu_data(), mask_, l.size(), l.alpha(), l.beta(), l.k(),
+                                  fused_relu_ ? CDNN_POOL_RELU : 0, reg.stream()),
+            "LRN + Pooling forward");
+    return;
+  }
   const cdnn_handle x = bottoms[0]->gpu_data();
   cdnn_ok(cdnn_pool_forward_ex(reg.context(), desc_, x, tops[0]->overwrite_gpu_data(), mask_,
                                fused_relu_ ? CDNN_POOL_RELU : 0, reg.stream()),
@@ -187,7 +195,7 @@ void PoolingLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const
 }
 
 void PoolingLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
-  if (!propagate_down(0)) return;
+  if (!propagate_down(0) || fused_lrn_) return;  // fused: runs inside LRNLayer::backward
   Registry& reg = *reg_;
   const cdnn_handle dy = tops[0]->gpu_diff();
   const cdnn_handle gate = relu_gate_ ? bottoms[0]->gpu_data() : 0;

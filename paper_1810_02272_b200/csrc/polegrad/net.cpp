@@ -210,6 +210,27 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
     consumer->set_relu_gate(true);
     relu->set_backward_fused(true);
   }
+  // Fuse LRN with the MAX pooling that is its top's only reader (AlexNet norm -> pool):
+  // one pass over the LRN bottom forward and backward (ops_lrnpool.cu); the LRN top
+  // stays materialised, its diff and the scale tensor are not.
+  for (std::size_t i = 0; !compat && i + 1 < layers_.size(); ++i) {
+    auto* lrn = dynamic_cast<LRNLayer*>(layers_[i].get());
+    auto* pool = dynamic_cast<PoolingLayer*>(layers_[i + 1].get());
+    if (!lrn || !pool || !pool->is_max() || bottoms_[i + 1].size() != 1 || bottoms_[i + 1][0] != tops_[i][0]) continue;
+    Blob* t = tops_[i][0];
+    bool other_use = t == bottoms_[i][0];
+    for (std::size_t k = i + 2; k < layers_.size() && !other_use; ++k) {
+      for (Blob* b : bottoms_[k])
+        if (b == t) other_use = true;
+      for (Blob* b : tops_[k])
+        if (b == t) other_use = true;
+    }
+    int ok = 0;
+    cdnn_ok(cdnn_lrn_pool_supported(registry_->context(), pool->desc(), lrn->size(), &ok), "LRN + Pooling fusion");
+    if (other_use || !ok) continue;
+    lrn->fuse_pool(pool, tops_[i + 1][0]);
+    pool->fuse_lrn(lrn, bottoms_[i][0]);
+  }
   pack_params();
 }
 

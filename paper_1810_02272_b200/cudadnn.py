@@ -45,7 +45,8 @@ EXPORTS = [
     "cdnn_conv_backward_filter", "cdnn_pool_forward", "cdnn_pool_backward", "cdnn_pool_backward_ex", "cdnn_relu_forward",
     "cdnn_relu_backward", "cdnn_sigmoid_forward", "cdnn_sigmoid_backward", "cdnn_softmax_forward",
     "cdnn_softmax_backward", "cdnn_softmax_loss_forward", "cdnn_softmax_loss_backward", "cdnn_solver_apply",
-    "cdnn_nccl_available", "cdnn_nccl_unique_id", "cdnn_nccl_comm_create", "cdnn_nccl_comm_info", "cdnn_allreduce_sum",
+    "cdnn_nccl_available", "cdnn_nccl_unique_id", "cdnn_nccl_comm_create", "cdnn_nccl_comm_info", "cdnn_lrn_pool_supported", "cdnn_lrn_pool_forward",
+    "cdnn_lrn_pool_backward", "cdnn_allreduce_sum",
     "cdnn_broadcast", "cdnn_copy_range", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_lrn_backward_ex", "cdnn_dropout", "cdnn_counter_increment",
     "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
     "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
@@ -133,6 +134,9 @@ def load() -> C.CDLL:
             "cdnn_nccl_available": ([C.POINTER(i)], i), "cdnn_nccl_unique_id": ([C.c_char_p], i),
             "cdnn_nccl_comm_create": ([vp, i, i, C.c_char_p, ph], i),
             "cdnn_nccl_comm_info": ([vp, u64, C.POINTER(i), C.POINTER(i)], i),
+            "cdnn_lrn_pool_supported": ([vp, h, i, C.POINTER(i)], i),
+            "cdnn_lrn_pool_forward": ([vp, h, h, h, h, h, i, d, d, d, i, h], i),
+            "cdnn_lrn_pool_backward": ([vp, h, h, h, h, h, h, i, d, d, d, h], i),
             "cdnn_allreduce_sum": ([vp, h, h, u64, u64, h], i), "cdnn_broadcast": ([vp, h, h, u64, i, h], i),
             "cdnn_lrn_forward": ([vp, h, h, h, i, i, i, i, d, d, d, h], i),
             "cdnn_lrn_backward": ([vp, h, h, h, h, h, i, i, i, i, d, d, h], i),

@@ -1,9 +1,15 @@
 """Oracle pinning and boundary-input parity on the CPU (no GPU needed).
 
 * reftests_ref  — the reference's own unit tests (backend, blob, layers, net,
-  solver, prototxt, imagedb: 88 cases / ~4.5k assertions, incl. the gemm / softmax / FD
-  known-answer tests of SURVEY §8(c)) compiled against the UNMODIFIED reference
-  core: the oracle is the reference, and this proves the build is faithful.
+  solver, prototxt, trainer, cartpole, imagedb: 111 cases / ~7.6k assertions, incl.
+  the gemm / softmax / FD known-answer tests of SURVEY §8(c) and the episode
+  finite-difference check trainer_test.cpp:242-290) compiled against the
+  UNMODIFIED reference core: the oracle is the reference, and this proves the
+  build is faithful.
+* acceptance_ref — the reference's acceptance program (acceptance.cpp, included
+  unmodified by oracle/acceptance_driver.cpp), criteria 1-7: the paper's Figure-6
+  and Figure-9 worked-example tables, the 20-seed finite-difference checks,
+  cart-pole learning, model round trips, sampler statistics, dynamics.
 * reftests_b200 prototxt cases — the same unmodified prototxt tests compiled
   against the B200 library's parser/printer (host code, runs without a GPU),
   in reference-compat mode; in extended mode exactly one assertion (that
@@ -29,7 +35,18 @@ def _run(args, env=None):
 def test_reference_suite_passes_on_reference_core():
     rc, out = _run([REF_BIN])
     assert rc == 0, out[-3000:]
-    assert "88 passed | 0 failed" in out
+    assert "111 passed | 0 failed" in out
+
+
+ACC_REF = os.path.join(ROOT, "oracle", "_ref", "acceptance_ref")
+
+
+@pytest.mark.skipif(not (os.path.exists(ACC_REF) and HAVE_REF), reason="acceptance_ref not built here")
+def test_reference_acceptance_criteria_pass_on_reference_core():
+    rc, out = _run([ACC_REF, "1", "2", "3", "4", "5", "6", "7"])
+    assert rc == 0, out[-3000:]
+    for i in range(1, 8):
+        assert f"PASS {i}/9" in out, out
 
 
 @pytest.mark.skipif(not (os.path.exists(B200_BIN) and HAVE_REF), reason="reftests_b200 not built here")

@@ -5,6 +5,7 @@ inputs rounded to nearest), accumulates in fp32; relative L2 error of a GEMM
 is ~1e-4..1e-3, so float checks use rel-L2 <= 2e-3 (north_star's TF32 bar);
 FP64 checks use 1e-12.
 """
+import ctypes as C
 import numpy as np
 import pytest
 import torch
@@ -435,3 +436,50 @@ def test_pool_fixed_window_kernels_equal_generic():
                            timeout=300, check=True)
         out[generic] = r.stdout.strip().splitlines()[-1]
     assert out["0"] == out["1"]
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("n,c,h,w,size,k,s", [(3, 96, 55, 55, 5, 3, 2),   # AlexNet norm1 -> pool1 shape
+                                              (2, 40, 27, 27, 5, 3, 2),   # norm2 -> pool2 shape
+                                              (2, 7, 13, 11, 3, 3, 2),    # ragged, C not a multiple of 4
+                                              (2, 6, 12, 10, 5, 2, 2),    # 2x2/2 windows
+                                              (1, 3, 9, 9, 5, 3, 2)])     # fewer channels than the window
+def test_lrn_pool_fused_bit_identical_to_unfused(ctx, dtype, n, c, h, w, size, k, s):
+    """cdnn_lrn_pool_forward / _backward (ops_lrnpool.cu) == LRN then MAX pooling, bit
+    for bit: the LRN top, the pooled top, the argmax mask and the bottom gradient
+    (with the fused ReLU gate on x)."""
+    rng = np.random.default_rng(n * c + h + size)
+    dt = NP[dtype]
+    x = rng.standard_normal((n, c, h, w)).astype(dt)  # negatives exercise the ReLU gate
+    alpha, beta, kk = 1e-4 * 100, 0.75, 2.0
+    d = ctx.pool_desc(n, c, h, w, cd.POOL_MAX, k, s, 0)
+    ok = C.c_int()
+    ctx.call("cdnn_lrn_pool_supported", d, size, C.byref(ok))
+    assert ok.value == 1
+    ph, pw = ctx.pool_output_shape(d)[2:]
+    nin, nout = x.size, n * c * ph * pw
+    hx = ctx.upload(x)
+    # unfused: LRN forward, pool forward; pool backward, LRN backward (gate = x)
+    hy, hs, hp, hm = ctx.alloc(nin, dtype), ctx.alloc(nin, dtype), ctx.alloc(nout, dtype), ctx.alloc(nout, cd.I32)
+    ctx.call("cdnn_lrn_forward", hx, hy, hs, n, c, h * w, size, alpha, beta, kk, 0)
+    ctx.call("cdnn_pool_forward", d, hy, hp, hm, 0)
+    dy = rng.standard_normal(nout).astype(dt)
+    hdy = ctx.upload(dy)
+    hdn, hdx = ctx.alloc(nin, dtype), ctx.alloc(nin, dtype)
+    ctx.call("cdnn_pool_backward", d, hdy, hm, hdn, 0)
+    ctx.call("cdnn_lrn_backward_ex", hx, hy, hs, hdn, hdx, n, c, h * w, size, alpha, beta, hx, 0)
+    # fused
+    fy, fp, fm, fdx = ctx.alloc(nin, dtype), ctx.alloc(nout, dtype), ctx.alloc(nout, cd.I32), ctx.alloc(nin, dtype)
+    ctx.call("cdnn_lrn_pool_forward", d, hx, fy, fp, fm, size, alpha, beta, kk, 0, 0)
+    ctx.call("cdnn_lrn_pool_backward", d, hx, hdy, hm, fdx, hx, size, alpha, beta, kk, 0)
+    assert np.array_equal(ctx.read(fy), ctx.read(hy))
+    assert np.array_equal(ctx.read(fp), ctx.read(hp))
+    assert np.array_equal(ctx.read(fm), ctx.read(hm))
+    assert np.array_equal(ctx.read(fdx), ctx.read(hdx))
+    # and the fused backward without the gate == pool backward + plain LRN backward
+    ctx.call("cdnn_lrn_backward", hx, hy, hs, hdn, hdx, n, c, h * w, size, alpha, beta, 0)
+    ctx.call("cdnn_lrn_pool_backward", d, hx, hdy, hm, fdx, 0, size, alpha, beta, kk, 0)
+    assert np.array_equal(ctx.read(fdx), ctx.read(hdx))
+    for hnd in (hx, hy, hs, hp, hm, hdy, hdn, hdx, fy, fp, fm, fdx):
+        ctx.free(hnd)
+    ctx.call("cdnn_desc_free", d)
