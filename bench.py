@@ -56,6 +56,12 @@ WORKLOADS = {
                     solver=dict(method="sgd", lr=0.001, momentum=0.9, weight_decay=5e-4)),
     "resnet20": dict(batch=128, img=(3, 32, 32), classes=10, ref_batch=8, cpu_batch=16,
                      solver=dict(method="sgd", lr=0.1, momentum=0.9, weight_decay=1e-4)),
+    # configs[2]: the reference's pg_softmax graph (4-10-2 + Softmax + MemoryLoss) at batch
+    # 1024; the unit is Cart-Pole states per second (BASELINE.md §3 times the same
+    # iteration on the unmodified reference Net: enqueue, forward, logits diff,
+    # backward_from("logits"), plain SGD)
+    "pg_mlp": dict(batch=1024, img=(4, 1, 1), classes=2, ref_batch=1024, cpu_batch=1024,
+                   solver=dict(method="sgd", lr=0.001, momentum=0.0, weight_decay=0.0)),
 }
 DEFAULT_WORKLOAD = "alexnet"
 WORKLOAD = DEFAULT_WORKLOAD
@@ -273,24 +279,50 @@ def cpu_baseline_sample(iters: int = 2) -> dict:
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                 "sample": "oracle/_ref not built on this host"}
     cb = WORKLOADS[WORKLOAD]["cpu_batch"]
-    text = model_text(cb)
-    net = pyoracle.OracleNet(text, seed=1, dtype="f32")
-    solver = pyoracle.OracleSolver(net, **SOLVER)
-    rng = np.random.default_rng(2)
-    x = rng.uniform(-1, 1, (cb,) + IMG)
-    y = np.floor(rng.uniform(0, 1, cb) * CLASSES)
-    t0 = time.perf_counter()
-    for _ in range(iters):
-        net.set_batch(x, y)
-        net.forward()
-        net.backward()
-        solver.apply()
-    dt = time.perf_counter() - t0
-    return {"value": iters * cb / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+    dt = ref_steps(cb, iters, 0, 2)
+    unit = "states/s" if WORKLOAD == "pg_mlp" else UNIT
+    what = ("the UNMODIFIED reference Net (pg_softmax graph, reference prototxt parser; enqueue, forward, "
+            "logits diff, backward_from, SGD)" if WORKLOAD == "pg_mlp" else
+            "unmodified reference core (kernels::gemm, InnerProduct, ReLU, solver) + reference-style "
+            "Convolution/Pooling/SoftmaxWithLoss extension")
+    return {"value": iters * cb / dt, "unit": unit, "cores": 1, "kind": "reference",
             "ms_per_step": 1000 * dt / iters, **host_cpu(),
-            "sample": f"{iters} iterations of {WORKLOAD} at batch {cb} (f32) on oracle/_ref: unmodified "
-                      f"reference core (kernels::gemm, InnerProduct, ReLU, solver) + reference-style "
-                      f"Convolution/Pooling/SoftmaxWithLoss extension, 1 thread"}
+            "sample": f"{iters} iterations of {WORKLOAD} at batch {cb} ({DTYPE}) on oracle/_ref: {what}, 1 thread"}
+
+
+def ref_steps(nb: int, steps: int, warmup: int, seed: int) -> float:
+    """Seconds for `steps` reference-CPU iterations of the workload at batch nb (after
+    `warmup` untimed ones) on oracle/_ref."""
+    from oracle import pyoracle
+    text = model_text(nb)
+    net = pyoracle.OracleNet(text, seed=1, dtype=DTYPE)
+    solver = pyoracle.OracleSolver(net, **SOLVER)
+    rng = np.random.default_rng(seed)
+    if WORKLOAD == "pg_mlp":
+        st, act, ret = pg_inputs(rng, 1, nb, np.float64)
+        g = rng.uniform(-1, 1, (nb, 2))  # modulated log-prob gradients at the logits
+
+        def one():
+            net.set_batch(st[0])
+            net.forward()
+            net.set_blob("logits", g, diff=True)
+            net.backward_from("logits")
+            solver.apply()
+    else:
+        x = rng.uniform(-1, 1, (nb,) + IMG)
+        y = np.floor(rng.uniform(0, 1, nb) * CLASSES)
+
+        def one():
+            net.set_batch(x, y)
+            net.forward()
+            net.backward()
+            solver.apply()
+    for _ in range(warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    return time.perf_counter() - t0
 
 
 # --------------------------------------------------------------------------------------
@@ -589,6 +621,92 @@ def run_b200(args) -> None:
 
 
 # --------------------------------------------------------------------------------------
+def pg_inputs(rng, n, batch, npd):
+    """Cart-Pole-shaped states (acceptance.cpp:518-522 ranges), sampled actions and
+    normalised returns (the modulated-gradient inputs of trainer.cpp:94-109)."""
+    lo = np.array([-2.0, -3.0, -0.3, -3.0])
+    st = (lo + (-2 * lo) * rng.uniform(0, 1, (n, batch, 4))).astype(npd).reshape(n, batch, 4, 1, 1)
+    act = np.floor(rng.uniform(0, 1, (n, batch)) * 2).astype(npd)
+    ret = rng.standard_normal((n, batch)).astype(npd)
+    return st, act, ret
+
+
+def run_pg_b200(args) -> None:
+    """configs[2]: one policy-gradient update of the whole episode batch on the device:
+    states in, forward, device-side modulated log-prob gradients at the logits
+    (Net::pg_backward, SURVEY §8(f) row 3), backward_from, SGD.  Launch / latency
+    bound (0.33 MFLOP); eager steps (the actions / returns H2D is part of the step)."""
+    from paper_1810_02272_b200 import cudadnn, polegrad
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and int(os.environ.get("RANK", "0")) != 0:
+        return  # the 288-byte gradient does not shard usefully: replicas only, rank 0 reports
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    npd = polegrad.NP_DTYPE[DTYPE]
+    net = polegrad.Net(model_text(BATCH), seed=1, dtype=DTYPE, device=local)
+    solver = polegrad.Solver(net, **SOLVER)
+    cx = CtxView(net.context_ptr())
+    rng = np.random.default_rng(2)
+    nb = 3
+    st, act, ret = pg_inputs(rng, nb, BATCH, npd)
+    pins = []
+    for j in range(nb):
+        px = cudadnn.PinnedBuffer((BATCH, 4, 1, 1), npd)
+        px.array[...] = st[j]
+        pins.append(px)
+    prob = cudadnn.PinnedBuffer((BATCH, 2), npd)
+
+    def step(i, feed):
+        if feed:
+            net.set_batch_ptr(pins[i % nb].ptr, None)
+        polegrad._check(net.lib, net.lib.pg_net_forward(net.ptr))
+        net.pg_backward(act[i % nb], ret[i % nb])
+        solver.apply()
+        if feed:  # the policy's probabilities back to the host (action sampling)
+            polegrad._check(net.lib, net.lib.pg_blob_get(net.ptr, b"prob", 0, C.c_void_p(prob.ptr)))
+
+    net.set_batch_ptr(pins[0].ptr, None)
+    l0 = cx.launches()
+    step(0, False)
+    net.sync()
+    launches = cx.launches() - l0
+    for i in range(args.warmup):
+        step(i, False)
+    net.sync()
+    out = {}
+    for key, feed in (("value", False), ("e2e", True)):
+        a, b = cx.event(), cx.event()
+        net.sync()
+        t0 = time.perf_counter()
+        with ClockSampler(local) as clk:
+            cx.record(a)
+            for i in range(args.steps):
+                step(i, feed)
+            cx.record(b)
+            net.sync()
+        out[key] = (cx.elapsed(a, b), 1000 * (time.perf_counter() - t0))
+        if key == "value":
+            clocks = clk.summary()
+    value = BATCH * args.steps / (out["value"][0] / 1000.0)
+    e2e = BATCH * args.steps / (out["e2e"][0] / 1000.0)
+    cpu = cpu_baseline_sample(args.cpu_iters * 50) if not args.no_cpu_baseline else None
+    esz = 8 if DTYPE == "f64" else 4
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "states/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(out["value"][0] / args.steps, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(), "data": "synthetic",
+        "config": config(1), "step": "eager (launch-bound: 0.33 MFLOP per step)",
+        "e2e": {"value": round(e2e, 1), "unit": "states/s", "ms_per_step": round(out["e2e"][0] / args.steps, 5),
+                "wall_ms_per_step": round(out["e2e"][1] / args.steps, 5),
+                "h2d_bytes_per_step": int(BATCH * 4 * esz + 2 * BATCH * esz),
+                "d2h_bytes_per_step": int(BATCH * 2 * esz)},
+        "gpu_launches": int(launches * args.steps), "launches_per_step": int(launches),
+        "roofline": {"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
+                     "kernel": "launch-bound (BASELINE.md §5: ideal 0.04 us)"},
+        "cpu_baseline": cpu, "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------
 def ref_batch_per_process(procs: int) -> int:
     """Images per reference step per host process: the bench batch split over the
     host cores, capped by the workload's bounded-sample size (AlexNet: one image per
@@ -598,25 +716,7 @@ def ref_batch_per_process(procs: int) -> int:
 
 def _ref_worker(args_tuple):
     steps, warmup, seed, nb = args_tuple
-    from oracle import pyoracle
-    text = model_text(nb)
-    net = pyoracle.OracleNet(text, seed=1, dtype=DTYPE)
-    solver = pyoracle.OracleSolver(net, **SOLVER)
-    rng = np.random.default_rng(seed)
-    x = rng.uniform(-1, 1, (nb,) + IMG)
-    y = np.floor(rng.uniform(0, 1, nb) * CLASSES)
-    for _ in range(warmup):
-        net.set_batch(x, y)
-        net.forward()
-        net.backward()
-        solver.apply()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        net.set_batch(x, y)
-        net.forward()
-        net.backward()
-        solver.apply()
-    return time.perf_counter() - t0
+    return ref_steps(nb, steps, warmup, seed)
 
 
 def run_reference(args) -> None:
@@ -643,13 +743,16 @@ def run_reference(args) -> None:
               + f", {args.warmup} warm-up + {steps} timed SGD iterations, slowest process timed; oracle/_ref: "
               f"unmodified reference core + reference-style conv/pool/loss extension, {DTYPE}")
     line = {
-        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "metric": METRIC, "value": round(value, 3), "unit": "states/s" if WORKLOAD == "pg_mlp" else UNIT,
+        "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": round(1000 * t / steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic", "impl": "reference",
         "config": config(world),
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": "reference",
+        "cpu_baseline": {"value": round(value, 3), "unit": "states/s" if WORKLOAD == "pg_mlp" else UNIT,
+                         "cores": procs, "kind": "reference",
                          "sample": sample, **host_cpu()},
-        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": round(value, 3), "unit": "states/s" if WORKLOAD == "pg_mlp" else UNIT,
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -690,6 +793,8 @@ def main() -> None:
         log("note: timing rules ask for >= 3 warm-up steps")
     if args.impl == "reference":
         run_reference(args)
+    elif WORKLOAD == "pg_mlp":
+        run_pg_b200(args)
     else:
         run_b200(args)
 

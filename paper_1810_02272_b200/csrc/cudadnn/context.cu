@@ -200,12 +200,7 @@ const CUtensorMap* tmap_generic(Ctx* c, const float* ptr, int rank, const uint64
                                 : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                 : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
-  const char* l2e = std::getenv("CDNN_TMA_L2");
-  const int l2 = l2e ? std::atoi(l2e) : 0;
-  const CUtensorMapL2promotion promo = l2 == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                                       : l2 == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                       : l2 == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                                 : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<float*>(ptr), gd, gs,
                            bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(CDNN_CUDA_ERROR, "cuTensorMapEncodeTiled (generic) failed (" + std::to_string(int(r)) + ")");

@@ -21,30 +21,6 @@
 namespace cdnn {
 namespace {
 
-bool conv_tma_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("CDNN_CONV_TMA");
-    return !(v && std::string(v) == "0");
-  }();
-  return on;
-}
-
-bool cf_route_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("CDNN_CONV_CF");
-    return !(v && std::string(v) == "0");
-  }();
-  return on;
-}
-
-bool conv_tap_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("CDNN_CONV_TAP");
-    return !(v && std::string(v) == "0");
-  }();
-  return on;
-}
-
 // Group-aware repack of W[Co][Cg][R][S] into the per-tap K-major operand, padded to
 // kpad channels, (hi, lo) TF32 split:
 //   forward : dst[tap][co][ci]      (ci within the group)
@@ -91,37 +67,8 @@ void launch_conv_tap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const CUtenso
     CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_smem[c->device & 15] = smem;
   }
-  static const bool trace = std::getenv("CDNN_TAP_TRACE") != nullptr;
-  if (!trace) {
-    kern<<<grid, tctap::kThreads, smem, st>>>(twh, twl, a);
-    check_launch("conv_tap_kernel");
-    count_launch(c);
-    return;
-  }
-  // debug timeline: per-CTA globaltimer stamps, printed as offsets from the earliest start
-  const size_t n = size_t(grid.x) * tctap::kTraceSlots;
-  unsigned long long* dbg = nullptr;
-  CDNN_CUDA(cudaMalloc(&dbg, n * 8));
-  CDNN_CUDA(cudaMemset(dbg, 0, n * 8));
-  tctap::TapArgs at = a;
-  at.trace = dbg;
-  CDNN_CUDA(cudaStreamSynchronize(st));
-  kern<<<grid, tctap::kThreads, smem, st>>>(twh, twl, at);
+  kern<<<grid, tctap::kThreads, smem, st>>>(twh, twl, a);
   check_launch("conv_tap_kernel");
-  CDNN_CUDA(cudaStreamSynchronize(st));
-  std::vector<unsigned long long> h(n);
-  CDNN_CUDA(cudaMemcpy(h.data(), dbg, n * 8, cudaMemcpyDeviceToHost));
-  cudaFree(dbg);
-  unsigned long long t0 = ~0ull;
-  for (unsigned i = 0; i < grid.x; ++i) t0 = std::min(t0, h[i * tctap::kTraceSlots]);
-  for (unsigned i = 0; i < grid.x; i += std::max(1u, grid.x / 6)) {
-    std::fprintf(stderr, "tap cta %3u:", i);
-    for (int s = 0; s < tctap::kTraceSlots; ++s) {
-      const unsigned long long v = h[i * tctap::kTraceSlots + s];
-      if (v) std::fprintf(stderr, " %d:%.2f", s, (v - t0) / 1000.0);
-    }
-    std::fprintf(stderr, "\n");
-  }
   count_launch(c);
 }
 
@@ -131,13 +78,12 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
               const float* bias, float* out, cdnn_handle stream, bool relu = false, const float* gate = nullptr) {
   ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
   const ConvGeom& g = d.geom;
-  if (!conv_tap_enabled() || g.sh != 1 || g.sw != 1) return false;
+  if (g.sh != 1 || g.sw != 1) return false;
   // 2-7 input channels with wide filters (CIFAR conv1): the window-staging kernel
   // (conv_tma.cuh) measures faster (profiles/r01_conv_bench.txt); it takes them when eligible
   {
     const int cin = backward_data ? g.Cog : g.Cg, win = backward_data ? g.Q : g.W;
-    if (g.group == 1 && g.dh == 1 && g.dw == 1 && cin > 1 && cin < 8 && cin * g.S > 8 && win % 4 == 0 &&
-        conv_tma_enabled())
+    if (g.group == 1 && g.dh == 1 && g.dw == 1 && cin > 1 && cin < 8 && cin * g.S > 8 && win % 4 == 0)
       return false;
   }
   const int G = g.group;
@@ -154,11 +100,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   a.Wv = Q + g.dw * (g.S - 1);
   if (int64_t(g.N) * a.Hv * a.Wv >= (int64_t(1) << 31)) return false;
   a.Mv = g.N * a.Hv * a.Wv;
-  static const bool fold_ok = [] {
-    const char* v = std::getenv("CDNN_TAP_FOLD");
-    return !(v && std::string(v) == "0");
-  }();
-  a.fold = (fold_ok && Cin < 16 && Cin * g.S <= 32) ? 1 : 0;
+  a.fold = (Cin < 16 && Cin * g.S <= 32) ? 1 : 0;
   a.rows = (128 + g.dh * (g.R - 1) * a.Wv + (a.fold ? 0 : g.dw * (g.S - 1)) + 7) & ~7;
   a.cblocks = a.fold ? 1 : (Cin + 31) / 32;
   a.in_cstride = Hin * Win;
@@ -176,13 +118,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   // convolutions): size the CTA for two per SM.  The two CTAs' staging, MMA issue
   // and epilogues interleave on the SM's tensor core (CIFAR conv2 39.4 -> 35.3 us,
   // the column-folded conv1 53 -> 48.5 us); TMEM 2 x <= 256 columns.
-  const int taps_eff = a.fold ? g.R : g.R * g.S;
-  const int nk8_max = ((a.fold ? g.S * Cin : std::min(32, Cin)) + 7) >> 3;
-  static const int two_cta_macs = [] {  // CDNN_TAP_2CTA: max MMA work (taps x k8 steps) per staged tile
-    const char* v = std::getenv("CDNN_TAP_2CTA");
-    return v ? std::atoi(v) : (1 << 30);
-  }();
-  const bool staging_bound = a.cblocks == 1 && taps_eff * nk8_max <= two_cta_macs;
+  const bool staging_bound = a.cblocks == 1;
   int ctas_per_sm = 1;
   // (32-wide tiles only: their kernel is register-bounded for two CTAs per SM)
   if (staging_bound && bn == 32 && tctap::smem_bytes(a.rows, 1, 2, bn, split) <= 113 * 1024) {
@@ -260,7 +196,7 @@ void launch_conv_wtap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const tcwtap
 bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* dy, float* dw, float* db,
                     cdnn_handle stream) {
   const ConvGeom& g = d.geom;
-  if (!conv_tap_enabled() || g.sh != 1 || g.sw != 1 || g.Cg < 16) return false;
+  if (g.sh != 1 || g.sw != 1 || g.Cg < 16) return false;
   const bool split = c->math_mode == CDNN_MATH_TF32X3;
   tcwtap::WtapArgs a{};
   a.N = g.N; a.Cg = g.Cg; a.H = g.H; a.W = g.W; a.Cog = g.Cog; a.P = g.P; a.Q = g.Q;
@@ -392,7 +328,7 @@ bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, con
                      const float* bias, float* out, cdnn_handle stream, bool relu = false) {
   ConvDescSlot& d = const_cast<ConvDescSlot&>(dconst);
   const ConvGeom& g = d.geom;
-  if (!conv_tma_enabled() || g.group != 1 || g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1) return false;
+  if (g.group != 1 || g.sh != 1 || g.sw != 1 || g.dh != 1 || g.dw != 1) return false;
   // direct-conv extents
   const int Cin = backward_data ? g.Co : g.C, Hin = backward_data ? g.P : g.H, Win = backward_data ? g.Q : g.W;
   const int Cout = backward_data ? g.C : g.Co, P = backward_data ? g.H : g.P, Q = backward_data ? g.W : g.Q;
@@ -476,7 +412,7 @@ bool conv_direct_tma(Ctx* c, const ConvDescSlot& dconst, bool backward_data, con
 // (11x11, stride 4, 3 channels) becomes a 3x3 convolution over 48 channels that the
 // tap-shift kernels run on the tensor cores.
 bool s2d_eligible(const ConvGeom& g) {
-  return conv_tap_enabled() && g.sh == g.sw && g.sh >= 2 && g.dh == 1 && g.dw == 1 && g.group == 1 &&
+  return g.sh == g.sw && g.sh >= 2 && g.dh == 1 && g.dw == 1 && g.group == 1 &&
          g.C * g.sh * g.sw <= 128 && (g.R + g.sh - 1) / g.sh <= 4 && (g.S + g.sw - 1) / g.sw <= 4;
 }
 
@@ -681,7 +617,7 @@ bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float
 // filter on conv_wtap, which needs >= 16 channels), instead of staging 3-channel
 // rows with scalar gathers.
 bool cf_eligible(const ConvGeom& g) {
-  return conv_tap_enabled() && g.sh == 1 && g.sw == 1 && g.dh == 1 && g.dw == 1 && g.group == 1 && g.C < 16 &&
+  return g.sh == 1 && g.sw == 1 && g.dh == 1 && g.dw == 1 && g.group == 1 && g.C < 16 &&
          g.C * g.S <= 32 && g.S > 1 && g.pw < g.S;
 }
 
@@ -745,15 +681,6 @@ __global__ void cf_weight_kernel(const float* __restrict__ w, float* __restrict_
   }
 }
 
-// dW[co][c][r][s] += dW'[co][s*C + c][r]
-__global__ void cf_dweight_kernel(const float* __restrict__ dwf, float* __restrict__ dw, ConvGeom g, ConvGeom h) {
-  const int total = g.Co * g.C * g.R * g.S;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int s = i % g.S, r = (i / g.S) % g.R, c = (i / (g.S * g.R)) % g.C, co = i / (g.S * g.R * g.C);
-    dw[i] += dwf[(co * h.C + s * g.C + c) * h.R + r];
-  }
-}
-
 bool conv_forward_cf(Ctx* c, const ConvDescSlot& d, const float* x, const float* w, const float* bias, float* y,
                      cdnn_handle stream, bool relu) {
   if (!cf_eligible(d.geom)) return false;
@@ -769,27 +696,6 @@ bool conv_forward_cf(Ctx* c, const ConvDescSlot& d, const float* x, const float*
   return conv_tap(c, e, false, xf, wf, bias, y, stream, relu);
 }
 
-bool conv_wgrad_cf(Ctx* c, const ConvDescSlot& d, const float* x, const float* dy, float* dw, float* db,
-                   cdnn_handle stream) {
-  if (!cf_eligible(d.geom)) return false;
-  ConvDescSlot& e = cf_desc(d);
-  const ConvGeom &g = d.geom, &h = e.geom;
-  cudaStream_t st = stream_of(c, stream);
-  float* xf = cf_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
-  float* dwf = dw ? cf_buffer(c, d, 3, size_t(h.Co) * h.C * h.R) : nullptr;
-  cf_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32, 256), 256, 0, st>>>(x, xf, g, h);
-  check_launch("column fold");
-  count_launch(c);
-  if (dwf) CDNN_CUDA(cudaMemsetAsync(dwf, 0, size_t(h.Co) * h.C * h.R * 4, st));
-  if (!conv_wgrad_tap(c, e, xf, dy, dwf, db, stream)) return false;
-  if (dw) {
-    cf_dweight_kernel<<<grid_for(int64_t(g.Co) * g.C * g.R * g.S, 256), 256, 0, st>>>(dwf, dw, g, h);
-    check_launch("cf_dweight");
-    count_launch(c);
-  }
-  return true;
-}
-
 template <typename T>
 void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const BufferSlot& Wt,
                     const BufferSlot* B, BufferSlot& Y, cdnn_handle stream, bool relu) {
@@ -802,8 +708,7 @@ void conv_forward_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const Bu
                          B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream,
                          relu))
       return;
-    if (cf_route_enabled() &&
-        conv_forward_cf(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
+    if (conv_forward_cf(c, d, reinterpret_cast<const float*>(X.dev), reinterpret_cast<const float*>(Wt.dev),
                         B ? reinterpret_cast<const float*>(B->dev) : nullptr, reinterpret_cast<float*>(Y.dev), stream,
                         relu))
       return;
@@ -964,7 +869,7 @@ void conv_backward_data_impl(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt
         conv_dgrad_s2d(c, d, reinterpret_cast<const float*>(Wt.dev), reinterpret_cast<const float*>(DY.dev),
                        reinterpret_cast<float*>(DX.dev), stream))
       return;
-    if ((g.sh > 1 || g.sw > 1) && conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 &&
+    if ((g.sh > 1 || g.sw > 1) && g.sh <= 2 && g.sw <= 2 &&
         with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, 0, [&](const float* up) {
           return conv_tap(c, d, true, up, reinterpret_cast<const float*>(Wt.dev), nullptr,
                           reinterpret_cast<float*>(DX.dev), stream);
@@ -1017,14 +922,11 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
     float* db = DB ? reinterpret_cast<float*>(DB->dev) : nullptr;
     const float* x = reinterpret_cast<const float*>(X.dev);
     if (g.sh == 1 && g.sw == 1) {
-      // (the column fold is slower than the gather engine for the backward filter; forward only)
-      if (cf_route_enabled() && std::getenv("CDNN_CF_WGRAD") &&
-          conv_wgrad_cf(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream))
-        return;
+      // (a column fold of the backward filter measured slower than the gather engine; forward only)
       if (conv_wgrad_tap(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) return;
     } else if (conv_wgrad_s2d(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) {
       return;
-    } else if (conv_tap_enabled() && g.sh <= 2 && g.sw <= 2 && g.Cg >= 16 &&
+    } else if (g.sh <= 2 && g.sw <= 2 && g.Cg >= 16 &&
                with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, 1,
                                   [&](const float* up) { return conv_wgrad_tap(c, d, x, up, dw, db, stream); })) {
       return;

@@ -13,11 +13,8 @@
 
 namespace cdnn {
 
-// fp32 GEMMs up to this many multiply-adds take the SIMT engine (CDNN_SIMT_MACS overrides)
-const int64_t kSimtMaxMacs = [] {
-  const char* v = std::getenv("CDNN_SIMT_MACS");
-  return v ? std::atoll(v) : (int64_t(1) << 26);
-}();
+// fp32 GEMMs up to this many multiply-adds take the SIMT engine
+constexpr int64_t kSimtMaxMacs = int64_t(1) << 26;
 
 GemmPlan plan_tc(int M, int N, int K) {
   GemmPlan p;
@@ -91,16 +88,9 @@ DenseView<float> k_major_copy(Ctx* c, cudaStream_t st, Workspace& scratch, size_
 template <typename T>
 static bool small_gemm(Ctx* c, cudaStream_t st, int M, int N, int K, const DenseView<T>& va, const DenseView<T>& vb,
                        const StoreEpi<T>& epi) {
-  static const bool on = [] {
-    const char* v = std::getenv("CDNN_SMALL_GEMM");
-    return !(v && std::string(v) == "0");
-  }();
   const int64_t outs = int64_t(M) * N;
-  if (!on) return false;
-  static const int64_t warp_outs = [] {  // K in [64, 256): warp-per-output up to this many outputs
-    const char* v = std::getenv("CDNN_SMALL_GEMM_WARP_OUTS");
-    return v ? int64_t(std::atoll(v)) : int64_t(2048);  // LeNet ip2 dW (5000) measured faster per thread
-  }();
+  // K in [64, 256): warp-per-output up to this many outputs (LeNet ip2 dW, 5000, measured faster per thread)
+  constexpr int64_t warp_outs = 2048;
   // few outputs: a warp per output (CIFAR ip2 dW 640 x K=100: 29 -> 5.5 us)
   if (outs <= 16384 && (K >= 256 || (K >= 64 && outs <= warp_outs))) {
     const int64_t threads = outs * 32;

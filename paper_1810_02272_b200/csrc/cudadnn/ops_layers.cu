@@ -8,6 +8,7 @@
 // buffer), and the iteration counter lives in device memory so a captured CUDA
 // graph draws a fresh mask on every replay.
 #include "launch.cuh"
+#include "lrn_math.cuh"
 
 namespace cdnn {
 namespace {
@@ -30,11 +31,7 @@ int blocks(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n + k
 // One thread per pixel (img, hw) walks the channels with a running window sum
 // (entering square added, leaving square subtracted; the leaving value is an
 // L1 hit), so the tensor is read ~once, coalesced across threads (consecutive hw).
-template <typename T>
-__device__ __forceinline__ T neg_pow(T sc, T beta) {
-  if constexpr (sizeof(T) == 4) return exp2f(-beta * log2f(sc));
-  else return pow(sc, -beta);
-}
+// (the arithmetic itself is lrn_math.cuh, shared with the fused LRN + pooling kernels)
 
 // Forward: channels are processed in groups of four, the group's entering,
 // leaving and own values loaded together before any arithmetic (12 independent
@@ -55,7 +52,7 @@ __global__ void lrn_fwd(const T* __restrict__ x, T* __restrict__ y, T* __restric
     T s = T(0);  // sum of squares over [c - pre, c + post]
     for (int cc = 0; cc < post && cc < C; ++cc) {
       const T v = __ldg(xb + int64_t(cc) * HW);
-      s += v * v;
+      s = lrn::sq_acc(s, v);
     }
     for (int c0 = 0; c0 < C; c0 += kLrnU) {
       T vin[kLrnU], vout[kLrnU], vx[kLrnU];
@@ -70,13 +67,13 @@ __global__ void lrn_fwd(const T* __restrict__ x, T* __restrict__ y, T* __restric
       for (int u = 0; u < kLrnU; ++u) {
         const int c = c0 + u;
         if (c >= C) break;
-        s += vin[u] * vin[u];
-        s -= vout[u] * vout[u];
+        s = lrn::sq_acc(s, vin[u]);
+        s = lrn::fma_(-vout[u], vout[u], s);
         s = s > T(0) ? s : T(0);
         const int64_t o = ob + int64_t(c) * HW;
-        const T sc = k + aN * s;
+        const T sc = lrn::scale(s, aN, k);
         scale[o] = sc;
-        y[o] = vx[u] * neg_pow(sc, beta);
+        y[o] = lrn::top(vx[u], lrn::neg_pow(sc, beta));
       }
     }
   }
@@ -95,16 +92,16 @@ __global__ void lrn_bwd(const T* __restrict__ x, const T* __restrict__ y, const 
     const int64_t base = img * C * HW + hw;
     auto t = [&](int cc) {
       const int64_t o = base + int64_t(cc) * HW;
-      return dy[o] * y[o] / scale[o];
+      return lrn::term(dy[o], y[o], scale[o]);
     };
     T acc = T(0);  // sum of t over [c - post, c + pre]
-    for (int cc = 0; cc < pre && cc < C; ++cc) acc += t(cc);
+    for (int cc = 0; cc < pre && cc < C; ++cc) acc = lrn::add_(acc, t(cc));
     for (int c = 0; c < C; ++c) {
       const int cin = c + pre, cout = c - post - 1;
-      if (cin < C) acc += t(cin);
-      if (cout >= 0) acc -= t(cout);
+      if (cin < C) acc = lrn::add_(acc, t(cin));
+      if (cout >= 0) acc = lrn::sub_(acc, t(cout));
       const int64_t o = base + int64_t(c) * HW;
-      const T g = dy[o] * neg_pow(scale[o], beta) - coef * x[o] * acc;
+      const T g = lrn::grad(dy[o], lrn::neg_pow(scale[o], beta), coef, x[o], acc);
       dx[o] = (gate && !(gate[o] > T(0))) ? T(0) : g;
     }
   }
@@ -142,11 +139,11 @@ __global__ void lrn_fwd_ring(const T* __restrict__ x, T* __restrict__ y, T* __re
         if (c >= C) break;
         T sum = T(0);
 #pragma unroll
-        for (int j = 0; j < SIZE; ++j) sum += xr[j] * xr[j];
+        for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xr[j]);
         const int64_t o = base + int64_t(c) * HW;
-        const T sc = k + aN * sum;
+        const T sc = lrn::scale(sum, aN, k);
         scale[o] = sc;
-        y[o] = xr[pre] * neg_pow(sc, beta);
+        y[o] = lrn::top(xr[pre], lrn::neg_pow(sc, beta));
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
         xr[SIZE - 1] = nx[u];
@@ -174,7 +171,7 @@ __global__ void lrn_bwd_ring(const T* __restrict__ x, const T* __restrict__ y, c
         const int64_t o = base + int64_t(cc) * HW;
         dyr[j] = __ldg(dy + o);
         scr[j] = __ldg(scale + o);
-        tr[j] = dyr[j] * __ldg(y + o) / scr[j];
+        tr[j] = lrn::term(dyr[j], __ldg(y + o), scr[j]);
       } else {
         dyr[j] = T(0); scr[j] = T(1); tr[j] = T(0);
       }
@@ -197,8 +194,8 @@ __global__ void lrn_bwd_ring(const T* __restrict__ x, const T* __restrict__ y, c
         if (c >= C) break;
         T acc = T(0);
 #pragma unroll
-        for (int j = 0; j < SIZE; ++j) acc += tr[j];
-        const T g = dyr[post] * neg_pow(scr[post], beta) - coef * xv[u] * acc;
+        for (int j = 0; j < SIZE; ++j) acc = lrn::add_(acc, tr[j]);
+        const T g = lrn::grad(dyr[post], lrn::neg_pow(scr[post], beta), coef, xv[u], acc);
         // fused backward of an in-place ReLU on this layer's bottom (gate = its data:
         // normally the very buffer x, whose value is already in a register)
         const bool open = !gate || (gate == x ? xv[u] > T(0) : __ldg(gate + base + int64_t(c) * HW) > T(0));
@@ -207,7 +204,7 @@ __global__ void lrn_bwd_ring(const T* __restrict__ x, const T* __restrict__ y, c
         for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; scr[j] = scr[j + 1]; }
         dyr[SIZE - 1] = ndy[u];
         scr[SIZE - 1] = nsc[u];
-        tr[SIZE - 1] = ndy[u] * ny[u] / nsc[u];
+        tr[SIZE - 1] = lrn::term(ndy[u], ny[u], nsc[u]);
       }
     }
   }

@@ -25,31 +25,32 @@
 // LRN top diff (the pool backward gather over the <= R x R windows holding the
 // pixel, in max_pool_bwd_k's order), then dx(c) from the rings of lrn_bwd_ring.
 #include "launch.cuh"
+#include "lrn_math.cuh"
 
 namespace cdnn {
 namespace {
 
-template <typename T>
-__device__ __forceinline__ T lrn_neg_pow(T sc, T beta) {  // == ops_layers.cu neg_pow
-  if constexpr (sizeof(T) == 4) return exp2f(-beta * log2f(sc));
-  else return pow(sc, -beta);
-}
-
-constexpr int kG = 4;  // channels per step (loads in flight; one block barrier per step)
+constexpr int kG = 4;     // channels per step (loads in flight; one block barrier per step)
+constexpr int kSeg = 32;  // channels per thread / block segment (segments run in parallel)
 
 struct LrnPoolGeom {
   int N, C, H, W, PH, PW;
   int TR, rows_in;  // pooled rows per band, input rows per band
   int bands;
+  int segs;         // channel segments of kSeg
 };
 
+// Forward: block (band, channel segment, image).  The x loads of step i+1 are issued
+// before step i's arithmetic and barrier (lookahead of one step).
 template <typename T, int SIZE, int K, int S>
-__global__ void lrn_maxpool_fwd(const T* __restrict__ x, T* __restrict__ ynorm, T* __restrict__ ypool,
-                                int* __restrict__ mask, LrnPoolGeom g, T alpha, T beta, T k, bool relu) {
+__global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x, T* __restrict__ ynorm,
+                                                        T* __restrict__ ypool, int* __restrict__ mask,
+                                                        LrnPoolGeom g, T alpha, T beta, T k, bool relu) {
   constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
   extern __shared__ uint8_t smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);  // [2][kG][rows_in * W]
-  const int band = blockIdx.x, img = blockIdx.y;
+  const int band = blockIdx.x, img = blockIdx.z;
+  const int cs0 = blockIdx.y * kSeg, cs1 = min(g.C, cs0 + kSeg);
   const int pr0 = band * g.TR, pr1 = min(g.PH, pr0 + g.TR);
   const int r0 = pr0 * S, r1 = min(g.H, (pr1 - 1) * S + K);
   // rows whose LRN top this band stores (halo rows belong to the next band)
@@ -62,56 +63,65 @@ __global__ void lrn_maxpool_fwd(const T* __restrict__ x, T* __restrict__ ynorm, 
   const int h = r0 + (active ? p / g.W : 0);
   const int64_t base = int64_t(img) * g.C * HW + int64_t(h) * g.W + (active ? p % g.W : 0);
   const bool own = active && h < own1;
-  T xr[SIZE];
+  T xr[SIZE];  // x(c - pre .. c + post)
 #pragma unroll
   for (int j = 0; j < SIZE; ++j) {
-    const int cc = j - pre;
+    const int cc = cs0 + j - pre;
     xr[j] = (active && cc >= 0 && cc < g.C) ? __ldg(x + base + int64_t(cc) * HW) : T(0);
   }
-  const int items = kG * (pr1 - pr0) * g.PW;
-  for (int c0 = 0, step = 0; c0 < g.C; c0 += kG, ++step) {
+  auto load_step = [&](int c0, T (&nx)[kG]) {
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const int cin = c0 + u + post + 1;
+      nx[u] = (active && c0 + u < cs1 && cin < g.C) ? __ldg(x + base + int64_t(cin) * HW) : T(0);
+    }
+  };
+  T nxt[kG];
+  load_step(cs0, nxt);
+  const int prows = pr1 - pr0;
+  for (int c0 = cs0, step = 0; c0 < cs1; c0 += kG, ++step) {
+    T cur[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) cur[u] = nxt[u];
+    if (c0 + kG < cs1) load_step(c0 + kG, nxt);
     T* buf = tile + (step & 1) * kG * tsz;
     if (active) {
-      T nx[kG];
-#pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        const int cin = c0 + u + post + 1;
-        nx[u] = cin < g.C ? __ldg(x + base + int64_t(cin) * HW) : T(0);
-      }
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         const int c = c0 + u;
-        if (c >= g.C) break;
+        if (c >= cs1) break;
         T sum = T(0);
 #pragma unroll
-        for (int j = 0; j < SIZE; ++j) sum += xr[j] * xr[j];
-        const T sc = k + aN * sum;
-        const T yv = xr[pre] * lrn_neg_pow(sc, beta);
+        for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xr[j]);
+        const T sc = lrn::scale(sum, aN, k);
+        const T yv = lrn::top(xr[pre], lrn::neg_pow(sc, beta));
         buf[u * tsz + p] = yv;
         if (own) ynorm[base + int64_t(c) * HW] = yv;
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
-        xr[SIZE - 1] = nx[u];
+        xr[SIZE - 1] = cur[u];
       }
     }
     __syncthreads();
+    const int items = min(kG, cs1 - c0) * prows * g.PW;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int u = it / ((pr1 - pr0) * g.PW);
-      const int c = c0 + u;
-      if (c >= g.C) continue;
-      const int rem = it - u * ((pr1 - pr0) * g.PW);
+      const int u = it / (prows * g.PW);
+      const int rem = it - u * (prows * g.PW);
       const int prl = rem / g.PW, pw = rem - prl * g.PW;
       const int hs = (pr0 + prl) * S, ws = pw * S;
-      const int he = min(hs + K, g.H), we = min(ws + K, g.W);
-      const T* t = buf + u * tsz;
+      const T* t = buf + u * tsz + (hs - r0) * g.W;
       T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
       int arg = -1;
-      for (int hh = hs; hh < he; ++hh)
-        for (int ww = ws; ww < we; ++ww) {
-          const T v = t[(hh - r0) * g.W + ww];
-          if (v > best) { best = v; arg = hh * g.W + ww; }
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          if (hs + a < g.H && ws + b < g.W) {
+            const T v = t[a * g.W + ws + b];
+            if (v > best) { best = v; arg = (hs + a) * g.W + ws + b; }
+          }
         }
-      const int64_t o = (int64_t(img) * g.C + c) * PHW + int64_t(pr0 + prl) * g.PW + pw;
+      const int64_t o = (int64_t(img) * g.C + c0 + u) * PHW + int64_t(pr0 + prl) * g.PW + pw;
       ypool[o] = relu ? (best > T(0) ? best : T(0)) : best;
       mask[o] = arg;
     }
@@ -119,6 +129,7 @@ __global__ void lrn_maxpool_fwd(const T* __restrict__ x, T* __restrict__ ynorm, 
   }
 }
 
+// Backward: one thread per (pixel, channel segment).
 template <typename T, int SIZE, int K, int S>
 __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
                                                        const int* __restrict__ mask, T* __restrict__ dx,
@@ -127,17 +138,21 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
   constexpr int R = (K + S - 1) / S;
   const int HW = g.H * g.W, PHW = g.PH * g.PW;
   const int64_t pixels = int64_t(g.N) * HW;
+  const int64_t work = pixels * g.segs;
   const T aN = alpha / T(SIZE);
   const T coef = T(2) * alpha * beta / T(SIZE);
-  for (int64_t pix = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; pix < pixels;
-       pix += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t wi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; wi < work; wi += int64_t(gridDim.x) * blockDim.x) {
+    // consecutive threads: consecutive pixels of one segment (coalesced)
+    const int seg = int(wi / pixels);
+    const int64_t pix = wi - int64_t(seg) * pixels;
+    const int cs0 = seg * kSeg, cs1 = min(g.C, cs0 + kSeg);
     const int img = int(pix / HW), hw = int(pix - int64_t(img) * HW);
-    const int h = hw / g.W, w = hw - (hw / g.W) * g.W;
+    const int h = hw / g.W, w = hw - h * g.W;
     const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
     const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
     const int64_t base = int64_t(img) * g.C * HW + hw;
     const int64_t pbase = int64_t(img) * g.C * PHW + int64_t(phs) * g.PW + pws;
-    // the LRN top diff of channel cc at this pixel: max_pool_bwd_k's gather
+    // the LRN top diff of channel cc at this pixel: max_pool_bwd_k's gather, in its order
     auto gather = [&](int cc, int (&m)[R][R], T (&v)[R][R]) {
 #pragma unroll
       for (int a = 0; a < R; ++a)
@@ -150,83 +165,101 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
         }
     };
     auto ndy_of = [&](const int (&m)[R][R], const T (&v)[R][R]) {
-      T s = T(0);
+      T sdy = T(0);
 #pragma unroll
       for (int a = 0; a < R; ++a)
 #pragma unroll
         for (int b = 0; b < R; ++b)
-          if (m[a][b] == hw) s += v[a][b];
-      return s;
+          if (m[a][b] == hw) sdy += v[a][b];
+      return sdy;
     };
-    // rings over channels c - post .. c + pre: t = dy*y/scale, dy, scale (lrn_bwd_ring).
-    // Before the step for channel c they hold channels c-1-post .. c-1+pre (index 0 is
-    // shifted out first); so ahead of c = 0, index j holds channel j - 1 - post.
-    T tr[SIZE], dyr[SIZE], scr[SIZE];
+    // rings over channels c - post .. c + pre: t = dy*y/scale, dy, scale^-beta (lrn_bwd_ring;
+    // scale^-beta is the same function of the same scale, computed once per channel).
+    // Ahead of the step for channel c they hold c-1-post .. c-1+pre (index 0 shifts out first).
+    T tr[SIZE], dyr[SIZE], npr[SIZE];
 #pragma unroll
-    for (int j = 0; j < SIZE; ++j) { dyr[j] = T(0); scr[j] = T(1); tr[j] = T(0); }
+    for (int j = 0; j < SIZE; ++j) { dyr[j] = T(0); npr[j] = T(1); tr[j] = T(0); }
 #pragma unroll
     for (int j = 1; j < SIZE; ++j) {
-      const int cc = j - 1 - post;  // channels -post .. pre-1; only 0 .. pre-1 are real
+      const int cc = cs0 + j - 1 - post;
       if (cc >= 0 && cc < g.C) {
         T sum = T(0);
 #pragma unroll
         for (int q = 0; q < SIZE; ++q) {
           const int cx = cc - pre + q;
-          const T xv = (cx >= 0 && cx < g.C) ? __ldg(x + base + int64_t(cx) * HW) : T(0);
-          sum += xv * xv;
+          sum = lrn::sq_acc(sum, (cx >= 0 && cx < g.C) ? __ldg(x + base + int64_t(cx) * HW) : T(0));
         }
-        const T sc = k + aN * sum;
-        const T yv = __ldg(x + base + int64_t(cc) * HW) * lrn_neg_pow(sc, beta);
+        const T sc = lrn::scale(sum, aN, k);
+        const T np = lrn::neg_pow(sc, beta);
+        const T yv = lrn::top(__ldg(x + base + int64_t(cc) * HW), np);
         int m[R][R];
         T v[R][R];
         gather(cc, m, v);
         const T d = ndy_of(m, v);
         dyr[j] = d;
-        scr[j] = sc;
-        tr[j] = d * yv / sc;
+        npr[j] = np;
+        tr[j] = lrn::term(d, yv, sc);
       }
     }
     // x ring: x(c .. c + SIZE - 1), the window of the entering channel c + pre
     T xr[SIZE];
 #pragma unroll
-    for (int j = 0; j < SIZE - 1; ++j) xr[j] = (j < g.C) ? __ldg(x + base + int64_t(j) * HW) : T(0);
+    for (int j = 0; j < SIZE - 1; ++j) {
+      const int cc = cs0 + j;
+      xr[j] = cc < g.C ? __ldg(x + base + int64_t(cc) * HW) : T(0);
+    }
     xr[SIZE - 1] = T(0);
-    for (int c0 = 0; c0 < g.C; c0 += kG) {
-      T nx[kG];
-      int nm[kG][R][R];
-      T nv[kG][R][R];
+    auto load_step = [&](int c0, T (&nx)[kG], int (&nm)[kG][R][R], T (&nv)[kG][R][R]) {
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         const int cin = c0 + u + SIZE - 1;
-        nx[u] = cin < g.C ? __ldg(x + base + int64_t(cin) * HW) : T(0);
-        gather(c0 + u + pre, nm[u], nv[u]);
+        nx[u] = (c0 + u < cs1 && cin < g.C) ? __ldg(x + base + int64_t(cin) * HW) : T(0);
+        gather(c0 + u < cs1 ? c0 + u + pre : g.C, nm[u], nv[u]);
       }
+    };
+    T nx[kG];
+    int nm[kG][R][R];
+    T nv[kG][R][R];
+    load_step(cs0, nx, nm, nv);
+    for (int c0 = cs0; c0 < cs1; c0 += kG) {
+      T cx[kG];
+      int cm[kG][R][R];
+      T cv[kG][R][R];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        cx[u] = nx[u];
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int b = 0; b < R; ++b) { cm[u][a][b] = nm[u][a][b]; cv[u][a][b] = nv[u][a][b]; }
+      }
+      if (c0 + kG < cs1) load_step(c0 + kG, nx, nm, nv);  // in flight during this step
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         const int c = c0 + u;
-        if (c >= g.C) break;
-        xr[SIZE - 1] = nx[u];  // x(c .. c + SIZE - 1)
+        if (c >= cs1) break;
+        xr[SIZE - 1] = cx[u];  // x(c .. c + SIZE - 1)
 #pragma unroll
-        for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; scr[j] = scr[j + 1]; }
-        const int e = c + pre;
-        if (e < g.C) {
+        for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; npr[j] = npr[j + 1]; }
+        if (c + pre < g.C) {
           T sum = T(0);
 #pragma unroll
-          for (int j = 0; j < SIZE; ++j) sum += xr[j] * xr[j];
-          const T sc = k + aN * sum;
-          const T yv = xr[pre] * lrn_neg_pow(sc, beta);
-          const T d = ndy_of(nm[u], nv[u]);
+          for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xr[j]);
+          const T sc = lrn::scale(sum, aN, k);
+          const T np = lrn::neg_pow(sc, beta);
+          const T yv = lrn::top(xr[pre], np);
+          const T d = ndy_of(cm[u], cv[u]);
           dyr[SIZE - 1] = d;
-          scr[SIZE - 1] = sc;
-          tr[SIZE - 1] = d * yv / sc;
+          npr[SIZE - 1] = np;
+          tr[SIZE - 1] = lrn::term(d, yv, sc);
         } else {
-          dyr[SIZE - 1] = T(0); scr[SIZE - 1] = T(1); tr[SIZE - 1] = T(0);
+          dyr[SIZE - 1] = T(0); npr[SIZE - 1] = T(1); tr[SIZE - 1] = T(0);
         }
         T acc = T(0);
 #pragma unroll
-        for (int j = 0; j < SIZE; ++j) acc += tr[j];
+        for (int j = 0; j < SIZE; ++j) acc = lrn::add_(acc, tr[j]);
         const T xc = xr[0];
-        const T gval = dyr[post] * lrn_neg_pow(scr[post], beta) - coef * xc * acc;
+        const T gval = lrn::grad(dyr[post], npr[post], coef, xc, acc);
         dx[base + int64_t(c) * HW] = (!gate_x || xc > T(0)) ? gval : T(0);
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
@@ -237,7 +270,7 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
 
 LrnPoolGeom lrn_pool_geom(const PoolDescSlot& d, int smem_cap_elems) {
   const auto& p = d.p;
-  LrnPoolGeom g{p.n, p.c, p.h, p.w, d.PH, d.PW, 1, 0, 0};
+  LrnPoolGeom g{p.n, p.c, p.h, p.w, d.PH, d.PW, 1, 0, 0, (p.c + kSeg - 1) / kSeg};
   const int K = p.kernel_h, S = p.stride_h;
   // band height: about 512 input pixels per block
   int tr = std::max(1, ((512 / std::max(1, p.w)) - K) / S + 1);
@@ -264,8 +297,8 @@ void launch_fwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, T* y
   const LrnPoolGeom g = lrn_pool_geom(d, 1024);
   const int threads = ((g.rows_in * g.W + 31) / 32) * 32;
   const size_t smem = size_t(2) * kG * g.rows_in * g.W * sizeof(T);
-  lrn_maxpool_fwd<T, SIZE, K, S><<<dim3(g.bands, g.N), threads, smem, st>>>(x, yn, yp, m, g, T(alpha), T(beta),
-                                                                            T(k), relu);
+  lrn_maxpool_fwd<T, SIZE, K, S><<<dim3(g.bands, g.segs, g.N), threads, smem, st>>>(x, yn, yp, m, g, T(alpha),
+                                                                                    T(beta), T(k), relu);
   check_launch("lrn_maxpool_fwd");
   count_launch(c);
 }
@@ -274,9 +307,9 @@ template <typename T, int SIZE, int K, int S>
 void launch_bwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, const T* pdy, const int* m, T* dx,
                 double alpha, double beta, double k, bool gate_x) {
   const LrnPoolGeom g = lrn_pool_geom(d, 1024);
-  const int64_t pixels = int64_t(g.N) * g.H * g.W;
-  lrn_maxpool_bwd<T, SIZE, K, S><<<grid_for(pixels, 256), 256, 0, st>>>(x, pdy, m, dx, g, T(alpha), T(beta), T(k),
-                                                                         gate_x);
+  const int64_t work = int64_t(g.N) * g.H * g.W * g.segs;
+  lrn_maxpool_bwd<T, SIZE, K, S><<<grid_for(work, 256), 256, 0, st>>>(x, pdy, m, dx, g, T(alpha), T(beta), T(k),
+                                                                       gate_x);
   check_launch("lrn_maxpool_bwd");
   count_launch(c);
 }

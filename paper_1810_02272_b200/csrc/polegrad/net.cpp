@@ -155,12 +155,8 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
     layers_[i]->set_clobbered(top, bottom);
   }
 
-  // Fuse BatchNorm + the Scale reading its top (CDNN_FUSE_BN_SCALE=0 keeps them apart).
-  static const bool fuse_bn = [] {
-    const char* v = std::getenv("CDNN_FUSE_BN_SCALE");
-    return !(v && std::string(v) == "0");
-  }();
-  for (std::size_t i = 0; fuse_bn && i + 1 < layers_.size(); ++i) {
+  // Fuse BatchNorm + the Scale reading its top.
+  for (std::size_t i = 0; i + 1 < layers_.size(); ++i) {
     auto* bn = dynamic_cast<BatchNormLayer*>(layers_[i].get());
     auto* sc = dynamic_cast<ScaleLayer*>(layers_[i + 1].get());
     if (bn && sc && bottoms_[i + 1][0] == tops_[i][0]) {
@@ -187,13 +183,8 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
   // Fuse an in-place ReLU's backward into the backward of the layer that consumes
   // its top (Pooling, LRN, Convolution dgrad): that layer writes the ReLU blob's
   // diff gated by the blob's data, and the ReLU pass disappears.  Only when the
-  // consumer directly follows the ReLU and nothing else reads or rewrites the blob
-  // (CDNN_FUSE_RELU_BWD=0 keeps them apart).
-  static const bool fuse_relu_bwd = [] {
-    const char* v = std::getenv("CDNN_FUSE_RELU_BWD");
-    return !(v && std::string(v) == "0");
-  }();
-  for (std::size_t i = 0; fuse_relu_bwd && !compat && i + 1 < layers_.size(); ++i) {
+  // consumer directly follows the ReLU and nothing else reads or rewrites the blob.
+  for (std::size_t i = 0; !compat && i + 1 < layers_.size(); ++i) {
     auto* relu = dynamic_cast<ReluLayer*>(layers_[i].get());
     if (!relu || bottoms_[i].size() != 1 || tops_[i].size() != 1 || bottoms_[i][0] != tops_[i][0]) continue;
     Blob* b = tops_[i][0];
@@ -304,23 +295,13 @@ std::map<std::string, Blob*> Net::forward() {
   return outputs;
 }
 
-namespace {
-bool split_backward_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("CDNN_SPLIT_BACKWARD");
-    return !(v && std::string(v) == "0");
-  }();
-  return on;
-}
-}  // namespace
-
 // Layer i's backward.  Splittable layers (Convolution with a bottom gradient,
 // InnerProduct) fork their parameter-gradient half onto the side stream: it
 // only reads the top diff and bottom data and writes parameter diffs, none of
 // which the remaining bottom-gradient chain touches; the solver joins it.
 void Net::backward_layer(std::size_t i, bool& forked) {
   Layer& l = *layers_[i];
-  const bool split = split_backward_enabled() && !reference_compat() && l.can_split_backward();
+  const bool split = !reference_compat() && l.can_split_backward();
   if (!split) {
     l.backward(tops_[i], bottoms_[i]);
     return;

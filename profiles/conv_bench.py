@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--math", default="tf32x3")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--only", default="")
+    ap.add_argument("--ops", default="", help="comma list of ops to time (fwd,dgrad,wgrad,dgrad_gate,bwd)")
     args = ap.parse_args()
     ctx = cd.Context(0)
     ctx.call("cdnn_set_math_mode", cd.MATH_TF32X3 if args.math == "tf32x3" else cd.MATH_TF32)
@@ -77,6 +78,8 @@ def main():
             "dgrad_gate": lambda: ctx.call("cdnn_conv_backward_data_ex", d, wt, dy, dx, x, 0),
         }
         for op, fn in ops.items():
+            if args.ops and op not in args.ops.split(","):
+                continue
             ms = timeit(ctx, fn, args.reps)
             print(json.dumps({"op": f"{name}.{op}", "math": args.math, "ms": round(ms, 5),
                               "tflops": round(flops / ms / 1e9, 3), "gflop": round(flops / 1e9, 4)}), flush=True)
@@ -102,6 +105,8 @@ def main():
             "bwd": (lambda: ctx.call("cdnn_ip_backward", x, wt, dy, dw, db, dx, rows, k, o, 0), 2 * flops),
         }
         for op, (fn, fl) in ops.items():
+            if args.ops and op not in args.ops.split(","):
+                continue
             ms = timeit(ctx, fn, args.reps)
             print(json.dumps({"op": f"{name}.{op}", "math": args.math, "ms": round(ms, 5),
                               "tflops": round(fl / ms / 1e9, 3), "gflop": round(fl / 1e9, 4)}), flush=True)

@@ -31,6 +31,21 @@ CONFIGS = {
 }
 
 
+def report(section: str, key: str, data) -> None:
+    """Achieved errors, collected into $PARITY_REPORT_DIR/parity.json when set
+    (committed as profiles/r02_parity.json)."""
+    import json
+    d = os.environ.get("PARITY_REPORT_DIR")
+    if not d:
+        return
+    os.makedirs(d, exist_ok=True)
+    path = os.path.join(d, "parity.json")
+    cur = json.load(open(path)) if os.path.exists(path) else {}
+    cur.setdefault(section, {})[key] = data
+    with open(path, "w") as f:
+        json.dump(cur, f, indent=1, default=float)
+
+
 def rel_l2(a, b) -> float:
     a = np.asarray(a, np.float64).ravel()
     b = np.asarray(b, np.float64).ravel()
@@ -60,14 +75,18 @@ def feed_forward_state(text: str, net, orc) -> dict:
     the MAX-pool argmax masks) into the oracle so both backward passes start
     from identical activations and routing decisions.  Returns how many
     pooling-mask entries / ReLU gates differed before the copy (near-tie flips)."""
-    flips = {"pool": 0, "relu": 0, "elements": 0}
+    flips = {"pool": 0, "relu": 0, "elements": 0, "top_rel": {}}
     for name, ltype, tops in pyoracle.layer_tops(text):
         if ltype in ("MemoryData", "SoftmaxWithLoss", "MemoryLoss"):
             continue
         for top in tops:
             mine = net.blob(top).astype(np.float64)
+            theirs = orc.blob(top)
+            # every layer's top against the oracle's own forward, before it is overwritten
+            # (in-place layers report the blob after the last in-place writer)
+            flips["top_rel"][top] = rel_l2(mine, theirs)
             if ltype == "ReLU":
-                flips["relu"] += int(np.count_nonzero((mine > 0) != (orc.blob(top) > 0)))
+                flips["relu"] += int(np.count_nonzero((mine > 0) != (theirs > 0)))
             orc.set_blob(top, mine)
             flips["elements"] += mine.size
         if ltype == "Pooling":

@@ -12,7 +12,7 @@ inputs.
 import numpy as np
 import pytest
 
-from parity_util import TOL, float_vs_truth, lockstep, pyoracle, polegrad, rel_l2, synthetic_batches
+from parity_util import TOL, float_vs_truth, lockstep, pyoracle, polegrad, rel_l2, report, synthetic_batches
 
 pytestmark = pytest.mark.gpu
 
@@ -77,8 +77,17 @@ def test_ten_iterations_gradients_on_synced_weights(config, dtype):
             assert f["pool"] + f["relu"] <= max(2, f["elements"] // 100000), (it, f)
             if dtype == "f64":  # exact ties at ReLU zeros can still split by 1 ulp
                 assert f["pool"] + f["relu"] <= 2, (it, f)
-    print(config, dtype, "max grad rel (synced, oracle-fed)", worst,
-          "flips", [h["flips"] for h in r["hist"] if h["flips"]][:3])
+            # every layer's forward top against the oracle's (same weights and inputs)
+            worst_top = max(f["top_rel"].items(), key=lambda kv: kv[1])
+            assert worst_top[1] <= tol, (it, worst_top)
+    tops = [h["flips"]["top_rel"] for h in r["hist"] if h["flips"]]
+    report("synced_weights", f"{config}.{dtype}", {
+        "bar": tol, "grad_rel_max": worst,
+        "grad_rel_per_tensor_max": {n: max(h["grad_rel"][i] for h in r["hist"]) for i, (n, _) in enumerate(r["params"])},
+        "loss_rel_max": max(abs(h["loss"] - h["oracle_loss"]) / max(abs(h["oracle_loss"]), 1e-12) for h in r["hist"]),
+        "top_rel_max": {k: max(t[k] for t in tops) for k in tops[0]} if tops else None,
+        "flips": [{k: v for k, v in h["flips"].items() if k != "top_rel"} for h in r["hist"] if h["flips"]]})
+    print(config, dtype, "max grad rel (synced, oracle-fed)", worst)
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
