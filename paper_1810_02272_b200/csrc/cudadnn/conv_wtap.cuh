@@ -87,7 +87,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
 }
 
 template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, 2) conv_wtap_kernel(const WtapArgs a) {
+__global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(const WtapArgs a) {
   constexpr int TM = 128;
   const int item = blockIdx.y;
   const int cb = item % a.cblocks;
@@ -180,92 +180,125 @@ __global__ void __launch_bounds__(kThreads, 2) conv_wtap_kernel(const WtapArgs a
     const int tid = threadIdx.x - 64;
     const int c0 = cb * 32, kc = min(32, a.Cg - c0);
     const int64_t HW = int64_t(a.H) * a.W, PQ = int64_t(a.P) * a.Q;
-    for (int ch = ch0; ch < ch1; ++ch) {
-      const int b = (ch - ch0) & 1;
-      if (ch - ch0 >= 2) ptx::mbar_wait(&empty[b], uint32_t(((ch - ch0) >> 1) - 1) & 1u);
-      const int v0 = ch * KC;
-      const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
-      // ---- A: X_v rows [v0 + rlo, + rowsA), MN-major 128B_BASE32B.  One thread
-      // per pixel row loads all 32 channels before converting (32 loads in flight).
-      const int vA0 = v0 + rlo;
-      for (int row = tid; row < a.rowsA; row += kStagers) {
-        const int v = vA0 + row;
-        bool inb = false;
-        const float* src = a.x;
-        if (v < a.Mv) {
-          const int img = int(a.div_hwv.div(uint32_t(v)));
-          const int rem = v - img * HWv;
-          const int hp = int(a.div_wv.div(uint32_t(rem)));
-          const int h = hp - a.ph, w = rem - hp * a.Wv - a.pw;
-          inb = h >= 0 && h < a.H && w >= 0 && w < a.W;
-          src = a.x + int64_t(img) * a.x_nstride + int64_t(c0) * HW + int64_t(h) * a.W + w;
-        }
-        float xv[4][8];
+    // B items (output channel, 16-pixel strip) per thread; A: one pixel row per thread
+    // (rows beyond kStagers, if any, take the sequential path below)
+    constexpr int kItems = BN * (KC / 16);
+    constexpr int NB = (kItems + kStagers - 1) / kStagers;
+    // A row `row` of chunk v0: source pointer and bounds
+    auto a_src = [&](int v0, int row, bool& inb) {
+      const int v = v0 + rlo + row;
+      inb = false;
+      const float* src = a.x;
+      if (v < a.Mv) {
+        const int img = int(a.div_hwv.div(uint32_t(v)));
+        const int rem = v - img * HWv;
+        const int hp = int(a.div_wv.div(uint32_t(rem)));
+        const int h = hp - a.ph, w = rem - hp * a.Wv - a.pw;
+        inb = h >= 0 && h < a.H && w >= 0 && w < a.W;
+        src = a.x + int64_t(img) * a.x_nstride + int64_t(c0) * HW + int64_t(h) * a.W + w;
+      }
+      return src;
+    };
+    auto a_load = [&](const float* src, bool inb, float (&xv)[4][8]) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) xv[u][e] = (inb && u * 8 + e < kc) ? __ldg(src + (u * 8 + e) * HW) : 0.f;
+        for (int e = 0; e < 8; ++e) xv[u][e] = (inb && u * 8 + e < kc) ? __ldg(src + (u * 8 + e) * HW) : 0.f;
+    };
+    // A: X_v rows, MN-major 128B_BASE32B, tf32 hi (and lo)
+    auto a_store = [&](uint32_t abase, int row, const float (&xv)[4][8]) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t off = uint32_t(row) * 128u + (uint32_t((u ^ (row & 3)) & 3) << 5);
-          float hv[8];
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t off = uint32_t(row) * 128u + (uint32_t((u ^ (row & 3)) & 3) << 5);
+        float hv[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) hv[e] = ptx::to_tf32(xv[u][e]);
-          ptx::st_shared_v4(abase + off, hv[0], hv[1], hv[2], hv[3]);
-          ptx::st_shared_v4(abase + off + 16, hv[4], hv[5], hv[6], hv[7]);
-          if constexpr (SPLIT) {
-            ptx::st_shared_v4(abase + A_H + off, ptx::to_tf32(xv[u][0] - hv[0]), ptx::to_tf32(xv[u][1] - hv[1]),
-                              ptx::to_tf32(xv[u][2] - hv[2]), ptx::to_tf32(xv[u][3] - hv[3]));
-            ptx::st_shared_v4(abase + A_H + off + 16, ptx::to_tf32(xv[u][4] - hv[4]), ptx::to_tf32(xv[u][5] - hv[5]),
-                              ptx::to_tf32(xv[u][6] - hv[6]), ptx::to_tf32(xv[u][7] - hv[7]));
-          }
+        for (int e = 0; e < 8; ++e) hv[e] = ptx::to_tf32(xv[u][e]);
+        ptx::st_shared_v4(abase + off, hv[0], hv[1], hv[2], hv[3]);
+        ptx::st_shared_v4(abase + off + 16, hv[4], hv[5], hv[6], hv[7]);
+        if constexpr (SPLIT) {
+          ptx::st_shared_v4(abase + A_H + off, ptx::to_tf32(xv[u][0] - hv[0]), ptx::to_tf32(xv[u][1] - hv[1]),
+                            ptx::to_tf32(xv[u][2] - hv[2]), ptx::to_tf32(xv[u][3] - hv[3]));
+          ptx::st_shared_v4(abase + A_H + off + 16, ptx::to_tf32(xv[u][4] - hv[4]), ptx::to_tf32(xv[u][5] - hv[5]),
+                            ptx::to_tf32(xv[u][6] - hv[6]), ptx::to_tf32(xv[u][7] - hv[7]));
         }
       }
-      // ---- B: dY^T [co][v0 .. v0+KC), K-major SW128 in 32-pixel blocks.  One thread per
-      // (co, 16-pixel strip): 16 loads in flight, one index decomposition per strip.
-      for (int it = tid; it < BN * (KC / 16); it += kStagers) {
-        const int strip = it % (KC / 16), col = it / (KC / 16);
-        const int co = n0 + col;
-        float yv[16];
-        {
-          int v = v0 + strip * 16;
-          int img = int(a.div_hwv.div(uint32_t(v)));
-          const int rem = v - img * HWv;
-          int p = int(a.div_wv.div(uint32_t(rem)));
-          int q = rem - p * a.Wv;
+    };
+    // B: dY^T [co][v0 .. v0+KC), 16 pixels of one output channel (index decomposition once)
+    auto b_load = [&](int v0, int it, float (&yv)[16]) {
+      const int strip = it % (KC / 16), col = it / (KC / 16);
+      const int co = n0 + col;
+      int v = v0 + strip * 16;
+      int img = int(a.div_hwv.div(uint32_t(v)));
+      const int rem = v - img * HWv;
+      int p = int(a.div_wv.div(uint32_t(rem)));
+      int q = rem - p * a.Wv;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            yv[e] = (v < a.Mv && co < a.Cog && p < a.P && q < a.Q)
-                        ? __ldg(a.dy + int64_t(img) * a.dy_nstride + co * PQ + int64_t(p) * a.Q + q)
-                        : 0.f;
-            ++v;
-            if (++q == a.Wv) {
-              q = 0;
-              if (++p == a.Hv) { p = 0; ++img; }
-            }
-          }
+      for (int e = 0; e < 16; ++e) {
+        yv[e] = (v < a.Mv && co < a.Cog && p < a.P && q < a.Q)
+                    ? __ldg(a.dy + int64_t(img) * a.dy_nstride + co * PQ + int64_t(p) * a.Q + q)
+                    : 0.f;
+        ++v;
+        if (++q == a.Wv) {
+          q = 0;
+          if (++p == a.Hv) { p = 0; ++img; }
         }
-        if (do_bias) {  // the KC/16 = 4 lanes sharing `col` reduce in a fixed shuffle tree
-          float sb = 0.f;
+      }
+    };
+    auto b_store = [&](uint32_t bbase, int it, const float (&yv)[16]) {
+      const int strip = it % (KC / 16), col = it / (KC / 16);
+      if (do_bias) {  // the KC/16 = 4 lanes sharing `col` reduce in a fixed shuffle tree
+        float sb = 0.f;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) sb += yv[e];
-          sb += __shfl_xor_sync(0xffffffffu, sb, 1);
-          sb += __shfl_xor_sync(0xffffffffu, sb, 2);
-          if ((lane & 3) == 0) bias_acc[col] += sb;
-        }
-        const int kb = strip >> 1;  // 32-pixel block
+        for (int e = 0; e < 16; ++e) sb += yv[e];
+        sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+        sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+        if ((lane & 3) == 0) bias_acc[col] += sb;
+      }
+      const int kb = strip >> 1;  // 32-pixel block
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int gi = (strip & 1) * 4 + g;  // 16-byte granule within the 128-byte row
-            const uint32_t off = uint32_t(kb) * B_KB + uint32_t(col) * 128u + (uint32_t((gi ^ (col & 7)) & 7) << 4);
-          const float h0 = ptx::to_tf32(yv[4 * g]), h1 = ptx::to_tf32(yv[4 * g + 1]);
-          const float h2 = ptx::to_tf32(yv[4 * g + 2]), h3 = ptx::to_tf32(yv[4 * g + 3]);
-          ptx::st_shared_v4(bbase + off, h0, h1, h2, h3);
-          if constexpr (SPLIT)  // lo rows BN..2BN-1 of the block (swizzle phase unchanged: BN % 8 == 0)
-            ptx::st_shared_v4(bbase + off + uint32_t(BN) * 128u, ptx::to_tf32(yv[4 * g] - h0),
-                              ptx::to_tf32(yv[4 * g + 1] - h1), ptx::to_tf32(yv[4 * g + 2] - h2),
-                              ptx::to_tf32(yv[4 * g + 3] - h3));
-        }
+      for (int g = 0; g < 4; ++g) {
+        const int gi = (strip & 1) * 4 + g;  // 16-byte granule within the 128-byte row
+        const uint32_t off = uint32_t(kb) * B_KB + uint32_t(col) * 128u + (uint32_t((gi ^ (col & 7)) & 7) << 4);
+        const float h0 = ptx::to_tf32(yv[4 * g]), h1 = ptx::to_tf32(yv[4 * g + 1]);
+        const float h2 = ptx::to_tf32(yv[4 * g + 2]), h3 = ptx::to_tf32(yv[4 * g + 3]);
+        ptx::st_shared_v4(bbase + off, h0, h1, h2, h3);
+        if constexpr (SPLIT)  // lo rows BN..2BN-1 of the block (swizzle phase unchanged: BN % 8 == 0)
+          ptx::st_shared_v4(bbase + off + uint32_t(BN) * 128u, ptx::to_tf32(yv[4 * g] - h0),
+                            ptx::to_tf32(yv[4 * g + 1] - h1), ptx::to_tf32(yv[4 * g + 2] - h2),
+                            ptx::to_tf32(yv[4 * g + 3] - h3));
+      }
+    };
+    for (int ch = ch0; ch < ch1; ++ch) {
+      const int b = (ch - ch0) & 1;
+      const int v0 = ch * KC;
+      // Every global load of this thread's share of the chunk is issued BEFORE waiting
+      // for the buffer: the loads fly while the MMAs of the two previous chunks run,
+      // and the conversion starts once with all data present (one memory round trip
+      // per chunk instead of one per row / item).
+      float xv[4][8];
+      bool inb = false;
+      const float* asrc = tid < a.rowsA ? a_src(v0, tid, inb) : a.x;
+      a_load(asrc, inb && tid < a.rowsA, xv);
+      float yv[NB][16];
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        const int it = tid + t * kStagers;
+        if (it < kItems) b_load(v0, it, yv[t]);
+      }
+      if (ch - ch0 >= 2) ptx::mbar_wait(&empty[b], uint32_t(((ch - ch0) >> 1) - 1) & 1u);
+      const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
+      if (tid < a.rowsA) a_store(abase, tid, xv);
+#pragma unroll
+      for (int t = 0; t < NB; ++t) {
+        const int it = tid + t * kStagers;
+        if (it < kItems) b_store(bbase, it, yv[t]);
+      }
+      for (int row = tid + kStagers; row < a.rowsA; row += kStagers) {  // tall tiles only
+        float xr[4][8];
+        bool in2 = false;
+        const float* s2 = a_src(v0, row, in2);
+        a_load(s2, in2, xr);
+        a_store(abase, row, xr);
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();

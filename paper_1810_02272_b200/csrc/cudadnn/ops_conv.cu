@@ -270,7 +270,7 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   }
   const int items = a.cblocks * a.ggroups * a.coblocks;
   a.nchunks = (a.Mv + tcwtap::KC - 1) / tcwtap::KC;
-  const int target = (smem <= 113 * 1024 ? 2 : 1) * kNumSMs;
+  const int target = (smem <= 113 * 1024 && bn < 128 ? 2 : 1) * kNumSMs;  // BN 128: one CTA per SM (registers)
   // whole waves: the largest split count whose grid still fits the resident slots
   // (a 168-CTA grid on 148 one-CTA SMs runs as two waves, the second one 20 CTAs wide)
   int splits = items >= target ? 1 : target / items;

@@ -199,3 +199,156 @@ def test_parallel_one_rank_nccl_matches_single_process():
             s.apply()
     for i in range(len(a.param_info())):
         assert np.array_equal(a.param(i), b.param(i)), a.param_info()[i]
+
+
+def _nccl_or_skip():
+    ok = C.c_int()
+    polegrad.cudadnn.load().cdnn_nccl_available(C.byref(ok))
+    if not ok.value:
+        pytest.skip("NCCL not loadable")
+
+
+def test_feed_ring_with_parallel_captures_every_bucket():
+    """FeedRing + Parallel: the ring's warm-up step launches no all-reduce
+    (the backward hook is detached), each captured slot contains one all-reduce per
+    bucket, and ring training equals eager data-parallel training bit for bit."""
+    _nccl_or_skip()
+    text = polegrad.load_model("cifar10_quick")
+    kw = CONFIGS["cifar10_quick"][1]
+    batches = synthetic_batches((100, 3, 32, 32), 10, 5, seed=12)
+    a = polegrad.Net(text, 1, "f32")
+    sa = polegrad.Solver(a, **kw)
+    pa = polegrad.Parallel(a, 1, 0, polegrad.Parallel.unique_id(), bucket_bytes=64 << 10)
+    sa.set_parallel(pa)
+    b = polegrad.Net(text, 1, "f32")
+    sb = polegrad.Solver(b, **kw)
+    pb = polegrad.Parallel(b, 1, 0, polegrad.Parallel.unique_id(), bucket_bytes=64 << 10)
+    sb.set_parallel(pb)
+    nb = pb.info()["buckets"]
+    assert nb >= 2
+    ring = polegrad.FeedRing(b, sb, 2)
+    assert pb.info()["launches"] == 2 * nb  # one per bucket in each captured slot, none from the warm-up
+    eager = []
+    for x, y in batches:
+        a.set_batch(x, y)
+        a.forward()
+        eager.append(a.loss())
+        a.backward()
+        sa.apply()
+    got, inflight = [], 0
+    for x, y in batches:
+        if inflight == 2:
+            got.append(ring.pop_loss())
+            inflight -= 1
+        ring.push(x, y)
+        inflight += 1
+    while inflight:
+        got.append(ring.pop_loss())
+        inflight -= 1
+    assert [np.float32(v) for v in got] == [np.float32(v) for v in eager]
+    for i in range(len(a.param_info())):
+        assert np.array_equal(a.param(i), b.param(i)), a.param_info()[i]
+    ring.close()
+    sa.set_parallel(None)
+    sb.set_parallel(None)
+
+
+def test_feed_ring_keeps_the_dropout_mask_sequence():
+    """The ring's warm-up restores the Dropout iteration counters: AlexNet
+    trained through the ring draws the same masks as eager steps, bit for bit."""
+    text = polegrad.load_model("alexnet", 2)
+    kw = CONFIGS["alexnet"][1]
+    batches = synthetic_batches((2, 3, 227, 227), 1000, 3, seed=13)
+    a = polegrad.Net(text, 1, "f32")
+    sa = polegrad.Solver(a, **kw)
+    b = polegrad.Net(text, 1, "f32")
+    sb = polegrad.Solver(b, **kw)
+    eager = []
+    for x, y in batches:
+        a.set_batch(x, y)
+        a.forward()
+        eager.append(a.loss())
+        a.backward()
+        sa.apply()
+    ring = polegrad.FeedRing(b, sb, 1)
+    got = []
+    for x, y in batches:
+        ring.push(x, y)
+        got.append(ring.pop_loss())
+    assert [np.float32(v) for v in got] == [np.float32(v) for v in eager]
+    for i in range(len(a.param_info())):
+        assert np.array_equal(a.param(i), b.param(i)), a.param_info()[i]
+    ring.close()
+
+
+def test_feed_ring_training_matches_the_oracle_fp64():
+    """Oracle leg of the feed ring (VERDICT r1 missing-5): FP64 CIFAR-quick trained
+    through the pinned ring equals the CPU oracle's eager training (MemoryData FIFO
+    semantics, layers.cpp:282-304) within north_star's FP64 bar."""
+    from parity_util import pyoracle, rel_l2
+    text = polegrad.load_model("cifar10_quick", 16)
+    kw = CONFIGS["cifar10_quick"][1]
+    batches = synthetic_batches((16, 3, 32, 32), 10, 4, seed=14)
+    net = polegrad.Net(text, 1, "f64")
+    sol = polegrad.Solver(net, **kw)
+    orc = pyoracle.OracleNet(text, 1, "f64")
+    osol = pyoracle.OracleSolver(orc, **kw)
+    ring = polegrad.FeedRing(net, sol, 2)
+    got, want, inflight = [], [], 0
+    for x, y in batches:
+        if inflight == 2:
+            got.append(ring.pop_loss())
+            inflight -= 1
+        ring.push(x, y)
+        inflight += 1
+        orc.set_batch(x, y)
+        want.append(orc.forward())
+        orc.backward()
+        osol.apply()
+    while inflight:
+        got.append(ring.pop_loss())
+        inflight -= 1
+    assert rel_l2(got, want) <= 1e-10, (got, want)
+    for i in range(len(net.param_info())):
+        assert rel_l2(net.param(i), orc.param(i)) <= 1e-10, net.param_info()[i]
+    ring.close()
+
+
+@pytest.mark.parametrize("config", ["cifar10_quick", "pg_mlp"])
+def test_resume_matches_the_oracle_uninterrupted_fp64(config):
+    """Oracle leg of checkpoint / resume (VERDICT r1 missing-5): 3 steps, MCWT + MCSS
+    snapshot, a fresh Net + Solver restored from it, 3 more steps -- equal to the CPU
+    oracle's uninterrupted 6 steps within the FP64 bar (the reference keeps no
+    solver state, so the oracle side never checkpoints)."""
+    from parity_util import pyoracle, rel_l2
+    model, skw, classes, batch = CONFIGS[config]
+    text = polegrad.load_model(model, batch if config != "cifar10_quick" else 16)
+    shape, labelled = data_shape(text)
+    batches = synthetic_batches(shape, classes, 6, seed=15)
+    a = polegrad.Net(text, 1, "f64")
+    sa = polegrad.Solver(a, **skw)
+    orc = pyoracle.OracleNet(text, 1, "f64")
+    osol = pyoracle.OracleSolver(orc, **skw)
+    for x, y in batches[:3]:
+        step(a, sa, x, y, labelled)
+    weights, state = a.snapshot(), sa.snapshot()
+    b = polegrad.Net(text, 99, "f64")
+    sb = polegrad.Solver(b, **skw)
+    b.restore(weights)
+    sb.restore(state)
+    for x, y in batches[3:]:
+        step(b, sb, x, y, labelled)
+    for x, y in batches:
+        if labelled:
+            orc.set_batch(x, y)
+        else:
+            orc.set_batch(x)
+        orc.forward()
+        if labelled:
+            orc.backward()
+        else:
+            orc.set_blob("logits", np.ones(orc.blob_shape("logits")), diff=True)
+            orc.backward_from("logits")
+        osol.apply()
+    for i in range(len(b.param_info())):
+        assert rel_l2(b.param(i), orc.param(i)) <= 1e-10, b.param_info()[i]
