@@ -73,7 +73,7 @@ struct WtapArgs {
 __host__ __device__ constexpr uint32_t a_bytes(int rowsA, bool split) { return uint32_t(rowsA) * 128u * (split ? 2u : 1u); }
 __host__ __device__ constexpr uint32_t b_bytes(int bn, bool split) { return uint32_t(bn) * KC * 4u * (split ? 2u : 1u); }
 inline int smem_bytes(int rowsA, int bn, bool split) {
-  return 1024 + 2 * int(a_bytes(rowsA, split) + b_bytes(bn, split)) + bn * 4 + 8 * 8 + 16;
+  return 1024 + 2 * int(a_bytes(rowsA, split) + b_bytes(bn, split)) + 2 * bn * 4 + 8 * 8 + 16;
 }
 
 __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -105,8 +105,8 @@ __global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(
   const uint32_t A_B = a_bytes(a.rowsA, SPLIT), A_H = uint32_t(a.rowsA) * 128u;
   constexpr uint32_t B_B = b_bytes(BN, SPLIT);
   const uint32_t STAGE = A_B + B_B;  // multiple of 1024 (rowsA % 8 == 0, BN*KC*4 % 1024 == 0)
-  float* bias_acc = reinterpret_cast<float*>(smem + 2 * STAGE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(bias_acc + BN);
+  float* bias_part = reinterpret_cast<float*>(smem + 2 * STAGE);  // [pixel half][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(bias_part + 2 * BN);
   uint64_t* empty = full + 2;
   uint64_t* accum = empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(
     ptx::mbar_init(accum, 1);
     ptx::fence_mbar_init();
   }
-  for (int i = threadIdx.x; i < BN; i += kThreads) bias_acc[i] = 0.f;
+  for (int i = threadIdx.x; i < 2 * BN; i += kThreads) bias_part[i] = 0.f;
   if (warp == 1) ptx::tmem_alloc(tmem_slot, tmem_cols);
   ptx::tc_fence_before();
   __syncthreads();
@@ -180,10 +180,17 @@ __global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(
     const int tid = threadIdx.x - 64;
     const int c0 = cb * 32, kc = min(32, a.Cg - c0);
     const int64_t HW = int64_t(a.H) * a.W, PQ = int64_t(a.P) * a.Q;
-    // B items (output channel, 16-pixel strip) per thread; A: one pixel row per thread
-    // (rows beyond kStagers, if any, take the sequential path below)
-    constexpr int kItems = BN * (KC / 16);
-    constexpr int NB = (kItems + kStagers - 1) / kStagers;
+    // B = dY^T [co][v0 .. v0+KC): lane = one virtual pixel (its index decomposed once per
+    // chunk), warp = one 32-pixel half and a quarter of the BN output channels, so each
+    // element costs one load at base + co*PQ and two 4-byte stores; a warp's 32 lanes
+    // fill one 128-byte K-major row (conflict free).  A: one pixel row per thread (rows
+    // beyond kStagers, if any, take the sequential path below).
+    static_assert(KC == 64, "two 32-pixel halves per chunk");
+    constexpr int CPW = BN / 4;  // output channels per warp
+    const int sw = tid >> 5, khalf = sw & 1, cw0 = (sw >> 1) * CPW;
+    float bsum[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) bsum[c] = 0.f;
     // A row `row` of chunk v0: source pointer and bounds
     auto a_src = [&](int v0, int row, bool& inb) {
       const int v = v0 + rlo + row;
@@ -223,49 +230,27 @@ __global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(
         }
       }
     };
-    // B: dY^T [co][v0 .. v0+KC), 16 pixels of one output channel (index decomposition once)
-    auto b_load = [&](int v0, int it, float (&yv)[16]) {
-      const int strip = it % (KC / 16), col = it / (KC / 16);
-      const int co = n0 + col;
-      int v = v0 + strip * 16;
-      int img = int(a.div_hwv.div(uint32_t(v)));
+    auto b_load = [&](int v0, float (&yv)[CPW]) {
+      const int v = v0 + khalf * 32 + lane;
+      const int img = int(a.div_hwv.div(uint32_t(v)));
       const int rem = v - img * HWv;
-      int p = int(a.div_wv.div(uint32_t(rem)));
-      int q = rem - p * a.Wv;
+      const int p = int(a.div_wv.div(uint32_t(rem)));
+      const int q = rem - p * a.Wv;
+      const bool ok = v < a.Mv && p < a.P && q < a.Q;
+      const float* src = a.dy + (ok ? int64_t(img) * a.dy_nstride + int64_t(p) * a.Q + q : 0) + int64_t(n0 + cw0) * PQ;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        yv[e] = (v < a.Mv && co < a.Cog && p < a.P && q < a.Q)
-                    ? __ldg(a.dy + int64_t(img) * a.dy_nstride + co * PQ + int64_t(p) * a.Q + q)
-                    : 0.f;
-        ++v;
-        if (++q == a.Wv) {
-          q = 0;
-          if (++p == a.Hv) { p = 0; ++img; }
-        }
-      }
+      for (int c = 0; c < CPW; ++c) yv[c] = (ok && n0 + cw0 + c < a.Cog) ? __ldg(src + c * PQ) : 0.f;
     };
-    auto b_store = [&](uint32_t bbase, int it, const float (&yv)[16]) {
-      const int strip = it % (KC / 16), col = it / (KC / 16);
-      if (do_bias) {  // the KC/16 = 4 lanes sharing `col` reduce in a fixed shuffle tree
-        float sb = 0.f;
+    auto b_store = [&](uint32_t bbase, const float (&yv)[CPW]) {
+      const uint32_t lane_off = uint32_t(khalf) * B_KB + uint32_t(lane & 3) * 4u;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) sb += yv[e];
-        sb += __shfl_xor_sync(0xffffffffu, sb, 1);
-        sb += __shfl_xor_sync(0xffffffffu, sb, 2);
-        if ((lane & 3) == 0) bias_acc[col] += sb;
-      }
-      const int kb = strip >> 1;  // 32-pixel block
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int gi = (strip & 1) * 4 + g;  // 16-byte granule within the 128-byte row
-        const uint32_t off = uint32_t(kb) * B_KB + uint32_t(col) * 128u + (uint32_t((gi ^ (col & 7)) & 7) << 4);
-        const float h0 = ptx::to_tf32(yv[4 * g]), h1 = ptx::to_tf32(yv[4 * g + 1]);
-        const float h2 = ptx::to_tf32(yv[4 * g + 2]), h3 = ptx::to_tf32(yv[4 * g + 3]);
-        ptx::st_shared_v4(bbase + off, h0, h1, h2, h3);
-        if constexpr (SPLIT)  // lo rows BN..2BN-1 of the block (swizzle phase unchanged: BN % 8 == 0)
-          ptx::st_shared_v4(bbase + off + uint32_t(BN) * 128u, ptx::to_tf32(yv[4 * g] - h0),
-                            ptx::to_tf32(yv[4 * g + 1] - h1), ptx::to_tf32(yv[4 * g + 2] - h2),
-                            ptx::to_tf32(yv[4 * g + 3] - h3));
+      for (int c = 0; c < CPW; ++c) {
+        const int col = cw0 + c;
+        const uint32_t off = lane_off + uint32_t(col) * 128u + (uint32_t(((lane >> 2) ^ (col & 7)) & 7) << 4);
+        const float h = ptx::to_tf32(yv[c]);
+        ptx::st_shared_f32(bbase + off, h);
+        if constexpr (SPLIT) ptx::st_shared_f32(bbase + off + uint32_t(BN) * 128u, ptx::to_tf32(yv[c] - h));
+        if (do_bias) bsum[c] += yv[c];
       }
     };
     for (int ch = ch0; ch < ch1; ++ch) {
@@ -279,20 +264,12 @@ __global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(
       bool inb = false;
       const float* asrc = tid < a.rowsA ? a_src(v0, tid, inb) : a.x;
       a_load(asrc, inb && tid < a.rowsA, xv);
-      float yv[NB][16];
-#pragma unroll
-      for (int t = 0; t < NB; ++t) {
-        const int it = tid + t * kStagers;
-        if (it < kItems) b_load(v0, it, yv[t]);
-      }
+      float yv[CPW];
+      b_load(v0, yv);
       if (ch - ch0 >= 2) ptx::mbar_wait(&empty[b], uint32_t(((ch - ch0) >> 1) - 1) & 1u);
       const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
       if (tid < a.rowsA) a_store(abase, tid, xv);
-#pragma unroll
-      for (int t = 0; t < NB; ++t) {
-        const int it = tid + t * kStagers;
-        if (it < kItems) b_store(bbase, it, yv[t]);
-      }
+      b_store(bbase, yv);
       for (int row = tid + kStagers; row < a.rowsA; row += kStagers) {  // tall tiles only
         float xr[4][8];
         bool in2 = false;
@@ -304,6 +281,16 @@ __global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&full[b]);
     }
+    if (do_bias) {  // per output channel: fixed xor tree over the warp's 32 pixels, then the two halves
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        float t = bsum[c];
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+        if (lane == 0) bias_part[khalf * BN + cw0 + c] = t;
+      }
+    }
+    ptx::named_bar_sync(1, kStagers);  // stager warps only: bias partials complete
     // ---- epilogue (warps 2-5): TMEM lane (j*32 + c) of group g = tap (r, s0 + j), channel c
     if (warp >= 6) goto done;
     {
@@ -345,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(
     }
     if (do_bias && warp == 2) {
       for (int col = lane; col < BN; col += 32)
-        if (n0 + col < a.Cog) wsz[int64_t(n0 + col) * (a.Kc + 1) + a.Kc] = bias_acc[col];
+        if (n0 + col < a.Cog) wsz[int64_t(n0 + col) * (a.Kc + 1) + a.Kc] = bias_part[col] + bias_part[BN + col];
     }
     }
   }
