@@ -29,15 +29,34 @@ __device__ __forceinline__ T sq_acc(T s, T x) { return fma_(x, x, s); }
 // scale = k + aN * sum
 template <typename T>
 __device__ __forceinline__ T scale(T sum, T aN, T k) { return fma_(aN, sum, k); }
+// float: the SFU's approximate base-2 logarithm / exponential / reciprocal (relative
+// error ~2^-22; scale >= k > 0, so no denormal inputs) -- deterministic single
+// instructions, where the IEEE-exact powf / division cost a function call each
+__device__ __forceinline__ float lg2_(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double rcp_(double x) { return __drcp_rn(x); }
 // scale^-beta
-__device__ __forceinline__ float neg_pow(float sc, float beta) { return exp2f(mul_(-beta, log2f(sc))); }
+__device__ __forceinline__ float neg_pow(float sc, float beta) { return ex2_(mul_(-beta, lg2_(sc))); }
 __device__ __forceinline__ double neg_pow(double sc, double beta) { return pow(sc, -beta); }
 // forward top
 template <typename T>
 __device__ __forceinline__ T top(T x, T np) { return mul_(x, np); }
 // backward window term dy * y / scale
-template <typename T>
-__device__ __forceinline__ T term(T dy, T y, T sc) { return div_(mul_(dy, y), sc); }
+__device__ __forceinline__ float term(float dy, float y, float sc) { return mul_(mul_(dy, y), rcp_(sc)); }
+__device__ __forceinline__ double term(double dy, double y, double sc) { return div_(mul_(dy, y), sc); }
 // backward: dy * np - coef * x * acc
 template <typename T>
 __device__ __forceinline__ T grad(T dy, T np, T coef, T x, T acc) { return sub_(mul_(dy, np), mul_(mul_(coef, x), acc)); }

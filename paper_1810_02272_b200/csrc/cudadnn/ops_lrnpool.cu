@@ -61,19 +61,21 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
   const int p = threadIdx.x;
   const bool active = p < npix;
   const int h = r0 + (active ? p / g.W : 0);
-  const int64_t base = int64_t(img) * g.C * HW + int64_t(h) * g.W + (active ? p % g.W : 0);
+  const size_t base = size_t(img) * g.C * HW + size_t(h) * g.W + (active ? p % g.W : 0);
+  const T* xp = x + base;
+  T* yp = ynorm + base;
   const bool own = active && h < own1;
   T xr[SIZE];  // x(c - pre .. c + post)
 #pragma unroll
   for (int j = 0; j < SIZE; ++j) {
     const int cc = cs0 + j - pre;
-    xr[j] = (active && cc >= 0 && cc < g.C) ? __ldg(x + base + int64_t(cc) * HW) : T(0);
+    xr[j] = (active && cc >= 0 && cc < g.C) ? __ldg(xp + uint32_t(cc) * uint32_t(HW)) : T(0);
   }
   auto load_step = [&](int c0, T (&nx)[kG]) {
 #pragma unroll
     for (int u = 0; u < kG; ++u) {
       const int cin = c0 + u + post + 1;
-      nx[u] = (active && c0 + u < cs1 && cin < g.C) ? __ldg(x + base + int64_t(cin) * HW) : T(0);
+      nx[u] = (active && c0 + u < cs1 && cin < g.C) ? __ldg(xp + uint32_t(cin) * uint32_t(HW)) : T(0);
     }
   };
   T nxt[kG];
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
         const T sc = lrn::scale(sum, aN, k);
         const T yv = lrn::top(xr[pre], lrn::neg_pow(sc, beta));
         buf[u * tsz + p] = yv;
-        if (own) ynorm[base + int64_t(c) * HW] = yv;
+        if (own) yp[uint32_t(c) * uint32_t(HW)] = yv;
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
         xr[SIZE - 1] = cur[u];
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
             if (v > best) { best = v; arg = (hs + a) * g.W + ws + b; }
           }
         }
-      const int64_t o = (int64_t(img) * g.C + c0 + u) * PHW + int64_t(pr0 + prl) * g.PW + pw;
+      const uint32_t o = (uint32_t(img) * g.C + c0 + u) * uint32_t(PHW) + uint32_t((pr0 + prl) * g.PW + pw);
       ypool[o] = relu ? (best > T(0) ? best : T(0)) : best;
       mask[o] = arg;
     }
@@ -129,39 +131,53 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
   }
 }
 
-// Backward: one thread per (pixel, channel segment).
+// Backward: one thread per (pixel, channel segment).  32-bit element offsets (the
+// tensors are < 2^31 elements: fusable()); the pixel's <= R x R window offsets into
+// the pooled plane are computed once.
 template <typename T, int SIZE, int K, int S>
 __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
                                                        const int* __restrict__ mask, T* __restrict__ dx,
                                                        LrnPoolGeom g, T alpha, T beta, T k, bool gate_x) {
   constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
   constexpr int R = (K + S - 1) / S;
-  const int HW = g.H * g.W, PHW = g.PH * g.PW;
-  const int64_t pixels = int64_t(g.N) * HW;
-  const int64_t work = pixels * g.segs;
+  const uint32_t HW = uint32_t(g.H * g.W), PHW = uint32_t(g.PH * g.PW);
+  const uint32_t pixels = uint32_t(g.N) * HW;
+  const uint32_t work = pixels * uint32_t(g.segs);
   const T aN = alpha / T(SIZE);
   const T coef = T(2) * alpha * beta / T(SIZE);
-  for (int64_t wi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; wi < work; wi += int64_t(gridDim.x) * blockDim.x) {
+  for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < work; wi += gridDim.x * blockDim.x) {
     // consecutive threads: consecutive pixels of one segment (coalesced)
-    const int seg = int(wi / pixels);
-    const int64_t pix = wi - int64_t(seg) * pixels;
-    const int cs0 = seg * kSeg, cs1 = min(g.C, cs0 + kSeg);
-    const int img = int(pix / HW), hw = int(pix - int64_t(img) * HW);
-    const int h = hw / g.W, w = hw - h * g.W;
+    const uint32_t seg = wi / pixels;
+    const uint32_t pix = wi - seg * pixels;
+    const int cs0 = int(seg) * kSeg, cs1 = min(g.C, cs0 + kSeg);
+    const uint32_t img = pix / HW, hw = pix - img * HW;
+    const int h = int(hw) / g.W, w = int(hw) - h * g.W;
     const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
     const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
-    const int64_t base = int64_t(img) * g.C * HW + hw;
-    const int64_t pbase = int64_t(img) * g.C * PHW + int64_t(phs) * g.PW + pws;
+    const T* xp = x + size_t(img) * g.C * HW + hw;
+    T* dxp = dx + size_t(img) * g.C * HW + hw;
+    const int* mp = mask + size_t(img) * g.C * PHW;
+    const T* dp = pdy + size_t(img) * g.C * PHW;
+    uint32_t woff[R][R];
+    bool wok[R][R];
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        wok[a][b] = phs + a < phe && pws + b < pwe;
+        woff[a][b] = uint32_t((phs + a) * g.PW + pws + b);
+      }
+    auto xat = [&](int cc) { return (cc >= 0 && cc < g.C) ? __ldg(xp + uint32_t(cc) * HW) : T(0); };
     // the LRN top diff of channel cc at this pixel: max_pool_bwd_k's gather, in its order
     auto gather = [&](int cc, int (&m)[R][R], T (&v)[R][R]) {
+      const uint32_t co = uint32_t(cc) * PHW;
 #pragma unroll
       for (int a = 0; a < R; ++a)
 #pragma unroll
         for (int b = 0; b < R; ++b) {
-          const bool ok = cc < g.C && phs + a < phe && pws + b < pwe;
-          const int64_t o = pbase + int64_t(cc) * PHW + a * g.PW + b;
-          m[a][b] = ok ? __ldg(mask + o) : -1;
-          v[a][b] = ok ? __ldg(pdy + o) : T(0);
+          const bool ok = cc < g.C && wok[a][b];
+          m[a][b] = ok ? __ldg(mp + co + woff[a][b]) : -1;
+          v[a][b] = ok ? __ldg(dp + co + woff[a][b]) : T(0);
         }
     };
     auto ndy_of = [&](const int (&m)[R][R], const T (&v)[R][R]) {
@@ -170,7 +186,7 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
       for (int a = 0; a < R; ++a)
 #pragma unroll
         for (int b = 0; b < R; ++b)
-          if (m[a][b] == hw) sdy += v[a][b];
+          if (m[a][b] == int(hw)) sdy += v[a][b];
       return sdy;
     };
     // rings over channels c - post .. c + pre: t = dy*y/scale, dy, scale^-beta (lrn_bwd_ring;
@@ -185,13 +201,10 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
       if (cc >= 0 && cc < g.C) {
         T sum = T(0);
 #pragma unroll
-        for (int q = 0; q < SIZE; ++q) {
-          const int cx = cc - pre + q;
-          sum = lrn::sq_acc(sum, (cx >= 0 && cx < g.C) ? __ldg(x + base + int64_t(cx) * HW) : T(0));
-        }
+        for (int q = 0; q < SIZE; ++q) sum = lrn::sq_acc(sum, xat(cc - pre + q));
         const T sc = lrn::scale(sum, aN, k);
         const T np = lrn::neg_pow(sc, beta);
-        const T yv = lrn::top(__ldg(x + base + int64_t(cc) * HW), np);
+        const T yv = lrn::top(xat(cc), np);
         int m[R][R];
         T v[R][R];
         gather(cc, m, v);
@@ -204,16 +217,12 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
     // x ring: x(c .. c + SIZE - 1), the window of the entering channel c + pre
     T xr[SIZE];
 #pragma unroll
-    for (int j = 0; j < SIZE - 1; ++j) {
-      const int cc = cs0 + j;
-      xr[j] = cc < g.C ? __ldg(x + base + int64_t(cc) * HW) : T(0);
-    }
+    for (int j = 0; j < SIZE - 1; ++j) xr[j] = xat(cs0 + j);
     xr[SIZE - 1] = T(0);
     auto load_step = [&](int c0, T (&nx)[kG], int (&nm)[kG][R][R], T (&nv)[kG][R][R]) {
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
-        const int cin = c0 + u + SIZE - 1;
-        nx[u] = (c0 + u < cs1 && cin < g.C) ? __ldg(x + base + int64_t(cin) * HW) : T(0);
+        nx[u] = c0 + u < cs1 ? xat(c0 + u + SIZE - 1) : T(0);
         gather(c0 + u < cs1 ? c0 + u + pre : g.C, nm[u], nv[u]);
       }
     };
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
         for (int j = 0; j < SIZE; ++j) acc = lrn::add_(acc, tr[j]);
         const T xc = xr[0];
         const T gval = lrn::grad(dyr[post], npr[post], coef, xc, acc);
-        dx[base + int64_t(c) * HW] = (!gate_x || xc > T(0)) ? gval : T(0);
+        dxp[uint32_t(c) * HW] = (!gate_x || xc > T(0)) ? gval : T(0);
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
       }
@@ -288,7 +297,8 @@ bool fusable(const PoolDescSlot& d, int size) {
                       ((p.kernel_h == 3 && p.stride_h == 2) || (p.kernel_h == 2 && p.stride_h == 2));
   return p.method == CDNN_POOL_MAX && !p.global_pooling && p.pad_h == 0 && p.pad_w == 0 && window &&
          (size == 3 || size == 5) && p.kernel_h * p.w <= 1024 &&
-         uint64_t(p.n) * p.c * p.h * p.w < (1ull << 31);
+         uint64_t(p.n) * p.c * p.h * p.w < (1ull << 31) &&
+         uint64_t(p.n) * p.h * p.w * ((p.c + kSeg - 1) / kSeg) < (1ull << 31);
 }
 
 template <typename T, int SIZE, int K, int S>
