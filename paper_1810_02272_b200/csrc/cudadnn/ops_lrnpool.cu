@@ -26,6 +26,7 @@
 // pixel, in max_pool_bwd_k's order), then dx(c) from the rings of lrn_bwd_ring.
 #include "launch.cuh"
 #include "lrn_math.cuh"
+#include "ptx.cuh"
 
 namespace cdnn {
 namespace {
@@ -40,6 +41,25 @@ struct LrnPoolGeom {
   int bands;
   int segs;   // channel segments of kCB
 };
+
+// channels [cfirst, cfirst + n) x npix consecutive elements of each plane -> smem tile
+// [n][npix], by cp.async (no register round trip: every load of the tile is in flight
+// at once); channels outside [0, C) are zero-filled.
+template <typename T>
+__device__ __forceinline__ void tile_async(T* tile, const T* base, int cfirst, int n, int C, uint32_t plane,
+                                           int npix) {
+  const uint32_t s0 = ptx::smem_u32(tile);
+  for (int cl = 0; cl < n; ++cl) {
+    const int c = cfirst + cl;
+    const bool in = c >= 0 && c < C;
+    const T* src = base + uint32_t(in ? c : 0) * plane;
+    for (int p = threadIdx.x; p < npix; p += kThreads) {
+      const uint32_t dst = s0 + uint32_t(cl * npix + p) * uint32_t(sizeof(T));
+      if constexpr (sizeof(T) == 4) ptx::cp_async_4(dst, src + p, in ? 4u : 0u);
+      else ptx::cp_async_8(dst, src + p, in ? 8u : 0u);
+    }
+  }
+}
 
 // Forward: block (band of TRP pooled rows, channel segment, image).
 //   A  x tile: channels [c0-pre, c1+post) x the band's input rows -> smem (coalesced rows)
@@ -61,13 +81,8 @@ __global__ void __launch_bounds__(kThreads) lrn_maxpool_fwd(const T* __restrict_
   const uint32_t HW = uint32_t(g.H * g.W), PHW = uint32_t(g.PH * g.PW);
   T* xs = reinterpret_cast<T*>(smem_raw);       // [nc + SIZE - 1][npix]
   T* ys = xs + (kCB + SIZE - 1) * npix;         // [nc][npix]
-  const T* xb = x + size_t(img) * g.C * HW + uint32_t(r0 * g.W);
-  for (int cl = 0; cl < nc + SIZE - 1; ++cl) {
-    const int c = c0 - pre + cl;
-    const bool in = c >= 0 && c < g.C;
-    const T* src = xb + uint32_t(in ? c : 0) * HW;
-    for (int p = threadIdx.x; p < npix; p += kThreads) xs[cl * npix + p] = in ? __ldg(src + p) : T(0);
-  }
+  tile_async(xs, x + size_t(img) * g.C * HW + uint32_t(r0 * g.W), c0 - pre, nc + SIZE - 1, g.C, HW, npix);
+  ptx::cp_async_wait_all();
   __syncthreads();
   const T aN = alpha / T(SIZE);
   T* yb = ynorm + size_t(img) * g.C * HW + uint32_t(r0 * g.W);
@@ -131,65 +146,59 @@ __global__ void __launch_bounds__(kThreads) lrn_maxpool_bwd(const T* __restrict_
   T* nd = reinterpret_cast<T*>(smem_raw);   // [ndc][npix]: LRN top diff, then p1 (own channels)
   T* xs = nd + (kCB + SIZE - 1) * npix;     // [nc + 2(SIZE-1)][npix]
   T* ts = xs + (kCB + 2 * (SIZE - 1)) * npix;  // [ndc][npix]
+  // the x tile flies (cp.async) while the pooled diffs are scattered
+  tile_async(xs, x + size_t(img) * g.C * HW + uint32_t(r0 * g.W), c0 - (SIZE - 1), nc + 2 * (SIZE - 1), g.C, HW,
+             npix);
   for (int i = threadIdx.x; i < ndc * npix; i += kThreads) nd[i] = T(0);
   // pooled rows whose windows reach the owned rows
   const int ph0 = max(0, (r0 - K + S) / S), ph1 = min(g.PH, (r1 - 1) / S + 1);
   const int per_c = (ph1 - ph0) * g.PW, nitems = ndc * per_c;
-  const size_t pbase = size_t(img) * g.C * PHW;
-  int im[kMaxItems];
+  const int* mb = mask + size_t(img) * g.C * PHW;
+  const T* db0 = pdy + size_t(img) * g.C * PHW;
+  // one pooled element -> (tile cell of its argmax or -1, pass); the pass is the
+  // position of this window in max_pool_bwd_k's gather order for that pixel
+  auto locate = [&](int it, int& cell, int& pass, T& v) {
+    const int cl = it / per_c, rem = it - cl * per_c;
+    const int c = c0 - post + cl;
+    cell = -1;
+    pass = 0;
+    v = T(0);
+    if (c < 0 || c >= g.C) return;
+    const uint32_t o = uint32_t(c) * PHW + uint32_t(ph0 * g.PW + rem);
+    const int m = __ldg(mb + o);
+    v = __ldg(db0 + o);
+    if (m < 0) return;
+    const int mh = m / g.W;
+    if (mh < r0 || mh >= r1) return;
+    const int prl = rem / g.PW, ph = ph0 + prl, pw = rem - prl * g.PW, mw = m - mh * g.W;
+    const int a = (K > S && mh == ph * S && ph > 0) ? 1 : 0;  // second window of that row
+    const int b = (K > S && mw == pw * S && pw > 0) ? 1 : 0;
+    cell = cl * npix + (m - r0 * g.W);
+    pass = a * 2 + b;
+  };
+  int icell[kMaxItems], ipass[kMaxItems];
   T iv[kMaxItems];
 #pragma unroll
   for (int q = 0; q < kMaxItems; ++q) {
     const int it = threadIdx.x + q * kThreads;
-    im[q] = -1;
+    icell[q] = -1;
+    ipass[q] = 0;
     iv[q] = T(0);
-    if (it < nitems) {
-      const int cl = it / per_c, rem = it - cl * per_c;
-      const int c = c0 - post + cl;
-      if (c >= 0 && c < g.C) {
-        const uint32_t o = uint32_t(c) * PHW + uint32_t(ph0 * g.PW + rem);
-        im[q] = __ldg(mask + pbase + o);
-        iv[q] = __ldg(pdy + pbase + o);
-      }
-    }
+    if (it < nitems) locate(it, icell[q], ipass[q], iv[q]);
   }
   for (int pass = 0; pass < 4; ++pass) {
     __syncthreads();
-    for (int q = 0; q < kMaxItems + 1; ++q) {  // the last round re-reads items beyond the register budget
-      for (int it = threadIdx.x + q * kThreads; it < nitems; it += (q < kMaxItems ? nitems : kThreads)) {
-        int m;
-        T v;
-        const int cl = it / per_c, rem = it - cl * per_c;
-        if (q < kMaxItems) {
-          m = im[q];
-          v = iv[q];
-        } else {
-          const int c = c0 - post + cl;
-          if (c < 0 || c >= g.C) continue;
-          const uint32_t o = uint32_t(c) * PHW + uint32_t(ph0 * g.PW + rem);
-          m = __ldg(mask + pbase + o);
-          v = __ldg(pdy + pbase + o);
-        }
-        if (m < 0) continue;
-        const int ph = ph0 + rem / g.PW, pw = rem - (rem / g.PW) * g.PW;
-        const int mh = m / g.W, mw = m - mh * g.W;
-        if (mh < r0 || mh >= r1) continue;
-        const int a = (K > S && mh == ph * S && ph > 0) ? 1 : 0;  // second window of that row
-        const int b = (K > S && mw == pw * S && pw > 0) ? 1 : 0;
-        if (a * 2 + b != pass) continue;
-        T* cell = nd + cl * npix + (m - r0 * g.W);
-        *cell += v;
-      }
+#pragma unroll
+    for (int q = 0; q < kMaxItems; ++q)
+      if (icell[q] >= 0 && ipass[q] == pass) nd[icell[q]] += iv[q];
+    for (int it = threadIdx.x + kMaxItems * kThreads; it < nitems; it += kThreads) {  // beyond the registers
+      int cell, ps;
+      T v;
+      locate(it, cell, ps, v);
+      if (cell >= 0 && ps == pass) nd[cell] += v;
     }
   }
-  // x tile (no dependence on the scatter)
-  const T* xb = x + size_t(img) * g.C * HW + uint32_t(r0 * g.W);
-  for (int cl = 0; cl < nc + 2 * (SIZE - 1); ++cl) {
-    const int c = c0 - (SIZE - 1) + cl;
-    const bool in = c >= 0 && c < g.C;
-    const T* src = xb + uint32_t(in ? c : 0) * HW;
-    for (int p = threadIdx.x; p < npix; p += kThreads) xs[cl * npix + p] = in ? __ldg(src + p) : T(0);
-  }
+  ptx::cp_async_wait_all();
   __syncthreads();
   const T aN = alpha / T(SIZE);
   for (int cl = 0; cl < ndc; ++cl) {  // channel c' = c0 - post + cl
