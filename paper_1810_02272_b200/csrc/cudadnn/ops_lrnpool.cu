@@ -26,258 +26,289 @@
 // pixel, in max_pool_bwd_k's order), then dx(c) from the rings of lrn_bwd_ring.
 #include "launch.cuh"
 #include "lrn_math.cuh"
-#include "ptx.cuh"
 
 namespace cdnn {
 namespace {
 
-constexpr int kCB = 16;       // LRN channels per block (the channel halos are loaded / computed twice)
-constexpr int kThreads = 256;
-constexpr int kMaxItems = 12;  // pooled (mask, dy) pairs one thread holds in the backward scatter
+constexpr int kG = 4;     // channels per step (loads in flight; one block barrier per step)
+constexpr int kSeg = 32;  // channels per thread / block segment (segments run in parallel)
 
 struct LrnPoolGeom {
   int N, C, H, W, PH, PW;
-  int TRP;    // pooled rows per band
+  int TR, rows_in;  // pooled rows per band, input rows per band
   int bands;
-  int segs;   // channel segments of kCB
+  int segs;         // channel segments of kSeg
 };
 
-// channels [cfirst, cfirst + n) x npix consecutive elements of each plane -> smem tile
-// [n][npix], by cp.async (no register round trip: every load of the tile is in flight
-// at once); channels outside [0, C) are zero-filled.
-template <typename T>
-__device__ __forceinline__ void tile_async(T* tile, const T* base, int cfirst, int n, int C, uint32_t plane,
-                                           int npix) {
-  const uint32_t s0 = ptx::smem_u32(tile);
-  for (int cl = 0; cl < n; ++cl) {
-    const int c = cfirst + cl;
-    const bool in = c >= 0 && c < C;
-    const T* src = base + uint32_t(in ? c : 0) * plane;
-    for (int p = threadIdx.x; p < npix; p += kThreads) {
-      const uint32_t dst = s0 + uint32_t(cl * npix + p) * uint32_t(sizeof(T));
-      if constexpr (sizeof(T) == 4) ptx::cp_async_4(dst, src + p, in ? 4u : 0u);
-      else ptx::cp_async_8(dst, src + p, in ? 8u : 0u);
-    }
-  }
-}
-
-// Forward: block (band of TRP pooled rows, channel segment, image).
-//   A  x tile: channels [c0-pre, c1+post) x the band's input rows -> smem (coalesced rows)
-//   B  LRN top for [c0, c1) from the tile (window sum in lrn_fwd_ring's order) -> smem,
-//      and to HBM for the rows this band owns (halo rows belong to the next band)
-//   C  the pooled maxima / argmax of the band from the smem tile
+// Forward: block (band, channel segment, image).  The x loads of step i+1 are issued
+// before step i's arithmetic and barrier (lookahead of one step).
 template <typename T, int SIZE, int K, int S>
-__global__ void __launch_bounds__(kThreads) lrn_maxpool_fwd(const T* __restrict__ x, T* __restrict__ ynorm,
-                                                            T* __restrict__ ypool, int* __restrict__ mask,
-                                                            LrnPoolGeom g, T alpha, T beta, T k, bool relu) {
-  constexpr int pre = (SIZE - 1) / 2;
-  extern __shared__ uint8_t smem_raw[];
-  const int band = blockIdx.x, img = blockIdx.z;
-  const int c0 = blockIdx.y * kCB, c1 = min(g.C, c0 + kCB), nc = c1 - c0;
-  const int pr0 = band * g.TRP, pr1 = min(g.PH, pr0 + g.TRP);
-  const int r0 = pr0 * S, r1 = min(g.H, (pr1 - 1) * S + K);
-  const int own1 = band + 1 == g.bands ? g.H : min(g.H, pr1 * S);
-  const int npix = (r1 - r0) * g.W, nown = (own1 - r0) * g.W;
-  const uint32_t HW = uint32_t(g.H * g.W), PHW = uint32_t(g.PH * g.PW);
-  T* xs = reinterpret_cast<T*>(smem_raw);       // [nc + SIZE - 1][npix]
-  T* ys = xs + (kCB + SIZE - 1) * npix;         // [nc][npix]
-  tile_async(xs, x + size_t(img) * g.C * HW + uint32_t(r0 * g.W), c0 - pre, nc + SIZE - 1, g.C, HW, npix);
-  ptx::cp_async_wait_all();
-  __syncthreads();
-  const T aN = alpha / T(SIZE);
-  T* yb = ynorm + size_t(img) * g.C * HW + uint32_t(r0 * g.W);
-  for (int cl = 0; cl < nc; ++cl) {
-    T* dst = yb + uint32_t(c0 + cl) * HW;
-    for (int p = threadIdx.x; p < npix; p += kThreads) {
-      T sum = T(0);
-#pragma unroll
-      for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xs[(cl + j) * npix + p]);
-      const T sc = lrn::scale(sum, aN, k);
-      const T yv = lrn::top(xs[(cl + pre) * npix + p], lrn::neg_pow(sc, beta));
-      ys[cl * npix + p] = yv;
-      if (p < nown) dst[p] = yv;
-    }
-  }
-  __syncthreads();
-  const int prows = pr1 - pr0, per_c = prows * g.PW;
-  for (int it = threadIdx.x; it < nc * per_c; it += kThreads) {
-    const int cl = it / per_c, rem = it - cl * per_c;
-    const int prl = rem / g.PW, pw = rem - prl * g.PW;
-    const int hs = (pr0 + prl) * S, ws = pw * S;
-    const T* t = ys + cl * npix + (hs - r0) * g.W;
-    T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
-    int arg = -1;
-#pragma unroll
-    for (int a = 0; a < K; ++a)
-#pragma unroll
-      for (int b = 0; b < K; ++b)
-        if (hs + a < g.H && ws + b < g.W) {
-          const T v = t[a * g.W + ws + b];
-          if (v > best) { best = v; arg = (hs + a) * g.W + ws + b; }
-        }
-    const uint32_t o = (uint32_t(img) * g.C + c0 + cl) * PHW + uint32_t((pr0 + prl) * g.PW + pw);
-    ypool[o] = relu ? (best > T(0) ? best : T(0)) : best;
-    mask[o] = arg;
-  }
-}
-
-// Backward: block (band of TRP pooled rows = the pixel rows it owns, channel segment, image).
-//   0  LRN top diff of channels [c0-post, c1+pre) on the owned pixels by a deterministic
-//      scatter of the pooled diffs through the argmax mask: four passes in the order
-//      max_pool_bwd_k's gather adds a pixel's windows ((a, b) = (0,0), (0,1), (1,0), (1,1)
-//      relative to its first window), so the sums are bit-identical; within a pass no
-//      two windows share a pixel
-//   1  x tile: channels [c0-(SIZE-1), c1+(SIZE-1)) on the owned pixels
-//   2  t = dy*y/scale for [c0-post, c1+pre); p1 = dy*scale^-beta kept for [c0, c1)
-//   3  dx for [c0, c1) (ring sum in lrn_bwd_ring's order), gated, coalesced stores
-template <typename T, int SIZE, int K, int S>
-__global__ void __launch_bounds__(kThreads) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
-                                                            const int* __restrict__ mask, T* __restrict__ dx,
-                                                            LrnPoolGeom g, T alpha, T beta, T k, bool gate_x) {
+__global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x, T* __restrict__ ynorm,
+                                                        T* __restrict__ ypool, int* __restrict__ mask,
+                                                        LrnPoolGeom g, T alpha, T beta, T k, bool relu) {
   constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
   extern __shared__ uint8_t smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);  // [2][kG][rows_in * W]
   const int band = blockIdx.x, img = blockIdx.z;
-  const int c0 = blockIdx.y * kCB, c1 = min(g.C, c0 + kCB), nc = c1 - c0;
-  const int pr0 = band * g.TRP, pr1 = min(g.PH, pr0 + g.TRP);
-  const int r0 = pr0 * S, r1 = band + 1 == g.bands ? g.H : min(g.H, pr1 * S);  // owned pixel rows
-  const int npix = (r1 - r0) * g.W;
-  const uint32_t HW = uint32_t(g.H * g.W), PHW = uint32_t(g.PH * g.PW);
-  const int ndc = nc + SIZE - 1;            // channels with a top diff / t
-  T* nd = reinterpret_cast<T*>(smem_raw);   // [ndc][npix]: LRN top diff, then p1 (own channels)
-  T* xs = nd + (kCB + SIZE - 1) * npix;     // [nc + 2(SIZE-1)][npix]
-  T* ts = xs + (kCB + 2 * (SIZE - 1)) * npix;  // [ndc][npix]
-  // the x tile flies (cp.async) while the pooled diffs are scattered
-  tile_async(xs, x + size_t(img) * g.C * HW + uint32_t(r0 * g.W), c0 - (SIZE - 1), nc + 2 * (SIZE - 1), g.C, HW,
-             npix);
-  for (int i = threadIdx.x; i < ndc * npix; i += kThreads) nd[i] = T(0);
-  // pooled rows whose windows reach the owned rows
-  const int ph0 = max(0, (r0 - K + S) / S), ph1 = min(g.PH, (r1 - 1) / S + 1);
-  const int per_c = (ph1 - ph0) * g.PW, nitems = ndc * per_c;
-  const int* mb = mask + size_t(img) * g.C * PHW;
-  const T* db0 = pdy + size_t(img) * g.C * PHW;
-  // one pooled element -> (tile cell of its argmax or -1, pass); the pass is the
-  // position of this window in max_pool_bwd_k's gather order for that pixel
-  auto locate = [&](int it, int& cell, int& pass, T& v) {
-    const int cl = it / per_c, rem = it - cl * per_c;
-    const int c = c0 - post + cl;
-    cell = -1;
-    pass = 0;
-    v = T(0);
-    if (c < 0 || c >= g.C) return;
-    const uint32_t o = uint32_t(c) * PHW + uint32_t(ph0 * g.PW + rem);
-    const int m = __ldg(mb + o);
-    v = __ldg(db0 + o);
-    if (m < 0) return;
-    const int mh = m / g.W;
-    if (mh < r0 || mh >= r1) return;
-    const int prl = rem / g.PW, ph = ph0 + prl, pw = rem - prl * g.PW, mw = m - mh * g.W;
-    const int a = (K > S && mh == ph * S && ph > 0) ? 1 : 0;  // second window of that row
-    const int b = (K > S && mw == pw * S && pw > 0) ? 1 : 0;
-    cell = cl * npix + (m - r0 * g.W);
-    pass = a * 2 + b;
-  };
-  int icell[kMaxItems], ipass[kMaxItems];
-  T iv[kMaxItems];
-#pragma unroll
-  for (int q = 0; q < kMaxItems; ++q) {
-    const int it = threadIdx.x + q * kThreads;
-    icell[q] = -1;
-    ipass[q] = 0;
-    iv[q] = T(0);
-    if (it < nitems) locate(it, icell[q], ipass[q], iv[q]);
-  }
-  for (int pass = 0; pass < 4; ++pass) {
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kMaxItems; ++q)
-      if (icell[q] >= 0 && ipass[q] == pass) nd[icell[q]] += iv[q];
-    for (int it = threadIdx.x + kMaxItems * kThreads; it < nitems; it += kThreads) {  // beyond the registers
-      int cell, ps;
-      T v;
-      locate(it, cell, ps, v);
-      if (cell >= 0 && ps == pass) nd[cell] += v;
-    }
-  }
-  ptx::cp_async_wait_all();
-  __syncthreads();
+  const int cs0 = blockIdx.y * kSeg, cs1 = min(g.C, cs0 + kSeg);
+  const int pr0 = band * g.TR, pr1 = min(g.PH, pr0 + g.TR);
+  const int r0 = pr0 * S, r1 = min(g.H, (pr1 - 1) * S + K);
+  // rows whose LRN top this band stores (halo rows belong to the next band)
+  const int own1 = band + 1 == g.bands ? g.H : min(g.H, pr1 * S);
+  const int npix = (r1 - r0) * g.W, tsz = g.rows_in * g.W;
+  const int HW = g.H * g.W, PHW = g.PH * g.PW;
   const T aN = alpha / T(SIZE);
-  for (int cl = 0; cl < ndc; ++cl) {  // channel c' = c0 - post + cl
-    const int c = c0 - post + cl;
-    const bool in = c >= 0 && c < g.C;
-    const bool own = c >= c0 && c < c1;
-    for (int p = threadIdx.x; p < npix; p += kThreads) {
-      T t = T(0);
-      if (in) {
+  const int p = threadIdx.x;
+  const bool active = p < npix;
+  const int h = r0 + (active ? p / g.W : 0);
+  const size_t base = size_t(img) * g.C * HW + size_t(h) * g.W + (active ? p % g.W : 0);
+  const T* xp = x + base;
+  T* yp = ynorm + base;
+  const bool own = active && h < own1;
+  T xr[SIZE];  // x(c - pre .. c + post)
+#pragma unroll
+  for (int j = 0; j < SIZE; ++j) {
+    const int cc = cs0 + j - pre;
+    xr[j] = (active && cc >= 0 && cc < g.C) ? __ldg(xp + uint32_t(cc) * uint32_t(HW)) : T(0);
+  }
+  auto load_step = [&](int c0, T (&nx)[kG]) {
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const int cin = c0 + u + post + 1;
+      nx[u] = (active && c0 + u < cs1 && cin < g.C) ? __ldg(xp + uint32_t(cin) * uint32_t(HW)) : T(0);
+    }
+  };
+  T nxt[kG];
+  load_step(cs0, nxt);
+  const int prows = pr1 - pr0;
+  for (int c0 = cs0, step = 0; c0 < cs1; c0 += kG, ++step) {
+    T cur[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) cur[u] = nxt[u];
+    if (c0 + kG < cs1) load_step(c0 + kG, nxt);
+    T* buf = tile + (step & 1) * kG * tsz;
+    if (active) {
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int c = c0 + u;
+        if (c >= cs1) break;
         T sum = T(0);
 #pragma unroll
-        for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xs[(cl + j) * npix + p]);
+        for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xr[j]);
+        const T sc = lrn::scale(sum, aN, k);
+        const T yv = lrn::top(xr[pre], lrn::neg_pow(sc, beta));
+        buf[u * tsz + p] = yv;
+        if (own) yp[uint32_t(c) * uint32_t(HW)] = yv;
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
+        xr[SIZE - 1] = cur[u];
+      }
+    }
+    __syncthreads();
+    const int items = min(kG, cs1 - c0) * prows * g.PW;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int u = it / (prows * g.PW);
+      const int rem = it - u * (prows * g.PW);
+      const int prl = rem / g.PW, pw = rem - prl * g.PW;
+      const int hs = (pr0 + prl) * S, ws = pw * S;
+      const T* t = buf + u * tsz + (hs - r0) * g.W;
+      T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
+      int arg = -1;
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          if (hs + a < g.H && ws + b < g.W) {
+            const T v = t[a * g.W + ws + b];
+            if (v > best) { best = v; arg = (hs + a) * g.W + ws + b; }
+          }
+        }
+      const uint32_t o = (uint32_t(img) * g.C + c0 + u) * uint32_t(PHW) + uint32_t((pr0 + prl) * g.PW + pw);
+      ypool[o] = relu ? (best > T(0) ? best : T(0)) : best;
+      mask[o] = arg;
+    }
+    // the next step writes the other buffer; the one after waits at its barrier
+  }
+}
+
+// Backward: one thread per (pixel, channel segment).  32-bit element offsets (the
+// tensors are < 2^31 elements: fusable()); the pixel's <= R x R window offsets into
+// the pooled plane are computed once.
+template <typename T, int SIZE, int K, int S>
+__global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
+                                                       const int* __restrict__ mask, T* __restrict__ dx,
+                                                       LrnPoolGeom g, T alpha, T beta, T k, bool gate_x) {
+  constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
+  constexpr int R = (K + S - 1) / S;
+  const uint32_t HW = uint32_t(g.H * g.W), PHW = uint32_t(g.PH * g.PW);
+  const uint32_t pixels = uint32_t(g.N) * HW;
+  const uint32_t work = pixels * uint32_t(g.segs);
+  const T aN = alpha / T(SIZE);
+  const T coef = T(2) * alpha * beta / T(SIZE);
+  for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < work; wi += gridDim.x * blockDim.x) {
+    // consecutive threads: consecutive pixels of one segment (coalesced)
+    const uint32_t seg = wi / pixels;
+    const uint32_t pix = wi - seg * pixels;
+    const int cs0 = int(seg) * kSeg, cs1 = min(g.C, cs0 + kSeg);
+    const uint32_t img = pix / HW, hw = pix - img * HW;
+    const int h = int(hw) / g.W, w = int(hw) - h * g.W;
+    const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
+    const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
+    const T* xp = x + size_t(img) * g.C * HW + hw;
+    T* dxp = dx + size_t(img) * g.C * HW + hw;
+    const int* mp = mask + size_t(img) * g.C * PHW;
+    const T* dp = pdy + size_t(img) * g.C * PHW;
+    uint32_t woff[R][R];
+    bool wok[R][R];
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        wok[a][b] = phs + a < phe && pws + b < pwe;
+        woff[a][b] = uint32_t((phs + a) * g.PW + pws + b);
+      }
+    auto xat = [&](int cc) { return (cc >= 0 && cc < g.C) ? __ldg(xp + uint32_t(cc) * HW) : T(0); };
+    // the LRN top diff of channel cc at this pixel: max_pool_bwd_k's gather, in its order
+    auto gather = [&](int cc, int (&m)[R][R], T (&v)[R][R]) {
+      const uint32_t co = uint32_t(cc) * PHW;
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          const bool ok = cc < g.C && wok[a][b];
+          m[a][b] = ok ? __ldg(mp + co + woff[a][b]) : -1;
+          v[a][b] = ok ? __ldg(dp + co + woff[a][b]) : T(0);
+        }
+    };
+    auto ndy_of = [&](const int (&m)[R][R], const T (&v)[R][R]) {
+      T sdy = T(0);
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int b = 0; b < R; ++b)
+          if (m[a][b] == int(hw)) sdy += v[a][b];
+      return sdy;
+    };
+    // rings over channels c - post .. c + pre: t = dy*y/scale, dy, scale^-beta (lrn_bwd_ring;
+    // scale^-beta is the same function of the same scale, computed once per channel).
+    // Ahead of the step for channel c they hold c-1-post .. c-1+pre (index 0 shifts out first).
+    T tr[SIZE], dyr[SIZE], npr[SIZE];
+#pragma unroll
+    for (int j = 0; j < SIZE; ++j) { dyr[j] = T(0); npr[j] = T(1); tr[j] = T(0); }
+#pragma unroll
+    for (int j = 1; j < SIZE; ++j) {
+      const int cc = cs0 + j - 1 - post;
+      if (cc >= 0 && cc < g.C) {
+        T sum = T(0);
+#pragma unroll
+        for (int q = 0; q < SIZE; ++q) sum = lrn::sq_acc(sum, xat(cc - pre + q));
         const T sc = lrn::scale(sum, aN, k);
         const T np = lrn::neg_pow(sc, beta);
-        const T d = nd[cl * npix + p];
-        t = lrn::term(d, lrn::top(xs[(cl + pre) * npix + p], np), sc);
-        if (own) nd[cl * npix + p] = lrn::mul_(d, np);
+        const T yv = lrn::top(xat(cc), np);
+        int m[R][R];
+        T v[R][R];
+        gather(cc, m, v);
+        const T d = ndy_of(m, v);
+        dyr[j] = d;
+        npr[j] = np;
+        tr[j] = lrn::term(d, yv, sc);
       }
-      ts[cl * npix + p] = t;
     }
-  }
-  __syncthreads();
-  const T coef = T(2) * alpha * beta / T(SIZE);
-  T* db = dx + size_t(img) * g.C * HW + uint32_t(r0 * g.W);
-  for (int cl = 0; cl < nc; ++cl) {
-    T* dst = db + uint32_t(c0 + cl) * HW;
-    for (int p = threadIdx.x; p < npix; p += kThreads) {
-      T acc = T(0);
+    // x ring: x(c .. c + SIZE - 1), the window of the entering channel c + pre
+    T xr[SIZE];
 #pragma unroll
-      for (int j = 0; j < SIZE; ++j) acc = lrn::add_(acc, ts[(cl + j) * npix + p]);
-      const T xc = xs[(cl + SIZE - 1) * npix + p];
-      const T gv = lrn::sub_(nd[(cl + post) * npix + p], lrn::mul_(lrn::mul_(coef, xc), acc));
-      dst[p] = (!gate_x || xc > T(0)) ? gv : T(0);
+    for (int j = 0; j < SIZE - 1; ++j) xr[j] = xat(cs0 + j);
+    xr[SIZE - 1] = T(0);
+    auto load_step = [&](int c0, T (&nx)[kG], int (&nm)[kG][R][R], T (&nv)[kG][R][R]) {
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        nx[u] = c0 + u < cs1 ? xat(c0 + u + SIZE - 1) : T(0);
+        gather(c0 + u < cs1 ? c0 + u + pre : g.C, nm[u], nv[u]);
+      }
+    };
+    T nx[kG];
+    int nm[kG][R][R];
+    T nv[kG][R][R];
+    load_step(cs0, nx, nm, nv);
+    for (int c0 = cs0; c0 < cs1; c0 += kG) {
+      T cx[kG];
+      int cm[kG][R][R];
+      T cv[kG][R][R];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        cx[u] = nx[u];
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int b = 0; b < R; ++b) { cm[u][a][b] = nm[u][a][b]; cv[u][a][b] = nv[u][a][b]; }
+      }
+      if (c0 + kG < cs1) load_step(c0 + kG, nx, nm, nv);  // in flight during this step
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int c = c0 + u;
+        if (c >= cs1) break;
+        xr[SIZE - 1] = cx[u];  // x(c .. c + SIZE - 1)
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; npr[j] = npr[j + 1]; }
+        if (c + pre < g.C) {
+          T sum = T(0);
+#pragma unroll
+          for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xr[j]);
+          const T sc = lrn::scale(sum, aN, k);
+          const T np = lrn::neg_pow(sc, beta);
+          const T yv = lrn::top(xr[pre], np);
+          const T d = ndy_of(cm[u], cv[u]);
+          dyr[SIZE - 1] = d;
+          npr[SIZE - 1] = np;
+          tr[SIZE - 1] = lrn::term(d, yv, sc);
+        } else {
+          dyr[SIZE - 1] = T(0); npr[SIZE - 1] = T(1); tr[SIZE - 1] = T(0);
+        }
+        T acc = T(0);
+#pragma unroll
+        for (int j = 0; j < SIZE; ++j) acc = lrn::add_(acc, tr[j]);
+        const T xc = xr[0];
+        const T gval = lrn::grad(dyr[post], npr[post], coef, xc, acc);
+        dxp[uint32_t(c) * HW] = (!gate_x || xc > T(0)) ? gval : T(0);
+#pragma unroll
+        for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
+      }
     }
   }
 }
 
-// owned pixel rows of the widest band
-int bwd_rows(const LrnPoolGeom& g, int S) { return std::max(g.TRP * S, g.H - (g.bands - 1) * g.TRP * S); }
-
-size_t fwd_smem_bytes(const LrnPoolGeom& g, int size, int K, int S, size_t es) {
-  return size_t(2 * kCB + size - 1) * size_t((g.TRP - 1) * S + K) * g.W * es;
-}
-size_t bwd_smem_bytes(const LrnPoolGeom& g, int size, int S, size_t es) {
-  return size_t(3 * kCB + 4 * (size - 1)) * size_t(bwd_rows(g, S)) * g.W * es;
-}
-
-// Bands of TRP pooled rows: as many as keep both tiles within ~100 KB (two blocks per
-// SM), at most ~512 owned pixels; TRP = 0 when not even one pooled row fits.
-LrnPoolGeom lrn_pool_geom(const PoolDescSlot& d, int size, size_t es) {
+LrnPoolGeom lrn_pool_geom(const PoolDescSlot& d, int smem_cap_elems) {
   const auto& p = d.p;
-  LrnPoolGeom g{p.n, p.c, p.h, p.w, d.PH, d.PW, 1, 0, (p.c + kCB - 1) / kCB};
+  LrnPoolGeom g{p.n, p.c, p.h, p.w, d.PH, d.PW, 1, 0, 0, (p.c + kSeg - 1) / kSeg};
   const int K = p.kernel_h, S = p.stride_h;
-  for (int trp = std::max(1, std::min(d.PH, 512 / std::max(1, S * p.w))); trp >= 1; --trp) {
-    g.TRP = trp;
-    g.bands = (d.PH + trp - 1) / trp;
-    if (bwd_smem_bytes(g, size, S, es) <= 100 * 1024 && fwd_smem_bytes(g, size, K, S, es) <= 100 * 1024) return g;
-  }
-  g.TRP = 0;
+  // band height: about 512 input pixels per block
+  int tr = std::max(1, ((512 / std::max(1, p.w)) - K) / S + 1);
+  tr = std::min(tr, d.PH);
+  while (tr > 1 && ((tr - 1) * S + K) * p.w > std::min(1024, smem_cap_elems)) --tr;
+  g.TR = tr;
+  g.rows_in = (tr - 1) * S + K;
+  g.bands = (d.PH + tr - 1) / tr;
   return g;
 }
 
-bool fusable(const PoolDescSlot& d, int size, size_t es) {
+bool fusable(const PoolDescSlot& d, int size) {
   const auto& p = d.p;
   const bool window = p.kernel_h == p.kernel_w && p.stride_h == p.stride_w &&
                       ((p.kernel_h == 3 && p.stride_h == 2) || (p.kernel_h == 2 && p.stride_h == 2));
   return p.method == CDNN_POOL_MAX && !p.global_pooling && p.pad_h == 0 && p.pad_w == 0 && window &&
-         (size == 3 || size == 5) && uint64_t(p.n) * p.c * p.h * p.w < (1ull << 31) &&
-         lrn_pool_geom(d, size, es).TRP > 0;
+         (size == 3 || size == 5) && p.kernel_h * p.w <= 1024 &&
+         uint64_t(p.n) * p.c * p.h * p.w < (1ull << 31) &&
+         uint64_t(p.n) * p.h * p.w * ((p.c + kSeg - 1) / kSeg) < (1ull << 31);
 }
 
 template <typename T, int SIZE, int K, int S>
 void launch_fwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, T* yn, T* yp, int* m, double alpha,
                 double beta, double k, bool relu) {
-  const LrnPoolGeom g = lrn_pool_geom(d, SIZE, sizeof(T));
-  const size_t smem = fwd_smem_bytes(g, SIZE, K, S, sizeof(T));
-  auto kern = lrn_maxpool_fwd<T, SIZE, K, S>;
-  CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  kern<<<dim3(g.bands, g.segs, g.N), kThreads, smem, st>>>(x, yn, yp, m, g, T(alpha), T(beta), T(k), relu);
+  const LrnPoolGeom g = lrn_pool_geom(d, 1024);
+  const int threads = ((g.rows_in * g.W + 31) / 32) * 32;
+  const size_t smem = size_t(2) * kG * g.rows_in * g.W * sizeof(T);
+  lrn_maxpool_fwd<T, SIZE, K, S><<<dim3(g.bands, g.segs, g.N), threads, smem, st>>>(x, yn, yp, m, g, T(alpha),
+                                                                                    T(beta), T(k), relu);
   check_launch("lrn_maxpool_fwd");
   count_launch(c);
 }
@@ -285,11 +316,10 @@ void launch_fwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, T* y
 template <typename T, int SIZE, int K, int S>
 void launch_bwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, const T* pdy, const int* m, T* dx,
                 double alpha, double beta, double k, bool gate_x) {
-  const LrnPoolGeom g = lrn_pool_geom(d, SIZE, sizeof(T));
-  const size_t smem = bwd_smem_bytes(g, SIZE, S, sizeof(T));
-  auto kern = lrn_maxpool_bwd<T, SIZE, K, S>;
-  CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  kern<<<dim3(g.bands, g.segs, g.N), kThreads, smem, st>>>(x, pdy, m, dx, g, T(alpha), T(beta), T(k), gate_x);
+  const LrnPoolGeom g = lrn_pool_geom(d, 1024);
+  const int64_t work = int64_t(g.N) * g.H * g.W * g.segs;
+  lrn_maxpool_bwd<T, SIZE, K, S><<<grid_for(work, 256), 256, 0, st>>>(x, pdy, m, dx, g, T(alpha), T(beta), T(k),
+                                                                       gate_x);
   check_launch("lrn_maxpool_bwd");
   count_launch(c);
 }
@@ -313,8 +343,7 @@ extern "C" {
 int cdnn_lrn_pool_supported(cdnn_ctx ctx, cdnn_handle pool_desc_h, int local_size, int* out) {
   return guarded([&] {
     Ctx* c = need_ctx(ctx);
-    // the float path decides for the net; the double tiles are checked at launch
-    *out = fusable(pool_desc(c, pool_desc_h), local_size, sizeof(float)) ? 1 : 0;
+    *out = fusable(pool_desc(c, pool_desc_h), local_size) ? 1 : 0;
   });
 }
 
@@ -324,9 +353,8 @@ int cdnn_lrn_pool_forward(cdnn_ctx ctx, cdnn_handle pool_desc_h, cdnn_handle x, 
   return guarded([&] {
     Ctx* c = need_ctx(ctx);
     const PoolDescSlot d = pool_desc(c, pool_desc_h);
+    if (!fusable(d, local_size)) fail(CDNN_INVALID_ARGUMENT, "lrn_pool: unsupported LRN / pooling combination");
     BufferSlot& X = buffer(c, x, "lrn_pool x");
-    if (!fusable(d, local_size, dtype_size(X.dtype)))
-      fail(CDNN_INVALID_ARGUMENT, "lrn_pool: unsupported LRN / pooling combination");
     BufferSlot& YN = buffer(c, lrn_top, "lrn_pool lrn top");
     BufferSlot& YP = buffer(c, pool_top, "lrn_pool pool top");
     BufferSlot& M = buffer(c, mask, "lrn_pool mask");
@@ -363,10 +391,9 @@ int cdnn_lrn_pool_backward(cdnn_ctx ctx, cdnn_handle pool_desc_h, cdnn_handle x,
   return guarded([&] {
     Ctx* c = need_ctx(ctx);
     const PoolDescSlot d = pool_desc(c, pool_desc_h);
+    if (!fusable(d, local_size)) fail(CDNN_INVALID_ARGUMENT, "lrn_pool: unsupported LRN / pooling combination");
     if (gate && gate != x) fail(CDNN_INVALID_ARGUMENT, "lrn_pool backward: the ReLU gate must be the LRN bottom x");
     BufferSlot& X = buffer(c, x, "lrn_pool_bwd x");
-    if (!fusable(d, local_size, dtype_size(X.dtype)))
-      fail(CDNN_INVALID_ARGUMENT, "lrn_pool: unsupported LRN / pooling combination");
     BufferSlot& DY = buffer(c, pool_dy, "lrn_pool_bwd pool dy");
     BufferSlot& M = buffer(c, mask, "lrn_pool_bwd mask");
     BufferSlot& DX = buffer(c, dx, "lrn_pool_bwd dx");
