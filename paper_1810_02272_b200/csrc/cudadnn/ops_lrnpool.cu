@@ -30,9 +30,8 @@
 namespace cdnn {
 namespace {
 
-constexpr int kG = 4;     // forward: channels per step (loads in flight; one block barrier per step)
-constexpr int kSeg = 30;  // channels per thread / block segment (segments run in parallel); a
-                          // multiple of the backward's group of SIZE (3 or 5) channels
+constexpr int kG = 4;     // channels per step (loads in flight; one block barrier per step)
+constexpr int kSeg = 32;  // channels per thread / block segment (segments run in parallel)
 
 struct LrnPoolGeom {
   int N, C, H, W, PH, PW;
@@ -136,7 +135,7 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
 // tensors are < 2^31 elements: fusable()); the pixel's <= R x R window offsets into
 // the pooled plane are computed once.
 template <typename T, int SIZE, int K, int S>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
+__global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
                                                        const int* __restrict__ mask, T* __restrict__ dx,
                                                        LrnPoolGeom g, T alpha, T beta, T k, bool gate_x) {
   constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
@@ -220,21 +219,32 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) lrn_maxpool_bwd(c
 #pragma unroll
     for (int j = 0; j < SIZE - 1; ++j) xr[j] = xat(cs0 + j);
     xr[SIZE - 1] = T(0);
-    // Groups of G = SIZE channels: after SIZE shifts every ring slot holds a value
-    // produced inside the group, so the unrolled group needs no register moves for the
-    // rings; two load buffers alternate (ping-pong), the next group's loads in flight
-    // while this group computes.
-    constexpr int G = SIZE;
-    auto load_step = [&](int c0, T (&nx)[G], int (&nm)[G][R][R], T (&nv)[G][R][R]) {
+    auto load_step = [&](int c0, T (&nx)[kG], int (&nm)[kG][R][R], T (&nv)[kG][R][R]) {
 #pragma unroll
-      for (int u = 0; u < G; ++u) {
+      for (int u = 0; u < kG; ++u) {
         nx[u] = c0 + u < cs1 ? xat(c0 + u + SIZE - 1) : T(0);
         gather(c0 + u < cs1 ? c0 + u + pre : g.C, nm[u], nv[u]);
       }
     };
-    auto run_group = [&](int c0, const T (&cx)[G], const int (&cm)[G][R][R], const T (&cv)[G][R][R]) {
+    T nx[kG];
+    int nm[kG][R][R];
+    T nv[kG][R][R];
+    load_step(cs0, nx, nm, nv);
+    for (int c0 = cs0; c0 < cs1; c0 += kG) {
+      T cx[kG];
+      int cm[kG][R][R];
+      T cv[kG][R][R];
 #pragma unroll
-      for (int u = 0; u < G; ++u) {
+      for (int u = 0; u < kG; ++u) {
+        cx[u] = nx[u];
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int b = 0; b < R; ++b) { cm[u][a][b] = nm[u][a][b]; cv[u][a][b] = nv[u][a][b]; }
+      }
+      if (c0 + kG < cs1) load_step(c0 + kG, nx, nm, nv);  // in flight during this step
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
         const int c = c0 + u;
         if (c >= cs1) break;
         xr[SIZE - 1] = cx[u];  // x(c .. c + SIZE - 1)
@@ -263,17 +273,6 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) lrn_maxpool_bwd(c
 #pragma unroll
         for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
       }
-    };
-    T ax[G], bx[G];
-    int am[G][R][R], bm[G][R][R];
-    T av[G][R][R], bv[G][R][R];
-    load_step(cs0, ax, am, av);
-    for (int c0 = cs0; c0 < cs1; c0 += 2 * G) {
-      if (c0 + G < cs1) load_step(c0 + G, bx, bm, bv);
-      run_group(c0, ax, am, av);
-      if (c0 + G >= cs1) break;
-      if (c0 + 2 * G < cs1) load_step(c0 + 2 * G, ax, am, av);
-      run_group(c0 + G, bx, bm, bv);
     }
   }
 }
