@@ -654,16 +654,16 @@ def run_pg_b200(args) -> None:
         pins.append(px)
     prob = cudadnn.PinnedBuffer((BATCH, 2), npd)
 
-    def step(i, feed):
-        if feed:
-            net.set_batch_ptr(pins[i % nb].ptr, None)
+    def step(i, readback):
+        # the MemoryData feed is consumed by every forward (reference FIFO semantics): the
+        # episode's states are staged every step (pinned H2D) in both timings
+        net.set_batch_ptr(pins[i % nb].ptr, None)
         polegrad._check(net.lib, net.lib.pg_net_forward(net.ptr))
         net.pg_backward(act[i % nb], ret[i % nb])
         solver.apply()
-        if feed:  # the policy's probabilities back to the host (action sampling)
+        if readback:  # the policy's probabilities back to the host (action sampling)
             polegrad._check(net.lib, net.lib.pg_blob_get(net.ptr, b"prob", 0, C.c_void_p(prob.ptr)))
 
-    net.set_batch_ptr(pins[0].ptr, None)
     l0 = cx.launches()
     step(0, False)
     net.sync()
