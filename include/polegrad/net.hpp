@@ -106,6 +106,11 @@ class Net {
   // per-step accumulate_step (trainer.cpp:204-216).  One H2D of 2n values.
   void pg_backward(const std::string& logit_blob, const std::string& prob_blob, std::span<const real> actions,
                    std::span<const real> returns, bool sigmoid);
+  // The same with the n actions / returns read asynchronously on the stream from host
+  // memory that stays valid (page-locked for a CUDA-graph capture): no host
+  // synchronisation, so a whole episode update can be captured and replayed.
+  void pg_backward_async(const std::string& logit_blob, const std::string& prob_blob, const real* actions,
+                         const real* returns, std::size_t n, bool sigmoid);
   // Zero every parameter gradient on the device (one fill over the grad arena).
   void zero_param_diffs();
   // Stream of the parameter-gradient halves of the two-stream backward (0 until used).

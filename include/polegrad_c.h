@@ -111,6 +111,14 @@ PG_API int pg_rng_free(pg_rng* rng);
 PG_API int pg_step_capture(pg_net* net, pg_solver* s, const void* data, const void* labels, void* loss_out,
                            uint64_t* graph);
 PG_API int pg_step_replay(pg_net* net, uint64_t graph);
+/* One captured policy-gradient update of an episode batch (configs[2]): H2D of the
+ * states into the feed, forward, the modulated log-prob gradients of n steps at the
+ * logits (Net::pg_backward_async), backward_from, the solver update, and the D2H of the
+ * probabilities blob into prob_out.  states / actions / returns / prob_out must be
+ * page-locked and stay valid; write the next episode into them, then replay. */
+PG_API int pg_pg_step_capture(pg_net* net, pg_solver* s, const void* states, const void* actions,
+                              const void* returns, uint64_t n, const char* logit_blob, const char* prob_blob,
+                              int sigmoid, void* prob_out, uint64_t* graph);
 /* data == NULL: no feed copy, the batch already resident in the data blob is reused */
 /* one eager forward+backward with events between layers (per-layer ms, layer order) */
 PG_API int pg_net_profile(pg_net* net, float* fwd_ms, float* bwd_ms, int cap);

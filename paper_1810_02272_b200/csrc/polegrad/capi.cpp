@@ -345,6 +345,39 @@ int pg_step_capture(pg_net* n, pg_solver* s, const void* data, const void* label
   });
 }
 
+int pg_pg_step_capture(pg_net* n, pg_solver* s, const void* states, const void* actions, const void* returns,
+                       uint64_t count, const char* logit_blob, const char* prob_blob, int sigmoid, void* prob_out,
+                       uint64_t* graph) {
+  return run([&] {
+    polegrad::Net& net = net_of(n);
+    polegrad::Registry& reg = *net.registry();
+    if (!states || !actions || !returns) throw polegrad::InvalidArgument("pg step capture: null input buffer");
+    // one eager update first: lazily allocated buffers must exist before the capture
+    reg.synchronize();
+    cdnn_ok(cdnn_graph_begin(reg.context(), reg.stream()), "pg step capture");
+    try {
+      net.set_batch(static_cast<const real*>(states), nullptr);
+      net.forward();
+      net.pg_backward_async(logit_blob, prob_blob, static_cast<const real*>(actions),
+                            static_cast<const real*>(returns), count, sigmoid != 0);
+      s->solver->apply_update(net);
+      if (prob_out) {
+        polegrad::Blob& prob = net.blob(prob_blob);
+        cdnn_ok(cdnn_read_async(reg.context(), prob.gpu_data(), 0, prob_out, prob.count(), reg.stream()),
+                "pg step capture");
+      }
+    } catch (...) {
+      cdnn_handle dead = 0;
+      cdnn_graph_end(reg.context(), reg.stream(), &dead);
+      if (dead) cdnn_graph_free(reg.context(), dead);
+      throw;
+    }
+    cdnn_handle g = 0;
+    cdnn_ok(cdnn_graph_end(reg.context(), reg.stream(), &g), "pg step capture");
+    *graph = g;
+  });
+}
+
 int pg_net_profile(pg_net* n, float* fwd_ms, float* bwd_ms, int cap) {
   return run([&] {
     std::vector<float> f, b;

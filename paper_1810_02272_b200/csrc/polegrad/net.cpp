@@ -449,6 +449,31 @@ void Net::set_dropout_counters(const std::vector<double>& values) {
   if (k != values.size()) throw InvalidArgument("set_dropout_counters: too many values");
 }
 
+void Net::pg_backward_async(const std::string& logit_blob, const std::string& prob_blob, const real* actions,
+                            const real* returns, std::size_t n, bool sigmoid) {
+  Blob& logit = blob(logit_blob);
+  Blob& prob = blob(prob_blob);
+  const int rows = logit.shape().n();
+  const int classes = int(logit.count() / std::size_t(rows));
+  if (prob.count() != logit.count()) throw InvalidArgument("pg_backward: prob and logit blobs differ in size");
+  if (n > std::size_t(rows))
+    throw InvalidArgument("pg_backward: " + std::to_string(n) + " steps exceed the batch of " + std::to_string(rows));
+  Registry& reg = *registry_;
+  if (!pg_actions_) {
+    pg_actions_ = reg.alloc_buffer(std::size_t(rows));
+    pg_returns_ = reg.alloc_buffer(std::size_t(rows));
+  }
+  if (n) {
+    cdnn_ok(cdnn_write_async(reg.context(), reg.in(pg_actions_), 0, actions, n, reg.stream()), "pg_backward");
+    cdnn_ok(cdnn_write_async(reg.context(), reg.in(pg_returns_), 0, returns, n, reg.stream()), "pg_backward");
+  }
+  // rows >= n get a zero diff (cdnn_pg_diff), so the buffers need no padding
+  cdnn_ok(cdnn_pg_diff(reg.context(), prob.gpu_data(), reg.in(pg_actions_), reg.in(pg_returns_),
+                       logit.overwrite_gpu_diff(), rows, int(n), classes, sigmoid ? 1 : 0, reg.stream()),
+          "pg_backward");
+  backward_from(logit_blob);
+}
+
 void Net::zero_param_diffs() {
   if (!param_total_) return;
   Registry& reg = *registry_;

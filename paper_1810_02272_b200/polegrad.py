@@ -36,7 +36,7 @@ EXPORTS = [
     "pg_solver_restore", "pg_solver_iterations", "pg_feed_ring_create", "pg_feed_ring_free", "pg_feed_ring_push", "pg_feed_ring_push_pinned",
     "pg_feed_ring_pop_loss", "pg_net_pg_backward", "pg_feed_ring_push_sampled", "pg_imagedb_load",
     "pg_imagedb_free", "pg_imagedb_size", "pg_imagedb_set_boost", "pg_imagedb_sample", "pg_rng_create",
-    "pg_rng_free", "pg_parallel_create_host", "pg_parallel_info",
+    "pg_rng_free", "pg_parallel_create_host", "pg_parallel_info", "pg_pg_step_capture",
 ]
 
 # int transport(void* user, int op, void* host, uint64_t offset, uint64_t n)
@@ -78,6 +78,7 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_feed_ring_push": ([vp, vp, u64, vp, u64], i),
             "pg_feed_ring_push_pinned": ([vp, vp, u64, vp, u64], i), "pg_feed_ring_pop_loss": ([vp, C.POINTER(d)], i),
             "pg_step_capture": ([vp, vp, vp, vp, vp, C.POINTER(u64)], i), "pg_step_replay": ([vp, u64], i),
+            "pg_pg_step_capture": ([vp, vp, vp, vp, vp, u64, cp, cp, i, vp, C.POINTER(u64)], i),
             "pg_graph_free": ([vp, u64], i), "pg_parallel_unique_id": ([cp], i),
             "pg_net_profile": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
             "pg_parallel_create": ([vp, i, i, cp, u64, C.POINTER(vp)], i), "pg_parallel_free": ([vp], i),
@@ -341,6 +342,29 @@ class StepGraph:
         _check(net.lib, net.lib.pg_step_capture(net.ptr, solver.ptr, C.c_void_p(data_ptr),
                                                 C.c_void_p(labels_ptr) if labels_ptr else None,
                                                 C.c_void_p(loss_ptr), C.byref(g)))
+        self.graph = g.value
+
+    def replay(self) -> None:
+        _check(self.net.lib, self.net.lib.pg_step_replay(self.net.ptr, self.graph))
+
+
+class PGStepGraph:
+    """One captured policy-gradient update of an episode batch (pg_pg_step_capture):
+    states -> forward -> device-side modulated log-prob gradients of `n` steps ->
+    backward_from(logits) -> update -> probabilities to `prob`.  The buffers are
+    cudadnn.PinnedBuffer of the net's real type; write the next episode into them and
+    replay().  Capture after at least one eager update (lazy device buffers)."""
+
+    def __init__(self, net: Net, solver: "Solver", states, actions, returns, n: int, prob=None,
+                 logit: str = "logits", prob_blob: str = "prob", sigmoid: bool = False):
+        self.net = net
+        self._keep = (solver, states, actions, returns, prob)
+        g = C.c_uint64()
+        _check(net.lib, net.lib.pg_pg_step_capture(net.ptr, solver.ptr, C.c_void_p(states.ptr),
+                                                   C.c_void_p(actions.ptr), C.c_void_p(returns.ptr), n,
+                                                   logit.encode(), prob_blob.encode(), int(sigmoid),
+                                                   C.c_void_p(prob.ptr) if prob is not None else None,
+                                                   C.byref(g)))
         self.graph = g.value
 
     def replay(self) -> None:

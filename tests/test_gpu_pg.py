@@ -57,3 +57,47 @@ def test_batched_episode_gradient_matches_per_step_reference(dtype, steps):
     for i, (name, _) in enumerate(net.param_info()):
         err = rel_l2(net.param(i, diff=True), orc.param(i, diff=True))
         assert err <= TOL[dtype], (name, err)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_captured_pg_update_equals_eager(dtype):
+    """The captured episode update (PGStepGraph: states / actions / returns H2D, forward,
+    device diffs, backward_from, RMSProp, probabilities D2H) replayed on fresh episodes
+    trains exactly like the eager Net.pg_backward path, bit for bit."""
+    from paper_1810_02272_b200 import cudadnn
+    rng = np.random.default_rng(5)
+    n, batch = 200, 256
+    np_t = np.float64 if dtype == "f64" else np.float32
+    episodes = [(rng.uniform(-1, 1, (batch, 4, 1, 1)), np.floor(rng.uniform(0, 1, batch) * 2),
+                 rng.standard_normal(batch)) for _ in range(4)]
+    text = polegrad.load_model("pg_mlp", batch)
+    kw = dict(method="rmsprop", lr=1e-3, rms_decay=0.99, epsilon=1e-8)
+    a = polegrad.Net(text, 1, dtype)
+    sa = polegrad.Solver(a, **kw)
+    b = polegrad.Net(text, 1, dtype)
+    sb = polegrad.Solver(b, **kw)
+    probs_a = []
+    for s, act, ret in episodes:
+        a.set_batch(s)
+        a.forward()
+        a.pg_backward(act[:n], ret[:n])
+        sa.apply()
+        probs_a.append(a.blob("prob").copy())
+    # b: one eager update on the first episode (lazy buffers), then the captured graph
+    s, act, ret = episodes[0]
+    b.set_batch(s)
+    b.forward()
+    b.pg_backward(act[:n], ret[:n])
+    sb.apply()
+    ps, pa, pr = (cudadnn.PinnedBuffer(shape, np_t) for shape in ((batch, 4, 1, 1), (batch,), (batch,)))
+    pp = cudadnn.PinnedBuffer((batch, 2), np_t)
+    g = polegrad.PGStepGraph(b, sb, ps, pa, pr, n, pp)  # the capture itself applies no update
+    for k, (s, act, ret) in enumerate(episodes[1:], start=1):
+        ps.array[...] = s
+        pa.array[...] = act
+        pr.array[...] = ret
+        g.replay()
+        b.sync()
+        assert np.array_equal(pp.array.reshape(probs_a[k].shape), probs_a[k].astype(np_t))
+    for i in range(len(a.param_info())):
+        assert np.array_equal(a.param(i), b.param(i)), a.param_info()[i]
