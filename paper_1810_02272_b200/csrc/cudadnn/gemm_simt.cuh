@@ -115,6 +115,31 @@ __global__ void __launch_bounds__(256) dot_warp_kernel(const VA va, const VB vb,
   if (lane == 0) epi.store(m, n, s, 0);
 }
 
+// One block (8 warps) per output (m, n) for very few outputs with long K (the PG-MLP /
+// LeNet / CIFAR dW at batch 1024 rows): threads stride k, a fixed xor tree per warp, the
+// eight warp sums added in warp order by thread 0 (deterministic).
+template <typename T, class VA, class VB, class EPI>
+__global__ void __launch_bounds__(256) dot_block_kernel(const VA va, const VB vb, const EPI epi, int M, int N, int K) {
+  __shared__ T part[8];
+  const int o = blockIdx.x;
+  const int m = o % M, n = o / M;
+  const auto ra = va.row(m);
+  const auto rb = vb.row(n);
+  T s = T(0);
+#pragma unroll 4
+  for (int k = threadIdx.x; k < K; k += 256) s += va.at(ra, k) * vb.at(rb, k);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T t = part[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) t += part[w];
+    epi.store(m, n, t, 0);
+  }
+}
+
 template <typename T, int UNROLL, class VA, class VB, class EPI>
 __global__ void __launch_bounds__(256) dot_thread_kernel(const VA va, const VB vb, const EPI epi, int M, int N, int K) {
   const int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -91,6 +91,11 @@ static bool small_gemm(Ctx* c, cudaStream_t st, int M, int N, int K, const Dense
   const int64_t outs = int64_t(M) * N;
   // K in [64, 256): warp-per-output up to this many outputs (LeNet ip2 dW, 5000, measured faster per thread)
   constexpr int64_t warp_outs = 2048;
+  // very few outputs, long K (PG-MLP dW over 1024 rows: a warp per output was 9.5 us):
+  // a block per output
+  if (outs <= 2 * kNumSMs && K >= 512) {
+    simt::dot_block_kernel<T><<<int(outs), 256, 0, st>>>(va, vb, epi, M, N, K);
+  } else
   // few outputs: a warp per output (CIFAR ip2 dW 640 x K=100: 29 -> 5.5 us)
   if (outs <= 16384 && (K >= 256 || (K >= 64 && outs <= warp_outs))) {
     const int64_t threads = outs * 32;
@@ -182,6 +187,25 @@ __global__ void __launch_bounds__(256) colsum_accum_kernel(const T* __restrict__
   }
 }
 
+// Few columns, many rows (the PG-MLP's 10 / 2 bias columns over 1024 rows: the 32-column
+// kernel above walked 128 rows per thread, 13 us): a block per column, threads stride
+// the rows, fixed-shape tree in shared memory (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_accum_col_kernel(const T* __restrict__ dy, T* __restrict__ db, int rows,
+                                                               int cols) {
+  __shared__ T part[256];
+  const int j = blockIdx.x;
+  T s = T(0);
+  for (int r = threadIdx.x; r < rows; r += 256) s += dy[int64_t(r) * cols + j];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) db[j] += part[0];
+}
+
 }  // namespace cdnn
 
 using namespace cdnn;
@@ -270,8 +294,11 @@ int cdnn_ip_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle w, cdnn_handle dy,
         dense_gemm<T>(c, stream, k, o, rows, va, vb, epi);
       }
       if (DB) {  // db += column sums of dY (layers.cpp:157-163)
-        colsum_accum_kernel<T><<<(o + 31) / 32, 256, 0, stream_of(c, stream)>>>(
-            dyp, reinterpret_cast<T*>(DB->dev), rows, o);
+        if (o <= 64 && rows >= 512)
+          colsum_accum_col_kernel<T><<<o, 256, 0, stream_of(c, stream)>>>(dyp, reinterpret_cast<T*>(DB->dev), rows, o);
+        else
+          colsum_accum_kernel<T><<<(o + 31) / 32, 256, 0, stream_of(c, stream)>>>(
+              dyp, reinterpret_cast<T*>(DB->dev), rows, o);
         check_launch("colsum");
         count_launch(c);
       }

@@ -55,7 +55,7 @@ def test_tf32x3_reaches_fp32_accuracy(ctx):
 @pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("m,n,k", [(2, 1, 2), (64, 500, 800), (100, 64, 1024), (37, 19, 300), (256, 128, 96),
-                                   (1024, 2, 10), (300, 260, 4100)])
+                                   (1024, 2, 10), (300, 260, 4100), (2, 10, 1024), (10, 4, 2048)])
 def test_gemm(ctx, math, dtype, ta, tb, m, n, k):
     rng = np.random.default_rng(m * 7 + n * 3 + k)
     A = rng.uniform(-1, 1, (k, m) if ta else (m, k))
@@ -483,3 +483,24 @@ def test_lrn_pool_fused_bit_identical_to_unfused(ctx, dtype, n, c, h, w, size, k
     for hnd in (hx, hy, hs, hp, hm, hdy, hdn, hdx, fy, fp, fm, fdx):
         ctx.free(hnd)
     ctx.call("cdnn_desc_free", d)
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("rows,k,o", [(1024, 4, 10), (1024, 10, 2), (600, 33, 64), (100, 64, 10)])
+def test_ip_backward_small(ctx, dtype, rows, k, o):
+    """InnerProduct backward on the few-output shapes (PG-MLP batch 1024: block-per-output
+    dW and block-per-column bias sums): dW += dY^T X, db += colsum(dY), dX = dY W."""
+    rng = np.random.default_rng(rows + k + o)
+    dt = NP[dtype]
+    x, w, dy = (rng.uniform(-1, 1, s).astype(dt) for s in ((rows, k), (o, k), (rows, o)))
+    dw0, db0 = rng.uniform(-1, 1, (o, k)).astype(dt), rng.uniform(-1, 1, o).astype(dt)
+    hx, hw, hdy, hdw, hdb = (ctx.upload(a) for a in (x, w, dy, dw0, db0))
+    hdx = ctx.alloc(rows * k, dtype)
+    ctx.call("cdnn_ip_backward", hx, hw, hdy, hdw, hdb, hdx, rows, k, o, 0)
+    X, W, DY = (a.astype(np.float64) for a in (x, w, dy))
+    tol = 1e-5 if dtype == cd.F32 else 1e-12
+    assert rel_l2(ctx.read(hdw).reshape(o, k), dw0 + DY.T @ X) <= tol
+    assert rel_l2(ctx.read(hdb), db0 + DY.sum(0)) <= tol
+    assert rel_l2(ctx.read(hdx).reshape(rows, k), DY @ W) <= tol
+    for h in (hx, hw, hdy, hdw, hdb, hdx):
+        ctx.free(h)
