@@ -199,6 +199,12 @@ template <class V>
 struct is_tma { static constexpr bool value = false; };
 template <>
 struct is_tma<TmaView> { static constexpr bool value = true; };
+template <>
+struct is_tma<TmaSplitView> { static constexpr bool value = true; };
+template <class V>
+struct is_presplit { static constexpr bool value = false; };
+template <>
+struct is_presplit<TmaSplitView> { static constexpr bool value = true; };
 
 // 3xTF32 with a TMA-fed operand: TMA lands the raw fp32 tile (128B-swizzled,
 // K-major) in the hi buffer; the producer warps then round it to tf32 in place
@@ -221,12 +227,16 @@ __device__ __forceinline__ void split_in_place(uint32_t hi, uint32_t lo, int t) 
 template <int BN, bool SPLIT, class VA, class VB, class EPI>
 __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmA_lo, const __grid_constant__ CUtensorMap tmB_lo,
                    const VA va, const VB vb, const EPI epi, int M, int N, int K, int kt_per_split) {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
   constexpr bool kTmaA = is_tma<VA>::value;
   constexpr bool kTmaB = is_tma<VB>::value;
-  // 3xTF32 + TMA: TMA lands raw tiles (landed[]), the producers split them
-  constexpr bool kSplitTma = SPLIT && (kTmaA || kTmaB);
+  // pre-split operands (3xTF32): TMA brings the hi and lo copies, nothing to convert
+  constexpr bool kPreA = SPLIT && is_presplit<VA>::value;
+  constexpr bool kPreB = SPLIT && is_presplit<VB>::value;
+  // 3xTF32 + raw TMA tiles: TMA lands them (landed[]), the producers split them
+  constexpr bool kSplitTma = SPLIT && ((kTmaA && !kPreA) || (kTmaB && !kPreB));
   constexpr int STAGES = stages_for<BN, SPLIT>();
   constexpr uint32_t A_BYTES = BM * BK * 4;
   constexpr uint32_t B_BYTES = BN * BK * 4;
@@ -276,18 +286,43 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
     if (lane == 0) {
       if constexpr (kTmaA) ptx::tma_prefetch_desc(&tmA);
       if constexpr (kTmaB) ptx::tma_prefetch_desc(&tmB);
+      if constexpr (kPreA) ptx::tma_prefetch_desc(&tmA_lo);
+      if constexpr (kPreB) ptx::tma_prefetch_desc(&tmB_lo);
       int stage = 0;
       uint32_t phase = 0;
       for (int kt = 0; kt < nkt; ++kt) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         constexpr uint32_t bytes = (kTmaA ? A_BYTES : 0) + (kTmaB ? B_BYTES : 0);
         if constexpr (kSplitTma) {
-          // raw tiles -> landed[]; the producers split them and complete full[]
-          ptx::mbar_arrive_expect_tx(&landed[stage], bytes);
+          // raw tiles -> landed[]; the producers split them and complete full[]; pre-split
+          // operands' hi + lo land on full[] directly
+          constexpr uint32_t raw = (kTmaA && !kPreA ? A_BYTES : 0) + (kTmaB && !kPreB ? B_BYTES : 0);
+          constexpr uint32_t pre = (kPreA ? 2 * A_BYTES : 0) + (kPreB ? 2 * B_BYTES : 0);
+          ptx::mbar_arrive_expect_tx(&landed[stage], raw);
           const int kc = (kt_begin + kt) * BK;
-          if constexpr (kTmaA) ptx::tma_load_2d(a_hi(stage), &tmA, &landed[stage], kc, m0);
-          if constexpr (kTmaB) ptx::tma_load_2d(b_hi(stage), &tmB, &landed[stage], kc, n0);
-          ptx::mbar_arrive(&full[stage]);
+          if constexpr (kTmaA && !kPreA) ptx::tma_load_2d(a_hi(stage), &tmA, &landed[stage], kc, m0);
+          if constexpr (kTmaB && !kPreB) ptx::tma_load_2d(b_hi(stage), &tmB, &landed[stage], kc, n0);
+          if constexpr (pre > 0) {
+            ptx::mbar_arrive_expect_tx(&full[stage], pre);
+            if constexpr (kPreA) {
+              ptx::tma_load_2d(a_hi(stage), &tmA, &full[stage], kc, m0);
+              ptx::tma_load_2d(a_lo(stage), &tmA_lo, &full[stage], kc, m0);
+            }
+            if constexpr (kPreB) {
+              ptx::tma_load_2d(b_hi(stage), &tmB, &full[stage], kc, n0);
+              ptx::tma_load_2d(b_lo(stage), &tmB_lo, &full[stage], kc, n0);
+            }
+          } else {
+            ptx::mbar_arrive(&full[stage]);
+          }
+        } else if constexpr (kPreA || kPreB) {
+          constexpr uint32_t all = (kTmaA ? A_BYTES : 0) * (kPreA ? 2 : 1) + (kTmaB ? B_BYTES : 0) * (kPreB ? 2 : 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], all);
+          const int kc = (kt_begin + kt) * BK;
+          if constexpr (kTmaA) ptx::tma_load_2d(a_hi(stage), &tmA, &full[stage], kc, m0);
+          if constexpr (kPreA) ptx::tma_load_2d(a_lo(stage), &tmA_lo, &full[stage], kc, m0);
+          if constexpr (kTmaB) ptx::tma_load_2d(b_hi(stage), &tmB, &full[stage], kc, n0);
+          if constexpr (kPreB) ptx::tma_load_2d(b_lo(stage), &tmB_lo, &full[stage], kc, n0);
         } else if constexpr (bytes > 0) {
           ptx::mbar_arrive_expect_tx(&full[stage], bytes);
           const int kc = (kt_begin + kt) * BK;
@@ -344,8 +379,8 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
         gather_slab<BN, SPLIT>(vb, ptx::smem_u32(b_hi(stage)), ptx::smem_u32(b_lo(stage)), n0, kc, t);
       if constexpr (kSplitTma) {
         ptx::mbar_wait(&landed[stage], phase);
-        if constexpr (kTmaA) split_in_place<BM>(ptx::smem_u32(a_hi(stage)), ptx::smem_u32(a_lo(stage)), t);
-        if constexpr (kTmaB) split_in_place<BN>(ptx::smem_u32(b_hi(stage)), ptx::smem_u32(b_lo(stage)), t);
+        if constexpr (kTmaA && !kPreA) split_in_place<BM>(ptx::smem_u32(a_hi(stage)), ptx::smem_u32(a_lo(stage)), t);
+        if constexpr (kTmaB && !kPreB) split_in_place<BN>(ptx::smem_u32(b_hi(stage)), ptx::smem_u32(b_lo(stage)), t);
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();

@@ -24,6 +24,7 @@ struct TmaReq {
   const float* p = nullptr;
   int rows = 0, K = 0;
   int64_t ld = 0;
+  const float* p_lo = nullptr;  // TmaSplitView: the lo copy (same layout)
 };
 
 inline bool tma_eligible(const float* p, int rows, int K, int64_t ld, int box_rows) {
@@ -92,8 +93,8 @@ inline int grid_for(int64_t n, int threads) {
 
 template <int BN, bool SPLIT, class VA, class VB, class EPI>
 void launch_tc_kernel(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& ta,
-                      const CUtensorMap& tb, const VA& va, const VB& vb, const EPI& epi, int M,
-                      int N, int K, int kt_per_split) {
+                      const CUtensorMap& tb, const CUtensorMap& ta_lo, const CUtensorMap& tb_lo, const VA& va,
+                      const VB& vb, const EPI& epi, int M, int N, int K, int kt_per_split) {
   constexpr int smem = tc::smem_bytes<BN, SPLIT>();
   auto kern = tc::tc_gemm_kernel<BN, SPLIT, VA, VB, EPI>;
   static bool attr_set[16] = {};
@@ -101,7 +102,7 @@ void launch_tc_kernel(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& ta,
     CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set[c->device & 15] = true;
   }
-  kern<<<grid, tc::kThreads, smem, st>>>(ta, tb, va, vb, epi, M, N, K, kt_per_split);
+  kern<<<grid, tc::kThreads, smem, st>>>(ta, tb, ta_lo, tb_lo, va, vb, epi, M, N, K, kt_per_split);
   check_launch("tc_gemm_kernel");
   count_launch(c);
 }
@@ -109,18 +110,22 @@ void launch_tc_kernel(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& ta,
 template <int BN, bool SPLIT, class VA, class VB, class EPI>
 void run_tc_bn(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
                const VA& va, const VB& vb, const EPI& epi, const TmaReq& ra, const TmaReq& rb) {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tal, tbl;
   std::memset(&ta, 0, sizeof ta);
   std::memset(&tb, 0, sizeof tb);
+  std::memset(&tal, 0, sizeof tal);
+  std::memset(&tbl, 0, sizeof tbl);
   if (tc::is_tma<VA>::value) ta = *tmap_k_major(c, ra.p, ra.rows, ra.K, ra.ld, tc::BM);
   if (tc::is_tma<VB>::value) tb = *tmap_k_major(c, rb.p, rb.rows, rb.K, rb.ld, BN);
+  if (tc::is_presplit<VA>::value) tal = *tmap_k_major(c, ra.p_lo, ra.rows, ra.K, ra.ld, tc::BM);
+  if (tc::is_presplit<VB>::value) tbl = *tmap_k_major(c, rb.p_lo, rb.rows, rb.K, rb.ld, BN);
   dim3 grid((M + tc::BM - 1) / tc::BM, (N + BN - 1) / BN, pl.splits);
   if (pl.splits == 1) {
-    launch_tc_kernel<BN, SPLIT>(c, st, grid, ta, tb, va, vb, epi, M, N, K, pl.kt_per_split);
+    launch_tc_kernel<BN, SPLIT>(c, st, grid, ta, tb, tal, tbl, va, vb, epi, M, N, K, pl.kt_per_split);
   } else {
     float* wsp = static_cast<float*>(ws.get(size_t(pl.splits) * M * N * sizeof(float), c->device));
     PartialEpi<float> pe{wsp, M, N};
-    launch_tc_kernel<BN, SPLIT>(c, st, grid, ta, tb, va, vb, pe, M, N, K, pl.kt_per_split);
+    launch_tc_kernel<BN, SPLIT>(c, st, grid, ta, tb, tal, tbl, va, vb, pe, M, N, K, pl.kt_per_split);
     launch_reduce<float>(c, st, wsp, M, N, pl.splits, epi);
   }
 }

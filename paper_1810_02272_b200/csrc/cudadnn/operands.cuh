@@ -74,6 +74,9 @@ struct DenseView {
 };
 
 // Marker: the operand is K-contiguous and 16-byte aligned, loaded by TMA.
+// Marks an operand pre-split into tf32 hi / lo copies in HBM (3xTF32): TMA loads both
+// halves, the producer warps do no conversion.
+struct TmaSplitView;
 struct TmaView {
   struct Row { int off; bool ok; };
   struct Kx { int off; bool ok; };
@@ -84,6 +87,7 @@ struct TmaView {
   __device__ __forceinline__ float at(const Row&, int) const { return 0.f; }
   __device__ __forceinline__ bool m_contig() const { return false; }
 };
+struct TmaSplitView : TmaView {};
 
 // Per-k offsets of a convolution filter tap, shared by forward (A, k = (ci,kr,ks))
 // and backward-filter (A, rows = (ci,kr,ks)):  x_off = ci*H*W + kr*dh*W + ks*dw.

@@ -56,31 +56,79 @@ GemmPlan plan_simt(int M, int N, int K) {
 }
 
 // Tiled transpose: in [R][C] (leading dimension ld) -> out [C][R] (leading dimension R).
-__global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out, int R, int C, int64_t ld) {
-  __shared__ float tile[32][33];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-  for (int j = threadIdx.y; j < 32; j += 8) {
-    const int r = r0 + j, c = c0 + threadIdx.x;
-    tile[j][threadIdx.x] = (r < R && c < C) ? in[int64_t(r) * ld + c] : 0.f;
-  }
+// A block moves four 32 x 32 tiles (a 32 x 128 strip of the input): every load of the
+// strip is issued before the barrier (16 per thread in flight), four times fewer blocks
+// than one tile each (AlexNet fc6's 4096 x 9216 weight: 36864 latency-bound blocks,
+// 2.5 TB/s).
+constexpr int kTrTiles = 4;
+// SPLIT: the output is written as its tf32 hi part and the tf32 residual lo
+// (3xTF32 operands pre-split once in HBM; the GEMM's TMA then brings both).
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                        float* __restrict__ out_lo, int R, int C, int64_t ld) {
+  __shared__ float tile[kTrTiles][32][33];
+  const int c0 = blockIdx.x * 32 * kTrTiles, r0 = blockIdx.y * 32;
+  float v[kTrTiles][4];
+#pragma unroll
+  for (int t = 0; t < kTrTiles; ++t)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + threadIdx.y + 8 * i, c = c0 + t * 32 + threadIdx.x;
+      v[t][i] = (r < R && c < C) ? __ldg(in + int64_t(r) * ld + c) : 0.f;
+    }
+#pragma unroll
+  for (int t = 0; t < kTrTiles; ++t)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tile[t][threadIdx.y + 8 * i][threadIdx.x] = v[t][i];
   __syncthreads();
-  for (int j = threadIdx.y; j < 32; j += 8) {
-    const int c = c0 + j, r = r0 + threadIdx.x;
-    if (c < C && r < R) out[int64_t(c) * R + r] = tile[threadIdx.x][j];
-  }
+#pragma unroll
+  for (int t = 0; t < kTrTiles; ++t)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = c0 + t * 32 + threadIdx.y + 8 * i, r = r0 + threadIdx.x;
+      if (c < C && r < R) {
+        const float x = tile[t][threadIdx.x][threadIdx.y + 8 * i];
+        if constexpr (SPLIT) {
+          const float hi = ptx::to_tf32(x);
+          out[int64_t(c) * R + r] = hi;
+          out_lo[int64_t(c) * R + r] = ptx::to_tf32(x - hi);
+        } else {
+          out[int64_t(c) * R + r] = x;
+        }
+      }
+    }
 }
 
 // An MN-contiguous operand of a large tensor-core GEMM, copied K-major: the
 // producers then load 16-byte K vectors instead of scalars (one extra HBM pass,
-// repaid many times by the contraction).
-DenseView<float> k_major_copy(Ctx* c, cudaStream_t st, Workspace& scratch, size_t offset_elems,
-                              const DenseView<float>& v) {
+// repaid many times by the contraction).  In 3xTF32 mode the copy is written
+// pre-split (hi at offset_elems, lo right after it): the GEMM does no conversion.
+struct KCopy {
+  DenseView<float> v;
+  const float* lo = nullptr;
+};
+KCopy k_major_copy(Ctx* c, cudaStream_t st, Workspace& scratch, size_t offset_elems, const DenseView<float>& v,
+                   bool split) {
   float* out = static_cast<float*>(scratch.ptr) + offset_elems;
-  dim3 grid((v.rows + 31) / 32, (v.K + 31) / 32);
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(v.p, out, v.K, v.rows, v.sk);
+  float* lo = split ? out + ((size_t(v.rows) * v.K + 3) & ~size_t(3)) : nullptr;  // 16-byte aligned
+  dim3 grid((v.rows + 32 * kTrTiles - 1) / (32 * kTrTiles), (v.K + 31) / 32);
+  if (split) transpose_kernel<true><<<grid, dim3(32, 8), 0, st>>>(v.p, out, lo, v.K, v.rows, v.sk);
+  else transpose_kernel<false><<<grid, dim3(32, 8), 0, st>>>(v.p, out, nullptr, v.K, v.rows, v.sk);
   check_launch("transpose");
   count_launch(c);
-  return DenseView<float>{out, int64_t(v.K), 1, v.rows, v.K, false};
+  return KCopy{DenseView<float>{out, int64_t(v.K), 1, v.rows, v.K, false}, lo};
+}
+
+// A K-major copy as a GEMM operand: pre-split TMA when it carries a lo copy (the copy
+// is only made pre-split when TMA can take it, see dense_gemm).
+template <class F>
+void with_copy(Ctx* c, const KCopy& k, int box_rows, TmaReq& req, F&& f) {
+  if (k.lo) {
+    req = TmaReq{k.v.p, k.v.rows, k.v.K, k.v.sr, k.lo};
+    f(TmaSplitView{});
+  } else {
+    with_operand(c, k.v, box_rows, req, f);
+  }
 }
 
 // One GEMM D[m][n] = sum_k A(m,k) B(n,k) with dense views, routed by dtype.
@@ -130,13 +178,20 @@ static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const De
     const GemmPlan pl = plan_tc(M, N, K);
     if (int64_t(M) * N * K >= (int64_t(1) << 28) && (va.mcontig || vb.mcontig)) {
       Workspace& aux = ws.aux();
-      const size_t na = va.mcontig ? size_t(va.rows) * va.K : 0, nb = vb.mcontig ? size_t(vb.rows) * vb.K : 0;
-      aux.get((na + nb) * sizeof(float), c->device);
-      const DenseView<float> ka = va.mcontig ? k_major_copy(c, st, aux, 0, va) : va;
-      const DenseView<float> kb = vb.mcontig ? k_major_copy(c, st, aux, na, vb) : vb;
+      const bool split = c->math_mode == CDNN_MATH_TF32X3;
+      const size_t f = split ? 2 : 1;
+      // 16-byte aligned halves (row counts are multiples of 4 elements only by chance)
+      auto round4 = [](size_t n) { return (n + 3) & ~size_t(3); };
+      const size_t na = va.mcontig ? round4(size_t(va.rows) * va.K) : 0;
+      const size_t nb = vb.mcontig ? round4(size_t(vb.rows) * vb.K) : 0;
+      aux.get((na + nb) * f * sizeof(float), c->device);
+      // the copy of an operand with `rows` rows is TMA-eligible (aligned, K >= 32, rows >= box)
+      auto presplit = [&](const DenseView<float>& v, int box) { return split && v.K >= 32 && v.K % 4 == 0 && v.rows >= box; };
+      const KCopy ka = va.mcontig ? k_major_copy(c, st, aux, 0, va, presplit(va, tc::BM)) : KCopy{va, nullptr};
+      const KCopy kb = vb.mcontig ? k_major_copy(c, st, aux, na * f, vb, presplit(vb, pl.bn)) : KCopy{vb, nullptr};
       TmaReq ra2, rb2;
-      with_operand(c, ka, tc::BM, ra2, [&](const auto& a) {
-        with_operand(c, kb, pl.bn, rb2, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra2, rb2); });
+      with_copy(c, ka, tc::BM, ra2, [&](const auto& a) {
+        with_copy(c, kb, pl.bn, rb2, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra2, rb2); });
       });
       return;
     }
