@@ -87,7 +87,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
 }
 
 template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, BN >= 128 ? 1 : 2) conv_wtap_kernel(const WtapArgs a) {
+__global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(const WtapArgs a) {
   constexpr int TM = 128;
   const int item = blockIdx.y;
   const int cb = item % a.cblocks;

@@ -72,6 +72,27 @@ void launch_conv_tap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const CUtenso
   count_launch(c);
 }
 
+// Output-channel tile width: the candidate with the least padding (ceil(Cout/bn)*bn),
+// ties to the wider tile; N = 48 / 96 tiles fit AlexNet's 48 (conv2 backward-data),
+// 96 (conv1) and 192 (conv4 / conv5 groups) channels exactly, where 64 / 128 tiles
+// padded 25% of the MMA work.  Narrower while the grid would not fill the SMs.
+int pick_bn(int cout, int tiles_m, int groups, std::initializer_list<int> cands) {
+  int best = 0;
+  int64_t best_pad = 0;
+  for (int bn : cands) {
+    const int64_t pad = int64_t((cout + bn - 1) / bn) * bn;
+    if (!best || pad < best_pad || (pad == best_pad && bn > best)) { best = bn; best_pad = pad; }
+  }
+  while (best > 32 && int64_t(tiles_m) * groups * ((cout + best - 1) / best) < kNumSMs) {
+    int smaller = 0;
+    for (int bn : cands)
+      if (bn < best && bn > smaller) smaller = bn;
+    if (!smaller) break;
+    best = smaller;
+  }
+  return best;
+}
+
 // Tap-shift implicit GEMM (conv_tap.cuh): stride 1, any dilation, any group count.
 // Returns false when the staged tile does not fit shared memory.
 bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const float* in, const float* w,
@@ -110,8 +131,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   a.div_wv = FastDiv(uint32_t(a.Wv));
   const bool split = c->math_mode == CDNN_MATH_TF32X3;
   const int tiles = (a.Mv + 127) / 128;
-  int bn = Cout <= 32 ? 32 : (Cout <= 64 ? 64 : 128);
-  if (bn > 32 && tiles * G * ((Cout + bn - 1) / bn) < kNumSMs) bn = bn == 128 ? 64 : 32;
+  const int bn = pick_bn(Cout, tiles, G, {32, 48, 64, 96, 128});
   // shared memory: A buffers (double-buffered over channel blocks when they fit) + B ring
   int budget = 227 * 1024;
   // 32-wide tiles (<= 32 output channels per block, the CIFAR / LeNet / ResNet stage-1
@@ -168,7 +188,9 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
       constexpr bool SP = decltype(split_tag)::value;
       switch (bn) {
         case 32: launch_conv_tap<32, SP>(c, st, grid, smem, *twh, *twl, ag); break;
+        case 48: launch_conv_tap<48, SP>(c, st, grid, smem, *twh, *twl, ag); break;
         case 64: launch_conv_tap<64, SP>(c, st, grid, smem, *twh, *twl, ag); break;
+        case 96: launch_conv_tap<96, SP>(c, st, grid, smem, *twh, *twl, ag); break;
         default: launch_conv_tap<128, SP>(c, st, grid, smem, *twh, *twl, ag); break;
       }
     };
@@ -210,7 +232,7 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   a.Kc = g.Cg * g.R * g.S;
   a.div_hwv = FastDiv(uint32_t(a.Hv * a.Wv));
   a.div_wv = FastDiv(uint32_t(a.Wv));
-  const int bn = g.Cog <= 32 ? 32 : (g.Cog <= 64 ? 64 : 128);
+  const int bn = pick_bn(g.Cog, 1 << 20, 1, {32, 64, 96, 128});  // (split-K fills the grid)
   a.cblocks = (g.Cg + 31) / 32;
   a.coblocks = (g.Cog + bn - 1) / bn;
   // pack the taps into groups of four equally spaced X rows: along kernel rows
@@ -270,7 +292,7 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   }
   const int items = a.cblocks * a.ggroups * a.coblocks;
   a.nchunks = (a.Mv + tcwtap::KC - 1) / tcwtap::KC;
-  const int target = (smem <= 113 * 1024 && bn < 128 ? 2 : 1) * kNumSMs;  // BN 128: one CTA per SM (registers)
+  const int target = (smem <= 113 * 1024 && bn < 96 ? 2 : 1) * kNumSMs;  // BN >= 96: one CTA per SM (registers)
   // whole waves: the largest split count whose grid still fits the resident slots
   // (a 168-CTA grid on 148 one-CTA SMs runs as two waves, the second one 20 CTAs wide)
   int splits = items >= target ? 1 : target / items;
@@ -293,6 +315,7 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
       switch (bn) {
         case 32: launch_conv_wtap<32, SP>(c, st, grid, smem, ag); break;
         case 64: launch_conv_wtap<64, SP>(c, st, grid, smem, ag); break;
+        case 96: launch_conv_wtap<96, SP>(c, st, grid, smem, ag); break;
         default: launch_conv_wtap<128, SP>(c, st, grid, smem, ag); break;
       }
     };

@@ -107,6 +107,9 @@ CONV_CASES = [
     (2, 64, 8, 8, 32, 1, 1, 0, 1, 1),       # 1x1
     (1, 64, 13, 13, 256, 3, 1, 1, 1, 1),    # two 128-wide output blocks
     (2, 8, 12, 10, 8, 3, 1, 0, 3, 1),       # dilation 3, no padding
+    (2, 3, 39, 39, 96, 11, 4, 0, 1, 1),     # AlexNet conv1 (96 outputs: N = 96 tiles)
+    (2, 96, 15, 15, 256, 5, 1, 2, 1, 2),    # AlexNet conv2 (backward-data to 48 channels: N = 48 tiles)
+    (2, 384, 13, 13, 384, 3, 1, 1, 1, 2),   # AlexNet conv4 (192 per group: N = 96 tiles)
 ]
 
 
