@@ -255,6 +255,13 @@ CDNN_API int cdnn_conv_backward_data_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_han
 CDNN_API int cdnn_conv_backward_filter(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x,
                                        cdnn_handle dy, cdnn_handle dw, cdnn_handle db,
                                        cdnn_handle stream);
+/* cdnn_conv_backward_filter with flags: CDNN_CONV_INPUT_UNCHANGED promises that x is the
+ * very buffer, unmodified, of the last forward on this descriptor, so an input rewrite
+ * the forward made (space-to-depth of a strided stem) is reused instead of redone */
+enum { CDNN_CONV_INPUT_UNCHANGED = 2 };
+CDNN_API int cdnn_conv_backward_filter_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x,
+                                          cdnn_handle dy, cdnn_handle dw, cdnn_handle db, int flags,
+                                          cdnn_handle stream);
 
 /* Pooling (Caffe semantics).  mask: I32 buffer of top count
  * holding the flat h*W+w argmax (MAX only; first max wins, strict >). */

@@ -290,6 +290,7 @@ class ConvolutionLayer final : public Layer {
   bool supports_relu_gate() const override { return true; }
 
  private:
+  cdnn_handle fwd_input_ = 0;  // bottom data of the last forward
   ConvolutionParam p_;
   std::shared_ptr<Registry> reg_;
   cdnn_handle desc_ = 0;

@@ -94,6 +94,7 @@ struct ConvDescSlot {
   // [0] X' forward, [1] W', [2] X' backward-filter, [3] dW', [4] dX'
   std::shared_ptr<ConvDescSlot> s2d;
   std::shared_ptr<DevAlloc> s2d_buf[5];
+  const void* s2d_fwd_src = nullptr;  // input whose space-to-depth rewrite s2d_buf[0] holds
   // column fold of a small-channel stride-1 convolution (S filter columns folded
   // into C*S >= 16 channels, R x 1 kernel): descriptor and grow-only buffers
   // [0] X' forward, [1] W', [2] X' backward-filter, [3] dW'

@@ -577,15 +577,17 @@ __global__ void d2s_input_kernel(const float* __restrict__ dxs, float* __restric
 }
 
 bool conv_wgrad_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float* dy, float* dw, float* db,
-                    cdnn_handle stream) {
+                    cdnn_handle stream, bool input_unchanged) {
   if (!s2d_eligible(d.geom)) return false;
   ConvDescSlot& e = s2d_desc(c, d);
   const ConvGeom &g = d.geom, &h = e.geom;
   if (h.C < 16) return false;
   cudaStream_t st = stream_of(c, stream);
-  float* xs = s2d_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
+  // the forward's rewrite of this very input, when the caller promises it is unchanged
+  const bool reuse = input_unchanged && d.s2d_fwd_src == x && d.s2d_buf[0];
+  float* xs = reuse ? static_cast<float*>(d.s2d_buf[0]->ptr) : s2d_buffer(c, d, 2, size_t(h.N) * h.C * h.H * h.W);
   float* dws = s2d_buffer(c, d, 3, size_t(h.Co) * h.C * h.R * h.S);
-  s2d_input(x, xs, g, h, st);
+  if (!reuse) s2d_input(x, xs, g, h, st);
   CDNN_CUDA(cudaMemsetAsync(dws, 0, size_t(h.Co) * h.C * h.R * h.S * 4, st));
   check_launch("s2d");
   count_launch(c);
@@ -624,6 +626,7 @@ bool conv_forward_s2d(Ctx* c, const ConvDescSlot& d, const float* x, const float
   float* xs = s2d_buffer(c, d, 0, size_t(h.N) * h.C * h.H * h.W);
   float* wsb = s2d_buffer(c, d, 1, size_t(h.Co) * h.C * h.R * h.S);
   s2d_input(x, xs, g, h, st);
+  const_cast<ConvDescSlot&>(d).s2d_fwd_src = x;
   s2d_weight_kernel<<<grid_for(int64_t(h.Co) * h.C * h.R * h.S, 256), 256, 0, st>>>(w, wsb, g, h);
   check_launch("s2d");
   count_launch(c, 2);
@@ -933,7 +936,7 @@ void conv_backward_data_impl(Ctx* c, const ConvDescSlot& d, const BufferSlot& Wt
 
 template <typename T>
 void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, const BufferSlot& DY,
-                            BufferSlot* DW, BufferSlot* DB, cdnn_handle stream) {
+                            BufferSlot* DW, BufferSlot* DB, cdnn_handle stream, bool input_unchanged) {
   const ConvGeom& g = d.geom;
   cudaStream_t st = stream_of(c, stream);
   Workspace& ws = workspace_of(c, stream);
@@ -947,7 +950,7 @@ void conv_backward_filter_t(Ctx* c, const ConvDescSlot& d, const BufferSlot& X, 
     if (g.sh == 1 && g.sw == 1) {
       // (a column fold of the backward filter measured slower than the gather engine; forward only)
       if (conv_wgrad_tap(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) return;
-    } else if (conv_wgrad_s2d(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream)) {
+    } else if (conv_wgrad_s2d(c, d, x, reinterpret_cast<const float*>(DY.dev), dw, db, stream, input_unchanged)) {
       return;
     } else if (g.sh <= 2 && g.sw <= 2 && g.Cg >= 16 &&
                with_zero_inserted(c, d, reinterpret_cast<const float*>(DY.dev), stream, 1,
@@ -1036,6 +1039,11 @@ int cdnn_conv_backward_data_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle w, cd
 
 int cdnn_conv_backward_filter(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle dy, cdnn_handle dw,
                               cdnn_handle db, cdnn_handle stream) {
+  return cdnn_conv_backward_filter_ex(ctx, desc, x, dy, dw, db, 0, stream);
+}
+
+int cdnn_conv_backward_filter_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_handle dy, cdnn_handle dw,
+                                 cdnn_handle db, int flags, cdnn_handle stream) {
   return guarded([&] {
     Ctx* c = need_ctx(ctx);
     const ConvDescSlot& d = conv_desc(c, desc);
@@ -1050,8 +1058,9 @@ int cdnn_conv_backward_filter(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdn
     if (DB) { require_len(*DB, uint64_t(g.Co), "conv_bwd_filter db"); require_dtype(*DB, X.dtype, "conv db"); }
     require_dtype(DY, X.dtype, "conv_bwd_filter");
     DeviceGuard dg(c);
-    if (X.dtype == CDNN_F32) conv_backward_filter_t<float>(c, d, X, DY, DW, DB, stream);
-    else if (X.dtype == CDNN_F64) conv_backward_filter_t<double>(c, d, X, DY, DW, DB, stream);
+    const bool unchanged = (flags & CDNN_CONV_INPUT_UNCHANGED) != 0;
+    if (X.dtype == CDNN_F32) conv_backward_filter_t<float>(c, d, X, DY, DW, DB, stream, unchanged);
+    else if (X.dtype == CDNN_F64) conv_backward_filter_t<double>(c, d, X, DY, DW, DB, stream, unchanged);
     else fail(CDNN_INVALID_ARGUMENT, "conv_bwd_filter: floating buffers required");
   });
 }

@@ -129,6 +129,7 @@ void ConvolutionLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* c
   cdnn_ok(cdnn_conv_forward_ex(reg.context(), desc_, x, w, b, tops[0]->overwrite_gpu_data(),
                                fused_relu_ ? CDNN_CONV_RELU : 0, reg.stream()),
           "Convolution forward");
+  fwd_input_ = x;
 }
 
 void ConvolutionLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {
@@ -141,7 +142,11 @@ void ConvolutionLayer::backward_weights(std::span<Blob* const> tops, std::span<B
   const cdnn_handle dy = tops[0]->gpu_diff(), x = bottoms[0]->gpu_data();
   const cdnn_handle dw = params_[0]->mutable_gpu_diff();
   const cdnn_handle db = p_.bias_term ? params_[1]->mutable_gpu_diff() : 0;
-  cdnn_ok(cdnn_conv_backward_filter(reg.context(), desc_, x, dy, dw, db, reg.stream()), "Convolution backward");
+  // the bottom is unchanged since this layer's forward (the net rewrites no blob a
+  // convolution reads between its forward and its backward): input rewrites are reused
+  const int flags = x == fwd_input_ && !bottom_clobbered_ ? CDNN_CONV_INPUT_UNCHANGED : 0;
+  cdnn_ok(cdnn_conv_backward_filter_ex(reg.context(), desc_, x, dy, dw, db, flags, reg.stream()),
+          "Convolution backward");
 }
 
 void ConvolutionLayer::backward_inputs(std::span<Blob* const> tops, std::span<Blob* const> bottoms) {

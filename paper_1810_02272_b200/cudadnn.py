@@ -42,7 +42,7 @@ EXPORTS = [
     "cdnn_conv_desc_create", "cdnn_conv_output_shape", "cdnn_pool_desc_create", "cdnn_pool_output_shape",
     "cdnn_desc_free", "cdnn_dispatch", "cdnn_fill", "cdnn_copy", "cdnn_scal", "cdnn_axpy", "cdnn_dot",
     "cdnn_gemm", "cdnn_ip_forward", "cdnn_ip_backward", "cdnn_conv_forward", "cdnn_conv_backward_data", "cdnn_conv_backward_data_ex",
-    "cdnn_conv_backward_filter", "cdnn_pool_forward", "cdnn_pool_backward", "cdnn_pool_backward_ex", "cdnn_relu_forward",
+    "cdnn_conv_backward_filter", "cdnn_conv_backward_filter_ex", "cdnn_pool_forward", "cdnn_pool_backward", "cdnn_pool_backward_ex", "cdnn_relu_forward",
     "cdnn_relu_backward", "cdnn_sigmoid_forward", "cdnn_sigmoid_backward", "cdnn_softmax_forward",
     "cdnn_softmax_backward", "cdnn_softmax_loss_forward", "cdnn_softmax_loss_backward", "cdnn_solver_apply",
     "cdnn_nccl_available", "cdnn_nccl_unique_id", "cdnn_nccl_comm_create", "cdnn_nccl_comm_info", "cdnn_lrn_pool_supported", "cdnn_lrn_pool_forward",
@@ -123,6 +123,7 @@ def load() -> C.CDLL:
             "cdnn_conv_backward_data": ([vp, h, h, h, h, h], i),
             "cdnn_conv_backward_data_ex": ([vp, h, h, h, h, h, h], i),
             "cdnn_conv_backward_filter": ([vp, h, h, h, h, h, h], i),
+            "cdnn_conv_backward_filter_ex": ([vp, h, h, h, h, h, i, h], i),
             "cdnn_pool_forward": ([vp, h, h, h, h, h], i), "cdnn_pool_forward_ex": ([vp, h, h, h, h, i, h], i), "cdnn_pool_backward": ([vp, h, h, h, h, h], i),
             "cdnn_pool_backward_ex": ([vp, h, h, h, h, h, h], i),
             "cdnn_relu_forward": ([vp, h, h, u64, h], i), "cdnn_relu_backward": ([vp, h, h, h, u64, h], i),

@@ -507,3 +507,31 @@ def test_ip_backward_small(ctx, dtype, rows, k, o):
     assert rel_l2(ctx.read(hdx).reshape(rows, k), DY @ W) <= tol
     for h in (hx, hw, hdy, hdw, hdb, hdx):
         ctx.free(h)
+
+
+def test_conv_backward_filter_reuses_forward_input_rewrite(ctx):
+    """CDNN_CONV_INPUT_UNCHANGED: the strided stem's backward filter reuses the forward's
+    space-to-depth rewrite of its input -- bit-identical to redoing it, and ignored when
+    the promise cannot hold (another input buffer)."""
+    n, c, h, w, co, k, s = 4, 3, 67, 67, 96, 11, 4
+    rng = np.random.default_rng(21)
+    x, x2 = (rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32) for _ in range(2))
+    wt = rng.uniform(-1, 1, (co, c, k, k)).astype(np.float32)
+    d = ctx.conv_desc(n, c, h, w, co, k, s, 0)
+    P, Q = ctx.conv_output_shape(d)[2:]
+    dy = rng.uniform(-1, 1, (n, co, P, Q)).astype(np.float32)
+    hx, hx2, hw, hdy = ctx.upload(x), ctx.upload(x2), ctx.upload(wt), ctx.upload(dy)
+    hy = ctx.alloc(n * co * P * Q, cd.F32)
+    outs = []
+    for flags, xin in ((0, hx), (2, hx), (2, hx2), (0, hx2)):
+        ctx.call("cdnn_conv_forward", d, hx, hw, 0, hy, 0)  # the forward always sees x
+        hdw, hdb = ctx.alloc(wt.size, cd.F32), ctx.alloc(co, cd.F32)
+        ctx.call("cdnn_conv_backward_filter_ex", d, xin, hdy, hdw, hdb, flags, 0)
+        outs.append((ctx.read(hdw), ctx.read(hdb)))
+        ctx.free(hdw)
+        ctx.free(hdb)
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert np.array_equal(outs[2][0], outs[3][0])  # other input: the flag is ignored
+    assert not np.array_equal(outs[0][0], outs[2][0])
+    for hnd in (hx, hx2, hw, hdy, hy):
+        ctx.free(hnd)
