@@ -78,14 +78,19 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
       nx[u] = (active && c0 + u < cs1 && cin < g.C) ? __ldg(xp + uint32_t(cin) * uint32_t(HW)) : T(0);
     }
   };
-  T nxt[kG];
+  // x of the entering channels two steps ahead (HBM bytes in flight across the barrier)
+  T nxt[kG], nxt2[kG];
   load_step(cs0, nxt);
+  load_step(cs0 + kG, nxt2);
   const int prows = pr1 - pr0;
   for (int c0 = cs0, step = 0; c0 < cs1; c0 += kG, ++step) {
     T cur[kG];
 #pragma unroll
-    for (int u = 0; u < kG; ++u) cur[u] = nxt[u];
-    if (c0 + kG < cs1) load_step(c0 + kG, nxt);
+    for (int u = 0; u < kG; ++u) {
+      cur[u] = nxt[u];
+      nxt[u] = nxt2[u];
+    }
+    if (c0 + 2 * kG < cs1) load_step(c0 + 2 * kG, nxt2);
     T* buf = tile + (step & 1) * kG * tsz;
     if (active) {
 #pragma unroll
@@ -219,17 +224,21 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
 #pragma unroll
     for (int j = 0; j < SIZE - 1; ++j) xr[j] = xat(cs0 + j);
     xr[SIZE - 1] = T(0);
-    auto load_step = [&](int c0, T (&nx)[kG], int (&nm)[kG][R][R], T (&nv)[kG][R][R]) {
+    // x (the HBM stream) two steps ahead, the pooled gather (mostly cache hits) one step
+    auto load_x = [&](int c0, T (&nx)[kG]) {
 #pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        nx[u] = c0 + u < cs1 ? xat(c0 + u + SIZE - 1) : T(0);
-        gather(c0 + u < cs1 ? c0 + u + pre : g.C, nm[u], nv[u]);
-      }
+      for (int u = 0; u < kG; ++u) nx[u] = c0 + u < cs1 ? xat(c0 + u + SIZE - 1) : T(0);
     };
-    T nx[kG];
+    auto load_g = [&](int c0, int (&nm)[kG][R][R], T (&nv)[kG][R][R]) {
+#pragma unroll
+      for (int u = 0; u < kG; ++u) gather(c0 + u < cs1 ? c0 + u + pre : g.C, nm[u], nv[u]);
+    };
+    T nx[kG], nx2[kG];
     int nm[kG][R][R];
     T nv[kG][R][R];
-    load_step(cs0, nx, nm, nv);
+    load_x(cs0, nx);
+    load_x(cs0 + kG, nx2);
+    load_g(cs0, nm, nv);
     for (int c0 = cs0; c0 < cs1; c0 += kG) {
       T cx[kG];
       int cm[kG][R][R];
@@ -237,12 +246,14 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         cx[u] = nx[u];
+        nx[u] = nx2[u];
 #pragma unroll
         for (int a = 0; a < R; ++a)
 #pragma unroll
           for (int b = 0; b < R; ++b) { cm[u][a][b] = nm[u][a][b]; cv[u][a][b] = nv[u][a][b]; }
       }
-      if (c0 + kG < cs1) load_step(c0 + kG, nx, nm, nv);  // in flight during this step
+      if (c0 + 2 * kG < cs1) load_x(c0 + 2 * kG, nx2);  // in flight during this step and the next
+      if (c0 + kG < cs1) load_g(c0 + kG, nm, nv);
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         const int c = c0 + u;
