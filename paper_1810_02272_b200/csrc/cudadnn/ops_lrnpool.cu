@@ -78,19 +78,14 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
       nx[u] = (active && c0 + u < cs1 && cin < g.C) ? __ldg(xp + uint32_t(cin) * uint32_t(HW)) : T(0);
     }
   };
-  // x of the entering channels two steps ahead (HBM bytes in flight across the barrier)
-  T nxt[kG], nxt2[kG];
+  T nxt[kG];
   load_step(cs0, nxt);
-  load_step(cs0 + kG, nxt2);
   const int prows = pr1 - pr0;
   for (int c0 = cs0, step = 0; c0 < cs1; c0 += kG, ++step) {
     T cur[kG];
 #pragma unroll
-    for (int u = 0; u < kG; ++u) {
-      cur[u] = nxt[u];
-      nxt[u] = nxt2[u];
-    }
-    if (c0 + 2 * kG < cs1) load_step(c0 + 2 * kG, nxt2);
+    for (int u = 0; u < kG; ++u) cur[u] = nxt[u];
+    if (c0 + kG < cs1) load_step(c0 + kG, nxt);
     T* buf = tile + (step & 1) * kG * tsz;
     if (active) {
 #pragma unroll
