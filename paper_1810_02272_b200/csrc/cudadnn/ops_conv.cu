@@ -548,8 +548,59 @@ __global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict_
   }
 }
 
+// Compile-time stride S (AlexNet's stem: 4) and X' rows of at most 64: a warp takes
+// NG consecutive groups and issues every load of them (NG x 2 x S per lane) before any
+// store -- the per-group kernel above kept one group's 2 x 8 loads in flight
+// (AlexNet conv1: 318 MB in 146 us, 2.2 TB/s).
+template <int S, int NG>
+__global__ void __launch_bounds__(256) s2d_input_k(const float* __restrict__ x, float* __restrict__ xs, ConvGeom g,
+                                                   ConvGeom h) {
+  const int groups = h.N * g.C * S * h.H;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const size_t plane = size_t(h.H) * h.W;
+  const size_t step = size_t(g.C) * plane;
+  for (int g0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NG; g0 < groups; g0 += warps * NG) {
+    float v[NG][2][S];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+      const int grp = g0 + q;
+      const int h2 = grp % h.H, t = grp / h.H;
+      const int dy = t % S, c = (t / S) % g.C, n = t / (S * g.C);
+      const int y = S * h2 + dy - g.ph;
+      const bool ok = grp < groups && y >= 0 && y < g.H;
+      const float* in = x + (size_t(n) * g.C + c) * g.H * g.W + size_t(ok ? y : 0) * g.W;
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          const int w2 = lane + 32 * r, xx = S * w2 + j - g.pw;
+          v[q][r][j] = (ok && w2 < h.W && xx >= 0 && xx < g.W) ? __ldg(in + xx) : 0.f;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+      const int grp = g0 + q;
+      if (grp >= groups) break;
+      const int h2 = grp % h.H, t = grp / h.H;
+      const int dy = t % S, c = (t / S) % g.C, n = t / (S * g.C);
+      float* out = xs + (size_t(n) * h.C + size_t(dy) * S * g.C + c) * plane + size_t(h2) * h.W;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int w2 = lane + 32 * r;
+        if (w2 < h.W)
+#pragma unroll
+          for (int j = 0; j < S; ++j) out[j * step + w2] = v[q][r][j];
+      }
+    }
+  }
+}
+
 void s2d_input(const float* x, float* xs, const ConvGeom& g, const ConvGeom& h, cudaStream_t st) {
-  if (g.sh >= 4)
+  if (g.sh == 4 && h.W <= 64) {
+    constexpr int NG = 4;
+    s2d_input_k<4, NG><<<grid_for(int64_t(h.N) * g.C * 4 * h.H * 32 / NG, 256), 256, 0, st>>>(x, xs, g, h);
+  } else if (g.sh >= 4)
     s2d_input_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32 / g.sh, 256), 256, 0, st>>>(x, xs, g, h);
   else
     s2d_input_rows_kernel<<<grid_for(int64_t(h.N) * h.C * h.H * 32, 256), 256, 0, st>>>(x, xs, g, h);
