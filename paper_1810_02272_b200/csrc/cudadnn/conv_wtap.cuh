@@ -40,8 +40,8 @@ namespace tcwtap {
 
 constexpr int kThreads = 320;  // warp 1 MMA, warps 2-9 stage (2-5 also run the epilogue)
 constexpr int kStagers = 256;
-constexpr int KC = 64;  // virtual pixels per chunk (K per pipeline stage)
 constexpr int kMaxGroups = 32;
+constexpr int kMaxStages = 4;  // pipeline stages (chunks of KC virtual pixels) in shared memory
 
 // Four taps whose X rows sit a constant number of virtual rows apart (along a
 // kernel row: dw; along a kernel column: dh*Wv) form one MMA's M atoms.
@@ -66,14 +66,18 @@ struct WtapArgs {
   int rows_lo[kMaxGroups];         // per set: first staged row offset
   int splits, chunks_per_split, nchunks;
   int rowsA;                      // staged X rows per chunk (multiple of 8)
+  int stages;                     // pipeline depth (2..kMaxStages)
   int want_bias;
   FastDiv div_hwv, div_wv;
 };
 
 __host__ __device__ constexpr uint32_t a_bytes(int rowsA, bool split) { return uint32_t(rowsA) * 128u * (split ? 2u : 1u); }
-__host__ __device__ constexpr uint32_t b_bytes(int bn, bool split) { return uint32_t(bn) * KC * 4u * (split ? 2u : 1u); }
-inline int smem_bytes(int rowsA, int bn, bool split) {
-  return 1024 + 2 * int(a_bytes(rowsA, split) + b_bytes(bn, split)) + 2 * bn * 4 + 8 * 8 + 16;
+__host__ __device__ constexpr uint32_t b_bytes(int bn, bool split, int kc) {
+  return uint32_t(bn) * uint32_t(kc) * 4u * (split ? 2u : 1u);
+}
+inline int smem_bytes(int rowsA, int bn, bool split, int kc, int stages) {
+  return 1024 + stages * int(a_bytes(rowsA, split) + b_bytes(bn, split, kc)) + 2 * bn * 4 + (2 * kMaxStages + 2) * 8 +
+         16;
 }
 
 __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -86,7 +90,9 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
   return d;
 }
 
-template <int BN, bool SPLIT>
+// KC: virtual pixels per pipeline chunk (64, or 32 with up to four stages when one CTA
+// owns the SM: smaller stages, a deeper pipeline)
+template <int BN, bool SPLIT, int KC>
 __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(const WtapArgs a) {
   constexpr int TM = 128;
   const int item = blockIdx.y;
@@ -103,12 +109,13 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t A_B = a_bytes(a.rowsA, SPLIT), A_H = uint32_t(a.rowsA) * 128u;
-  constexpr uint32_t B_B = b_bytes(BN, SPLIT);
+  constexpr uint32_t B_B = b_bytes(BN, SPLIT, KC);
   const uint32_t STAGE = A_B + B_B;  // multiple of 1024 (rowsA % 8 == 0, BN*KC*4 % 1024 == 0)
-  float* bias_part = reinterpret_cast<float*>(smem + 2 * STAGE);  // [pixel half][BN]
+  const int NS = a.stages;
+  float* bias_part = reinterpret_cast<float*>(smem + NS * STAGE);  // [pixel half][BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(bias_part + 2 * BN);
-  uint64_t* empty = full + 2;
-  uint64_t* accum = empty + 2;
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* accum = empty + kMaxStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
   // 3xTF32 with BN <= 64: [dY_hi | dY_lo] concatenated along N (one MMA gives
   // X_hi*dY_hi and X_hi*dY_lo in two column halves; X_lo*dY_hi adds into the
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NS; ++b) {
       ptx::mbar_init(&full[b], kStagers / 32);
       ptx::mbar_init(&empty[b], 1);
     }
@@ -144,9 +151,8 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
                                  (uint32_t(TM >> 4) << 24);
       constexpr uint32_t idesc_cat = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
                                      (uint32_t((2 * BN) >> 3) << 17) | (uint32_t(TM >> 4) << 24);
-      for (int ch = ch0; ch < ch1; ++ch) {
-        const int b = (ch - ch0) & 1;
-        ptx::mbar_wait(&full[b], uint32_t((ch - ch0) >> 1) & 1u);
+      for (int ch = ch0, b = 0, ph = 0; ch < ch1; ++ch) {
+        ptx::mbar_wait(&full[b], uint32_t(ph));
         ptx::tc_fence_after();
         const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
         for (int k8 = 0; k8 < KC / 8; ++k8) {
@@ -172,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
           }
         }
         ptx::mma_commit_elect(&empty[b]);
+        if (++b == NS) { b = 0; ph ^= 1; }
       }
       ptx::mma_commit_elect(accum);
     }
@@ -185,9 +192,10 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
     // element costs one load at base + co*PQ and two 4-byte stores; a warp's 32 lanes
     // fill one 128-byte K-major row (conflict free).  A: one pixel row per thread (rows
     // beyond kStagers, if any, take the sequential path below).
-    static_assert(KC == 64, "two 32-pixel halves per chunk");
-    constexpr int CPW = BN / 4;  // output channels per warp
-    const int sw = tid >> 5, khalf = sw & 1, cw0 = (sw >> 1) * CPW;
+    static_assert(KC == 64 || KC == 32, "one or two 32-pixel halves per chunk");
+    constexpr int KH = KC / 32;        // 32-pixel halves per chunk
+    constexpr int CPW = BN * KH / 8;   // output channels per warp
+    const int sw = tid >> 5, khalf = sw % KH, cw0 = (sw / KH) * CPW;
     float bsum[CPW];
 #pragma unroll
     for (int c = 0; c < CPW; ++c) bsum[c] = 0.f;
@@ -253,8 +261,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
         if (do_bias) bsum[c] += yv[c];
       }
     };
-    for (int ch = ch0; ch < ch1; ++ch) {
-      const int b = (ch - ch0) & 1;
+    for (int ch = ch0, b = 0, ph = 0; ch < ch1; ++ch) {
       const int v0 = ch * KC;
       // Every global load of this thread's share of the chunk is issued BEFORE waiting
       // for the buffer: the loads fly while the MMAs of the two previous chunks run,
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
       a_load(asrc, inb && tid < a.rowsA, xv);
       float yv[CPW];
       b_load(v0, yv);
-      if (ch - ch0 >= 2) ptx::mbar_wait(&empty[b], uint32_t(((ch - ch0) >> 1) - 1) & 1u);
+      if (ch - ch0 >= NS) ptx::mbar_wait(&empty[b], uint32_t(ph ^ 1));
       const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
       if (tid < a.rowsA) a_store(abase, tid, xv);
       b_store(bbase, yv);
@@ -280,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&full[b]);
+      if (++b == NS) { b = 0; ph ^= 1; }
     }
     if (do_bias) {  // per output channel: fixed xor tree over the warp's 32 pixels, then the two halves
 #pragma unroll

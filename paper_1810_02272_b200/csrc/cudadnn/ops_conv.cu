@@ -218,9 +218,9 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   return true;
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, int KC>
 void launch_conv_wtap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const tcwtap::WtapArgs& a) {
-  auto kern = tcwtap::conv_wtap_kernel<BN, SPLIT>;
+  auto kern = tcwtap::conv_wtap_kernel<BN, SPLIT, KC>;
   static int attr_smem[16] = {};
   if (attr_smem[c->device & 15] < smem) {
     CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -295,8 +295,9 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
       a.rows_lo[i] = lo;
       rows_max = std::max(rows_max, hi - lo);
     }
-    a.rowsA = (tcwtap::KC + rows_max + 7) & ~7;
-    smem = tcwtap::smem_bytes(a.rowsA, bn, split);
+    a.rowsA = (64 + rows_max + 7) & ~7;
+    a.stages = 2;
+    smem = tcwtap::smem_bytes(a.rowsA, bn, split, 64, 2);
     // one CTA per SM anyway (shared memory): use the whole 512-column TMEM
     if (!widened && smem > 113 * 1024 && per_set < 512 / acc_cols) {
       widened = true;
@@ -308,8 +309,30 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
     per_set = std::max(1, per_set / 2);
   }
   const int items = a.cblocks * a.ggroups * a.coblocks;
-  a.nchunks = (a.Mv + tcwtap::KC - 1) / tcwtap::KC;
-  const int target = (smem <= 113 * 1024 && bn < 96 ? 2 : 1) * kNumSMs;  // BN >= 96: one CTA per SM (registers)
+  const bool two_per_sm = smem <= 113 * 1024 && bn < 96;  // BN >= 96: one CTA per SM (registers)
+  // One CTA per SM: a deeper pipeline.  64-pixel chunks when three stages fit, else
+  // 32-pixel chunks (half the stage, a larger share of halo rows) with up to four.
+  int kc = 64;
+  if (!two_per_sm) {
+    int rows_max = a.rowsA - 64;
+    auto stages_fit = [&](int k) {
+      const int rows = (k + rows_max + 7) & ~7;
+      int st = 0;
+      while (st < tcwtap::kMaxStages && tcwtap::smem_bytes(rows, bn, split, k, st + 1) <= kBudget) ++st;
+      return st;
+    };
+    const int s64 = stages_fit(64), s32 = stages_fit(32);
+    if (s64 < 3 && s32 >= 3) {
+      kc = 32;
+      a.stages = s32;
+      a.rowsA = (32 + rows_max + 7) & ~7;
+    } else {
+      a.stages = std::max(2, s64);
+    }
+    smem = tcwtap::smem_bytes(a.rowsA, bn, split, kc, a.stages);
+  }
+  a.nchunks = (a.Mv + kc - 1) / kc;
+  const int target = (two_per_sm ? 2 : 1) * kNumSMs;
   // whole waves: the largest split count whose grid still fits the resident slots
   // (a 168-CTA grid on 148 one-CTA SMs runs as two waves, the second one 20 CTAs wide)
   int splits = items >= target ? 1 : target / items;
@@ -329,11 +352,20 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
     ag.ws = ws;
     auto go = [&](auto split_tag) {
       constexpr bool SP = decltype(split_tag)::value;
-      switch (bn) {
-        case 32: launch_conv_wtap<32, SP>(c, st, grid, smem, ag); break;
-        case 64: launch_conv_wtap<64, SP>(c, st, grid, smem, ag); break;
-        case 96: launch_conv_wtap<96, SP>(c, st, grid, smem, ag); break;
-        default: launch_conv_wtap<128, SP>(c, st, grid, smem, ag); break;
+      if (kc == 32) {
+        switch (bn) {
+          case 32: launch_conv_wtap<32, SP, 32>(c, st, grid, smem, ag); break;
+          case 64: launch_conv_wtap<64, SP, 32>(c, st, grid, smem, ag); break;
+          case 96: launch_conv_wtap<96, SP, 32>(c, st, grid, smem, ag); break;
+          default: launch_conv_wtap<128, SP, 32>(c, st, grid, smem, ag); break;
+        }
+      } else {
+        switch (bn) {
+          case 32: launch_conv_wtap<32, SP, 64>(c, st, grid, smem, ag); break;
+          case 64: launch_conv_wtap<64, SP, 64>(c, st, grid, smem, ag); break;
+          case 96: launch_conv_wtap<96, SP, 64>(c, st, grid, smem, ag); break;
+          default: launch_conv_wtap<128, SP, 64>(c, st, grid, smem, ag); break;
+        }
       }
     };
     if (split) go(std::true_type{});
