@@ -310,27 +310,9 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
   }
   const int items = a.cblocks * a.ggroups * a.coblocks;
   const bool two_per_sm = smem <= 113 * 1024 && bn < 96;  // BN >= 96: one CTA per SM (registers)
-  // One CTA per SM: a deeper pipeline.  64-pixel chunks when three stages fit, else
-  // 32-pixel chunks (half the stage, a larger share of halo rows) with up to four.
-  int kc = 64;
-  if (!two_per_sm) {
-    int rows_max = a.rowsA - 64;
-    auto stages_fit = [&](int k) {
-      const int rows = (k + rows_max + 7) & ~7;
-      int st = 0;
-      while (st < tcwtap::kMaxStages && tcwtap::smem_bytes(rows, bn, split, k, st + 1) <= kBudget) ++st;
-      return st;
-    };
-    const int s64 = stages_fit(64), s32 = stages_fit(32);
-    if (s64 < 3 && s32 >= 3) {
-      kc = 32;
-      a.stages = s32;
-      a.rowsA = (32 + rows_max + 7) & ~7;
-    } else {
-      a.stages = std::max(2, s64);
-    }
-    smem = tcwtap::smem_bytes(a.rowsA, bn, split, kc, a.stages);
-  }
+  // (deeper pipelines -- three 64-pixel stages, or four 32-pixel ones -- measured slower
+  // on AlexNet's weight gradients: 0.54 -> 0.61 ms for conv3; two 64-pixel stages stay)
+  const int kc = 64;
   a.nchunks = (a.Mv + kc - 1) / kc;
   const int target = (two_per_sm ? 2 : 1) * kNumSMs;
   // whole waves: the largest split count whose grid still fits the resident slots
@@ -352,20 +334,11 @@ bool conv_wgrad_tap(Ctx* c, const ConvDescSlot& d, const float* x, const float* 
     ag.ws = ws;
     auto go = [&](auto split_tag) {
       constexpr bool SP = decltype(split_tag)::value;
-      if (kc == 32) {
-        switch (bn) {
-          case 32: launch_conv_wtap<32, SP, 32>(c, st, grid, smem, ag); break;
-          case 64: launch_conv_wtap<64, SP, 32>(c, st, grid, smem, ag); break;
-          case 96: launch_conv_wtap<96, SP, 32>(c, st, grid, smem, ag); break;
-          default: launch_conv_wtap<128, SP, 32>(c, st, grid, smem, ag); break;
-        }
-      } else {
-        switch (bn) {
-          case 32: launch_conv_wtap<32, SP, 64>(c, st, grid, smem, ag); break;
-          case 64: launch_conv_wtap<64, SP, 64>(c, st, grid, smem, ag); break;
-          case 96: launch_conv_wtap<96, SP, 64>(c, st, grid, smem, ag); break;
-          default: launch_conv_wtap<128, SP, 64>(c, st, grid, smem, ag); break;
-        }
+      switch (bn) {
+        case 32: launch_conv_wtap<32, SP, 64>(c, st, grid, smem, ag); break;
+        case 64: launch_conv_wtap<64, SP, 64>(c, st, grid, smem, ag); break;
+        case 96: launch_conv_wtap<96, SP, 64>(c, st, grid, smem, ag); break;
+        default: launch_conv_wtap<128, SP, 64>(c, st, grid, smem, ag); break;
       }
     };
     if (split) go(std::true_type{});
