@@ -351,11 +351,29 @@ def run_b200(args) -> None:
         return float(t.item())
 
     text = model_text(BATCH)
+    if args.dp_transport == "host":  # validation runs may put several ranks on one GPU
+        local = local % max(1, cudadnn.device_count())
     net = polegrad.Net(text, seed=1, dtype=DTYPE, device=local)
     solver = polegrad.Solver(net, **SOLVER)
     cx = CtxView(net.context_ptr())
     par = None
-    if world > 1:
+    if world > 1 and args.dp_transport == "host":
+        # validation of the N > 1 path where NCCL cannot run (several ranks on one GPU):
+        # the product's Parallel with its host transport over gloo (eager steps only)
+        import torch
+
+        def transport(op, arr, offset):
+            t = torch.from_numpy(arr)
+            if op == 0:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            else:
+                dist.broadcast(t, src=0)
+
+        par = polegrad.Parallel.host(net, world, rank, transport)
+        par.broadcast()
+        solver.set_parallel(par)
+        args.no_graph = True
+    elif world > 1:
         uid = [polegrad.Parallel.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         par = polegrad.Parallel(net, world, rank, uid[0])
@@ -794,6 +812,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the captured CUDA graph")
+    ap.add_argument("--dp-transport", choices=["nccl", "host"], default="nccl",
+                    help="N > 1 gradient exchange: NCCL (product), or the Parallel host transport over gloo "
+                         "(validation of the multi-rank path with several ranks on one GPU; eager steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD,
