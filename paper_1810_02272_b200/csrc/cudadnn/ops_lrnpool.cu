@@ -30,10 +30,8 @@
 namespace cdnn {
 namespace {
 
-// channels per step = the LRN window (5): the register rings rotate back to their slots
-// within an unrolled step, so no ring moves; one block barrier per step (forward)
-constexpr int kG = 5;
-constexpr int kSeg = 30;  // channels per thread / block segment (segments run in parallel)
+constexpr int kG = 4;     // channels per step (loads in flight; one block barrier per step)
+constexpr int kSeg = 32;  // channels per thread / block segment (segments run in parallel)
 
 struct LrnPoolGeom {
   int N, C, H, W, PH, PW;
