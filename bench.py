@@ -381,7 +381,7 @@ def run_b200(args) -> None:
         solver.set_parallel(par)
     nccl_ranks = par.info() if par else None
     if nccl_ranks:
-        log(f"rank {rank}: NCCL communicator reports {nccl_ranks['nranks']} ranks (this one {nccl_ranks['rank']}), "
+        log(f"rank {rank}: the Parallel communicator reports {nccl_ranks['nranks']} ranks (this one {nccl_ranks['rank']}), "
             f"{nccl_ranks['buckets']} gradient buckets")
         if nccl_ranks["nranks"] != world:
             raise RuntimeError(f"NCCL communicator has {nccl_ranks['nranks']} ranks, WORLD_SIZE {world}")
