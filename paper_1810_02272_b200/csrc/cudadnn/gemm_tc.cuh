@@ -448,5 +448,159 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
   }
 }
 
+// Persistent 3xTF32 GEMM for two PRE-SPLIT TMA operands (the K-major copies of the
+// accumulate-heavy InnerProduct GEMMs, e.g. AlexNet fc6 dW += dY^T X: M = 9216, N = 4096,
+// K = 256 -- 2304 short tiles, which the one-tile-per-CTA kernel above ran with the
+// epilogue (read-modify-write of the old dW) serialised after the MMAs: 17 us per
+// 6144-cycle tile).  One CTA per SM walks the tiles; two TMEM accumulators let the
+// epilogue warps drain tile i while the MMA warp runs tile i+1.
+//   warp 0  TMA: A_hi, A_lo, B_hi, B_lo per 32-wide k-slab into a stage ring
+//   warp 1  TMEM owner + MMA issuer
+//   2-5     epilogue: the old C row is read before waiting for the accumulator
+constexpr int kPStages = 3;
+template <int BN>
+__host__ __device__ constexpr int persist_smem_bytes() {
+  return 1024 + kPStages * (BM * BK * 4 + BN * BK * 4) * 2 + (2 * kPStages + 4) * 8 + 16;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmA_lo, const __grid_constant__ CUtensorMap tmB_lo,
+                           const StoreEpi<float> epi, int M, int N, int K) {
+  constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+  constexpr uint32_t STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  constexpr uint32_t TMEM_COLS = tmem_cols_for(2 * BN);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  auto a_hi = [&](int st) { return smem + st * STAGE_BYTES; };
+  auto b_hi = [&](int st) { return smem + st * STAGE_BYTES + A_BYTES; };
+  auto a_lo = [&](int st) { return smem + st * STAGE_BYTES + A_BYTES + B_BYTES; };
+  auto b_lo = [&](int st) { return smem + st * STAGE_BYTES + 2 * A_BYTES + B_BYTES; };
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPStages * STAGE_BYTES);
+  uint64_t* empty = full + kPStages;
+  uint64_t* t_full = empty + kPStages;  // [2]
+  uint64_t* t_empty = t_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (M + BM - 1) / BM, tiles = tiles_m * ((N + BN - 1) / BN);
+  const int nkt = (K + BK - 1) / BK;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kPStages; ++st) {
+      ptx::mbar_init(&full[st], 1);
+      ptx::mbar_init(&empty[st], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&t_full[b], 1);
+      ptx::mbar_init(&t_empty[b], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmA);
+      ptx::tma_prefetch_desc(&tmB);
+      ptx::tma_prefetch_desc(&tmA_lo);
+      ptx::tma_prefetch_desc(&tmB_lo);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+        for (int kt = 0; kt < nkt; ++kt) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          const int kc = kt * BK;
+          ptx::tma_load_2d(a_hi(stage), &tmA, &full[stage], kc, m0);
+          ptx::tma_load_2d(a_lo(stage), &tmA_lo, &full[stage], kc, m0);
+          ptx::tma_load_2d(b_hi(stage), &tmB, &full[stage], kc, n0);
+          ptx::tma_load_2d(b_lo(stage), &tmB_lo, &full[stage], kc, n0);
+          if (++stage == kPStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = make_idesc_tf32(BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int ts = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ts) {
+      const int buf = ts & 1;
+      if (ts >= 2) ptx::mbar_wait(&t_empty[buf], uint32_t((ts >> 1) - 1) & 1u);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem + uint32_t(buf * BN);
+      for (int kt = 0; kt < nkt; ++kt) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint64_t ah = make_sw128_desc(ptx::smem_u32(a_hi(stage)));
+        const uint64_t bh = make_sw128_desc(ptx::smem_u32(b_hi(stage)));
+        const uint64_t al = make_sw128_desc(ptx::smem_u32(a_lo(stage)));
+        const uint64_t bl = make_sw128_desc(ptx::smem_u32(b_lo(stage)));
+#pragma unroll
+        for (int j = 0; j < BK / 8; ++j) {
+          const uint64_t dk = uint64_t(2 * j);
+          ptx::mma_tf32_elect(d_tmem, al + dk, bh + dk, idesc, (kt > 0 || j > 0) ? 1u : 0u);  // small terms first
+          ptx::mma_tf32_elect(d_tmem, ah + dk, bl + dk, idesc, 1u);
+          ptx::mma_tf32_elect(d_tmem, ah + dk, bh + dk, idesc, 1u);
+        }
+        ptx::mma_commit_elect(&empty[stage]);
+        if (++stage == kPStages) { stage = 0; phase ^= 1; }
+      }
+      ptx::mma_commit_elect(&t_full[buf]);
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    int ts = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ts) {
+      const int buf = ts & 1;
+      const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+      const int m = m0 + q * 32 + lane;
+      const bool rowok = m < M;
+      float* orow = epi.out + int64_t(m) * epi.sm + int64_t(n0) * epi.sn;
+      float prev[BN];
+#pragma unroll
+      for (int j = 0; j < BN; ++j)
+        prev[j] = (rowok && epi.beta != 0.f && n0 + j < N) ? orow[int64_t(j) * epi.sn] : 0.f;
+      ptx::mbar_wait(&t_full[buf], uint32_t(ts >> 1) & 1u);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BN + c), r);
+        ptx::tmem_ld_wait();
+        if (rowok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = n0 + c + j;
+            if (n < N) {
+              float v = epi.alpha * __uint_as_float(r[j]);
+              if (epi.beta != 0.f) v += epi.beta * prev[c + j];
+              if (epi.bias) v += epi.bias[epi.bias_on_m ? m : n];
+              if (epi.relu) v = v > 0.f ? v : 0.f;
+              orow[int64_t(c + j) * epi.sn] = v;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&t_empty[buf]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
 }  // namespace tc
 }  // namespace cdnn

@@ -110,6 +110,29 @@ void launch_tc_kernel(Ctx* c, cudaStream_t st, dim3 grid, const CUtensorMap& ta,
 template <int BN, bool SPLIT, class VA, class VB, class EPI>
 void run_tc_bn(Ctx* c, cudaStream_t st, Workspace& ws, const GemmPlan& pl, int M, int N, int K,
                const VA& va, const VB& vb, const EPI& epi, const TmaReq& ra, const TmaReq& rb) {
+  if constexpr (SPLIT && BN == 128 && tc::is_presplit<VA>::value && tc::is_presplit<VB>::value &&
+                std::is_same_v<EPI, StoreEpi<float>>) {
+    // both operands pre-split and many tiles: the persistent kernel (epilogue of tile i
+    // under the MMAs of tile i+1)
+    const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + BN - 1) / BN);
+    if (pl.splits == 1 && tiles >= 2 * kNumSMs) {
+      const CUtensorMap ta = *tmap_k_major(c, ra.p, ra.rows, ra.K, ra.ld, tc::BM);
+      const CUtensorMap tb = *tmap_k_major(c, rb.p, rb.rows, rb.K, rb.ld, BN);
+      const CUtensorMap tal = *tmap_k_major(c, ra.p_lo, ra.rows, ra.K, ra.ld, tc::BM);
+      const CUtensorMap tbl = *tmap_k_major(c, rb.p_lo, rb.rows, rb.K, rb.ld, BN);
+      constexpr int smem = tc::persist_smem_bytes<BN>();
+      auto kern = tc::tc_gemm_persist_kernel<BN>;
+      static bool attr_set[16] = {};
+      if (!attr_set[c->device & 15]) {
+        CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_set[c->device & 15] = true;
+      }
+      kern<<<std::min(tiles, kNumSMs), tc::kThreads, smem, st>>>(ta, tb, tal, tbl, epi, M, N, K);
+      check_launch("tc_gemm_persist_kernel");
+      count_launch(c);
+      return;
+    }
+  }
   CUtensorMap ta, tb, tal, tbl;
   std::memset(&ta, 0, sizeof ta);
   std::memset(&tb, 0, sizeof tb);
