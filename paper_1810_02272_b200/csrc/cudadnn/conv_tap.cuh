@@ -100,12 +100,12 @@ __device__ __forceinline__ void put_row8(uint32_t rbase, uint32_t lo_off, int ro
   for (int h = 0; h < 2; ++h) {
     const int g4 = g8 * 2 + h;
     const uint32_t off = rbase + (uint32_t((g4 ^ (row & 7)) & 7) << 4);
-    const float h0 = ptx::to_tf32(x[4 * h]), h1 = ptx::to_tf32(x[4 * h + 1]);
-    const float h2 = ptx::to_tf32(x[4 * h + 2]), h3 = ptx::to_tf32(x[4 * h + 3]);
+    const float h0 = ptx::tf32_major<SPLIT>(x[4 * h]), h1 = ptx::tf32_major<SPLIT>(x[4 * h + 1]);
+    const float h2 = ptx::tf32_major<SPLIT>(x[4 * h + 2]), h3 = ptx::tf32_major<SPLIT>(x[4 * h + 3]);
     ptx::st_shared_v4(off, h0, h1, h2, h3);
     if constexpr (SPLIT)
-      ptx::st_shared_v4(off + lo_off, ptx::to_tf32(x[4 * h] - h0), ptx::to_tf32(x[4 * h + 1] - h1),
-                        ptx::to_tf32(x[4 * h + 2] - h2), ptx::to_tf32(x[4 * h + 3] - h3));
+      ptx::st_shared_v4(off + lo_off, ptx::tf32_lo(x[4 * h], h0), ptx::tf32_lo(x[4 * h + 1], h1),
+                        ptx::tf32_lo(x[4 * h + 2], h2), ptx::tf32_lo(x[4 * h + 3], h3));
   }
 }
 

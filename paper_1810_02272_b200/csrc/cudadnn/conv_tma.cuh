@@ -244,11 +244,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v0 = s[src_e[0]], v1 = s[src_e[1]], v2 = s[src_e[2]], v3 = s[src_e[3]];
         if (row >= nat * CB) v0 = v1 = v2 = v3 = 0.f;  // atoms past the tile (partial tiles)
         const uint32_t off = atom32_off(uint32_t(row), uint32_t(col4 * 4));
-        const float h0 = ptx::to_tf32(v0), h1 = ptx::to_tf32(v1), h2 = ptx::to_tf32(v2), h3 = ptx::to_tf32(v3);
+        const float h0 = ptx::tf32_major<SPLIT>(v0), h1 = ptx::tf32_major<SPLIT>(v1), h2 = ptx::tf32_major<SPLIT>(v2),
+                    h3 = ptx::tf32_major<SPLIT>(v3);
         ptx::st_shared_v4(hi + off, h0, h1, h2, h3);
         if constexpr (SPLIT)
-          ptx::st_shared_v4(lo + off, ptx::to_tf32(v0 - h0), ptx::to_tf32(v1 - h1), ptx::to_tf32(v2 - h2),
-                            ptx::to_tf32(v3 - h3));
+          ptx::st_shared_v4(lo + off, ptx::tf32_lo(v0, h0), ptx::tf32_lo(v1, h1), ptx::tf32_lo(v2, h2),
+                            ptx::tf32_lo(v3, h3));
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
@@ -314,9 +315,9 @@ __global__ void repack_weights_kernel(const float* __restrict__ w, float* __rest
       if (k < Co && row < Ci) v = w[((k * Ci + row) * R + (R - 1 - kr)) * S + (S - 1 - ks)];
     }
     if (split) {
-      const float h = ptx::to_tf32(v);
+      const float h = ptx::tf32_hi(v);
       hi[i] = h;
-      lo[i] = ptx::to_tf32(v - h);
+      lo[i] = ptx::tf32_lo(v, h);
     } else {
       hi[i] = v;
     }

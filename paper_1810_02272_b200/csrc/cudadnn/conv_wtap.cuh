@@ -227,14 +227,14 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
         const uint32_t off = uint32_t(row) * 128u + (uint32_t((u ^ (row & 3)) & 3) << 5);
         float hv[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) hv[e] = ptx::to_tf32(xv[u][e]);
+        for (int e = 0; e < 8; ++e) hv[e] = ptx::tf32_major<SPLIT>(xv[u][e]);
         ptx::st_shared_v4(abase + off, hv[0], hv[1], hv[2], hv[3]);
         ptx::st_shared_v4(abase + off + 16, hv[4], hv[5], hv[6], hv[7]);
         if constexpr (SPLIT) {
-          ptx::st_shared_v4(abase + A_H + off, ptx::to_tf32(xv[u][0] - hv[0]), ptx::to_tf32(xv[u][1] - hv[1]),
-                            ptx::to_tf32(xv[u][2] - hv[2]), ptx::to_tf32(xv[u][3] - hv[3]));
-          ptx::st_shared_v4(abase + A_H + off + 16, ptx::to_tf32(xv[u][4] - hv[4]), ptx::to_tf32(xv[u][5] - hv[5]),
-                            ptx::to_tf32(xv[u][6] - hv[6]), ptx::to_tf32(xv[u][7] - hv[7]));
+          ptx::st_shared_v4(abase + A_H + off, ptx::tf32_lo(xv[u][0], hv[0]), ptx::tf32_lo(xv[u][1], hv[1]),
+                            ptx::tf32_lo(xv[u][2], hv[2]), ptx::tf32_lo(xv[u][3], hv[3]));
+          ptx::st_shared_v4(abase + A_H + off + 16, ptx::tf32_lo(xv[u][4], hv[4]), ptx::tf32_lo(xv[u][5], hv[5]),
+                            ptx::tf32_lo(xv[u][6], hv[6]), ptx::tf32_lo(xv[u][7], hv[7]));
         }
       }
     };
@@ -255,9 +255,9 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
       for (int c = 0; c < CPW; ++c) {
         const int col = cw0 + c;
         const uint32_t off = lane_off + uint32_t(col) * 128u + (uint32_t(((lane >> 2) ^ (col & 7)) & 7) << 4);
-        const float h = ptx::to_tf32(yv[c]);
+        const float h = ptx::tf32_major<SPLIT>(yv[c]);
         ptx::st_shared_f32(bbase + off, h);
-        if constexpr (SPLIT) ptx::st_shared_f32(bbase + off + uint32_t(BN) * 128u, ptx::to_tf32(yv[c] - h));
+        if constexpr (SPLIT) ptx::st_shared_f32(bbase + off + uint32_t(BN) * 128u, ptx::tf32_lo(yv[c], h));
         if (do_bias) bsum[c] += yv[c];
       }
     };

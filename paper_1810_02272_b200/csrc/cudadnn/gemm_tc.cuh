@@ -102,11 +102,12 @@ struct has_ones<V, std::void_t<decltype(V::kHasOnes)>> { static constexpr bool v
 
 template <bool SPLIT>
 __device__ __forceinline__ void store4(uint32_t hi_tile, uint32_t lo_tile, uint32_t off, float4 x) {
-  const float a = ptx::to_tf32(x.x), b = ptx::to_tf32(x.y), c = ptx::to_tf32(x.z), d = ptx::to_tf32(x.w);
+  const float a = ptx::tf32_major<SPLIT>(x.x), b = ptx::tf32_major<SPLIT>(x.y), c = ptx::tf32_major<SPLIT>(x.z),
+              d = ptx::tf32_major<SPLIT>(x.w);
   ptx::st_shared_v4(hi_tile + off, a, b, c, d);
   if constexpr (SPLIT) {
-    ptx::st_shared_v4(lo_tile + off, ptx::to_tf32(x.x - a), ptx::to_tf32(x.y - b), ptx::to_tf32(x.z - c),
-                      ptx::to_tf32(x.w - d));
+    ptx::st_shared_v4(lo_tile + off, ptx::tf32_lo(x.x, a), ptx::tf32_lo(x.y, b), ptx::tf32_lo(x.z, c),
+                      ptx::tf32_lo(x.w, d));
   }
 }
 

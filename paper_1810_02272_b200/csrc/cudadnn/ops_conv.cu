@@ -52,9 +52,9 @@ __global__ void repack_tap_kernel(const float* __restrict__ w, float* __restrict
         v = w[(((grp * Cog + k) * Cg + (row - grp * Cg)) * R + (R - 1 - kr)) * S + (S - 1 - ks)];
       }
     }
-    const float h = split ? ptx::to_tf32(v) : v;
+    const float h = split ? ptx::tf32_hi(v) : v;
     hi[i] = h;
-    if (split) lo[i] = ptx::to_tf32(v - h);
+    if (split) lo[i] = ptx::tf32_lo(v, h);
   }
 }
 

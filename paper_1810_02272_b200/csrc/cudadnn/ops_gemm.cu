@@ -89,9 +89,9 @@ __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict_
       if (c < C && r < R) {
         const float x = tile[t][threadIdx.x][threadIdx.y + 8 * i];
         if constexpr (SPLIT) {
-          const float hi = ptx::to_tf32(x);
+          const float hi = ptx::tf32_hi(x);
           out[int64_t(c) * R + r] = hi;
-          out_lo[int64_t(c) * R + r] = ptx::to_tf32(x - hi);
+          out_lo[int64_t(c) * R + r] = ptx::tf32_lo(x, hi);
         } else {
           out[int64_t(c) * R + r] = x;
         }
