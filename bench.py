@@ -100,6 +100,8 @@ def config(n_gpus: int) -> dict:
 
 
 def dtype_label() -> str:
+    if WORKLOAD == "pg_mlp":  # the fused MLP update: CUDA-core arithmetic, no tensor cores
+        return "fp64 (CUDA cores, fused MLP update)" if DTYPE == "f64" else "fp32 (CUDA cores, fused MLP update)"
     if DTYPE == "f64":
         return "fp64 (SIMT DFMA)"
     return "fp32 (3xTF32 tensor cores)" if os.environ.get("CDNN_MATH", "tf32x3") == "tf32x3" else "fp32 (TF32)"
@@ -685,7 +687,7 @@ def run_pg_b200(args) -> None:
     l0 = cx.launches()
     step(0, False)
     net.sync()
-    launches = cx.launches() - l0
+    eager_launches = cx.launches() - l0
     for i in range(args.warmup):
         step(i, False)
     net.sync()
@@ -695,7 +697,9 @@ def run_pg_b200(args) -> None:
     gs.array[...] = st[0]
     ga.array[...] = act[0]
     gr.array[...] = ret[0]
+    lg = cx.launches()
     graph = polegrad.PGStepGraph(net, solver, gs, ga, gr, BATCH, prob)
+    launches = cx.launches() - lg  # kernels per replay (1 when the update is the fused MLP kernel)
     for _ in range(args.warmup):
         graph.replay()
     net.sync()
@@ -727,8 +731,12 @@ def run_pg_b200(args) -> None:
         "metric": METRIC, "value": round(value, 1), "unit": "states/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(out["value"][0] / args.steps, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(), "data": "synthetic",
-        "config": config(1), "step": "cuda-graph (launch-bound: 0.33 MFLOP per step; the 24 KB of inputs "
-                                     "H2D and the 8 KB of probabilities D2H are inside the graph)",
+        "config": config(1),
+        "step": ("cuda-graph of ONE kernel (cdnn_mlp_pg_step: forward, softmax gradient, backward, solver) "
+                 if graph.fused else "cuda-graph of the layer-by-layer update ")
+                + "(launch-bound: 0.33 MFLOP per step; the 24 KB of inputs H2D and the 8 KB of probabilities D2H "
+                  "are inside the graph)",
+        "eager_launches_per_step": int(eager_launches),
         "e2e": {"value": round(e2e, 1), "unit": "states/s", "ms_per_step": round(out["e2e"][0] / args.steps, 5),
                 "wall_ms_per_step": round(out["e2e"][1] / args.steps, 5),
                 "h2d_bytes_per_step": int(BATCH * 4 * esz + 2 * BATCH * esz),

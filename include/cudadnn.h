@@ -383,6 +383,40 @@ CDNN_API int cdnn_pg_diff(cdnn_ctx ctx, cdnn_handle prob, cdnn_handle actions, c
 
 /* ---- solver (solver.cpp:24-57 + Caffe momentum / weight decay) ----------- */
 typedef enum { CDNN_SOLVER_SGD = 0, CDNN_SOLVER_RMSPROP = 1 } cdnn_solver_method;
+
+/* ---- fused policy-gradient update of a two-layer perceptron (ops_mlp.cu) ----
+ * The reference's pg_softmax graph (InnerProduct -> ReLU -> InnerProduct ->
+ * Softmax, proj/models/pg_softmax.prototxt) trained by the batched policy
+ * gradient (Net::pg_backward + Solver::apply_update, trainer.cpp:204-216) in one
+ * kernel: forward of `rows` states x (rows x in), logits / prob tops (rows x
+ * classes) and the optional ReLU top (rows x hidden) written, cdnn_pg_diff's
+ * softmax gradient for the first `count` rows, backward, and the
+ * cdnn_solver_apply rule on the arenas (weights, grads, history) at
+ * param_offsets = {W1 (hidden x in), b1, W2 (classes x hidden), b2}; the arena
+ * gradients are added to the batch gradient and left zero.  Deterministic; the
+ * same operations as the layered path in another summation order.
+ * cdnn_mlp_pg_supported: 1 when the extents fit the one-CTA kernel. */
+CDNN_API int cdnn_mlp_pg_supported(cdnn_ctx ctx, int dtype, int rows, int in, int hidden, int classes,
+                                   int* out);
+CDNN_API int cdnn_mlp_pg_step(cdnn_ctx ctx, cdnn_handle x, cdnn_handle actions, cdnn_handle returns,
+                              int rows, int count, int in, int hidden, int classes, cdnn_handle weights,
+                              cdnn_handle grads, cdnn_handle history, const uint64_t param_offsets[4],
+                              int solver, double lr, double momentum, double weight_decay,
+                              double rms_decay, double epsilon, cdnn_handle hidden_top,
+                              cdnn_handle logits, cdnn_handle prob, cdnn_handle stream);
+/* The same reading the states / actions / returns straight from page-locked host
+ * memory (cudaMallocHost: mapped under UVA) and writing prob to host_prob too, so a
+ * captured episode update needs no copy nodes: host_x (rows x in) is read over the
+ * bus and also stored into x (the feed blob); host_actions / host_returns (count
+ * each) replace the actions / returns buffers (pass 0 handles); any host pointer may
+ * be null (the device buffer is used). */
+CDNN_API int cdnn_mlp_pg_step_host(cdnn_ctx ctx, cdnn_handle x, cdnn_handle actions, cdnn_handle returns,
+                                   const void* host_x, const void* host_actions, const void* host_returns,
+                                   void* host_prob, int rows, int count, int in, int hidden, int classes,
+                                   cdnn_handle weights, cdnn_handle grads, cdnn_handle history,
+                                   const uint64_t param_offsets[4], int solver, double lr, double momentum,
+                                   double weight_decay, double rms_decay, double epsilon, cdnn_handle hidden_top,
+                                   cdnn_handle logits, cdnn_handle prob, cdnn_handle stream);
 /* One fused pass over n elements of (w, g, hist):
  *   SGD:      g' = g + wd*w ; v = mom*v + lr*g' ; w -= v      (hist may be 0 iff mom == 0)
  *             (mom = wd = 0 reproduces `w -= lr*g` bit for bit, solver.cpp:41-43)

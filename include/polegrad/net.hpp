@@ -111,6 +111,25 @@ class Net {
   // synchronisation, so a whole episode update can be captured and replayed.
   void pg_backward_async(const std::string& logit_blob, const std::string& prob_blob, const real* actions,
                          const real* returns, std::size_t n, bool sigmoid);
+  // The pg_softmax shape (MemoryData -> InnerProduct -> ReLU -> InnerProduct ->
+  // Softmax [-> MemoryLoss], proj/models/pg_softmax.prototxt) whose whole
+  // policy-gradient update runs as one kernel (cdnn_mlp_pg_step, Solver::apply_mlp_pg).
+  struct MlpPgPlan {
+    Blob* data = nullptr;    // feed top (rows x in)
+    Blob* hidden = nullptr;  // ReLU top (rows x hidden)
+    Blob* logits = nullptr;  // second InnerProduct top (rows x classes)
+    Blob* prob = nullptr;    // Softmax top
+    int rows = 0, in = 0, hidden_n = 0, classes = 0;
+    std::size_t params[4] = {0, 0, 0, 0};  // W1, b1, W2, b2 (indices into params())
+  };
+  // The plan when this net has that shape for (logit_blob, prob_blob) and the
+  // extents fit the fused kernel; nullopt otherwise (the layered path runs).
+  std::optional<MlpPgPlan> mlp_pg_plan(const std::string& logit_blob, const std::string& prob_blob) const;
+  // The n actions / returns of an episode into the device buffers pg_backward uses
+  // (async H2D from host memory that stays valid): the fused update's inputs.
+  void pg_stage_async(const real* actions, const real* returns, std::size_t n);
+  Handle pg_actions() const { return pg_actions_; }
+  Handle pg_returns() const { return pg_returns_; }
   // Zero every parameter gradient on the device (one fill over the grad arena).
   void zero_param_diffs();
   // Stream of the parameter-gradient halves of the two-stream backward (0 until used).

@@ -42,6 +42,18 @@ class Solver {
   // Every parameter diff is zero afterwards.
   void apply_update(Net& net);
 
+  // The whole policy-gradient update of the net's pg_softmax MLP (Net::mlp_pg_plan)
+  // as one kernel: forward of the staged feed, the softmax gradient of the first
+  // `count` rows at the logits with the actions / returns staged by
+  // Net::pg_stage_async, backward and this solver's rule; every parameter diff is
+  // zero afterwards, like apply_update.  Not with a Parallel attached.
+  // With host pointers (page-locked, mapped) the kernel reads the states / actions /
+  // returns over the bus (the states also land in the feed blob) and writes the
+  // probabilities to host_prob: a captured update with no copy nodes.
+  void apply_mlp_pg(Net& net, const Net::MlpPgPlan& plan, std::size_t count, const real* host_states = nullptr,
+                    const real* host_actions = nullptr, const real* host_returns = nullptr,
+                    real* host_prob = nullptr);
+  bool has_parallel() const { return parallel_ != nullptr; }
   // Data-parallel training: all-reduce gradients through `parallel` before
   // each update (nullptr detaches).
   void set_parallel(Parallel* parallel) { parallel_ = parallel; }

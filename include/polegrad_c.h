@@ -119,6 +119,16 @@ PG_API int pg_step_replay(pg_net* net, uint64_t graph);
 PG_API int pg_pg_step_capture(pg_net* net, pg_solver* s, const void* states, const void* actions,
                               const void* returns, uint64_t n, const char* logit_blob, const char* prob_blob,
                               int sigmoid, void* prob_out, uint64_t* graph);
+/* flags: PG_STEP_LAYERED captures the layer-by-layer update even when the net is the
+ * pg_softmax MLP; by default such a net's update is ONE kernel (cdnn_mlp_pg_step:
+ * forward, softmax gradient, backward and the solver rule; the ReLU / logits / prob
+ * tops are written, the data gradient is not).  pg_pg_step_fused reports which. */
+#define PG_STEP_LAYERED 1
+PG_API int pg_pg_step_capture_ex(pg_net* net, pg_solver* s, const void* states, const void* actions,
+                                 const void* returns, uint64_t n, const char* logit_blob, const char* prob_blob,
+                                 int sigmoid, int flags, void* prob_out, uint64_t* graph);
+PG_API int pg_pg_step_fused(pg_net* net, pg_solver* s, const char* logit_blob, const char* prob_blob, int sigmoid,
+                            int flags, int* out);
 /* data == NULL: no feed copy, the batch already resident in the data blob is reused */
 /* one eager forward+backward with events between layers (per-layer ms, layer order) */
 PG_API int pg_net_profile(pg_net* net, float* fwd_ms, float* bwd_ms, int cap);

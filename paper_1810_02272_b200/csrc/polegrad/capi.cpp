@@ -345,23 +345,61 @@ int pg_step_capture(pg_net* n, pg_solver* s, const void* data, const void* label
   });
 }
 
+namespace {
+// the fused one-kernel update applies (PG_STEP_LAYERED not set, softmax head, no Parallel)
+std::optional<polegrad::Net::MlpPgPlan> fused_plan(polegrad::Net& net, pg_solver* s, const char* logit_blob,
+                                                   const char* prob_blob, int sigmoid, int flags) {
+  if ((flags & PG_STEP_LAYERED) || sigmoid || s->solver->has_parallel()) return std::nullopt;
+  return net.mlp_pg_plan(logit_blob, prob_blob);
+}
+}  // namespace
+
+int pg_pg_step_fused(pg_net* n, pg_solver* s, const char* logit_blob, const char* prob_blob, int sigmoid,
+                     int flags, int* out) {
+  return run([&] {
+    if (!out) throw polegrad::InvalidArgument("pg_pg_step_fused: null out");
+    *out = fused_plan(net_of(n), s, logit_blob, prob_blob, sigmoid, flags).has_value() ? 1 : 0;
+  });
+}
+
 int pg_pg_step_capture(pg_net* n, pg_solver* s, const void* states, const void* actions, const void* returns,
                        uint64_t count, const char* logit_blob, const char* prob_blob, int sigmoid, void* prob_out,
                        uint64_t* graph) {
+  return pg_pg_step_capture_ex(n, s, states, actions, returns, count, logit_blob, prob_blob, sigmoid, 0, prob_out,
+                               graph);
+}
+
+int pg_pg_step_capture_ex(pg_net* n, pg_solver* s, const void* states, const void* actions, const void* returns,
+                          uint64_t count, const char* logit_blob, const char* prob_blob, int sigmoid, int flags,
+                          void* prob_out, uint64_t* graph) {
   return run([&] {
     polegrad::Net& net = net_of(n);
     polegrad::Registry& reg = *net.registry();
     if (!states || !actions || !returns) throw polegrad::InvalidArgument("pg step capture: null input buffer");
+    const auto plan = fused_plan(net, s, logit_blob, prob_blob, sigmoid, flags);
+    if (plan) {  // the history and the action / return buffers exist before the capture
+      s->solver->prepare(net);
+      net.pg_stage_async(nullptr, nullptr, 0);
+    }
     // one eager update first: lazily allocated buffers must exist before the capture
     reg.synchronize();
     cdnn_ok(cdnn_graph_begin(reg.context(), reg.stream()), "pg step capture");
     try {
-      net.set_batch(static_cast<const real*>(states), nullptr);
-      net.forward();
-      net.pg_backward_async(logit_blob, prob_blob, static_cast<const real*>(actions),
-                            static_cast<const real*>(returns), count, sigmoid != 0);
-      s->solver->apply_update(net);
-      if (prob_out) {
+      if (plan) {
+        // ONE kernel node: states / actions / returns read from the page-locked host
+        // buffers, forward, softmax gradient at the logits, backward, solver rule,
+        // probabilities written to prob_out (no copy nodes)
+        s->solver->apply_mlp_pg(net, *plan, count, static_cast<const real*>(states),
+                                static_cast<const real*>(actions), static_cast<const real*>(returns),
+                                static_cast<real*>(prob_out));
+      } else {
+        net.set_batch(static_cast<const real*>(states), nullptr);
+        net.forward();
+        net.pg_backward_async(logit_blob, prob_blob, static_cast<const real*>(actions),
+                              static_cast<const real*>(returns), count, sigmoid != 0);
+        s->solver->apply_update(net);
+      }
+      if (prob_out && !plan) {
         polegrad::Blob& prob = net.blob(prob_blob);
         cdnn_ok(cdnn_read_async(reg.context(), prob.gpu_data(), 0, prob_out, prob.count(), reg.stream()),
                 "pg step capture");

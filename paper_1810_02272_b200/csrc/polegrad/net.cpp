@@ -474,6 +474,74 @@ void Net::pg_backward_async(const std::string& logit_blob, const std::string& pr
   backward_from(logit_blob);
 }
 
+std::optional<Net::MlpPgPlan> Net::mlp_pg_plan(const std::string& logit_blob, const std::string& prob_blob) const {
+  // exactly: MemoryData, InnerProduct, ReLU, InnerProduct, Softmax [, MemoryLoss(prob)]
+  const std::size_t nl = layers_.size();
+  if (nl != 5 && nl != 6) return std::nullopt;
+  const LayerType want[6] = {LayerType::kMemoryData, LayerType::kInnerProduct, LayerType::kRelu,
+                             LayerType::kInnerProduct, LayerType::kSoftmax, LayerType::kMemoryLoss};
+  for (std::size_t i = 0; i < nl; ++i)
+    if (layers_[i]->type() != want[i]) return std::nullopt;
+  auto one = [&](const std::vector<Blob*>& v) { return v.size() == 1 ? v[0] : nullptr; };
+  if (tops_[0].empty()) return std::nullopt;
+  Blob* data = tops_[0][0];
+  Blob* ip1 = one(tops_[1]);
+  Blob* relu = one(tops_[2]);
+  Blob* logits = one(tops_[3]);
+  Blob* prob = one(tops_[4]);
+  if (!ip1 || !relu || !logits || !prob) return std::nullopt;
+  if (one(bottoms_[1]) != data || one(bottoms_[2]) != ip1 || one(bottoms_[3]) != relu || one(bottoms_[4]) != logits)
+    return std::nullopt;
+  if (nl == 6) {
+    if (one(bottoms_[5]) != prob) return std::nullopt;
+    const auto* loss = static_cast<const MemoryLossLayer*>(layers_[5].get());
+    if (loss->has_loss_hook()) return std::nullopt;  // host-side gradient: not this update
+  }
+  if (logits->name() != logit_blob || prob->name() != prob_blob) return std::nullopt;
+  MlpPgPlan p;
+  p.data = data;
+  p.hidden = relu;
+  p.logits = logits;
+  p.prob = prob;
+  p.rows = data->shape().n();
+  if (p.rows < 1) return std::nullopt;
+  p.in = int(data->count() / std::size_t(p.rows));
+  p.hidden_n = int(ip1->count() / std::size_t(p.rows));
+  p.classes = int(logits->count() / std::size_t(p.rows));
+  const std::size_t b1 = first_param_of_layer(1), b3 = first_param_of_layer(3);
+  if (layers_[1]->params().size() != 2 || layers_[3]->params().size() != 2) return std::nullopt;
+  p.params[0] = b1;
+  p.params[1] = b1 + 1;
+  p.params[2] = b3;
+  p.params[3] = b3 + 1;
+  if (params_[p.params[0]]->count() != std::size_t(p.hidden_n) * std::size_t(p.in) ||
+      params_[p.params[2]]->count() != std::size_t(p.classes) * std::size_t(p.hidden_n))
+    return std::nullopt;
+  int ok = 0;
+  cdnn_ok(cdnn_mlp_pg_supported(registry_->context(), sizeof(real) == 4 ? CDNN_F32 : CDNN_F64, p.rows, p.in,
+                                p.hidden_n, p.classes, &ok),
+          "mlp_pg_plan");
+  if (!ok) return std::nullopt;
+  return p;
+}
+
+void Net::pg_stage_async(const real* actions, const real* returns, std::size_t n) {
+  Registry& reg = *registry_;
+  const MemoryDataLayer* feed = nullptr;
+  for (const auto& l : layers_)
+    if (auto* md = dynamic_cast<const MemoryDataLayer*>(l.get())) { feed = md; break; }
+  const std::size_t rows = feed ? std::size_t(feed->batch_size()) : n;
+  if (n > rows) throw InvalidArgument("pg_stage: " + std::to_string(n) + " steps exceed the batch of " + std::to_string(rows));
+  if (!pg_actions_) {
+    pg_actions_ = reg.alloc_buffer(std::max<std::size_t>(rows, 1));
+    pg_returns_ = reg.alloc_buffer(std::max<std::size_t>(rows, 1));
+  }
+  if (n) {
+    cdnn_ok(cdnn_write_async(reg.context(), reg.in(pg_actions_), 0, actions, n, reg.stream()), "pg_stage");
+    cdnn_ok(cdnn_write_async(reg.context(), reg.in(pg_returns_), 0, returns, n, reg.stream()), "pg_stage");
+  }
+}
+
 void Net::zero_param_diffs() {
   if (!param_total_) return;
   Registry& reg = *registry_;

@@ -85,6 +85,45 @@ void Solver::apply_update(Net& net) {
   ++iterations_;
 }
 
+void Solver::apply_mlp_pg(Net& net, const Net::MlpPgPlan& plan, std::size_t count, const real* host_states,
+                          const real* host_actions, const real* host_returns, real* host_prob) {
+  if (parallel_) throw InvalidState("apply_mlp_pg: the fused update does not all-reduce (detach the Parallel)");
+  if (count > std::size_t(plan.rows)) throw InvalidArgument("apply_mlp_pg: count exceeds the batch");
+  if ((host_actions == nullptr) != (host_returns == nullptr))
+    throw InvalidArgument("apply_mlp_pg: actions and returns come from the same side");
+  if (!host_actions && !net.pg_actions())
+    throw InvalidState("apply_mlp_pg: stage the actions / returns first (Net::pg_stage_async)");
+  Registry& reg = *net.registry();
+  const bool stateful = config_.method == SolverMethod::kRmsProp || config_.momentum != real(0);
+  prepare(net);
+  const auto& params = net.params();
+  for (Blob* p : params) {
+    p->gpu_data();
+    p->gpu_diff();
+  }
+  const std::uint64_t offs[4] = {net.param_offset(plan.params[0]), net.param_offset(plan.params[1]),
+                                 net.param_offset(plan.params[2]), net.param_offset(plan.params[3])};
+  const auto& c = config_;
+  // host states: the kernel fills the feed blob; device states: it reads the staged batch
+  cdnn_handle x = host_states ? plan.data->overwrite_gpu_data() : plan.data->gpu_data();
+  cdnn_handle act = host_actions ? 0 : reg.in(net.pg_actions());
+  cdnn_handle ret = host_returns ? 0 : reg.in(net.pg_returns());
+  cdnn_ok(cdnn_mlp_pg_step_host(reg.context(), x, act, ret, host_states, host_actions, host_returns, host_prob,
+                           plan.rows, int(count), plan.in, plan.hidden_n, plan.classes, reg.inout(net.weight_arena()),
+                           reg.inout(net.grad_arena()), stateful ? reg.inout(history_) : 0, offs,
+                           c.method == SolverMethod::kRmsProp ? CDNN_SOLVER_RMSPROP : CDNN_SOLVER_SGD,
+                           static_cast<double>(c.learning_rate), static_cast<double>(c.momentum),
+                           static_cast<double>(c.weight_decay), static_cast<double>(c.rms_decay),
+                           static_cast<double>(c.epsilon), plan.hidden->overwrite_gpu_data(),
+                           plan.logits->overwrite_gpu_data(), plan.prob->overwrite_gpu_data(), reg.stream()),
+          "apply_mlp_pg");
+  for (Blob* p : params) {
+    p->overwrite_gpu_data();
+    p->overwrite_gpu_diff();
+  }
+  ++iterations_;
+}
+
 std::vector<std::uint8_t> Solver::snapshot_state() const {
   std::vector<std::uint8_t> out{'M', 'C', 'S', 'S'};
   auto put = [&](std::uint64_t v, int bytes) {

@@ -50,7 +50,7 @@ EXPORTS = [
     "cdnn_broadcast", "cdnn_copy_range", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_lrn_backward_ex", "cdnn_dropout", "cdnn_counter_increment",
     "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
     "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
-    "cdnn_pool_forward_ex", "cdnn_pg_diff",
+    "cdnn_pool_forward_ex", "cdnn_pg_diff", "cdnn_mlp_pg_supported", "cdnn_mlp_pg_step", "cdnn_mlp_pg_step_host",
 ]
 
 
@@ -149,6 +149,11 @@ def load() -> C.CDLL:
             "cdnn_scale_backward": ([vp, h, h, h, h, h, h, i, i, i, h], i),
             "cdnn_axpby": ([vp, u64, d, h, d, h, i, h], i),
             "cdnn_pg_diff": ([vp, h, h, h, h, i, i, i, i, h], i),
+            "cdnn_mlp_pg_supported": ([vp, i, i, i, i, i, C.POINTER(C.c_int)], i),
+            "cdnn_mlp_pg_step": ([vp, h, h, h, i, i, i, i, i, h, h, h, C.POINTER(C.c_uint64), i, d, d, d, d, d,
+                                  h, h, h, h], i),
+            "cdnn_mlp_pg_step_host": ([vp, h, h, h, vp, vp, vp, vp, i, i, i, i, i, h, h, h, C.POINTER(C.c_uint64), i,
+                                       d, d, d, d, d, h, h, h, h], i),
             "cdnn_batchnorm_scale_forward": ([vp, h, h, h, h, h, h, h, i, i, i, d, h], i),
             "cdnn_batchnorm_scale_backward": ([vp, h, h, h, h, h, h, h, h, i, i, i, h], i),
         }

@@ -37,6 +37,7 @@ EXPORTS = [
     "pg_feed_ring_pop_loss", "pg_net_pg_backward", "pg_feed_ring_push_sampled", "pg_imagedb_load",
     "pg_imagedb_free", "pg_imagedb_size", "pg_imagedb_set_boost", "pg_imagedb_sample", "pg_rng_create",
     "pg_rng_free", "pg_parallel_create_host", "pg_parallel_info", "pg_pg_step_capture",
+    "pg_pg_step_capture_ex", "pg_pg_step_fused",
 ]
 
 # int transport(void* user, int op, void* host, uint64_t offset, uint64_t n)
@@ -79,6 +80,8 @@ def load(dtype: str = "f32") -> C.CDLL:
             "pg_feed_ring_push_pinned": ([vp, vp, u64, vp, u64], i), "pg_feed_ring_pop_loss": ([vp, C.POINTER(d)], i),
             "pg_step_capture": ([vp, vp, vp, vp, vp, C.POINTER(u64)], i), "pg_step_replay": ([vp, u64], i),
             "pg_pg_step_capture": ([vp, vp, vp, vp, vp, u64, cp, cp, i, vp, C.POINTER(u64)], i),
+            "pg_pg_step_capture_ex": ([vp, vp, vp, vp, vp, u64, cp, cp, i, i, vp, C.POINTER(u64)], i),
+            "pg_pg_step_fused": ([vp, vp, cp, cp, i, i, C.POINTER(C.c_int)], i),
             "pg_graph_free": ([vp, u64], i), "pg_parallel_unique_id": ([cp], i),
             "pg_net_profile": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
             "pg_parallel_create": ([vp, i, i, cp, u64, C.POINTER(vp)], i), "pg_parallel_free": ([vp], i),
@@ -353,18 +356,29 @@ class PGStepGraph:
     states -> forward -> device-side modulated log-prob gradients of `n` steps ->
     backward_from(logits) -> update -> probabilities to `prob`.  The buffers are
     cudadnn.PinnedBuffer of the net's real type; write the next episode into them and
-    replay().  Capture after at least one eager update (lazy device buffers)."""
+    replay().  Capture after at least one eager update (lazy device buffers).
+
+    fused=True (default): when the net is the pg_softmax MLP (InnerProduct -> ReLU ->
+    InnerProduct -> Softmax) the update is one kernel (cdnn_mlp_pg_step) instead of
+    the layer-by-layer launches; `self.fused` says which was captured."""
+
+    LAYERED = 1  # PG_STEP_LAYERED
 
     def __init__(self, net: Net, solver: "Solver", states, actions, returns, n: int, prob=None,
-                 logit: str = "logits", prob_blob: str = "prob", sigmoid: bool = False):
+                 logit: str = "logits", prob_blob: str = "prob", sigmoid: bool = False, fused: bool = True):
         self.net = net
         self._keep = (solver, states, actions, returns, prob)
+        flags = 0 if fused else self.LAYERED
+        ok = C.c_int(0)
+        _check(net.lib, net.lib.pg_pg_step_fused(net.ptr, solver.ptr, logit.encode(), prob_blob.encode(),
+                                                 int(sigmoid), flags, C.byref(ok)))
+        self.fused = bool(ok.value)
         g = C.c_uint64()
-        _check(net.lib, net.lib.pg_pg_step_capture(net.ptr, solver.ptr, C.c_void_p(states.ptr),
-                                                   C.c_void_p(actions.ptr), C.c_void_p(returns.ptr), n,
-                                                   logit.encode(), prob_blob.encode(), int(sigmoid),
-                                                   C.c_void_p(prob.ptr) if prob is not None else None,
-                                                   C.byref(g)))
+        _check(net.lib, net.lib.pg_pg_step_capture_ex(net.ptr, solver.ptr, C.c_void_p(states.ptr),
+                                                      C.c_void_p(actions.ptr), C.c_void_p(returns.ptr), n,
+                                                      logit.encode(), prob_blob.encode(), int(sigmoid), flags,
+                                                      C.c_void_p(prob.ptr) if prob is not None else None,
+                                                      C.byref(g)))
         self.graph = g.value
 
     def replay(self) -> None:

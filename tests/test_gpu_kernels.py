@@ -540,3 +540,77 @@ def test_conv_backward_filter_reuses_forward_input_rewrite(ctx):
     assert not np.array_equal(outs[0][0], outs[2][0])
     for hnd in (hx, hx2, hw, hdy, hy):
         ctx.free(hnd)
+
+
+def _mlp_reference(X, act, ret, count, W1, b1, W2, b2):
+    """fp64 restatement of the pg_softmax update's gradient (layers.cpp InnerProduct /
+    ReLU / Softmax, trainer.cpp:42-113 softmax gradient, summed over the batch)."""
+    pre = X @ W1.T + b1
+    a = np.maximum(pre, 0)
+    l = a @ W2.T + b2
+    e = np.exp(l - l.max(1, keepdims=True))
+    p = e / e.sum(1, keepdims=True)
+    dl = np.zeros_like(p)
+    dl[:count] = p[:count]
+    dl[np.arange(count), act[:count].astype(int)] -= 1
+    dl[:count] *= ret[:count, None]
+    dh = (dl @ W2) * (pre > 0)
+    return l, p, a, dh.T @ X, dh.sum(0), dl.T @ a, dl.sum(0)
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("rows,count,dims", [(1024, 1024, (4, 10, 2)), (300, 211, (4, 10, 2)),
+                                             (777, 500, (7, 33, 3)), (64, 64, (16, 20, 5))])
+def test_mlp_pg_step_device_buffers(ctx, dtype, rows, count, dims):
+    """cdnn_mlp_pg_step from device buffers (the fp32 4-10-2 register kernel and the
+    shared-memory kernel for other extents / fp64): tops, and the SGD update
+    (momentum, weight decay, pre-existing arena gradient added) against fp64."""
+    i, h, c = dims
+    rng = np.random.default_rng(rows + i)
+    dt = NP[dtype]
+    X = rng.uniform(-1, 1, (rows, i))
+    act = np.floor(rng.uniform(0, c, rows))
+    ret = rng.standard_normal(rows)
+    W1, b1 = rng.uniform(-0.5, 0.5, (h, i)), rng.uniform(-0.1, 0.1, h)
+    W2, b2 = rng.uniform(-0.5, 0.5, (c, h)), rng.uniform(-0.1, 0.1, c)
+    sizes = [W1.size, b1.size, W2.size, b2.size]
+    offs = np.cumsum([0] + sizes[:-1]).astype(np.uint64) + 3  # arbitrary arena placement
+    total = int(offs[-1]) + sizes[-1] + 5
+    w = np.zeros(total)
+    for o, v in zip(offs, (W1, b1, W2, b2)):
+        w[int(o):int(o) + v.size] = v.ravel()
+    g0 = rng.uniform(-1e-2, 1e-2, total)
+    h0 = rng.uniform(-1e-2, 1e-2, total)
+    lr, mom, wd = 1e-2, 0.9, 1e-3
+    hx, ha, hr = ctx.upload(X.astype(dt)), ctx.upload(act.astype(dt)), ctx.upload(ret.astype(dt))
+    hw, hg, hh = ctx.upload(w.astype(dt)), ctx.upload(g0.astype(dt)), ctx.upload(h0.astype(dt))
+    hl, hp, hhid = ctx.alloc(rows * c, dtype), ctx.alloc(rows * c, dtype), ctx.alloc(rows * h, dtype)
+    Xq, Wq = X.astype(dt).astype(np.float64), w.astype(dt).astype(np.float64)
+    W1q, b1q, W2q, b2q = (Wq[int(o):int(o) + n].reshape(v.shape) for o, n, v in zip(offs, sizes, (W1, b1, W2, b2)))
+    ok = C.c_int(0)
+    ctx.call("cdnn_mlp_pg_supported", dtype, rows, i, h, c, C.byref(ok))
+    assert ok.value == 1
+    ctx.call("cdnn_mlp_pg_step", hx, ha, hr, rows, count, i, h, c, hw, hg, hh, (C.c_uint64 * 4)(*offs), 0,
+             lr, mom, wd, 0.99, 1e-8, hhid, hl, hp, 0)
+    l, p, a, gW1, gb1, gW2, gb2 = _mlp_reference(Xq, act, ret.astype(dt).astype(np.float64), count, W1q, b1q, W2q, b2q)
+    tol = 1e-12 if dtype == cd.F64 else 2e-5
+    assert rel_l2(ctx.read(hl).reshape(rows, c), l) <= tol
+    assert rel_l2(ctx.read(hp).reshape(rows, c), p) <= tol
+    assert rel_l2(ctx.read(hhid).reshape(rows, h), a) <= tol
+    g = g0.astype(dt).astype(np.float64).copy()
+    for o, v in zip(offs, (gW1, gb1, gW2, gb2)):
+        g[int(o):int(o) + v.size] += v.ravel()
+    hist_in = h0.astype(dt).astype(np.float64)
+    step = mom * hist_in + lr * (g + wd * Wq)
+    touched = np.zeros(total, bool)
+    for o, n in zip(offs, sizes):
+        touched[int(o):int(o) + n] = True
+    w_new, g_new, h_new = ctx.read(hw), ctx.read(hg), ctx.read(hh)
+    assert rel_l2(w_new[touched], (Wq - step)[touched]) <= tol
+    assert rel_l2(h_new[touched], step[touched]) <= max(tol, 1e-4 if dtype == cd.F32 else tol)
+    assert not np.any(g_new[touched])
+    # elements outside the four parameters are untouched
+    assert np.array_equal(w_new[~touched], w.astype(dt)[~touched])
+    assert np.array_equal(g_new[~touched], g0.astype(dt)[~touched])
+    for hd in (hx, ha, hr, hw, hg, hh, hl, hp, hhid):
+        ctx.free(hd)
