@@ -144,12 +144,13 @@ __device__ __forceinline__ float to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// 3xTF32 operand split, x = hi + lo: hi is x with the 13 low mantissa bits cleared
-// (exact tf32; NaN / Inf stay in hi), lo the exact fp32 residual x - hi
-// (|lo| < 2^-10 |x|) rounded to the nearest tf32 by an integer add, so x - hi - lo
-// is within 2^-21 |x|.  Four integer / fp32 ops per element, where two
-// cvt.rna.tf32.f32 (emulated on sm_100: range checks + rounding) cost about ten.
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// 3xTF32 operand split, x = hi + lo: hi = x rounded to the nearest tf32
+// (cvt.rna: NaN / Inf stay in hi), lo = the exact fp32 residual x - hi
+// (|lo| <= 2^-11 |x|) rounded to the nearest tf32 by an integer add, so
+// x - hi - lo is within 2^-23 |x| -- the same split as two cvt.rna, with the
+// second (emulated on sm_100: range checks + rounding) replaced by two integer ops
+// (lo is finite whenever x is; for a non-finite x the product is carried by hi).
+__device__ __forceinline__ float tf32_hi(float x) { return to_tf32(x); }
 __device__ __forceinline__ float tf32_lo(float x, float hi) {
   return __uint_as_float((__float_as_uint(x - hi) + 0x1000u) & 0xFFFFE000u);
 }
