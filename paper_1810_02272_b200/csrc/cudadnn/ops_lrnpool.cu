@@ -33,6 +33,13 @@ namespace {
 constexpr int kG = 4;     // channels per step (loads in flight; one block barrier per step)
 constexpr int kSeg = 32;  // channels per thread / block segment (segments run in parallel)
 
+// a pointer the optimiser cannot see through (keeps base + 32-bit offset addressing)
+template <class P>
+__device__ __forceinline__ P* opaque(P* p) {
+  asm("" : "+l"(p));
+  return p;
+}
+
 struct LrnPoolGeom {
   int N, C, H, W, PH, PW;
   int TR, rows_in;  // pooled rows per band, input rows per band
@@ -62,8 +69,8 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
   const bool active = p < npix;
   const int h = r0 + (active ? p / g.W : 0);
   const size_t base = size_t(img) * g.C * HW + size_t(h) * g.W + (active ? p % g.W : 0);
-  const T* xp = x + base;
-  T* yp = ynorm + base;
+  const T* xp = opaque(x + base);
+  T* yp = opaque(ynorm + base);
   const bool own = active && h < own1;
   T xr[SIZE];  // x(c - pre .. c + post)
 #pragma unroll
@@ -81,6 +88,29 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
   T nxt[kG];
   load_step(cs0, nxt);
   const int prows = pr1 - pr0;
+  // the thread's first pool item (channel u0 of the step, pooled row / column) is the
+  // same every step: its window origin, output offset and bounds are computed once
+  // (two integer divisions per step and item otherwise; items beyond blockDim, if
+  // any, take the general loop below)
+  const int per_u = prows * g.PW;
+  const int it0 = threadIdx.x;
+  const bool has0 = it0 < kG * per_u;
+  int u0 = 0, toff0 = 0, po0 = 0, abase0 = 0;
+  uint32_t wbits0 = 0;
+  if (has0) {
+    u0 = it0 / per_u;
+    const int rem = it0 - u0 * per_u;
+    const int prl = rem / g.PW, pw = rem - prl * g.PW;
+    const int hs = (pr0 + prl) * S, ws = pw * S;
+    toff0 = u0 * tsz + (hs - r0) * g.W + ws;
+    po0 = (pr0 + prl) * g.PW + pw;
+    abase0 = hs * g.W + ws;
+#pragma unroll
+    for (int a = 0; a < K; ++a)
+#pragma unroll
+      for (int b = 0; b < K; ++b)
+        if (hs + a < g.H && ws + b < g.W) wbits0 |= 1u << (a * K + b);
+  }
   for (int c0 = cs0, step = 0; c0 < cs1; c0 += kG, ++step) {
     T cur[kG];
 #pragma unroll
@@ -105,8 +135,26 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
       }
     }
     __syncthreads();
-    const int items = min(kG, cs1 - c0) * prows * g.PW;
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int nu = min(kG, cs1 - c0);
+    if (has0 && u0 < nu) {
+      const T* t = buf + toff0;
+      T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
+      int arg = -1;
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          if (wbits0 & (1u << (a * K + b))) {
+            const T v = t[a * g.W + b];
+            if (v > best) { best = v; arg = abase0 + a * g.W + b; }
+          }
+        }
+      const uint32_t o = (uint32_t(img) * g.C + c0 + u0) * uint32_t(PHW) + uint32_t(po0);
+      ypool[o] = relu ? (best > T(0) ? best : T(0)) : best;
+      mask[o] = arg;
+    }
+    const int items = nu * per_u;
+    for (int it = threadIdx.x + blockDim.x; it < items; it += blockDim.x) {
       const int u = it / (prows * g.PW);
       const int rem = it - u * (prows * g.PW);
       const int prl = rem / g.PW, pw = rem - prl * g.PW;
@@ -154,31 +202,38 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
     const int h = int(hw) / g.W, w = int(hw) - h * g.W;
     const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
     const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
-    const T* xp = x + size_t(img) * g.C * HW + hw;
-    T* dxp = dx + size_t(img) * g.C * HW + hw;
-    const int* mp = mask + size_t(img) * g.C * PHW;
-    const T* dp = pdy + size_t(img) * g.C * PHW;
-    uint32_t woff[R][R];
+    // opaque per-image base pointers: element offsets are then one IMAD.WIDE each
+    // (otherwise the compiler re-associates the 64-bit image offset into every
+    // address: ~6 integer ops per load)
+    const T* xp = opaque(x + size_t(img) * g.C * HW + hw);
+    T* dxp = opaque(dx + size_t(img) * g.C * HW + hw);
+    const int* mp = opaque(mask + size_t(img) * g.C * PHW);
+    const T* dp = opaque(pdy + size_t(img) * g.C * PHW);
+    // the pixel's <= R x R pooling windows: rows phs.., columns pws.. of the pooled
+    // plane, i.e. element offsets woff0 + a*PW + b (one base pointer per window row,
+    // the column step an immediate offset)
     bool wok[R][R];
 #pragma unroll
     for (int a = 0; a < R; ++a)
 #pragma unroll
-      for (int b = 0; b < R; ++b) {
-        wok[a][b] = phs + a < phe && pws + b < pwe;
-        woff[a][b] = uint32_t((phs + a) * g.PW + pws + b);
-      }
+      for (int b = 0; b < R; ++b) wok[a][b] = phs + a < phe && pws + b < pwe;
+    const uint32_t woff0 = uint32_t(phs * g.PW + pws);
     auto xat = [&](int cc) { return (cc >= 0 && cc < g.C) ? __ldg(xp + uint32_t(cc) * HW) : T(0); };
     // the LRN top diff of channel cc at this pixel: max_pool_bwd_k's gather, in its order
     auto gather = [&](int cc, int (&m)[R][R], T (&v)[R][R]) {
-      const uint32_t co = uint32_t(cc) * PHW;
+      const bool live = cc < g.C;
+      const uint32_t o0 = (live ? uint32_t(cc) : 0u) * PHW + woff0;
 #pragma unroll
-      for (int a = 0; a < R; ++a)
+      for (int a = 0; a < R; ++a) {
+        const int* mr = mp + (o0 + uint32_t(a * g.PW));
+        const T* dr = dp + (o0 + uint32_t(a * g.PW));
 #pragma unroll
         for (int b = 0; b < R; ++b) {
-          const bool ok = cc < g.C && wok[a][b];
-          m[a][b] = ok ? __ldg(mp + co + woff[a][b]) : -1;
-          v[a][b] = ok ? __ldg(dp + co + woff[a][b]) : T(0);
+          const bool ok = live && wok[a][b];
+          m[a][b] = ok ? __ldg(mr + b) : -1;
+          v[a][b] = ok ? __ldg(dr + b) : T(0);
         }
+      }
     };
     auto ndy_of = [&](const int (&m)[R][R], const T (&v)[R][R]) {
       T sdy = T(0);
