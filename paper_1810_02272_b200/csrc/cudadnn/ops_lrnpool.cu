@@ -31,7 +31,14 @@ namespace cdnn {
 namespace {
 
 constexpr int kG = 4;     // channels per step (loads in flight; one block barrier per step)
-constexpr int kSeg = 32;  // channels per thread / block segment (segments run in parallel)
+#ifndef CDNN_LRN_FWD_SEG
+#define CDNN_LRN_FWD_SEG 128
+#endif
+constexpr int kSeg = CDNN_LRN_FWD_SEG;  // forward: channels per block segment (segments run in parallel)
+#ifndef CDNN_LRN_BWD_SEG
+#define CDNN_LRN_BWD_SEG 128
+#endif
+constexpr int kSegB = CDNN_LRN_BWD_SEG;  // backward: channels per thread (each segment re-primes SIZE-1 channels)
 
 // a pointer the optimiser cannot see through (keeps base + 32-bit offset addressing)
 template <class P>
@@ -190,14 +197,15 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
   constexpr int R = (K + S - 1) / S;
   const uint32_t HW = uint32_t(g.H * g.W), PHW = uint32_t(g.PH * g.PW);
   const uint32_t pixels = uint32_t(g.N) * HW;
-  const uint32_t work = pixels * uint32_t(g.segs);
+  const uint32_t segs = uint32_t((g.C + kSegB - 1) / kSegB);
+  const uint32_t work = pixels * segs;
   const T aN = alpha / T(SIZE);
   const T coef = T(2) * alpha * beta / T(SIZE);
   for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < work; wi += gridDim.x * blockDim.x) {
     // consecutive threads: consecutive pixels of one segment (coalesced)
     const uint32_t seg = wi / pixels;
     const uint32_t pix = wi - seg * pixels;
-    const int cs0 = int(seg) * kSeg, cs1 = min(g.C, cs0 + kSeg);
+    const int cs0 = int(seg) * kSegB, cs1 = min(g.C, cs0 + kSegB);
     const uint32_t img = pix / HW, hw = pix - img * HW;
     const int h = int(hw) / g.W, w = int(hw) - h * g.W;
     const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
@@ -378,7 +386,7 @@ template <typename T, int SIZE, int K, int S>
 void launch_bwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, const T* pdy, const int* m, T* dx,
                 double alpha, double beta, double k, bool gate_x) {
   const LrnPoolGeom g = lrn_pool_geom(d, 1024);
-  const int64_t work = int64_t(g.N) * g.H * g.W * g.segs;
+  const int64_t work = int64_t(g.N) * g.H * g.W * ((g.C + kSegB - 1) / kSegB);
   lrn_maxpool_bwd<T, SIZE, K, S><<<grid_for(work, 256), 256, 0, st>>>(x, pdy, m, dx, g, T(alpha), T(beta), T(k),
                                                                        gate_x);
   check_launch("lrn_maxpool_bwd");
