@@ -92,7 +92,14 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
 
 // KC: virtual pixels per pipeline chunk (64, or 32 with up to four stages when one CTA
 // owns the SM: smaller stages, a deeper pipeline)
-template <int BN, bool SPLIT, int KC>
+// CL: CTAs per thread-block cluster along the 32-channel blocks.  They share the
+// chunk sequence and the output-channel block, so their B operand (the dY chunk) is
+// identical: each CTA stages 1/CL of its output channels and writes them into every
+// CTA's buffer (distributed shared memory), arriving on every CTA's `full` barrier;
+// each MMA warp's commit arrives on every CTA's `empty` barrier (multicast), so a
+// buffer is refilled only when all CL tensor cores have consumed it.  The dY loads,
+// conversions and index math per CTA drop by CL.
+template <int BN, bool SPLIT, int KC, int CL = 1>
 __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(const WtapArgs a) {
   constexpr int TM = 128;
   const int item = blockIdx.y;
@@ -104,7 +111,10 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
   const int n0 = cob * BN;
   const int z = blockIdx.x;
   const int ch0 = z * a.chunks_per_split, ch1 = min(a.nchunks, ch0 + a.chunks_per_split);
-  const bool do_bias = a.want_bias && cb == 0 && gg == 0;
+  // bias partials: the first cluster of channel blocks, each CTA for its output-channel share
+  const bool do_bias = a.want_bias && cb < CL && gg == 0;
+  const uint32_t crank = CL > 1 ? ptx::cluster_ctarank() : 0u;
+  constexpr int BNS = BN / CL;  // output channels this CTA stages (and whose bias it sums)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -130,8 +140,8 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int b = 0; b < NS; ++b) {
-      ptx::mbar_init(&full[b], kStagers / 32);
-      ptx::mbar_init(&empty[b], 1);
+      ptx::mbar_init(&full[b], (kStagers / 32) * CL);
+      ptx::mbar_init(&empty[b], CL);
     }
     ptx::mbar_init(accum, 1);
     ptx::fence_mbar_init();
@@ -140,6 +150,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
   if (warp == 1) ptx::tmem_alloc(tmem_slot, tmem_cols);
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) ptx::cluster_sync_all();  // every CTA's barriers exist before remote arrivals
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int HWv = a.Hv * a.Wv;
@@ -152,7 +163,8 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
       constexpr uint32_t idesc_cat = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
                                      (uint32_t((2 * BN) >> 3) << 17) | (uint32_t(TM >> 4) << 24);
       for (int ch = ch0, b = 0, ph = 0; ch < ch1; ++ch) {
-        ptx::mbar_wait(&full[b], uint32_t(ph));
+        if constexpr (CL > 1) ptx::mbar_wait_cluster(&full[b], uint32_t(ph));
+        else ptx::mbar_wait(&full[b], uint32_t(ph));
         ptx::tc_fence_after();
         const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
         for (int k8 = 0; k8 < KC / 8; ++k8) {
@@ -177,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
             }
           }
         }
-        ptx::mma_commit_elect(&empty[b]);
+        if constexpr (CL > 1) ptx::mma_commit_mc_elect(&empty[b], uint16_t((1u << CL) - 1u));
+        else ptx::mma_commit_elect(&empty[b]);
         if (++b == NS) { b = 0; ph ^= 1; }
       }
       ptx::mma_commit_elect(accum);
@@ -194,8 +207,9 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
     // beyond kStagers, if any, take the sequential path below).
     static_assert(KC == 64 || KC == 32, "one or two 32-pixel halves per chunk");
     constexpr int KH = KC / 32;        // 32-pixel halves per chunk
-    constexpr int CPW = BN * KH / 8;   // output channels per warp
-    const int sw = tid >> 5, khalf = sw % KH, cw0 = (sw / KH) * CPW;
+    constexpr int CPW = BNS * KH / 8;  // output channels per warp (of this CTA's BN / CL share)
+    static_assert(BNS * KH % 8 == 0, "cluster share of the output channels per warp");
+    const int sw = tid >> 5, khalf = sw % KH, cw0 = int(crank) * BNS + (sw / KH) * CPW;
     float bsum[CPW];
 #pragma unroll
     for (int c = 0; c < CPW; ++c) bsum[c] = 0.f;
@@ -256,8 +270,18 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
         const int col = cw0 + c;
         const uint32_t off = lane_off + uint32_t(col) * 128u + (uint32_t(((lane >> 2) ^ (col & 7)) & 7) << 4);
         const float h = ptx::tf32_major<SPLIT>(yv[c]);
+        const float l = SPLIT ? ptx::tf32_lo(yv[c], h) : 0.f;
         ptx::st_shared_f32(bbase + off, h);
-        if constexpr (SPLIT) ptx::st_shared_f32(bbase + off + uint32_t(BN) * 128u, ptx::tf32_lo(yv[c], h));
+        if constexpr (SPLIT) ptx::st_shared_f32(bbase + off + uint32_t(BN) * 128u, l);
+        if constexpr (CL > 1) {  // the same slot of every other CTA of the cluster
+#pragma unroll
+          for (uint32_t r = 1; r < uint32_t(CL); ++r) {
+            const uint32_t peer = (crank + r) % uint32_t(CL);
+            const uint32_t rb = ptx::mapa(bbase + off, peer);
+            ptx::st_cluster_f32(rb, h);
+            if constexpr (SPLIT) ptx::st_cluster_f32(rb + uint32_t(BN) * 128u, l);
+          }
+        }
         if (do_bias) bsum[c] += yv[c];
       }
     };
@@ -273,7 +297,10 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
       a_load(asrc, inb && tid < a.rowsA, xv);
       float yv[CPW];
       b_load(v0, yv);
-      if (ch - ch0 >= NS) ptx::mbar_wait(&empty[b], uint32_t(ph ^ 1));
+      if (ch - ch0 >= NS) {
+        if constexpr (CL > 1) ptx::mbar_wait_cluster(&empty[b], uint32_t(ph ^ 1));
+        else ptx::mbar_wait(&empty[b], uint32_t(ph ^ 1));
+      }
       const uint32_t abase = ptx::smem_u32(smem + b * STAGE), bbase = abase + A_B;
       if (tid < a.rowsA) a_store(abase, tid, xv);
       b_store(bbase, yv);
@@ -284,9 +311,20 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
         a_load(s2, in2, xr);
         a_store(abase, row, xr);
       }
-      ptx::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&full[b]);
+      if constexpr (CL > 1) {
+        ptx::fence_proxy_async_all();  // local and remote generic stores -> the tensor cores' reads
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&full[b]);
+          const uint32_t fb = ptx::smem_u32(&full[b]);
+#pragma unroll
+          for (uint32_t r = 1; r < uint32_t(CL); ++r) ptx::mbar_arrive_cluster(ptx::mapa(fb, (crank + r) % uint32_t(CL)));
+        }
+      } else {
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&full[b]);
+      }
       if (++b == NS) { b = 0; ph ^= 1; }
     }
     if (do_bias) {  // per output channel: fixed xor tree over the warp's 32 pixels, then the two halves
@@ -339,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
       }
     }
     if (do_bias && warp == 2) {
-      for (int col = lane; col < BN; col += 32)
+      for (int col = int(crank) * BNS + lane; col < int(crank + 1) * BNS; col += 32)
         if (n0 + col < a.Cog) wsz[int64_t(n0 + col) * (a.Kc + 1) + a.Kc] = bias_part[col] + bias_part[BN + col];
     }
     }
@@ -347,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, BN >= 96 ? 1 : 2) conv_wtap_kernel(c
 done:
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) ptx::cluster_sync_all();  // no CTA leaves while peers may write or arrive into it
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, tmem_cols);
