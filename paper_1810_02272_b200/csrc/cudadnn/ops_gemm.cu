@@ -119,6 +119,31 @@ KCopy k_major_copy(Ctx* c, cudaStream_t st, Workspace& scratch, size_t offset_el
   return KCopy{DenseView<float>{out, int64_t(v.K), 1, v.rows, v.K, false}, lo};
 }
 
+// A K-contiguous operand written pre-split (hi, lo; rows of K, compact) so the GEMM's
+// producers convert only the other operand (the large InnerProducts' activations and
+// top diffs: 2.4 M elements against a 37.7 M-element weight for AlexNet fc6).
+__global__ void __launch_bounds__(256) split_rows_kernel(const float* __restrict__ in, float* __restrict__ hi,
+                                                         float* __restrict__ lo, int rows, int K, int64_t ld) {
+  const int64_t total = int64_t(rows) * K;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / K, k = i - r * K;
+    const float x = __ldg(in + r * ld + k);
+    const float h = ptx::tf32_hi(x);
+    hi[i] = h;
+    lo[i] = ptx::tf32_lo(x, h);
+  }
+}
+KCopy split_copy(Ctx* c, cudaStream_t st, Workspace& scratch, size_t offset_elems, const DenseView<float>& v) {
+  float* out = static_cast<float*>(scratch.ptr) + offset_elems;
+  float* lo = out + ((size_t(v.rows) * v.K + 3) & ~size_t(3));
+  const int64_t total = int64_t(v.rows) * v.K;
+  const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(kNumSMs) * 8));
+  split_rows_kernel<<<blocks, 256, 0, st>>>(v.p, out, lo, v.rows, v.K, v.sr);
+  check_launch("split_rows");
+  count_launch(c);
+  return KCopy{DenseView<float>{out, int64_t(v.K), 1, v.rows, v.K, false}, lo};
+}
+
 // A K-major copy as a GEMM operand: pre-split TMA when it carries a lo copy (the copy
 // is only made pre-split when TMA can take it, see dense_gemm).
 template <class F>
@@ -176,19 +201,31 @@ static void dense_gemm(Ctx* c, cdnn_handle stream, int M, int N, int K, const De
       return;
     }
     const GemmPlan pl = plan_tc(M, N, K);
-    if (int64_t(M) * N * K >= (int64_t(1) << 28) && (va.mcontig || vb.mcontig)) {
+    const bool split = c->math_mode == CDNN_MATH_TF32X3;
+    // the copy of an operand with `rows` rows is TMA-eligible (aligned, K >= 32, rows >= box)
+    auto presplit = [&](const DenseView<float>& v, int box) { return split && v.K >= 32 && v.K % 4 == 0 && v.rows >= box; };
+    // a K-contiguous operand at most a quarter the size of the other one: pre-split copy
+    // (one cheap pass) so only the large operand is converted in the kernel
+    auto small_split = [&](const DenseView<float>& v, const DenseView<float>& o, int box) {
+      return !v.mcontig && presplit(v, box) && v.sk == 1 && 4 * int64_t(v.rows) <= int64_t(o.rows);
+    };
+    // (contractions of >= 2^32 MACs: below that the extra launch does not pay, AlexNet fc8)
+    const bool big = int64_t(M) * N * K >= (int64_t(1) << 32);
+    const bool sa = big && small_split(va, vb, tc::BM), sb = big && small_split(vb, va, pl.bn);
+    if (int64_t(M) * N * K >= (int64_t(1) << 28) && (va.mcontig || vb.mcontig || sa || sb)) {
       Workspace& aux = ws.aux();
-      const bool split = c->math_mode == CDNN_MATH_TF32X3;
       const size_t f = split ? 2 : 1;
       // 16-byte aligned halves (row counts are multiples of 4 elements only by chance)
       auto round4 = [](size_t n) { return (n + 3) & ~size_t(3); };
-      const size_t na = va.mcontig ? round4(size_t(va.rows) * va.K) : 0;
-      const size_t nb = vb.mcontig ? round4(size_t(vb.rows) * vb.K) : 0;
+      const size_t na = (va.mcontig || sa) ? round4(size_t(va.rows) * va.K) : 0;
+      const size_t nb = (vb.mcontig || sb) ? round4(size_t(vb.rows) * vb.K) : 0;
       aux.get((na + nb) * f * sizeof(float), c->device);
-      // the copy of an operand with `rows` rows is TMA-eligible (aligned, K >= 32, rows >= box)
-      auto presplit = [&](const DenseView<float>& v, int box) { return split && v.K >= 32 && v.K % 4 == 0 && v.rows >= box; };
-      const KCopy ka = va.mcontig ? k_major_copy(c, st, aux, 0, va, presplit(va, tc::BM)) : KCopy{va, nullptr};
-      const KCopy kb = vb.mcontig ? k_major_copy(c, st, aux, na * f, vb, presplit(vb, pl.bn)) : KCopy{vb, nullptr};
+      const KCopy ka = va.mcontig ? k_major_copy(c, st, aux, 0, va, presplit(va, tc::BM))
+                       : sa       ? split_copy(c, st, aux, 0, va)
+                                  : KCopy{va, nullptr};
+      const KCopy kb = vb.mcontig ? k_major_copy(c, st, aux, na * f, vb, presplit(vb, pl.bn))
+                       : sb       ? split_copy(c, st, aux, na * f, vb)
+                                  : KCopy{vb, nullptr};
       TmaReq ra2, rb2;
       with_copy(c, ka, tc::BM, ra2, [&](const auto& a) {
         with_copy(c, kb, pl.bn, rb2, [&](const auto& b) { run_tc(c, st, ws, pl, M, N, K, a, b, epi, ra2, rb2); });
