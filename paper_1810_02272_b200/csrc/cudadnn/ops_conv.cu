@@ -149,7 +149,10 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   a.div_wv = FastDiv(uint32_t(a.Wv));
   const bool split = c->math_mode == CDNN_MATH_TF32X3;
   const int tiles = (a.Mv + 127) / 128;
-  const int bn = pick_bn(Cout, tiles, G, {32, 48, 64, 96, 128});
+  // 192-wide tiles for 192 / 384 output channels (AlexNet conv3-5): the N = 192 MMA
+  // costs 96 cycles (full rate) where N = 96 costs 56, and the A tile is staged once
+  // per 192 channels
+  const int bn = pick_bn(Cout, tiles, G, {32, 48, 64, 96, 128, 192});
   // shared memory: A buffers (double-buffered over channel blocks when they fit) + B ring
   int budget = 227 * 1024;
   // 32-wide tiles (<= 32 output channels per block, the CIFAR / LeNet / ResNet stage-1
@@ -209,6 +212,7 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
         case 48: launch_conv_tap<48, SP>(c, st, grid, smem, *twh, *twl, ag); break;
         case 64: launch_conv_tap<64, SP>(c, st, grid, smem, *twh, *twl, ag); break;
         case 96: launch_conv_tap<96, SP>(c, st, grid, smem, *twh, *twl, ag); break;
+        case 192: launch_conv_tap<192, SP>(c, st, grid, smem, *twh, *twl, ag); break;
         default: launch_conv_tap<128, SP>(c, st, grid, smem, *twh, *twl, ag); break;
       }
     };
