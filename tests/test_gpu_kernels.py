@@ -110,6 +110,8 @@ CONV_CASES = [
     (2, 3, 39, 39, 96, 11, 4, 0, 1, 1),     # AlexNet conv1 (96 outputs: N = 96 tiles)
     (2, 96, 15, 15, 256, 5, 1, 2, 1, 2),    # AlexNet conv2 (backward-data to 48 channels: N = 48 tiles)
     (2, 384, 13, 13, 384, 3, 1, 1, 1, 2),   # AlexNet conv4 (192 per group: N = 96 tiles)
+    (100, 32, 16, 16, 32, 5, 1, 2, 1, 1),   # CIFAR-quick conv2 at bench size (split-K clusters of 8 CTAs)
+    (64, 16, 32, 32, 16, 3, 1, 1, 1, 1),    # ResNet-20 stage 1, half the bench batch (split-K clusters)
 ]
 
 
