@@ -90,44 +90,106 @@ __global__ void __launch_bounds__(256) max_pool_bwd(const T* __restrict__ dy, co
   }
 }
 
-// Fixed-window MAX backward: one bottom element per thread, consecutive threads on
-// consecutive columns (coalesced gate loads and dx stores); at most R = ceil(K/S)
-// windows per dimension cover an element, visited in the same (ph, pw) order as
-// max_pool_bwd, so the sums are bit-identical.  The kernel is latency-bound (a
-// resident thread walks ~250 AlexNet pool1 elements), so every load of an element
-// -- gate, the R*R mask entries and the R*R top diffs -- is issued at once: one
-// memory round trip per element instead of gate -> mask -> diff in series.
+// Fixed-window MAX backward over S x S blocks of bottom elements: with K <= 2S the
+// block (padded rows S*j .. S*j+S-1, columns S*k ..) is covered only by the windows
+// (j-D .. j) x (k-D .. k), D = (K-1)/S, so one thread loads those (D+1)^2 mask entries
+// and top diffs once for S*S elements (AlexNet 3x3/2: 4 windows for 4 elements instead
+// of 4 per element) and decomposes one index.  A window whose argmax is the element
+// covers it, so the mask test alone selects the contributions; they are added in
+// ascending (ph, pw) order like max_pool_bwd, so the sums are bit-identical.
 template <typename T, int K, int S>
-__global__ void __launch_bounds__(256) max_pool_bwd_k(const T* __restrict__ dy, const int* __restrict__ mask,
-                                                      T* __restrict__ dx, PoolGeom g, uint32_t total,
-                                                      const T* __restrict__ gate) {
-  constexpr int R = (K + S - 1) / S;
+__global__ void __launch_bounds__(256) max_pool_bwd_blk(const T* __restrict__ dy, const int* __restrict__ mask,
+                                                        T* __restrict__ dx, PoolGeom g, FastDiv div_bw,
+                                                        FastDiv div_bhw, uint32_t BW, uint32_t BHW, uint32_t total,
+                                                        const T* __restrict__ gate) {
+  constexpr int D = (K - 1) / S;
+  static_assert(K <= 2 * S, "block covers at most (D+1)^2 windows");
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const Idx3 q = split3(i, g.divHW, g.divW, uint32_t(g.H * g.W), uint32_t(g.W));
-    const int h = int(q.h) + g.ph, w = int(q.w) + g.pw;
-    const int phs = h < K ? 0 : (h - K) / S + 1, phe = min(h / S + 1, g.PH);
-    const int pws = w < K ? 0 : (w - K) / S + 1, pwe = min(w / S + 1, g.PW);
-    const int me = int(q.h) * g.W + int(q.w);
+    const Idx3 q = split3(i, div_bhw, div_bw, BHW, BW);
+    const int j = int(q.h), k = int(q.w);
     const size_t base = size_t(q.plane) * uint32_t(g.PH * g.PW);
-    const bool open = !gate || __ldg(gate + i) > T(0);
-    int m[R][R];
-    T v[R][R];
+    int m[D + 1][D + 1];
+    T v[D + 1][D + 1];
 #pragma unroll
-    for (int a = 0; a < R; ++a)
+    for (int a = 0; a <= D; ++a)
 #pragma unroll
-      for (int b = 0; b < R; ++b) {
-        const bool ok = phs + a < phe && pws + b < pwe;
-        const size_t o = base + (phs + a) * g.PW + pws + b;
+      for (int b = 0; b <= D; ++b) {
+        const int ph = j - D + a, pw = k - D + b;
+        const bool ok = ph >= 0 && ph < g.PH && pw >= 0 && pw < g.PW;
+        const size_t o = base + ph * g.PW + pw;
         m[a][b] = ok ? __ldg(mask + o) : -1;
         v[a][b] = ok ? __ldg(dy + o) : T(0);
       }
-    T s = T(0);
+    const size_t pbase = size_t(q.plane) * uint32_t(g.H * g.W);
+    bool in[S][S];
+    T gv[S][S];
 #pragma unroll
-    for (int a = 0; a < R; ++a)
+    for (int r = 0; r < S; ++r)
 #pragma unroll
-      for (int b = 0; b < R; ++b)
-        if (m[a][b] == me) s += v[a][b];
-    dx[i] = open ? s : T(0);
+      for (int c = 0; c < S; ++c) {
+        const int h = j * S + r - g.ph, w = k * S + c - g.pw;
+        in[r][c] = h >= 0 && h < g.H && w >= 0 && w < g.W;
+        gv[r][c] = (gate && in[r][c]) ? __ldg(gate + pbase + h * g.W + w) : T(1);
+      }
+#pragma unroll
+    for (int r = 0; r < S; ++r)
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        if (!in[r][c]) continue;
+        const int h = j * S + r - g.ph, w = k * S + c - g.pw;
+        const int me = h * g.W + w;
+        T s = T(0);
+#pragma unroll
+        for (int a = 0; a <= D; ++a)
+#pragma unroll
+          for (int b = 0; b <= D; ++b)
+            if (m[a][b] == me) s += v[a][b];
+        dx[pbase + me] = gv[r][c] > T(0) ? s : T(0);
+      }
+  }
+}
+
+// Fixed-window MAX forward, two vertically adjacent outputs per thread (S < K: the
+// shared window rows are loaded once; consecutive threads take consecutive output
+// columns, so every store is coalesced); every load issued before the scan, which
+// keeps max_pool_fwd's h-major order and strict '>' (bit-identical).
+template <typename T, int K, int S>
+__global__ void __launch_bounds__(256) max_pool_fwd_k2(const T* __restrict__ x, T* __restrict__ y,
+                                                       int* __restrict__ mask, PoolGeom g, FastDiv div_pw,
+                                                       FastDiv div_phw2, uint32_t PHW2, uint32_t total, bool relu) {
+  constexpr int RW = K + S;  // input rows of the two windows
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Idx3 q = split3(i, div_phw2, div_pw, PHW2, uint32_t(g.PW));
+    const int oh = int(q.h) * 2, ow = int(q.w);
+    const int hs = oh * S - g.ph, ws = ow * S - g.pw;
+    const T* plane = x + size_t(q.plane) * uint32_t(g.H * g.W);
+    T v[RW][K];
+    bool ok[RW][K];
+#pragma unroll
+    for (int a = 0; a < RW; ++a)
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const int h = hs + a, w = ws + b;
+        ok[a][b] = h >= 0 && h < g.H && w >= 0 && w < g.W;
+        v[a][b] = ok[a][b] ? __ldg(plane + h * g.W + w) : T(0);
+      }
+    const size_t ob = size_t(q.plane) * uint32_t(g.PH * g.PW) + size_t(oh) * g.PW + ow;
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      if (oh + o >= g.PH) break;
+      T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
+      int arg = -1;
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b)
+          if (ok[o * S + a][b] && v[o * S + a][b] > best) {
+            best = v[o * S + a][b];
+            arg = (hs + o * S + a) * g.W + ws + b;
+          }
+      y[ob + o * g.PW] = relu ? (best > T(0) ? best : T(0)) : best;
+      if (mask) mask[ob + o * g.PW] = arg;
+    }
   }
 }
 
@@ -295,8 +357,20 @@ int cdnn_pool_forward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle x, cdnn_han
       T* yp = reinterpret_cast<T*>(Y.dev);
       int* mp = M ? reinterpret_cast<int*>(M->dev) : nullptr;
       if (d.p.method == CDNN_POOL_MAX) {
-        // (an unrolled 3x3/2 variant measured slower: AlexNet pool1 158 vs 148 us)
-        max_pool_fwd<T><<<blocks, 256, 0, st>>>(xp, yp, mp, g, uint32_t(nout), relu);
+        const int fw = fixed_window(g);
+        if (fw) {  // two outputs per thread
+          const uint32_t PH2 = uint32_t(g.PH + 1) / 2, PHW2 = PH2 * uint32_t(g.PW);
+          const uint64_t n2 = uint64_t(g.N) * g.C * PHW2;
+          const int b2 = grid_for(int64_t(n2), 256);
+          if (fw == 32)
+            max_pool_fwd_k2<T, 3, 2><<<b2, 256, 0, st>>>(xp, yp, mp, g, g.divPW, FastDiv(PHW2), PHW2, uint32_t(n2),
+                                                         relu);
+          else
+            max_pool_fwd_k2<T, 2, 2><<<b2, 256, 0, st>>>(xp, yp, mp, g, g.divPW, FastDiv(PHW2), PHW2, uint32_t(n2),
+                                                         relu);
+        } else {
+          max_pool_fwd<T><<<blocks, 256, 0, st>>>(xp, yp, mp, g, uint32_t(nout), relu);
+        }
       } else {
         switch (fixed_window(g)) {
           case 32: ave_pool_fwd_k<T, 3, 2><<<blocks, 256, 0, st>>>(xp, yp, g, uint32_t(nout), relu); break;
@@ -349,8 +423,16 @@ int cdnn_pool_backward_ex(cdnn_ctx ctx, cdnn_handle desc, cdnn_handle dy, cdnn_h
       const T* gp = G ? reinterpret_cast<const T*>(G->dev) : nullptr;
       if (fw && d.p.method == CDNN_POOL_MAX) {
         const int* mp = reinterpret_cast<const int*>(M->dev);
-        if (fw == 32) max_pool_bwd_k<T, 3, 2><<<blocks, 256, 0, st>>>(dyp, mp, dxp, g, uint32_t(nin), gp);
-        else max_pool_bwd_k<T, 2, 2><<<blocks, 256, 0, st>>>(dyp, mp, dxp, g, uint32_t(nin), gp);
+        // S x S blocks of bottom elements per thread (S = 2 for both fixed windows)
+        const uint32_t BW = uint32_t(g.W + g.pw + 1) / 2, BH = uint32_t(g.H + g.ph + 1) / 2;
+        const uint64_t nb = uint64_t(g.N) * g.C * BH * BW;
+        const int bb = grid_for(int64_t(nb), 256);
+        if (fw == 32)
+          max_pool_bwd_blk<T, 3, 2><<<bb, 256, 0, st>>>(dyp, mp, dxp, g, FastDiv(BW), FastDiv(BH * BW), BW, BH * BW,
+                                                         uint32_t(nb), gp);
+        else
+          max_pool_bwd_blk<T, 2, 2><<<bb, 256, 0, st>>>(dyp, mp, dxp, g, FastDiv(BW), FastDiv(BH * BW), BW, BH * BW,
+                                                         uint32_t(nb), gp);
       } else if (fw) {
         if (fw == 32) ave_pool_bwd_k<T, 3, 2><<<blocks, 256, 0, st>>>(dyp, dxp, g, uint32_t(nin), gp);
         else ave_pool_bwd_k<T, 2, 2><<<blocks, 256, 0, st>>>(dyp, dxp, g, uint32_t(nin), gp);
