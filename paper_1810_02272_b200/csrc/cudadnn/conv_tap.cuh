@@ -322,39 +322,52 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
                 put_row8<SPLIT>(rbase, A_HALF, row, g8, xx);
               }
           }
-        } else
-        for (int row = tid; row < a.rows; row += 128) {
-          const int v = m0 + row;
-          bool inb = false;
-          const float* src = a.in;
-          if (v < a.Mv) {
-            const int img = int(a.div_hwv.div(uint32_t(v)));
-            const int rem = v - img * HWv;
-            const int hp = int(a.div_wv.div(uint32_t(rem)));
-            const int h = hp - a.oh, w = rem - hp * a.Wv - a.ow;
-            inb = h >= 0 && h < a.Hin && w >= 0 && w < a.Win;
-            src = a.in + int64_t(img) * a.in_nstride + int64_t(c0) * a.in_cstride + h * a.Win + w;
-          }
-          const uint32_t rbase = hi + uint32_t(row) * 128u;
-          if (g8n == 4 && kc == 32) {
-            // full block: issue all 32 loads before any conversion (latency hiding)
-            float x[4][8];
+        } else {
+          // two rows per thread per round with every load (up to 64, partial blocks
+          // predicated) issued before any conversion: one memory round trip per two
+          // rows, instead of one per row (per 8 channels for a partial block) -- the
+          // staging of tall tiles (AlexNet conv1's 57-wide grid: 244 rows per 128
+          // pixels) otherwise outlasts the MMAs it feeds
+          auto row_src = [&](int row, bool& inb) {
+            const int v = m0 + row;
+            inb = false;
+            const float* src = a.in;
+            if (row < a.rows && v < a.Mv) {
+              const int img = int(a.div_hwv.div(uint32_t(v)));
+              const int rem = v - img * HWv;
+              const int hp = int(a.div_wv.div(uint32_t(rem)));
+              const int h = hp - a.oh, w = rem - hp * a.Wv - a.ow;
+              inb = h >= 0 && h < a.Hin && w >= 0 && w < a.Win;
+              src = a.in + int64_t(img) * a.in_nstride + int64_t(c0) * a.in_cstride + h * a.Win + w;
+            }
+            return src;
+          };
+          auto load32 = [&](const float* src, bool inb, float (&x)[4][8]) {
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8)
 #pragma unroll
-              for (int e = 0; e < 8; ++e) x[g8][e] = inb ? __ldg(src + int64_t(g8 * 8 + e) * a.in_cstride) : 0.f;
+              for (int e = 0; e < 8; ++e)
+                x[g8][e] = (inb && g8 * 8 + e < kc) ? __ldg(src + int64_t(g8 * 8 + e) * a.in_cstride) : 0.f;
+          };
+          auto put32 = [&](int row, const float (&x)[4][8]) {
+            const uint32_t rbase = hi + uint32_t(row) * 128u;
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) put_row8<SPLIT>(rbase, A_HALF, row, g8, x[g8]);
-          } else {
-            for (int g8 = 0; g8 < g8n; ++g8) {
-              float x[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int c = g8 * 8 + e;
-                x[e] = (inb && c < kc) ? __ldg(src + int64_t(c) * a.in_cstride) : 0.f;
-              }
-              put_row8<SPLIT>(rbase, A_HALF, row, g8, x);
+            for (int g8 = 0; g8 < 4; ++g8)
+              if (g8 < g8n) put_row8<SPLIT>(rbase, A_HALF, row, g8, x[g8]);
+          };
+          // (one row per round for BN <= 32: two CTAs share the SM's registers)
+          constexpr int RPT = BN > 32 ? 2 : 1;
+          for (int row = tid; row < a.rows; row += 128 * RPT) {
+            bool ia, ib = false;
+            const float* sa = row_src(row, ia);
+            float xa[4][8], xb[4][8];
+            load32(sa, ia, xa);
+            if constexpr (RPT == 2) {
+              const float* sb = row_src(row + 128, ib);
+              load32(sb, ib, xb);
             }
+            put32(row, xa);
+            if (RPT == 2 && row + 128 < a.rows) put32(row + 128, xb);
           }
         }
         ptx::fence_proxy_async_smem();
