@@ -219,6 +219,14 @@ CDNN_API int cdnn_scal(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cd
 CDNN_API int cdnn_axpy(cdnn_ctx ctx, uint64_t n, double alpha, cdnn_handle x, cdnn_handle y,
                        cdnn_handle stream);
 CDNN_API int cdnn_dot(cdnn_ctx ctx, uint64_t n, cdnn_handle x, cdnn_handle y, double* result);
+/* Fan-out in one pass (Split forward: dst_k = src when alpha is NULL; Eltwise SUM
+ * backward: dst_k = alpha[k] * src); 1..8 destinations, 0 handles skipped. */
+CDNN_API int cdnn_fan_out(cdnn_ctx ctx, cdnn_handle src, const cdnn_handle* dsts, const double* alpha, int ndst,
+                          uint64_t n, cdnn_handle stream);
+/* Fan-in in one pass (Split backward): dst = src_0 + src_1 + ... in order, rounded as
+ * cdnn_copy followed by cdnn_axpy(1.0) per further source; 1..8 sources. */
+CDNN_API int cdnn_fan_in(cdnn_ctx ctx, const cdnn_handle* srcs, int nsrc, cdnn_handle dst, uint64_t n,
+                         cdnn_handle stream);
 /* Row-major C = alpha*op(A)*op(B) + beta*C; beta == 0 never reads C.
  * F32 buffers run on tcgen05 TF32 tensor cores, F64 on the SIMT FP64 path. */
 CDNN_API int cdnn_gemm(cdnn_ctx ctx, int trans_a, int trans_b, int m, int n, int k, double alpha,

@@ -41,6 +41,36 @@ __global__ void axpy_kernel(const T* __restrict__ x, T* __restrict__ y, uint64_t
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     y[i] = add_rn(y[i], mul_rn(a, x[i]));
 }
+// Fan-out / fan-in of Split and Eltwise SUM (up to kFan blobs) in one pass: every
+// destination written from one read of the source (Split forward, Eltwise backward:
+// y_k = a_k * x, a plain product as in axpby), or the top diffs summed in order with
+// the same roundings as copy + axpy (Split backward: ((d0 + 1*d1) + 1*d2) ...).
+constexpr int kFan = 8;
+template <typename T>
+struct FanPtrs {
+  T* p[kFan];
+  T a[kFan];
+};
+template <typename T>
+__global__ void fan_out_kernel(const T* __restrict__ x, FanPtrs<T> d, int nd, bool scaled, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const T v = x[i];
+#pragma unroll
+    for (int k = 0; k < kFan; ++k)
+      if (k < nd && d.p[k]) d.p[k][i] = scaled ? mul_rn(d.a[k], v) : v;
+  }
+}
+template <typename T>
+__global__ void fan_in_kernel(FanPtrs<T> s, int ns, T* __restrict__ y, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    T acc = s.p[0][i];
+#pragma unroll
+    for (int k = 1; k < kFan; ++k)
+      if (k < ns) acc = add_rn(acc, mul_rn(T(1), s.p[k][i]));
+    y[i] = acc;
+  }
+}
+
 // Deterministic dot: fixed grid, per-block tree, then one block sums partials in order.
 template <typename T>
 __global__ void dot_partial_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t n, T* __restrict__ part) {
@@ -357,6 +387,64 @@ int cdnn_copy(cdnn_ctx ctx, cdnn_handle src, cdnn_handle dst, uint64_t n, cdnn_h
       copy_kernel<T><<<blocks_for(n), kThreads, 0, st>>>(dptr<T>(S), dptr<T>(D), n);
     });
     check_launch("copy");
+    count_launch(c);
+  });
+}
+
+// Split forward (alpha == null: dst_k = src) and Eltwise SUM backward (dst_k = alpha_k * src);
+// zero destination handles are skipped
+int cdnn_fan_out(cdnn_ctx ctx, cdnn_handle src, const cdnn_handle* dsts, const double* alpha, int ndst, uint64_t n,
+                 cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (ndst < 1 || ndst > kFan || !dsts) fail(CDNN_INVALID_ARGUMENT, "fan_out: 1..8 destinations");
+    BufferSlot& S = buffer(c, src, "fan_out src");
+    require_len(S, n, "fan_out src");
+    BufferSlot* D[kFan] = {};
+    for (int k = 0; k < ndst; ++k)
+      if (dsts[k]) {
+        D[k] = &buffer(c, dsts[k], "fan_out dst");
+        require_len(*D[k], n, "fan_out dst");
+        require_dtype(*D[k], S.dtype, "fan_out");
+      }
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(S.dtype, "fan_out", [&](auto tag) {
+      using T = decltype(tag);
+      FanPtrs<T> f{};
+      for (int k = 0; k < ndst; ++k) {
+        f.p[k] = D[k] ? dptr<T>(*D[k]) : nullptr;
+        f.a[k] = alpha ? T(alpha[k]) : T(1);
+      }
+      fan_out_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(dptr<T>(S), f, ndst, alpha != nullptr, n);
+    });
+    check_launch("fan_out");
+    count_launch(c);
+  });
+}
+
+// Split backward: dst = src_0 + src_1 + ... (in order; the roundings of copy + axpy)
+int cdnn_fan_in(cdnn_ctx ctx, const cdnn_handle* srcs, int nsrc, cdnn_handle dst, uint64_t n, cdnn_handle stream) {
+  return guarded([&] {
+    Ctx* c = need_ctx(ctx);
+    if (nsrc < 1 || nsrc > kFan || !srcs) fail(CDNN_INVALID_ARGUMENT, "fan_in: 1..8 sources");
+    BufferSlot& Y = buffer(c, dst, "fan_in dst");
+    require_len(Y, n, "fan_in dst");
+    BufferSlot* S[kFan] = {};
+    for (int k = 0; k < nsrc; ++k) {
+      S[k] = &buffer(c, srcs[k], "fan_in src");
+      require_len(*S[k], n, "fan_in src");
+      require_dtype(*S[k], Y.dtype, "fan_in");
+    }
+    if (n == 0) return;
+    DeviceGuard g(c);
+    by_dtype(Y.dtype, "fan_in", [&](auto tag) {
+      using T = decltype(tag);
+      FanPtrs<T> f{};
+      for (int k = 0; k < nsrc; ++k) f.p[k] = dptr<T>(*S[k]);
+      fan_in_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(f, nsrc, dptr<T>(Y), n);
+    });
+    check_launch("fan_in");
     count_launch(c);
   });
 }

@@ -310,6 +310,16 @@ void EltwiseLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> 
   Registry& reg = bottoms[0]->registry();
   const std::size_t n = tops[0]->count();
   const cdnn_handle dy = tops[0]->gpu_diff();
+  if (bottoms.size() <= 8) {  // every bottom diff from one read of dy
+    cdnn_handle d[8] = {};
+    double a[8] = {};
+    for (std::size_t k = 0; k < bottoms.size(); ++k) {
+      a[k] = coeff_[k];
+      d[k] = propagate_down(k) ? bottoms[k]->overwrite_gpu_diff() : 0;
+    }
+    cdnn_ok(cdnn_fan_out(reg.context(), dy, d, a, int(bottoms.size()), n, reg.stream()), "Eltwise backward");
+    return;
+  }
   for (std::size_t k = 0; k < bottoms.size(); ++k) {
     if (!propagate_down(k)) continue;
     cdnn_ok(cdnn_axpby(reg.context(), n, coeff_[k], dy, 0.0, bottoms[k]->overwrite_gpu_diff(), 0, reg.stream()),

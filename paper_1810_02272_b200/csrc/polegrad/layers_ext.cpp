@@ -258,6 +258,13 @@ std::vector<Shape> SplitLayer::setup(const std::vector<Shape>& s, const std::sha
 void SplitLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
   Registry& reg = bottoms[0]->registry();
   const cdnn_handle x = bottoms[0]->gpu_data();
+  if (tops.size() <= 8) {  // every copy from one read of x
+    cdnn_handle d[8] = {};
+    for (std::size_t t = 0; t < tops.size(); ++t) d[t] = tops[t]->overwrite_gpu_data();
+    cdnn_ok(cdnn_fan_out(reg.context(), x, d, nullptr, int(tops.size()), bottoms[0]->count(), reg.stream()),
+            "Split forward");
+    return;
+  }
   for (Blob* t : tops)
     cdnn_ok(cdnn_copy(reg.context(), x, t->overwrite_gpu_data(), t->count(), reg.stream()), "Split forward");
 }
@@ -267,6 +274,12 @@ void SplitLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bo
   Registry& reg = bottoms[0]->registry();
   const std::size_t n = bottoms[0]->count();
   const cdnn_handle dx = bottoms[0]->overwrite_gpu_diff();
+  if (tops.size() <= 8) {  // the diffs summed in one pass (same order and roundings as copy + axpy)
+    cdnn_handle d[8] = {};
+    for (std::size_t t = 0; t < tops.size(); ++t) d[t] = tops[t]->gpu_diff();
+    cdnn_ok(cdnn_fan_in(reg.context(), d, int(tops.size()), dx, n, reg.stream()), "Split backward");
+    return;
+  }
   cdnn_ok(cdnn_copy(reg.context(), tops[0]->gpu_diff(), dx, n, reg.stream()), "Split backward");
   for (std::size_t t = 1; t < tops.size(); ++t)
     cdnn_ok(cdnn_axpy(reg.context(), n, 1.0, tops[t]->gpu_diff(), dx, reg.stream()), "Split backward");

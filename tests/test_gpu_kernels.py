@@ -216,6 +216,43 @@ def test_sgd_momentum_bit_exact(ctx, dtype):
     assert not ctx.read(hg).any()
 
 
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("k", [2, 3])
+def test_fan_out_fan_in_match_copy_axpy(ctx, dtype, k):
+    """Split forward / backward and Eltwise backward in one pass (cdnn_fan_out / cdnn_fan_in)
+    are bit-identical to the copy / axpy / axpby sequences they replace."""
+    import ctypes as C
+    rng = np.random.default_rng(11 + k)
+    dt = NP[dtype]
+    n = 5003
+    x = rng.standard_normal(n).astype(dt)
+    srcs = [rng.standard_normal(n).astype(dt) for _ in range(k)]
+    hx = ctx.upload(x)
+    # fan-out, unscaled (Split forward) and scaled (Eltwise backward), one destination skipped
+    outs = [ctx.alloc(n, dtype) for _ in range(k)]
+    arr = (C.c_uint64 * k)(*[int(o) for o in outs])
+    ctx.call("cdnn_fan_out", hx, arr, None, k, n, 0)
+    for o in outs:
+        assert np.array_equal(ctx.read(o), x)
+    coeff = [1.0, -0.5, 3.0][:k]
+    arr2 = (C.c_uint64 * k)(*([int(o) for o in outs[:-1]] + [0]))
+    ctx.call("cdnn_fan_out", hx, arr2, (C.c_double * k)(*coeff), k, n, 0)
+    for j in range(k - 1):
+        ref = ctx.alloc(n, dtype)
+        ctx.call("cdnn_axpby", n, coeff[j], hx, 0.0, ref, 0, 0)
+        assert np.array_equal(ctx.read(outs[j]), ctx.read(ref))
+    assert np.array_equal(ctx.read(outs[-1]), x)  # skipped
+    # fan-in (Split backward) against copy + axpy(1.0)
+    hs = [ctx.upload(v) for v in srcs]
+    y = ctx.alloc(n, dtype)
+    ctx.call("cdnn_fan_in", (C.c_uint64 * k)(*[int(v) for v in hs]), k, y, n, 0)
+    ref = ctx.alloc(n, dtype)
+    ctx.call("cdnn_copy", hs[0], ref, n, 0)
+    for v in hs[1:]:
+        ctx.call("cdnn_axpy", n, 1.0, v, ref, 0)
+    assert np.array_equal(ctx.read(y), ctx.read(ref))
+
+
 # ---- config 4-5 layers (LRN, Dropout, BatchNorm, Scale, Eltwise) vs torch fp64 -----------
 
 @pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
