@@ -58,6 +58,7 @@ struct TapArgs {
   int64_t in_nstride;    // image stride of `in`
   int64_t out_nstride;   // image stride of `out`
   int nbuf, stages;      // A buffers (1|2), weight ring depth
+  int tps;               // filter taps per weight-ring stage (one mbarrier wait + one commit per stage)
   int relu;              // fused in-place ReLU in the epilogue (forward)
   int fold;              // S folded into the channels (k = s*Cin + c, Cin*S <= 32): R taps of K = S*Cin
   const float* gate;     // backward-data: fused in-place ReLU backward, out = gate > 0 ? out : 0 (same layout)
@@ -78,8 +79,8 @@ constexpr int kTraceSlots = 32;
 __host__ __device__ constexpr uint32_t b_stage_bytes(int bn, bool split) { return uint32_t(bn) * 128u * (split ? 2u : 1u); }
 __host__ __device__ constexpr uint32_t a_buf_bytes(int rows, bool split) { return uint32_t(rows) * 128u * (split ? 2u : 1u); }
 
-inline int smem_bytes(int rows, int nbuf, int stages, int bn, bool split) {
-  return 1024 + nbuf * int(a_buf_bytes(rows, split)) + stages * int(b_stage_bytes(bn, split)) +
+inline int smem_bytes(int rows, int nbuf, int stages, int bn, bool split, int tps = 1) {
+  return 1024 + nbuf * int(a_buf_bytes(rows, split)) + stages * tps * int(b_stage_bytes(bn, split)) +
          (2 * kMaxStages + 8 + 1) * 8 + 16;
 }
 
@@ -128,7 +129,8 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
   const uint32_t A_BUF = a_buf_bytes(a.rows, SPLIT), A_HALF = uint32_t(a.rows) * 128u;
   uint8_t* abase = smem;
   uint8_t* bbase = smem + a.nbuf * A_BUF;
-  uint64_t* full = reinterpret_cast<uint64_t*>(bbase + a.stages * B_STAGE);
+  const uint32_t B_RING = uint32_t(a.tps) * B_STAGE;  // one ring stage = tps taps' weights
+  uint64_t* full = reinterpret_cast<uint64_t*>(bbase + a.stages * B_RING);
   uint64_t* empty = full + kMaxStages;
   uint64_t* a_full = empty + kMaxStages;
   uint64_t* a_empty = a_full + 2;
@@ -173,13 +175,16 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
       for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
         const int n0 = a.n0_base + (t / a.tiles_m) * BN;
         for (int cb = 0; cb < a.cblocks; ++cb)
-          for (int it = 0; it < taps; ++it) {
-            const int tap = it + rot < taps ? it + rot : it + rot - taps;
+          for (int it = 0; it < taps; it += a.tps) {
+            const int cnt = min(a.tps, taps - it);
             ptx::mbar_wait(&empty[stage], phase ^ 1);
-            ptx::mbar_arrive_expect_tx(&full[stage], B_STAGE);
-            uint8_t* b = bbase + stage * B_STAGE;
-            ptx::tma_load_2d(b, &tm_w_hi, &full[stage], cb * 32, tap * a.wrows + n0);
-            if constexpr (SPLIT) ptx::tma_load_2d(b + B_HALF, &tm_w_lo, &full[stage], cb * 32, tap * a.wrows + n0);
+            ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(cnt) * B_STAGE);
+            for (int j = 0; j < cnt; ++j) {
+              const int tap = it + j + rot < taps ? it + j + rot : it + j + rot - taps;
+              uint8_t* b = bbase + stage * B_RING + j * B_STAGE;
+              ptx::tma_load_2d(b, &tm_w_hi, &full[stage], cb * 32, tap * a.wrows + n0);
+              if constexpr (SPLIT) ptx::tma_load_2d(b + B_HALF, &tm_w_lo, &full[stage], cb * 32, tap * a.wrows + n0);
+            }
             if (++stage == a.stages) { stage = 0; phase ^= 1; }
           }
       }
@@ -217,46 +222,49 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
           const uint64_t dAl = dA + (A_HALF >> 4);
           uint32_t shift = shift_rot;
           int r = r_rot, s = s_rot;
-          for (int it = 0; it < taps; ++it) {
+          for (int it = 0; it < taps; it += a.tps) {
+            const int cnt = min(a.tps, taps - it);
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            const uint64_t dB = desc_sw128(b0 + uint32_t(stage) * B_STAGE);
-            const uint64_t dBl = dB + (B_HALF >> 4);
-            const uint64_t ah = dA + shift, al = dAl + shift;
-            auto k8 = [&](int j, uint32_t acc) {
-              const uint64_t kj = uint64_t(j) * 2u;  // +32 B per k8 step
-              if constexpr (CAT) {
-                // [B_hi | B_lo] are contiguous BN-row blocks: one N = 2*BN operand
-                ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc_cat, acc);
-                ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, 1u);
-              } else {
-                if constexpr (SPLIT) {
-                  ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, acc);
-                  ptx::mma_tf32_elect(d_tmem, ah + kj, dBl + kj, idesc, 1u);
-                  acc = 1u;
+            for (int j = 0; j < cnt; ++j) {
+              const uint64_t dB = desc_sw128(b0 + uint32_t(stage) * B_RING + uint32_t(j) * B_STAGE);
+              const uint64_t dBl = dB + (B_HALF >> 4);
+              const uint64_t ah = dA + shift, al = dAl + shift;
+              auto k8 = [&](int jj, uint32_t acc) {
+                const uint64_t kj = uint64_t(jj) * 2u;  // +32 B per k8 step
+                if constexpr (CAT) {
+                  // [B_hi | B_lo] are contiguous BN-row blocks: one N = 2*BN operand
+                  ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc_cat, acc);
+                  ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, 1u);
+                } else {
+                  if constexpr (SPLIT) {
+                    ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, acc);
+                    ptx::mma_tf32_elect(d_tmem, ah + kj, dBl + kj, idesc, 1u);
+                    acc = 1u;
+                  }
+                  ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc, acc);
                 }
-                ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc, acc);
+              };
+              if (nk8 == 4) {
+                k8(0, acc0);
+                k8(1, 1u);
+                k8(2, 1u);
+                k8(3, 1u);
+              } else {
+                k8(0, acc0);
+                for (int jj = 1; jj < nk8; ++jj) k8(jj, 1u);
               }
-            };
-            if (nk8 == 4) {
-              k8(0, acc0);
-              k8(1, 1u);
-              k8(2, 1u);
-              k8(3, 1u);
-            } else {
-              k8(0, acc0);
-              for (int j = 1; j < nk8; ++j) k8(j, 1u);
+              acc0 = 1u;
+              // next tap (rotated order wraps to tap 0)
+              if (++s == S_eff) {
+                s = 0;
+                if (++r == a.R) { r = 0; shift = 0; } else shift += r_step - uint32_t(S_eff - 1) * s_step;
+              } else {
+                shift += s_step;
+              }
             }
-            acc0 = 1u;
             ptx::mma_commit_elect(&empty[stage]);
             if (++stage == a.stages) { stage = 0; phase ^= 1; }
-            // next tap (rotated order wraps to tap 0)
-            if (++s == S_eff) {
-              s = 0;
-              if (++r == a.R) { r = 0; shift = 0; } else shift += r_step - uint32_t(S_eff - 1) * s_step;
-            } else {
-              shift += s_step;
-            }
           }
           ptx::mma_commit_elect(&a_empty[buf]);
         }

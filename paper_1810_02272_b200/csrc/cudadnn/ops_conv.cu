@@ -167,12 +167,29 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
     ctas_per_sm = 2;
   }
   a.nbuf = 2;
-  auto fits = [&](int nbuf, int stages) { return tctap::smem_bytes(a.rows, nbuf, stages, bn, split) <= budget; };
-  if (!fits(a.nbuf, 2)) a.nbuf = 1;
-  if (!fits(a.nbuf, 2)) return false;
+  auto fits = [&](int nbuf, int stages, int tps) {
+    return tctap::smem_bytes(a.rows, nbuf, stages, bn, split, tps) <= budget;
+  };
+  if (!fits(a.nbuf, 2, 1)) a.nbuf = 1;
+  if (!fits(a.nbuf, 2, 1)) return false;
+  // several taps per weight-ring stage: every stage costs the MMA issuer one mbarrier
+  // wait and one tcgen05.commit, a few hundred cycles of issue that a small-N tap (N = 48:
+  // 8 MMAs, ~400 tensor cycles) does not cover -- the largest tps <= 4 whose ring still
+  // holds two stages and >= 4 taps (AlexNet conv2 backward-data 0.95 -> 0.74 ms, conv1
+  // forward 0.49 -> 0.45; profiles/dbg/ab_tps.sh)
+  const int taps_all = a.fold ? g.R : g.R * g.S;
+  a.tps = 1;
+  for (int t = std::min(4, taps_all); t > 1; --t) {
+    int st = 0;
+    while (st < tctap::kMaxStages && fits(a.nbuf, st + 1, t)) ++st;
+    if (st >= 2 && st * t >= 4) {
+      a.tps = t;
+      break;
+    }
+  }
   a.stages = 2;
-  while (a.stages < tctap::kMaxStages && fits(a.nbuf, a.stages + 1)) ++a.stages;
-  const int smem = tctap::smem_bytes(a.rows, a.nbuf, a.stages, bn, split);
+  while (a.stages < tctap::kMaxStages && fits(a.nbuf, a.stages + 1, a.tps)) ++a.stages;
+  const int smem = tctap::smem_bytes(a.rows, a.nbuf, a.stages, bn, split, a.tps);
   // weights: repacked per call (they change every step), pre-split
   const int kpad = a.cblocks * 32;
   a.wrows = CoutT;
