@@ -38,6 +38,15 @@ namespace cdnn {
 namespace tctap {
 
 constexpr int kThreads = 320;
+// Output-channel tiles 48..128 wide run a second MMA-issuing warp (warp 10): the two
+// issuers take alternate weight-ring stages into two TMEM accumulators (summed by the
+// epilogue), so each one's per-stage mbarrier wait and tcgen05.commit overlap the other
+// one's MMAs.  (192-wide tiles need the TMEM for double buffering; 32-wide tiles run
+// two CTAs per SM instead.)
+template <int BN>
+__host__ __device__ constexpr bool dual_issue() { return BN > 32 && BN <= 128; }
+template <int BN>
+__host__ __device__ constexpr int threads_for() { return dual_issue<BN>() ? 352 : 320; }
 constexpr int kMaxStages = 16;
 
 struct TapArgs {
@@ -59,6 +68,7 @@ struct TapArgs {
   int64_t out_nstride;   // image stride of `out`
   int nbuf, stages;      // A buffers (1|2), weight ring depth
   int tps;               // filter taps per weight-ring stage (one mbarrier wait + one commit per stage)
+  int dual;              // two MMA issuers (dual_issue<BN>() and >= 2 ring stages per tile)
   int relu;              // fused in-place ReLU in the epilogue (forward)
   int fold;              // S folded into the channels (k = s*Cin + c, Cin*S <= 32): R taps of K = S*Cin
   const float* gate;     // backward-data: fused in-place ReLU backward, out = gate > 0 ? out : 0 (same layout)
@@ -111,7 +121,7 @@ __device__ __forceinline__ void put_row8(uint32_t rbase, uint32_t lo_off, int ro
 }
 
 template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
+__global__ void __launch_bounds__(threads_for<BN>(), BN <= 32 ? 2 : 1)
     conv_tap_kernel(const __grid_constant__ CUtensorMap tm_w_hi, const __grid_constant__ CUtensorMap tm_w_lo,
                     const TapArgs a) {
   // 3xTF32 with BN <= 64: one MMA against [B_hi | B_lo] (N = 2*BN) gives A_hi*B_hi
@@ -120,7 +130,9 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
   // less A traffic (the A operand's shared-memory reads bound N <= 64 tiles).
   constexpr bool CAT = SPLIT && BN <= 64;
   constexpr int ACC = CAT ? 2 * BN : BN;  // accumulator columns per buffer
-  constexpr uint32_t TMEM_COLS = tc::tmem_cols_for(2 * ACC);
+  constexpr bool DUAL = dual_issue<BN>();
+  const int NI = DUAL && a.dual ? 2 : 1;  // MMA issuers = accumulators per TMEM buffer
+  constexpr uint32_t TMEM_COLS = tc::tmem_cols_for(2 * ACC * (DUAL ? 2 : 1));
   constexpr uint32_t B_STAGE = b_stage_bytes(BN, SPLIT);
   constexpr uint32_t B_HALF = uint32_t(BN) * 128u;
 
@@ -152,8 +164,8 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&a_full[b], 4);
-      ptx::mbar_init(&a_empty[b], 1);
-      ptx::mbar_init(&t_full[b], 1);
+      ptx::mbar_init(&a_empty[b], NI);
+      ptx::mbar_init(&t_full[b], NI);
       ptx::mbar_init(&t_empty[b], 4);
     }
     ptx::fence_mbar_init();
@@ -189,9 +201,11 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
           }
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
-    {
+  } else if (warp == 1 || (DUAL && warp == 10)) {
+    // ---------------- MMA issuer(s) (whole warp, one elected lane issues) ----------------
+    // Issuer pi takes the global ring stages g with g % NI == pi into accumulator pi.
+    const int pi = warp == 1 ? 0 : 1;
+    if (pi < NI) {
       constexpr uint32_t idesc = tc::make_idesc_tf32(BN);  // A, B K-major
       constexpr uint32_t idesc_cat = tc::make_idesc_tf32(2 * BN);
       // Everything the loop needs is derived from kernel parameters and loop
@@ -204,12 +218,13 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
       const uint32_t a0 = ptx::smem_u32(abase), b0 = ptx::smem_u32(bbase);
       int stage = 0;
       uint32_t phase = 0;
+      int gsel = 0;  // global stage counter modulo NI
       int aseq = 0, ts = 0;
       for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++ts) {
         const int acc_buf = ts & 1;
         if (ts >= 2) ptx::mbar_wait(&t_empty[acc_buf], uint32_t((ts >> 1) - 1) & 1u);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem + uint32_t(acc_buf * ACC);
+        const uint32_t d_tmem = tmem + uint32_t((acc_buf * NI + pi) * ACC);
         uint32_t acc0 = 0u;  // first MMA of the tile overwrites the accumulator
         for (int cb = 0; cb < a.cblocks; ++cb, ++aseq) {
           const int buf = aseq % a.nbuf;
@@ -222,39 +237,45 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
           const uint64_t dAl = dA + (A_HALF >> 4);
           uint32_t shift = shift_rot;
           int r = r_rot, s = s_rot;
+          bool used = false;
           for (int it = 0; it < taps; it += a.tps) {
             const int cnt = min(a.tps, taps - it);
-            ptx::mbar_wait(&full[stage], phase);
-            ptx::tc_fence_after();
+            const bool mine = gsel == pi;
+            if (mine) {
+              ptx::mbar_wait(&full[stage], phase);
+              ptx::tc_fence_after();
+            }
             for (int j = 0; j < cnt; ++j) {
-              const uint64_t dB = desc_sw128(b0 + uint32_t(stage) * B_RING + uint32_t(j) * B_STAGE);
-              const uint64_t dBl = dB + (B_HALF >> 4);
-              const uint64_t ah = dA + shift, al = dAl + shift;
-              auto k8 = [&](int jj, uint32_t acc) {
-                const uint64_t kj = uint64_t(jj) * 2u;  // +32 B per k8 step
-                if constexpr (CAT) {
-                  // [B_hi | B_lo] are contiguous BN-row blocks: one N = 2*BN operand
-                  ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc_cat, acc);
-                  ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, 1u);
-                } else {
-                  if constexpr (SPLIT) {
-                    ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, acc);
-                    ptx::mma_tf32_elect(d_tmem, ah + kj, dBl + kj, idesc, 1u);
-                    acc = 1u;
+              if (mine) {
+                const uint64_t dB = desc_sw128(b0 + uint32_t(stage) * B_RING + uint32_t(j) * B_STAGE);
+                const uint64_t dBl = dB + (B_HALF >> 4);
+                const uint64_t ah = dA + shift, al = dAl + shift;
+                auto k8 = [&](int jj, uint32_t acc) {
+                  const uint64_t kj = uint64_t(jj) * 2u;  // +32 B per k8 step
+                  if constexpr (CAT) {
+                    // [B_hi | B_lo] are contiguous BN-row blocks: one N = 2*BN operand
+                    ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc_cat, acc);
+                    ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, 1u);
+                  } else {
+                    if constexpr (SPLIT) {
+                      ptx::mma_tf32_elect(d_tmem, al + kj, dB + kj, idesc, acc);
+                      ptx::mma_tf32_elect(d_tmem, ah + kj, dBl + kj, idesc, 1u);
+                      acc = 1u;
+                    }
+                    ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc, acc);
                   }
-                  ptx::mma_tf32_elect(d_tmem, ah + kj, dB + kj, idesc, acc);
+                };
+                if (nk8 == 4) {
+                  k8(0, acc0);
+                  k8(1, 1u);
+                  k8(2, 1u);
+                  k8(3, 1u);
+                } else {
+                  k8(0, acc0);
+                  for (int jj = 1; jj < nk8; ++jj) k8(jj, 1u);
                 }
-              };
-              if (nk8 == 4) {
-                k8(0, acc0);
-                k8(1, 1u);
-                k8(2, 1u);
-                k8(3, 1u);
-              } else {
-                k8(0, acc0);
-                for (int jj = 1; jj < nk8; ++jj) k8(jj, 1u);
+                acc0 = 1u;
               }
-              acc0 = 1u;
               // next tap (rotated order wraps to tap 0)
               if (++s == S_eff) {
                 s = 0;
@@ -263,13 +284,19 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
                 shift += s_step;
               }
             }
-            ptx::mma_commit_elect(&empty[stage]);
+            if (mine) {
+              ptx::mma_commit_elect(&empty[stage]);
+              used = true;
+            }
             if (++stage == a.stages) { stage = 0; phase ^= 1; }
+            if (++gsel == NI) gsel = 0;
           }
-          ptx::mma_commit_elect(&a_empty[buf]);
+          if (used) ptx::mma_commit_elect(&a_empty[buf]);
+          else if (lane == 0) ptx::mbar_arrive(&a_empty[buf]);  // this issuer read nothing of it
+          __syncwarp();
         }
         ptx::mma_commit_elect(&t_full[acc_buf]);
-        if (lane == 0) TAP_TRACE(3 + 3 * ts);
+        if (lane == 0 && pi == 0) TAP_TRACE(3 + 3 * ts);
       }
     }
     __syncwarp();
@@ -405,13 +432,28 @@ __global__ void __launch_bounds__(kThreads, BN <= 32 ? 2 : 1)
       // One output chunk: 16 accumulator columns -> (+ bias, ReLU, gate) -> NCHW stores.
       auto store_chunk = [&](int cc, const float (&gv)[16]) {
         uint32_t r[16];
-        ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * ACC + cc), r);
+        const uint32_t lane_base = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * NI * ACC + cc);
+        ptx::tmem_ld16(lane_base, r);
         if constexpr (CAT) {
           uint32_t r2[16];
-          ptx::tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + uint32_t(acc_buf * ACC + BN + cc), r2);
+          ptx::tmem_ld16(lane_base + BN, r2);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+        }
+        if (DUAL && NI == 2) {  // second issuer's accumulator (and its [hi | lo] halves)
+          uint32_t r3[16];
+          ptx::tmem_ld16(lane_base + ACC, r3);
+          if constexpr (CAT) {
+            uint32_t r4[16];
+            ptx::tmem_ld16(lane_base + ACC + BN, r4);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r3[j] = __float_as_uint(__uint_as_float(r3[j]) + __uint_as_float(r4[j]));
+          }
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r3[j]));
         }
         ptx::tmem_ld_wait();
         if (valid) {

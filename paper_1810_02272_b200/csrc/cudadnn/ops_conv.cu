@@ -67,7 +67,7 @@ void launch_conv_tap(Ctx* c, cudaStream_t st, dim3 grid, int smem, const CUtenso
     CDNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_smem[c->device & 15] = smem;
   }
-  kern<<<grid, tctap::kThreads, smem, st>>>(twh, twl, a);
+  kern<<<grid, tctap::threads_for<BN>(), smem, st>>>(twh, twl, a);
   check_launch("conv_tap_kernel");
   count_launch(c);
 }
@@ -190,6 +190,11 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   a.stages = 2;
   while (a.stages < tctap::kMaxStages && fits(a.nbuf, a.stages + 1, a.tps)) ++a.stages;
   const int smem = tctap::smem_bytes(a.rows, a.nbuf, a.stages, bn, split, a.tps);
+  // two MMA issuers on alternate ring stages when every tile has at least two stages
+  // (AlexNet conv2 forward 0.67 -> 0.52 ms, backward-data 0.79 -> 0.68, conv1 forward
+  // 0.48 -> 0.43; profiles/dbg/ab_dual.sh)
+  const bool dual_bn = bn > 32 && bn <= 128;
+  a.dual = dual_bn && a.cblocks * ((taps_all + a.tps - 1) / a.tps) >= 2 ? 1 : 0;
   // weights: repacked per call (they change every step), pre-split
   const int kpad = a.cblocks * 32;
   a.wrows = CoutT;
