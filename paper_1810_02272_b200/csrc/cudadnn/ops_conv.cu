@@ -189,12 +189,19 @@ bool conv_tap(Ctx* c, const ConvDescSlot& dconst, bool backward_data, const floa
   }
   a.stages = 2;
   while (a.stages < tctap::kMaxStages && fits(a.nbuf, a.stages + 1, a.tps)) ++a.stages;
-  const int smem = tctap::smem_bytes(a.rows, a.nbuf, a.stages, bn, split, a.tps);
+  int smem = tctap::smem_bytes(a.rows, a.nbuf, a.stages, bn, split, a.tps);
   // two MMA issuers on alternate ring stages when every tile has at least two stages
-  // (AlexNet conv2 forward 0.67 -> 0.52 ms, backward-data 0.79 -> 0.68, conv1 forward
-  // 0.48 -> 0.43; profiles/dbg/ab_dual.sh)
+  // (AlexNet conv2 backward-data 0.79 -> 0.68 ms, conv1 forward 0.48 -> 0.43, conv3
+  // backward-data 0.39 -> 0.36; profiles/dbg/ab_dual.sh, iter_dual2.sh)
   const bool dual_bn = bn > 32 && bn <= 128;
   a.dual = dual_bn && a.cblocks * ((taps_all + a.tps - 1) / a.tps) >= 2 ? 1 : 0;
+  // an even ring: issuer g % 2 always owns the same slots (slot % 2) and so waits on every
+  // phase of them -- with an odd ring an issuer would skip phases, and a parity wait can
+  // then return on a phase two fills old
+  if (a.dual && (a.stages & 1)) {
+    --a.stages;
+    smem = tctap::smem_bytes(a.rows, a.nbuf, a.stages, bn, split, a.tps);
+  }
   // weights: repacked per call (they change every step), pre-split
   const int kpad = a.cblocks * 32;
   a.wrows = CoutT;
