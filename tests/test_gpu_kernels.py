@@ -111,7 +111,9 @@ CONV_CASES = [
     (2, 96, 15, 15, 256, 5, 1, 2, 1, 2),    # AlexNet conv2 (backward-data to 48 channels: N = 48 tiles)
     (2, 384, 13, 13, 384, 3, 1, 1, 1, 2),   # AlexNet conv4 (192 per group: N = 96 tiles)
     (100, 32, 16, 16, 32, 5, 1, 2, 1, 1),   # CIFAR-quick conv2 at bench size (split-K clusters of 8 CTAs)
-    (64, 16, 32, 32, 16, 3, 1, 1, 1, 1),    # ResNet-20 stage 1, half the bench batch (split-K clusters)
+    (64, 16, 32, 32, 16, 3, 1, 1, 1, 1),    # ResNet-20 stage 1, half the bench batch
+    (3, 96, 9, 9, 64, 1, 1, 0, 1, 1),       # dual MMA issuers, one-tap blocks: the issuers alternate blocks
+    (5, 32, 13, 13, 64, 3, 1, 1, 1, 1),     # dual MMA issuers, 3 ring stages per tile: parity alternates per tile
 ]
 
 
