@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
 // tensors are < 2^31 elements: fusable()); the pixel's <= R x R window offsets into
 // the pooled plane are computed once.
 template <typename T, int SIZE, int K, int S>
-__global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
+__global__ void __launch_bounds__(256, 2) lrn_maxpool_bwd(const T* __restrict__ x, const T* __restrict__ pdy,
                                                        const int* __restrict__ mask, T* __restrict__ dx,
                                                        LrnPoolGeom g, T alpha, T beta, T k, bool gate_x) {
   constexpr int pre = (SIZE - 1) / 2, post = SIZE - 1 - pre;
@@ -297,7 +297,76 @@ __global__ void __launch_bounds__(256) lrn_maxpool_bwd(const T* __restrict__ x, 
     load_x(cs0, nx);
     load_x(cs0 + kG, nx2);
     load_g(cs0, nm, nv);
-    for (int c0 = cs0; c0 < cs1; c0 += kG) {
+    int c0 = cs0;
+    // Fast path (the interior of the segment): steps whose channels, entering channels and
+    // prefetches are all in range run without bounds tests, address the tensors with
+    // running 32-bit offsets, and are unrolled over SIZE steps so the rings rotate back
+    // to their registers (no moves).  Same values, same operations as the general loop
+    // below (which finishes the segment): bit-identical.  The general loop's integer and
+    // move work was ~half of this issue-bound kernel's instructions.
+    {
+      uint32_t ox = uint32_t(c0 + 2 * kG + SIZE - 1) * HW;  // next x prefetch (channel c0 + 2kG + SIZE - 1)
+      uint32_t og = uint32_t(c0 + kG + pre) * PHW + woff0;  // next gather (channel c0 + kG + pre)
+      uint32_t od = uint32_t(c0) * HW;                      // dx of channel c0
+      while (c0 + (SIZE + 2) * kG <= cs1 && c0 + (SIZE + 2) * kG + SIZE - 2 < g.C) {
+#pragma unroll
+        for (int st = 0; st < SIZE; ++st) {
+          T cx[kG];
+          int cm[kG][R][R];
+          T cv[kG][R][R];
+#pragma unroll
+          for (int u = 0; u < kG; ++u) {
+            cx[u] = nx[u];
+            nx[u] = nx2[u];
+#pragma unroll
+            for (int a = 0; a < R; ++a)
+#pragma unroll
+              for (int b = 0; b < R; ++b) { cm[u][a][b] = nm[u][a][b]; cv[u][a][b] = nv[u][a][b]; }
+          }
+#pragma unroll
+          for (int u = 0; u < kG; ++u) nx2[u] = __ldg(xp + (ox + uint32_t(u) * HW));
+#pragma unroll
+          for (int u = 0; u < kG; ++u)
+#pragma unroll
+            for (int a = 0; a < R; ++a)
+#pragma unroll
+              for (int b = 0; b < R; ++b) {
+                const uint32_t o = og + uint32_t(u) * PHW + uint32_t(a * g.PW + b);
+                nm[u][a][b] = wok[a][b] ? __ldg(mp + o) : -1;
+                nv[u][a][b] = wok[a][b] ? __ldg(dp + o) : T(0);
+              }
+          ox += uint32_t(kG) * HW;
+          og += uint32_t(kG) * PHW;
+#pragma unroll
+          for (int u = 0; u < kG; ++u) {
+            xr[SIZE - 1] = cx[u];
+#pragma unroll
+            for (int j = 0; j + 1 < SIZE; ++j) { tr[j] = tr[j + 1]; dyr[j] = dyr[j + 1]; npr[j] = npr[j + 1]; }
+            T sum = T(0);
+#pragma unroll
+            for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xr[j]);
+            const T sc = lrn::scale(sum, aN, k);
+            const T np = lrn::neg_pow(sc, beta);
+            const T yv = lrn::top(xr[pre], np);
+            const T d = ndy_of(cm[u], cv[u]);
+            dyr[SIZE - 1] = d;
+            npr[SIZE - 1] = np;
+            tr[SIZE - 1] = lrn::term(d, yv, sc);
+            T acc = T(0);
+#pragma unroll
+            for (int j = 0; j < SIZE; ++j) acc = lrn::add_(acc, tr[j]);
+            const T xc = xr[0];
+            const T gval = lrn::grad(dyr[post], npr[post], coef, xc, acc);
+            dxp[od] = (!gate_x || xc > T(0)) ? gval : T(0);
+            od += HW;
+#pragma unroll
+            for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
+          }
+          c0 += kG;
+        }
+      }
+    }
+    for (; c0 < cs1; c0 += kG) {
       T cx[kG];
       int cm[kG][R][R];
       T cv[kG][R][R];
