@@ -118,7 +118,66 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
       for (int b = 0; b < K; ++b)
         if (hs + a < g.H && ws + b < g.W) wbits0 |= 1u << (a * K + b);
   }
-  for (int c0 = cs0, step = 0; c0 < cs1; c0 += kG, ++step) {
+  int c0 = cs0, step = 0;
+  // Fast path (block-uniform: depends on the segment only): steps whose channels and
+  // next loads are all in range run without bounds tests, with running 32-bit offsets,
+  // unrolled over SIZE steps so the x ring rotates back to its registers.  Same values,
+  // same operations and barriers as the general loop below: bit-identical.
+  {
+    uint32_t oxn = uint32_t(c0 + kG + post + 1) * uint32_t(HW);  // next step's first loaded channel
+    uint32_t oy = uint32_t(c0) * uint32_t(HW);
+    uint32_t opool = (uint32_t(img) * g.C + c0 + u0) * uint32_t(PHW) + uint32_t(po0);
+    const bool extra_items = kG * per_u > int(blockDim.x);
+    while (!extra_items && c0 + (SIZE + 1) * kG <= cs1 && c0 + (SIZE + 1) * kG + post < g.C) {
+#pragma unroll
+      for (int st = 0; st < SIZE; ++st) {
+        T cur[kG];
+#pragma unroll
+        for (int u = 0; u < kG; ++u) cur[u] = nxt[u];
+#pragma unroll
+        for (int u = 0; u < kG; ++u) nxt[u] = active ? __ldg(xp + (oxn + uint32_t(u) * uint32_t(HW))) : T(0);
+        oxn += uint32_t(kG) * uint32_t(HW);
+        T* buf = tile + (step & 1) * kG * tsz;
+        if (active) {
+#pragma unroll
+          for (int u = 0; u < kG; ++u) {
+            T sum = T(0);
+#pragma unroll
+            for (int j = 0; j < SIZE; ++j) sum = lrn::sq_acc(sum, xr[j]);
+            const T sc = lrn::scale(sum, aN, k);
+            const T yv = lrn::top(xr[pre], lrn::neg_pow(sc, beta));
+            buf[u * tsz + p] = yv;
+            if (own) yp[oy + uint32_t(u) * uint32_t(HW)] = yv;
+#pragma unroll
+            for (int j = 0; j + 1 < SIZE; ++j) xr[j] = xr[j + 1];
+            xr[SIZE - 1] = cur[u];
+          }
+        }
+        oy += uint32_t(kG) * uint32_t(HW);
+        __syncthreads();
+        if (has0) {
+          const T* t = buf + toff0;
+          T best = sizeof(T) == 4 ? T(-3.402823466e+38f) : T(-1.7976931348623157e+308);
+          int arg = -1;
+#pragma unroll
+          for (int a = 0; a < K; ++a)
+#pragma unroll
+            for (int b = 0; b < K; ++b) {
+              if (wbits0 & (1u << (a * K + b))) {
+                const T v = t[a * g.W + b];
+                if (v > best) { best = v; arg = abase0 + a * g.W + b; }
+              }
+            }
+          ypool[opool] = relu ? (best > T(0) ? best : T(0)) : best;
+          mask[opool] = arg;
+        }
+        opool += uint32_t(kG) * uint32_t(PHW);
+        c0 += kG;
+        ++step;
+      }
+    }
+  }
+  for (; c0 < cs1; c0 += kG, ++step) {
     T cur[kG];
 #pragma unroll
     for (int u = 0; u < kG; ++u) cur[u] = nxt[u];

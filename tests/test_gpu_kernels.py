@@ -492,7 +492,9 @@ def test_pool_fixed_window_kernels_equal_generic():
                                               (2, 40, 27, 27, 5, 3, 2),   # norm2 -> pool2 shape
                                               (2, 7, 13, 11, 3, 3, 2),    # ragged, C not a multiple of 4
                                               (2, 6, 12, 10, 5, 2, 2),    # 2x2/2 windows
-                                              (1, 3, 9, 9, 5, 3, 2)])     # fewer channels than the window
+                                              (1, 3, 9, 9, 5, 3, 2),      # fewer channels than the window
+                                              (1, 256, 13, 13, 3, 3, 2),  # two 128-channel segments, fast paths
+                                              (2, 130, 15, 15, 5, 3, 2)])  # a 2-channel second segment
 def test_lrn_pool_fused_bit_identical_to_unfused(ctx, dtype, n, c, h, w, size, k, s):
     """cdnn_lrn_pool_forward / _backward (ops_lrnpool.cu) == LRN then MAX pooling, bit
     for bit: the LRN top, the pooled top, the argmax mask and the bottom gradient
