@@ -7,7 +7,7 @@
 #  5. ncu --set full metrics of conv2's backward kernels and conv1 forward (summaries only)
 # Each ncu command runs only after the same command exited 0 without ncu.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-O=gpurun_out/fin4
+O=gpurun_out/fin5
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; echo tests rc=$?; tail -2 $O/gpu_tests.log
 bash profiles/dbg/bench_all.sh $O/bench
