@@ -26,11 +26,18 @@
 // pixel, in max_pool_bwd_k's order), then dx(c) from the rings of lrn_bwd_ring.
 #include "launch.cuh"
 #include "lrn_math.cuh"
+#include "ptx.cuh"
 
 namespace cdnn {
 namespace {
 
 constexpr int kG = 4;     // channels per step (loads in flight; one block barrier per step)
+// forward fast path: x prefetched kPF - 1 steps ahead into a per-thread shared-memory ring
+// by cp.async (the loads hold no registers while in flight; one step of register
+// lookahead left too few bytes in flight at two 512-thread blocks per SM).  AlexNet
+// norm1+pool1 / norm2+pool2 forward, ms: register lookahead 0.205 / 0.150; ring depth
+// 2: 0.194 / 0.142, 3: 0.183 / 0.129, 4: 0.187 / 0.131, 6: 0.199 / 0.133, 8: 0.205 / 0.140
+constexpr int kPF = 3;
 #ifndef CDNN_LRN_FWD_SEG
 #define CDNN_LRN_FWD_SEG 128
 #endif
@@ -123,20 +130,45 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
   // next loads are all in range run without bounds tests, with running 32-bit offsets,
   // unrolled over SIZE steps so the x ring rotates back to its registers.  Same values,
   // same operations and barriers as the general loop below: bit-identical.
-  {
-    uint32_t oxn = uint32_t(c0 + kG + post + 1) * uint32_t(HW);  // next step's first loaded channel
+  auto fast_ok = [&](int cc) {
+    return cc + (SIZE + 1) * kG <= cs1 && cc + (SIZE + kPF - 1) * kG + post < g.C;
+  };
+  const bool extra_items = kG * per_u > int(blockDim.x);
+  if (!extra_items && fast_ok(c0)) {
+    // prefetch ring: slot j holds a step's kG entering channels, [slot][u][thread]
+    T* pf = tile + 2 * kG * tsz;
+    const uint32_t pf0 = ptx::smem_u32(pf) + uint32_t(threadIdx.x) * uint32_t(sizeof(T));
+    const uint32_t pf_u = uint32_t(blockDim.x) * uint32_t(sizeof(T)), pf_slot = uint32_t(kG) * pf_u;
+    const uint32_t pbytes = active ? uint32_t(sizeof(T)) : 0u;  // zero-fill for idle threads
+    uint32_t oxn = uint32_t(c0 + kG + post + 1) * uint32_t(HW);  // step c0 + kG's first entering channel
+    auto prefetch = [&](uint32_t slot) {  // the step at oxn into `slot`, one cp.async group
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const uint32_t dst = pf0 + slot * pf_slot + uint32_t(u) * pf_u;
+        const T* src = xp + (oxn + uint32_t(u) * uint32_t(HW));
+        if constexpr (sizeof(T) == 4) ptx::cp_async_4(dst, src, pbytes);
+        else ptx::cp_async_8(dst, src, pbytes);
+      }
+      ptx::cp_async_commit();
+      oxn += uint32_t(kG) * uint32_t(HW);
+    };
+    // slot 0: step c0 (already in registers); slots 1 .. kPF-1: the next steps
+#pragma unroll
+    for (int u = 0; u < kG; ++u) pf[u * blockDim.x + threadIdx.x] = nxt[u];
+#pragma unroll
+    for (int j = 1; j < kPF; ++j) prefetch(uint32_t(j));
+    uint32_t slot = 0;
     uint32_t oy = uint32_t(c0) * uint32_t(HW);
     uint32_t opool = (uint32_t(img) * g.C + c0 + u0) * uint32_t(PHW) + uint32_t(po0);
-    const bool extra_items = kG * per_u > int(blockDim.x);
-    while (!extra_items && c0 + (SIZE + 1) * kG <= cs1 && c0 + (SIZE + 1) * kG + post < g.C) {
+    while (fast_ok(c0)) {
 #pragma unroll
       for (int st = 0; st < SIZE; ++st) {
         T cur[kG];
+        ptx::cp_async_wait<kPF - 2>();  // this step's group has landed
 #pragma unroll
-        for (int u = 0; u < kG; ++u) cur[u] = nxt[u];
-#pragma unroll
-        for (int u = 0; u < kG; ++u) nxt[u] = active ? __ldg(xp + (oxn + uint32_t(u) * uint32_t(HW))) : T(0);
-        oxn += uint32_t(kG) * uint32_t(HW);
+        for (int u = 0; u < kG; ++u) cur[u] = pf[(slot * kG + u) * blockDim.x + threadIdx.x];
+        prefetch(slot);  // the step kPF - 1 ahead into the slot just read
+        slot = slot + 1 == uint32_t(kPF) ? 0u : slot + 1;
         T* buf = tile + (step & 1) * kG * tsz;
         if (active) {
 #pragma unroll
@@ -176,6 +208,10 @@ __global__ void __launch_bounds__(1024) lrn_maxpool_fwd(const T* __restrict__ x,
         ++step;
       }
     }
+    // the general loop continues with step c0's values in registers
+    ptx::cp_async_wait_all();
+#pragma unroll
+    for (int u = 0; u < kG; ++u) nxt[u] = pf[(slot * kG + u) * blockDim.x + threadIdx.x];
   }
   for (; c0 < cs1; c0 += kG, ++step) {
     T cur[kG];
@@ -503,7 +539,13 @@ void launch_fwd(Ctx* c, cudaStream_t st, const PoolDescSlot& d, const T* x, T* y
                 double beta, double k, bool relu) {
   const LrnPoolGeom g = lrn_pool_geom(d, 1024);
   const int threads = ((g.rows_in * g.W + 31) / 32) * 32;
-  const size_t smem = size_t(2) * kG * g.rows_in * g.W * sizeof(T);
+  const size_t smem = (size_t(2) * kG * g.rows_in * g.W + size_t(kPF) * kG * threads) * sizeof(T);
+  static size_t attr_smem[16] = {};
+  if (smem > 48 * 1024 && attr_smem[c->device & 15] < smem) {
+    CDNN_CUDA(cudaFuncSetAttribute(lrn_maxpool_fwd<T, SIZE, K, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    attr_smem[c->device & 15] = smem;
+  }
   lrn_maxpool_fwd<T, SIZE, K, S><<<dim3(g.bands, g.segs, g.N), threads, smem, st>>>(x, yn, yp, m, g, T(alpha),
                                                                                     T(beta), T(k), relu);
   check_launch("lrn_maxpool_fwd");
