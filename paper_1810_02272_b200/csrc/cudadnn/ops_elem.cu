@@ -24,22 +24,78 @@ template <typename T> __device__ __forceinline__ T sub_rn(T a, T b);
 template <> __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 template <> __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
+// The elementwise kernels below move 16-byte packs (4 floats / 2 doubles) when every
+// pointer is 16-byte aligned (whole-buffer calls always are), the tail and unaligned
+// views element by element; the arithmetic per element is unchanged.  The scalar
+// grid-stride form reached 3.7 TB/s on a 158 MB copy, a third below the HBM copy rate.
+template <typename T>
+struct alignas(16) Pack {
+  static constexpr int W = 16 / int(sizeof(T));
+  T v[W];
+};
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+template <typename T>
+__device__ __forceinline__ Pack<T> ld_pack(const T* p, uint64_t j) { return reinterpret_cast<const Pack<T>*>(p)[j]; }
+template <typename T>
+__device__ __forceinline__ void st_pack(T* p, uint64_t j, const Pack<T>& v) { reinterpret_cast<Pack<T>*>(p)[j] = v; }
+
 template <typename T>
 __global__ void fill_kernel(T* __restrict__ d, uint64_t n, T v) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) d[i] = v;
+  constexpr int W = Pack<T>::W;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (aligned16(d)) {
+    Pack<T> pv;
+#pragma unroll
+    for (int e = 0; e < W; ++e) pv.v[e] = v;
+    for (uint64_t j = i; j < n / W; j += stride) st_pack(d, j, pv);
+    i += n / W * W;
+  }
+  for (; i < n; i += stride) d[i] = v;
 }
 template <typename T>
 __global__ void copy_kernel(const T* __restrict__ s, T* __restrict__ d, uint64_t n) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) d[i] = s[i];
+  constexpr int W = Pack<T>::W;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (aligned16(s) && aligned16(d)) {
+    for (uint64_t j = i; j < n / W; j += stride) st_pack(d, j, ld_pack(s, j));
+    i += n / W * W;
+  }
+  for (; i < n; i += stride) d[i] = s[i];
 }
 template <typename T>
 __global__ void scal_kernel(T* __restrict__ x, uint64_t n, T a) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) x[i] = mul_rn(x[i], a);
+  constexpr int W = Pack<T>::W;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (aligned16(x)) {
+    for (uint64_t j = i; j < n / W; j += stride) {
+      Pack<T> v = ld_pack(x, j);
+#pragma unroll
+      for (int e = 0; e < W; ++e) v.v[e] = mul_rn(v.v[e], a);
+      st_pack(x, j, v);
+    }
+    i += n / W * W;
+  }
+  for (; i < n; i += stride) x[i] = mul_rn(x[i], a);
 }
 template <typename T>
 __global__ void axpy_kernel(const T* __restrict__ x, T* __restrict__ y, uint64_t n, T a) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    y[i] = add_rn(y[i], mul_rn(a, x[i]));
+  constexpr int W = Pack<T>::W;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (aligned16(x) && aligned16(y)) {
+    for (uint64_t j = i; j < n / W; j += stride) {
+      const Pack<T> xv = ld_pack(x, j);
+      Pack<T> yv = ld_pack(y, j);
+#pragma unroll
+      for (int e = 0; e < W; ++e) yv.v[e] = add_rn(yv.v[e], mul_rn(a, xv.v[e]));
+      st_pack(y, j, yv);
+    }
+    i += n / W * W;
+  }
+  for (; i < n; i += stride) y[i] = add_rn(y[i], mul_rn(a, x[i]));
 }
 // Fan-out / fan-in of Split and Eltwise SUM (up to kFan blobs) in one pass: every
 // destination written from one read of the source (Split forward, Eltwise backward:
@@ -53,7 +109,28 @@ struct FanPtrs {
 };
 template <typename T>
 __global__ void fan_out_kernel(const T* __restrict__ x, FanPtrs<T> d, int nd, bool scaled, uint64_t n) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+  constexpr int W = Pack<T>::W;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  bool al = aligned16(x);
+#pragma unroll
+  for (int k = 0; k < kFan; ++k)
+    if (k < nd && d.p[k]) al = al && aligned16(d.p[k]);
+  if (al) {
+    for (uint64_t j = i; j < n / W; j += stride) {
+      const Pack<T> v = ld_pack(x, j);
+#pragma unroll
+      for (int k = 0; k < kFan; ++k)
+        if (k < nd && d.p[k]) {
+          Pack<T> o;
+#pragma unroll
+          for (int e = 0; e < W; ++e) o.v[e] = scaled ? mul_rn(d.a[k], v.v[e]) : v.v[e];
+          st_pack(d.p[k], j, o);
+        }
+    }
+    i += n / W * W;
+  }
+  for (; i < n; i += stride) {
     const T v = x[i];
 #pragma unroll
     for (int k = 0; k < kFan; ++k)
@@ -62,7 +139,28 @@ __global__ void fan_out_kernel(const T* __restrict__ x, FanPtrs<T> d, int nd, bo
 }
 template <typename T>
 __global__ void fan_in_kernel(FanPtrs<T> s, int ns, T* __restrict__ y, uint64_t n) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+  constexpr int W = Pack<T>::W;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  bool al = aligned16(y);
+#pragma unroll
+  for (int k = 0; k < kFan; ++k)
+    if (k < ns) al = al && aligned16(s.p[k]);
+  if (al) {
+    for (uint64_t j = i; j < n / W; j += stride) {
+      Pack<T> acc = ld_pack<T>(s.p[0], j);
+#pragma unroll
+      for (int k = 1; k < kFan; ++k)
+        if (k < ns) {
+          const Pack<T> v = ld_pack<T>(s.p[k], j);
+#pragma unroll
+          for (int e = 0; e < W; ++e) acc.v[e] = add_rn(acc.v[e], mul_rn(T(1), v.v[e]));
+        }
+      st_pack(y, j, acc);
+    }
+    i += n / W * W;
+  }
+  for (; i < n; i += stride) {
     T acc = s.p[0][i];
 #pragma unroll
     for (int k = 1; k < kFan; ++k)
