@@ -240,6 +240,19 @@ __global__ void bump_kernel(unsigned long long* iter) { *iter += 1; }
 
 enum ChanOp { kSumSq = 0, kSumDot = 1 };  // (x, x*x) | (a, a*b)
 
+// 16-byte packs (4 floats / 2 doubles): the per-channel passes walk a block's planes as
+// one flat run of packs (HW % W == 0: no pack crosses a plane), so every thread is busy
+// even on 8 x 8 planes (a thread per plane element left 3/4 of a 256-thread block idle)
+template <typename T>
+struct alignas(16) Pk {
+  static constexpr int W = 16 / int(sizeof(T));
+  T v[W];
+};
+template <typename T>
+__device__ __forceinline__ bool packable(const T* p, int HW) {
+  return HW % Pk<T>::W == 0 && (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
 template <typename T, int OP>
 __global__ void __launch_bounds__(kT) chan_partials(const T* __restrict__ u, const T* __restrict__ w, double2* part,
                                                     int N, int C, int HW, int splits) {
@@ -247,12 +260,32 @@ __global__ void __launch_bounds__(kT) chan_partials(const T* __restrict__ u, con
   const int c = blockIdx.x, sp = blockIdx.y;
   const int n0 = int(int64_t(N) * sp / splits), n1 = int(int64_t(N) * (sp + 1) / splits);
   double s0 = 0, s1 = 0;
-  for (int n = n0; n < n1; ++n) {
-    const int64_t off = (int64_t(n) * C + c) * HW;
-    for (int i = threadIdx.x; i < HW; i += kT) {
-      const double a = double(u[off + i]);
-      if (OP == kSumSq) { s0 += a; s1 += a * a; }
-      else { s0 += a; s1 += a * double(w[off + i]); }
+  constexpr int W = Pk<T>::W;
+  if (packable(u, HW) && (OP == kSumSq || packable(w, HW))) {
+    const uint32_t hwv = uint32_t(HW / W), total = uint32_t(n1 - n0) * hwv;
+    const Pk<T>* up = reinterpret_cast<const Pk<T>*>(u);
+    const Pk<T>* wp = reinterpret_cast<const Pk<T>*>(w);
+    for (uint32_t j = threadIdx.x; j < total; j += kT) {
+      const uint32_t k = j / hwv, i = j - k * hwv;
+      const int64_t off = (int64_t(n0 + int(k)) * C + c) * hwv + i;
+      const Pk<T> a = up[off];
+      if (OP == kSumSq) {
+#pragma unroll
+        for (int e = 0; e < W; ++e) { const double v = double(a.v[e]); s0 += v; s1 += v * v; }
+      } else {
+        const Pk<T> b = wp[off];
+#pragma unroll
+        for (int e = 0; e < W; ++e) { const double v = double(a.v[e]); s0 += v; s1 += v * double(b.v[e]); }
+      }
+    }
+  } else {
+    for (int n = n0; n < n1; ++n) {
+      const int64_t off = (int64_t(n) * C + c) * HW;
+      for (int i = threadIdx.x; i < HW; i += kT) {
+        const double a = double(u[off + i]);
+        if (OP == kSumSq) { s0 += a; s1 += a * a; }
+        else { s0 += a; s1 += a * double(w[off + i]); }
+      }
     }
   }
   sh0[threadIdx.x] = s0;
@@ -263,6 +296,25 @@ __global__ void __launch_bounds__(kT) chan_partials(const T* __restrict__ u, con
     __syncthreads();
   }
   if (threadIdx.x == 0) part[int64_t(c) * splits + sp] = make_double2(sh0[0], sh1[0]);
+}
+
+// A channel-major elementwise pass: block (c, sp) covers channel c of images
+// [n0, n1) (the chan_partials split), f(base offset, count) applied pack by pack
+template <typename T, class F>
+__device__ __forceinline__ void chan_apply(int N, int C, int HW, int splits, bool packed, F f) {
+  const int c = blockIdx.x, sp = blockIdx.y;
+  const int n0 = int(int64_t(N) * sp / splits), n1 = int(int64_t(N) * (sp + 1) / splits);
+  if (packed) {
+    constexpr int W = Pk<T>::W;
+    const uint32_t hwv = uint32_t(HW / W), total = uint32_t(n1 - n0) * hwv;
+    for (uint32_t j = threadIdx.x; j < total; j += kT) {
+      const uint32_t k = j / hwv, i = j - k * hwv;
+      f((int64_t(n0 + int(k)) * C + c) * hwv + i, std::integral_constant<bool, true>{});
+    }
+  } else {
+    for (int n = n0; n < n1; ++n)
+      for (int i = threadIdx.x; i < HW; i += kT) f((int64_t(n) * C + c) * HW + i, std::integral_constant<bool, false>{});
+  }
 }
 
 __device__ __forceinline__ double2 sum_parts(const double2* part, int c, int splits) {
@@ -343,20 +395,6 @@ __global__ void scale_bwd_data(const T* __restrict__ dy, const T* __restrict__ g
 }
 
 // ---- fused BatchNorm + Scale (z = gamma*xn + beta, xn = (x - mean)*invstd) ----------
-template <typename T>
-__global__ void bn_scale_apply(const T* __restrict__ x, const T* __restrict__ mean, const T* __restrict__ invstd,
-                               const T* __restrict__ g, const T* __restrict__ bta, T* __restrict__ xn,
-                               T* __restrict__ z, int C, int HW) {
-  const int c = blockIdx.y % C;
-  const T m = mean[c], is = invstd[c], gc = g[c], bc = bta ? bta[c] : T(0);
-  const int64_t off = int64_t(blockIdx.y) * HW;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) {
-    const T v = (x[off + i] - m) * is;
-    xn[off + i] = v;
-    z[off + i] = v * gc + bc;
-  }
-}
-
 // backward sums (S0 = sum dz, S1 = sum dz*xn): dbeta += S0, dgamma += S1,
 // a = S0/M, b = S1/M for dx = gamma*invstd*(dz - a - xn*b)
 template <typename T>
@@ -370,15 +408,98 @@ __global__ void bn_scale_finalize(const double2* part, int splits, int C, double
   b[c] = T(s.y / cnt);
 }
 
+// The channel's split partials summed by warp 0 (lane-strided, then a fixed xor tree):
+// one round of parallel loads instead of `splits` dependent ones; deterministic.
+__device__ __forceinline__ double2 sum_parts_warp(const double2* part, int c, int splits) {
+  double s0 = 0, s1 = 0;
+  for (int k = int(threadIdx.x); k < splits; k += 32) {
+    const double2 v = part[int64_t(c) * splits + k];
+    s0 += v.x;
+    s1 += v.y;
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, m);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, m);
+  }
+  return make_double2(s0, s1);
+}
+
+// Fused BatchNorm + Scale passes on the chan_partials grid with the finalize folded in:
+// each block sums the channel's split partials (bn_finalize's / bn_scale_finalize's
+// formulas), block (c, 0) stores the statistics / accumulates dgamma,
+// dbeta -- two launches per pass instead of three.
 template <typename T>
-__global__ void bn_scale_bwd_apply(const T* __restrict__ xn, const T* __restrict__ dz, const T* __restrict__ a,
-                                   const T* __restrict__ b, const T* __restrict__ invstd, const T* __restrict__ g,
-                                   T* __restrict__ dx, int C, int HW) {
-  const int c = blockIdx.y % C;
-  const T ac = a[c], bc = b[c], k = invstd[c] * g[c];
-  const int64_t off = int64_t(blockIdx.y) * HW;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x)
-    dx[off + i] = (dz[off + i] - ac - xn[off + i] * bc) * k;
+__global__ void __launch_bounds__(kT) bn_scale_apply_c(const T* __restrict__ x, const double2* __restrict__ part,
+                                                       int splits, double cnt, double eps, T* __restrict__ mean,
+                                                       T* __restrict__ invstd, const T* __restrict__ g,
+                                                       const T* __restrict__ bta, T* __restrict__ xn,
+                                                       T* __restrict__ z, int N, int C, int HW) {
+  __shared__ T st[2];
+  const int c = blockIdx.x;
+  if (threadIdx.x < 32) {
+    const double2 s = sum_parts_warp(part, c, splits);
+    if (threadIdx.x == 0) {
+      const double m = s.x / cnt, var = s.y / cnt - m * m;
+      st[0] = T(m);
+      st[1] = T(1.0 / sqrt(var + eps));
+      if (blockIdx.y == 0) { mean[c] = st[0]; invstd[c] = st[1]; }
+    }
+  }
+  __syncthreads();
+  const T m = st[0], is = st[1], gc = g[c], bc = bta ? bta[c] : T(0);
+  const bool packed = packable(x, HW) && packable(xn, HW) && packable(z, HW);
+  chan_apply<T>(N, C, HW, splits, packed, [&](int64_t o, auto pk) {
+    if constexpr (decltype(pk)::value) {
+      Pk<T> a = reinterpret_cast<const Pk<T>*>(x)[o], b;
+#pragma unroll
+      for (int e = 0; e < Pk<T>::W; ++e) {
+        a.v[e] = (a.v[e] - m) * is;
+        b.v[e] = a.v[e] * gc + bc;
+      }
+      reinterpret_cast<Pk<T>*>(xn)[o] = a;
+      reinterpret_cast<Pk<T>*>(z)[o] = b;
+    } else {
+      const T v = (x[o] - m) * is;
+      xn[o] = v;
+      z[o] = v * gc + bc;
+    }
+  });
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kT) bn_scale_bwd_apply_c(const T* __restrict__ xn, const T* __restrict__ dz,
+                                                           const double2* __restrict__ part, int splits, double cnt,
+                                                           const T* __restrict__ invstd, const T* __restrict__ g,
+                                                           T* __restrict__ dg, T* __restrict__ db,
+                                                           T* __restrict__ dx, int N, int C, int HW) {
+  __shared__ T st[2];
+  const int c = blockIdx.x;
+  if (threadIdx.x < 32) {
+    const double2 s = sum_parts_warp(part, c, splits);
+    if (threadIdx.x == 0) {
+      if (blockIdx.y == 0) {
+        if (db) db[c] += T(s.x);
+        if (dg) dg[c] += T(s.y);
+      }
+      st[0] = T(s.x / cnt);
+      st[1] = T(s.y / cnt);
+    }
+  }
+  __syncthreads();
+  const T ac = st[0], bc = st[1], k = invstd[c] * g[c];
+  const bool packed = packable(xn, HW) && packable(dz, HW) && packable(dx, HW);
+  chan_apply<T>(N, C, HW, splits, packed, [&](int64_t o, auto pk) {
+    if constexpr (decltype(pk)::value) {
+      const Pk<T> a = reinterpret_cast<const Pk<T>*>(xn)[o];
+      Pk<T> d = reinterpret_cast<const Pk<T>*>(dz)[o];
+#pragma unroll
+      for (int e = 0; e < Pk<T>::W; ++e) d.v[e] = (d.v[e] - ac - a.v[e] * bc) * k;
+      reinterpret_cast<Pk<T>*>(dx)[o] = d;
+    } else {
+      dx[o] = (dz[o] - ac - xn[o] * bc) * k;
+    }
+  });
 }
 
 // ---- policy-gradient diff injection (trainer.cpp:42-113 restated on the device) ----------
@@ -415,8 +536,21 @@ inline dim3 plane_grid(int N, int C, int HW) {
 
 template <typename T>
 __global__ void axpby_kernel(const T* __restrict__ x, T* __restrict__ y, uint64_t n, T a, T b, bool read_y) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    y[i] = read_y ? a * x[i] + b * y[i] : a * x[i];
+  constexpr int W = Pk<T>::W;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0) {  // 16-byte packs
+    for (uint64_t j = i; j < n / W; j += stride) {
+      const Pk<T> xv = reinterpret_cast<const Pk<T>*>(x)[j];
+      Pk<T> yv;
+      if (read_y) yv = reinterpret_cast<const Pk<T>*>(y)[j];
+#pragma unroll
+      for (int e = 0; e < W; ++e) yv.v[e] = read_y ? a * xv.v[e] + b * yv.v[e] : a * xv.v[e];
+      reinterpret_cast<Pk<T>*>(y)[j] = yv;
+    }
+    i += n / W * W;
+  }
+  for (; i < n; i += stride) y[i] = read_y ? a * x[i] + b * y[i] : a * x[i];
 }
 
 }  // namespace
@@ -671,12 +805,11 @@ int cdnn_batchnorm_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle xnorm,
     by_dtype(X.dtype, "bn_scale", [&](auto tag) {
       using T = decltype(tag);
       chan_partials<T, kSumSq><<<dim3(c, splits), kT, 0, st>>>(P<T>(X), nullptr, part, n, c, hw, splits);
-      bn_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, double(n) * hw, eps, P<T>(M), P<T>(V));
-      bn_scale_apply<T><<<plane_grid(n, c, hw), kT, 0, st>>>(P<T>(X), P<T>(M), P<T>(V), P<T>(G), B ? P<T>(*B) : nullptr,
-                                                            P<T>(XN), P<T>(Z), c, hw);
+      bn_scale_apply_c<T><<<dim3(c, splits), kT, 0, st>>>(P<T>(X), part, splits, double(n) * hw, eps, P<T>(M), P<T>(V),
+                                                         P<T>(G), B ? P<T>(*B) : nullptr, P<T>(XN), P<T>(Z), n, c, hw);
     });
     check_launch("bn_scale_fwd");
-    count_launch(cx, 3);
+    count_launch(cx, 2);
   });
 }
 
@@ -709,14 +842,16 @@ int cdnn_batchnorm_scale_backward(cdnn_ctx ctx, cdnn_handle xnorm, cdnn_handle i
       T* a = P<T>(S);
       T* b = a + c;
       chan_partials<T, kSumDot><<<dim3(c, splits), kT, 0, st>>>(P<T>(DZ), P<T>(XN), part, n, c, hw, splits);
-      bn_scale_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, double(n) * hw, DG ? P<T>(*DG) : nullptr,
-                                                           DB ? P<T>(*DB) : nullptr, a, b);
       if (DX)
-        bn_scale_bwd_apply<T><<<plane_grid(n, c, hw), kT, 0, st>>>(P<T>(XN), P<T>(DZ), a, b, P<T>(V), P<T>(G),
-                                                                  P<T>(*DX), c, hw);
+        bn_scale_bwd_apply_c<T><<<dim3(c, splits), kT, 0, st>>>(P<T>(XN), P<T>(DZ), part, splits, double(n) * hw,
+                                                               P<T>(V), P<T>(G), DG ? P<T>(*DG) : nullptr,
+                                                               DB ? P<T>(*DB) : nullptr, P<T>(*DX), n, c, hw);
+      else
+        bn_scale_finalize<T><<<(c + 127) / 128, 128, 0, st>>>(part, splits, c, double(n) * hw, DG ? P<T>(*DG) : nullptr,
+                                                             DB ? P<T>(*DB) : nullptr, a, b);
     });
     check_launch("bn_scale_bwd");
-    count_launch(cx, DX ? 3 : 2);
+    count_launch(cx, 2);
   });
 }
 
