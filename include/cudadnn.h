@@ -363,6 +363,13 @@ CDNN_API int cdnn_batchnorm_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_hand
                                           cdnn_handle mean, cdnn_handle invstd, cdnn_handle gamma,
                                           cdnn_handle beta, int n, int c, int hw, double eps,
                                           cdnn_handle stream);
+/* cdnn_batchnorm_scale_forward with flags: CDNN_BN_RELU stores z = max(gamma*xnorm + beta, 0)
+ * (an in-place ReLU on the Scale's top, whose forward pass then disappears); xnorm unchanged */
+enum { CDNN_BN_RELU = 1 };
+CDNN_API int cdnn_batchnorm_scale_forward_ex(cdnn_ctx ctx, cdnn_handle x, cdnn_handle xnorm, cdnn_handle z,
+                                             cdnn_handle mean, cdnn_handle invstd, cdnn_handle gamma,
+                                             cdnn_handle beta, int n, int c, int hw, double eps, int flags,
+                                             cdnn_handle stream);
 /* dbeta += sum dz ; dgamma += sum dz*xnorm ;
  * dx = gamma*invstd*(dz - mean(dz) - xnorm*mean(dz*xnorm)) (skipped when dx == 0); scratch 2*c */
 CDNN_API int cdnn_batchnorm_scale_backward(cdnn_ctx ctx, cdnn_handle xnorm, cdnn_handle invstd,

@@ -441,8 +441,11 @@ class BatchNormLayer final : public Layer {
   // z = gamma*xnorm + beta directly, backward reads its top diff and produces the
   // Scale's parameter gradients too (one reduction pass each way).
   void fuse_scale(ScaleLayer* scale, Blob* scale_top) { fused_ = scale; z_ = scale_top; }
+  // ... and an in-place ReLU on the Scale's top (set by Net): z is stored clamped at 0
+  void fuse_relu(bool on) { fused_relu_ = on; }
 
  private:
+  bool fused_relu_ = false;
   ScaleLayer* fused_ = nullptr;
   Blob* z_ = nullptr;
   double eps_;

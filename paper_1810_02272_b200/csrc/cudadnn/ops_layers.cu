@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kT) bn_scale_apply_c(const T* __restrict__ x, 
                                                        int splits, double cnt, double eps, T* __restrict__ mean,
                                                        T* __restrict__ invstd, const T* __restrict__ g,
                                                        const T* __restrict__ bta, T* __restrict__ xn,
-                                                       T* __restrict__ z, int N, int C, int HW) {
+                                                       T* __restrict__ z, int N, int C, int HW, bool relu) {
   __shared__ T st[2];
   const int c = blockIdx.x;
   if (threadIdx.x < 32) {
@@ -456,13 +456,15 @@ __global__ void __launch_bounds__(kT) bn_scale_apply_c(const T* __restrict__ x, 
       for (int e = 0; e < Pk<T>::W; ++e) {
         a.v[e] = (a.v[e] - m) * is;
         b.v[e] = a.v[e] * gc + bc;
+        if (relu) b.v[e] = b.v[e] > T(0) ? b.v[e] : T(0);
       }
       reinterpret_cast<Pk<T>*>(xn)[o] = a;
       reinterpret_cast<Pk<T>*>(z)[o] = b;
     } else {
       const T v = (x[o] - m) * is;
       xn[o] = v;
-      z[o] = v * gc + bc;
+      const T zv = v * gc + bc;
+      z[o] = relu ? (zv > T(0) ? zv : T(0)) : zv;
     }
   });
 }
@@ -783,7 +785,14 @@ int cdnn_scale_backward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle gamma, cdnn_han
 int cdnn_batchnorm_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle xnorm, cdnn_handle z, cdnn_handle mean,
                                  cdnn_handle invstd, cdnn_handle gamma, cdnn_handle beta, int n, int c, int hw,
                                  double eps, cdnn_handle stream) {
+  return cdnn_batchnorm_scale_forward_ex(ctx, x, xnorm, z, mean, invstd, gamma, beta, n, c, hw, eps, 0, stream);
+}
+
+int cdnn_batchnorm_scale_forward_ex(cdnn_ctx ctx, cdnn_handle x, cdnn_handle xnorm, cdnn_handle z, cdnn_handle mean,
+                                    cdnn_handle invstd, cdnn_handle gamma, cdnn_handle beta, int n, int c, int hw,
+                                    double eps, int flags, cdnn_handle stream) {
   return guarded([&] {
+    const bool relu = (flags & CDNN_BN_RELU) != 0;
     Ctx* cx = need_ctx(ctx);
     BufferSlot& X = buffer(cx, x, "bn_scale x");
     BufferSlot& XN = buffer(cx, xnorm, "bn_scale xnorm");
@@ -806,7 +815,8 @@ int cdnn_batchnorm_scale_forward(cdnn_ctx ctx, cdnn_handle x, cdnn_handle xnorm,
       using T = decltype(tag);
       chan_partials<T, kSumSq><<<dim3(c, splits), kT, 0, st>>>(P<T>(X), nullptr, part, n, c, hw, splits);
       bn_scale_apply_c<T><<<dim3(c, splits), kT, 0, st>>>(P<T>(X), part, splits, double(n) * hw, eps, P<T>(M), P<T>(V),
-                                                         P<T>(G), B ? P<T>(*B) : nullptr, P<T>(XN), P<T>(Z), n, c, hw);
+                                                         P<T>(G), B ? P<T>(*B) : nullptr, P<T>(XN), P<T>(Z), n, c, hw,
+                                                         relu);
     });
     check_launch("bn_scale_fwd");
     count_launch(cx, 2);

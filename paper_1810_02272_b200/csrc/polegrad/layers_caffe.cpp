@@ -194,10 +194,10 @@ void BatchNormLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* con
     const cdnn_handle x = bottoms[0]->gpu_data();
     const cdnn_handle z = z_ == bottoms[0] ? z_->mutable_gpu_data() : z_->overwrite_gpu_data();
     Blob* beta = fused_->beta();
-    cdnn_ok(cdnn_batchnorm_scale_forward(reg.context(), x, xnorm_->overwrite_gpu_data(), z,
-                                         mean_->overwrite_gpu_data(), invstd_->overwrite_gpu_data(),
-                                         fused_->gamma().gpu_data(), beta ? beta->gpu_data() : 0, n_, c_, hw_, eps_,
-                                         reg.stream()),
+    cdnn_ok(cdnn_batchnorm_scale_forward_ex(reg.context(), x, xnorm_->overwrite_gpu_data(), z,
+                                            mean_->overwrite_gpu_data(), invstd_->overwrite_gpu_data(),
+                                            fused_->gamma().gpu_data(), beta ? beta->gpu_data() : 0, n_, c_, hw_,
+                                            eps_, fused_relu_ ? CDNN_BN_RELU : 0, reg.stream()),
             "BatchNorm+Scale forward");
     (void)tops;
     return;

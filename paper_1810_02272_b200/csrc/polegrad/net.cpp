@@ -162,6 +162,12 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
     if (bn && sc && bottoms_[i + 1][0] == tops_[i][0]) {
       bn->fuse_scale(sc, tops_[i + 1][0]);
       sc->set_fused(true);
+      // ... and an in-place ReLU on the Scale's top: applied when z is stored
+      auto* relu = i + 2 < layers_.size() ? dynamic_cast<ReluLayer*>(layers_[i + 2].get()) : nullptr;
+      if (!compat && relu && bottoms_[i + 2][0] == tops_[i + 1][0] && tops_[i + 2][0] == tops_[i + 1][0]) {
+        bn->fuse_relu(true);
+        relu->set_forward_fused(true);
+      }
     }
   }
 

@@ -26,6 +26,7 @@ STATUS = {
 F32, F64, I32 = 0, 1, 2
 MATH_TF32, MATH_TF32X3 = 0, 1
 POOL_MAX, POOL_AVE = 0, 1
+BN_RELU = 1  # cdnn_batchnorm_scale_forward_ex flags (CDNN_BN_RELU)
 SOLVER_SGD, SOLVER_RMSPROP = 0, 1
 _NP = {F32: np.float32, F64: np.float64, I32: np.int32}
 
@@ -49,7 +50,7 @@ EXPORTS = [
     "cdnn_lrn_pool_backward", "cdnn_allreduce_sum",
     "cdnn_broadcast", "cdnn_copy_range", "cdnn_lrn_forward", "cdnn_lrn_backward", "cdnn_lrn_backward_ex", "cdnn_dropout", "cdnn_counter_increment",
     "cdnn_batchnorm_forward", "cdnn_batchnorm_backward", "cdnn_scale_forward", "cdnn_scale_backward",
-    "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
+    "cdnn_axpby", "cdnn_batchnorm_scale_forward", "cdnn_batchnorm_scale_forward_ex", "cdnn_batchnorm_scale_backward", "cdnn_conv_forward_ex",
     "cdnn_pool_forward_ex", "cdnn_pg_diff", "cdnn_mlp_pg_supported", "cdnn_mlp_pg_step", "cdnn_mlp_pg_step_host",
 ]
 
@@ -157,6 +158,7 @@ def load() -> C.CDLL:
             "cdnn_mlp_pg_step_host": ([vp, h, h, h, vp, vp, vp, vp, i, i, i, i, i, h, h, h, C.POINTER(C.c_uint64), i,
                                        d, d, d, d, d, h, h, h, h], i),
             "cdnn_batchnorm_scale_forward": ([vp, h, h, h, h, h, h, h, i, i, i, d, h], i),
+            "cdnn_batchnorm_scale_forward_ex": ([vp, h, h, h, h, h, h, h, i, i, i, d, i, h], i),
             "cdnn_batchnorm_scale_backward": ([vp, h, h, h, h, h, h, h, h, i, i, i, h], i),
         }
         for name, (args, res) in sig.items():

@@ -318,6 +318,45 @@ def test_batchnorm(ctx, dtype, shape):
 
 
 @pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
+@pytest.mark.parametrize("shape", [(128, 16, 32, 32), (8, 64, 8, 8), (3, 5, 3, 3), (64, 8, 7, 7)])
+def test_batchnorm_scale_fused(ctx, dtype, shape):
+    """cdnn_batchnorm_scale_forward[_ex] / _backward (the fused BatchNorm+Scale[+ReLU] of
+    ResNet-20) against torch fp64: packed (HW % 4 == 0) and element-wise planes, many and
+    few channel splits; CDNN_BN_RELU stores exactly max(z, 0) with xnorm unchanged."""
+    n, c, h, w = shape
+    rng = np.random.default_rng(n + c)
+    dt = NP[dtype]
+    x = (rng.standard_normal(shape) * 2 + 1).astype(dt)
+    g = rng.uniform(0.5, 1.5, c).astype(dt)
+    b = rng.uniform(-1, 1, c).astype(dt)
+    dz = rng.uniform(-1, 1, shape).astype(dt)
+    xt = torch.from_numpy(x.astype(np.float64)).requires_grad_()
+    gt = torch.from_numpy(g.astype(np.float64)).requires_grad_()
+    bt = torch.from_numpy(b.astype(np.float64)).requires_grad_()
+    xnt = torch.nn.functional.batch_norm(xt, None, None, training=True, eps=1e-5)
+    zt = xnt * gt[None, :, None, None] + bt[None, :, None, None]
+    zt.backward(torch.from_numpy(dz.astype(np.float64)))
+    hx, hg, hb = ctx.upload(x), ctx.upload(g), ctx.upload(b)
+    hxn, hz, hzr = ctx.alloc(x.size, dtype), ctx.alloc(x.size, dtype), ctx.alloc(x.size, dtype)
+    hm, hv, hs = ctx.alloc(c, dtype), ctx.alloc(c, dtype), ctx.alloc(2 * c, dtype)
+    ctx.call("cdnn_batchnorm_scale_forward", hx, hxn, hz, hm, hv, hg, hb, n, c, h * w, 1e-5, 0)
+    tol = 1e-5 if dtype == cd.F32 else 1e-12
+    assert rel_l2(ctx.read(hxn), xnt.detach().numpy()) <= tol
+    assert rel_l2(ctx.read(hz), zt.detach().numpy()) <= tol
+    xn0 = ctx.read(hxn).copy()
+    ctx.call("cdnn_batchnorm_scale_forward_ex", hx, hxn, hzr, hm, hv, hg, hb, n, c, h * w, 1e-5, cd.BN_RELU, 0)
+    assert np.array_equal(ctx.read(hzr), np.maximum(ctx.read(hz), 0))
+    assert np.array_equal(ctx.read(hxn), xn0)
+    dg0 = rng.standard_normal(c).astype(dt)  # parameter gradients accumulate
+    hdz, hdx = ctx.upload(dz), ctx.alloc(x.size, dtype)
+    hdg, hdb = ctx.upload(dg0), ctx.upload(np.zeros(c, dt))
+    ctx.call("cdnn_batchnorm_scale_backward", hxn, hv, hg, hdz, hdx, hdg, hdb, hs, n, c, h * w, 0)
+    assert rel_l2(ctx.read(hdx), xt.grad.numpy()) <= tol * 10
+    assert rel_l2(ctx.read(hdg), dg0 + gt.grad.numpy()) <= tol * 10
+    assert rel_l2(ctx.read(hdb), bt.grad.numpy()) <= tol * 10
+
+
+@pytest.mark.parametrize("dtype", [cd.F32, cd.F64])
 @pytest.mark.parametrize("bias", [True, False])
 def test_scale_and_axpby(ctx, dtype, bias):
     n, c, h, w = 16, 32, 8, 8
