@@ -2,6 +2,7 @@
 // ResNet-20: BatchNorm, Scale, Eltwise), Caffe semantics, on the CudaDnn
 // C-ABI (csrc/cudadnn/ops_layers.cu).  The reference has none of them
 // (SURVEY §8(f)); the CPU oracle restates each in oracle/ext/ext_layers.cpp.
+#include <algorithm>
 #include <cmath>
 #include <string>
 
@@ -300,6 +301,15 @@ void EltwiseLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const
   Registry& reg = bottoms[0]->registry();
   const std::size_t n = tops[0]->count();
   const cdnn_handle y = tops[0]->overwrite_gpu_data();
+  // plain sum (every coefficient 1, the ResNet shortcut): one pass over all bottoms with
+  // the roundings of the axpby sequence below (products by 1 are exact, each partial sum
+  // rounded once, in bottom order)
+  if (bottoms.size() <= 8 && std::all_of(coeff_.begin(), coeff_.end(), [](double a) { return a == 1.0; })) {
+    cdnn_handle xs[8] = {};
+    for (std::size_t k = 0; k < bottoms.size(); ++k) xs[k] = bottoms[k]->gpu_data();
+    cdnn_ok(cdnn_fan_in(reg.context(), xs, int(bottoms.size()), y, n, reg.stream()), "Eltwise forward");
+    return;
+  }
   cdnn_ok(cdnn_axpby(reg.context(), n, coeff_[0], bottoms[0]->gpu_data(), 0.0, y, 0, reg.stream()), "Eltwise forward");
   for (std::size_t k = 1; k < bottoms.size(); ++k)
     cdnn_ok(cdnn_axpby(reg.context(), n, coeff_[k], bottoms[k]->gpu_data(), 1.0, y, 1, reg.stream()),
