@@ -484,9 +484,14 @@ class EltwiseLayer final : public Layer {
                            Rng& rng) override;
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  // a plain sum (every coefficient 1) of at most 8 bottoms: one pass, ReLU-fusable
+  bool unit_sum() const;
+  // an in-place ReLU on the top, applied by the one-pass sum (set by Net)
+  void fuse_relu(bool on) { fused_relu_ = on; }
 
  private:
   std::vector<double> coeff_;
+  bool fused_relu_ = false;
 };
 
 // Cross-entropy gradient at a softmax output: probs - one-hot target

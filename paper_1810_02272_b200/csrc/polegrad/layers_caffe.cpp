@@ -297,6 +297,10 @@ std::vector<Shape> EltwiseLayer::setup(const std::vector<Shape>& s, const std::s
   return {s[0]};
 }
 
+bool EltwiseLayer::unit_sum() const {
+  return coeff_.size() <= 8 && std::all_of(coeff_.begin(), coeff_.end(), [](double a) { return a == 1.0; });
+}
+
 void EltwiseLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) {
   Registry& reg = bottoms[0]->registry();
   const std::size_t n = tops[0]->count();
@@ -304,10 +308,12 @@ void EltwiseLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const
   // plain sum (every coefficient 1, the ResNet shortcut): one pass over all bottoms with
   // the roundings of the axpby sequence below (products by 1 are exact, each partial sum
   // rounded once, in bottom order)
-  if (bottoms.size() <= 8 && std::all_of(coeff_.begin(), coeff_.end(), [](double a) { return a == 1.0; })) {
+  if (unit_sum()) {
     cdnn_handle xs[8] = {};
     for (std::size_t k = 0; k < bottoms.size(); ++k) xs[k] = bottoms[k]->gpu_data();
-    cdnn_ok(cdnn_fan_in(reg.context(), xs, int(bottoms.size()), y, n, reg.stream()), "Eltwise forward");
+    cdnn_ok(cdnn_fan_in_ex(reg.context(), xs, int(bottoms.size()), y, n, fused_relu_ ? CDNN_FAN_RELU : 0,
+                           reg.stream()),
+            "Eltwise forward");
     return;
   }
   cdnn_ok(cdnn_axpby(reg.context(), n, coeff_[0], bottoms[0]->gpu_data(), 0.0, y, 0, reg.stream()), "Eltwise forward");

@@ -171,6 +171,16 @@ void Net::build(const NetDef& def, std::uint64_t seed, int device) {
     }
   }
 
+  // Fuse a plain Eltwise sum + in-place ReLU: the one-pass sum stores max(sum, 0).
+  for (std::size_t i = 0; !compat && i + 1 < layers_.size(); ++i) {
+    auto* el = dynamic_cast<EltwiseLayer*>(layers_[i].get());
+    auto* relu = dynamic_cast<ReluLayer*>(layers_[i + 1].get());
+    if (el && relu && el->unit_sum() && bottoms_[i + 1][0] == tops_[i][0] && tops_[i + 1][0] == tops_[i][0]) {
+      el->fuse_relu(true);
+      relu->set_forward_fused(true);
+    }
+  }
+
   // Fuse InnerProduct / Convolution + in-place ReLU: the ReLU runs in the epilogue.
   for (std::size_t i = 0; i + 1 < layers_.size(); ++i) {
     auto* relu = dynamic_cast<ReluLayer*>(layers_[i + 1].get());

@@ -27,6 +27,7 @@ F32, F64, I32 = 0, 1, 2
 MATH_TF32, MATH_TF32X3 = 0, 1
 POOL_MAX, POOL_AVE = 0, 1
 BN_RELU = 1  # cdnn_batchnorm_scale_forward_ex flags (CDNN_BN_RELU)
+FAN_RELU = 1  # cdnn_fan_in_ex flags (CDNN_FAN_RELU)
 SOLVER_SGD, SOLVER_RMSPROP = 0, 1
 _NP = {F32: np.float32, F64: np.float64, I32: np.int32}
 
@@ -41,7 +42,7 @@ EXPORTS = [
     "cdnn_graph_launch", "cdnn_graph_free", "cdnn_event_create", "cdnn_event_record", "cdnn_event_elapsed",
     "cdnn_event_free", "cdnn_event_sync", "cdnn_rng_create", "cdnn_rng_next_u64", "cdnn_rng_uniform", "cdnn_subsystem_free",
     "cdnn_conv_desc_create", "cdnn_conv_output_shape", "cdnn_pool_desc_create", "cdnn_pool_output_shape",
-    "cdnn_desc_free", "cdnn_dispatch", "cdnn_fill", "cdnn_copy", "cdnn_scal", "cdnn_axpy", "cdnn_dot", "cdnn_fan_out", "cdnn_fan_in",
+    "cdnn_desc_free", "cdnn_dispatch", "cdnn_fill", "cdnn_copy", "cdnn_scal", "cdnn_axpy", "cdnn_dot", "cdnn_fan_out", "cdnn_fan_in", "cdnn_fan_in_ex",
     "cdnn_gemm", "cdnn_ip_forward", "cdnn_ip_backward", "cdnn_conv_forward", "cdnn_conv_backward_data", "cdnn_conv_backward_data_ex",
     "cdnn_conv_backward_filter", "cdnn_conv_backward_filter_ex", "cdnn_pool_forward", "cdnn_pool_backward", "cdnn_pool_backward_ex", "cdnn_relu_forward",
     "cdnn_relu_backward", "cdnn_sigmoid_forward", "cdnn_sigmoid_backward", "cdnn_softmax_forward",
@@ -118,6 +119,7 @@ def load() -> C.CDLL:
             "cdnn_dot": ([vp, u64, h, h, C.POINTER(d)], i),
             "cdnn_fan_out": ([vp, h, C.POINTER(h), C.POINTER(d), i, u64, h], i),
             "cdnn_fan_in": ([vp, C.POINTER(h), i, h, u64, h], i),
+            "cdnn_fan_in_ex": ([vp, C.POINTER(h), i, h, u64, i, h], i),
             "cdnn_gemm": ([vp, i, i, i, i, i, d, h, h, d, h, h], i),
             "cdnn_ip_forward": ([vp, h, h, h, h, i, i, i, i, h], i),
             "cdnn_ip_backward": ([vp, h, h, h, h, h, h, i, i, i, h], i),
