@@ -144,10 +144,16 @@ void copy_to_staging(void* dst, const void* src, std::size_t bytes) {
   std::vector<std::thread> pool;
   pool.reserve(nt - 1);
   const std::size_t per = (bytes + nt - 1) / nt;
-  for (std::size_t t = 1; t < nt; ++t) {
-    const std::size_t b0 = t * per, b1 = std::min(bytes, b0 + per);
-    if (b0 < b1)
-      pool.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0); });
+  try {
+    for (std::size_t t = 1; t < nt; ++t) {
+      const std::size_t b0 = t * per, b1 = std::min(bytes, b0 + per);
+      if (b0 < b1)
+        pool.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0); });
+    }
+  } catch (...) {  // no thread to spare: finish on this one
+    for (std::thread& th : pool) th.join();
+    std::memcpy(dst, src, bytes);
+    return;
   }
   std::memcpy(dst, src, std::min(bytes, per));
   for (std::thread& th : pool) th.join();
