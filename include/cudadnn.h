@@ -227,11 +227,13 @@ CDNN_API int cdnn_fan_out(cdnn_ctx ctx, cdnn_handle src, const cdnn_handle* dsts
  * cdnn_copy followed by cdnn_axpy(1.0) per further source; 1..8 sources. */
 CDNN_API int cdnn_fan_in(cdnn_ctx ctx, const cdnn_handle* srcs, int nsrc, cdnn_handle dst, uint64_t n,
                          cdnn_handle stream);
-/* cdnn_fan_in with flags: CDNN_FAN_RELU stores max(sum, 0) (Eltwise SUM followed by an
- * in-place ReLU, whose forward pass then disappears) */
+/* cdnn_fan_in with flags and a gate: CDNN_FAN_RELU stores max(sum, 0) (Eltwise SUM followed
+ * by an in-place ReLU, whose forward pass then disappears); a nonzero gate stores
+ * (gate > 0 ? sum : 0) (Split backward fused with the backward of the in-place ReLU whose
+ * data is the gate) */
 enum { CDNN_FAN_RELU = 1 };
 CDNN_API int cdnn_fan_in_ex(cdnn_ctx ctx, const cdnn_handle* srcs, int nsrc, cdnn_handle dst, uint64_t n, int flags,
-                            cdnn_handle stream);
+                            cdnn_handle gate, cdnn_handle stream);
 /* Row-major C = alpha*op(A)*op(B) + beta*C; beta == 0 never reads C.
  * F32 buffers run on tcgen05 TF32 tensor cores, F64 on the SIMT FP64 path. */
 CDNN_API int cdnn_gemm(cdnn_ctx ctx, int trans_a, int trans_b, int m, int n, int k, double alpha,

@@ -371,6 +371,8 @@ class SplitLayer final : public Layer {
                            Rng& rng) override;
   void forward(std::span<Blob* const> bottoms, std::span<Blob* const> tops) override;
   void backward(std::span<Blob* const> tops, std::span<Blob* const> bottoms) override;
+  // the one-pass backward (<= 8 tops) can gate its sum by the bottom's data
+  bool supports_relu_gate() const override { return spec_.tops.size() <= 8; }
 };
 
 // ---- configs 4-5 (AlexNet, ResNet-20), Caffe semantics -------------

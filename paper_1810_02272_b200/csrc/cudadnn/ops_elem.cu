@@ -138,11 +138,12 @@ __global__ void fan_out_kernel(const T* __restrict__ x, FanPtrs<T> d, int nd, bo
   }
 }
 template <typename T>
-__global__ void fan_in_kernel(FanPtrs<T> s, int ns, T* __restrict__ y, uint64_t n, bool relu) {
+__global__ void fan_in_kernel(FanPtrs<T> s, int ns, T* __restrict__ y, uint64_t n, bool relu,
+                              const T* __restrict__ gate) {
   constexpr int W = Pack<T>::W;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  bool al = aligned16(y);
+  bool al = aligned16(y) && (!gate || aligned16(gate));
 #pragma unroll
   for (int k = 0; k < kFan; ++k)
     if (k < ns) al = al && aligned16(s.p[k]);
@@ -160,6 +161,11 @@ __global__ void fan_in_kernel(FanPtrs<T> s, int ns, T* __restrict__ y, uint64_t 
 #pragma unroll
         for (int e = 0; e < W; ++e) acc.v[e] = acc.v[e] > T(0) ? acc.v[e] : T(0);
       }
+      if (gate) {
+        const Pack<T> gv = ld_pack(gate, j);
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc.v[e] = gv.v[e] > T(0) ? acc.v[e] : T(0);
+      }
       st_pack(y, j, acc);
     }
     i += n / W * W;
@@ -169,7 +175,8 @@ __global__ void fan_in_kernel(FanPtrs<T> s, int ns, T* __restrict__ y, uint64_t 
 #pragma unroll
     for (int k = 1; k < kFan; ++k)
       if (k < ns) acc = add_rn(acc, mul_rn(T(1), s.p[k][i]));
-    y[i] = relu ? (acc > T(0) ? acc : T(0)) : acc;
+    if (relu) acc = acc > T(0) ? acc : T(0);
+    y[i] = (gate && !(gate[i] > T(0))) ? T(0) : acc;
   }
 }
 
@@ -527,17 +534,19 @@ int cdnn_fan_out(cdnn_ctx ctx, cdnn_handle src, const cdnn_handle* dsts, const d
 
 // Split backward: dst = src_0 + src_1 + ... (in order; the roundings of copy + axpy)
 int cdnn_fan_in(cdnn_ctx ctx, const cdnn_handle* srcs, int nsrc, cdnn_handle dst, uint64_t n, cdnn_handle stream) {
-  return cdnn_fan_in_ex(ctx, srcs, nsrc, dst, n, 0, stream);
+  return cdnn_fan_in_ex(ctx, srcs, nsrc, dst, n, 0, 0, stream);
 }
 
 int cdnn_fan_in_ex(cdnn_ctx ctx, const cdnn_handle* srcs, int nsrc, cdnn_handle dst, uint64_t n, int flags,
-                   cdnn_handle stream) {
+                   cdnn_handle gate, cdnn_handle stream) {
   return guarded([&] {
     const bool relu = (flags & CDNN_FAN_RELU) != 0;
     Ctx* c = need_ctx(ctx);
     if (nsrc < 1 || nsrc > kFan || !srcs) fail(CDNN_INVALID_ARGUMENT, "fan_in: 1..8 sources");
     BufferSlot& Y = buffer(c, dst, "fan_in dst");
     require_len(Y, n, "fan_in dst");
+    BufferSlot* G = buffer_or_null(c, gate, "fan_in gate");
+    if (G) { require_len(*G, n, "fan_in gate"); require_dtype(*G, Y.dtype, "fan_in gate"); }
     BufferSlot* S[kFan] = {};
     for (int k = 0; k < nsrc; ++k) {
       S[k] = &buffer(c, srcs[k], "fan_in src");
@@ -550,7 +559,8 @@ int cdnn_fan_in_ex(cdnn_ctx ctx, const cdnn_handle* srcs, int nsrc, cdnn_handle 
       using T = decltype(tag);
       FanPtrs<T> f{};
       for (int k = 0; k < nsrc; ++k) f.p[k] = dptr<T>(*S[k]);
-      fan_in_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(f, nsrc, dptr<T>(Y), n, relu);
+      fan_in_kernel<T><<<blocks_for(n), kThreads, 0, stream_of(c, stream)>>>(f, nsrc, dptr<T>(Y), n, relu,
+                                                                              G ? dptr<T>(*G) : nullptr);
     });
     check_launch("fan_in");
     count_launch(c);

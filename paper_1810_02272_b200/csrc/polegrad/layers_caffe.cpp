@@ -311,7 +311,7 @@ void EltwiseLayer::forward(std::span<Blob* const> bottoms, std::span<Blob* const
   if (unit_sum()) {
     cdnn_handle xs[8] = {};
     for (std::size_t k = 0; k < bottoms.size(); ++k) xs[k] = bottoms[k]->gpu_data();
-    cdnn_ok(cdnn_fan_in_ex(reg.context(), xs, int(bottoms.size()), y, n, fused_relu_ ? CDNN_FAN_RELU : 0,
+    cdnn_ok(cdnn_fan_in_ex(reg.context(), xs, int(bottoms.size()), y, n, fused_relu_ ? CDNN_FAN_RELU : 0, 0,
                            reg.stream()),
             "Eltwise forward");
     return;

@@ -277,7 +277,10 @@ void SplitLayer::backward(std::span<Blob* const> tops, std::span<Blob* const> bo
   if (tops.size() <= 8) {  // the diffs summed in one pass (same order and roundings as copy + axpy)
     cdnn_handle d[8] = {};
     for (std::size_t t = 0; t < tops.size(); ++t) d[t] = tops[t]->gpu_diff();
-    cdnn_ok(cdnn_fan_in(reg.context(), d, int(tops.size()), dx, n, reg.stream()), "Split backward");
+    // (gated by the bottom's data when the in-place ReLU producing it has its backward fused here)
+    cdnn_ok(cdnn_fan_in_ex(reg.context(), d, int(tops.size()), dx, n, 0, relu_gate_ ? bottoms[0]->gpu_data() : 0,
+                           reg.stream()),
+            "Split backward");
     return;
   }
   cdnn_ok(cdnn_copy(reg.context(), tops[0]->gpu_diff(), dx, n, reg.stream()), "Split backward");

@@ -119,7 +119,7 @@ def load() -> C.CDLL:
             "cdnn_dot": ([vp, u64, h, h, C.POINTER(d)], i),
             "cdnn_fan_out": ([vp, h, C.POINTER(h), C.POINTER(d), i, u64, h], i),
             "cdnn_fan_in": ([vp, C.POINTER(h), i, h, u64, h], i),
-            "cdnn_fan_in_ex": ([vp, C.POINTER(h), i, h, u64, i, h], i),
+            "cdnn_fan_in_ex": ([vp, C.POINTER(h), i, h, u64, i, h, h], i),
             "cdnn_gemm": ([vp, i, i, i, i, i, d, h, h, d, h, h], i),
             "cdnn_ip_forward": ([vp, h, h, h, h, i, i, i, i, h], i),
             "cdnn_ip_backward": ([vp, h, h, h, h, h, h, i, i, i, h], i),

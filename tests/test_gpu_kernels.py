@@ -255,8 +255,12 @@ def test_fan_out_fan_in_match_copy_axpy(ctx, dtype, k):
     assert np.array_equal(ctx.read(y), ctx.read(ref))
     # Eltwise SUM + in-place ReLU in the same pass (CDNN_FAN_RELU)
     yr = ctx.alloc(n, dtype)
-    ctx.call("cdnn_fan_in_ex", (C.c_uint64 * k)(*[int(v) for v in hs]), k, yr, n, cd.FAN_RELU, 0)
+    ctx.call("cdnn_fan_in_ex", (C.c_uint64 * k)(*[int(v) for v in hs]), k, yr, n, cd.FAN_RELU, 0, 0)
     assert np.array_equal(ctx.read(yr), np.maximum(ctx.read(ref), 0))
+    # Split backward + the backward of the in-place ReLU producing its bottom (gate = that data)
+    gate = ctx.upload(srcs[-1])
+    ctx.call("cdnn_fan_in_ex", (C.c_uint64 * k)(*[int(v) for v in hs]), k, yr, n, 0, gate, 0)
+    assert np.array_equal(ctx.read(yr), np.where(srcs[-1] > 0, ctx.read(ref), 0))
 
 
 # ---- config 4-5 layers (LRN, Dropout, BatchNorm, Scale, Eltwise) vs torch fp64 -----------
